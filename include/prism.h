@@ -1,0 +1,161 @@
+/*
+ * prism.h -- C ABI of libprism.so, the B200 (sm_100a) implementation of the
+ * PRISM scheduling-memory hot path: the demand-aware radix tree (DART) and
+ * the query-aware scheduler (QAS).
+ *
+ * Plain pointers and sizes only; no torch types cross this boundary.  Every
+ * entry point replaces one reference interface (paths relative to
+ * /root/reference/pkg/src/prefixsim/); the Python binding a maintainer adds
+ * on the reference side is shown in INTEGRATION.md.
+ *
+ * Conventions
+ *   - Tokens are uint32 (the reference token
+ *     layout tops out near 3.0e9, workload.py:21-22).
+ *   - Segment ids are int32 >= 0; PRISM_SEG_NONE stands for Python None.
+ *   - Node kinds: 0 SYSTEM, 1 REUSABLE, 2 PRIVATE (kvcache.py:26-29).
+ *   - Policies:   0 DART, 1 LRU, 2 LRU_ACTIVE, 3 LFU (kvcache.py:19-23).
+ *   - A node handle is (slot, node_id): slot indexes the device SoA, node_id
+ *     is the reference's creation-order id (kvcache.py:135-138).
+ *   - Every call returns a status: PRISM_OK, PRISM_CAPACITY (the reference
+ *     raises CapacityError), PRISM_RELEASE (ReleaseError), PRISM_INVALID
+ *     (ValueError), PRISM_CUDA / PRISM_FATAL (device failure); the message is
+ *     available from prism_last_error().
+ *   - Per-call entry points take HOST buffers and are synchronous (the
+ *     reference consumes each result immediately, engine.py:203-213).  The
+ *     *_device variants take DEVICE buffers and a cudaStream_t (as void*).
+ *   - There is no CPU fallback: without a CUDA device prism_tree_create fails.
+ */
+#ifndef PRISM_H
+#define PRISM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PRISM_OK 0
+#define PRISM_CAPACITY 1
+#define PRISM_RELEASE 2
+#define PRISM_INVALID 3
+#define PRISM_CUDA 4
+#define PRISM_FATAL 5
+
+#define PRISM_SEG_NONE ((int32_t)0x80000000)
+
+typedef struct prism_tree prism_tree;
+
+const char *prism_last_error(void);
+int prism_device_count(void);
+
+/* RadixCache.__init__(CacheConfig) -- kvcache.py:120-131, CacheConfig kvcache.py:66-76.
+ * initial_slots / initial_arena_tokens are allocation hints (0 = default);
+ * all device arrays grow on demand.  device = CUDA ordinal. */
+prism_tree *prism_tree_create(int64_t capacity_tokens, int32_t policy, int64_t protect_budget,
+                              int64_t initial_slots, int64_t initial_arena_tokens, int32_t device);
+void prism_tree_destroy(prism_tree *t);
+
+/* RadixCache.match_prefix -- kvcache.py:146-171.
+ * visited_slots / visited_ids (capacity n) may be NULL. */
+int prism_match(prism_tree *t, const uint32_t *path, int64_t n, int64_t *hit,
+                int32_t *visited_slots, int64_t *visited_ids, int64_t *n_visited);
+
+/* RadixCache.insert_path -- kvcache.py:190-241 (incl. _reserve 243-273 and
+ * its evict).  Anchors as parallel arrays (Anchor, kvcache.py:56-63):
+ * a_off[na], a_kind[na], a_seg[na], a_snap[3*na]. */
+int prism_insert(prism_tree *t, const uint32_t *path, int64_t n, int64_t na, const int32_t *a_off,
+                 const int8_t *a_kind, const int32_t *a_seg, const int32_t *a_snap,
+                 int32_t *leaf_slot, int64_t *leaf_id);
+
+/* RadixCache.release_path -- kvcache.py:350-360, for n leaves in order. */
+int prism_release(prism_tree *t, int64_t n, const int32_t *slots, const int64_t *ids);
+
+/* RadixCache.evict -- kvcache.py:425-460. */
+int prism_evict(prism_tree *t, int64_t k_free, int64_t *freed);
+
+/* RadixCache.set_protection -- kvcache.py:364-383.  The dispatch priority
+ * map (scheduler.py:247-251) as (segs[n], vals[n]); out_ids receives at most
+ * protect_budget protected node ids, *n_out their count. */
+int prism_set_protection(prism_tree *t, int64_t n, const int32_t *segs, const double *vals,
+                         int64_t *out_ids, int64_t *n_out);
+
+/* RadixCache.note_active_segments -- kvcache.py:385-393. */
+int prism_note_active(prism_tree *t, int64_t n, const int32_t *segs);
+
+/* The engine's admission loop for one wave -- engine.py:200-213: for each
+ * member in order, match_prefix then insert_path; stops at the first
+ * CapacityError.  Paths as CSR (path_off[B+1], tokens), anchors as CSR
+ * (anc_off[B+1] into a_*).  Outputs for the admitted prefix: hits[B],
+ * leaf_slots[B], leaf_ids[B]; *n_admitted.  Host buffers, synchronous. */
+int prism_admit_wave(prism_tree *t, int64_t B, const int64_t *path_off, const uint32_t *tokens,
+                     const int64_t *anc_off, const int32_t *a_off, const int8_t *a_kind,
+                     const int32_t *a_seg, const int32_t *a_snap, int64_t *hits,
+                     int32_t *leaf_slots, int64_t *leaf_ids, int64_t *n_admitted);
+
+/* Same, with every array a DEVICE pointer; outputs written on device, the
+ * admitted count to *n_admitted_host after an internal stream sync. */
+int prism_admit_wave_device(prism_tree *t, int64_t B, const int64_t *path_off,
+                            const uint32_t *tokens, const int64_t *anc_off, const int32_t *a_off,
+                            const int8_t *a_kind, const int32_t *a_seg, const int32_t *a_snap,
+                            int64_t *hits, int32_t *leaf_slots, int64_t *leaf_ids,
+                            int64_t *n_admitted_host, void *stream);
+
+/* Batched release of device-resident leaves (engine.py:177-181 for a whole
+ * completion batch); the leaves must hold valid pins. */
+int prism_release_device(prism_tree *t, int64_t n, const int32_t *slots, const int64_t *ids,
+                         void *stream);
+
+/* ---------------------------------------------------------- introspection */
+/* out[16]: resident_tokens, clock, next_id, slot high-water mark, live nodes,
+ * arena tokens used, hash live, hash tombstones, victims logged (total),
+ * evict calls, list builds, slot capacity, arena capacity, hash capacity,
+ * fast-path members, slow-path members. */
+int prism_stats(prism_tree *t, int64_t *out);
+/* Victim records [first, first+count) of the cumulative victim log:
+ * ids, kinds, segs, first_tok, edge_len, edge_off (arena offset at eviction;
+ * valid until the next arena compaction). */
+int prism_victims(prism_tree *t, int64_t first, int64_t count, int64_t *ids, int8_t *kinds,
+                  int32_t *segs, uint32_t *first_tok, int32_t *edge_len, int64_t *edge_off);
+/* Copy the slot SoA [0, hw) to host for debug_nodes (kvcache.py:473-521).
+ * Arrays sized >= hw: node_id, parent slot, edge_len, kind, seg, ref, last,
+ * hits, protected, has_anchor, first_tok, anchor_kind, anchor_seg, anchor_off,
+ * snap (3*hw), edge_off.  *hw_out receives hw. */
+int prism_snapshot(prism_tree *t, int64_t cap, int64_t *hw_out, int64_t *node_id, int32_t *parent,
+                   int32_t *edge_len, int8_t *kind, int32_t *seg, int32_t *ref, int64_t *last,
+                   int32_t *hits, int8_t *prot, int8_t *has_anchor, uint32_t *first_tok,
+                   int8_t *anchor_kind, int32_t *anchor_seg, int32_t *anchor_off, int32_t *snap,
+                   int64_t *edge_off);
+/* Tokens [off, off+n) of the token arena. */
+int prism_arena_read(prism_tree *t, int64_t off, int64_t n, uint32_t *out);
+/* Raw evict_key (kvcache.py:397-414) of one slot as the 192-bit packed key. */
+int prism_evict_key(prism_tree *t, int32_t slot, uint64_t *key3);
+/* Details of the last per-call op: out[5] = evict called, victim-log begin,
+ * victim-log end, tokens freed, status (what last_evicted reflects,
+ * kvcache.py:435). */
+int prism_last_op(prism_tree *t, int64_t *out);
+/* Number of token-arena compactions so far. */
+int64_t prism_compactions(prism_tree *t);
+
+/* ------------------------------------------------------------------- QAS */
+typedef struct {
+  int64_t dispatch_budget, cold_quota, front_width, signature_size;
+  double w_g, w_a, w_n, alpha_size, beta_util;
+} prism_qas_config; /* SchedulerConfig + PriorityWeights, scheduler.py:19-43 */
+
+typedef struct prism_qas prism_qas;
+prism_qas *prism_qas_create(int32_t device);
+void prism_qas_destroy(prism_qas *q);
+
+/* schedule_round -- scheduler.py:192-273 over dense segment ids [0, nseg).
+ * Host buffers.  Outputs as in oracle/oracle.h oq_round. */
+int prism_qas_round(prism_qas *q, int64_t P, const int64_t *ids, const double *arrival,
+                    const int64_t *sk_off, const int32_t *sk, const uint8_t *reorderable,
+                    int64_t A, const int64_t *act_off, const int32_t *act_sk, int32_t nseg,
+                    const prism_qas_config *cfg, int64_t *hot, int64_t *nhot, int64_t *cold,
+                    int64_t *ncold, int32_t *aligned, int32_t *sig, int32_t *siglen, int64_t *rank,
+                    int64_t *bucket, double *bscore, int64_t *nbuckets, int32_t *g, int32_t *a,
+                    int32_t *nd, double *prio, uint8_t *dom);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,875 @@
+// dart.cu -- host runtime + C ABI of the device DART tree (see include/prism.h).
+//
+// The host side owns the device memory (slot SoA, child table, token arena,
+// eviction list, victim log), launches the kernels of dart_kernels.cuh on
+// one stream per tree, and services the commit kernel's resumable stops:
+// NEED_BUILD (eviction order), NEED_SLOTS / NEED_ARENA / NEED_HASH (grow,
+// compact, rehash).  All tree state lives in HBM; nothing is mirrored on the
+// host, and there is no CPU execution path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <cub/cub.cuh>
+#include <string>
+#include <vector>
+
+#include "../../include/prism.h"
+#include "dart_kernels.cuh"
+
+using namespace prism;
+
+namespace {
+thread_local std::string g_err;
+
+struct Key3Decomp {
+  __host__ __device__ ::cuda::std::tuple<uint64_t &, uint64_t &, uint64_t &> operator()(Key3 &k) const {
+    return {k.w0, k.w1, k.w2};
+  }
+};
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(x)                                                                                \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(PRISM_CUDA, std::string("CUDA error ") + cudaGetErrorString(e_) + " in " #x); \
+  } while (0)
+
+template <class T>
+cudaError_t dalloc(T **p, int64_t n) {
+  return cudaMalloc((void **)p, sizeof(T) * (size_t)std::max<int64_t>(n, 1));
+}
+
+int64_t next_pow2(int64_t x) {
+  int64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+constexpr int TPB = 256;
+inline unsigned blocks_for(int64_t n, int tpb = TPB) { return (unsigned)((n + tpb - 1) / tpb); }
+}  // namespace
+
+struct prism_tree {
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  DT d{};
+  Ctrl *hctrl = nullptr;  // pinned
+  int64_t protect_budget = 0;
+  // candidate buffers (gather output / sort input), sized S
+  Key3 *ck = nullptr;
+  uint64_t *cv = nullptr;
+  int64_t *d_count = nullptr;
+  int64_t *h_small = nullptr;  // pinned scratch
+  void *cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  // per-call staging
+  uint32_t *d_path = nullptr;
+  int64_t path_cap = 0;
+  int32_t *d_aoff = nullptr, *d_aseg = nullptr, *d_asnap = nullptr;
+  int8_t *d_akind = nullptr;
+  int64_t anc_cap = 0;
+  OpRes *d_res = nullptr, *h_res = nullptr;
+  int32_t *d_vis_slots = nullptr;
+  int64_t *d_vis_ids = nullptr;
+  int64_t vis_cap = 0;
+  // wave staging for the host-buffer entry point
+  int64_t *d_poff = nullptr, *d_aoffs = nullptr;
+  int64_t woff_cap = 0;
+  uint32_t *d_wtok = nullptr;
+  int64_t wtok_cap = 0;
+  int32_t *d_waoff = nullptr, *d_waseg = nullptr, *d_wasnap = nullptr;
+  int8_t *d_wakind = nullptr;
+  int64_t wanc_cap = 0;
+  int64_t *d_hits = nullptr, *d_lids = nullptr;
+  int32_t *d_lslots = nullptr;
+  int64_t wout_cap = 0;
+  // pre-match
+  int32_t *d_pm_meta = nullptr, *d_pm_chain = nullptr;
+  int64_t pm_cap = 0;
+  // protection scratch
+  int64_t *d_prot_ids = nullptr;
+  int64_t prot_cap = 0;
+  int64_t compactions = 0;
+};
+
+namespace {
+
+// ----------------------------------------------------------------- slot arrays
+struct SlotField {
+  void **ptr;
+  size_t elem;
+};
+
+std::vector<SlotField> slot_fields(prism_tree *t) {
+  DT &d = t->d;
+  return {
+      {(void **)&d.nid, 8},    {(void **)&d.par, 4},    {(void **)&d.ftok, 4},   {(void **)&d.eoff, 8},
+      {(void **)&d.elen, 4},   {(void **)&d.dend, 4},   {(void **)&d.nch, 4},    {(void **)&d.ref, 4},
+      {(void **)&d.last, 8},   {(void **)&d.hits, 4},   {(void **)&d.kind, 1},   {(void **)&d.seg, 4},
+      {(void **)&d.prot, 1},   {(void **)&d.hasanc, 1}, {(void **)&d.akind, 1},  {(void **)&d.aseg, 4},
+      {(void **)&d.aoff, 4},   {(void **)&d.snap, 12},  {(void **)&d.hslot, 4},  {(void **)&d.kver, 4},
+      {(void **)&d.wmod, 4},   {(void **)&d.wchild, 4}, {(void **)&d.waitf, 4},  {(void **)&d.guard, 4},
+      {(void **)&d.kw, sizeof(Key3)}, {(void **)&d.eff, 4}, {(void **)&d.freelist, 4},
+      {(void **)&d.Lk, sizeof(Key3)}, {(void **)&d.Lv, 8},
+  };
+}
+
+int alloc_slots(prism_tree *t, int32_t S) {
+  for (auto &f : slot_fields(t)) {
+    CK(cudaMalloc(f.ptr, f.elem * (size_t)S));
+    CK(cudaMemsetAsync(*f.ptr, 0, f.elem * (size_t)S, t->st));
+  }
+  CK(dalloc(&t->ck, S));
+  CK(dalloc(&t->cv, S));
+  t->d.S = S;
+  return PRISM_OK;
+}
+
+int grow_slots(prism_tree *t, int64_t need_total) {
+  int64_t S2 = (int64_t)t->d.S * 2;
+  while (S2 < need_total) S2 *= 2;
+  if (S2 > 0x7fffff00) return fail(PRISM_FATAL, "slot capacity overflow");
+  const int32_t S = t->d.S;
+  for (auto &f : slot_fields(t)) {
+    void *np = nullptr;
+    CK(cudaMalloc(&np, f.elem * (size_t)S2));
+    CK(cudaMemsetAsync(np, 0, f.elem * (size_t)S2, t->st));
+    CK(cudaMemcpyAsync(np, *f.ptr, f.elem * (size_t)S, cudaMemcpyDeviceToDevice, t->st));
+    CK(cudaStreamSynchronize(t->st));
+    CK(cudaFree(*f.ptr));
+    *f.ptr = np;
+  }
+  CK(cudaFree(t->ck));
+  CK(cudaFree(t->cv));
+  CK(dalloc(&t->ck, S2));
+  CK(dalloc(&t->cv, S2));
+  t->d.S = (int32_t)S2;
+  return PRISM_OK;
+}
+
+int pull_ctrl(prism_tree *t) {
+  CK(cudaMemcpyAsync(t->hctrl, t->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  return PRISM_OK;
+}
+
+int push_ctrl(prism_tree *t) {
+  CK(cudaMemcpyAsync(t->d.ctrl, t->hctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, t->st));
+  return PRISM_OK;
+}
+
+int ensure_cub(prism_tree *t, size_t bytes) {
+  if (bytes <= t->cub_bytes) return PRISM_OK;
+  if (t->cub_tmp) CK(cudaFree(t->cub_tmp));
+  t->cub_bytes = bytes + bytes / 4 + 4096;
+  CK(cudaMalloc(&t->cub_tmp, t->cub_bytes));
+  return PRISM_OK;
+}
+
+// sort n Key3/uint64 pairs from (t->ck, t->cv) into (kout, vout)
+int sort_pairs(prism_tree *t, int64_t n, Key3 *kout, uint64_t *vout, int bits) {
+  if (n <= 0) return PRISM_OK;
+  size_t bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, t->ck, kout, t->cv, vout, (int)n, Key3Decomp{}, 0,
+                                     bits, t->st));
+  int rc = ensure_cub(t, bytes);
+  if (rc) return rc;
+  bytes = t->cub_bytes;
+  CK(cub::DeviceRadixSort::SortPairs(t->cub_tmp, bytes, t->ck, kout, t->cv, vout, (int)n, Key3Decomp{}, 0,
+                                     bits, t->st));
+  return PRISM_OK;
+}
+
+// ------------------------------------------------------------ eviction order
+int build_list(prism_tree *t) {
+  const int32_t hw = t->hctrl->hw;
+  CK(cudaMemsetAsync(t->d_count, 0, sizeof(int64_t), t->st));
+  k_build_keys<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw);
+  k_propagate<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw);
+  k_gather<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw, t->ck, t->cv, t->d_count);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(t->h_small, t->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  const int64_t m = t->h_small[0];
+  int rc = sort_pairs(t, m, t->d.Lk, t->d.Lv, evict_key_bits(t->d.policy));
+  if (rc) return rc;
+  k_list_ready<<<1, 1, 0, t->st>>>(t->d, t->d_count);
+  CK(cudaGetLastError());
+  return PRISM_OK;
+}
+
+int rehash(prism_tree *t, int64_t extra) {
+  int64_t live = t->hctrl->hlive + extra;
+  const int64_t cap = (int64_t)(t->d.hmask + 1);
+  const int64_t want = std::max<int64_t>(cap, next_pow2(4 * (live + 64)));  // never shrinks
+  HEnt *nt = nullptr;
+  CK(dalloc(&nt, want));
+  CK(cudaMemsetAsync(nt, 0xFF, sizeof(HEnt) * (size_t)want, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  CK(cudaFree(t->d.ht));
+  t->d.ht = nt;
+  t->d.hmask = (uint64_t)(want - 1);
+  CK(cudaMemsetAsync(t->d_count, 0, sizeof(int64_t), t->st));
+  const int32_t hw = t->hctrl->hw;
+  k_rehash<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw, t->d_count);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(t->h_small, t->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  t->hctrl->hlive = t->h_small[0];
+  t->hctrl->htomb = 0;
+  return push_ctrl(t);
+}
+
+int compact_arena(prism_tree *t, int64_t need) {
+  const int32_t hw = t->hctrl->hw;
+  int64_t *len = nullptr, *off = nullptr;
+  CK(dalloc(&len, hw + 1));
+  CK(dalloc(&off, hw + 1));
+  k_compact_len<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw, len);
+  size_t bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, len, off, (int)hw, t->st));
+  int rc = ensure_cub(t, bytes);
+  if (rc) return rc;
+  bytes = t->cub_bytes;
+  CK(cub::DeviceScan::ExclusiveSum(t->cub_tmp, bytes, len, off, (int)hw, t->st));
+  int64_t h2[2];
+  CK(cudaMemcpyAsync(&h2[0], off + hw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaMemcpyAsync(&h2[1], len + hw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  const int64_t live = h2[0] + h2[1];
+  int64_t cap = t->d.acap;
+  while (live + need > cap / 2) cap *= 2;
+  uint32_t *na = nullptr;
+  CK(dalloc(&na, cap));
+  k_compact_copy<<<blocks_for((int64_t)hw * 32), TPB, 0, t->st>>>(t->d, hw, off, na);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(t->st));
+  CK(cudaFree(t->d.tok));
+  CK(cudaFree(len));
+  CK(cudaFree(off));
+  t->d.tok = na;
+  t->d.acap = cap;
+  t->hctrl->arena_top = live;
+  t->compactions++;
+  return push_ctrl(t);
+}
+
+// run the commit kernel until DONE/CAPACITY, servicing resumable stops
+int run_commit(prism_tree *t, CommitArgs a) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)COMMIT_SMEM));
+    attr_set = true;
+  }
+  for (int iter = 0; iter < 1000000; iter++) {
+    k_commit<<<1, 32, COMMIT_SMEM, t->st>>>(t->d, a);
+    CK(cudaGetLastError());
+    int rc = pull_ctrl(t);
+    if (rc) return rc;
+    a.reset = 0;
+    Ctrl &c = *t->hctrl;
+    if (c.fatal) return fail(PRISM_FATAL, "device commit fatal error code " + std::to_string(c.fatal));
+    switch (c.status) {
+      case ST_DONE:
+      case ST_CAPACITY:
+        return PRISM_OK;
+      case ST_NEED_BUILD:
+      case ST_NEED_REBUILD:
+        rc = build_list(t);
+        break;
+      case ST_NEED_SLOTS:
+        rc = grow_slots(t, (int64_t)c.hw + 2 + MAX_ANCH);
+        break;
+      case ST_NEED_ARENA: {
+        const int64_t n = a.mode == 1 ? (int64_t)MAX_PATH : a.op_n;
+        rc = compact_arena(t, n);
+        break;
+      }
+      case ST_NEED_HASH:
+        rc = rehash(t, 2 + MAX_ANCH);
+        break;
+      default:
+        return fail(PRISM_FATAL, "unexpected commit status " + std::to_string(c.status));
+    }
+    if (rc) return rc;
+  }
+  return fail(PRISM_FATAL, "commit did not converge");
+}
+
+template <class T>
+int ensure_buf(T **p, int64_t &cap, int64_t need) {
+  if (need <= cap && *p) return PRISM_OK;
+  if (*p) CK(cudaFree(*p));
+  int64_t c = std::max<int64_t>(next_pow2(std::max<int64_t>(need, 1)), 64);
+  CK(dalloc(p, c));
+  cap = c;
+  return PRISM_OK;
+}
+
+int stage_anchors(prism_tree *t, int64_t na, const int32_t *a_off, const int8_t *a_kind,
+                  const int32_t *a_seg, const int32_t *a_snap) {
+  if (na > t->anc_cap || !t->d_aoff) {
+    int64_t c = std::max<int64_t>(next_pow2(na), 64);
+    if (t->d_aoff) {
+      CK(cudaFree(t->d_aoff));
+      CK(cudaFree(t->d_akind));
+      CK(cudaFree(t->d_aseg));
+      CK(cudaFree(t->d_asnap));
+    }
+    CK(dalloc(&t->d_aoff, c));
+    CK(dalloc(&t->d_akind, c));
+    CK(dalloc(&t->d_aseg, c));
+    CK(dalloc(&t->d_asnap, 3 * c));
+    t->anc_cap = c;
+  }
+  if (na > 0) {
+    CK(cudaMemcpyAsync(t->d_aoff, a_off, sizeof(int32_t) * na, cudaMemcpyHostToDevice, t->st));
+    CK(cudaMemcpyAsync(t->d_akind, a_kind, sizeof(int8_t) * na, cudaMemcpyHostToDevice, t->st));
+    CK(cudaMemcpyAsync(t->d_aseg, a_seg, sizeof(int32_t) * na, cudaMemcpyHostToDevice, t->st));
+    CK(cudaMemcpyAsync(t->d_asnap, a_snap, sizeof(int32_t) * 3 * na, cudaMemcpyHostToDevice, t->st));
+  }
+  return PRISM_OK;
+}
+
+CommitArgs one_op(prism_tree *t, int type, int64_t n, int64_t na, int64_t k) {
+  CommitArgs a{};
+  a.mode = 0;
+  a.reset = 1;
+  a.op_type = type;
+  a.nops = 1;
+  a.op_k = k;
+  a.op_n = n;
+  a.op_na = na;
+  a.tok = t->d_path;
+  a.a_off = t->d_aoff;
+  a.a_kind = t->d_akind;
+  a.a_seg = t->d_aseg;
+  a.a_snap = t->d_asnap;
+  a.res = t->d_res;
+  return a;
+}
+
+int validate_anchors(int64_t n, int64_t na, const int32_t *a_off, const int8_t *a_kind,
+                     const int32_t *a_seg) {
+  for (int64_t j = 1; j < na; j++)
+    if (a_off[j] < a_off[j - 1]) return fail(PRISM_INVALID, "anchor offsets must be sorted");
+  if (na > 0 && a_off[na - 1] > n) return fail(PRISM_INVALID, "anchor offset beyond path length");
+  for (int64_t j = 0; j < na; j++) {
+    if (a_kind[j] < 0 || a_kind[j] > 2) return fail(PRISM_INVALID, "bad anchor kind");
+    if (a_kind[j] == K_REUSABLE && a_seg[j] == SEG_NONE)
+      return fail(PRISM_INVALID, "reusable anchor requires segment_id");
+  }
+  if (na > MAX_ANCH) return fail(PRISM_INVALID, "too many anchors for one insert");
+  return PRISM_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char *prism_last_error(void) { return g_err.c_str(); }
+
+int prism_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+prism_tree *prism_tree_create(int64_t capacity_tokens, int32_t policy, int64_t protect_budget,
+                              int64_t initial_slots, int64_t initial_arena_tokens, int32_t device) {
+  if (capacity_tokens <= 0 || protect_budget < 0 || policy < 0 || policy > 3) {
+    fail(PRISM_INVALID, "invalid CacheConfig");
+    return nullptr;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    fail(PRISM_CUDA, "no CUDA device: the PRISM device tree has no CPU fallback");
+    return nullptr;
+  }
+  prism_tree *t = new prism_tree();
+  t->dev = device;
+  auto bad = [&](const char *m) {
+    fail(PRISM_CUDA, std::string("prism_tree_create: ") + m + ": " + cudaGetErrorString(cudaGetLastError()));
+    delete t;
+    return (prism_tree *)nullptr;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) return bad("cudaSetDevice");
+  if (cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking) != cudaSuccess) return bad("stream");
+  int64_t S = std::max<int64_t>(initial_slots > 0 ? initial_slots : 4096, 64);
+  S = std::min<int64_t>(next_pow2(S), 1ll << 30);
+  t->d.policy = policy;
+  t->d.capacity = capacity_tokens;
+  t->protect_budget = protect_budget;
+  if (alloc_slots(t, (int32_t)S)) return bad("slots");
+  const int64_t H = next_pow2(4 * S);
+  if (dalloc(&t->d.ht, H) != cudaSuccess) return bad("hash");
+  cudaMemsetAsync(t->d.ht, 0xFF, sizeof(HEnt) * H, t->st);
+  t->d.hmask = (uint64_t)(H - 1);
+  t->d.acap = std::max<int64_t>(initial_arena_tokens > 0 ? initial_arena_tokens : 1 << 16, MAX_PATH * 2);
+  if (dalloc(&t->d.tok, t->d.acap) != cudaSuccess) return bad("arena");
+  t->d.Hcap = 8192;
+  if (dalloc(&t->d.Hk, t->d.Hcap) != cudaSuccess || dalloc(&t->d.Hv, t->d.Hcap) != cudaSuccess)
+    return bad("heap");
+  t->d.vcap = 1 << 20;
+  if (dalloc(&t->d.vlog, t->d.vcap) != cudaSuccess) return bad("vlog");
+  t->d.npri = 0;
+  t->d.nact = 0;
+  if (dalloc(&t->d.pri, 1) != cudaSuccess || dalloc(&t->d.act, 1) != cudaSuccess) return bad("pri");
+  if (dalloc(&t->d.ctrl, 1) != cudaSuccess) return bad("ctrl");
+  if (cudaMallocHost((void **)&t->hctrl, sizeof(Ctrl)) != cudaSuccess) return bad("pinned");
+  if (cudaMallocHost((void **)&t->h_small, 64 * sizeof(int64_t)) != cudaSuccess) return bad("pinned");
+  if (cudaMallocHost((void **)&t->h_res, sizeof(OpRes)) != cudaSuccess) return bad("pinned");
+  if (dalloc(&t->d_res, 1) != cudaSuccess || dalloc(&t->d_count, 4) != cudaSuccess) return bad("res");
+  // root (kvcache.py:123-124): id 0, SYSTEM, empty edge
+  memset(t->hctrl, 0, sizeof(Ctrl));
+  t->hctrl->hw = 1;
+  t->hctrl->next_id = 1;
+  int32_t negi = -1;
+  uint8_t sys = K_SYSTEM;
+  int32_t none = SEG_NONE;
+  cudaMemcpyAsync(t->d.par, &negi, sizeof(int32_t), cudaMemcpyHostToDevice, t->st);
+  cudaMemcpyAsync(t->d.kind, &sys, 1, cudaMemcpyHostToDevice, t->st);
+  cudaMemcpyAsync(t->d.seg, &none, sizeof(int32_t), cudaMemcpyHostToDevice, t->st);
+  cudaMemcpyAsync(t->d.hslot, &negi, sizeof(int32_t), cudaMemcpyHostToDevice, t->st);
+  if (push_ctrl(t) != PRISM_OK) return bad("ctrl init");
+  if (cudaStreamSynchronize(t->st) != cudaSuccess) return bad("init sync");
+  return t;
+}
+
+void prism_tree_destroy(prism_tree *t) {
+  if (!t) return;
+  cudaSetDevice(t->dev);
+  cudaStreamSynchronize(t->st);
+  for (auto &f : slot_fields(t)) cudaFree(*f.ptr);
+  void *bufs[] = {t->d.ht,     t->d.tok,     t->d.Hk,      t->d.Hv,     t->d.vlog,    t->d.pri,
+                  t->d.act,    t->d.ctrl,    t->ck,        t->cv,       t->d_count,   t->cub_tmp,
+                  t->d_path,   t->d_aoff,    t->d_akind,   t->d_aseg,   t->d_asnap,   t->d_res,
+                  t->d_vis_slots, t->d_vis_ids, t->d_poff, t->d_aoffs,  t->d_wtok,    t->d_waoff,
+                  t->d_waseg,  t->d_wasnap,  t->d_wakind,  t->d_hits,   t->d_lids,    t->d_lslots,
+                  t->d_pm_meta, t->d_pm_chain, t->d_prot_ids};
+  for (void *p : bufs)
+    if (p) cudaFree(p);
+  cudaFreeHost(t->hctrl);
+  cudaFreeHost(t->h_small);
+  cudaFreeHost(t->h_res);
+  cudaStreamDestroy(t->st);
+  delete t;
+}
+
+int prism_match(prism_tree *t, const uint32_t *path, int64_t n, int64_t *hit, int32_t *visited_slots,
+                int64_t *visited_ids, int64_t *n_visited) {
+  if (n < 0 || n > MAX_PATH) return fail(PRISM_INVALID, "path length out of range");
+  cudaSetDevice(t->dev);
+  int rc = ensure_buf(&t->d_path, t->path_cap, n);
+  if (rc) return rc;
+  if (n > t->vis_cap || !t->d_vis_slots) {
+    if (t->d_vis_slots) {
+      CK(cudaFree(t->d_vis_slots));
+      CK(cudaFree(t->d_vis_ids));
+    }
+    t->vis_cap = std::max<int64_t>(next_pow2(n), 64);
+    CK(dalloc(&t->d_vis_slots, t->vis_cap));
+    CK(dalloc(&t->d_vis_ids, t->vis_cap));
+  }
+  if (n) CK(cudaMemcpyAsync(t->d_path, path, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, t->st));
+  CommitArgs a = one_op(t, OP_MATCH, n, 0, 0);
+  a.vis_slots = t->d_vis_slots;
+  a.vis_ids = t->d_vis_ids;
+  rc = run_commit(t, a);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(t->h_res, t->d_res, sizeof(OpRes), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  *hit = t->h_res->hit;
+  const int64_t nv = t->h_res->nvis;
+  if (n_visited) *n_visited = nv;
+  if (nv > 0 && visited_slots)
+    CK(cudaMemcpyAsync(visited_slots, t->d_vis_slots, sizeof(int32_t) * nv, cudaMemcpyDeviceToHost, t->st));
+  if (nv > 0 && visited_ids)
+    CK(cudaMemcpyAsync(visited_ids, t->d_vis_ids, sizeof(int64_t) * nv, cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  return PRISM_OK;
+}
+
+// last-op details for the Python binding: [evicted, vbeg, vend, freed, status]
+int prism_last_op(prism_tree *t, int64_t *out) {
+  out[0] = t->h_res->evicted;
+  out[1] = t->h_res->vbeg;
+  out[2] = t->h_res->vend;
+  out[3] = t->h_res->freed;
+  out[4] = t->h_res->status;
+  return PRISM_OK;
+}
+
+int prism_insert(prism_tree *t, const uint32_t *path, int64_t n, int64_t na, const int32_t *a_off,
+                 const int8_t *a_kind, const int32_t *a_seg, const int32_t *a_snap, int32_t *leaf_slot,
+                 int64_t *leaf_id) {
+  if (n < 0 || n > MAX_PATH) return fail(PRISM_INVALID, "path length out of range");
+  int rc = validate_anchors(n, na, a_off, a_kind, a_seg);
+  if (rc) return rc;
+  cudaSetDevice(t->dev);
+  rc = ensure_buf(&t->d_path, t->path_cap, n);
+  if (rc) return rc;
+  rc = stage_anchors(t, na, a_off, a_kind, a_seg, a_snap);
+  if (rc) return rc;
+  if (n) CK(cudaMemcpyAsync(t->d_path, path, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, t->st));
+  rc = run_commit(t, one_op(t, OP_INSERT, n, na, 0));
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(t->h_res, t->d_res, sizeof(OpRes), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  if (t->h_res->status == ST_CAPACITY) return fail(PRISM_CAPACITY, "path cannot fit even after maximal eviction");
+  *leaf_slot = t->h_res->leaf_slot;
+  *leaf_id = t->h_res->leaf_id;
+  return PRISM_OK;
+}
+
+int prism_release(prism_tree *t, int64_t n, const int32_t *slots, const int64_t *ids) {
+  if (n <= 0) return PRISM_OK;
+  cudaSetDevice(t->dev);
+  int32_t *ds = nullptr;
+  int64_t *di = nullptr, *dout = nullptr;
+  CK(dalloc(&ds, n));
+  CK(dalloc(&di, n));
+  CK(dalloc(&dout, 1));
+  CK(cudaMemcpyAsync(ds, slots, sizeof(int32_t) * n, cudaMemcpyHostToDevice, t->st));
+  CK(cudaMemcpyAsync(di, ids, sizeof(int64_t) * n, cudaMemcpyHostToDevice, t->st));
+  k_release_seq<<<1, 32, 0, t->st>>>(t->d, n, ds, di, dout);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(t->h_small, dout, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  cudaFree(ds);
+  cudaFree(di);
+  cudaFree(dout);
+  if (t->h_small[0] >= 0) return fail(PRISM_RELEASE, "release of a path that is not currently pinned");
+  return PRISM_OK;
+}
+
+int prism_release_device(prism_tree *t, int64_t n, const int32_t *slots, const int64_t *ids, void *stream) {
+  (void)ids;
+  if (n <= 0) return PRISM_OK;
+  cudaSetDevice(t->dev);
+  cudaStream_t s = stream ? (cudaStream_t)stream : t->st;
+  k_release_par<<<blocks_for(n), TPB, 0, s>>>(t->d, n, slots);
+  CK(cudaGetLastError());
+  return PRISM_OK;
+}
+
+int prism_evict(prism_tree *t, int64_t k_free, int64_t *freed) {
+  if (k_free < 0) return fail(PRISM_INVALID, "k_free must be >= 0");
+  cudaSetDevice(t->dev);
+  int rc = run_commit(t, one_op(t, OP_EVICT, 0, 0, k_free));
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(t->h_res, t->d_res, sizeof(OpRes), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  *freed = t->h_res->freed;
+  return PRISM_OK;
+}
+
+int prism_set_protection(prism_tree *t, int64_t n, const int32_t *segs, const double *vals,
+                         int64_t *out_ids, int64_t *n_out) {
+  cudaSetDevice(t->dev);
+  int32_t nseg = 0;
+  for (int64_t i = 0; i < n; i++) {
+    if (segs[i] < 0 || segs[i] == SEG_NONE) return fail(PRISM_INVALID, "segment ids must be >= 0");
+    if (vals[i] != vals[i]) return fail(PRISM_INVALID, "NaN dispatch priority");
+    nseg = std::max(nseg, segs[i] + 1);
+  }
+  std::vector<double> dense((size_t)std::max(nseg, 1), 0.0);
+  for (int64_t i = 0; i < n; i++) dense[segs[i]] = vals[i];  // dict(): last write wins
+  if (nseg > t->d.npri) {
+    CK(cudaFree(t->d.pri));
+    CK(dalloc(&t->d.pri, nseg));
+  }
+  if (nseg) CK(cudaMemcpyAsync(t->d.pri, dense.data(), sizeof(double) * nseg, cudaMemcpyHostToDevice, t->st));
+  t->d.npri = nseg;
+  int rc = pull_ctrl(t);
+  if (rc) return rc;
+  const int32_t hw = t->hctrl->hw;
+  CK(cudaMemsetAsync(t->d_count, 0, sizeof(int64_t), t->st));
+  k_prot_gather<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw, t->ck, t->cv, t->d_count);
+  k_prot_clear<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(t->h_small, t->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  const int64_t m = t->h_small[0];
+  const int64_t f = std::min<int64_t>(t->protect_budget, m);
+  if (f > 0) {
+    rc = sort_pairs(t, m, t->d.Lk, t->d.Lv, 64 + 32 + 40);  // Lk/Lv as scratch: no list survives a call
+    if (rc) return rc;
+    rc = ensure_buf(&t->d_prot_ids, t->prot_cap, f);
+    if (rc) return rc;
+    k_prot_set<<<blocks_for(f), TPB, 0, t->st>>>(t->d, t->d.Lv, f, t->d_prot_ids);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out_ids, t->d_prot_ids, sizeof(int64_t) * f, cudaMemcpyDeviceToHost, t->st));
+  }
+  CK(cudaStreamSynchronize(t->st));
+  *n_out = f;
+  return PRISM_OK;
+}
+
+int prism_note_active(prism_tree *t, int64_t n, const int32_t *segs) {
+  cudaSetDevice(t->dev);
+  int32_t nseg = 0;
+  for (int64_t i = 0; i < n; i++) {
+    if (segs[i] < 0 || segs[i] == SEG_NONE) return fail(PRISM_INVALID, "segment ids must be >= 0");
+    nseg = std::max(nseg, segs[i] + 1);
+  }
+  std::vector<uint8_t> dense((size_t)std::max(nseg, 1), 0);
+  for (int64_t i = 0; i < n; i++) dense[segs[i]] = 1;
+  if (nseg > t->d.nact) {
+    CK(cudaFree(t->d.act));
+    CK(dalloc(&t->d.act, nseg));
+  }
+  if (nseg) CK(cudaMemcpyAsync(t->d.act, dense.data(), (size_t)nseg, cudaMemcpyHostToDevice, t->st));
+  t->d.nact = nseg;
+  int rc = pull_ctrl(t);
+  if (rc) return rc;
+  const int32_t hw = t->hctrl->hw;
+  k_note_active<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(t->st));
+  return PRISM_OK;
+}
+
+int prism_admit_wave_device(prism_tree *t, int64_t B, const int64_t *path_off, const uint32_t *tokens,
+                            const int64_t *anc_off, const int32_t *a_off, const int8_t *a_kind,
+                            const int32_t *a_seg, const int32_t *a_snap, int64_t *hits,
+                            int32_t *leaf_slots, int64_t *leaf_ids, int64_t *n_admitted_host,
+                            void *stream) {
+  cudaSetDevice(t->dev);
+  if (B <= 0) {
+    *n_admitted_host = 0;
+    return PRISM_OK;
+  }
+  if (stream) {  // order after the caller's producers
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, (cudaStream_t)stream));
+    CK(cudaStreamWaitEvent(t->st, ev, 0));
+    CK(cudaEventDestroy(ev));
+  }
+  if (B > t->pm_cap || !t->d_pm_meta) {
+    if (t->d_pm_meta) {
+      CK(cudaFree(t->d_pm_meta));
+      CK(cudaFree(t->d_pm_chain));
+    }
+    t->pm_cap = std::max<int64_t>(next_pow2(B), 64);
+    CK(dalloc(&t->d_pm_meta, 4 * t->pm_cap));
+    CK(dalloc(&t->d_pm_chain, PM_MAX * t->pm_cap));
+  }
+  k_prematch<<<blocks_for(B * 32), TPB, 0, t->st>>>(t->d, B, path_off, tokens, t->d_pm_meta, t->d_pm_chain);
+  CK(cudaGetLastError());
+  CommitArgs a{};
+  a.mode = 1;
+  a.reset = 1;
+  a.nops = (int32_t)(2 * B);
+  a.poff = path_off;
+  a.tok = tokens;
+  a.aoffs = anc_off;
+  a.a_off = a_off;
+  a.a_kind = a_kind;
+  a.a_seg = a_seg;
+  a.a_snap = a_snap;
+  a.pm_meta = t->d_pm_meta;
+  a.pm_chain = t->d_pm_chain;
+  a.hits = hits;
+  a.leaf_slots = leaf_slots;
+  a.leaf_ids = leaf_ids;
+  int rc = run_commit(t, a);
+  if (rc) return rc;
+  *n_admitted_host = t->hctrl->n_admitted;
+  if (stream) {
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, t->st));
+    CK(cudaStreamWaitEvent((cudaStream_t)stream, ev, 0));
+    CK(cudaEventDestroy(ev));
+  }
+  return PRISM_OK;
+}
+
+int prism_admit_wave(prism_tree *t, int64_t B, const int64_t *path_off, const uint32_t *tokens,
+                     const int64_t *anc_off, const int32_t *a_off, const int8_t *a_kind, const int32_t *a_seg,
+                     const int32_t *a_snap, int64_t *hits, int32_t *leaf_slots, int64_t *leaf_ids,
+                     int64_t *n_admitted) {
+  cudaSetDevice(t->dev);
+  if (B <= 0) {
+    *n_admitted = 0;
+    return PRISM_OK;
+  }
+  for (int64_t j = 0; j < B; j++) {
+    const int64_t n = path_off[j + 1] - path_off[j];
+    if (n < 0 || n > MAX_PATH) return fail(PRISM_INVALID, "path length out of range");
+    const int64_t a0 = anc_off[j], na = anc_off[j + 1] - a0;
+    int rc = validate_anchors(n, na, a_off + a0, a_kind + a0, a_seg + a0);
+    if (rc) return rc;
+  }
+  const int64_t ntok = path_off[B], nanc = anc_off[B];
+  int64_t aoffs_cap = t->woff_cap;
+  int rc = ensure_buf(&t->d_poff, t->woff_cap, B + 1);
+  if (rc) return rc;
+  rc = ensure_buf(&t->d_aoffs, aoffs_cap, B + 1);
+  if (rc) return rc;
+  rc = ensure_buf(&t->d_wtok, t->wtok_cap, ntok);
+  if (rc) return rc;
+  if (nanc > t->wanc_cap || !t->d_waoff) {
+    int64_t c = std::max<int64_t>(next_pow2(std::max<int64_t>(nanc, 1)), 64);
+    if (t->d_waoff) {
+      CK(cudaFree(t->d_waoff));
+      CK(cudaFree(t->d_wakind));
+      CK(cudaFree(t->d_waseg));
+      CK(cudaFree(t->d_wasnap));
+    }
+    CK(dalloc(&t->d_waoff, c));
+    CK(dalloc(&t->d_wakind, c));
+    CK(dalloc(&t->d_waseg, c));
+    CK(dalloc(&t->d_wasnap, 3 * c));
+    t->wanc_cap = c;
+  }
+  if (B > t->wout_cap || !t->d_hits) {
+    if (t->d_hits) {
+      CK(cudaFree(t->d_hits));
+      CK(cudaFree(t->d_lids));
+      CK(cudaFree(t->d_lslots));
+    }
+    t->wout_cap = std::max<int64_t>(next_pow2(B), 64);
+    CK(dalloc(&t->d_hits, t->wout_cap));
+    CK(dalloc(&t->d_lids, t->wout_cap));
+    CK(dalloc(&t->d_lslots, t->wout_cap));
+  }
+  CK(cudaMemcpyAsync(t->d_poff, path_off, sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, t->st));
+  CK(cudaMemcpyAsync(t->d_aoffs, anc_off, sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, t->st));
+  if (ntok) CK(cudaMemcpyAsync(t->d_wtok, tokens, sizeof(uint32_t) * ntok, cudaMemcpyHostToDevice, t->st));
+  if (nanc) {
+    CK(cudaMemcpyAsync(t->d_waoff, a_off, sizeof(int32_t) * nanc, cudaMemcpyHostToDevice, t->st));
+    CK(cudaMemcpyAsync(t->d_wakind, a_kind, sizeof(int8_t) * nanc, cudaMemcpyHostToDevice, t->st));
+    CK(cudaMemcpyAsync(t->d_waseg, a_seg, sizeof(int32_t) * nanc, cudaMemcpyHostToDevice, t->st));
+    CK(cudaMemcpyAsync(t->d_wasnap, a_snap, sizeof(int32_t) * 3 * nanc, cudaMemcpyHostToDevice, t->st));
+  }
+  int64_t nadm = 0;
+  rc = prism_admit_wave_device(t, B, t->d_poff, t->d_wtok, t->d_aoffs, t->d_waoff, t->d_wakind, t->d_waseg,
+                               t->d_wasnap, t->d_hits, t->d_lslots, t->d_lids, &nadm, nullptr);
+  if (rc) return rc;
+  *n_admitted = nadm;
+  if (nadm > 0) {
+    CK(cudaMemcpyAsync(hits, t->d_hits, sizeof(int64_t) * nadm, cudaMemcpyDeviceToHost, t->st));
+    CK(cudaMemcpyAsync(leaf_slots, t->d_lslots, sizeof(int32_t) * nadm, cudaMemcpyDeviceToHost, t->st));
+    CK(cudaMemcpyAsync(leaf_ids, t->d_lids, sizeof(int64_t) * nadm, cudaMemcpyDeviceToHost, t->st));
+  }
+  CK(cudaStreamSynchronize(t->st));
+  return PRISM_OK;
+}
+
+int prism_stats(prism_tree *t, int64_t *out) {
+  cudaSetDevice(t->dev);
+  int rc = pull_ctrl(t);
+  if (rc) return rc;
+  const Ctrl &c = *t->hctrl;
+  out[0] = c.resident;
+  out[1] = c.clock;
+  out[2] = c.next_id;
+  out[3] = c.hw;
+  out[4] = (int64_t)c.hw - c.free_top;
+  out[5] = c.arena_top;
+  out[6] = c.hlive;
+  out[7] = c.htomb;
+  out[8] = c.vlog_count;
+  out[9] = c.evict_calls;
+  out[10] = c.builds;
+  out[11] = t->d.S;
+  out[12] = t->d.acap;
+  out[13] = (int64_t)(t->d.hmask + 1);
+  out[14] = c.fast_members;
+  out[15] = c.slow_members;
+  return PRISM_OK;
+}
+
+int prism_victims(prism_tree *t, int64_t first, int64_t count, int64_t *ids, int8_t *kinds, int32_t *segs,
+                  uint32_t *first_tok, int32_t *edge_len, int64_t *edge_off) {
+  cudaSetDevice(t->dev);
+  int rc = pull_ctrl(t);
+  if (rc) return rc;
+  if (first < 0 || first + count > t->hctrl->vlog_count || first < t->hctrl->vlog_count - t->d.vcap)
+    return fail(PRISM_INVALID, "victim log range unavailable");
+  std::vector<VRec> buf((size_t)std::max<int64_t>(count, 1));
+  for (int64_t i = 0; i < count;) {
+    const int64_t pos = (first + i) % t->d.vcap;
+    const int64_t run = std::min(count - i, t->d.vcap - pos);
+    CK(cudaMemcpyAsync(buf.data() + i, t->d.vlog + pos, sizeof(VRec) * run, cudaMemcpyDeviceToHost, t->st));
+    i += run;
+  }
+  CK(cudaStreamSynchronize(t->st));
+  for (int64_t i = 0; i < count; i++) {
+    if (ids) ids[i] = buf[i].id;
+    if (kinds) kinds[i] = buf[i].kind;
+    if (segs) segs[i] = buf[i].seg;
+    if (first_tok) first_tok[i] = buf[i].ftok;
+    if (edge_len) edge_len[i] = buf[i].elen;
+    if (edge_off) edge_off[i] = buf[i].eoff;
+  }
+  return PRISM_OK;
+}
+
+int prism_snapshot(prism_tree *t, int64_t cap, int64_t *hw_out, int64_t *node_id, int32_t *parent,
+                   int32_t *edge_len, int8_t *kind, int32_t *seg, int32_t *ref, int64_t *last, int32_t *hits,
+                   int8_t *prot, int8_t *has_anchor, uint32_t *first_tok, int8_t *anchor_kind,
+                   int32_t *anchor_seg, int32_t *anchor_off, int32_t *snap, int64_t *edge_off) {
+  cudaSetDevice(t->dev);
+  int rc = pull_ctrl(t);
+  if (rc) return rc;
+  const int64_t hw = t->hctrl->hw;
+  *hw_out = hw;
+  if (cap < hw) return PRISM_OK;  // caller retries with a larger buffer
+  const DT &d = t->d;
+#define CP(dst, src, T)                                                                            \
+  if (dst) CK(cudaMemcpyAsync(dst, src, sizeof(T) * hw, cudaMemcpyDeviceToHost, t->st))
+  CP(node_id, d.nid, int64_t);
+  CP(parent, d.par, int32_t);
+  CP(edge_len, d.elen, int32_t);
+  CP(kind, d.kind, int8_t);
+  CP(seg, d.seg, int32_t);
+  CP(ref, d.ref, int32_t);
+  CP(last, d.last, int64_t);
+  CP(hits, d.hits, int32_t);
+  CP(prot, d.prot, int8_t);
+  CP(has_anchor, d.hasanc, int8_t);
+  CP(first_tok, d.ftok, uint32_t);
+  CP(anchor_kind, d.akind, int8_t);
+  CP(anchor_seg, d.aseg, int32_t);
+  CP(anchor_off, d.aoff, int32_t);
+  if (snap) CK(cudaMemcpyAsync(snap, d.snap, sizeof(int32_t) * 3 * hw, cudaMemcpyDeviceToHost, t->st));
+  CP(edge_off, d.eoff, int64_t);
+#undef CP
+  CK(cudaStreamSynchronize(t->st));
+  return PRISM_OK;
+}
+
+int prism_arena_read(prism_tree *t, int64_t off, int64_t n, uint32_t *out) {
+  cudaSetDevice(t->dev);
+  if (off < 0 || n < 0 || off + n > t->d.acap) return fail(PRISM_INVALID, "arena range");
+  if (n) CK(cudaMemcpyAsync(out, t->d.tok + off, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  return PRISM_OK;
+}
+
+int prism_evict_key(prism_tree *t, int32_t slot, uint64_t *key3) {
+  cudaSetDevice(t->dev);
+  Key3 *dk = nullptr;
+  CK(dalloc(&dk, 1));
+  k_key_of<<<1, 32, 0, t->st>>>(t->d, slot, dk);
+  CK(cudaMemcpyAsync(key3, dk, sizeof(Key3), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  cudaFree(dk);
+  return PRISM_OK;
+}
+
+int64_t prism_compactions(prism_tree *t) { return t->compactions; }
+
+}  // extern "C"

@@ -1,0 +1,784 @@
+// qas.cu -- the query-aware scheduler round (scheduler.py:192-273) on sm_100a.
+//
+// One round over a frozen pending snapshot, all passes data-parallel:
+//   q_count        segment counters g (pending) / a (active) / n (dispatch)   (83-89, 205-206, 248)
+//   q_align        per request: front alignment + order-sensitive signature  (109-143)
+//   q_bucket_*     signature buckets in first-seen order, rank inside bucket  (211-223)
+//   q_pairs/...    distinct (bucket, segment) pairs -> utility -> score       (146-171, 225-232)
+//   hot fill       buckets by (-score, creation) with a prefix sum            (234-240)
+//   cold lane      leftovers by (arrival, id)                                 (242-245)
+//   q_prio         dispatch priorities P-hat over the counter domain          (247-251)
+// Float arithmetic uses explicit round-to-nearest intrinsics (no FMA), so the
+// results equal the reference's Python float expressions; bucket utility sums
+// are exact whenever every term is integer-valued (the default weights).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cub/cub.cuh>
+#include <string>
+#include <vector>
+
+#include "../../include/prism.h"
+
+namespace {
+
+constexpr int QMAXK = 64;
+constexpr int TPB = 256;
+constexpr uint64_t QEMPTY = ~0ull;
+inline unsigned nblk(int64_t n) { return (unsigned)((n + TPB - 1) / TPB); }
+
+thread_local std::string q_err;
+int qfail(int code, const std::string &m) {
+  q_err = m;
+  return code;
+}
+#define QCK(x)                                                                                \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess) return qfail(PRISM_CUDA, std::string("CUDA error ") + cudaGetErrorString(e_) + " in " #x); \
+  } while (0)
+
+struct QCfg {
+  int64_t budget, cold, front, kappa;
+  double wg, wa, wn, alpha, beta;
+};
+
+struct K3 {
+  uint64_t w0, w1, w2;
+};
+struct K3Decomp {
+  __host__ __device__ ::cuda::std::tuple<uint64_t &, uint64_t &, uint64_t &> operator()(K3 &k) const {
+    return {k.w0, k.w1, k.w2};
+  }
+};
+
+__device__ inline uint64_t qmix(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+
+__device__ inline uint64_t ord_f64(double d) {
+  if (d == 0.0) d = 0.0;
+  const uint64_t b = (uint64_t)__double_as_longlong(d);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// pri0(r) = w_g*g + w_a*a   (scheduler.py:208-209)
+__device__ inline double pri0(const QCfg &c, const int32_t *g, const int32_t *a, int32_t s) {
+  return __dadd_rn(__dmul_rn(c.wg, (double)g[s]), __dmul_rn(c.wa, (double)a[s]));
+}
+
+// count_segments: each request contributes once per distinct segment
+__global__ void q_count(int64_t P, const int64_t *__restrict__ off, const int32_t *__restrict__ sk,
+                        int32_t *__restrict__ cnt, const int64_t *__restrict__ subset) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P) return;
+  const int64_t i = subset ? subset[t] : t;
+  const int64_t b = off[i], e = off[i + 1];
+  for (int64_t j = b; j < e; j++) {
+    const int32_t s = sk[j];
+    bool dup = false;
+    for (int64_t q = b; q < j && !dup; q++) dup = sk[q] == s;
+    if (!dup) atomicAdd(&cnt[s], 1);
+  }
+}
+
+// (-pri, seg, index) ascending == pri descending, then seg, then position
+__device__ inline bool rank_before(double pa, int32_t sa, int ia, double pb, int32_t sb, int ib) {
+  if (pa != pb) return pa > pb;
+  if (sa != sb) return sa < sb;
+  return ia < ib;
+}
+
+__global__ void q_align(int64_t P, const int64_t *__restrict__ off, const int32_t *__restrict__ sk,
+                        const uint8_t *__restrict__ reo, const int32_t *__restrict__ g,
+                        const int32_t *__restrict__ a, QCfg c, int32_t *__restrict__ aligned,
+                        int32_t *__restrict__ sig, int32_t *__restrict__ siglen,
+                        uint32_t *__restrict__ sighash, int32_t *__restrict__ err) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const int64_t b = off[i];
+  const int k = (int)(off[i + 1] - b);
+  if (k > QMAXK) {
+    *err = 1;
+    return;
+  }
+  int32_t s[QMAXK];
+  double p[QMAXK];
+  int ord[QMAXK];
+  for (int j = 0; j < k; j++) {
+    s[j] = sk[b + j];
+    p[j] = pri0(c, g, a, s[j]);
+  }
+  int32_t al[QMAXK];
+  // front_align (scheduler.py:109-129)
+  if (!reo[i] || k == 0) {
+    for (int j = 0; j < k; j++) al[j] = s[j];
+  } else {
+    for (int j = 0; j < k; j++) {  // stable insertion sort of indices
+      int q = j;
+      while (q > 0 && rank_before(p[j], s[j], j, p[ord[q - 1]], s[ord[q - 1]], ord[q - 1])) {
+        ord[q] = ord[q - 1];
+        q--;
+      }
+      ord[q] = j;
+    }
+    const int f = (int)(c.front < k ? c.front : k);
+    uint64_t chosen = 0;
+    int w = 0;
+    for (int q = 0; q < f; q++) {
+      al[w++] = s[ord[q]];
+      chosen |= 1ull << ord[q];
+    }
+    for (int j = 0; j < k; j++)
+      if (!((chosen >> j) & 1ull)) al[w++] = s[j];
+  }
+  for (int j = 0; j < k; j++) aligned[b + j] = al[j];
+  // make_signature (scheduler.py:132-143): top-kappa by rank, emitted in aligned order
+  int sl = 0;
+  if (k > 0) {
+    double pa[QMAXK];
+    for (int j = 0; j < k; j++) {
+      pa[j] = pri0(c, g, a, al[j]);
+      int q = j;
+      while (q > 0 && rank_before(pa[j], al[j], j, pa[ord[q - 1]], al[ord[q - 1]], ord[q - 1])) {
+        ord[q] = ord[q - 1];
+        q--;
+      }
+      ord[q] = j;
+    }
+    const int kk = (int)(c.kappa < k ? c.kappa : k);
+    uint64_t chosen = 0;
+    for (int q = 0; q < kk; q++) chosen |= 1ull << ord[q];
+    for (int j = 0; j < k; j++)
+      if ((chosen >> j) & 1ull) sig[i * c.kappa + sl++] = al[j];
+  }
+  siglen[i] = sl;
+  uint32_t h = 2166136261u ^ (uint32_t)sl;
+  for (int j = 0; j < sl; j++) h = (h ^ (uint32_t)sig[i * c.kappa + j]) * 16777619u;
+  sighash[i] = h;
+}
+
+__device__ inline bool sig_eq(const int32_t *sig, const int32_t *siglen, int64_t kappa, int64_t x, int64_t y) {
+  if (siglen[x] != siglen[y]) return false;
+  for (int j = 0; j < siglen[x]; j++)
+    if (sig[x * kappa + j] != sig[y * kappa + j]) return false;
+  return true;
+}
+
+// signature -> bucket slot; table key = hash << 32 | representative request
+__global__ void q_bucket_insert(int64_t P, const int32_t *__restrict__ sig, const int32_t *__restrict__ siglen,
+                                const uint32_t *__restrict__ sighash, int64_t kappa, uint64_t *tkey,
+                                int32_t *tmin, uint64_t tmask, int32_t *__restrict__ slot_of) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const uint32_t h = sighash[i];
+  const uint64_t mine = ((uint64_t)h << 32) | (uint32_t)i;
+  uint64_t pidx = qmix(h) & tmask;
+  for (;;) {
+    const unsigned long long prev = atomicCAS((unsigned long long *)&tkey[pidx], QEMPTY, mine);
+    if (prev == QEMPTY) {
+      atomicMin(&tmin[pidx], (int32_t)i);
+      slot_of[i] = (int32_t)pidx;
+      return;
+    }
+    if ((uint32_t)(prev >> 32) == h && sig_eq(sig, siglen, kappa, (int64_t)(prev & 0xffffffffu), i)) {
+      atomicMin(&tmin[pidx], (int32_t)i);
+      slot_of[i] = (int32_t)pidx;
+      return;
+    }
+    pidx = (pidx + 1) & tmask;
+  }
+}
+
+__global__ void q_bucket_list(int64_t T, const uint64_t *__restrict__ tkey, const int32_t *__restrict__ tmin,
+                              int32_t *__restrict__ bmin, int32_t *__restrict__ bslot, int64_t *count) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= T || tkey[p] == QEMPTY) return;
+  const int64_t pos = (int64_t)atomicAdd((unsigned long long *)count, 1ull);
+  bmin[pos] = tmin[p];
+  bslot[pos] = (int32_t)p;
+}
+
+__global__ void q_bucket_index(int64_t nb, const int32_t *__restrict__ sorted_slot, int32_t *__restrict__ bidx_of_slot) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < nb) bidx_of_slot[sorted_slot[q]] = (int32_t)q;
+}
+
+__global__ void q_bucket_of(int64_t P, const int32_t *__restrict__ slot_of, const int32_t *__restrict__ bidx_of_slot,
+                            int32_t *__restrict__ bucket, int32_t *__restrict__ iota) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  bucket[i] = bidx_of_slot[slot_of[i]];
+  iota[i] = (int32_t)i;
+}
+
+// sorted (bucket, index) -> bucket start / rank inside bucket
+__global__ void q_rank(int64_t P, const int32_t *__restrict__ sb, const int32_t *__restrict__ si,
+                       int32_t *__restrict__ bstart, int32_t *__restrict__ bend) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= P) return;
+  if (q == 0 || sb[q] != sb[q - 1]) bstart[sb[q]] = (int32_t)q;
+  if (q == P - 1 || sb[q] != sb[q + 1]) bend[sb[q]] = (int32_t)q + 1;
+}
+
+__global__ void q_rank2(int64_t P, const int32_t *__restrict__ sb, const int32_t *__restrict__ si,
+                        const int32_t *__restrict__ bstart, int32_t *__restrict__ rank) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= P) return;
+  rank[si[q]] = (int32_t)q - bstart[sb[q]];
+}
+
+__global__ void q_pair_count(int64_t P, const int64_t *__restrict__ off, const int32_t *__restrict__ sk,
+                             int64_t *__restrict__ cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const int64_t b = off[i], e = off[i + 1];
+  int64_t n = 0;
+  for (int64_t j = b; j < e; j++) {
+    bool dup = false;
+    for (int64_t q = b; q < j && !dup; q++) dup = sk[q] == sk[j];
+    n += !dup;
+  }
+  cnt[i] = n;
+}
+
+// distinct (bucket, segment) pairs of every member; value = provisional flag
+__global__ void q_pair_emit(int64_t P, const int64_t *__restrict__ off, const int32_t *__restrict__ sk,
+                            const int32_t *__restrict__ bucket, const int32_t *__restrict__ rank,
+                            int64_t hot_cap, const int64_t *__restrict__ pos0, uint64_t *__restrict__ pk,
+                            int32_t *__restrict__ pv) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const int64_t b = off[i], e = off[i + 1];
+  int64_t w = pos0[i];
+  const int32_t prov = rank[i] < hot_cap ? 1 : 0;  // members[:hot_capacity] (scheduler.py:229)
+  for (int64_t j = b; j < e; j++) {
+    bool dup = false;
+    for (int64_t q = b; q < j && !dup; q++) dup = sk[q] == sk[j];
+    if (dup) continue;
+    pk[w] = ((uint64_t)(uint32_t)bucket[i] << 32) | (uint32_t)sk[j];
+    pv[w] = prov;
+    w++;
+  }
+}
+
+__global__ void q_heads(int64_t E, const uint64_t *__restrict__ pk, int32_t *__restrict__ head) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < E) head[q] = (q == 0 || pk[q] != pk[q - 1]) ? 1 : 0;
+}
+
+// one thread per distinct (bucket, seg): term = w_g*g + w_a*a + w_n*n_b
+__global__ void q_terms(int64_t E, const uint64_t *__restrict__ pk, const int32_t *__restrict__ head,
+                        const int32_t *__restrict__ hpos, const int32_t *__restrict__ prov_pref,
+                        const int32_t *__restrict__ g, const int32_t *__restrict__ a, QCfg c,
+                        int32_t *__restrict__ hstart, double *__restrict__ term, int32_t *__restrict__ hbucket) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= E || !head[q]) return;
+  const int32_t j = hpos[q];
+  hstart[j] = (int32_t)q;
+  int64_t end = q + 1;
+  while (end < E && !head[end]) end++;
+  const int32_t nbv = prov_pref[end] - prov_pref[q];
+  const int32_t r = (int32_t)(pk[q] & 0xffffffffu);
+  const double t1 = __dmul_rn(c.wg, (double)g[r]);
+  const double t2 = __dmul_rn(c.wa, (double)a[r]);
+  const double t3 = __dmul_rn(c.wn, (double)nbv);
+  term[j] = __dadd_rn(__dadd_rn(t1, t2), t3);
+  hbucket[j] = (int32_t)(pk[q] >> 32);
+}
+
+__global__ void q_bucket_range(int64_t NH, const int32_t *__restrict__ hbucket, int32_t *__restrict__ hb0,
+                               int32_t *__restrict__ hb1) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= NH) return;
+  if (j == 0 || hbucket[j] != hbucket[j - 1]) hb0[hbucket[j]] = (int32_t)j;
+  if (j == NH - 1 || hbucket[j] != hbucket[j + 1]) hb1[hbucket[j]] = (int32_t)j + 1;
+}
+
+// bucket_score (scheduler.py:146-171), one warp per bucket.  The sum runs in
+// ascending segment order; when every term is an exact integer below 2^53
+// the warp sums exactly in int64 (order-free, bit-identical).
+__global__ void q_score(int64_t nb, const int32_t *__restrict__ hb0, const int32_t *__restrict__ hb1,
+                        const double *__restrict__ term, const int32_t *__restrict__ bstart,
+                        const int32_t *__restrict__ bend, QCfg c, double *__restrict__ score,
+                        uint64_t *__restrict__ skey, int32_t *__restrict__ sval) {
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (b >= nb) return;
+  const int32_t j0 = hb0[b], j1 = hb1[b];
+  const int32_t ns = j1 - j0;
+  bool integral = true;
+  long long isum = 0;
+  for (int32_t j = j0 + lane; j < j1; j += 32) {
+    const double t = term[j];
+    if (t != floor(t) || fabs(t) >= 9007199254740992.0) integral = false;
+    else isum += (long long)t;
+  }
+  integral = __all_sync(0xffffffffu, integral);
+  for (int o = 16; o > 0; o >>= 1) isum += __shfl_xor_sync(0xffffffffu, isum, o);
+  double util = 0.0;
+  if (ns > 0) {
+    double sum;
+    if (integral && llabs(isum) < 9007199254740992ll) {
+      sum = (double)isum;
+    } else {
+      sum = 0.0;
+      for (int32_t j = j0; j < j1; j++) sum = (j == j0) ? term[j] : __dadd_rn(sum, term[j]);
+    }
+    util = __ddiv_rn(sum, (double)ns);
+  }
+  const double sz = (double)(bend[b] - bstart[b]);
+  const double sc = __dadd_rn(__dmul_rn(c.alpha, sz), __dmul_rn(c.beta, util));
+  if (lane == 0) {
+    score[b] = sc;
+    skey[b] = ord_f64(-sc);  // sort (-score, creation order): stable radix sort keeps b order
+    sval[b] = (int32_t)b;
+  }
+}
+
+__global__ void q_sizes_sorted(int64_t nb, const int32_t *__restrict__ order, const int32_t *__restrict__ bstart,
+                               const int32_t *__restrict__ bend, int64_t *__restrict__ sz) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < nb) sz[q] = bend[order[q]] - bstart[order[q]];
+}
+
+__global__ void q_take(int64_t nb, const int32_t *__restrict__ order, const int64_t *__restrict__ pre,
+                       const int64_t *__restrict__ sz, int64_t hot_cap, int64_t *__restrict__ take,
+                       int64_t *__restrict__ base) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nb) return;
+  const int32_t b = order[q];
+  int64_t t = hot_cap - pre[q];
+  t = t < 0 ? 0 : (t > sz[q] ? sz[q] : t);
+  take[b] = t;
+  base[b] = pre[q] < hot_cap ? pre[q] : hot_cap;
+}
+
+__global__ void q_hot(int64_t P, const int32_t *__restrict__ bucket, const int32_t *__restrict__ rank,
+                      const int64_t *__restrict__ take, const int64_t *__restrict__ base, int64_t *__restrict__ hot,
+                      uint8_t *__restrict__ sel) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const int32_t b = bucket[i];
+  const bool h = rank[i] < take[b];
+  sel[i] = h ? 1 : 0;
+  if (h) hot[base[b] + rank[i]] = i;
+}
+
+// cold-lane key: (selected, arrival, id) -- leftovers sorted by (arrival, id)
+__global__ void q_cold_keys(int64_t P, const uint8_t *__restrict__ sel, const double *__restrict__ arrival,
+                            const int64_t *__restrict__ ids, K3 *__restrict__ k, int64_t *__restrict__ v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  K3 x;
+  x.w0 = sel[i];
+  x.w1 = ord_f64(arrival[i]);
+  x.w2 = (uint64_t)ids[i] ^ 0x8000000000000000ull;
+  k[i] = x;
+  v[i] = i;
+}
+
+__global__ void q_prio(int32_t nseg, const int32_t *__restrict__ g, const int32_t *__restrict__ a,
+                       const int32_t *__restrict__ nd, QCfg c, double *__restrict__ prio, uint8_t *__restrict__ dom) {
+  const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nseg) return;
+  const bool in = g[r] > 0 || a[r] > 0 || nd[r] > 0;
+  dom[r] = in ? 1 : 0;
+  prio[r] = in ? __dadd_rn(pri0(c, g, a, r), __dmul_rn(c.wn, (double)nd[r])) : 0.0;
+}
+
+template <class T>
+cudaError_t grow(T **p, int64_t &cap, int64_t need) {
+  if (need <= cap && *p) return cudaSuccess;
+  if (*p) cudaFree(*p);
+  int64_t c = 64;
+  while (c < need) c <<= 1;
+  cap = c;
+  return cudaMalloc((void **)p, sizeof(T) * (size_t)c);
+}
+
+}  // namespace
+
+struct prism_qas {
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  void *tmp = nullptr;
+  size_t tmp_bytes = 0;
+  // buffers (device) with capacities
+#define QBUF(T, name) \
+  T *name = nullptr;  \
+  int64_t name##_cap = 0;
+  QBUF(int64_t, ids)
+  QBUF(double, arrival)
+  QBUF(int64_t, off)
+  QBUF(int32_t, sk)
+  QBUF(uint8_t, reo)
+  QBUF(int64_t, aoff)
+  QBUF(int32_t, ask)
+  QBUF(int32_t, g)
+  QBUF(int32_t, a)
+  QBUF(int32_t, nd)
+  QBUF(double, prio)
+  QBUF(uint8_t, dom)
+  QBUF(int32_t, aligned)
+  QBUF(int32_t, sig)
+  QBUF(int32_t, siglen)
+  QBUF(uint32_t, sighash)
+  QBUF(uint64_t, tkey)
+  QBUF(int32_t, tmin)
+  QBUF(int32_t, slot_of)
+  QBUF(int32_t, bmin)
+  QBUF(int32_t, bslot)
+  QBUF(int32_t, bmin2)
+  QBUF(int32_t, bslot2)
+  QBUF(int32_t, bidx_of_slot)
+  QBUF(int32_t, bucket)
+  QBUF(int32_t, iota)
+  QBUF(int32_t, sb)
+  QBUF(int32_t, si)
+  QBUF(int32_t, bstart)
+  QBUF(int32_t, bend)
+  QBUF(int32_t, rank)
+  QBUF(int64_t, pcnt)
+  QBUF(int64_t, ppos)
+  QBUF(uint64_t, pk)
+  QBUF(int32_t, pv)
+  QBUF(uint64_t, pk2)
+  QBUF(int32_t, pv2)
+  QBUF(int32_t, head)
+  QBUF(int32_t, hpos)
+  QBUF(int32_t, ppref)
+  QBUF(int32_t, hstart)
+  QBUF(double, term)
+  QBUF(int32_t, hbucket)
+  QBUF(int32_t, hb0)
+  QBUF(int32_t, hb1)
+  QBUF(double, score)
+  QBUF(uint64_t, skey)
+  QBUF(int32_t, sval)
+  QBUF(uint64_t, skey2)
+  QBUF(int32_t, sval2)
+  QBUF(int64_t, ssz)
+  QBUF(int64_t, spre)
+  QBUF(int64_t, take)
+  QBUF(int64_t, base)
+  QBUF(int64_t, hot)
+  QBUF(uint8_t, sel)
+  QBUF(K3, ck)
+  QBUF(int64_t, cv)
+  QBUF(K3, ck2)
+  QBUF(int64_t, cv2)
+  QBUF(int64_t, small)
+  QBUF(int32_t, err)
+#undef QBUF
+};
+
+namespace {
+int ensure_tmp(prism_qas *q, size_t b) {
+  if (b <= q->tmp_bytes) return PRISM_OK;
+  if (q->tmp) QCK(cudaFree(q->tmp));
+  q->tmp_bytes = b + b / 4 + 4096;
+  QCK(cudaMalloc(&q->tmp, q->tmp_bytes));
+  return PRISM_OK;
+}
+
+// the full round; every pointer argument is DEVICE memory inside q
+int qas_run(prism_qas *q, int64_t P, int64_t A, int32_t nseg, const QCfg &c, int64_t *nhot, int64_t *ncold,
+            int64_t *nbuckets) {
+  cudaStream_t st = q->st;
+  const int32_t S1 = std::max(nseg, 1);
+  QCK(grow(&q->g, q->g_cap, S1));
+  QCK(grow(&q->a, q->a_cap, S1));
+  QCK(grow(&q->nd, q->nd_cap, S1));
+  QCK(grow(&q->prio, q->prio_cap, S1));
+  QCK(grow(&q->dom, q->dom_cap, S1));
+  QCK(grow(&q->err, q->err_cap, 1));
+  QCK(grow(&q->small, q->small_cap, 8));
+  QCK(cudaMemsetAsync(q->g, 0, sizeof(int32_t) * S1, st));
+  QCK(cudaMemsetAsync(q->a, 0, sizeof(int32_t) * S1, st));
+  QCK(cudaMemsetAsync(q->nd, 0, sizeof(int32_t) * S1, st));
+  QCK(cudaMemsetAsync(q->err, 0, sizeof(int32_t), st));
+  const int64_t P1 = std::max<int64_t>(P, 1);
+  if (P > 0) q_count<<<nblk(P), TPB, 0, st>>>(P, q->off, q->sk, q->g, nullptr);
+  if (A > 0) q_count<<<nblk(A), TPB, 0, st>>>(A, q->aoff, q->ask, q->a, nullptr);
+  *nhot = *ncold = *nbuckets = 0;
+  if (P == 0) {
+    q_prio<<<nblk(S1), TPB, 0, st>>>(nseg, q->g, q->a, q->nd, c, q->prio, q->dom);
+    QCK(cudaGetLastError());
+    return PRISM_OK;
+  }
+  int64_t nsk = 0;
+  QCK(cudaMemcpyAsync(&nsk, q->off + P, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  QCK(grow(&q->aligned, q->aligned_cap, std::max<int64_t>(nsk, 1)));
+  QCK(grow(&q->sig, q->sig_cap, P1 * c.kappa));
+  QCK(grow(&q->siglen, q->siglen_cap, P1));
+  QCK(grow(&q->sighash, q->sighash_cap, P1));
+  q_align<<<nblk(P), TPB, 0, st>>>(P, q->off, q->sk, q->reo, q->g, q->a, c, q->aligned, q->sig, q->siglen,
+                                   q->sighash, q->err);
+  // buckets
+  int64_t T = 64;
+  while (T < 2 * P) T <<= 1;
+  QCK(grow(&q->tkey, q->tkey_cap, T));
+  QCK(grow(&q->tmin, q->tmin_cap, T));
+  QCK(grow(&q->slot_of, q->slot_of_cap, P1));
+  QCK(cudaMemsetAsync(q->tkey, 0xFF, sizeof(uint64_t) * T, st));
+  QCK(cudaMemsetAsync(q->tmin, 0x7F, sizeof(int32_t) * T, st));
+  q_bucket_insert<<<nblk(P), TPB, 0, st>>>(P, q->sig, q->siglen, q->sighash, c.kappa, q->tkey, q->tmin,
+                                           (uint64_t)(T - 1), q->slot_of);
+  QCK(grow(&q->bmin, q->bmin_cap, P1));
+  QCK(grow(&q->bslot, q->bslot_cap, P1));
+  QCK(grow(&q->bmin2, q->bmin2_cap, P1));
+  QCK(grow(&q->bslot2, q->bslot2_cap, P1));
+  QCK(cudaMemsetAsync(q->small, 0, sizeof(int64_t), st));
+  q_bucket_list<<<nblk(T), TPB, 0, st>>>(T, q->tkey, q->tmin, q->bmin, q->bslot, q->small);
+  int64_t nb = 0;
+  int32_t err = 0;
+  QCK(cudaMemcpyAsync(&nb, q->small, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  QCK(cudaMemcpyAsync(&err, q->err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  QCK(cudaStreamSynchronize(st));
+  if (err) return qfail(PRISM_INVALID, "skeleton longer than 64 segments");
+  size_t bytes = 0;
+  QCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, q->bmin, q->bmin2, q->bslot, q->bslot2, (int)nb, 0, 32, st));
+  if (ensure_tmp(q, bytes)) return PRISM_CUDA;
+  bytes = q->tmp_bytes;
+  QCK(cub::DeviceRadixSort::SortPairs(q->tmp, bytes, q->bmin, q->bmin2, q->bslot, q->bslot2, (int)nb, 0, 32, st));
+  QCK(grow(&q->bidx_of_slot, q->bidx_of_slot_cap, T));
+  q_bucket_index<<<nblk(nb), TPB, 0, st>>>(nb, q->bslot2, q->bidx_of_slot);
+  QCK(grow(&q->bucket, q->bucket_cap, P1));
+  QCK(grow(&q->iota, q->iota_cap, P1));
+  q_bucket_of<<<nblk(P), TPB, 0, st>>>(P, q->slot_of, q->bidx_of_slot, q->bucket, q->iota);
+  // rank inside bucket: stable sort of (bucket, index)
+  QCK(grow(&q->sb, q->sb_cap, P1));
+  QCK(grow(&q->si, q->si_cap, P1));
+  bytes = 0;
+  QCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, q->bucket, q->sb, q->iota, q->si, (int)P, 0, 32, st));
+  if (ensure_tmp(q, bytes)) return PRISM_CUDA;
+  bytes = q->tmp_bytes;
+  QCK(cub::DeviceRadixSort::SortPairs(q->tmp, bytes, q->bucket, q->sb, q->iota, q->si, (int)P, 0, 32, st));
+  QCK(grow(&q->bstart, q->bstart_cap, std::max<int64_t>(nb, 1)));
+  QCK(grow(&q->bend, q->bend_cap, std::max<int64_t>(nb, 1)));
+  QCK(grow(&q->rank, q->rank_cap, P1));
+  q_rank<<<nblk(P), TPB, 0, st>>>(P, q->sb, q->si, q->bstart, q->bend);
+  q_rank2<<<nblk(P), TPB, 0, st>>>(P, q->sb, q->si, q->bstart, q->rank);
+  // distinct (bucket, segment) pairs
+  const int64_t hot_cap = c.budget - c.cold;
+  QCK(grow(&q->pcnt, q->pcnt_cap, P1 + 1));
+  QCK(grow(&q->ppos, q->ppos_cap, P1 + 1));
+  QCK(cudaMemsetAsync(q->pcnt + P, 0, sizeof(int64_t), st));
+  q_pair_count<<<nblk(P), TPB, 0, st>>>(P, q->off, q->sk, q->pcnt);
+  bytes = 0;
+  QCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, q->pcnt, q->ppos, (int)(P + 1), st));
+  if (ensure_tmp(q, bytes)) return PRISM_CUDA;
+  bytes = q->tmp_bytes;
+  QCK(cub::DeviceScan::ExclusiveSum(q->tmp, bytes, q->pcnt, q->ppos, (int)(P + 1), st));
+  int64_t E = 0;
+  QCK(cudaMemcpyAsync(&E, q->ppos + P, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  QCK(cudaStreamSynchronize(st));
+  const int64_t E1 = std::max<int64_t>(E, 1);
+  QCK(grow(&q->pk, q->pk_cap, E1));
+  QCK(grow(&q->pv, q->pv_cap, E1));
+  QCK(grow(&q->pk2, q->pk2_cap, E1));
+  QCK(grow(&q->pv2, q->pv2_cap, E1));
+  QCK(grow(&q->head, q->head_cap, E1 + 1));
+  QCK(grow(&q->hpos, q->hpos_cap, E1 + 1));
+  QCK(grow(&q->ppref, q->ppref_cap, E1 + 1));
+  QCK(grow(&q->hb0, q->hb0_cap, std::max<int64_t>(nb, 1)));
+  QCK(grow(&q->hb1, q->hb1_cap, std::max<int64_t>(nb, 1)));
+  QCK(cudaMemsetAsync(q->hb0, 0, sizeof(int32_t) * std::max<int64_t>(nb, 1), st));
+  QCK(cudaMemsetAsync(q->hb1, 0, sizeof(int32_t) * std::max<int64_t>(nb, 1), st));
+  QCK(grow(&q->hstart, q->hstart_cap, E1));
+  QCK(grow(&q->term, q->term_cap, E1));
+  QCK(grow(&q->hbucket, q->hbucket_cap, E1));
+  if (E > 0) {
+    q_pair_emit<<<nblk(P), TPB, 0, st>>>(P, q->off, q->sk, q->bucket, q->rank, hot_cap, q->ppos, q->pk, q->pv);
+    bytes = 0;
+    QCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, q->pk, q->pk2, q->pv, q->pv2, (int)E, 0, 64, st));
+    if (ensure_tmp(q, bytes)) return PRISM_CUDA;
+    bytes = q->tmp_bytes;
+    QCK(cub::DeviceRadixSort::SortPairs(q->tmp, bytes, q->pk, q->pk2, q->pv, q->pv2, (int)E, 0, 64, st));
+    q_heads<<<nblk(E), TPB, 0, st>>>(E, q->pk2, q->head);
+    QCK(cudaMemsetAsync(q->head + E, 0, sizeof(int32_t), st));
+    QCK(cudaMemsetAsync(q->pv2 + E, 0, sizeof(int32_t), st));
+    bytes = 0;
+    QCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, q->head, q->hpos, (int)(E + 1), st));
+    if (ensure_tmp(q, bytes)) return PRISM_CUDA;
+    bytes = q->tmp_bytes;
+    QCK(cub::DeviceScan::ExclusiveSum(q->tmp, bytes, q->head, q->hpos, (int)(E + 1), st));
+    bytes = 0;
+    QCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, q->pv2, q->ppref, (int)(E + 1), st));
+    if (ensure_tmp(q, bytes)) return PRISM_CUDA;
+    bytes = q->tmp_bytes;
+    QCK(cub::DeviceScan::ExclusiveSum(q->tmp, bytes, q->pv2, q->ppref, (int)(E + 1), st));
+    int64_t NH = 0;
+    int32_t nh32 = 0;
+    QCK(cudaMemcpyAsync(&nh32, q->hpos + E, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    QCK(cudaStreamSynchronize(st));
+    NH = nh32;
+    q_terms<<<nblk(E), TPB, 0, st>>>(E, q->pk2, q->head, q->hpos, q->ppref, q->g, q->a, c, q->hstart, q->term,
+                                     q->hbucket);
+    q_bucket_range<<<nblk(NH), TPB, 0, st>>>(NH, q->hbucket, q->hb0, q->hb1);
+  }
+  // scores and hot lane
+  QCK(grow(&q->score, q->score_cap, std::max<int64_t>(nb, 1)));
+  QCK(grow(&q->skey, q->skey_cap, std::max<int64_t>(nb, 1)));
+  QCK(grow(&q->sval, q->sval_cap, std::max<int64_t>(nb, 1)));
+  QCK(grow(&q->skey2, q->skey2_cap, std::max<int64_t>(nb, 1)));
+  QCK(grow(&q->sval2, q->sval2_cap, std::max<int64_t>(nb, 1)));
+  q_score<<<nblk(nb * 32), TPB, 0, st>>>(nb, q->hb0, q->hb1, q->term, q->bstart, q->bend, c, q->score, q->skey,
+                                         q->sval);
+  bytes = 0;
+  QCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, q->skey, q->skey2, q->sval, q->sval2, (int)nb, 0, 64, st));
+  if (ensure_tmp(q, bytes)) return PRISM_CUDA;
+  bytes = q->tmp_bytes;
+  QCK(cub::DeviceRadixSort::SortPairs(q->tmp, bytes, q->skey, q->skey2, q->sval, q->sval2, (int)nb, 0, 64, st));
+  QCK(grow(&q->ssz, q->ssz_cap, std::max<int64_t>(nb, 1)));
+  QCK(grow(&q->spre, q->spre_cap, std::max<int64_t>(nb, 1)));
+  QCK(grow(&q->take, q->take_cap, std::max<int64_t>(nb, 1)));
+  QCK(grow(&q->base, q->base_cap, std::max<int64_t>(nb, 1)));
+  q_sizes_sorted<<<nblk(nb), TPB, 0, st>>>(nb, q->sval2, q->bstart, q->bend, q->ssz);
+  bytes = 0;
+  QCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, q->ssz, q->spre, (int)nb, st));
+  if (ensure_tmp(q, bytes)) return PRISM_CUDA;
+  bytes = q->tmp_bytes;
+  QCK(cub::DeviceScan::ExclusiveSum(q->tmp, bytes, q->ssz, q->spre, (int)nb, st));
+  q_take<<<nblk(nb), TPB, 0, st>>>(nb, q->sval2, q->spre, q->ssz, hot_cap, q->take, q->base);
+  QCK(grow(&q->hot, q->hot_cap, P1));
+  QCK(grow(&q->sel, q->sel_cap, P1));
+  q_hot<<<nblk(P), TPB, 0, st>>>(P, q->bucket, q->rank, q->take, q->base, q->hot, q->sel);
+  const int64_t nh = std::min<int64_t>(std::max<int64_t>(hot_cap, 0), P);
+  // cold lane
+  const int64_t nc = std::min<int64_t>(c.cold, P - nh);
+  QCK(grow(&q->ck, q->ck_cap, P1));
+  QCK(grow(&q->cv, q->cv_cap, P1));
+  QCK(grow(&q->ck2, q->ck2_cap, P1));
+  QCK(grow(&q->cv2, q->cv2_cap, P1));
+  if (nc > 0) {
+    q_cold_keys<<<nblk(P), TPB, 0, st>>>(P, q->sel, q->arrival, q->ids, q->ck, q->cv);
+    bytes = 0;
+    QCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, q->ck, q->ck2, q->cv, q->cv2, (int)P, K3Decomp{}, 0,
+                                        1 + 128, st));
+    if (ensure_tmp(q, bytes)) return PRISM_CUDA;
+    bytes = q->tmp_bytes;
+    QCK(cub::DeviceRadixSort::SortPairs(q->tmp, bytes, q->ck, q->ck2, q->cv, q->cv2, (int)P, K3Decomp{}, 0,
+                                        1 + 128, st));
+    // n_disp over hot + cold (scheduler.py:247-248)
+    q_count<<<nblk(nc), TPB, 0, st>>>(nc, q->off, q->sk, q->nd, q->cv2);
+  }
+  if (nh > 0) q_count<<<nblk(nh), TPB, 0, st>>>(nh, q->off, q->sk, q->nd, q->hot);
+  q_prio<<<nblk(S1), TPB, 0, st>>>(nseg, q->g, q->a, q->nd, c, q->prio, q->dom);
+  QCK(cudaGetLastError());
+  *nhot = nh;
+  *ncold = nc;
+  *nbuckets = nb;
+  return PRISM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+prism_qas *prism_qas_create(int32_t device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    qfail(PRISM_CUDA, "no CUDA device: QAS has no CPU fallback");
+    return nullptr;
+  }
+  prism_qas *q = new prism_qas();
+  q->dev = device;
+  cudaSetDevice(device);
+  if (cudaStreamCreateWithFlags(&q->st, cudaStreamNonBlocking) != cudaSuccess) {
+    delete q;
+    return nullptr;
+  }
+  return q;
+}
+
+void prism_qas_destroy(prism_qas *q) {
+  if (!q) return;
+  cudaSetDevice(q->dev);
+  cudaStreamSynchronize(q->st);
+  void *bufs[] = {q->tmp,   q->ids,     q->arrival, q->off,    q->sk,     q->reo,    q->aoff,    q->ask,
+                  q->g,     q->a,       q->nd,      q->prio,   q->dom,    q->aligned, q->sig,    q->siglen,
+                  q->sighash, q->tkey,  q->tmin,    q->slot_of, q->bmin,  q->bslot,  q->bmin2,   q->bslot2,
+                  q->bidx_of_slot, q->bucket, q->iota, q->sb,  q->si,     q->bstart, q->bend,    q->rank,
+                  q->pcnt,  q->ppos,    q->pk,      q->pv,     q->pk2,    q->pv2,    q->head,    q->hpos,
+                  q->ppref, q->hstart,  q->term,    q->hbucket, q->hb0,   q->hb1,    q->score,   q->skey,
+                  q->sval,  q->skey2,   q->sval2,   q->ssz,    q->spre,   q->take,   q->base,    q->hot,
+                  q->sel,   q->ck,      q->cv,      q->ck2,    q->cv2,    q->small,  q->err};
+  for (void *p : bufs)
+    if (p) cudaFree(p);
+  cudaStreamDestroy(q->st);
+  delete q;
+}
+
+int prism_qas_round(prism_qas *q, int64_t P, const int64_t *ids, const double *arrival, const int64_t *sk_off,
+                    const int32_t *sk, const uint8_t *reorderable, int64_t A, const int64_t *act_off,
+                    const int32_t *act_sk, int32_t nseg, const prism_qas_config *cfg, int64_t *hot, int64_t *nhot,
+                    int64_t *cold, int64_t *ncold, int32_t *aligned, int32_t *sig, int32_t *siglen,
+                    int64_t *rank, int64_t *bucket, double *bscore, int64_t *nbuckets, int32_t *g, int32_t *a,
+                    int32_t *nd, double *prio, uint8_t *dom) {
+  if (cfg->cold_quota > cfg->dispatch_budget || cfg->signature_size < 1 ||
+      cfg->front_width < cfg->signature_size)
+    return qfail(PRISM_INVALID, "invalid SchedulerConfig");
+  if (cfg->signature_size > QMAXK) return qfail(PRISM_INVALID, "signature_size too large");
+  cudaSetDevice(q->dev);
+  cudaStream_t st = q->st;
+  const int64_t P1 = std::max<int64_t>(P, 1), A1 = std::max<int64_t>(A, 1);
+  const int64_t nsk = sk_off[P], nask = act_off[A];
+  for (int64_t j = 0; j < nsk; j++)
+    if (sk[j] < 0 || sk[j] >= nseg) return qfail(PRISM_INVALID, "segment id out of range");
+  for (int64_t j = 0; j < nask; j++)
+    if (act_sk[j] < 0 || act_sk[j] >= nseg) return qfail(PRISM_INVALID, "segment id out of range");
+  QCK(grow(&q->ids, q->ids_cap, P1));
+  QCK(grow(&q->arrival, q->arrival_cap, P1));
+  QCK(grow(&q->off, q->off_cap, P1 + 1));
+  QCK(grow(&q->sk, q->sk_cap, std::max<int64_t>(nsk, 1)));
+  QCK(grow(&q->reo, q->reo_cap, P1));
+  QCK(grow(&q->aoff, q->aoff_cap, A1 + 1));
+  QCK(grow(&q->ask, q->ask_cap, std::max<int64_t>(nask, 1)));
+  if (P) {
+    QCK(cudaMemcpyAsync(q->ids, ids, sizeof(int64_t) * P, cudaMemcpyHostToDevice, st));
+    QCK(cudaMemcpyAsync(q->arrival, arrival, sizeof(double) * P, cudaMemcpyHostToDevice, st));
+    QCK(cudaMemcpyAsync(q->reo, reorderable, P, cudaMemcpyHostToDevice, st));
+  }
+  QCK(cudaMemcpyAsync(q->off, sk_off, sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice, st));
+  if (nsk) QCK(cudaMemcpyAsync(q->sk, sk, sizeof(int32_t) * nsk, cudaMemcpyHostToDevice, st));
+  QCK(cudaMemcpyAsync(q->aoff, act_off, sizeof(int64_t) * (A + 1), cudaMemcpyHostToDevice, st));
+  if (nask) QCK(cudaMemcpyAsync(q->ask, act_sk, sizeof(int32_t) * nask, cudaMemcpyHostToDevice, st));
+  QCfg c{cfg->dispatch_budget, cfg->cold_quota, cfg->front_width, cfg->signature_size,
+         cfg->w_g, cfg->w_a, cfg->w_n, cfg->alpha_size, cfg->beta_util};
+  int rc = qas_run(q, P, A, nseg, c, nhot, ncold, nbuckets);
+  if (rc) return rc;
+  if (*nhot) QCK(cudaMemcpyAsync(hot, q->hot, sizeof(int64_t) * *nhot, cudaMemcpyDeviceToHost, st));
+  if (*ncold) QCK(cudaMemcpyAsync(cold, q->cv2, sizeof(int64_t) * *ncold, cudaMemcpyDeviceToHost, st));
+  if (P) {
+    if (nsk) QCK(cudaMemcpyAsync(aligned, q->aligned, sizeof(int32_t) * nsk, cudaMemcpyDeviceToHost, st));
+    QCK(cudaMemcpyAsync(sig, q->sig, sizeof(int32_t) * P * cfg->signature_size, cudaMemcpyDeviceToHost, st));
+    QCK(cudaMemcpyAsync(siglen, q->siglen, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st));
+    std::vector<int32_t> r32((size_t)P), b32((size_t)P);
+    QCK(cudaMemcpyAsync(r32.data(), q->rank, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st));
+    QCK(cudaMemcpyAsync(b32.data(), q->bucket, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st));
+    if (*nbuckets) QCK(cudaMemcpyAsync(bscore, q->score, sizeof(double) * *nbuckets, cudaMemcpyDeviceToHost, st));
+    QCK(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < P; i++) {
+      rank[i] = r32[i];
+      bucket[i] = b32[i];
+    }
+  }
+  if (nseg > 0) {
+    QCK(cudaMemcpyAsync(g, q->g, sizeof(int32_t) * nseg, cudaMemcpyDeviceToHost, st));
+    QCK(cudaMemcpyAsync(a, q->a, sizeof(int32_t) * nseg, cudaMemcpyDeviceToHost, st));
+    QCK(cudaMemcpyAsync(nd, q->nd, sizeof(int32_t) * nseg, cudaMemcpyDeviceToHost, st));
+    QCK(cudaMemcpyAsync(prio, q->prio, sizeof(double) * nseg, cudaMemcpyDeviceToHost, st));
+    QCK(cudaMemcpyAsync(dom, q->dom, (size_t)nseg, cudaMemcpyDeviceToHost, st));
+  }
+  QCK(cudaStreamSynchronize(st));
+  return PRISM_OK;
+}
+
+}  // extern "C"
