@@ -1,0 +1,124 @@
+"""Device QAS: ``schedule_round`` (scheduler.py:192-273) on the B200.
+
+Same signature and result as the reference: ``schedule_round(pending,
+active_set, config, now) -> DispatchBatch`` holding the caller's own Request
+objects.  The round itself (counters, front alignment, signatures, buckets,
+scores, hot/cold lanes, dispatch priorities) runs as the device passes of
+csrc/qas.cu; this module only marshals the request list.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+import numpy as np
+
+from . import _lib
+from ._lib import check
+from .qas_host import RoundOutputs, build_batch, marshal_round
+from .types import DispatchBatch, SchedulerConfig
+
+
+class _QasCfg(C.Structure):
+    _fields_ = [
+        ("dispatch_budget", C.c_int64),
+        ("cold_quota", C.c_int64),
+        ("front_width", C.c_int64),
+        ("signature_size", C.c_int64),
+        ("w_g", C.c_double),
+        ("w_a", C.c_double),
+        ("w_n", C.c_double),
+        ("alpha_size", C.c_double),
+        ("beta_util", C.c_double),
+    ]
+
+
+def _cfg(config: SchedulerConfig) -> _QasCfg:
+    w = config.weights
+    return _QasCfg(config.dispatch_budget, config.cold_quota, config.front_width, config.signature_size,
+                   w.w_g, w.w_a, w.w_n, config.alpha_size, config.beta_util)
+
+
+class DeviceScheduler:
+    """Owns the device buffers of one QAS instance (one per GPU)."""
+
+    def __init__(self, device: int = 0):
+        _lib.require_device()
+        self._L = _lib.lib()
+        self._h = self._L.prism_qas_create(device)
+        if not self._h:
+            raise _lib.PrismError(_lib.last_error())
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._L.prism_qas_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover
+            pass
+
+    def round_arrays(self, m, config: SchedulerConfig) -> RoundOutputs:
+        if config.cold_quota > config.dispatch_budget:
+            raise ValueError("cold_quota must be <= dispatch_budget")
+        P = len(m.pending)
+        kappa = config.signature_size
+        nseg = m.nseg
+        n1 = max(P, 1)
+        s1 = max(nseg, 1)
+        hot = np.zeros(n1, np.int64)
+        cold = np.zeros(n1, np.int64)
+        nhot = np.zeros(1, np.int64)
+        ncold = np.zeros(1, np.int64)
+        aligned = np.zeros(max(len(m.sk), 1), np.int32)
+        sig = np.zeros(n1 * kappa, np.int32)
+        siglen = np.zeros(n1, np.int32)
+        rank = np.zeros(n1, np.int64)
+        bucket = np.zeros(n1, np.int64)
+        bscore = np.zeros(n1, np.float64)
+        nb = np.zeros(1, np.int64)
+        g = np.zeros(s1, np.int32)
+        a = np.zeros(s1, np.int32)
+        nd = np.zeros(s1, np.int32)
+        prio = np.zeros(s1, np.float64)
+        dom = np.zeros(s1, np.uint8)
+        sk = m.sk if len(m.sk) else np.zeros(1, np.int32)
+        ask = m.act_sk if len(m.act_sk) else np.zeros(1, np.int32)
+        ids = m.ids if P else np.zeros(1, np.int64)
+        arr = m.arrival if P else np.zeros(1, np.float64)
+        reo = m.reorderable if P else np.zeros(1, np.uint8)
+        cfg = _cfg(config)
+        p = lambda x: x.ctypes.data  # noqa: E731
+        check(self._L.prism_qas_round(
+            self._h, P, p(ids), p(arr), p(m.sk_off), p(sk), p(reo), len(m.act_off) - 1, p(m.act_off), p(ask),
+            nseg, C.addressof(cfg), p(hot), p(nhot), p(cold), p(ncold), p(aligned), p(sig), p(siglen),
+            p(rank), p(bucket), p(bscore), p(nb), p(g), p(a), p(nd), p(prio), p(dom),
+        ))
+        return RoundOutputs(
+            hot=hot[: nhot[0]], cold=cold[: ncold[0]], aligned=aligned[: len(m.sk)],
+            sig=sig[: P * kappa].reshape(P, kappa), siglen=siglen[:P], rank=rank[:P], bucket=bucket[:P],
+            bscore=bscore[: nb[0]], g=g[:nseg], a=a[:nseg], nd=nd[:nseg], prio=prio[:nseg], dom=dom[:nseg],
+        )
+
+    def schedule_round(self, pending, active_set, config: SchedulerConfig, now: float = 0.0) -> DispatchBatch:
+        m = marshal_round(pending, active_set)
+        return build_batch(m, self.round_arrays(m, config))
+
+
+_LOCAL = threading.local()
+
+
+def _default() -> DeviceScheduler:
+    s = getattr(_LOCAL, "sched", None)
+    if s is None:
+        s = DeviceScheduler()
+        _LOCAL.sched = s
+    return s
+
+
+def schedule_round(pending, active_set, config: SchedulerConfig, now: float) -> DispatchBatch:
+    """Drop-in for prefixsim.scheduler.schedule_round (scheduler.py:192-273)."""
+    return _default().schedule_round(pending, active_set, config, now)
