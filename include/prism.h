@@ -134,6 +134,14 @@ int prism_evict_key(prism_tree *t, int32_t slot, uint64_t *key3);
 int prism_last_op(prism_tree *t, int64_t *out);
 /* Number of token-arena compactions so far. */
 int64_t prism_compactions(prism_tree *t);
+/* Live device-time profile: with enable != 0 every phase is bracketed by
+ * CUDA events on the tree's stream.  prism_profile_read fills out[27]:
+ * device ms per phase [0..8) (commit, list build, protection, pre-match,
+ * release, note-active, maintenance), calls [8..16), own kernel launches
+ * [16..24), CUB primitive calls [24], matched chain nodes [25], inserted
+ * path tokens [26]. */
+int prism_profile(prism_tree *t, int32_t enable);
+int prism_profile_read(prism_tree *t, double *out);
 
 /* ------------------------------------------------------------------- QAS */
 typedef struct {
@@ -154,6 +162,50 @@ int prism_qas_round(prism_qas *q, int64_t P, const int64_t *ids, const double *a
                     int64_t *ncold, int32_t *aligned, int32_t *sig, int32_t *siglen, int64_t *rank,
                     int64_t *bucket, double *bscore, int64_t *nbuckets, int32_t *g, int32_t *a,
                     int32_t *nd, double *prio, uint8_t *dom);
+
+/* schedule_round with every input a DEVICE pointer; the outputs stay on the
+ * device inside q for prism_wave_step. */
+int prism_qas_round_device(prism_qas *q, int64_t P, const int64_t *ids, const double *arrival,
+                           const int64_t *sk_off, const int32_t *sk, const uint8_t *reorderable,
+                           int64_t A, const int64_t *act_off, const int32_t *act_sk, int32_t nseg,
+                           const prism_qas_config *cfg, int64_t *nhot, int64_t *ncold,
+                           int64_t *nbuckets);
+
+/* ---------------------------------------------------- fused wave (QAS + DART) */
+/* set_protection from a dense DEVICE P-hat array over [0, nseg)
+ * (kvcache.py:364-383 fed by scheduler.py:247-251). out_ids may be NULL. */
+int prism_set_protection_device(prism_tree *t, const double *d_pri, int32_t nseg,
+                                int64_t *out_ids, int64_t *n_out);
+/* note_active_segments from dense DEVICE counters: active = a > 0 or n > 0
+ * (engine.py:195-197). */
+int prism_note_active_device(prism_tree *t, const int32_t *d_a, const int32_t *d_nd, int32_t nseg);
+int32_t prism_tree_policy(prism_tree *t);
+/* The cudaStream_t (as void*) the QAS instance launches on; prism_wave_step
+ * completes on it, so events recorded there bracket a whole wave. */
+void *prism_qas_stream(prism_qas *q);
+/* out[4]: own kernel launches, CUB primitive calls, rounds so far, and the
+ * device microseconds of those rounds when profiling is on. */
+int prism_qas_counts(prism_qas *q, int64_t *out);
+int prism_qas_profile(prism_qas *q, int32_t enable);
+/* Copy the last round's pending demand counters g[0..nseg) (DEVICE int32) to
+ * dst (DEVICE) -- the per-window counter vector the replicas all-reduce. */
+int prism_qas_counters(prism_qas *q, int32_t *dst, int32_t nseg);
+
+/* One serving-loop wave entirely on the device (engine.py:189-213):
+ * schedule_round over the DEVICE-resident pending CSR, the protection (DART)
+ * or active-set (LRU_ACTIVE) hand-off, serialize_tokens of every member with
+ * its aligned skeleton (token layout workload.py:136-154: system prefix
+ * sys_len, chunk tokens per segment, per-request suffix length), the anchors
+ * of _build_anchors (engine.py:269-292), then ordered match+insert+evict.
+ * members_out[P] (dispatch order as pending indices, may be NULL), hits,
+ * leaf_slots, leaf_ids are DEVICE arrays; *n_members / *n_admitted host. */
+int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids,
+                    const double *arrival, const int64_t *sk_off, const int32_t *sk,
+                    const uint8_t *reorderable, const int32_t *suffix, int64_t A,
+                    const int64_t *act_off, const int32_t *act_sk, int32_t nseg,
+                    const prism_qas_config *cfg, int64_t sys_len, int64_t chunk,
+                    int64_t *members_out, int64_t *hits, int32_t *leaf_slots, int64_t *leaf_ids,
+                    int64_t *n_members, int64_t *n_admitted);
 
 #ifdef __cplusplus
 }

@@ -97,7 +97,31 @@ struct prism_tree {
   int64_t *d_prot_ids = nullptr;
   int64_t prot_cap = 0;
   int64_t compactions = 0;
+  // live device-time profile per phase (CUDA events on the tree stream)
+  int prof_on = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double prof_ms[8] = {};
+  int64_t prof_calls[8] = {};
+  int64_t launches[8] = {};  // own kernel launches per phase (always counted)
+  int64_t lib_calls = 0;     // CUB primitive invocations
 };
+
+enum { PH_COMMIT = 0, PH_BUILD = 1, PH_PROTECT = 2, PH_PREMATCH = 3, PH_RELEASE = 4, PH_NOTE = 5, PH_MAINT = 6 };
+
+namespace {
+inline void prof_begin(prism_tree *t) {
+  if (t->prof_on) cudaEventRecord(t->ev0, t->st);
+}
+inline void prof_end(prism_tree *t, int ph) {
+  t->prof_calls[ph]++;
+  if (!t->prof_on) return;
+  cudaEventRecord(t->ev1, t->st);
+  cudaEventSynchronize(t->ev1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, t->ev0, t->ev1);
+  t->prof_ms[ph] += ms;
+}
+}  // namespace
 
 namespace {
 
@@ -190,6 +214,7 @@ int sort_pairs(prism_tree *t, int64_t n, Key3 *kout, uint64_t *vout, int bits) {
 // ------------------------------------------------------------ eviction order
 int build_list(prism_tree *t) {
   const int32_t hw = t->hctrl->hw;
+  prof_begin(t);
   CK(cudaMemsetAsync(t->d_count, 0, sizeof(int64_t), t->st));
   k_build_keys<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw);
   k_propagate<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw);
@@ -202,6 +227,9 @@ int build_list(prism_tree *t) {
   if (rc) return rc;
   k_list_ready<<<1, 1, 0, t->st>>>(t->d, t->d_count);
   CK(cudaGetLastError());
+  t->launches[PH_BUILD] += 4;
+  t->lib_calls += 1;
+  prof_end(t, PH_BUILD);
   return PRISM_OK;
 }
 
@@ -269,8 +297,11 @@ int run_commit(prism_tree *t, CommitArgs a) {
     attr_set = true;
   }
   for (int iter = 0; iter < 1000000; iter++) {
+    prof_begin(t);
     k_commit<<<1, 32, COMMIT_SMEM, t->st>>>(t->d, a);
     CK(cudaGetLastError());
+    t->launches[PH_COMMIT]++;
+    prof_end(t, PH_COMMIT);
     int rc = pull_ctrl(t);
     if (rc) return rc;
     a.reset = 0;
@@ -558,6 +589,7 @@ int prism_release_device(prism_tree *t, int64_t n, const int32_t *slots, const i
   cudaStream_t s = stream ? (cudaStream_t)stream : t->st;
   k_release_par<<<blocks_for(n), TPB, 0, s>>>(t->d, n, slots);
   CK(cudaGetLastError());
+  t->launches[PH_RELEASE]++;
   return PRISM_OK;
 }
 
@@ -569,6 +601,38 @@ int prism_evict(prism_tree *t, int64_t k_free, int64_t *freed) {
   CK(cudaMemcpyAsync(t->h_res, t->d_res, sizeof(OpRes), cudaMemcpyDeviceToHost, t->st));
   CK(cudaStreamSynchronize(t->st));
   *freed = t->h_res->freed;
+  return PRISM_OK;
+}
+
+// top-f reusable anchors by (-P-hat, segment, id) with the current t->d.pri
+static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out) {
+  int rc = pull_ctrl(t);
+  if (rc) return rc;
+  const int32_t hw = t->hctrl->hw;
+  prof_begin(t);
+  t->launches[PH_PROTECT] += 3;
+  t->lib_calls += 1;
+  CK(cudaMemsetAsync(t->d_count, 0, sizeof(int64_t), t->st));
+  k_prot_gather<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw, t->ck, t->cv, t->d_count);
+  k_prot_clear<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(t->h_small, t->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  const int64_t m = t->h_small[0];
+  const int64_t f = std::min<int64_t>(t->protect_budget, m);
+  if (f > 0) {
+    rc = sort_pairs(t, m, t->d.Lk, t->d.Lv, 64 + 32 + 40);  // Lk/Lv as scratch: no list survives a call
+    if (rc) return rc;
+    rc = ensure_buf(&t->d_prot_ids, t->prot_cap, f);
+    if (rc) return rc;
+    k_prot_set<<<blocks_for(f), TPB, 0, t->st>>>(t->d, t->d.Lv, f, t->d_prot_ids);
+    CK(cudaGetLastError());
+    if (out_ids)
+      CK(cudaMemcpyAsync(out_ids, t->d_prot_ids, sizeof(int64_t) * f, cudaMemcpyDeviceToHost, t->st));
+  }
+  prof_end(t, PH_PROTECT);
+  CK(cudaStreamSynchronize(t->st));
+  if (n_out) *n_out = f;
   return PRISM_OK;
 }
 
@@ -589,30 +653,41 @@ int prism_set_protection(prism_tree *t, int64_t n, const int32_t *segs, const do
   }
   if (nseg) CK(cudaMemcpyAsync(t->d.pri, dense.data(), sizeof(double) * nseg, cudaMemcpyHostToDevice, t->st));
   t->d.npri = nseg;
+  return protect_current(t, out_ids, n_out);
+}
+
+// set_protection from a dense device P-hat array (the QAS round's output)
+int prism_set_protection_device(prism_tree *t, const double *d_pri, int32_t nseg, int64_t *out_ids,
+                                int64_t *n_out) {
+  cudaSetDevice(t->dev);
+  if (nseg > t->d.npri) {
+    CK(cudaFree(t->d.pri));
+    CK(dalloc(&t->d.pri, nseg));
+  }
+  if (nseg) CK(cudaMemcpyAsync(t->d.pri, d_pri, sizeof(double) * nseg, cudaMemcpyDeviceToDevice, t->st));
+  t->d.npri = nseg;
+  return protect_current(t, out_ids, n_out);
+}
+
+// LRU_ACTIVE hand-off (engine.py:195-197) from dense device counters:
+// active = segments with a count > 0 over the active set or the batch
+int prism_note_active_device(prism_tree *t, const int32_t *d_a, const int32_t *d_nd, int32_t nseg) {
+  cudaSetDevice(t->dev);
+  if (nseg > t->d.nact) {
+    CK(cudaFree(t->d.act));
+    CK(dalloc(&t->d.act, nseg));
+  }
+  t->d.nact = nseg;
+  if (nseg) k_active_flags<<<blocks_for(nseg), TPB, 0, t->st>>>(t->d, d_a, d_nd, nseg);
   int rc = pull_ctrl(t);
   if (rc) return rc;
   const int32_t hw = t->hctrl->hw;
-  CK(cudaMemsetAsync(t->d_count, 0, sizeof(int64_t), t->st));
-  k_prot_gather<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw, t->ck, t->cv, t->d_count);
-  k_prot_clear<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw);
+  k_note_active<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw);
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(t->h_small, t->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
-  CK(cudaStreamSynchronize(t->st));
-  const int64_t m = t->h_small[0];
-  const int64_t f = std::min<int64_t>(t->protect_budget, m);
-  if (f > 0) {
-    rc = sort_pairs(t, m, t->d.Lk, t->d.Lv, 64 + 32 + 40);  // Lk/Lv as scratch: no list survives a call
-    if (rc) return rc;
-    rc = ensure_buf(&t->d_prot_ids, t->prot_cap, f);
-    if (rc) return rc;
-    k_prot_set<<<blocks_for(f), TPB, 0, t->st>>>(t->d, t->d.Lv, f, t->d_prot_ids);
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(out_ids, t->d_prot_ids, sizeof(int64_t) * f, cudaMemcpyDeviceToHost, t->st));
-  }
-  CK(cudaStreamSynchronize(t->st));
-  *n_out = f;
   return PRISM_OK;
 }
+
+int32_t prism_tree_policy(prism_tree *t) { return t->d.policy; }
 
 int prism_note_active(prism_tree *t, int64_t n, const int32_t *segs) {
   cudaSetDevice(t->dev);
@@ -664,8 +739,11 @@ int prism_admit_wave_device(prism_tree *t, int64_t B, const int64_t *path_off, c
     CK(dalloc(&t->d_pm_meta, 4 * t->pm_cap));
     CK(dalloc(&t->d_pm_chain, PM_MAX * t->pm_cap));
   }
+  prof_begin(t);
   k_prematch<<<blocks_for(B * 32), TPB, 0, t->st>>>(t->d, B, path_off, tokens, t->d_pm_meta, t->d_pm_chain);
   CK(cudaGetLastError());
+  t->launches[PH_PREMATCH]++;
+  prof_end(t, PH_PREMATCH);
   CommitArgs a{};
   a.mode = 1;
   a.reset = 1;
@@ -871,5 +949,32 @@ int prism_evict_key(prism_tree *t, int32_t slot, uint64_t *key3) {
 }
 
 int64_t prism_compactions(prism_tree *t) { return t->compactions; }
+
+int prism_profile(prism_tree *t, int32_t enable) {
+  cudaSetDevice(t->dev);
+  if (enable && !t->ev0) {
+    CK(cudaEventCreate(&t->ev0));
+    CK(cudaEventCreate(&t->ev1));
+  }
+  t->prof_on = enable ? 1 : 0;
+  return PRISM_OK;
+}
+
+// out[24]: per phase (commit, build, protect, prematch, release, note, maint, -)
+// device ms [0..8), calls [8..16), own kernel launches [16..24); out[24] CUB calls;
+// out[25] chain nodes, out[26] inserted tokens (SURVEY.md 8(d) byte model)
+int prism_profile_read(prism_tree *t, double *out) {
+  int rc = pull_ctrl(t);
+  if (rc) return rc;
+  for (int i = 0; i < 8; i++) {
+    out[i] = t->prof_ms[i];
+    out[8 + i] = (double)t->prof_calls[i];
+    out[16 + i] = (double)t->launches[i];
+  }
+  out[24] = (double)t->lib_calls;
+  out[25] = (double)t->hctrl->chain_nodes;
+  out[26] = (double)t->hctrl->inserted_tokens;
+  return PRISM_OK;
+}
 
 }  // extern "C"

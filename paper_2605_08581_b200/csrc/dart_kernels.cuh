@@ -260,68 +260,135 @@ __device__ inline int32_t do_split(const DT &T, Ctrl &C, int32_t X, int32_t k) {
 
 // exact eviction from the sorted list L merged with the side heap H
 // (semantics of evict, kvcache.py:425-460)
+//
+// Entries of L are consumed in batches of 32: every lane prefetches one entry
+// together with its node's and its parent's state (3 dependent round trips
+// per batch instead of per victim); the warp then walks the batch in order
+// from registers, patching the prefetched copies whenever an eviction
+// changes them (child counts, duplicates, cascade-waiting flags).
+struct Cand {
+  Key3 k;
+  int64_t id, eoff;
+  int32_t s, p, nch, pnch, el, hs, seg;
+  uint32_t ftok;
+  int32_t kind;
+  bool ok, pw;
+};
+
+__device__ inline Cand load_cand(const DT &T, const Ctrl &C, Key3 k, uint64_t v) {
+  Cand c;
+  c.k = k;
+  c.s = (int32_t)(v & 0xffffffffu);
+  const uint32_t ver = (uint32_t)(v >> 32);
+  c.id = T.nid[c.s];
+  const uint32_t kv = T.kver[c.s];
+  c.p = T.par[c.s];
+  const int32_t rf = T.ref[c.s];
+  const uint32_t gd = T.guard[c.s];
+  c.kind = T.kind[c.s];
+  c.nch = T.nch[c.s];
+  c.el = T.elen[c.s];
+  c.hs = T.hslot[c.s];
+  c.seg = T.seg[c.s];
+  c.ftok = T.ftok[c.s];
+  c.eoff = T.eoff[c.s];
+  c.ok = kv == ver && c.id >= 0 && c.p >= 0 && rf == 0 && gd != C.gstamp &&
+         !(T.policy == P_DART && c.kind == K_SYSTEM);
+  c.pnch = 0;
+  c.pw = false;
+  if (c.ok) {
+    c.pnch = T.nch[c.p];
+    c.pw = T.waitf[c.p] == C.epoch;
+  }
+  return c;
+}
+
+__device__ inline Cand shfl_cand(const Cand &c, int src) {
+  Cand r;
+  r.k.w0 = __shfl_sync(FULL, c.k.w0, src);
+  r.k.w1 = __shfl_sync(FULL, c.k.w1, src);
+  r.k.w2 = __shfl_sync(FULL, c.k.w2, src);
+  r.id = __shfl_sync(FULL, c.id, src);
+  r.eoff = __shfl_sync(FULL, c.eoff, src);
+  r.s = __shfl_sync(FULL, c.s, src);
+  r.p = __shfl_sync(FULL, c.p, src);
+  r.nch = __shfl_sync(FULL, c.nch, src);
+  r.pnch = __shfl_sync(FULL, c.pnch, src);
+  r.el = __shfl_sync(FULL, c.el, src);
+  r.hs = __shfl_sync(FULL, c.hs, src);
+  r.seg = __shfl_sync(FULL, c.seg, src);
+  r.ftok = __shfl_sync(FULL, c.ftok, src);
+  r.kind = __shfl_sync(FULL, c.kind, src);
+  r.ok = __shfl_sync(FULL, (int)c.ok, src) != 0;
+  r.pw = __shfl_sync(FULL, (int)c.pw, src) != 0;
+  return r;
+}
+
 __device__ inline int64_t evict_loop(const DT &T, Ctrl &C, int64_t need) {
   int64_t freed = 0;
   const int lane = lane_id();
+  int nb = 0, i = 0;
+  int64_t base = 0;
+  Cand mine;  // this lane's prefetched batch entry
+  mine.ok = false;
+  mine.s = mine.p = -1;
+  mine.pw = false;
   while (freed < need) {
-    const bool hasL = C.L_cur < C.L_n;
+    if (i >= nb && C.L_cur < C.L_n) {  // prefetch the next batch of the sorted list
+      base = C.L_cur;
+      nb = (int)((C.L_n - base) < 32 ? (C.L_n - base) : 32);
+      i = 0;
+      mine.ok = false;
+      mine.s = mine.p = -1;
+      mine.pw = false;
+      if (lane < nb) mine = load_cand(T, C, T.Lk[base + lane], T.Lv[base + lane]);
+      __syncwarp();
+    }
+    const bool hasL = i < nb;
     const bool hasH = C.H_n > 0;
     if (!hasL && !hasH) break;
-    Key3 k;
-    uint64_t v;
+    Cand c;
     bool useH = false;
+    if (hasL) c = shfl_cand(mine, i);
     if (hasH) {
       const Key3 kh = T.Hk[0];
-      if (hasL) {
-        const Key3 kl = T.Lk[C.L_cur];
-        useH = key_less(kh, kl);
-        k = useH ? kh : kl;
-        v = useH ? T.Hv[0] : T.Lv[C.L_cur];
-      } else {
-        useH = true;
-        k = kh;
-        v = T.Hv[0];
+      useH = !hasL || key_less(kh, c.k);
+      if (useH) {
+        const uint64_t hv = T.Hv[0];
+        __syncwarp();
+        if (lane == 0) heap_pop(T, C.H_n);
+        C.H_n--;
+        __syncwarp();
+        c = load_cand(T, C, kh, hv);
       }
-    } else {
-      k = T.Lk[C.L_cur];
-      v = T.Lv[C.L_cur];
     }
-    __syncwarp();
-    if (useH) {
-      if (lane == 0) heap_pop(T, C.H_n);
-      C.H_n--;
-    } else {
-      C.L_cur++;
+    if (!useH) {
+      i++;
+      C.L_cur = base + i;
     }
-    __syncwarp();
-    const int32_t s = (int32_t)(v & 0xffffffffu);
-    const uint32_t ver = (uint32_t)(v >> 32);
-    if (T.kver[s] != ver || T.nid[s] < 0) continue;
-    const int32_t p = T.par[s];
-    if (p < 0 || T.ref[s] > 0 || T.guard[s] == C.gstamp) continue;
-    if (T.policy == P_DART && T.kind[s] == K_SYSTEM) continue;
-    if (T.nch[s] > 0) {  // not a leaf yet: wait for its last child (cascade)
+    if (!c.ok) continue;
+    const Key3 k = c.k;
+    const int32_t s = c.s, p = c.p;
+    if (c.nch > 0) {  // not a leaf yet: wait for its last child (cascade)
       if (lane == 0) T.waitf[s] = C.epoch;
+      if (mine.p == s) mine.pw = true;
       __syncwarp();
       continue;
     }
     // detach s (kvcache.py:452-459)
-    VRec rec;
-    rec.id = T.nid[s];
-    rec.eoff = T.eoff[s];
-    rec.ftok = T.ftok[s];
-    rec.elen = T.elen[s];
-    rec.seg = T.seg[s];
-    rec.kind = (int8_t)T.kind[s];
-    rec.pad[0] = rec.pad[1] = rec.pad[2] = 0;
-    const int32_t hs = T.hslot[s];
-    const int32_t nchp = T.nch[p] - 1;
-    const bool pwait = T.waitf[p] == C.epoch;
-    __syncwarp();
+    const int32_t nchp = c.pnch - 1;
     C.vctr++;
     if (lane == 0) {
+      VRec rec;
+      rec.id = c.id;
+      rec.eoff = c.eoff;
+      rec.ftok = c.ftok;
+      rec.elen = c.el;
+      rec.seg = c.seg;
+      rec.kind = (int8_t)c.kind;
+      rec.pad[0] = rec.pad[1] = rec.pad[2] = 0;
       T.nch[p] = nchp;
-      T.ht[hs].key = HTOMB;
+      T.ht[c.hs].key = HTOMB;
       T.vlog[C.vlog_count % T.vcap] = rec;
       T.nid[s] = -1;
       T.par[s] = -1;
@@ -329,12 +396,17 @@ __device__ inline int64_t evict_loop(const DT &T, Ctrl &C, int64_t need) {
       T.wmod[s] = C.epoch;
       T.freelist[C.free_top] = s;
     }
+    // patch the prefetched batch
+    if (mine.s == s) mine.ok = false;
+    if (mine.s == p) mine.nch -= 1;
+    if (mine.p == p) mine.pnch -= 1;
     C.free_top++;
     C.vlog_count++;
     C.hlive--;
     C.htomb++;
-    C.resident -= rec.elen;
-    freed += rec.elen;
+    C.resident -= c.el;
+    freed += c.el;
+    const bool pwait = c.pw;
     __syncwarp();
     if (nchp == 0 && pwait && C.H_n >= T.Hcap) C.fatal = 4;
     if (nchp == 0 && pwait && C.H_n < T.Hcap) {
@@ -487,10 +559,11 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
             Ps[i] = c;
             bad |= T.wmod[c] == C.epoch;
           }
-          // the failed child lookup at the chain end must still fail
-          if (!(fl & 1) && hit_pre < n && lane == 0) {
+          // the failed child lookup at the chain end must still fail: an earlier
+          // member may have added a child with exactly this first token
+          if (!(fl & 1) && hit_pre < n) {
             const int32_t tnode = d > 0 ? A.pm_chain[(int64_t)member * PM_MAX + d - 1] : ROOT;
-            bad |= T.wchild[tnode] == C.epoch;
+            if (ht_lookup(T, tnode, sp[hit_pre]) >= 0) bad = true;
           }
           valid = !__any_sync(FULL, bad);
           __syncwarp();
@@ -544,6 +617,8 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
 
     // ---- insert_path (kvcache.py:190-241)
     const int64_t hit = c_hit;
+    C.chain_nodes += c_d;
+    C.inserted_tokens += n;
     const int64_t shortfall = C.resident + (n - hit) - T.capacity;  // _reserve (243-273)
     if (shortfall > 0) {
       if (!C.L_valid) {
@@ -829,6 +904,12 @@ __global__ void k_note_active(DT T, int32_t hw) {
   if (!T.hasanc[s] || T.akind[s] != K_REUSABLE) return;
   const int32_t sg = T.aseg[s];
   T.snap[3 * (int64_t)s + 1] = (sg != SEG_NONE && sg >= 0 && sg < T.nact && T.act[sg]) ? 1 : 0;
+}
+
+__global__ void k_active_flags(DT T, const int32_t *__restrict__ a, const int32_t *__restrict__ nd,
+                               int32_t nseg) {
+  const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < nseg) T.act[r] = (a[r] > 0 || nd[r] > 0) ? 1 : 0;
 }
 
 // ------------------------------------------------------------ release

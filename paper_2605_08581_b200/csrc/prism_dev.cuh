@@ -76,6 +76,7 @@ struct Ctrl {
   int64_t hlive, htomb;
   int64_t vlog_count, evict_calls, builds;
   int64_t fast_members, slow_members;
+  int64_t chain_nodes, inserted_tokens;  // algorithmic-byte accounting
   int64_t L_n, L_cur;
   int32_t hw, free_top;
   int32_t status, op_cursor;

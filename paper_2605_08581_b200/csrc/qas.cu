@@ -476,7 +476,22 @@ struct prism_qas {
   QBUF(int64_t, cv2)
   QBUF(int64_t, small)
   QBUF(int32_t, err)
+  // fused wave step: dispatch order, serialized paths and anchors
+  QBUF(int64_t, members)
+  QBUF(int64_t, plen)
+  QBUF(int64_t, poff)
+  QBUF(int64_t, alen)
+  QBUF(int64_t, aoffs)
+  QBUF(uint32_t, tok)
+  QBUF(int32_t, a_off)
+  QBUF(int8_t, a_kind)
+  QBUF(int32_t, a_seg)
+  QBUF(int32_t, a_snap)
 #undef QBUF
+  int64_t launches = 0, lib_calls = 0, rounds = 0;
+  int prof_on = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  double ms_round = 0.0;  // QAS round + serialization device time (events on q->st)
 };
 
 namespace {
@@ -488,8 +503,19 @@ int ensure_tmp(prism_qas *q, size_t b) {
   return PRISM_OK;
 }
 
-// the full round; every pointer argument is DEVICE memory inside q
-int qas_run(prism_qas *q, int64_t P, int64_t A, int32_t nseg, const QCfg &c, int64_t *nhot, int64_t *ncold,
+// round inputs, all DEVICE pointers
+struct QIn {
+  const int64_t *ids;
+  const double *arrival;
+  const int64_t *off;
+  const int32_t *sk;
+  const uint8_t *reo;
+  const int64_t *aoff;
+  const int32_t *ask;
+};
+
+// the full round; outputs stay in q's device buffers
+int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, const QCfg &c, int64_t *nhot, int64_t *ncold,
             int64_t *nbuckets) {
   cudaStream_t st = q->st;
   const int32_t S1 = std::max(nseg, 1);
@@ -505,8 +531,8 @@ int qas_run(prism_qas *q, int64_t P, int64_t A, int32_t nseg, const QCfg &c, int
   QCK(cudaMemsetAsync(q->nd, 0, sizeof(int32_t) * S1, st));
   QCK(cudaMemsetAsync(q->err, 0, sizeof(int32_t), st));
   const int64_t P1 = std::max<int64_t>(P, 1);
-  if (P > 0) q_count<<<nblk(P), TPB, 0, st>>>(P, q->off, q->sk, q->g, nullptr);
-  if (A > 0) q_count<<<nblk(A), TPB, 0, st>>>(A, q->aoff, q->ask, q->a, nullptr);
+  if (P > 0) q_count<<<nblk(P), TPB, 0, st>>>(P, in.off, in.sk, q->g, nullptr);
+  if (A > 0) q_count<<<nblk(A), TPB, 0, st>>>(A, in.aoff, in.ask, q->a, nullptr);
   *nhot = *ncold = *nbuckets = 0;
   if (P == 0) {
     q_prio<<<nblk(S1), TPB, 0, st>>>(nseg, q->g, q->a, q->nd, c, q->prio, q->dom);
@@ -514,12 +540,12 @@ int qas_run(prism_qas *q, int64_t P, int64_t A, int32_t nseg, const QCfg &c, int
     return PRISM_OK;
   }
   int64_t nsk = 0;
-  QCK(cudaMemcpyAsync(&nsk, q->off + P, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  QCK(cudaMemcpyAsync(&nsk, in.off + P, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   QCK(grow(&q->aligned, q->aligned_cap, std::max<int64_t>(nsk, 1)));
   QCK(grow(&q->sig, q->sig_cap, P1 * c.kappa));
   QCK(grow(&q->siglen, q->siglen_cap, P1));
   QCK(grow(&q->sighash, q->sighash_cap, P1));
-  q_align<<<nblk(P), TPB, 0, st>>>(P, q->off, q->sk, q->reo, q->g, q->a, c, q->aligned, q->sig, q->siglen,
+  q_align<<<nblk(P), TPB, 0, st>>>(P, in.off, in.sk, in.reo, q->g, q->a, c, q->aligned, q->sig, q->siglen,
                                    q->sighash, q->err);
   // buckets
   int64_t T = 64;
@@ -571,7 +597,7 @@ int qas_run(prism_qas *q, int64_t P, int64_t A, int32_t nseg, const QCfg &c, int
   QCK(grow(&q->pcnt, q->pcnt_cap, P1 + 1));
   QCK(grow(&q->ppos, q->ppos_cap, P1 + 1));
   QCK(cudaMemsetAsync(q->pcnt + P, 0, sizeof(int64_t), st));
-  q_pair_count<<<nblk(P), TPB, 0, st>>>(P, q->off, q->sk, q->pcnt);
+  q_pair_count<<<nblk(P), TPB, 0, st>>>(P, in.off, in.sk, q->pcnt);
   bytes = 0;
   QCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, q->pcnt, q->ppos, (int)(P + 1), st));
   if (ensure_tmp(q, bytes)) return PRISM_CUDA;
@@ -596,7 +622,7 @@ int qas_run(prism_qas *q, int64_t P, int64_t A, int32_t nseg, const QCfg &c, int
   QCK(grow(&q->term, q->term_cap, E1));
   QCK(grow(&q->hbucket, q->hbucket_cap, E1));
   if (E > 0) {
-    q_pair_emit<<<nblk(P), TPB, 0, st>>>(P, q->off, q->sk, q->bucket, q->rank, hot_cap, q->ppos, q->pk, q->pv);
+    q_pair_emit<<<nblk(P), TPB, 0, st>>>(P, in.off, in.sk, q->bucket, q->rank, hot_cap, q->ppos, q->pk, q->pv);
     bytes = 0;
     QCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, q->pk, q->pk2, q->pv, q->pv2, (int)E, 0, 64, st));
     if (ensure_tmp(q, bytes)) return PRISM_CUDA;
@@ -659,7 +685,7 @@ int qas_run(prism_qas *q, int64_t P, int64_t A, int32_t nseg, const QCfg &c, int
   QCK(grow(&q->ck2, q->ck2_cap, P1));
   QCK(grow(&q->cv2, q->cv2_cap, P1));
   if (nc > 0) {
-    q_cold_keys<<<nblk(P), TPB, 0, st>>>(P, q->sel, q->arrival, q->ids, q->ck, q->cv);
+    q_cold_keys<<<nblk(P), TPB, 0, st>>>(P, q->sel, in.arrival, in.ids, q->ck, q->cv);
     bytes = 0;
     QCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, q->ck, q->ck2, q->cv, q->cv2, (int)P, K3Decomp{}, 0,
                                         1 + 128, st));
@@ -668,14 +694,18 @@ int qas_run(prism_qas *q, int64_t P, int64_t A, int32_t nseg, const QCfg &c, int
     QCK(cub::DeviceRadixSort::SortPairs(q->tmp, bytes, q->ck, q->ck2, q->cv, q->cv2, (int)P, K3Decomp{}, 0,
                                         1 + 128, st));
     // n_disp over hot + cold (scheduler.py:247-248)
-    q_count<<<nblk(nc), TPB, 0, st>>>(nc, q->off, q->sk, q->nd, q->cv2);
+    q_count<<<nblk(nc), TPB, 0, st>>>(nc, in.off, in.sk, q->nd, q->cv2);
   }
-  if (nh > 0) q_count<<<nblk(nh), TPB, 0, st>>>(nh, q->off, q->sk, q->nd, q->hot);
+  if (nh > 0) q_count<<<nblk(nh), TPB, 0, st>>>(nh, in.off, in.sk, q->nd, q->hot);
   q_prio<<<nblk(S1), TPB, 0, st>>>(nseg, q->g, q->a, q->nd, c, q->prio, q->dom);
   QCK(cudaGetLastError());
   *nhot = nh;
   *ncold = nc;
   *nbuckets = nb;
+  // launch accounting (own kernels / CUB primitives) for bench.py's gpu_launches
+  q->launches += (A > 0) + 1 + 8 + (E > 0 ? 4 : 0) + 4 + (nc > 0 ? 2 : 0) + (nh > 0) + 1;
+  q->lib_calls += 3 + (E > 0 ? 3 : 0) + 2 + (nc > 0);
+  q->rounds++;
   return PRISM_OK;
 }
 }  // namespace
@@ -752,7 +782,8 @@ int prism_qas_round(prism_qas *q, int64_t P, const int64_t *ids, const double *a
   if (nask) QCK(cudaMemcpyAsync(q->ask, act_sk, sizeof(int32_t) * nask, cudaMemcpyHostToDevice, st));
   QCfg c{cfg->dispatch_budget, cfg->cold_quota, cfg->front_width, cfg->signature_size,
          cfg->w_g, cfg->w_a, cfg->w_n, cfg->alpha_size, cfg->beta_util};
-  int rc = qas_run(q, P, A, nseg, c, nhot, ncold, nbuckets);
+  const QIn in{q->ids, q->arrival, q->off, q->sk, q->reo, q->aoff, q->ask};
+  int rc = qas_run(q, in, P, A, nseg, c, nhot, ncold, nbuckets);
   if (rc) return rc;
   if (*nhot) QCK(cudaMemcpyAsync(hot, q->hot, sizeof(int64_t) * *nhot, cudaMemcpyDeviceToHost, st));
   if (*ncold) QCK(cudaMemcpyAsync(cold, q->cv2, sizeof(int64_t) * *ncold, cudaMemcpyDeviceToHost, st));
@@ -779,6 +810,213 @@ int prism_qas_round(prism_qas *q, int64_t P, const int64_t *ids, const double *a
   }
   QCK(cudaStreamSynchronize(st));
   return PRISM_OK;
+}
+
+}  // extern "C"
+
+// ===================================================================== fused wave
+// The engine's per-wave hand-off (engine.py:189-213) without leaving the GPU:
+// QAS round -> dispatch order -> serialize_tokens with the aligned skeleton
+// (workload.py:136-164, K1) -> _build_anchors with the round's counter
+// snapshots (engine.py:269-292) -> protection / active-set hand-off ->
+// ordered admission (match + insert + evict per member).
+namespace {
+
+constexpr uint64_t SEGMENT_TOKEN_BASE = 1000000ull;
+constexpr uint64_t SUFFIX_TOKEN_BASE = 2000000000ull;
+
+__global__ void q_members(int64_t nh, int64_t nc, const int64_t *__restrict__ hot, const int64_t *__restrict__ cold,
+                          int64_t *__restrict__ members) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nh) members[i] = hot[i];
+  else if (i < nh + nc) members[i] = cold[i - nh];
+}
+
+__global__ void q_serial_len(int64_t B, const int64_t *__restrict__ members, const int64_t *__restrict__ off,
+                             const int32_t *__restrict__ suffix, int64_t sys, int64_t chunk,
+                             int64_t *__restrict__ plen, int64_t *__restrict__ alen) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  const int64_t m = members[i], k = off[m + 1] - off[m];
+  plen[i] = sys + k * chunk + suffix[m];
+  alen[i] = (sys > 0 ? 1 : 0) + k + (suffix[m] > 0 ? 1 : 0);
+}
+
+// one warp per member: token path and anchors
+__global__ void q_serialize(int64_t B, const int64_t *__restrict__ members, const int64_t *__restrict__ ids,
+                            const int64_t *__restrict__ off, const int32_t *__restrict__ aligned,
+                            const int32_t *__restrict__ suffix, int64_t sys, int64_t chunk,
+                            const int32_t *__restrict__ g, const int32_t *__restrict__ a,
+                            const int32_t *__restrict__ nd, const int64_t *__restrict__ poff,
+                            const int64_t *__restrict__ aoffs, uint32_t *__restrict__ tok,
+                            int32_t *__restrict__ a_off, int8_t *__restrict__ a_kind, int32_t *__restrict__ a_seg,
+                            int32_t *__restrict__ a_snap, int32_t *__restrict__ err) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= B) return;
+  const int64_t m = members[w], b = off[m], k = off[m + 1] - b, sfx = suffix[m];
+  uint32_t *p = tok + poff[w];
+  for (int64_t j = lane; j < sys; j += 32) p[j] = (uint32_t)j;
+  for (int64_t j = lane; j < k * chunk; j += 32) {
+    const int64_t r = aligned[b + j / chunk];
+    p[sys + j] = (uint32_t)(SEGMENT_TOKEN_BASE + (uint64_t)r * chunk + (uint64_t)(j % chunk));
+  }
+  const uint64_t sb = SUFFIX_TOKEN_BASE + (uint64_t)ids[m] * (uint64_t)sfx;
+  if (lane == 0 && sb + sfx > 0xFFFFFFFFull) *err = 2;  // token layout must fit uint32
+  for (int64_t j = lane; j < sfx; j += 32) p[sys + k * chunk + j] = (uint32_t)(sb + j);
+  if (lane == 0) {
+    int64_t q = aoffs[w];
+    if (sys > 0) {
+      a_off[q] = (int32_t)sys;
+      a_kind[q] = 0;  // SYSTEM
+      a_seg[q] = (int32_t)0x80000000;
+      a_snap[3 * q] = a_snap[3 * q + 1] = a_snap[3 * q + 2] = 0;
+      q++;
+    }
+    for (int64_t j = 0; j < k; j++, q++) {
+      const int32_t r = aligned[b + j];
+      a_off[q] = (int32_t)(sys + (j + 1) * chunk);
+      a_kind[q] = 1;  // REUSABLE, counter snapshot (g, a, n) of its segment
+      a_seg[q] = r;
+      a_snap[3 * q] = g[r];
+      a_snap[3 * q + 1] = a[r];
+      a_snap[3 * q + 2] = nd[r];
+    }
+    if (sfx > 0) {
+      a_off[q] = (int32_t)(sys + k * chunk + sfx);
+      a_kind[q] = 2;  // PRIVATE
+      a_seg[q] = (int32_t)0x80000000;
+      a_snap[3 * q] = a_snap[3 * q + 1] = a_snap[3 * q + 2] = 0;
+    }
+  }
+}
+
+int scan64(prism_qas *q, const int64_t *in, int64_t *out, int64_t n) {
+  size_t bytes = 0;
+  QCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)n, q->st));
+  if (ensure_tmp(q, bytes)) return PRISM_CUDA;
+  bytes = q->tmp_bytes;
+  QCK(cub::DeviceScan::ExclusiveSum(q->tmp, bytes, in, out, (int)n, q->st));
+  return PRISM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void *prism_qas_stream(prism_qas *q) { return (void *)q->st; }
+
+// out[4]: own kernel launches, CUB primitive calls, rounds, round device-us
+int prism_qas_counts(prism_qas *q, int64_t *out) {
+  out[0] = q->launches;
+  out[1] = q->lib_calls;
+  out[2] = q->rounds;
+  out[3] = (int64_t)(q->ms_round * 1000.0);
+  return PRISM_OK;
+}
+
+int prism_qas_profile(prism_qas *q, int32_t enable) {
+  cudaSetDevice(q->dev);
+  if (enable && !q->e0) {
+    QCK(cudaEventCreate(&q->e0));
+    QCK(cudaEventCreate(&q->e1));
+  }
+  q->prof_on = enable ? 1 : 0;
+  return PRISM_OK;
+}
+
+int prism_qas_counters(prism_qas *q, int32_t *dst, int32_t nseg) {
+  cudaSetDevice(q->dev);
+  if (nseg > q->g_cap) return qfail(PRISM_INVALID, "nseg exceeds the last round's counter vector");
+  if (nseg > 0) QCK(cudaMemcpyAsync(dst, q->g, sizeof(int32_t) * nseg, cudaMemcpyDeviceToDevice, q->st));
+  return PRISM_OK;
+}
+
+int prism_qas_round_device(prism_qas *q, int64_t P, const int64_t *ids, const double *arrival,
+                           const int64_t *sk_off, const int32_t *sk, const uint8_t *reorderable, int64_t A,
+                           const int64_t *act_off, const int32_t *act_sk, int32_t nseg,
+                           const prism_qas_config *cfg, int64_t *nhot, int64_t *ncold, int64_t *nbuckets) {
+  if (cfg->cold_quota > cfg->dispatch_budget || cfg->signature_size < 1 ||
+      cfg->front_width < cfg->signature_size || cfg->signature_size > QMAXK)
+    return qfail(PRISM_INVALID, "invalid SchedulerConfig");
+  cudaSetDevice(q->dev);
+  QCfg c{cfg->dispatch_budget, cfg->cold_quota, cfg->front_width, cfg->signature_size,
+         cfg->w_g, cfg->w_a, cfg->w_n, cfg->alpha_size, cfg->beta_util};
+  const QIn in{ids, arrival, sk_off, sk, reorderable, act_off, act_sk};
+  return qas_run(q, in, P, A, nseg, c, nhot, ncold, nbuckets);
+}
+
+int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, const double *arrival,
+                    const int64_t *sk_off, const int32_t *sk, const uint8_t *reorderable, const int32_t *suffix,
+                    int64_t A, const int64_t *act_off, const int32_t *act_sk, int32_t nseg,
+                    const prism_qas_config *cfg, int64_t sys_len, int64_t chunk, int64_t *members_out,
+                    int64_t *hits, int32_t *leaf_slots, int64_t *leaf_ids, int64_t *n_members,
+                    int64_t *n_admitted) {
+  cudaSetDevice(q->dev);
+  cudaStream_t st = q->st;
+  int64_t nh = 0, nc = 0, nb = 0;
+  if (q->prof_on) cudaEventRecord(q->e0, st);
+  int rc = prism_qas_round_device(q, P, ids, arrival, sk_off, sk, reorderable, A, act_off, act_sk, nseg, cfg, &nh,
+                                  &nc, &nb);
+  if (rc) return rc;
+  if (q->prof_on) {
+    cudaEventRecord(q->e1, st);
+    cudaEventSynchronize(q->e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, q->e0, q->e1);
+    q->ms_round += ms;
+  }
+  const int64_t B = nh + nc;
+  *n_members = B;
+  *n_admitted = 0;
+  if (B == 0) return PRISM_OK;  // engine.py:190-191
+  // protection / active hand-off (engine.py:193-197)
+  const int32_t pol = prism_tree_policy(t);
+  QCK(cudaStreamSynchronize(st));
+  if (pol == 0) {
+    rc = prism_set_protection_device(t, q->prio, nseg, nullptr, nullptr);
+  } else if (pol == 2) {
+    rc = prism_note_active_device(t, q->a, q->nd, nseg);
+  }
+  if (rc) return rc;
+  // dispatch order and serialization (K1)
+  int64_t *members = members_out;
+  if (!members) {
+    QCK(grow(&q->members, q->members_cap, B));
+    members = q->members;
+  }
+  q_members<<<nblk(B), TPB, 0, st>>>(nh, nc, q->hot, q->cv2, members);
+  QCK(grow(&q->plen, q->plen_cap, B + 1));
+  QCK(grow(&q->poff, q->poff_cap, B + 1));
+  QCK(grow(&q->alen, q->alen_cap, B + 1));
+  QCK(grow(&q->aoffs, q->aoffs_cap, B + 1));
+  QCK(cudaMemsetAsync(q->plen + B, 0, sizeof(int64_t), st));
+  QCK(cudaMemsetAsync(q->alen + B, 0, sizeof(int64_t), st));
+  q_serial_len<<<nblk(B), TPB, 0, st>>>(B, members, sk_off, suffix, sys_len, chunk, q->plen, q->alen);
+  if ((rc = scan64(q, q->plen, q->poff, B + 1))) return rc;
+  if ((rc = scan64(q, q->alen, q->aoffs, B + 1))) return rc;
+  int64_t tot[2];
+  QCK(cudaMemcpyAsync(&tot[0], q->poff + B, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  QCK(cudaMemcpyAsync(&tot[1], q->aoffs + B, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  QCK(cudaMemsetAsync(q->err, 0, sizeof(int32_t), st));
+  QCK(cudaStreamSynchronize(st));
+  QCK(grow(&q->tok, q->tok_cap, std::max<int64_t>(tot[0], 1)));
+  QCK(grow(&q->a_off, q->a_off_cap, std::max<int64_t>(tot[1], 1)));
+  QCK(grow(&q->a_kind, q->a_kind_cap, std::max<int64_t>(tot[1], 1)));
+  QCK(grow(&q->a_seg, q->a_seg_cap, std::max<int64_t>(tot[1], 1)));
+  QCK(grow(&q->a_snap, q->a_snap_cap, 3 * std::max<int64_t>(tot[1], 1)));
+  q_serialize<<<nblk(B * 32), TPB, 0, st>>>(B, members, ids, sk_off, q->aligned, suffix, sys_len, chunk, q->g, q->a,
+                                            q->nd, q->poff, q->aoffs, q->tok, q->a_off, q->a_kind, q->a_seg,
+                                            q->a_snap, q->err);
+  QCK(cudaGetLastError());
+  q->launches += 3;
+  q->lib_calls += 2;
+  int32_t err = 0;
+  QCK(cudaMemcpyAsync(&err, q->err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  QCK(cudaStreamSynchronize(st));
+  if (err) return qfail(PRISM_INVALID, "token layout overflows uint32");
+  return prism_admit_wave_device(t, B, q->poff, q->tok, q->aoffs, q->a_off, q->a_kind, q->a_seg, q->a_snap, hits,
+                                 leaf_slots, leaf_ids, n_admitted, (void *)st);
 }
 
 }  // extern "C"

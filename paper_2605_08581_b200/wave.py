@@ -1,0 +1,172 @@
+"""Fused device wave: one serving-loop wave of QAS + DART without host round trips.
+
+``WaveEngine.step(pending)`` runs engine.py:189-213 for a DEVICE-resident
+pending set (``DevicePending``, torch tensors used purely as device buffers):
+the QAS round, the protection / active-set hand-off, serialisation of every
+member's token path from its aligned skeleton, and ordered
+match+insert+evict, all inside libprism.so.  ``release`` drops the pins of
+a completed wave (engine.py:177-181).  This is the path bench.py measures.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check
+from .qas import _cfg
+from .types import CacheConfig, POLICY_CODE, SchedulerConfig, policy_of
+
+_p = C.c_void_p
+_i64 = C.c_int64
+
+
+def _bind(lib):
+    sig = {
+        "prism_wave_step": (C.c_int, [_p, _p, _i64, _p, _p, _p, _p, _p, _p, _i64, _p, _p, C.c_int32, _p,
+                                      _i64, _i64, _p, _p, _p, _p, _p, _p]),
+        "prism_qas_stream": (_p, [_p]),
+        "prism_qas_counters": (C.c_int, [_p, _p, C.c_int32]),
+        "prism_set_protection_device": (C.c_int, [_p, _p, C.c_int32, _p, _p]),
+        "prism_profile": (C.c_int, [_p, C.c_int32]),
+        "prism_profile_read": (C.c_int, [_p, _p]),
+        "prism_qas_counts": (C.c_int, [_p, _p]),
+        "prism_qas_profile": (C.c_int, [_p, C.c_int32]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+@dataclass
+class DevicePending:
+    """A pending snapshot as device CSR (ids, arrival, skeleton offsets/ids,
+    reorderable flags, suffix lengths); segment ids dense in [0, nseg)."""
+
+    ids: torch.Tensor  # int64 [P]
+    arrival: torch.Tensor  # float64 [P]
+    sk_off: torch.Tensor  # int64 [P+1]
+    sk: torch.Tensor  # int32
+    reorderable: torch.Tensor  # uint8 [P]
+    suffix: torch.Tensor  # int32 [P]
+
+    @property
+    def P(self) -> int:
+        return int(self.ids.shape[0])
+
+    @staticmethod
+    def from_host(ids, arrival, sk_off, sk, reorderable, suffix, device) -> "DevicePending":
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dt)  # noqa: E731
+        return DevicePending(t(ids, torch.int64), t(arrival, torch.float64), t(sk_off, torch.int64),
+                             t(sk, torch.int32), t(reorderable, torch.uint8), t(suffix, torch.int32))
+
+    def nbytes(self) -> int:
+        return sum(x.numel() * x.element_size() for x in
+                   (self.ids, self.arrival, self.sk_off, self.sk, self.reorderable, self.suffix))
+
+
+class WaveEngine:
+    """One replica: a device tree (DART) + a device scheduler (QAS)."""
+
+    def __init__(self, cache: CacheConfig, sched: SchedulerConfig, nseg: int, sys_len: int, chunk: int,
+                 device: int = 0, initial_slots: int = 0, initial_arena_tokens: int = 0):
+        _lib.require_device()
+        self.L = _bind(_lib.lib())
+        self.device = device
+        self.cache_cfg, self.sched = cache, sched
+        self.nseg, self.sys_len, self.chunk = nseg, sys_len, chunk
+        self.t = self.L.prism_tree_create(cache.capacity_tokens, POLICY_CODE[policy_of(cache.policy)],
+                                          cache.protect_budget, initial_slots, initial_arena_tokens, device)
+        if not self.t:
+            raise _lib.PrismError(_lib.last_error())
+        self.q = self.L.prism_qas_create(device)
+        if not self.q:
+            raise _lib.PrismError(_lib.last_error())
+        self._cfg = _cfg(sched)
+        dev = torch.device("cuda", device)
+        cap = max(sched.dispatch_budget, 1)
+        self.members = torch.empty(cap, dtype=torch.int64, device=dev)
+        self.hits = torch.empty(cap, dtype=torch.int64, device=dev)
+        self.leaf_slots = torch.empty(cap, dtype=torch.int32, device=dev)
+        self.leaf_ids = torch.empty(cap, dtype=torch.int64, device=dev)
+        self._act_off = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._act_sk = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._nm = np.zeros(1, np.int64)
+        self._na = np.zeros(1, np.int64)
+        self.stream = torch.cuda.ExternalStream(self.L.prism_qas_stream(self.q), device=dev)
+
+    def close(self) -> None:
+        if getattr(self, "t", None):
+            self.L.prism_tree_destroy(self.t)
+            self.t = None
+        if getattr(self, "q", None):
+            self.L.prism_qas_destroy(self.q)
+            self.q = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover
+            pass
+
+    def step(self, pend: DevicePending) -> tuple[int, int]:
+        """One wave; returns (members dispatched, members admitted)."""
+        P = pend.P
+        if P > self.members.shape[0]:
+            dev = self.members.device
+            self.members = torch.empty(P, dtype=torch.int64, device=dev)
+            self.hits = torch.empty(P, dtype=torch.int64, device=dev)
+            self.leaf_slots = torch.empty(P, dtype=torch.int32, device=dev)
+            self.leaf_ids = torch.empty(P, dtype=torch.int64, device=dev)
+        check(self.L.prism_wave_step(
+            self.t, self.q, P, pend.ids.data_ptr(), pend.arrival.data_ptr(), pend.sk_off.data_ptr(),
+            pend.sk.data_ptr(), pend.reorderable.data_ptr(), pend.suffix.data_ptr(), 0,
+            self._act_off.data_ptr(), self._act_sk.data_ptr(), self.nseg, C.addressof(self._cfg),
+            self.sys_len, self.chunk, self.members.data_ptr(), self.hits.data_ptr(), self.leaf_slots.data_ptr(),
+            self.leaf_ids.data_ptr(), self._nm.ctypes.data, self._na.ctypes.data,
+        ))
+        return int(self._nm[0]), int(self._na[0])
+
+    def release(self, slots: torch.Tensor, n: int) -> None:
+        """Drop the pins of n admitted leaves (completions, engine.py:177-181)."""
+        if n > 0:
+            check(self.L.prism_release_device(self.t, n, slots.data_ptr(), None,
+                                              self.L.prism_qas_stream(self.q)))
+
+    def demand_counters(self, dst: torch.Tensor) -> None:
+        """Last round's pending demand counters g (int32 [nseg]) into dst."""
+        check(self.L.prism_qas_counters(self.q, dst.data_ptr(), self.nseg))
+
+    def profile(self, enable: bool) -> None:
+        check(self.L.prism_profile(self.t, 1 if enable else 0))
+        check(self.L.prism_qas_profile(self.q, 1 if enable else 0))
+
+    PHASES = ("commit", "build", "protect", "prematch", "release", "note", "maint")
+
+    def profile_read(self) -> dict:
+        """Cumulative live profile: device ms / calls / launches per phase."""
+        out = np.zeros(27, dtype=np.float64)
+        check(self.L.prism_profile_read(self.t, out.ctypes.data))
+        qc = np.zeros(4, dtype=np.int64)
+        check(self.L.prism_qas_counts(self.q, qc.ctypes.data))
+        prof = {p: {"ms": float(out[i]), "calls": int(out[8 + i]), "launches": int(out[16 + i])}
+                for i, p in enumerate(self.PHASES)}
+        prof["qas"] = {"ms": qc[3] / 1000.0, "calls": int(qc[2]), "launches": int(qc[0])}
+        prof["lib_calls"] = int(out[24]) + int(qc[1])
+        prof["chain_nodes"] = int(out[25])
+        prof["inserted_tokens"] = int(out[26])
+        return prof
+
+    def stats(self) -> dict:
+        out = np.zeros(16, dtype=np.int64)
+        check(self.L.prism_stats(self.t, out.ctypes.data))
+        keys = ["resident", "clock", "next_id", "hw", "live_nodes", "arena_used", "hash_live", "hash_tomb",
+                "victims", "evict_calls", "builds", "slot_cap", "arena_cap", "hash_cap", "fast_members",
+                "slow_members"]
+        return dict(zip(keys, out.tolist()))
