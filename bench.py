@@ -466,6 +466,7 @@ def run_ours(args) -> None:
                 "members_per_rank": members, "victims": victims,
                 "fast_path_members": st2["fast_members"] - st1["fast_members"],
                 "slow_path_members": st2["slow_members"] - st1["slow_members"],
+                "commit": engine.wave_stats(),
             },
             "roofline": roofline,
             "cpu_baseline": cpu,

@@ -99,6 +99,23 @@ int prism_admit_wave_device(prism_tree *t, int64_t B, const int64_t *path_off,
                             int64_t *hits, int32_t *leaf_slots, int64_t *leaf_ids,
                             int64_t *n_admitted_host, void *stream);
 
+/* admit_wave_device for a SEGMENT-STRUCTURED wave (every path = system prefix
+ * sys_len + its aligned skeleton in chunk-token segments + a private suffix,
+ * anchors at every piece boundary -- what prism_wave_step produces).  The
+ * wave is committed by the exact data-parallel algorithm of wave_par.cuh;
+ * if one of its exactness guards trips, by the ordered commit (mode 1 forces
+ * the ordered commit).  members[B] index the pending CSR (sk_off, aligned). */
+int prism_admit_wave_segmented(prism_tree *t, int64_t B, const int64_t *path_off,
+                               const uint32_t *tokens, const int64_t *anc_off,
+                               const int32_t *a_off, const int8_t *a_kind, const int32_t *a_seg,
+                               const int32_t *a_snap, const int64_t *members,
+                               const int64_t *sk_off, const int32_t *aligned, int64_t sys_len,
+                               int64_t chunk, int32_t mode, int64_t *hits, int32_t *leaf_slots,
+                               int64_t *leaf_ids, int64_t *n_admitted_host, void *stream);
+/* out[3]: waves committed in parallel, waves committed in order, last
+ * fallback reason bit-set (wave_par.cuh WPF_*). */
+int prism_wave_stats(prism_tree *t, int64_t *out);
+
 /* Batched release of device-resident leaves (engine.py:177-181 for a whole
  * completion batch); the leaves must hold valid pins. */
 int prism_release_device(prism_tree *t, int64_t n, const int32_t *slots, const int64_t *ids,
@@ -183,6 +200,9 @@ int32_t prism_tree_policy(prism_tree *t);
 /* The cudaStream_t (as void*) the QAS instance launches on; prism_wave_step
  * completes on it, so events recorded there bracket a whole wave. */
 void *prism_qas_stream(prism_qas *q);
+/* Commit used by prism_wave_step: 0 = exact parallel commit with ordered
+ * fallback (default), 1 = ordered commit only (parity cross-check). */
+int prism_qas_set_commit_mode(prism_qas *q, int32_t mode);
 /* out[4]: own kernel launches, CUB primitive calls, rounds so far, and the
  * device microseconds of those rounds when profiling is on. */
 int prism_qas_counts(prism_qas *q, int64_t *out);

@@ -17,6 +17,7 @@
 
 #include "../../include/prism.h"
 #include "dart_kernels.cuh"
+#include "wave_par.cuh"
 
 using namespace prism;
 
@@ -104,6 +105,11 @@ struct prism_tree {
   int64_t prof_calls[8] = {};
   int64_t launches[8] = {};  // own kernel launches per phase (always counted)
   int64_t lib_calls = 0;     // CUB primitive invocations
+  // parallel wave commit scratch
+  WaveTmp wx{};
+  int64_t wx_cap = 0, wx_lt = 0, wx_T = 0;
+  int64_t par_waves = 0, seq_waves = 0;
+  int32_t last_fallback = 0;
 };
 
 enum { PH_COMMIT = 0, PH_BUILD = 1, PH_PROTECT = 2, PH_PREMATCH = 3, PH_RELEASE = 4, PH_NOTE = 5, PH_MAINT = 6 };
@@ -332,6 +338,202 @@ int run_commit(prism_tree *t, CommitArgs a) {
     if (rc) return rc;
   }
   return fail(PRISM_FATAL, "commit did not converge");
+}
+
+template <class T>
+cudaError_t regrow(T **p, int64_t n) {
+  if (*p) cudaFree(*p);
+  return dalloc(p, n);
+}
+
+int wx_ensure(prism_tree *t, int64_t B, int64_t levels, int64_t Tn) {
+  WaveTmp &X = t->wx;
+  if (B > t->wx_cap || !X.hit) {
+    const int64_t c = std::max<int64_t>(next_pow2(B + 1), 64);
+    CK(regrow(&X.hit, c));
+    CK(regrow(&X.pre, c));
+    CK(regrow(&X.npieces, c));
+    CK(regrow(&X.p0, c));
+    CK(regrow(&X.lcp_level, c));
+    CK(regrow(&X.cnew, c + 1));
+    CK(regrow(&X.tail, c + 1));
+    CK(regrow(&X.miss, c + 1));
+    CK(regrow(&X.idb, c + 1));
+    CK(regrow(&X.arb, c + 1));
+    CK(regrow(&X.dem, c + 1));
+    CK(regrow(&X.piece_slot, c * WP_MAXP));
+    CK(regrow(&X.owner, c * WP_MAXP));
+    CK(regrow(&X.cut, c));
+    if (!X.flags) CK(dalloc(&X.flags, 1));
+    if (!X.misc) CK(dalloc(&X.misc, 8));
+    t->wx_cap = c;
+  }
+  const int64_t lt = std::max<int64_t>(next_pow2(4 * levels + 64), 1024);
+  if (lt > t->wx_lt || !X.lt_key) {
+    CK(regrow(&X.lt_key, lt));
+    CK(regrow(&X.lt_min, lt));
+    t->wx_lt = lt;
+  }
+  X.lt_mask = (uint64_t)(lt - 1);
+  if (Tn > t->wx_T || !X.vlen) {
+    const int64_t c = std::max<int64_t>(next_pow2(Tn + 1), 1024);
+    CK(regrow(&X.vlen, c));
+    CK(regrow(&X.F, c));
+    t->wx_T = c;
+  }
+  return PRISM_OK;
+}
+
+template <class In, class Out>
+int cub_scan(prism_tree *t, In in, Out out, int64_t n, bool inclusive) {
+  size_t bytes = 0;
+  if (inclusive) CK(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out, (int)n, t->st));
+  else CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)n, t->st));
+  int rc = ensure_cub(t, bytes);
+  if (rc) return rc;
+  bytes = t->cub_bytes;
+  if (inclusive) CK(cub::DeviceScan::InclusiveSum(t->cub_tmp, bytes, in, out, (int)n, t->st));
+  else CK(cub::DeviceScan::ExclusiveSum(t->cub_tmp, bytes, in, out, (int)n, t->st));
+  t->lib_calls++;
+  return PRISM_OK;
+}
+
+// Parallel commit of a segment-structured wave (wave_par.cuh).  Returns
+// PRISM_OK with *applied = 1 when the wave was committed, *applied = 0 when an
+// exactness guard tripped (nothing was mutated; the caller runs k_commit).
+int admit_wave_par(prism_tree *t, const WaveIn &W, int64_t levels, int64_t *hits, int32_t *leaf_slots,
+                   int64_t *leaf_ids, int *applied) {
+  *applied = 0;
+  const int64_t B = W.B;
+  int rc = pull_ctrl(t);
+  if (rc) return rc;
+  Ctrl &C = *t->hctrl;
+  C.epoch++;
+  const uint32_t epoch = C.epoch;
+  rc = push_ctrl(t);
+  if (rc) return rc;
+  rc = wx_ensure(t, B, levels, 1);
+  if (rc) return rc;
+  WaveTmp &X = t->wx;
+  cudaStream_t st = t->st;
+  prof_begin(t);
+  CK(cudaMemsetAsync(X.lt_key, 0xFF, sizeof(uint64_t) * (size_t)t->wx_lt, st));
+  CK(cudaMemsetAsync(X.lt_min, 0x7F, sizeof(int32_t) * (size_t)t->wx_lt, st));
+  CK(cudaMemsetAsync(X.flags, 0, sizeof(int32_t), st));
+  CK(cudaMemsetAsync(X.cnew + B, 0, sizeof(int64_t), st));
+  CK(cudaMemsetAsync(X.tail + B, 0, sizeof(int64_t), st));
+  CK(cudaMemsetAsync(X.misc, 0, sizeof(int64_t) * 8, st));
+  const int64_t big = INT64_MAX;
+  CK(cudaMemcpyAsync(X.misc + 1, &big, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  k_wp_plan<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, epoch);
+  k_wp_hits<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X);
+  CK(cudaGetLastError());
+  t->launches[PH_COMMIT] += 2;
+  int32_t flags = 0;
+  CK(cudaMemcpyAsync(&flags, X.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (flags) {
+    t->last_fallback = flags;
+    return PRISM_OK;
+  }
+  if ((rc = cub_scan(t, X.cnew, X.idb, B + 1, false))) return rc;
+  if ((rc = cub_scan(t, X.tail, X.arb, B + 1, false))) return rc;
+  if ((rc = cub_scan(t, X.miss, X.dem, B, true))) return rc;
+  int64_t tot[3];
+  CK(cudaMemcpyAsync(&tot[0], X.idb + B, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&tot[1], X.arb + B, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&tot[2], X.dem + B - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const int64_t ncreate = tot[0], ntail = tot[1], nmiss = tot[2];
+  // capacity maintenance (semantics-free): slots, arena, child table
+  if ((int64_t)C.hw + ncreate + 2 > t->d.S) {
+    if ((rc = grow_slots(t, (int64_t)C.hw + ncreate + 2))) return rc;
+    if ((rc = wx_ensure(t, B, levels, 1))) return rc;
+  }
+  if (C.arena_top + ntail > t->d.acap) {
+    if ((rc = compact_arena(t, ntail))) return rc;
+  }
+  if ((C.hlive + C.htomb + ncreate + 64) * 2 > (int64_t)(t->d.hmask + 1)) {
+    if ((rc = rehash(t, ncreate + 64))) return rc;
+  }
+  if ((rc = pull_ctrl(t))) return rc;
+  prof_end(t, PH_COMMIT);
+  const int64_t R0 = C.resident, D = R0 + nmiss - t->d.capacity;
+  int64_t nv = 0, freed = 0, calls = 0;
+  if (D > 0) {
+    if ((rc = build_list(t))) return rc;
+    if ((rc = pull_ctrl(t))) return rc;
+    const int64_t Tn = C.L_n;
+    if (Tn == 0) {
+      t->last_fallback = WPF_CAPACITY;
+      return PRISM_OK;
+    }
+    if ((rc = wx_ensure(t, B, levels, Tn))) return rc;
+    k_wp_vlen<<<blocks_for(Tn), TPB, 0, st>>>(t->d, 0, Tn, X, epoch);
+    if ((rc = cub_scan(t, X.vlen, X.F, Tn, true))) return rc;
+    k_wp_cuts<<<blocks_for(B), TPB, 0, st>>>(B, X.dem, R0, t->d.capacity, X.F, Tn, X.cut, X.flags);
+    CK(cudaGetLastError());
+    t->launches[PH_COMMIT] += 2;
+    std::vector<int64_t> cut((size_t)B);
+    int64_t poison = 0;
+    CK(cudaMemcpyAsync(cut.data(), X.cut, sizeof(int64_t) * B, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&flags, X.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&poison, X.misc + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    nv = cut[B - 1];
+    if (flags || poison < nv) {
+      t->last_fallback = flags ? flags : WPF_VICTIM;
+      return PRISM_OK;
+    }
+    for (int64_t j = 0; j < B; j++) calls += cut[j] > (j ? cut[j - 1] : 0);
+    if (nv > 0) CK(cudaMemcpyAsync(&freed, X.F + nv - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  // ---- apply (from here on the wave is committed)
+  prof_begin(t);
+  const int64_t id0 = C.next_id, clock0 = C.clock, arena0 = C.arena_top;
+  const int32_t ft0 = C.free_top, hw0 = C.hw;
+  const uint32_t vctr0 = C.vctr;
+  if (nv > 0) {
+    k_wp_evict<<<blocks_for(nv), TPB, 0, st>>>(t->d, 0, nv, C.vlog_count, ft0, vctr0, epoch);
+    t->launches[PH_COMMIT]++;
+  }
+  const int32_t ft1 = ft0 + (int32_t)nv;
+  k_wp_alloc<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, id0, ft1, hw0, vctr0 + (uint32_t)nv, epoch);
+  k_wp_label_reset<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X);
+  k_wp_create<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, W, X, arena0, clock0);
+  k_wp_touch<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, clock0);
+  k_wp_label<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, hits, leaf_slots, leaf_ids);
+  CK(cudaGetLastError());
+  t->launches[PH_COMMIT] += 5;
+  int64_t reused = 0, acct[2] = {0, 0};
+  CK(cudaMemcpyAsync(&reused, X.misc + 2, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(acct, X.misc + 3, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  prof_end(t, PH_COMMIT);
+  const int64_t from_free = std::min<int64_t>(ncreate, ft1);
+  C.free_top = ft1 - (int32_t)from_free;
+  C.hw = hw0 + (int32_t)(ncreate - from_free);
+  C.resident = R0 + nmiss - freed;
+  C.clock = clock0 + 2 * B;
+  C.next_id = id0 + ncreate;
+  C.arena_top = arena0 + ntail;
+  C.vlog_count += nv;
+  C.hlive += ncreate - nv;
+  C.htomb += nv - reused;
+  C.evict_calls += calls;
+  C.vctr = vctr0 + (uint32_t)(nv + ncreate);
+  C.n_admitted = (int32_t)B;
+  C.fast_members += B;
+  C.inserted_tokens += acct[0];
+  C.chain_nodes += acct[1];
+  C.status = ST_DONE;
+  C.L_valid = 0;
+  C.H_n = 0;
+  rc = push_ctrl(t);
+  if (rc) return rc;
+  *applied = 1;
+  return PRISM_OK;
 }
 
 template <class T>
@@ -770,6 +972,70 @@ int prism_admit_wave_device(prism_tree *t, int64_t B, const int64_t *path_off, c
     CK(cudaStreamWaitEvent((cudaStream_t)stream, ev, 0));
     CK(cudaEventDestroy(ev));
   }
+  return PRISM_OK;
+}
+
+int prism_admit_wave_segmented(prism_tree *t, int64_t B, const int64_t *path_off, const uint32_t *tokens,
+                               const int64_t *anc_off, const int32_t *a_off, const int8_t *a_kind,
+                               const int32_t *a_seg, const int32_t *a_snap, const int64_t *members,
+                               const int64_t *sk_off, const int32_t *aligned, int64_t sys_len, int64_t chunk,
+                               int32_t mode, int64_t *hits, int32_t *leaf_slots, int64_t *leaf_ids,
+                               int64_t *n_admitted_host, void *stream) {
+  cudaSetDevice(t->dev);
+  if (B <= 0) {
+    *n_admitted_host = 0;
+    return PRISM_OK;
+  }
+  if (mode != 1 && chunk > 0) {
+    if (stream) {
+      cudaEvent_t ev;
+      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CK(cudaEventRecord(ev, (cudaStream_t)stream));
+      CK(cudaStreamWaitEvent(t->st, ev, 0));
+      CK(cudaEventDestroy(ev));
+    }
+    if (B > t->pm_cap || !t->d_pm_meta) {
+      if (t->d_pm_meta) {
+        CK(cudaFree(t->d_pm_meta));
+        CK(cudaFree(t->d_pm_chain));
+      }
+      t->pm_cap = std::max<int64_t>(next_pow2(B), 64);
+      CK(dalloc(&t->d_pm_meta, 4 * t->pm_cap));
+      CK(dalloc(&t->d_pm_chain, PM_MAX * t->pm_cap));
+    }
+    prof_begin(t);
+    k_prematch<<<blocks_for(B * 32), TPB, 0, t->st>>>(t->d, B, path_off, tokens, t->d_pm_meta, t->d_pm_chain);
+    CK(cudaGetLastError());
+    t->launches[PH_PREMATCH]++;
+    prof_end(t, PH_PREMATCH);
+    WaveIn W{B, sys_len, chunk, path_off, tokens, anc_off, a_kind, a_seg, a_snap, members, sk_off, aligned,
+             t->d_pm_meta, t->d_pm_chain};
+    int applied = 0;
+    int rc = admit_wave_par(t, W, B * WP_MAXP, hits, leaf_slots, leaf_ids, &applied);
+    if (rc) return rc;
+    if (applied) {
+      t->par_waves++;
+      *n_admitted_host = B;
+      if (stream) {
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev, t->st));
+        CK(cudaStreamWaitEvent((cudaStream_t)stream, ev, 0));
+        CK(cudaEventDestroy(ev));
+      }
+      return PRISM_OK;
+    }
+  }
+  t->seq_waves++;
+  return prism_admit_wave_device(t, B, path_off, tokens, anc_off, a_off, a_kind, a_seg, a_snap, hits, leaf_slots,
+                                 leaf_ids, n_admitted_host, stream);
+}
+
+// out[3]: waves committed in parallel, waves committed in order, last fallback reason flags
+int prism_wave_stats(prism_tree *t, int64_t *out) {
+  out[0] = t->par_waves;
+  out[1] = t->seq_waves;
+  out[2] = t->last_fallback;
   return PRISM_OK;
 }
 

@@ -489,6 +489,7 @@ struct prism_qas {
   QBUF(int32_t, a_snap)
 #undef QBUF
   int64_t launches = 0, lib_calls = 0, rounds = 0;
+  int32_t commit_mode = 0;
   int prof_on = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   double ms_round = 0.0;  // QAS round + serialization device time (events on q->st)
@@ -1015,8 +1016,15 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
   QCK(cudaMemcpyAsync(&err, q->err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   QCK(cudaStreamSynchronize(st));
   if (err) return qfail(PRISM_INVALID, "token layout overflows uint32");
-  return prism_admit_wave_device(t, B, q->poff, q->tok, q->aoffs, q->a_off, q->a_kind, q->a_seg, q->a_snap, hits,
-                                 leaf_slots, leaf_ids, n_admitted, (void *)st);
+  return prism_admit_wave_segmented(t, B, q->poff, q->tok, q->aoffs, q->a_off, q->a_kind, q->a_seg, q->a_snap,
+                                    members, sk_off, q->aligned, sys_len, chunk, q->commit_mode, hits, leaf_slots,
+                                    leaf_ids, n_admitted, (void *)st);
+}
+
+// 0: exact parallel wave commit with ordered fallback (default); 1: ordered commit only
+int prism_qas_set_commit_mode(prism_qas *q, int32_t mode) {
+  q->commit_mode = mode;
+  return PRISM_OK;
 }
 
 }  // extern "C"

@@ -1,0 +1,407 @@
+// wave_par.cuh -- exact PARALLEL commit of one segment-structured wave.
+//
+// The ordered commit (k_commit) replays engine.py:200-213 member by member.
+// For waves produced by the fused step -- every path is
+//   [system prefix sys][segment 1 .. k, chunk tokens each][private suffix]
+// with anchors at every piece boundary (engine.py:269-292) and segment
+// tokens unique per segment id (workload.py:136-154) -- the same result is
+// computed here with data-parallel passes:
+//
+//   * intra-wave sharing: the longest prefix member j shares with any earlier
+//     member is sys + chunk * (longest common aligned-skeleton prefix), found
+//     by a first-owner table over skeleton prefixes (atomicMin of member id);
+//   * hit_j = max(pre-wave match, intra-wave share) -- LCP against a union of
+//     prefix-closed path sets is the max of the LCPs;
+//   * node ids: member j creates its tail + one node per anchor inside it, ids
+//     by an exclusive prefix sum, tail keeps the base id, uppers get base+1..
+//     top-down (kvcache.py:213-236 split order);
+//   * eviction: the wave's victims are a prefix of the eviction stream L
+//     (subtree-max order, built on the pre-wave tree); member j's evict call
+//     consumes L until the cumulative freed tokens reach its cumulative
+//     demand D_j = R0 + sum_{i<=j} missing_i - capacity;
+//   * touches / pins / labels: atomics (hits += 2 per traversing member, last =
+//     max insert tick, ref += 1, label = last writer = max member index).
+//
+// Exactness guards (else the host falls back to k_commit for the wave): no
+// pre-match chain overflow, no partially matched pre-wave node, pre-wave
+// chain nodes aligned 1:1 with pieces, no skeleton-hash collision, no
+// consumed victim on any member's pre-wave chain, enough evictable tokens.
+#pragma once
+#include "dart_kernels.cuh"
+
+namespace prism {
+
+constexpr int WP_MAXP = 66;  // pieces per path: sys + 64 segments + suffix
+enum { WPF_OVERFLOW = 1, WPF_PARTIAL = 2, WPF_ALIGN = 4, WPF_COLLIDE = 8, WPF_VICTIM = 16, WPF_CAPACITY = 32,
+       WPF_SHAPE = 64 };
+
+struct WaveIn {
+  int64_t B, sys, chunk;
+  const int64_t *poff;
+  const uint32_t *tok;
+  const int64_t *aoffs;
+  const int8_t *a_kind;
+  const int32_t *a_seg;
+  const int32_t *a_snap;
+  const int64_t *members;
+  const int64_t *sk_off;
+  const int32_t *aligned;
+  const int32_t *pm_meta;
+  const int32_t *pm_chain;
+};
+
+struct WaveTmp {
+  int32_t *hit, *pre, *npieces, *p0, *lcp_level;
+  int64_t *cnew, *tail, *miss;       // per member (+1 for scans)
+  int64_t *idb, *arb, *dem;          // scans
+  int32_t *piece_slot;               // [B * WP_MAXP] own new pieces
+  int32_t *owner;                    // [B * WP_MAXP] owner member of shared pieces
+  uint64_t *lt_key;                  // level table
+  int32_t *lt_min;
+  uint64_t lt_mask;
+  int32_t *flags;                    // [1]
+  int64_t *vlen, *F;                 // eviction stream prefix
+  int64_t *cut;                      // per member: victims consumed through member j
+  int64_t *misc;                     // [8] device scalars
+};
+
+__device__ inline int64_t wp_end(const WaveIn &W, int p, int k, int64_t n) {
+  // end depth of piece p: [sys][seg 0..k-1][suffix]
+  const int has_sys = W.sys > 0;
+  if (has_sys && p == 0) return W.sys;
+  const int q = p - has_sys;  // segment index
+  if (q < k) return W.sys + (int64_t)(q + 1) * W.chunk;
+  return n;
+}
+
+__device__ inline int wp_level_of_piece(const WaveIn &W, int p) {
+  // number of segments covered through the end of piece p
+  return p + (W.sys > 0 ? 0 : 1);
+}
+
+__device__ inline uint64_t wp_level_key(int level, uint64_t h) {
+  uint64_t x = mix64(h ^ (0x9E3779B97F4A7C15ull * (uint64_t)(level + 1)));
+  return x >> 1;  // never HEMPTY
+}
+
+__device__ inline uint64_t wp_hash_next(uint64_t h, int32_t seg) { return mix64(h * 31 + (uint32_t)seg + 0x1234567ull); }
+
+__device__ inline int32_t wp_table(const WaveTmp &X, uint64_t key, int32_t j, bool insert) {
+  uint64_t h = mix64(key) & X.lt_mask;
+  for (;;) {
+    if (insert) {
+      const unsigned long long prev = atomicCAS((unsigned long long *)&X.lt_key[h], (unsigned long long)HEMPTY,
+                                                (unsigned long long)key);
+      if (prev == HEMPTY || prev == key) {
+        atomicMin(&X.lt_min[h], j);
+        return (int32_t)h;
+      }
+    } else {
+      const uint64_t k = X.lt_key[h];
+      if (k == key) return X.lt_min[h];
+      if (k == HEMPTY) return -1;
+    }
+    h = (h + 1) & X.lt_mask;
+  }
+}
+
+// W1: per-member plan checks + skeleton-prefix ownership table
+__global__ void k_wp_plan(DT T, WaveIn W, WaveTmp X, uint32_t epoch) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= W.B) return;
+  const int64_t m = W.members[j];
+  const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
+  const int32_t *s = W.aligned + W.sk_off[m];
+  const int64_t n = W.poff[j + 1] - W.poff[j];
+  const int64_t sfx = n - W.sys - (int64_t)k * W.chunk;
+  const int P = (W.sys > 0) + k + (sfx > 0);
+  int flag = 0;
+  if (sfx < 0 || P > WP_MAXP || W.aoffs[j + 1] - W.aoffs[j] != P) flag |= WPF_SHAPE;
+  const int32_t hit_pre = W.pm_meta[4 * j + 0], d = W.pm_meta[4 * j + 1], fl = W.pm_meta[4 * j + 3];
+  if (fl & 2) flag |= WPF_OVERFLOW;
+  if (fl & 1) flag |= WPF_PARTIAL;
+  // pre-wave chain nodes must coincide with the first d pieces
+  if (!flag) {
+    if (d > P) flag |= WPF_ALIGN;
+    for (int p = 0; p < d && !flag; p++) {
+      const int32_t c = W.pm_chain[j * PM_MAX + p];
+      if ((int64_t)T.dend[c] != wp_end(W, p, k, n)) flag |= WPF_ALIGN;
+      T.wchild[c] = epoch;  // "on some member's pre-wave chain" (victim guard)
+    }
+    if (!flag && (d > 0 ? wp_end(W, d - 1, k, n) : 0) != hit_pre) flag |= WPF_ALIGN;
+  }
+  if (flag) {
+    atomicOr(X.flags, flag);
+    return;
+  }
+  X.pre[j] = hit_pre;
+  X.npieces[j] = P;
+  // skeleton-prefix levels: level L = sys piece plus the first L segments
+  uint64_t h = 0x51ED270B27ull;
+  const int lmin = W.sys > 0 ? 0 : 1;
+  for (int L = 0; L <= k; L++) {
+    if (L > 0) h = wp_hash_next(h, s[L - 1]);
+    if (L >= lmin) wp_table(X, wp_level_key(L, h), (int32_t)j, true);
+  }
+}
+
+// W2: intra-wave share, hit, new pieces, demand
+__global__ void k_wp_hits(DT T, WaveIn W, WaveTmp X) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= W.B) return;
+  if (*X.flags) return;
+  const int64_t m = W.members[j];
+  const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
+  const int32_t *s = W.aligned + W.sk_off[m];
+  const int64_t n = W.poff[j + 1] - W.poff[j];
+  const int P = X.npieces[j];
+  const int lmin = W.sys > 0 ? 0 : 1;
+  uint64_t h = 0x51ED270B27ull;
+  int lstar = -1;
+  int32_t own_at[WP_MAXP];
+  for (int L = 0; L <= k; L++) {
+    if (L > 0) h = wp_hash_next(h, s[L - 1]);
+    if (L < lmin) continue;
+    const int32_t o = wp_table(X, wp_level_key(L, h), (int32_t)j, false);
+    if (o < 0 || o >= j) break;
+    own_at[L] = o;
+    lstar = L;
+  }
+  int64_t lcpw = 0;
+  if (lstar >= 0) {
+    // verify the owner really shares the skeleton prefix (hash collisions)
+    const int32_t o = own_at[lstar];
+    const int64_t mo = W.members[o];
+    const int ko = (int)(W.sk_off[mo + 1] - W.sk_off[mo]);
+    const int32_t *so = W.aligned + W.sk_off[mo];
+    bool same = ko >= lstar;
+    for (int q = 0; same && q < lstar; q++) same = so[q] == s[q];
+    if (!same) {
+      atomicOr(X.flags, WPF_COLLIDE);
+      return;
+    }
+    lcpw = W.sys + (int64_t)lstar * W.chunk;
+  }
+  const int64_t hit_pre = X.pre[j];
+  const int64_t hit = hit_pre > lcpw ? hit_pre : lcpw;
+  // first new piece and owners of the shared (intra-wave) pieces
+  int p0 = P;
+  for (int p = 0; p < P; p++) {
+    const int64_t e = wp_end(W, p, k, n);
+    if (e > hit) {
+      p0 = p;
+      break;
+    }
+    const int L = wp_level_of_piece(W, p);
+    X.owner[j * WP_MAXP + p] = (e > hit_pre && L <= lstar) ? own_at[L] : -1;
+  }
+  atomicAdd((unsigned long long *)&X.misc[3], (unsigned long long)n);   // inserted path tokens
+  atomicAdd((unsigned long long *)&X.misc[4], (unsigned long long)p0);  // matched nodes
+  X.hit[j] = (int32_t)hit;
+  X.p0[j] = p0;
+  X.lcp_level[j] = lstar;
+  X.cnew[j] = hit < n ? (P - p0) : 0;
+  X.tail[j] = n - hit;
+  X.miss[j] = n - hit;
+}
+
+// eviction stream prefix: token length of each list entry; misc[1] = first
+// entry that a member's pin or guard would make non-evictable (list entries
+// with children are fine: the stream puts every descendant first)
+__global__ void k_wp_vlen(DT T, int64_t T0, int64_t Tn, WaveTmp X, uint32_t epoch) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Tn) return;
+  const uint64_t v = T.Lv[T0 + i];
+  const int32_t s = (int32_t)(v & 0xffffffffu);
+  const bool valid = T.kver[s] == (uint32_t)(v >> 32) && T.nid[s] >= 0 && T.par[s] >= 0 && T.ref[s] == 0;
+  X.vlen[i] = valid ? T.elen[s] : 0;
+  if (!valid || T.wchild[s] == epoch) atomicMin((unsigned long long *)&X.misc[1], (unsigned long long)i);
+}
+
+// per member: number of list entries consumed through member j (first F >= D_j)
+__global__ void k_wp_cuts(int64_t B, const int64_t *__restrict__ dem, int64_t R0, int64_t cap,
+                          const int64_t *__restrict__ F, int64_t Tn, int64_t *__restrict__ cut,
+                          int32_t *flags) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= B) return;
+  const int64_t D = R0 + dem[j] - cap;  // dem = inclusive sum of missing
+  int64_t c = 0;
+  if (D > 0) {
+    int64_t lo = 0, hi = Tn;  // first idx with F[idx] >= D
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (F[mid] >= D) hi = mid;
+      else lo = mid + 1;
+    }
+    if (lo >= Tn) {
+      atomicOr(flags, WPF_CAPACITY);
+      c = Tn;
+    } else {
+      c = lo + 1;
+    }
+  }
+  cut[j] = c;
+}
+
+// apply the consumed victims [0, nv) of the stream (stream order == victim order)
+__global__ void k_wp_evict(DT T, int64_t T0, int64_t nv, int64_t vbase, int32_t free_top0, uint32_t vctr0,
+                           uint32_t epoch) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  const int32_t s = (int32_t)(T.Lv[T0 + i] & 0xffffffffu);
+  const int32_t p = T.par[s];
+  atomicSub(&T.nch[p], 1);
+  VRec rec;
+  rec.id = T.nid[s];
+  rec.eoff = T.eoff[s];
+  rec.ftok = T.ftok[s];
+  rec.elen = T.elen[s];
+  rec.seg = T.seg[s];
+  rec.kind = (int8_t)T.kind[s];
+  rec.pad[0] = rec.pad[1] = rec.pad[2] = 0;
+  T.ht[T.hslot[s]].key = HTOMB;
+  T.vlog[(vbase + i) % T.vcap] = rec;
+  T.nid[s] = -1;
+  T.par[s] = -1;
+  T.kver[s] = vctr0 + (uint32_t)i + 1;
+  T.wmod[s] = epoch;
+  T.freelist[free_top0 + i] = s;
+}
+
+// W6a: slot of every new piece (free list LIFO, then the high-water mark)
+__global__ void k_wp_alloc(DT T, WaveIn W, WaveTmp X, int64_t id0, int32_t free_top, int32_t hw,
+                           uint32_t vctr0, uint32_t epoch) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= W.B || X.cnew[j] == 0) return;
+  const int P = X.npieces[j], p0 = X.p0[j];
+  const int64_t g0 = X.idb[j];  // global index of this member's first new piece
+  for (int p = p0; p < P; p++) {
+    const int64_t g = g0 + (p - p0);
+    const int32_t s = g < free_top ? T.freelist[free_top - 1 - g] : (int32_t)(hw + (g - free_top));
+    X.piece_slot[j * WP_MAXP + p] = s;
+    // ids: the tail keeps the base id, uppers get base+1.. top-down
+    const int64_t id = (p == P - 1) ? id0 + g0 : id0 + g0 + 1 + (p - p0);
+    T.nid[s] = id;
+    T.nch[s] = 0;
+    T.ref[s] = 0;
+    T.kver[s] = vctr0 + (uint32_t)g + 1;
+    T.wmod[s] = epoch;
+    T.wchild[s] = 0;
+    T.waitf[s] = 0;
+    T.guard[s] = 0;
+    T.prot[s] = 0;
+    T.hasanc[s] = 0;
+    T.eff[s] = -1;  // label owner (reset)
+  }
+}
+
+__device__ inline int32_t wp_node(const WaveIn &W, const WaveTmp &X, int64_t j, int p) {
+  const int d = W.pm_meta[4 * j + 1];
+  if (p < d) return W.pm_chain[j * PM_MAX + p];
+  if (p < X.p0[j]) return X.piece_slot[X.owner[j * WP_MAXP + p] * WP_MAXP + p];
+  return X.piece_slot[j * WP_MAXP + p];
+}
+
+// W6b: fields, child-table entries and tokens of the new pieces (warp per member)
+__global__ void k_wp_create(DT T, WaveIn W, WaveTmp X, int64_t arena0, int64_t clock0) {
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = lane_id();
+  if (j >= W.B || X.cnew[j] == 0) return;
+  const int64_t m = W.members[j];
+  const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
+  const int64_t n = W.poff[j + 1] - W.poff[j];
+  const int64_t hit = X.hit[j];
+  const uint32_t *path = W.tok + W.poff[j];
+  const int64_t ab = arena0 + X.arb[j];
+  for (int64_t i = lane; i < n - hit; i += 32) T.tok[ab + i] = path[hit + i];
+  const int P = X.npieces[j], p0 = X.p0[j];
+  const int64_t tick = clock0 + 2 * j + 2;
+  for (int p = p0 + lane; p < P; p += 32) {
+    const int32_t s = X.piece_slot[j * WP_MAXP + p];
+    const int64_t b = p == 0 ? 0 : wp_end(W, p - 1, k, n);
+    const int64_t e = wp_end(W, p, k, n);
+    const int32_t parent = p == p0 ? (p == 0 ? ROOT : wp_node(W, X, j, p - 1)) : X.piece_slot[j * WP_MAXP + p - 1];
+    T.par[s] = parent;
+    T.ftok[s] = path[b];
+    T.eoff[s] = ab + (b - hit);
+    T.elen[s] = (int32_t)(e - b);
+    T.dend[s] = (int32_t)e;
+    T.last[s] = tick;
+    T.hits[s] = 1;
+    T.kind[s] = K_PRIVATE;
+    T.seg[s] = SEG_NONE;
+    atomicAdd(&T.nch[parent], 1);
+    const uint64_t key = ckey(parent, path[b]);
+    uint64_t h = mix64(key) & T.hmask;
+    for (;;) {
+      const uint64_t cur = T.ht[h].key;
+      if (cur == HEMPTY || cur == HTOMB) {
+        const unsigned long long prev = atomicCAS((unsigned long long *)&T.ht[h].key, cur, key);
+        if (prev == cur) {
+          if (cur == HTOMB) atomicAdd((unsigned long long *)&X.misc[2], 1ull);  // tombstone reused
+          break;
+        }
+        continue;  // lost the race for this cell: re-read it
+      }
+      h = (h + 1) & T.hmask;
+    }
+    T.ht[h].val = (uint32_t)s;
+    T.hslot[s] = (int32_t)h;
+  }
+}
+
+// W7: touches of pre-existing nodes, pins, and last-writer label election
+__global__ void k_wp_touch(DT T, WaveIn W, WaveTmp X, int64_t clock0) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= W.B) return;
+  const int P = X.npieces[j];
+  const int own0 = X.cnew[j] ? X.p0[j] : P;
+  const unsigned long long tick = (unsigned long long)(clock0 + 2 * j + 2);
+  for (int p = 0; p < P; p++) {
+    const int32_t s = wp_node(W, X, j, p);
+    if (p < own0) {  // existed before this member: match + insert touches
+      atomicAdd(&T.hits[s], 2);
+      atomicMax((unsigned long long *)&T.last[s], tick);
+    }
+    atomicAdd(&T.ref[s], 1);
+    atomicMax(&T.eff[s], (int32_t)j);
+  }
+  atomicAdd(&T.ref[ROOT], 1);  // _pin reaches the root (kvcache.py:344-348)
+}
+
+__global__ void k_wp_label_reset(DT T, WaveIn W, WaveTmp X) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= W.B) return;
+  const int own0 = X.cnew[j] ? X.p0[j] : X.npieces[j];
+  for (int p = 0; p < own0; p++) T.eff[wp_node(W, X, j, p)] = -1;
+}
+
+// W8: the elected (max-index) member writes kind/seg/anchor (kvcache.py:317-340)
+__global__ void k_wp_label(DT T, WaveIn W, WaveTmp X, int64_t *hits, int32_t *leaf_slots, int64_t *leaf_ids) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= W.B) return;
+  const int64_t m = W.members[j];
+  const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
+  const int64_t n = W.poff[j + 1] - W.poff[j];
+  const int P = X.npieces[j];
+  for (int p = 0; p < P; p++) {
+    const int32_t s = wp_node(W, X, j, p);
+    if (T.eff[s] != (int32_t)j) continue;
+    const int64_t a = W.aoffs[j] + p;
+    T.kind[s] = (uint8_t)W.a_kind[a];
+    T.seg[s] = W.a_seg[a];
+    T.hasanc[s] = 1;
+    T.akind[s] = (uint8_t)W.a_kind[a];
+    T.aseg[s] = W.a_seg[a];
+    T.aoff[s] = (int32_t)wp_end(W, p, k, n);
+    T.snap[3 * (int64_t)s] = W.a_snap[3 * a];
+    T.snap[3 * (int64_t)s + 1] = W.a_snap[3 * a + 1];
+    T.snap[3 * (int64_t)s + 2] = W.a_snap[3 * a + 2];
+  }
+  const int32_t leaf = P > 0 ? wp_node(W, X, j, P - 1) : ROOT;
+  if (hits) hits[j] = X.hit[j];
+  if (leaf_slots) leaf_slots[j] = leaf;
+  if (leaf_ids) leaf_ids[j] = T.nid[leaf];
+}
+
+}  // namespace prism

@@ -172,11 +172,29 @@ class DeviceRadixCache:
         self._snap_cache = None
         self._op = np.zeros(8, dtype=np.int64)
 
+    @classmethod
+    def attach(cls, handle, config: CacheConfig, record_victims: bool = True) -> "DeviceRadixCache":
+        """A non-owning view of an existing device tree (e.g. a WaveEngine's)."""
+        self = cls.__new__(cls)
+        self.config = config
+        self._policy = policy_of(config.policy)
+        self._L = _lib.lib()
+        self._h = handle
+        self._owner = False
+        self.device = None
+        self._record = record_victims
+        self._vlog_seen = 0
+        self._victim_ids = []
+        self._last = (0, 0)
+        self._snap_cache = None
+        self._op = np.zeros(8, dtype=np.int64)
+        return self
+
     def close(self) -> None:
         h = getattr(self, "_h", None)
-        if h:
+        if h and getattr(self, "_owner", True):
             self._L.prism_tree_destroy(h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         try:

@@ -36,6 +36,8 @@ def _bind(lib):
         "prism_profile_read": (C.c_int, [_p, _p]),
         "prism_qas_counts": (C.c_int, [_p, _p]),
         "prism_qas_profile": (C.c_int, [_p, C.c_int32]),
+        "prism_qas_set_commit_mode": (C.c_int, [_p, C.c_int32]),
+        "prism_wave_stats": (C.c_int, [_p, _p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -142,6 +144,21 @@ class WaveEngine:
     def demand_counters(self, dst: torch.Tensor) -> None:
         """Last round's pending demand counters g (int32 [nseg]) into dst."""
         check(self.L.prism_qas_counters(self.q, dst.data_ptr(), self.nseg))
+
+    def set_commit_mode(self, mode: int) -> None:
+        """0: exact parallel wave commit with ordered fallback; 1: ordered only."""
+        check(self.L.prism_qas_set_commit_mode(self.q, mode))
+
+    def wave_stats(self) -> dict:
+        out = np.zeros(3, dtype=np.int64)
+        check(self.L.prism_wave_stats(self.t, out.ctypes.data))
+        return {"parallel_waves": int(out[0]), "ordered_waves": int(out[1]), "last_fallback": int(out[2])}
+
+    def cache_view(self):
+        """The reference RadixCache API over this engine's tree (tests/debug)."""
+        from .dart import DeviceRadixCache
+
+        return DeviceRadixCache.attach(self.t, self.cache_cfg)
 
     def profile(self, enable: bool) -> None:
         check(self.L.prism_profile(self.t, 1 if enable else 0))

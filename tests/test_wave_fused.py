@@ -1,0 +1,137 @@
+"""The fused device wave (prism_wave_step) against the CPU oracle.
+
+Each wave: QAS round -> protection / active-set hand-off -> serialization ->
+admission, on the device (exact parallel commit with ordered fallback, and
+the ordered commit alone) and on the oracle driven exactly like
+engine.py:189-213.  Compared per wave: dispatch order, hit lengths, leaf
+node ids; at the end: the whole tree (debug_nodes) and every eviction victim.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle.oracle import OracleRadixCache, oracle_schedule_round
+from paper_2605_08581_b200.engine import build_anchors
+from paper_2605_08581_b200.types import (
+    CacheConfig,
+    CachePolicy,
+    CapacityError,
+    Request,
+    SchedulerConfig,
+    SegmentCatalog,
+    count_segments,
+    serialize_tokens,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+def _requests(rng, first_id, n, nseg, hot, kmin, kmax, suffixes, sys, chunk, zipf=1.3):
+    reqs = []
+    for i in range(n):
+        k = int(rng.integers(kmin, kmax + 1))
+        sk = []
+        if rng.random() < 0.7 and hot:
+            sk.append(int(min(rng.zipf(zipf), hot) - 1))
+        while len(sk) < k:
+            c = int(rng.integers(0, nseg))
+            if c not in sk:
+                sk.append(c)
+        sfx = int(rng.choice(suffixes))
+        reqs.append(Request(first_id + i, float(first_id + i) * 0.01, sk, True, [], sys, k * chunk, sfx))
+    return reqs
+
+
+def _pending_arrays(reqs):
+    P = len(reqs)
+    off = np.zeros(P + 1, np.int64)
+    np.cumsum([len(r.skeleton) for r in reqs], out=off[1:])
+    return (np.array([r.id for r in reqs], np.int64), np.array([r.arrival_time for r in reqs], np.float64), off,
+            np.array([s for r in reqs for s in r.skeleton], np.int32), np.ones(P, np.uint8),
+            np.array([r.suffix_len for r in reqs], np.int32))
+
+
+def run_case(seed, policy, mode, nseg=40, hot=6, kmin=2, kmax=5, suffixes=(2, 4), sys=8, chunk=4, cap=600,
+             wave=24, nwaves=8, protect=3, cold=2):
+    import torch
+
+    from paper_2605_08581_b200.wave import DevicePending, WaveEngine
+
+    rng = np.random.default_rng(seed)
+    cfg = CacheConfig(capacity_tokens=cap, policy=policy, protect_budget=protect)
+    scfg = SchedulerConfig(dispatch_budget=wave, cold_quota=cold)
+    eng = WaveEngine(cfg, scfg, nseg, sys, chunk, device=0)
+    eng.set_commit_mode(mode)
+    ora = OracleRadixCache(cfg)
+    cat = SegmentCatalog(num_segments=nseg, chunk_tokens=chunk, hot_set=tuple(range(min(hot, nseg))),
+                         sys_prefix_tokens=sys)
+    dev_prev = 0
+    ora_prev = []
+    next_id = 0
+    for w in range(nwaves):
+        reqs = _requests(rng, next_id, wave + int(rng.integers(0, 6)), nseg, hot, kmin, kmax, suffixes, sys, chunk)
+        next_id += len(reqs)
+        pend = DevicePending.from_host(*_pending_arrays(reqs), torch.device("cuda", 0))
+        eng.release(eng.leaf_slots, dev_prev)
+        nm, na = eng.step(pend)
+        dev_prev = na
+        members = eng.members[:nm].cpu().tolist()
+        hits = eng.hits[:na].cpu().tolist()
+        leaf_ids = eng.leaf_ids[:na].cpu().tolist()
+        # oracle, the engine's own order of operations
+        for leaf in ora_prev:
+            ora.release_path(leaf)
+        ora_prev = []
+        b = oracle_schedule_round(reqs, [], scfg, 0.0)
+        idx = {r.id: i for i, r in enumerate(reqs)}
+        assert members == [idx[r.id] for r in b.members], f"wave {w}: dispatch order"
+        if policy is CachePolicy.DART:
+            ora.set_protection(b.priorities)
+        elif policy is CachePolicy.LRU_ACTIVE:
+            counts = count_segments(b.members)
+            ora.note_active_segments(r for r, c in counts.items() if c > 0)
+        ohits, oleaves = [], []
+        for r in b.members:
+            h = b.hints[r.id]
+            path = serialize_tokens(r, cat, h.aligned_skeleton)
+            hit = ora.match_prefix(path)[0]
+            try:
+                oleaves.append(ora.insert_path(path, build_anchors(r, h.aligned_skeleton, h.counter_snapshot)))
+            except CapacityError:
+                break
+            ohits.append(hit)
+        ora_prev = oleaves
+        assert hits == ohits, f"wave {w}: hits"
+        assert leaf_ids == [x.node_id for x in oleaves], f"wave {w}: leaf ids"
+    view = eng.cache_view()
+    assert view.debug_nodes() == ora.debug_nodes()
+    assert view.victim_log() == ora.victim_log()
+    assert view.resident_tokens == ora.resident_tokens
+    return eng.wave_stats()
+
+
+@pytest.mark.parametrize("policy", list(CachePolicy))
+@pytest.mark.parametrize("seed", range(3))
+def test_parallel_commit_matches_oracle(policy, seed):
+    st = run_case(seed, policy, mode=0)
+    assert st["parallel_waves"] > 0, st
+
+
+@pytest.mark.parametrize("policy", [CachePolicy.DART, CachePolicy.LRU])
+def test_ordered_commit_matches_oracle(policy):
+    st = run_case(11, policy, mode=1)
+    assert st["parallel_waves"] == 0
+
+
+@pytest.mark.parametrize("variant", [
+    dict(suffixes=(0,), kmin=1, kmax=3),               # shared whole paths, prefix paths
+    dict(sys=0, suffixes=(0, 3)),                      # no system prompt
+    dict(cap=120, wave=16, nwaves=10),                 # capacity stops (ordered fallback)
+    dict(nseg=8, hot=4, kmin=3, kmax=6, wave=48),      # heavy intra-wave sharing
+    dict(chunk=1, sys=3, kmax=8, suffixes=(1, 2)),     # one-token segments
+    dict(cap=100_000, nwaves=4),                       # no eviction at all
+])
+def test_parallel_commit_variants(variant):
+    run_case(5, CachePolicy.DART, mode=0, **variant)
