@@ -325,6 +325,7 @@ def run_ours(args) -> None:
     st1 = engine.stats()
     clocks = Clocks(local)
     clocks.start()
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" scopes profiles here
     evs = []
     admitted = members = 0
     for s in range(args.warmup, nsteps):
@@ -339,6 +340,7 @@ def run_ours(args) -> None:
         admitted += na
         members += nm
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()

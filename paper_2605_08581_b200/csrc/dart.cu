@@ -17,6 +17,7 @@
 
 #include "../../include/prism.h"
 #include "dart_kernels.cuh"
+#include "select.cuh"
 #include "wave_par.cuh"
 
 using namespace prism;
@@ -63,9 +64,12 @@ struct prism_tree {
   DT d{};
   Ctrl *hctrl = nullptr;  // pinned
   int64_t protect_budget = 0;
-  // candidate buffers (gather output / sort input), sized S
-  Key3 *ck = nullptr;
-  uint64_t *cv = nullptr;
+  // candidate buffers (gather output / selection rounds / selected set), sized S
+  Key3 *ck = nullptr, *ck2 = nullptr, *ks = nullptr;
+  uint64_t *cv = nullptr, *cv2 = nullptr, *vs = nullptr;
+  int64_t *cw = nullptr, *cw2 = nullptr;
+  SelState *sel = nullptr;
+  Key3 *bmin = nullptr, *bmax = nullptr;
   int64_t *d_count = nullptr;
   int64_t *h_small = nullptr;  // pinned scratch
   void *cub_tmp = nullptr;
@@ -151,13 +155,35 @@ std::vector<SlotField> slot_fields(prism_tree *t) {
   };
 }
 
+// candidate / selection scratch, sized with the slot capacity
+int alloc_scratch(prism_tree *t, int64_t S) {
+  void **bufs[] = {(void **)&t->ck, (void **)&t->cv, (void **)&t->cw, (void **)&t->ck2, (void **)&t->cv2,
+                   (void **)&t->cw2, (void **)&t->ks, (void **)&t->vs};
+  for (void **b : bufs)
+    if (*b) CK(cudaFree(*b));
+  CK(dalloc(&t->ck, S));
+  CK(dalloc(&t->cv, S));
+  CK(dalloc(&t->cw, S));
+  CK(dalloc(&t->ck2, S));
+  CK(dalloc(&t->cv2, S));
+  CK(dalloc(&t->cw2, S));
+  CK(dalloc(&t->ks, S));
+  CK(dalloc(&t->vs, S));
+  if (!t->sel) {
+    CK(dalloc(&t->sel, 1));
+    CK(dalloc(&t->bmin, 2048));
+    CK(dalloc(&t->bmax, 2048));
+  }
+  return PRISM_OK;
+}
+
 int alloc_slots(prism_tree *t, int32_t S) {
   for (auto &f : slot_fields(t)) {
     CK(cudaMalloc(f.ptr, f.elem * (size_t)S));
     CK(cudaMemsetAsync(*f.ptr, 0, f.elem * (size_t)S, t->st));
   }
-  CK(dalloc(&t->ck, S));
-  CK(dalloc(&t->cv, S));
+  int rc = alloc_scratch(t, S);
+  if (rc) return rc;
   t->d.S = S;
   return PRISM_OK;
 }
@@ -176,10 +202,8 @@ int grow_slots(prism_tree *t, int64_t need_total) {
     CK(cudaFree(*f.ptr));
     *f.ptr = np;
   }
-  CK(cudaFree(t->ck));
-  CK(cudaFree(t->cv));
-  CK(dalloc(&t->ck, S2));
-  CK(dalloc(&t->cv, S2));
+  int rc = alloc_scratch(t, S2);
+  if (rc) return rc;
   t->d.S = (int32_t)S2;
   return PRISM_OK;
 }
@@ -203,38 +227,105 @@ int ensure_cub(prism_tree *t, size_t bytes) {
   return PRISM_OK;
 }
 
-// sort n Key3/uint64 pairs from (t->ck, t->cv) into (kout, vout)
-int sort_pairs(prism_tree *t, int64_t n, Key3 *kout, uint64_t *vout, int bits) {
+// sort n Key3/uint64 pairs (kin, vin) into (kout, vout) on the low `bits` bits
+int sort_pairs(prism_tree *t, int64_t n, const Key3 *kin, const uint64_t *vin, Key3 *kout, uint64_t *vout,
+               int bits) {
   if (n <= 0) return PRISM_OK;
   size_t bytes = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, t->ck, kout, t->cv, vout, (int)n, Key3Decomp{}, 0,
-                                     bits, t->st));
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int)n, Key3Decomp{}, 0, bits, t->st));
   int rc = ensure_cub(t, bytes);
   if (rc) return rc;
   bytes = t->cub_bytes;
-  CK(cub::DeviceRadixSort::SortPairs(t->cub_tmp, bytes, t->ck, kout, t->cv, vout, (int)n, Key3Decomp{}, 0,
-                                     bits, t->st));
+  CK(cub::DeviceRadixSort::SortPairs(t->cub_tmp, bytes, kin, kout, vin, vout, (int)n, Key3Decomp{}, 0, bits,
+                                     t->st));
+  t->lib_calls++;
+  return PRISM_OK;
+}
+
+// Sort n (Key3, value) pairs into (kout, vout): when the bits that vary across
+// the set fit 64, sort the order-preserving 64-bit compression of the keys
+// and gather; else sort the 192-bit keys directly.  (kin/vin != kout/vout.)
+int sort_compact(prism_tree *t, int64_t n, const Key3 *kin, const uint64_t *vin, Key3 *kout, uint64_t *vout,
+                 int bits) {
+  if (n <= 1) {
+    if (n == 1) {
+      CK(cudaMemcpyAsync(kout, kin, sizeof(Key3), cudaMemcpyDeviceToDevice, t->st));
+      CK(cudaMemcpyAsync(vout, vin, sizeof(uint64_t), cudaMemcpyDeviceToDevice, t->st));
+    }
+    return PRISM_OK;
+  }
+  if (n <= BSORT_MAX) {  // one CTA: bitonic sort in shared memory
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(k_block_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BSORT_SMEM));
+      attr = true;
+    }
+    k_block_sort<<<1, 1024, BSORT_SMEM, t->st>>>(kin, vin, (int)n, kout, vout);
+    CK(cudaGetLastError());
+    t->launches[PH_BUILD] += 1;
+    return PRISM_OK;
+  }
+  unsigned long long *dmask = (unsigned long long *)t->d_count + 4;  // d_count has 8 slots
+  CK(cudaMemsetAsync(dmask, 0, 3 * sizeof(unsigned long long), t->st));
+  const unsigned nb = std::min<unsigned>(blocks_for(n, SEL_TPB), 592u);
+  k_key_mask<<<nb, SEL_TPB, 0, t->st>>>(kin, n, dmask);
+  Key3 mask;
+  CK(cudaMemcpyAsync(&mask, dmask, sizeof(Key3), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  const int vb = __builtin_popcountll(mask.w0) + __builtin_popcountll(mask.w1) + __builtin_popcountll(mask.w2);
+  t->launches[PH_BUILD] += 1;
+  if (vb > 64) return sort_pairs(t, n, kin, vin, kout, vout, bits);
+  uint64_t *ck64 = t->cv2, *idx = (uint64_t *)t->cw2;
+  uint64_t *sk64 = (uint64_t *)t->ck2, *sidx = (uint64_t *)t->ck2 + t->d.S;  // ck2 holds 3*S words
+  k_key_compress<<<blocks_for(n), TPB, 0, t->st>>>(kin, n, mask, ck64, idx);
+  size_t bytes = 0;
+  const int eb = std::max(vb, 1);
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, ck64, sk64, idx, sidx, (int)n, 0, eb, t->st));
+  int rc = ensure_cub(t, bytes);
+  if (rc) return rc;
+  bytes = t->cub_bytes;
+  CK(cub::DeviceRadixSort::SortPairs(t->cub_tmp, bytes, ck64, sk64, idx, sidx, (int)n, 0, eb, t->st));
+  k_key_gather<<<blocks_for(n), TPB, 0, t->st>>>(kin, vin, sidx, n, kout, vout);
+  CK(cudaGetLastError());
+  t->lib_calls++;
+  t->launches[PH_BUILD] += 2;
+  return PRISM_OK;
+}
+
+// select_prefix (select.cuh): from the n candidates in (ck, cv, cw), the
+// smallest keys whose weights sum to >= W, into (ks, vs); returns the count
+int select_prefix(prism_tree *t, int64_t n, int64_t W, int64_t *nsel) {
+  const SelBufs b{t->ck, t->ck2, t->ks, t->cv, t->cv2, t->vs, t->cw, t->cw2, t->sel, t->bmin, t->bmax};
+  CK(sel_run(b, n, W, t->st, nsel, &t->launches[PH_BUILD]));
   return PRISM_OK;
 }
 
 // ------------------------------------------------------------ eviction order
-int build_list(prism_tree *t) {
+// Build the eviction order of the current tree, but only the prefix whose
+// tokens reach W (W <= 0: the whole order).
+int build_list(prism_tree *t, int64_t W) {
   const int32_t hw = t->hctrl->hw;
   prof_begin(t);
-  CK(cudaMemsetAsync(t->d_count, 0, sizeof(int64_t), t->st));
+  CK(cudaMemsetAsync(t->d_count, 0, 2 * sizeof(int64_t), t->st));
   k_build_keys<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw);
   k_propagate<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw);
-  k_gather<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw, t->ck, t->cv, t->d_count);
+  k_gather<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw, t->ck, t->cv, t->cw, t->d_count);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(t->h_small, t->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
   CK(cudaStreamSynchronize(t->st));
   const int64_t m = t->h_small[0];
-  int rc = sort_pairs(t, m, t->d.Lk, t->d.Lv, evict_key_bits(t->d.policy));
+  int64_t nsel = m;
+  int rc;
+  if (W > 0 && m > 2 * SEL_SMALL) {
+    if ((rc = select_prefix(t, m, W, &nsel))) return rc;
+    rc = sort_compact(t, nsel, t->ks, t->vs, t->d.Lk, t->d.Lv, evict_key_bits(t->d.policy));
+  } else {
+    rc = sort_compact(t, m, t->ck, t->cv, t->d.Lk, t->d.Lv, evict_key_bits(t->d.policy));
+  }
   if (rc) return rc;
-  k_list_ready<<<1, 1, 0, t->st>>>(t->d, t->d_count);
+  k_list_ready<<<1, 1, 0, t->st>>>(t->d, nsel, m);
   CK(cudaGetLastError());
   t->launches[PH_BUILD] += 4;
-  t->lib_calls += 1;
   prof_end(t, PH_BUILD);
   return PRISM_OK;
 }
@@ -319,7 +410,9 @@ int run_commit(prism_tree *t, CommitArgs a) {
         return PRISM_OK;
       case ST_NEED_BUILD:
       case ST_NEED_REBUILD:
-        rc = build_list(t);
+        // a prefix of the eviction order with 4x the tokens the stopped call
+        // still needs; a call that exhausts it resumes after a rebuild
+        rc = build_list(t, std::max<int64_t>(4 * c.need_hint, 1 << 18));
         break;
       case ST_NEED_SLOTS:
         rc = grow_slots(t, (int64_t)c.hw + 2 + MAX_ANCH);
@@ -461,25 +554,34 @@ int admit_wave_par(prism_tree *t, const WaveIn &W, int64_t levels, int64_t *hits
   const int64_t R0 = C.resident, D = R0 + nmiss - t->d.capacity;
   int64_t nv = 0, freed = 0, calls = 0;
   if (D > 0) {
-    if ((rc = build_list(t))) return rc;
-    if ((rc = pull_ctrl(t))) return rc;
-    const int64_t Tn = C.L_n;
-    if (Tn == 0) {
-      t->last_fallback = WPF_CAPACITY;
-      return PRISM_OK;
-    }
-    if ((rc = wx_ensure(t, B, levels, Tn))) return rc;
-    k_wp_vlen<<<blocks_for(Tn), TPB, 0, st>>>(t->d, 0, Tn, X, epoch);
-    if ((rc = cub_scan(t, X.vlen, X.F, Tn, true))) return rc;
-    k_wp_cuts<<<blocks_for(B), TPB, 0, st>>>(B, X.dem, R0, t->d.capacity, X.F, Tn, X.cut, X.flags);
-    CK(cudaGetLastError());
-    t->launches[PH_COMMIT] += 2;
     std::vector<int64_t> cut((size_t)B);
     int64_t poison = 0;
-    CK(cudaMemcpyAsync(cut.data(), X.cut, sizeof(int64_t) * B, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&flags, X.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&poison, X.misc + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    for (int attempt = 0; attempt < 2; attempt++) {
+      // the victims are a prefix of the eviction order: select just enough of
+      // it (D tokens plus slack); the complete order if that falls short
+      if ((rc = build_list(t, attempt == 0 ? D + D / 4 + 4096 : 0))) return rc;
+      if ((rc = pull_ctrl(t))) return rc;
+      const int64_t Tn = C.L_n;
+      if (Tn == 0) {
+        t->last_fallback = WPF_CAPACITY;
+        return PRISM_OK;
+      }
+      if ((rc = wx_ensure(t, B, levels, Tn))) return rc;
+      prof_begin(t);
+      CK(cudaMemsetAsync(X.flags, 0, sizeof(int32_t), st));
+      CK(cudaMemcpyAsync(X.misc + 1, &big, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+      k_wp_vlen<<<blocks_for(Tn), TPB, 0, st>>>(t->d, 0, Tn, X, epoch);
+      if ((rc = cub_scan(t, X.vlen, X.F, Tn, true))) return rc;
+      k_wp_cuts<<<blocks_for(B), TPB, 0, st>>>(B, X.dem, R0, t->d.capacity, X.F, Tn, X.cut, X.flags);
+      CK(cudaGetLastError());
+      t->launches[PH_COMMIT] += 2;
+      CK(cudaMemcpyAsync(cut.data(), X.cut, sizeof(int64_t) * B, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&flags, X.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&poison, X.misc + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      prof_end(t, PH_COMMIT);
+      if (!(flags & WPF_CAPACITY) || !C.L_partial) break;
+    }
     nv = cut[B - 1];
     if (flags || poison < nv) {
       t->last_fallback = flags ? flags : WPF_VICTIM;
@@ -660,7 +762,7 @@ prism_tree *prism_tree_create(int64_t capacity_tokens, int32_t policy, int64_t p
   if (cudaMallocHost((void **)&t->hctrl, sizeof(Ctrl)) != cudaSuccess) return bad("pinned");
   if (cudaMallocHost((void **)&t->h_small, 64 * sizeof(int64_t)) != cudaSuccess) return bad("pinned");
   if (cudaMallocHost((void **)&t->h_res, sizeof(OpRes)) != cudaSuccess) return bad("pinned");
-  if (dalloc(&t->d_res, 1) != cudaSuccess || dalloc(&t->d_count, 4) != cudaSuccess) return bad("res");
+  if (dalloc(&t->d_res, 1) != cudaSuccess || dalloc(&t->d_count, 8) != cudaSuccess) return bad("res");
   // root (kvcache.py:123-124): id 0, SYSTEM, empty edge
   memset(t->hctrl, 0, sizeof(Ctrl));
   t->hctrl->hw = 1;
@@ -687,9 +789,17 @@ void prism_tree_destroy(prism_tree *t) {
                   t->d_path,   t->d_aoff,    t->d_akind,   t->d_aseg,   t->d_asnap,   t->d_res,
                   t->d_vis_slots, t->d_vis_ids, t->d_poff, t->d_aoffs,  t->d_wtok,    t->d_waoff,
                   t->d_waseg,  t->d_wasnap,  t->d_wakind,  t->d_hits,   t->d_lids,    t->d_lslots,
-                  t->d_pm_meta, t->d_pm_chain, t->d_prot_ids};
+                  t->d_pm_meta, t->d_pm_chain, t->d_prot_ids, t->ck2, t->cv2, t->cw, t->cw2, t->ks,
+                  t->vs,       t->sel,       t->bmin,      t->bmax};
   for (void *p : bufs)
     if (p) cudaFree(p);
+  const WaveTmp &X = t->wx;
+  void *wbufs[] = {X.hit, X.pre, X.npieces, X.p0, X.lcp_level, X.cnew, X.tail, X.miss, X.idb, X.arb, X.dem,
+                   X.piece_slot, X.owner, X.lt_key, X.lt_min, X.flags, X.vlen, X.F, X.cut, X.misc};
+  for (void *p : wbufs)
+    if (p) cudaFree(p);
+  if (t->ev0) cudaEventDestroy(t->ev0);
+  if (t->ev1) cudaEventDestroy(t->ev1);
   cudaFreeHost(t->hctrl);
   cudaFreeHost(t->h_small);
   cudaFreeHost(t->h_res);
@@ -815,7 +925,7 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out) {
   t->launches[PH_PROTECT] += 3;
   t->lib_calls += 1;
   CK(cudaMemsetAsync(t->d_count, 0, sizeof(int64_t), t->st));
-  k_prot_gather<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw, t->ck, t->cv, t->d_count);
+  k_prot_gather<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw, t->ck, t->cv, t->cw, t->d_count);
   k_prot_clear<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(t->h_small, t->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
@@ -823,7 +933,15 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out) {
   const int64_t m = t->h_small[0];
   const int64_t f = std::min<int64_t>(t->protect_budget, m);
   if (f > 0) {
-    rc = sort_pairs(t, m, t->d.Lk, t->d.Lv, 64 + 32 + 40);  // Lk/Lv as scratch: no list survives a call
+    // top-f: select the f smallest keys, sort only those (Lk/Lv as scratch:
+    // no eviction list survives across calls)
+    int64_t nsel = m;
+    if (m > 2 * SEL_SMALL) {
+      if ((rc = select_prefix(t, m, f, &nsel))) return rc;
+      rc = sort_compact(t, nsel, t->ks, t->vs, t->d.Lk, t->d.Lv, 64 + 32 + 40);
+    } else {
+      rc = sort_compact(t, m, t->ck, t->cv, t->d.Lk, t->d.Lv, 64 + 32 + 40);
+    }
     if (rc) return rc;
     rc = ensure_buf(&t->d_prot_ids, t->prot_cap, f);
     if (rc) return rc;

@@ -453,6 +453,8 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
     C.L_cur = 0;
     C.H_n = 0;
     C.n_admitted = 0;
+    C.resume = 0;
+    C.resume_freed = 0;
   }
   C.status = ST_DONE;
   int32_t chain_member = -1;  // member whose match chain sits in Ps
@@ -517,12 +519,26 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
     if (type == OP_EVICT) {  // evict(k) (kvcache.py:425-460)
       r.evicted = 1;
       if (A.op_k > 0) {
+        const int64_t need = A.op_k - C.resume_freed;
         if (!C.L_valid) {
+          C.need_hint = need;
           C.status = ST_NEED_BUILD;
           break;
         }
         C.gstamp++;
-        r.freed = evict_loop(T, C, A.op_k);
+        if (C.resume) r.vbeg = C.resume_vbeg;
+        const int64_t got = evict_loop(T, C, need);
+        if (got < need && C.L_partial) {  // list prefix exhausted: rebuild, continue
+          C.resume = 1;
+          C.resume_freed += got;
+          C.resume_vbeg = r.vbeg;
+          C.need_hint = need - got;
+          C.status = ST_NEED_REBUILD;
+          break;
+        }
+        r.freed = got + C.resume_freed;
+        C.resume = 0;
+        C.resume_freed = 0;
       }
       C.evict_calls++;
       r.vend = C.vlog_count;
@@ -617,11 +633,10 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
 
     // ---- insert_path (kvcache.py:190-241)
     const int64_t hit = c_hit;
-    C.chain_nodes += c_d;
-    C.inserted_tokens += n;
     const int64_t shortfall = C.resident + (n - hit) - T.capacity;  // _reserve (243-273)
     if (shortfall > 0) {
       if (!C.L_valid) {
+        C.need_hint = shortfall;
         C.status = ST_NEED_BUILD;
         break;
       }
@@ -629,10 +644,24 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
       for (int32_t i = lane; i < c_d; i += 32) T.guard[Ps[i]] = C.gstamp;
       __syncwarp();
       r.evicted = 1;
-      r.freed = evict_loop(T, C, shortfall);
+      if (C.resume) r.vbeg = C.resume_vbeg;
+      const int64_t got = evict_loop(T, C, shortfall);
+      if (got < shortfall && C.L_partial) {
+        // the selected prefix of the eviction order ran out: rebuild the list
+        // from the current tree and continue this same evict call
+        C.resume = 1;
+        C.resume_freed += got;
+        C.resume_vbeg = r.vbeg;
+        C.need_hint = shortfall - got;
+        C.status = ST_NEED_REBUILD;
+        break;
+      }
+      r.freed = got + C.resume_freed;
+      C.resume = 0;
+      C.resume_freed = 0;
       C.evict_calls++;
       r.vend = C.vlog_count;
-      if (r.freed < shortfall) {
+      if (got < shortfall) {
         r.status = ST_CAPACITY;
         if (lane == 0 && A.res) A.res[o] = r;
         C.status = ST_CAPACITY;
@@ -640,6 +669,8 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
         break;
       }
     }
+    C.chain_nodes += c_d;
+    C.inserted_tokens += n;
     C.clock++;
     const int64_t now = C.clock;
     int32_t np = c_d;
@@ -823,7 +854,7 @@ __global__ void k_propagate(DT T, int32_t hw) {
 }
 
 __global__ void k_gather(DT T, int32_t hw, Key3 *__restrict__ ck, uint64_t *__restrict__ cv,
-                         int64_t *__restrict__ count) {
+                         int64_t *__restrict__ cw, int64_t *__restrict__ count) {
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   bool take = false;
   int32_t e = EFF_DEAD;
@@ -842,12 +873,15 @@ __global__ void k_gather(DT T, int32_t hw, Key3 *__restrict__ ck, uint64_t *__re
     const int64_t pos = base + __popc(m & ((1u << lane) - 1));
     ck[pos] = composite(T.kw[e], T.dend[s]);
     cv[pos] = ((uint64_t)T.kver[s] << 32) | (uint32_t)s;
+    cw[pos] = T.elen[s];
   }
 }
 
-__global__ void k_list_ready(DT T, const int64_t *count) {
+// the sorted list is ready: n entries out of `total` candidates
+__global__ void k_list_ready(DT T, int64_t n, int64_t total) {
   Ctrl *c = T.ctrl;
-  c->L_n = *count;
+  c->L_n = n;
+  c->L_partial = n < total ? 1 : 0;
   c->L_cur = 0;
   c->L_valid = 1;
   c->H_n = 0;
@@ -858,7 +892,7 @@ __global__ void k_list_ready(DT T, const int64_t *count) {
 
 // set_protection sort key (kvcache.py:375-381): (-P-hat, segment or -1, node_id)
 __global__ void k_prot_gather(DT T, int32_t hw, Key3 *__restrict__ ck, uint64_t *__restrict__ cv,
-                              int64_t *__restrict__ count) {
+                              int64_t *__restrict__ cw, int64_t *__restrict__ count) {
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   bool take = false;
   if (s < hw && s != ROOT) take = T.nid[s] >= 0 && T.par[s] >= 0 && T.hasanc[s] && T.akind[s] == K_REUSABLE;
@@ -879,6 +913,7 @@ __global__ void k_prot_gather(DT T, int32_t hw, Key3 *__restrict__ ck, uint64_t 
     shl_or(k, 40, (uint64_t)T.nid[s] & ((1ull << 40) - 1));
     ck[pos] = k;
     cv[pos] = (uint64_t)(uint32_t)s;
+    cw[pos] = 1;
   }
 }
 

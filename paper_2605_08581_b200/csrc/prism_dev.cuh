@@ -77,6 +77,9 @@ struct Ctrl {
   int64_t vlog_count, evict_calls, builds;
   int64_t fast_members, slow_members;
   int64_t chain_nodes, inserted_tokens;  // algorithmic-byte accounting
+  int64_t need_hint;                     // tokens the stopped evict call still needs
+  int64_t resume_freed, resume_vbeg;     // an evict call split by a list rebuild
+  int32_t resume, L_partial;             // resume pending; L is a strict prefix of the order
   int64_t L_n, L_cur;
   int32_t hw, free_top;
   int32_t status, op_cursor;

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/prism.h"
+#include "select.cuh"
 
 namespace {
 
@@ -373,7 +374,8 @@ __global__ void q_hot(int64_t P, const int32_t *__restrict__ bucket, const int32
 
 // cold-lane key: (selected, arrival, id) -- leftovers sorted by (arrival, id)
 __global__ void q_cold_keys(int64_t P, const uint8_t *__restrict__ sel, const double *__restrict__ arrival,
-                            const int64_t *__restrict__ ids, K3 *__restrict__ k, int64_t *__restrict__ v) {
+                            const int64_t *__restrict__ ids, K3 *__restrict__ k, int64_t *__restrict__ v,
+                            int64_t *__restrict__ w) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   K3 x;
@@ -382,6 +384,7 @@ __global__ void q_cold_keys(int64_t P, const uint8_t *__restrict__ sel, const do
   x.w2 = (uint64_t)ids[i] ^ 0x8000000000000000ull;
   k[i] = x;
   v[i] = i;
+  w[i] = sel[i] ? 0 : 1;  // only leftovers count toward the cold quota
 }
 
 __global__ void q_prio(int32_t nseg, const int32_t *__restrict__ g, const int32_t *__restrict__ a,
@@ -487,6 +490,16 @@ struct prism_qas {
   QBUF(int8_t, a_kind)
   QBUF(int32_t, a_seg)
   QBUF(int32_t, a_snap)
+  // cold-lane selection
+  QBUF(int64_t, cw0)
+  QBUF(int64_t, cw1)
+  QBUF(prism::Key3, ck1)
+  QBUF(uint64_t, cv1)
+  QBUF(prism::Key3, cks)
+  QBUF(uint64_t, cvs)
+  QBUF(prism::SelState, sst)
+  QBUF(prism::Key3, sbmin)
+  QBUF(prism::Key3, sbmax)
 #undef QBUF
   int64_t launches = 0, lib_calls = 0, rounds = 0;
   int32_t commit_mode = 0;
@@ -686,14 +699,41 @@ int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, con
   QCK(grow(&q->ck2, q->ck2_cap, P1));
   QCK(grow(&q->cv2, q->cv2_cap, P1));
   if (nc > 0) {
-    q_cold_keys<<<nblk(P), TPB, 0, st>>>(P, q->sel, in.arrival, in.ids, q->ck, q->cv);
-    bytes = 0;
-    QCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, q->ck, q->ck2, q->cv, q->cv2, (int)P, K3Decomp{}, 0,
-                                        1 + 128, st));
-    if (ensure_tmp(q, bytes)) return PRISM_CUDA;
-    bytes = q->tmp_bytes;
-    QCK(cub::DeviceRadixSort::SortPairs(q->tmp, bytes, q->ck, q->ck2, q->cv, q->cv2, (int)P, K3Decomp{}, 0,
-                                        1 + 128, st));
+    // the q_cold smallest (arrival, id) among the leftovers: mass-weighted
+    // selection (weight 1 per leftover) then a sort of the selected few
+    QCK(grow(&q->cw0, q->cw0_cap, P1));
+    QCK(grow(&q->cw1, q->cw1_cap, P1));
+    QCK(grow(&q->ck1, q->ck1_cap, P1));
+    QCK(grow(&q->cv1, q->cv1_cap, P1));
+    QCK(grow(&q->cks, q->cks_cap, P1));
+    QCK(grow(&q->cvs, q->cvs_cap, P1));
+    QCK(grow(&q->sst, q->sst_cap, 1));
+    QCK(grow(&q->sbmin, q->sbmin_cap, 1184));
+    QCK(grow(&q->sbmax, q->sbmax_cap, 1184));
+    q_cold_keys<<<nblk(P), TPB, 0, st>>>(P, q->sel, in.arrival, in.ids, q->ck, q->cv, q->cw0);
+    const prism::SelBufs sb{(prism::Key3 *)q->ck, q->ck1, q->cks, (uint64_t *)q->cv, q->cv1, q->cvs,
+                            q->cw0, q->cw1, q->sst, q->sbmin, q->sbmax};
+    int64_t nsel = 0;
+    QCK(prism::sel_run(sb, P, nc, st, &nsel, &q->launches));
+    if (nsel <= prism::BSORT_MAX) {
+      static bool attr = false;
+      if (!attr) {
+        QCK(cudaFuncSetAttribute(prism::k_block_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)prism::BSORT_SMEM));
+        attr = true;
+      }
+      prism::k_block_sort<<<1, 1024, prism::BSORT_SMEM, st>>>(q->cks, q->cvs, (int)nsel, (prism::Key3 *)q->ck2,
+                                                              (uint64_t *)q->cv2);
+      q->launches++;
+    } else {
+      bytes = 0;
+      QCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, (K3 *)q->cks, q->ck2, (int64_t *)q->cvs, q->cv2,
+                                          (int)nsel, K3Decomp{}, 0, 1 + 128, st));
+      if (ensure_tmp(q, bytes)) return PRISM_CUDA;
+      bytes = q->tmp_bytes;
+      QCK(cub::DeviceRadixSort::SortPairs(q->tmp, bytes, (K3 *)q->cks, q->ck2, (int64_t *)q->cvs, q->cv2,
+                                          (int)nsel, K3Decomp{}, 0, 1 + 128, st));
+    }
     // n_disp over hot + cold (scheduler.py:247-248)
     q_count<<<nblk(nc), TPB, 0, st>>>(nc, in.off, in.sk, q->nd, q->cv2);
   }
