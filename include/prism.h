@@ -151,6 +151,11 @@ int prism_evict_key(prism_tree *t, int32_t slot, uint64_t *key3);
 int prism_last_op(prism_tree *t, int64_t *out);
 /* Number of token-arena compactions so far. */
 int64_t prism_compactions(prism_tree *t);
+/* Sizing of the selected eviction-order prefix: key 0 = minimum tokens for
+ * the ordered commit (default 2^18), 1 = slack tokens for the parallel
+ * commit (4096), 2 = candidate count below which all are sorted (4096).
+ * Semantics do not depend on them (exhausted prefixes are rebuilt). */
+int prism_tune(prism_tree *t, int32_t key, int64_t value);
 /* Live device-time profile: with enable != 0 every phase is bracketed by
  * CUDA events on the tree's stream.  prism_profile_read fills out[27]:
  * device ms per phase [0..8) (commit, list build, protection, pre-match,

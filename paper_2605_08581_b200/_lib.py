@@ -38,6 +38,7 @@ _SIGS = {
     "prism_evict_key": (C.c_int, [_p, _i32, _p]),
     "prism_last_op": (C.c_int, [_p, _p]),
     "prism_compactions": (_i64, [_p]),
+    "prism_tune": (C.c_int, [_p, _i32, _i64]),
     "prism_qas_create": (_p, [_i32]),
     "prism_qas_destroy": (None, [_p]),
     "prism_qas_round": (C.c_int, [_p, _i64, _p, _p, _p, _p, _p, _i64, _p, _p, _i32, _p] + [_p] * 16),

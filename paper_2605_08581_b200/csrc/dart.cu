@@ -114,6 +114,10 @@ struct prism_tree {
   int64_t wx_cap = 0, wx_lt = 0, wx_T = 0;
   int64_t par_waves = 0, seq_waves = 0;
   int32_t last_fallback = 0;
+  // tunables (prism_tune): eviction-list prefix sizing
+  int64_t list_min_tokens = 1 << 18;   // ordered commit: select >= this many tokens
+  int64_t list_slack_tokens = 4096;    // parallel commit: demand + 25% + this
+  int64_t sel_min_candidates = 4096;   // below this many candidates, sort them all
 };
 
 enum { PH_COMMIT = 0, PH_BUILD = 1, PH_PROTECT = 2, PH_PREMATCH = 3, PH_RELEASE = 4, PH_NOTE = 5, PH_MAINT = 6 };
@@ -296,7 +300,7 @@ int sort_compact(prism_tree *t, int64_t n, const Key3 *kin, const uint64_t *vin,
 // smallest keys whose weights sum to >= W, into (ks, vs); returns the count
 int select_prefix(prism_tree *t, int64_t n, int64_t W, int64_t *nsel) {
   const SelBufs b{t->ck, t->ck2, t->ks, t->cv, t->cv2, t->vs, t->cw, t->cw2, t->sel, t->bmin, t->bmax};
-  CK(sel_run(b, n, W, t->st, nsel, &t->launches[PH_BUILD]));
+  CK(sel_run(b, n, W, t->st, nsel, &t->launches[PH_BUILD], std::min<int64_t>(SEL_SMALL, t->sel_min_candidates)));
   return PRISM_OK;
 }
 
@@ -316,7 +320,7 @@ int build_list(prism_tree *t, int64_t W) {
   const int64_t m = t->h_small[0];
   int64_t nsel = m;
   int rc;
-  if (W > 0 && m > 2 * SEL_SMALL) {
+  if (W > 0 && m > t->sel_min_candidates) {
     if ((rc = select_prefix(t, m, W, &nsel))) return rc;
     rc = sort_compact(t, nsel, t->ks, t->vs, t->d.Lk, t->d.Lv, evict_key_bits(t->d.policy));
   } else {
@@ -412,7 +416,7 @@ int run_commit(prism_tree *t, CommitArgs a) {
       case ST_NEED_REBUILD:
         // a prefix of the eviction order with 4x the tokens the stopped call
         // still needs; a call that exhausts it resumes after a rebuild
-        rc = build_list(t, std::max<int64_t>(4 * c.need_hint, 1 << 18));
+        rc = build_list(t, std::max<int64_t>(4 * c.need_hint, t->list_min_tokens));
         break;
       case ST_NEED_SLOTS:
         rc = grow_slots(t, (int64_t)c.hw + 2 + MAX_ANCH);
@@ -559,7 +563,7 @@ int admit_wave_par(prism_tree *t, const WaveIn &W, int64_t levels, int64_t *hits
     for (int attempt = 0; attempt < 2; attempt++) {
       // the victims are a prefix of the eviction order: select just enough of
       // it (D tokens plus slack); the complete order if that falls short
-      if ((rc = build_list(t, attempt == 0 ? D + D / 4 + 4096 : 0))) return rc;
+      if ((rc = build_list(t, attempt == 0 ? D + D / 4 + t->list_slack_tokens : 0))) return rc;
       if ((rc = pull_ctrl(t))) return rc;
       const int64_t Tn = C.L_n;
       if (Tn == 0) {
@@ -936,7 +940,7 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out) {
     // top-f: select the f smallest keys, sort only those (Lk/Lv as scratch:
     // no eviction list survives across calls)
     int64_t nsel = m;
-    if (m > 2 * SEL_SMALL) {
+    if (m > t->sel_min_candidates) {
       if ((rc = select_prefix(t, m, f, &nsel))) return rc;
       rc = sort_compact(t, nsel, t->ks, t->vs, t->d.Lk, t->d.Lv, 64 + 32 + 40);
     } else {
@@ -1333,6 +1337,18 @@ int prism_evict_key(prism_tree *t, int32_t slot, uint64_t *key3) {
 }
 
 int64_t prism_compactions(prism_tree *t) { return t->compactions; }
+
+// 0: list_min_tokens, 1: list_slack_tokens, 2: sel_min_candidates (tests use
+// tiny values to force partial eviction lists and their rebuild/resume path)
+int prism_tune(prism_tree *t, int32_t key, int64_t value) {
+  switch (key) {
+    case 0: t->list_min_tokens = std::max<int64_t>(value, 1); break;
+    case 1: t->list_slack_tokens = std::max<int64_t>(value, 0); break;
+    case 2: t->sel_min_candidates = std::max<int64_t>(value, 0); break;
+    default: return fail(PRISM_INVALID, "unknown tunable");
+  }
+  return PRISM_OK;
+}
 
 int prism_profile(prism_tree *t, int32_t enable) {
   cudaSetDevice(t->dev);

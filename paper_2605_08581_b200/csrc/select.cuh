@@ -36,6 +36,7 @@ struct SelState {
   int32_t take_all;  // take the whole crossing bucket this round
   int32_t cur;       // which U buffer is current (0/1)
   int32_t rounds;
+  int64_t small;     // a crossing bucket with at most this many keys is taken whole
   unsigned long long hist_n[256];
   long long hist_w[256];
 };
@@ -188,7 +189,7 @@ static __global__ void k_sel_pick(SelState *st) {
     const long long below = before + (q ? w8[q - 1] : 0);
     st->need -= below;
     st->dstar = d;
-    if ((int64_t)st->hist_n[d] <= SEL_SMALL) st->take_all = 1;
+    if ((int64_t)st->hist_n[d] <= st->small) st->take_all = 1;
   }
 }
 
@@ -385,8 +386,9 @@ struct SelBufs {
 // (ks, vs); *nsel receives its size (synchronizes the stream once at the end,
 // and at most three times before to stop launching finished rounds).
 inline cudaError_t sel_run(const SelBufs &b, int64_t n, int64_t W, cudaStream_t stream, int64_t *nsel,
-                           int64_t *launches) {
+                           int64_t *launches, int64_t small = SEL_SMALL) {
   SelState h{};
+  h.small = small;
   h.need = W > 0 ? W : 1;
   h.nU = n;
   h.done = n == 0;

@@ -212,6 +212,13 @@ class DeviceRadixCache:
             self._last = (int(self._op[1]), int(self._op[2]))
         self._dirty()
 
+    TUNABLES = {"list_min_tokens": 0, "list_slack_tokens": 1, "sel_min_candidates": 2}
+
+    def tune(self, **kw) -> None:
+        """Eviction-list prefix sizing (semantics-free; tests force tiny prefixes)."""
+        for k, v in kw.items():
+            check(self._L.prism_tune(self._h, self.TUNABLES[k], int(v)))
+
     def stats(self) -> dict:
         out = np.zeros(16, dtype=np.int64)
         check(self._L.prism_stats(self._h, _ptr(out)))

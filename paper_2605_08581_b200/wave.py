@@ -154,6 +154,13 @@ class WaveEngine:
         check(self.L.prism_wave_stats(self.t, out.ctypes.data))
         return {"parallel_waves": int(out[0]), "ordered_waves": int(out[1]), "last_fallback": int(out[2])}
 
+    def tune(self, **kw) -> None:
+        """Eviction-list prefix sizing (see DeviceRadixCache.tune)."""
+        from .dart import DeviceRadixCache
+
+        for k, v in kw.items():
+            check(self.L.prism_tune(self.t, DeviceRadixCache.TUNABLES[k], int(v)))
+
     def cache_view(self):
         """The reference RadixCache API over this engine's tree (tests/debug)."""
         from .dart import DeviceRadixCache

@@ -54,7 +54,7 @@ def _pending_arrays(reqs):
 
 
 def run_case(seed, policy, mode, nseg=40, hot=6, kmin=2, kmax=5, suffixes=(2, 4), sys=8, chunk=4, cap=600,
-             wave=24, nwaves=8, protect=3, cold=2):
+             wave=24, nwaves=8, protect=3, cold=2, tiny=False):
     import torch
 
     from paper_2605_08581_b200.wave import DevicePending, WaveEngine
@@ -64,6 +64,8 @@ def run_case(seed, policy, mode, nseg=40, hot=6, kmin=2, kmax=5, suffixes=(2, 4)
     scfg = SchedulerConfig(dispatch_budget=wave, cold_quota=cold)
     eng = WaveEngine(cfg, scfg, nseg, sys, chunk, device=0)
     eng.set_commit_mode(mode)
+    if tiny:  # minimal selected prefixes of the eviction order
+        eng.tune(list_min_tokens=1, list_slack_tokens=0, sel_min_candidates=0)
     ora = OracleRadixCache(cfg)
     cat = SegmentCatalog(num_segments=nseg, chunk_tokens=chunk, hot_set=tuple(range(min(hot, nseg))),
                          sys_prefix_tokens=sys)
@@ -132,6 +134,8 @@ def test_ordered_commit_matches_oracle(policy):
     dict(nseg=8, hot=4, kmin=3, kmax=6, wave=48),      # heavy intra-wave sharing
     dict(chunk=1, sys=3, kmax=8, suffixes=(1, 2)),     # one-token segments
     dict(cap=100_000, nwaves=4),                       # no eviction at all
+    dict(tiny=True),                                   # minimal eviction-order prefixes
+    dict(tiny=True, cap=150, wave=32, nwaves=10),      # ... with capacity stops
 ])
 def test_parallel_commit_variants(variant):
     run_case(5, CachePolicy.DART, mode=0, **variant)
