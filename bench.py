@@ -469,6 +469,7 @@ def run_ours(args) -> None:
                 "fast_path_members": st2["fast_members"] - st1["fast_members"],
                 "slow_path_members": st2["slow_members"] - st1["slow_members"],
                 "commit": engine.wave_stats(),
+                "last_list_build": engine.build_timeline(),
             },
             "roofline": roofline,
             "cpu_baseline": cpu,

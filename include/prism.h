@@ -156,6 +156,9 @@ int64_t prism_compactions(prism_tree *t);
  * commit (4096), 2 = candidate count below which all are sorted (4096).
  * Semantics do not depend on them (exhausted prefixes are rebuilt). */
 int prism_tune(prism_tree *t, int32_t key, int64_t value);
+/* Phase timeline of the last cooperative eviction-list build (diagnostics):
+ * out[0..*n) %globaltimer ns stamps, out[39] = selected-prefix size. */
+int prism_coop_timeline(prism_tree *t, uint64_t *out, int32_t *n);
 /* Live device-time profile: with enable != 0 every phase is bracketed by
  * CUDA events on the tree's stream.  prism_profile_read fills out[27]:
  * device ms per phase [0..8) (commit, list build, protection, pre-match,

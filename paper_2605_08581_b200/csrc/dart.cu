@@ -19,6 +19,7 @@
 #include "dart_kernels.cuh"
 #include "select.cuh"
 #include "wave_par.cuh"
+#include "coop.cuh"
 
 using namespace prism;
 
@@ -70,6 +71,10 @@ struct prism_tree {
   int64_t *cw = nullptr, *cw2 = nullptr;
   SelState *sel = nullptr;
   Key3 *bmin = nullptr, *bmax = nullptr;
+  Key3 *kt = nullptr;  // cooperative sort scratch
+  uint64_t *vt = nullptr;
+  CoopState *cst = nullptr;
+  int coop_grid = 0;
   int64_t *d_count = nullptr;
   int64_t *h_small = nullptr;  // pinned scratch
   void *cub_tmp = nullptr;
@@ -118,6 +123,7 @@ struct prism_tree {
   int64_t list_min_tokens = 1 << 18;   // ordered commit: select >= this many tokens
   int64_t list_slack_tokens = 4096;    // parallel commit: demand + 25% + this
   int64_t sel_min_candidates = 4096;   // below this many candidates, sort them all
+  int64_t use_coop = 1;                // cooperative single-kernel build / protection
 };
 
 enum { PH_COMMIT = 0, PH_BUILD = 1, PH_PROTECT = 2, PH_PREMATCH = 3, PH_RELEASE = 4, PH_NOTE = 5, PH_MAINT = 6 };
@@ -162,9 +168,12 @@ std::vector<SlotField> slot_fields(prism_tree *t) {
 // candidate / selection scratch, sized with the slot capacity
 int alloc_scratch(prism_tree *t, int64_t S) {
   void **bufs[] = {(void **)&t->ck, (void **)&t->cv, (void **)&t->cw, (void **)&t->ck2, (void **)&t->cv2,
-                   (void **)&t->cw2, (void **)&t->ks, (void **)&t->vs};
+                   (void **)&t->cw2, (void **)&t->ks, (void **)&t->vs, (void **)&t->kt, (void **)&t->vt};
   for (void **b : bufs)
     if (*b) CK(cudaFree(*b));
+  CK(dalloc(&t->kt, S));
+  CK(dalloc(&t->vt, S));
+  if (!t->cst) CK(dalloc(&t->cst, 1));
   CK(dalloc(&t->ck, S));
   CK(dalloc(&t->cv, S));
   CK(dalloc(&t->cw, S));
@@ -304,10 +313,51 @@ int select_prefix(prism_tree *t, int64_t n, int64_t W, int64_t *nsel) {
   return PRISM_OK;
 }
 
+// ------------------------------------------------------------ cooperative kernels
+int coop_grid(prism_tree *t) {
+  if (t->coop_grid > 0) return t->coop_grid;
+  CK(cudaFuncSetAttribute(k_build_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)COOP_SMEM));
+  CK(cudaFuncSetAttribute(k_protect_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)COOP_SMEM));
+  int per_sm = 0, sms = 0, dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_build_coop, COOP_TPB, COOP_SMEM));
+  int per_sm2 = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_protect_coop, COOP_TPB, COOP_SMEM));
+  per_sm = std::min(per_sm, per_sm2);
+  if (per_sm < 1) return fail(PRISM_FATAL, "cooperative kernels do not fit one CTA per SM");
+  t->coop_grid = std::min(sms * per_sm, 2048);
+  return t->coop_grid;
+}
+
+CoopBufs coop_bufs(prism_tree *t) {
+  return CoopBufs{t->ck, t->ck2, t->ks, t->kt, t->cv, t->cv2, t->vs, t->vt, t->cw, t->cw2, t->bmin, t->bmax,
+                  t->cst, t->d_prot_ids};
+}
+
 // ------------------------------------------------------------ eviction order
 // Build the eviction order of the current tree, but only the prefix whose
 // tokens reach W (W <= 0: the whole order).
 int build_list(prism_tree *t, int64_t W) {
+  if (t->use_coop) {  // one cooperative kernel, no host round trip
+    int grid = coop_grid(t);
+    if (grid < 0) return PRISM_FATAL;
+    prof_begin(t);
+    CK(cudaMemsetAsync(t->cst, 0, offsetof(CoopState, ts), t->st));
+    // keys / subtree maxima / gather at full occupancy over the slot range
+    // (each reads hw from the control block; the count lands in cst->cand)
+    const int64_t S = t->d.S;
+    k_build_keys<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1);
+    k_propagate<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1);
+    k_gather<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1, t->ck, t->cv, t->cw, (int64_t *)&t->cst->cand);
+    CoopBufs B = coop_bufs(t);
+    int64_t minc = t->sel_min_candidates, small = std::min<int64_t>(SEL_SMALL, t->sel_min_candidates);
+    void *args[] = {(void *)&t->d, (void *)&B, (void *)&W, (void *)&minc, (void *)&small};
+    CK(cudaLaunchCooperativeKernel((void *)k_build_coop, grid, COOP_TPB, args, COOP_SMEM, t->st));
+    t->launches[PH_BUILD] += 4;
+    prof_end(t, PH_BUILD);
+    return PRISM_OK;
+  }
   const int32_t hw = t->hctrl->hw;
   prof_begin(t);
   CK(cudaMemsetAsync(t->d_count, 0, 2 * sizeof(int64_t), t->st));
@@ -922,7 +972,33 @@ int prism_evict(prism_tree *t, int64_t k_free, int64_t *freed) {
 
 // top-f reusable anchors by (-P-hat, segment, id) with the current t->d.pri
 static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out) {
-  int rc = pull_ctrl(t);
+  int rc;
+  if (t->use_coop) {  // one cooperative kernel; no host round trip unless ids are wanted
+    int grid = coop_grid(t);
+    if (grid < 0) return PRISM_FATAL;
+    const int64_t f = t->protect_budget;
+    if ((rc = ensure_buf(&t->d_prot_ids, t->prot_cap, std::max<int64_t>(f, 1)))) return rc;
+    prof_begin(t);
+    CK(cudaMemsetAsync(t->cst, 0, offsetof(CoopState, ts), t->st));
+    CoopBufs B = coop_bufs(t);
+    int64_t minc = t->sel_min_candidates, small = std::min<int64_t>(SEL_SMALL, t->sel_min_candidates);
+    int64_t ff = f;
+    void *args[] = {(void *)&t->d, (void *)&B, (void *)&ff, (void *)&minc, (void *)&small};
+    CK(cudaLaunchCooperativeKernel((void *)k_protect_coop, grid, COOP_TPB, args, COOP_SMEM, t->st));
+    t->launches[PH_PROTECT] += 1;
+    prof_end(t, PH_PROTECT);
+    if (out_ids || n_out) {
+      int64_t nf = 0;
+      CK(cudaMemcpyAsync(&nf, &t->cst->prot_n, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
+      CK(cudaStreamSynchronize(t->st));
+      if (out_ids && nf > 0)
+        CK(cudaMemcpyAsync(out_ids, t->d_prot_ids, sizeof(int64_t) * nf, cudaMemcpyDeviceToHost, t->st));
+      CK(cudaStreamSynchronize(t->st));
+      if (n_out) *n_out = nf;
+    }
+    return PRISM_OK;
+  }
+  rc = pull_ctrl(t);
   if (rc) return rc;
   const int32_t hw = t->hctrl->hw;
   prof_begin(t);
@@ -1338,6 +1414,17 @@ int prism_evict_key(prism_tree *t, int32_t slot, uint64_t *key3) {
 
 int64_t prism_compactions(prism_tree *t) { return t->compactions; }
 
+// phase timeline of the last cooperative list build: out[0..n) %globaltimer
+// ns stamps (start, after each selection round, after the chunk sort, after
+// each merge round, end); out[39] = selected-prefix size
+int prism_coop_timeline(prism_tree *t, uint64_t *out, int32_t *n) {
+  cudaSetDevice(t->dev);
+  CK(cudaMemcpyAsync(out, t->cst->ts_build, 40 * sizeof(uint64_t), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaMemcpyAsync(n, &t->cst->nts_build, sizeof(int32_t), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  return PRISM_OK;
+}
+
 // 0: list_min_tokens, 1: list_slack_tokens, 2: sel_min_candidates (tests use
 // tiny values to force partial eviction lists and their rebuild/resume path)
 int prism_tune(prism_tree *t, int32_t key, int64_t value) {
@@ -1345,6 +1432,7 @@ int prism_tune(prism_tree *t, int32_t key, int64_t value) {
     case 0: t->list_min_tokens = std::max<int64_t>(value, 1); break;
     case 1: t->list_slack_tokens = std::max<int64_t>(value, 0); break;
     case 2: t->sel_min_candidates = std::max<int64_t>(value, 0); break;
+    case 3: t->use_coop = value ? 1 : 0; break;
     default: return fail(PRISM_INVALID, "unknown tunable");
   }
   return PRISM_OK;

@@ -817,7 +817,9 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
 
 // ------------------------------------------------------------ eviction-order build
 
+// (hw < 0: read the high-water mark from the control block -- no host sync)
 __global__ void k_build_keys(DT T, int32_t hw) {
+  if (hw < 0) hw = T.ctrl->hw;
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= hw) return;
   if (s == ROOT || T.nid[s] < 0 || T.par[s] < 0) {
@@ -833,6 +835,7 @@ __global__ void k_build_keys(DT T, int32_t hw) {
 // the subtree can never be evicted): each node carries its own value upward
 // until an ancestor already holds something at least as large.
 __global__ void k_propagate(DT T, int32_t hw) {
+  if (hw < 0) hw = T.ctrl->hw;
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= hw || s == ROOT || T.nid[s] < 0 || T.par[s] < 0) return;
   const bool blocked = T.ref[s] > 0 || (T.policy == P_DART && T.kind[s] == K_SYSTEM);
@@ -855,6 +858,7 @@ __global__ void k_propagate(DT T, int32_t hw) {
 
 __global__ void k_gather(DT T, int32_t hw, Key3 *__restrict__ ck, uint64_t *__restrict__ cv,
                          int64_t *__restrict__ cw, int64_t *__restrict__ count) {
+  if (hw < 0) hw = T.ctrl->hw;
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   bool take = false;
   int32_t e = EFF_DEAD;

@@ -161,6 +161,15 @@ class WaveEngine:
         for k, v in kw.items():
             check(self.L.prism_tune(self.t, DeviceRadixCache.TUNABLES[k], int(v)))
 
+    def build_timeline(self) -> dict:
+        """Phase durations (us) of the last cooperative eviction-list build."""
+        self.L.prism_coop_timeline.argtypes = [_p, _p, _p]
+        out = np.zeros(40, dtype=np.uint64)
+        n = np.zeros(1, dtype=np.int32)
+        check(self.L.prism_coop_timeline(self.t, out.ctypes.data, n.ctypes.data))
+        ts = out[: n[0]].astype(np.int64)
+        return {"phases_us": (np.diff(ts) / 1e3).round(1).tolist(), "selected": int(out[39])}
+
     def cache_view(self):
         """The reference RadixCache API over this engine's tree (tests/debug)."""
         from .dart import DeviceRadixCache

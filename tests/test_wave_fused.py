@@ -54,7 +54,7 @@ def _pending_arrays(reqs):
 
 
 def run_case(seed, policy, mode, nseg=40, hot=6, kmin=2, kmax=5, suffixes=(2, 4), sys=8, chunk=4, cap=600,
-             wave=24, nwaves=8, protect=3, cold=2, tiny=False):
+             wave=24, nwaves=8, protect=3, cold=2, tiny=False, coop=1):
     import torch
 
     from paper_2605_08581_b200.wave import DevicePending, WaveEngine
@@ -64,6 +64,7 @@ def run_case(seed, policy, mode, nseg=40, hot=6, kmin=2, kmax=5, suffixes=(2, 4)
     scfg = SchedulerConfig(dispatch_budget=wave, cold_quota=cold)
     eng = WaveEngine(cfg, scfg, nseg, sys, chunk, device=0)
     eng.set_commit_mode(mode)
+    eng.tune(use_coop=coop)
     if tiny:  # minimal selected prefixes of the eviction order
         eng.tune(list_min_tokens=1, list_slack_tokens=0, sel_min_candidates=0)
     ora = OracleRadixCache(cfg)
@@ -136,6 +137,8 @@ def test_ordered_commit_matches_oracle(policy):
     dict(cap=100_000, nwaves=4),                       # no eviction at all
     dict(tiny=True),                                   # minimal eviction-order prefixes
     dict(tiny=True, cap=150, wave=32, nwaves=10),      # ... with capacity stops
+    dict(coop=0),                                      # multi-kernel build / protection
+    dict(coop=0, tiny=True),
 ])
 def test_parallel_commit_variants(variant):
     run_case(5, CachePolicy.DART, mode=0, **variant)
