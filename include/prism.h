@@ -211,6 +211,10 @@ void *prism_qas_stream(prism_qas *q);
 /* Commit used by prism_wave_step: 0 = exact parallel commit with ordered
  * fallback (default), 1 = ordered commit only (parity cross-check). */
 int prism_qas_set_commit_mode(prism_qas *q, int32_t mode);
+/* Rounds over <= max_p pending requests (capped at 4096) with integral weights
+ * run in one CTA; 0: always the multi-kernel round (parity cross-check);
+ * 1: the default cutoff. */
+int prism_qas_set_small(prism_qas *q, int32_t max_p);
 /* out[4]: own kernel launches, CUB primitive calls, rounds so far, and the
  * device microseconds of those rounds when profiling is on. */
 int prism_qas_counts(prism_qas *q, int64_t *out);

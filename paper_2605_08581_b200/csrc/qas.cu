@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/prism.h"
+#include "qas_small.cuh"
 #include "select.cuh"
 
 namespace {
@@ -100,13 +101,14 @@ __global__ void q_align(int64_t P, const int64_t *__restrict__ off, const int32_
                         const uint8_t *__restrict__ reo, const int32_t *__restrict__ g,
                         const int32_t *__restrict__ a, QCfg c, int32_t *__restrict__ aligned,
                         int32_t *__restrict__ sig, int32_t *__restrict__ siglen,
-                        uint32_t *__restrict__ sighash, int32_t *__restrict__ err) {
+                        uint32_t *__restrict__ sighash, int32_t *__restrict__ nlong,
+                        int32_t *__restrict__ longl) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   const int64_t b = off[i];
   const int k = (int)(off[i + 1] - b);
-  if (k > QMAXK) {
-    *err = 1;
+  if (k > QMAXK) {  // aligned by a whole block in q_align_long
+    longl[atomicAdd(nlong, 1)] = (int32_t)i;
     return;
   }
   int32_t s[QMAXK];
@@ -163,6 +165,29 @@ __global__ void q_align(int64_t P, const int64_t *__restrict__ off, const int32_
   uint32_t h = 2166136261u ^ (uint32_t)sl;
   for (int j = 0; j < sl; j++) h = (h ^ (uint32_t)sig[i * c.kappa + j]) * 16777619u;
   sighash[i] = h;
+}
+
+// the requests q_align queued (skeletons longer than QMAXK): one block each
+__global__ void q_align_long(const int32_t *__restrict__ nlong, const int32_t *__restrict__ longl,
+                             const int64_t *__restrict__ off, const int32_t *__restrict__ sk,
+                             const uint8_t *__restrict__ reo, const int32_t *__restrict__ g,
+                             const int32_t *__restrict__ a, QCfg c, int32_t *__restrict__ aligned,
+                             int32_t *__restrict__ sig, int32_t *__restrict__ siglen,
+                             uint32_t *__restrict__ sighash, int32_t *__restrict__ rk) {
+  const int n = *nlong;
+  for (int t = blockIdx.x; t < n; t += gridDim.x) {
+    const int64_t i = longl[t];
+    const int64_t b = off[i];
+    const int k = (int)(off[i + 1] - b);
+    const int sl = qsmall::align_long_block(sk + b, k, reo[i] != 0, g, a, c.wg, c.wa, c.front, c.kappa,
+                                            aligned + b, sig + i * c.kappa, rk + b);
+    if (threadIdx.x == 0) {
+      siglen[i] = sl;
+      uint32_t h = 2166136261u ^ (uint32_t)sl;
+      for (int j = 0; j < sl; j++) h = (h ^ (uint32_t)sig[i * c.kappa + j]) * 16777619u;
+      sighash[i] = h;
+    }
+  }
 }
 
 __device__ inline bool sig_eq(const int32_t *sig, const int32_t *siglen, int64_t kappa, int64_t x, int64_t y) {
@@ -414,93 +439,105 @@ struct prism_qas {
   void *tmp = nullptr;
   size_t tmp_bytes = 0;
   // buffers (device) with capacities
+#define QAS_BUFFERS(X) \
+  X(int64_t, ids) \
+  X(double, arrival) \
+  X(int64_t, off) \
+  X(int32_t, sk) \
+  X(uint8_t, reo) \
+  X(int64_t, aoff) \
+  X(int32_t, ask) \
+  X(int32_t, g) \
+  X(int32_t, a) \
+  X(int32_t, nd) \
+  X(double, prio) \
+  X(uint8_t, dom) \
+  X(int32_t, aligned) \
+  X(int32_t, sig) \
+  X(int32_t, siglen) \
+  X(uint32_t, sighash) \
+  X(int32_t, longl) \
+  X(int32_t, rk) \
+  X(uint64_t, tkey) \
+  X(int32_t, tmin) \
+  X(int32_t, slot_of) \
+  X(int32_t, bmin) \
+  X(int32_t, bslot) \
+  X(int32_t, bmin2) \
+  X(int32_t, bslot2) \
+  X(int32_t, bidx_of_slot) \
+  X(int32_t, bucket) \
+  X(int32_t, iota) \
+  X(int32_t, sb) \
+  X(int32_t, si) \
+  X(int32_t, bstart) \
+  X(int32_t, bend) \
+  X(int32_t, rank) \
+  X(int64_t, pcnt) \
+  X(int64_t, ppos) \
+  X(uint64_t, pk) \
+  X(int32_t, pv) \
+  X(uint64_t, pk2) \
+  X(int32_t, pv2) \
+  X(int32_t, head) \
+  X(int32_t, hpos) \
+  X(int32_t, ppref) \
+  X(int32_t, hstart) \
+  X(double, term) \
+  X(int32_t, hbucket) \
+  X(int32_t, hb0) \
+  X(int32_t, hb1) \
+  X(double, score) \
+  X(uint64_t, skey) \
+  X(int32_t, sval) \
+  X(uint64_t, skey2) \
+  X(int32_t, sval2) \
+  X(int64_t, ssz) \
+  X(int64_t, spre) \
+  X(int64_t, take) \
+  X(int64_t, base) \
+  X(int64_t, hot) \
+  X(uint8_t, sel) \
+  X(K3, ck) \
+  X(int64_t, cv) \
+  X(K3, ck2) \
+  X(int64_t, cv2) \
+  X(int64_t, small) \
+  X(int32_t, err) \
+  /* fused wave step: dispatch order, serialized paths and anchors */ \
+  X(int64_t, members) \
+  X(int64_t, plen) \
+  X(int64_t, poff) \
+  X(int64_t, alen) \
+  X(int64_t, aoffs) \
+  X(uint32_t, tok) \
+  X(int32_t, a_off) \
+  X(int8_t, a_kind) \
+  X(int32_t, a_seg) \
+  X(int32_t, a_snap) \
+  /* cold-lane selection */ \
+  X(int64_t, cw0) \
+  X(int64_t, cw1) \
+  X(prism::Key3, ck1) \
+  X(uint64_t, cv1) \
+  X(prism::Key3, cks) \
+  X(uint64_t, cvs) \
+  X(prism::SelState, sst) \
+  X(prism::Key3, sbmin) \
+  X(prism::Key3, sbmax) \
+  /* one-CTA rounds */ \
+  X(int32_t, touched) \
+  X(int32_t, touched2) \
+  X(int32_t, tn) \
+  X(int64_t, qcounts)
 #define QBUF(T, name) \
   T *name = nullptr;  \
   int64_t name##_cap = 0;
-  QBUF(int64_t, ids)
-  QBUF(double, arrival)
-  QBUF(int64_t, off)
-  QBUF(int32_t, sk)
-  QBUF(uint8_t, reo)
-  QBUF(int64_t, aoff)
-  QBUF(int32_t, ask)
-  QBUF(int32_t, g)
-  QBUF(int32_t, a)
-  QBUF(int32_t, nd)
-  QBUF(double, prio)
-  QBUF(uint8_t, dom)
-  QBUF(int32_t, aligned)
-  QBUF(int32_t, sig)
-  QBUF(int32_t, siglen)
-  QBUF(uint32_t, sighash)
-  QBUF(uint64_t, tkey)
-  QBUF(int32_t, tmin)
-  QBUF(int32_t, slot_of)
-  QBUF(int32_t, bmin)
-  QBUF(int32_t, bslot)
-  QBUF(int32_t, bmin2)
-  QBUF(int32_t, bslot2)
-  QBUF(int32_t, bidx_of_slot)
-  QBUF(int32_t, bucket)
-  QBUF(int32_t, iota)
-  QBUF(int32_t, sb)
-  QBUF(int32_t, si)
-  QBUF(int32_t, bstart)
-  QBUF(int32_t, bend)
-  QBUF(int32_t, rank)
-  QBUF(int64_t, pcnt)
-  QBUF(int64_t, ppos)
-  QBUF(uint64_t, pk)
-  QBUF(int32_t, pv)
-  QBUF(uint64_t, pk2)
-  QBUF(int32_t, pv2)
-  QBUF(int32_t, head)
-  QBUF(int32_t, hpos)
-  QBUF(int32_t, ppref)
-  QBUF(int32_t, hstart)
-  QBUF(double, term)
-  QBUF(int32_t, hbucket)
-  QBUF(int32_t, hb0)
-  QBUF(int32_t, hb1)
-  QBUF(double, score)
-  QBUF(uint64_t, skey)
-  QBUF(int32_t, sval)
-  QBUF(uint64_t, skey2)
-  QBUF(int32_t, sval2)
-  QBUF(int64_t, ssz)
-  QBUF(int64_t, spre)
-  QBUF(int64_t, take)
-  QBUF(int64_t, base)
-  QBUF(int64_t, hot)
-  QBUF(uint8_t, sel)
-  QBUF(K3, ck)
-  QBUF(int64_t, cv)
-  QBUF(K3, ck2)
-  QBUF(int64_t, cv2)
-  QBUF(int64_t, small)
-  QBUF(int32_t, err)
-  // fused wave step: dispatch order, serialized paths and anchors
-  QBUF(int64_t, members)
-  QBUF(int64_t, plen)
-  QBUF(int64_t, poff)
-  QBUF(int64_t, alen)
-  QBUF(int64_t, aoffs)
-  QBUF(uint32_t, tok)
-  QBUF(int32_t, a_off)
-  QBUF(int8_t, a_kind)
-  QBUF(int32_t, a_seg)
-  QBUF(int32_t, a_snap)
-  // cold-lane selection
-  QBUF(int64_t, cw0)
-  QBUF(int64_t, cw1)
-  QBUF(prism::Key3, ck1)
-  QBUF(uint64_t, cv1)
-  QBUF(prism::Key3, cks)
-  QBUF(uint64_t, cvs)
-  QBUF(prism::SelState, sst)
-  QBUF(prism::Key3, sbmin)
-  QBUF(prism::Key3, sbmax)
+  QAS_BUFFERS(QBUF)
 #undef QBUF
+  int64_t small_max_p = 2048;  // one-CTA rounds up to this many pending (<= QS_MAXP)
+  bool full_reset = true;
+  int64_t small_rounds = 0;
   int64_t launches = 0, lib_calls = 0, rounds = 0;
   int32_t commit_mode = 0;
   int prof_on = 0;
@@ -528,11 +565,24 @@ struct QIn {
   const int32_t *ask;
 };
 
+int qas_run_multi(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, const QCfg &c, int64_t *nhot,
+                  int64_t *ncold, int64_t *nbuckets);
+
+// a one-CTA round whose skeleton entries overflowed its buffers (qcounts[3]) is redone
+// by the multi-kernel round, which overwrites every output and counter entry
+int qas_rerun_multi(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, const QCfg &c, int64_t *nhot,
+                    int64_t *ncold, int64_t *nbuckets) {
+  q->small_rounds--;
+  q->rounds--;
+  return qas_run_multi(q, in, P, A, nseg, c, nhot, ncold, nbuckets);
+}
+
 // the full round; outputs stay in q's device buffers
 int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, const QCfg &c, int64_t *nhot, int64_t *ncold,
             int64_t *nbuckets) {
   cudaStream_t st = q->st;
   const int32_t S1 = std::max(nseg, 1);
+  const int64_t gcap0 = q->g_cap;
   QCK(grow(&q->g, q->g_cap, S1));
   QCK(grow(&q->a, q->a_cap, S1));
   QCK(grow(&q->nd, q->nd_cap, S1));
@@ -540,6 +590,126 @@ int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, con
   QCK(grow(&q->dom, q->dom_cap, S1));
   QCK(grow(&q->err, q->err_cap, 1));
   QCK(grow(&q->small, q->small_cap, 8));
+  if (q->g_cap != gcap0) q->full_reset = true;  // fresh (uninitialised) counter arrays
+  // ---- one-CTA round for small pending sets with integral weights (qas_small.cuh)
+  const bool integral = c.wg == std::floor(c.wg) && c.wa == std::floor(c.wa) && c.wn == std::floor(c.wn) &&
+                        std::fabs(c.wg) < 1e9 && std::fabs(c.wa) < 1e9 && std::fabs(c.wn) < 1e9;
+  if (P > 0 && P <= q->small_max_p && integral && c.kappa <= qsmall::QS_MAXK) {
+    // touched-segment lists: a grown list loses the previous round's entries, so
+    // growing either one forces a full counter reset this round
+    const int64_t tneed = (int64_t)S1 + 1;  // distinct touched segments <= nseg
+    if (tneed > q->touched_cap || tneed > q->touched2_cap || !q->touched || !q->touched2) {
+      const int64_t cap = std::max<int64_t>(tneed, std::max(q->touched_cap, q->touched2_cap));
+      QCK(grow(&q->touched, q->touched_cap, cap));
+      QCK(grow(&q->touched2, q->touched2_cap, cap));
+      q->full_reset = true;
+    }
+    if (q->full_reset) {
+      QCK(cudaMemsetAsync(q->g, 0, sizeof(int32_t) * q->g_cap, st));
+      QCK(cudaMemsetAsync(q->a, 0, sizeof(int32_t) * q->a_cap, st));
+      QCK(cudaMemsetAsync(q->nd, 0, sizeof(int32_t) * q->nd_cap, st));
+      QCK(cudaMemsetAsync(q->prio, 0, sizeof(double) * q->prio_cap, st));
+      QCK(cudaMemsetAsync(q->dom, 0, (size_t)q->dom_cap, st));
+      QCK(grow(&q->tn, q->tn_cap, 2));
+      QCK(cudaMemsetAsync(q->tn, 0, 2 * sizeof(int32_t), st));
+      q->full_reset = false;
+    }
+    QCK(grow(&q->tn, q->tn_cap, 2));
+    QCK(grow(&q->aligned, q->aligned_cap, P * qsmall::QS_MAXK));
+    QCK(grow(&q->rk, q->rk_cap, q->aligned_cap));
+    QCK(grow(&q->longl, q->longl_cap, P));
+    QCK(grow(&q->sig, q->sig_cap, P * c.kappa));
+    QCK(grow(&q->siglen, q->siglen_cap, P));
+    int64_t bt = 64;
+    while (bt < 2 * P) bt <<= 1;
+    int64_t pt = 64;
+    while (pt < 2 * P * 16) pt <<= 1;  // pairs: distinct (bucket, seg) <= P*k
+    QCK(grow(&q->tkey, q->tkey_cap, bt));
+    QCK(grow(&q->tmin, q->tmin_cap, bt));
+    QCK(grow(&q->slot_of, q->slot_of_cap, P));
+    QCK(grow(&q->bmin, q->bmin_cap, P));
+    QCK(grow(&q->bstart, q->bstart_cap, P));
+    QCK(grow(&q->bend, q->bend_cap, P));
+    QCK(grow(&q->score, q->score_cap, P));
+    QCK(grow(&q->take, q->take_cap, P));
+    QCK(grow(&q->rank, q->rank_cap, P));
+    QCK(grow(&q->bucket, q->bucket_cap, P));
+    QCK(grow(&q->hot, q->hot_cap, P));
+    QCK(grow(&q->cv2, q->cv2_cap, P));
+    QCK(grow(&q->pk, q->pk_cap, pt));
+    QCK(grow(&q->pv, q->pv_cap, pt));
+    QCK(grow(&q->qcounts, q->qcounts_cap, 4));
+    QCK(cudaMemsetAsync(q->qcounts, 0, 4 * sizeof(int64_t), st));
+    qsmall::QsArgs qa{};
+    qa.P = P;
+    qa.A = A;
+    qa.ids = in.ids;
+    qa.arrival = in.arrival;
+    qa.off = in.off;
+    qa.sk = in.sk;
+    qa.reo = in.reo;
+    qa.aoff = in.aoff;
+    qa.ask = in.ask;
+    qa.g = q->g;
+    qa.a = q->a;
+    qa.nd = q->nd;
+    qa.prio = q->prio;
+    qa.dom = q->dom;
+    qa.touched = q->touched;
+    qa.touched_n = q->tn;
+    qa.prev_touched = q->touched2;
+    qa.aligned = q->aligned;
+    qa.sig = q->sig;
+    qa.siglen = q->siglen;
+    qa.rank = q->rank;
+    qa.bucket = q->bucket;
+    qa.hot = q->hot;
+    qa.cold = q->cv2;
+    qa.score = q->score;
+    qa.counts = q->qcounts;
+    qa.btab_key = q->tkey;
+    qa.btab_min = q->tmin;
+    qa.slot_of = q->slot_of;
+    qa.bidx = q->bmin;
+    qa.bsize = q->bstart;
+    qa.nsegs = q->bend;
+    qa.isum = (long long *)q->take;
+    qa.ptab_key = q->pk;
+    qa.ptab_cnt = q->pv;
+    qa.ptab_mask = pt - 1;
+    qa.btab_mask = bt - 1;
+    qa.longl = q->longl;
+    qa.rk = q->rk;
+    qa.aligned_cap = std::min(q->aligned_cap, q->rk_cap);
+    const qsmall::QsCfg qc{c.budget, c.cold, c.front, c.kappa, c.wg, c.wa, c.wn, c.alpha, c.beta};
+    static bool attr = false;
+    if (!attr) {
+      QCK(cudaFuncSetAttribute(qsmall::k_qas_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)qsmall::QS_SMEM));
+      attr = true;
+    }
+    qsmall::k_qas_small<<<1, qsmall::QS_TPB, qsmall::QS_SMEM, st>>>(qa, qc);
+    QCK(cudaGetLastError());
+    std::swap(q->touched, q->touched2);  // this round's list resets the next round
+    std::swap(q->touched_cap, q->touched2_cap);
+    const int64_t hot_cap = c.budget - c.cold;
+    *nhot = std::min<int64_t>(std::max<int64_t>(hot_cap, 0), P);
+    *ncold = std::min<int64_t>(c.cold, P - *nhot);
+    *nbuckets = -1;  // on the device (qcounts[2]); the host API reads it back
+    q->launches += 1;
+    q->rounds++;
+    q->small_rounds++;
+    return PRISM_OK;
+  }
+  return qas_run_multi(q, in, P, A, nseg, c, nhot, ncold, nbuckets);
+}
+
+// the multi-kernel round (any P, any skeleton length, any weights)
+int qas_run_multi(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, const QCfg &c, int64_t *nhot,
+                  int64_t *ncold, int64_t *nbuckets) {
+  cudaStream_t st = q->st;
+  const int32_t S1 = std::max(nseg, 1);
+  q->full_reset = true;  // the multi-kernel round writes every counter entry
   QCK(cudaMemsetAsync(q->g, 0, sizeof(int32_t) * S1, st));
   QCK(cudaMemsetAsync(q->a, 0, sizeof(int32_t) * S1, st));
   QCK(cudaMemsetAsync(q->nd, 0, sizeof(int32_t) * S1, st));
@@ -559,8 +729,12 @@ int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, con
   QCK(grow(&q->sig, q->sig_cap, P1 * c.kappa));
   QCK(grow(&q->siglen, q->siglen_cap, P1));
   QCK(grow(&q->sighash, q->sighash_cap, P1));
+  QCK(grow(&q->longl, q->longl_cap, P1));
+  QCK(grow(&q->rk, q->rk_cap, std::max<int64_t>(nsk, 1)));
   q_align<<<nblk(P), TPB, 0, st>>>(P, in.off, in.sk, in.reo, q->g, q->a, c, q->aligned, q->sig, q->siglen,
-                                   q->sighash, q->err);
+                                   q->sighash, q->err, q->longl);
+  q_align_long<<<148, 256, 0, st>>>(q->err, q->longl, in.off, in.sk, in.reo, q->g, q->a, c, q->aligned, q->sig,
+                                    q->siglen, q->sighash, q->rk);
   // buckets
   int64_t T = 64;
   while (T < 2 * P) T <<= 1;
@@ -578,11 +752,8 @@ int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, con
   QCK(cudaMemsetAsync(q->small, 0, sizeof(int64_t), st));
   q_bucket_list<<<nblk(T), TPB, 0, st>>>(T, q->tkey, q->tmin, q->bmin, q->bslot, q->small);
   int64_t nb = 0;
-  int32_t err = 0;
   QCK(cudaMemcpyAsync(&nb, q->small, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  QCK(cudaMemcpyAsync(&err, q->err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   QCK(cudaStreamSynchronize(st));
-  if (err) return qfail(PRISM_INVALID, "skeleton longer than 64 segments");
   size_t bytes = 0;
   QCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, q->bmin, q->bmin2, q->bslot, q->bslot2, (int)nb, 0, 32, st));
   if (ensure_tmp(q, bytes)) return PRISM_CUDA;
@@ -773,16 +944,13 @@ void prism_qas_destroy(prism_qas *q) {
   if (!q) return;
   cudaSetDevice(q->dev);
   cudaStreamSynchronize(q->st);
-  void *bufs[] = {q->tmp,   q->ids,     q->arrival, q->off,    q->sk,     q->reo,    q->aoff,    q->ask,
-                  q->g,     q->a,       q->nd,      q->prio,   q->dom,    q->aligned, q->sig,    q->siglen,
-                  q->sighash, q->tkey,  q->tmin,    q->slot_of, q->bmin,  q->bslot,  q->bmin2,   q->bslot2,
-                  q->bidx_of_slot, q->bucket, q->iota, q->sb,  q->si,     q->bstart, q->bend,    q->rank,
-                  q->pcnt,  q->ppos,    q->pk,      q->pv,     q->pk2,    q->pv2,    q->head,    q->hpos,
-                  q->ppref, q->hstart,  q->term,    q->hbucket, q->hb0,   q->hb1,    q->score,   q->skey,
-                  q->sval,  q->skey2,   q->sval2,   q->ssz,    q->spre,   q->take,   q->base,    q->hot,
-                  q->sel,   q->ck,      q->cv,      q->ck2,    q->cv2,    q->small,  q->err};
+#define QPTR(T, name) (void *)q->name,
+  void *bufs[] = {q->tmp, QAS_BUFFERS(QPTR)};
+#undef QPTR
   for (void *p : bufs)
     if (p) cudaFree(p);
+  if (q->e0) cudaEventDestroy(q->e0);
+  if (q->e1) cudaEventDestroy(q->e1);
   cudaStreamDestroy(q->st);
   delete q;
 }
@@ -826,6 +994,16 @@ int prism_qas_round(prism_qas *q, int64_t P, const int64_t *ids, const double *a
   const QIn in{q->ids, q->arrival, q->off, q->sk, q->reo, q->aoff, q->ask};
   int rc = qas_run(q, in, P, A, nseg, c, nhot, ncold, nbuckets);
   if (rc) return rc;
+  if (*nbuckets < 0) {  // one-CTA round: counts live on the device
+    int64_t qc[4];
+    QCK(cudaMemcpyAsync(qc, q->qcounts, sizeof(qc), cudaMemcpyDeviceToHost, st));
+    QCK(cudaStreamSynchronize(st));
+    if (qc[3]) {
+      if ((rc = qas_rerun_multi(q, in, P, A, nseg, c, nhot, ncold, nbuckets))) return rc;
+    } else {
+      *nbuckets = qc[2];
+    }
+  }
   if (*nhot) QCK(cudaMemcpyAsync(hot, q->hot, sizeof(int64_t) * *nhot, cudaMemcpyDeviceToHost, st));
   if (*ncold) QCK(cudaMemcpyAsync(cold, q->cv2, sizeof(int64_t) * *ncold, cudaMemcpyDeviceToHost, st));
   if (P) {
@@ -984,7 +1162,14 @@ int prism_qas_round_device(prism_qas *q, int64_t P, const int64_t *ids, const do
   QCfg c{cfg->dispatch_budget, cfg->cold_quota, cfg->front_width, cfg->signature_size,
          cfg->w_g, cfg->w_a, cfg->w_n, cfg->alpha_size, cfg->beta_util};
   const QIn in{ids, arrival, sk_off, sk, reorderable, act_off, act_sk};
-  return qas_run(q, in, P, A, nseg, c, nhot, ncold, nbuckets);
+  int rc = qas_run(q, in, P, A, nseg, c, nhot, ncold, nbuckets);
+  if (rc || *nbuckets >= 0) return rc;
+  int64_t qc[4];  // one-CTA round: bucket count and the redo flag
+  QCK(cudaMemcpyAsync(qc, q->qcounts, sizeof(qc), cudaMemcpyDeviceToHost, q->st));
+  QCK(cudaStreamSynchronize(q->st));
+  if (qc[3]) return qas_rerun_multi(q, in, P, A, nseg, c, nhot, ncold, nbuckets);
+  *nbuckets = qc[2];
+  return PRISM_OK;
 }
 
 int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, const double *arrival,
@@ -998,7 +1183,7 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
   int64_t nh = 0, nc = 0, nb = 0;
   if (q->prof_on) cudaEventRecord(q->e0, st);
   int rc = prism_qas_round_device(q, P, ids, arrival, sk_off, sk, reorderable, A, act_off, act_sk, nseg, cfg, &nh,
-                                  &nc, &nb);
+                                  &nc, &nb);  // (one-CTA rounds sync here for the bucket count / redo flag)
   if (rc) return rc;
   if (q->prof_on) {
     cudaEventRecord(q->e1, st);
@@ -1059,6 +1244,14 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
   return prism_admit_wave_segmented(t, B, q->poff, q->tok, q->aoffs, q->a_off, q->a_kind, q->a_seg, q->a_snap,
                                     members, sk_off, q->aligned, sys_len, chunk, q->commit_mode, hits, leaf_slots,
                                     leaf_ids, n_admitted, (void *)st);
+}
+
+// rounds over <= max_p pending requests with integral weights run in one CTA
+// (qas_small.cuh); 0: always the multi-kernel round; 1: the default cutoff
+int prism_qas_set_small(prism_qas *q, int32_t max_p) {
+  if (max_p < 0) return qfail(PRISM_INVALID, "max_p must be >= 0");
+  q->small_max_p = max_p == 1 ? 2048 : std::min<int64_t>(max_p, qsmall::QS_MAXP);
+  return PRISM_OK;
 }
 
 // 0: exact parallel wave commit with ordered fallback (default); 1: ordered commit only

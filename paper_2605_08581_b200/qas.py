@@ -50,6 +50,13 @@ class DeviceScheduler:
         if not self._h:
             raise _lib.PrismError(_lib.last_error())
 
+    def set_small(self, on: bool | int) -> None:
+        """One-CTA rounds for small pending sets with integral weights.
+        True: the default cutoff; False: never; an int: the largest P (<= 4096)."""
+        self._L.prism_qas_set_small.argtypes = [C.c_void_p, C.c_int32]
+        max_p = (1 if on else 0) if isinstance(on, bool) else int(on)
+        check(self._L.prism_qas_set_small(self._h, max_p))
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             self._L.prism_qas_destroy(self._h)

@@ -24,13 +24,79 @@ def make_request(rid, skeleton, arrival=0.0, reorderable=True, sys_len=10, chunk
     return Request(rid, arrival, list(skeleton), reorderable, [], sys_len, len(skeleton) * chunk, suffix)
 
 
-def test_golden_rounds():
+@pytest.mark.parametrize("small", [4096, True, False])
+def test_golden_rounds(small):
+    from paper_2605_08581_b200.qas import DeviceScheduler
+
+    ds = DeviceScheduler()
+    ds.set_small(small)  # one-CTA rounds vs the multi-kernel round
     for i, case in enumerate(G.load("qas_rounds.json.gz")):
         pending, active, cfg = G.qas_case(case)
         try:
-            G.assert_qas_case(case, sched(pending, active, cfg))
+            G.assert_qas_case(case, ds.schedule_round(pending, active, cfg, 0.0))
         except AssertionError as e:
             raise AssertionError(f"round {i}: {e}") from e
+
+
+def test_mixed_round_sizes_one_scheduler():
+    """Small (one-CTA) and large (multi-kernel) rounds interleaved on one
+    scheduler: the per-round counter reset (touched lists / full resets) must
+    never leak state between rounds."""
+    from paper_2605_08581_b200.qas import DeviceScheduler
+
+    ds = DeviceScheduler()
+    ds.set_small(4096)
+    rng = np.random.default_rng(31)
+    for P in (100, 5000, 200, 300, 8000, 50, 4096, 1):
+        nseg = int(rng.integers(20, 3000))
+        pend = [Request(i, float(rng.random()), [int(x) for x in rng.choice(nseg, size=int(rng.integers(1, 7)),
+                                                                          replace=False)], True, [], 8, 32, 4)
+                for i in range(P)]
+        act = [Request(10**6 + j, 0.0, [int(rng.integers(0, nseg))], True, [], 8, 8, 4) for j in range(3)]
+        cfg = SchedulerConfig(dispatch_budget=min(P, 512) or 1, cold_quota=min(2, min(P, 512) or 1))
+        bd = ds.schedule_round(pend, act, cfg, 0.0)
+        bo = oracle_schedule_round(pend, act, cfg)
+        assert [r.id for r in bd.members] == [r.id for r in bo.members], P
+        assert bd.priorities == bo.priorities, P
+        assert bd.bucket_scores == bo.bucket_scores, P
+        assert bd.counters.g == bo.counters.g and bd.counters.n == bo.counters.n, P
+
+
+@pytest.mark.parametrize("small", [4096, False])
+def test_long_skeletons(small):
+    """Skeletons longer than the per-thread limit (64) are aligned by a whole
+    block (rank counting); a round whose skeleton entries exceed the one-CTA
+    buffers is redone by the multi-kernel path.  Duplicated segments, fronts
+    wider than kappa and non-reorderable requests included; the next round
+    must see clean counters."""
+    from paper_2605_08581_b200.qas import DeviceScheduler
+
+    ds = DeviceScheduler()
+    ds.set_small(small)
+    rng = np.random.default_rng(5)
+    for r in range(8):
+        P = [40, 2, 300, 3, 40, 5000, 7, 64][r]
+        nseg = [200, 50, 1000, 30, 200, 3000, 400, 90][r]
+
+        def skel(i):
+            k = int(rng.choice([3, 70, 150, 700])) if i % 5 == r % 5 else int(rng.integers(1, 6))
+            return [int(x) for x in rng.integers(0, nseg, size=k)]  # duplicates allowed
+
+        pend = [Request(i, float(rng.integers(0, 50)), skel(i), bool(rng.random() < 0.8), [], 8, 32, 4)
+                for i in range(P)]
+        act = [Request(10**6 + j, 0.0, [int(x) for x in rng.integers(0, nseg, size=80)], True, [], 8, 8, 4)
+               for j in range(2)]
+        cfg = SchedulerConfig(dispatch_budget=min(P, 16), cold_quota=min(P, 2), front_width=[3, 90, 5][r % 3],
+                              signature_size=[2, 1, 4][r % 3])
+        bd = ds.schedule_round(pend, act, cfg, 0.0)
+        bo = oracle_schedule_round(pend, act, cfg)
+        assert [r_.id for r_ in bd.members] == [r_.id for r_ in bo.members], r
+        assert bd.priorities == bo.priorities and bd.bucket_scores == bo.bucket_scores, r
+        assert bd.counters.g == bo.counters.g and bd.counters.a == bo.counters.a, r
+        for rid, h in bo.hints.items():
+            d = bd.hints[rid]
+            assert (d.signature, d.rank, d.aligned_skeleton, d.counter_snapshot) == (
+                h.signature, h.rank, h.aligned_skeleton, h.counter_snapshot), (r, rid)
 
 
 class TestScheduleRound:
