@@ -212,13 +212,20 @@ void *prism_qas_stream(prism_qas *q);
  * fallback (default), 1 = ordered commit only (parity cross-check). */
 int prism_qas_set_commit_mode(prism_qas *q, int32_t mode);
 /* Rounds over <= max_p pending requests (capped at 4096) with integral weights
- * run in one CTA; 0: always the multi-kernel round (parity cross-check);
- * 1: the default cutoff. */
+ * run as one launch (one CTA or a cooperative grid); 0: always the
+ * multi-kernel round (parity cross-check); 1: the default cutoff. */
 int prism_qas_set_small(prism_qas *q, int32_t max_p);
+/* One-launch round shape: key 0 = max pending (as prism_qas_set_small),
+ * 1 = CTAs of the cooperative grid (0: auto), 2 = pending requests per CTA
+ * for the auto grid; key 3 writes the last round's CTA count to *out. */
+int prism_qas_tune(prism_qas *q, int32_t key, int64_t value, int64_t *out);
 /* out[4]: own kernel launches, CUB primitive calls, rounds so far, and the
  * device microseconds of those rounds when profiling is on. */
 int prism_qas_counts(prism_qas *q, int64_t *out);
 int prism_qas_profile(prism_qas *q, int32_t enable);
+/* Phase timeline of the last profiled one-CTA round: out_ns[i] = ns from the
+ * kernel's start to the end of phase i (13 phases; see qas_small.cuh). */
+int prism_qas_small_timeline(prism_qas *q, int64_t *out_ns, int32_t n);
 /* Copy the last round's pending demand counters g[0..nseg) (DEVICE int32) to
  * dst (DEVICE) -- the per-window counter vector the replicas all-reduce. */
 int prism_qas_counters(prism_qas *q, int32_t *dst, int32_t nseg);

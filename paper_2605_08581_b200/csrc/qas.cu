@@ -529,13 +529,19 @@ struct prism_qas {
   X(int32_t, touched) \
   X(int32_t, touched2) \
   X(int32_t, tn) \
-  X(int64_t, qcounts)
+  X(int64_t, qcounts) \
+  X(int32_t, plist) \
+  X(unsigned long long, qts)
 #define QBUF(T, name) \
   T *name = nullptr;  \
   int64_t name##_cap = 0;
   QAS_BUFFERS(QBUF)
 #undef QBUF
-  int64_t small_max_p = 2048;  // one-CTA rounds up to this many pending (<= QS_MAXP)
+  int64_t small_max_p = 4096;  // one-launch rounds up to this many pending (<= QS_MAXP)
+  int64_t small_grid = 0;      // CTAs of a one-launch round (0: from small_per_cta)
+  int64_t small_per_cta = 32;  // pending requests per CTA when sizing the grid
+  int32_t small_coresident = 0;
+  int64_t last_small_grid = 0;
   bool full_reset = true;
   int64_t small_rounds = 0;
   int64_t launches = 0, lib_calls = 0, rounds = 0;
@@ -594,7 +600,7 @@ int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, con
   // ---- one-CTA round for small pending sets with integral weights (qas_small.cuh)
   const bool integral = c.wg == std::floor(c.wg) && c.wa == std::floor(c.wa) && c.wn == std::floor(c.wn) &&
                         std::fabs(c.wg) < 1e9 && std::fabs(c.wa) < 1e9 && std::fabs(c.wn) < 1e9;
-  if (P > 0 && P <= q->small_max_p && integral && c.kappa <= qsmall::QS_MAXK) {
+  if (P > 0 && P <= q->small_max_p && integral && c.kappa <= QMAXK) {
     // touched-segment lists: a grown list loses the previous round's entries, so
     // growing either one forces a full counter reset this round
     const int64_t tneed = (int64_t)S1 + 1;  // distinct touched segments <= nseg
@@ -615,7 +621,7 @@ int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, con
       q->full_reset = false;
     }
     QCK(grow(&q->tn, q->tn_cap, 2));
-    QCK(grow(&q->aligned, q->aligned_cap, P * qsmall::QS_MAXK));
+    QCK(grow(&q->aligned, q->aligned_cap, P * qsmall::QS_SKCAP));
     QCK(grow(&q->rk, q->rk_cap, q->aligned_cap));
     QCK(grow(&q->longl, q->longl_cap, P));
     QCK(grow(&q->sig, q->sig_cap, P * c.kappa));
@@ -623,7 +629,7 @@ int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, con
     int64_t bt = 64;
     while (bt < 2 * P) bt <<= 1;
     int64_t pt = 64;
-    while (pt < 2 * P * 16) pt <<= 1;  // pairs: distinct (bucket, seg) <= P*k
+    while (pt < 2 * P * qsmall::QS_SKCAP) pt <<= 1;  // pairs: distinct (bucket, seg) <= nsk
     QCK(grow(&q->tkey, q->tkey_cap, bt));
     QCK(grow(&q->tmin, q->tmin_cap, bt));
     QCK(grow(&q->slot_of, q->slot_of_cap, P));
@@ -638,8 +644,9 @@ int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, con
     QCK(grow(&q->cv2, q->cv2_cap, P));
     QCK(grow(&q->pk, q->pk_cap, pt));
     QCK(grow(&q->pv, q->pv_cap, pt));
-    QCK(grow(&q->qcounts, q->qcounts_cap, 4));
-    QCK(cudaMemsetAsync(q->qcounts, 0, 4 * sizeof(int64_t), st));
+    QCK(grow(&q->plist, q->plist_cap, pt / 2));
+    QCK(grow(&q->qcounts, q->qcounts_cap, 8));
+    QCK(cudaMemsetAsync(q->qcounts, 0, 8 * sizeof(int64_t), st));
     qsmall::QsArgs qa{};
     qa.P = P;
     qa.A = A;
@@ -676,20 +683,37 @@ int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, con
     qa.isum = (long long *)q->take;
     qa.ptab_key = q->pk;
     qa.ptab_cnt = q->pv;
-    qa.ptab_mask = pt - 1;
+    qa.plist = q->plist;
+    qa.ptab_cap = std::min(q->pk_cap, q->pv_cap);
     qa.btab_mask = bt - 1;
     qa.longl = q->longl;
     qa.rk = q->rk;
     qa.aligned_cap = std::min(q->aligned_cap, q->rk_cap);
+    if (q->prof_on) QCK(grow(&q->qts, q->qts_cap, qsmall::QS_NTS));
+    qa.ts = q->prof_on ? q->qts : nullptr;
     const qsmall::QsCfg qc{c.budget, c.cold, c.front, c.kappa, c.wg, c.wa, c.wn, c.alpha, c.beta};
-    static bool attr = false;
-    if (!attr) {
+    if (!q->small_coresident) {
       QCK(cudaFuncSetAttribute(qsmall::k_qas_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)qsmall::QS_SMEM));
-      attr = true;
+      int nsm = 0, occ = 0;
+      QCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, q->dev));
+      QCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, qsmall::k_qas_small, qsmall::QS_TPB,
+                                                        qsmall::QS_SMEM));
+      q->small_coresident = std::max(1, nsm * occ);
     }
-    qsmall::k_qas_small<<<1, qsmall::QS_TPB, qsmall::QS_SMEM, st>>>(qa, qc);
+    // grid: one CTA for small sets (no grid barriers), else ~one CTA per
+    // small_per_cta pending requests, up to every SM
+    int64_t G = q->small_grid > 0 ? q->small_grid : (P + q->small_per_cta - 1) / q->small_per_cta;
+    G = std::max<int64_t>(1, std::min<int64_t>(G, q->small_coresident));
+    if (G == 1) {
+      qsmall::k_qas_small<<<1, qsmall::QS_TPB, qsmall::QS_SMEM, st>>>(qa, qc);
+    } else {
+      void *args[] = {(void *)&qa, (void *)&qc};
+      QCK(cudaLaunchCooperativeKernel((void *)qsmall::k_qas_small, dim3((unsigned)G), dim3(qsmall::QS_TPB), args,
+                                      qsmall::QS_SMEM, st));
+    }
     QCK(cudaGetLastError());
+    q->last_small_grid = G;
     std::swap(q->touched, q->touched2);  // this round's list resets the next round
     std::swap(q->touched_cap, q->touched2_cap);
     const int64_t hot_cap = c.budget - c.cold;
@@ -1144,6 +1168,16 @@ int prism_qas_profile(prism_qas *q, int32_t enable) {
   return PRISM_OK;
 }
 
+int prism_qas_small_timeline(prism_qas *q, int64_t *out_ns, int32_t n) {
+  cudaSetDevice(q->dev);
+  if (!q->qts) return qfail(PRISM_INVALID, "no profiled one-CTA round yet");
+  unsigned long long t[qsmall::QS_NTS];
+  QCK(cudaMemcpyAsync(t, q->qts, sizeof(t), cudaMemcpyDeviceToHost, q->st));
+  QCK(cudaStreamSynchronize(q->st));
+  for (int i = 0; i < n && i < qsmall::QS_NTS; i++) out_ns[i] = (int64_t)(t[i] - t[0]);
+  return PRISM_OK;
+}
+
 int prism_qas_counters(prism_qas *q, int32_t *dst, int32_t nseg) {
   cudaSetDevice(q->dev);
   if (nseg > q->g_cap) return qfail(PRISM_INVALID, "nseg exceeds the last round's counter vector");
@@ -1250,8 +1284,31 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
 // (qas_small.cuh); 0: always the multi-kernel round; 1: the default cutoff
 int prism_qas_set_small(prism_qas *q, int32_t max_p) {
   if (max_p < 0) return qfail(PRISM_INVALID, "max_p must be >= 0");
-  q->small_max_p = max_p == 1 ? 2048 : std::min<int64_t>(max_p, qsmall::QS_MAXP);
+  q->small_max_p = max_p == 1 ? qsmall::QS_MAXP : std::min<int64_t>(max_p, qsmall::QS_MAXP);
   return PRISM_OK;
+}
+
+// one-launch round shape: key 0 = max pending (as prism_qas_set_small),
+// 1 = CTAs (0: auto), 2 = pending requests per CTA for the auto grid;
+// key 3 (read-only through out) = CTAs of the last one-launch round
+int prism_qas_tune(prism_qas *q, int32_t key, int64_t value, int64_t *out) {
+  switch (key) {
+    case 0:
+      return prism_qas_set_small(q, (int32_t)value);
+    case 1:
+      if (value < 0) return qfail(PRISM_INVALID, "grid must be >= 0");
+      q->small_grid = value;
+      return PRISM_OK;
+    case 2:
+      if (value < 1) return qfail(PRISM_INVALID, "per-CTA count must be >= 1");
+      q->small_per_cta = value;
+      return PRISM_OK;
+    case 3:
+      if (out) *out = q->last_small_grid;
+      return PRISM_OK;
+    default:
+      return qfail(PRISM_INVALID, "unknown QAS tunable");
+  }
 }
 
 // 0: exact parallel wave commit with ordered fallback (default); 1: ordered commit only

@@ -1,25 +1,31 @@
-// qas_small.cuh -- one QAS round (scheduler.py:192-273) in ONE CTA.
+// qas_small.cuh -- one QAS round (scheduler.py:192-273) in ONE launch.
 //
-// For pending sets of up to QS_MAXP requests the whole round runs inside a
-// single 1024-thread CTA: no kernel launches between its phases, no host
-// round trips, shared-memory bitonic sorts for the bucket order and the cold
-// lane, a sequential warp pass for the in-bucket ranks (first-seen order),
-// and a hash aggregation of distinct (bucket, segment) pairs for the bucket
-// utilities.  Segment counters are reset through the list of segments the
-// previous round touched, so the cost is O(P*k), not O(num_segments).
+// For pending sets of up to QS_MAXP requests the whole round is one kernel:
+// a single 1024-thread CTA for small sets, a cooperative grid (grid barriers
+// between phases) for larger ones.  No host round trips; the parallel phases
+// (counters, alignment + signatures, bucket hashing, distinct (bucket,
+// segment) pairs, utility terms, hot-lane scatter, priorities) are strided over
+// the grid, the short serial ones run in block 0's shared memory: bucket
+// creation order and the in-bucket ranks (a warp pass in pending order), the
+// score sort, and the cold lane (a byte radix select of the oldest leftovers,
+// then a sort of just those).  Segment counters are reset through the list of
+// segments the previous round touched, so the cost is O(P*k), not
+// O(num_segments).
 //
 // Exactness: identical float expressions to qas.cu / the reference; the
 // utility sum uses int64 accumulation and is therefore only used when every
 // term is an exact integer (integral weights: the reference defaults) -- the
 // host selects this kernel only then.
 #pragma once
+#include <cooperative_groups.h>
 #include <cstdint>
 
 namespace qsmall {
 
 constexpr int QS_TPB = 1024;
 constexpr int QS_MAXP = 4096;  // bitonic sort capacity (shared memory)
-constexpr int QS_MAXK = 64;
+constexpr int QS_MAXK = 16;   // per-thread alignment; longer skeletons: a whole block
+constexpr int QS_SKCAP = 64;  // skeleton entries per request provisioned (aligned, pair table)
 constexpr uint64_t QS_EMPTY = ~0ull;
 
 struct QsCfg {
@@ -48,19 +54,22 @@ struct QsArgs {
   int32_t *aligned, *sig, *siglen, *rank, *bucket;
   int64_t *hot, *cold;
   double *score;  // per bucket, creation order
-  int64_t *counts;  // [0] nhot, [1] ncold, [2] nbuckets, [3] redo on the multi-kernel path
+  int64_t *counts;  // [0] nhot [1] ncold [2] nbuckets [3] redo multi-kernel [4] nlong [5] npairs
   // scratch (global)
   uint64_t *btab_key;  // signature table, size 2*QS_MAXP (power of two)
   int32_t *btab_min, *slot_of, *bidx;
   int32_t *bsize, *nsegs;
   long long *isum;
-  uint64_t *ptab_key;  // (bucket, seg) pair table
+  uint64_t *ptab_key;  // (bucket, seg) pair table (the kernel uses 2*nsk slots of it)
   int32_t *ptab_cnt;
-  int64_t ptab_mask, btab_mask;
+  int32_t *plist;      // inserted pair slots
+  int64_t ptab_cap, btab_mask;
   int32_t *longl;       // requests with skeletons longer than QS_MAXK
   int32_t *rk;          // rank scratch for them (aligned_cap ints)
   int64_t aligned_cap;  // capacity of aligned / rk in skeleton entries
+  unsigned long long *ts;  // QS_NTS phase stamps, or null
 };
+constexpr int QS_NTS = 11;
 
 __device__ inline uint64_t qmix64(uint64_t x) {
   x ^= x >> 33;
@@ -209,11 +218,14 @@ __device__ inline void block_bitonic(QKey *k, int32_t *v, int n) {
   }
 }
 
-constexpr size_t QS_SMEM = (sizeof(QKey) + sizeof(int32_t)) * QS_MAXP + sizeof(int32_t) * QS_MAXP;
+constexpr size_t QS_SMEM = (sizeof(QKey) + 3 * sizeof(int32_t)) * QS_MAXP;
 
 // 3. bucket of request i's signature tuple; first member via atomicMin
 // (scheduler.py:211-223).  Open addressing on (hash, first index seen).
+// Other CTAs compare against the signature published with the CAS: it is
+// fenced before, and read through L2 after.
 __device__ inline void qs_bucket_insert(const QsArgs &A, const QsCfg &c, int64_t i, int sl) {
+  __threadfence();
   uint32_t h = 2166136261u ^ (uint32_t)sl;
   for (int j = 0; j < sl; j++) h = (h ^ (uint32_t)A.sig[i * c.kappa + j]) * 16777619u;
   const uint64_t mine = ((uint64_t)h << 32) | (uint32_t)i;
@@ -223,8 +235,8 @@ __device__ inline void qs_bucket_insert(const QsArgs &A, const QsCfg &c, int64_t
     bool same = prev == QS_EMPTY;
     if (!same && (uint32_t)(prev >> 32) == h) {
       const int64_t o = (int64_t)(prev & 0xffffffffu);
-      same = A.siglen[o] == sl;
-      for (int j = 0; same && j < sl; j++) same = A.sig[o * c.kappa + j] == A.sig[i * c.kappa + j];
+      same = __ldcg(&A.siglen[o]) == sl;
+      for (int j = 0; same && j < sl; j++) same = __ldcg(&A.sig[o * c.kappa + j]) == A.sig[i * c.kappa + j];
     }
     if (same) {
       atomicMin(&A.btab_min[pos], (int32_t)i);
@@ -235,25 +247,171 @@ __device__ inline void qs_bucket_insert(const QsArgs &A, const QsCfg &c, int64_t
   }
 }
 
+__device__ inline unsigned long long qs_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// phase timeline (profiling only): ts[n] = %globaltimer at the end of phase n
+#define QS_TS(n)                                                         \
+  do {                                                                   \
+    if (A.ts && blockIdx.x == 0 && threadIdx.x == 0) A.ts[n] = qs_gtimer(); \
+  } while (0)
+
+// grid-wide barrier; a plain block barrier when the round runs in one CTA
+__device__ inline void qs_gsync() {
+  if (gridDim.x == 1) {
+    __syncthreads();
+  } else {
+    cooperative_groups::this_grid().sync();
+  }
+}
+
+__device__ inline int32_t qs_ld(const int32_t *p) { return __ldcg(p); }  // L2 (coherent across CTAs)
+
+// each distinct segment of skeleton [b, e) once (count_segments dedup, 83-89)
+template <class F>
+__device__ inline void qs_distinct(const int32_t *sk, int64_t b, int64_t e, F &&f) {
+  for (int64_t j = b; j < e; j++) {
+    const int32_t s = sk[j];
+    bool dup = false;
+    for (int64_t q = b; q < j && !dup; q++) dup = sk[q] == s;
+    if (!dup) f(s);
+  }
+}
+
+// cold lane (242-245) in block 0: the nc smallest leftovers by (arrival, id),
+// sorted.  Leftovers are compacted into shared memory; when fewer than all of
+// them are taken, an MSB-first byte radix select over the 128-bit keys finds
+// exactly the nc smallest (keys are distinct: ids are unique), so only those
+// are sorted.
+__device__ inline void qs_cold_lane(const QsArgs &A, const QsCfg &c, int64_t P, int64_t nc, QKey *sk,
+                                    int32_t *sv, int32_t *tmp, int32_t *swarp) {
+  __shared__ int32_t hist[256];
+  __shared__ int32_t s_need, s_digit, s_done;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int64_t i = tid; i < P; i += nt) tmp[i] = qs_ld(&A.bidx[i]) ? 0 : 1;  // bidx: hot flag
+  __syncthreads();
+  int32_t *lf = tmp + QS_MAXP;  // (sbk, free here) leftover flags kept for the fill
+  for (int64_t i = tid; i < P; i += nt) lf[i] = tmp[i];
+  const int m = block_exscan(tmp, (int)P, swarp);
+  for (int64_t i = tid; i < P; i += nt) {
+    if (lf[i]) {
+      sk[tmp[i]] = {qord(A.arrival[i]), (uint64_t)A.ids[i] ^ 0x8000000000000000ull};
+      sv[tmp[i]] = (int32_t)i;
+    }
+  }
+  __syncthreads();
+  int n = m;
+  if (nc < m) {
+    uint8_t *st = reinterpret_cast<uint8_t *>(tmp);  // 0 candidate, 1 taken, 2 dropped
+    for (int q = tid; q < m; q += nt) st[q] = 0;
+    if (tid == 0) {
+      s_need = (int32_t)nc;
+      s_done = 0;
+    }
+    __syncthreads();
+    for (int d = 15; d >= 0 && !s_done; d--) {
+      for (int x = tid; x < 256; x += nt) hist[x] = 0;
+      __syncthreads();
+      for (int q = tid; q < m; q += nt) {
+        if (st[q]) continue;
+        const uint64_t w = d >= 8 ? sk[q].hi : sk[q].lo;
+        atomicAdd(&hist[(w >> ((d & 7) * 8)) & 0xff], 1);
+      }
+      __syncthreads();
+      if (tid < 32) {  // the digit holding the need-th smallest candidate
+        int cnt[8], tot = 0;
+        for (int x = 0; x < 8; x++) tot += cnt[x] = hist[tid * 8 + x];
+        int incl = tot;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (tid >= o) incl += y;
+        }
+        int run = incl - tot;
+        const int need = s_need;
+        __syncwarp();
+        for (int x = 0; x < 8; x++) {
+          if (run < need && need <= run + cnt[x]) {
+            s_digit = tid * 8 + x;
+            s_need = need - run;
+            s_done = (need - run) == cnt[x];
+          }
+          run += cnt[x];
+        }
+      }
+      __syncthreads();
+      const int D = s_digit;
+      const bool all = s_done;
+      for (int q = tid; q < m; q += nt) {
+        if (st[q]) continue;
+        const uint64_t w = d >= 8 ? sk[q].hi : sk[q].lo;
+        const int dig = (int)((w >> ((d & 7) * 8)) & 0xff);
+        st[q] = dig < D ? 1 : (dig > D ? 2 : (all ? 1 : 0));
+      }
+      __syncthreads();
+    }
+    // compact the taken keys to the front (each thread reads before any write)
+    QKey kk[4];
+    int32_t vv[4], fl[4];
+    int own = 0;
+    for (int q = tid; q < m; q += nt, own++) {
+      kk[own] = sk[q];
+      vv[own] = sv[q];
+      fl[own] = st[q] == 1;
+    }
+    __syncthreads();
+    own = 0;
+    for (int q = tid; q < m; q += nt, own++) tmp[q] = fl[own];
+    __syncthreads();
+    n = block_exscan(tmp, m, swarp);
+    own = 0;
+    for (int q = tid; q < m; q += nt, own++) {
+      if (fl[own]) {
+        sk[tmp[q]] = kk[own];
+        sv[tmp[q]] = vv[own];
+      }
+    }
+    __syncthreads();
+  }
+  block_bitonic(sk, sv, n);
+  for (int q = tid; q < nc; q += nt) A.cold[q] = sv[q];
+  // n_disp of the cold members (247-248)
+  for (int q = tid; q < nc; q += nt) {
+    const int64_t i = sv[q];
+    qs_distinct(A.sk, A.off[i], A.off[i + 1], [&](int32_t s) { atomicAdd(&A.nd[s], 1); });
+  }
+}
+
+// One QAS round.  gridDim.x == 1: the whole round in one CTA (block barriers);
+// gridDim.x > 1: a cooperative launch, grid barriers between the phases, the
+// short serial phases (bucket order + in-bucket ranks, score sort + hot-lane
+// prefix, cold lane) in block 0's shared memory.
 __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   extern __shared__ __align__(16) unsigned char qs_smem[];
   QKey *sk = reinterpret_cast<QKey *>(qs_smem);
   int32_t *sv = reinterpret_cast<int32_t *>(sk + QS_MAXP);
-  int32_t *scnt = sv + QS_MAXP;  // per-bucket counters (ranks)
+  int32_t *scnt = sv + QS_MAXP;  // per-bucket counters / scan scratch
+  int32_t *sbk = scnt + QS_MAXP;  // bucket of each request (block 0)
   __shared__ int32_t swarp[32];
-  __shared__ int32_t s_nb, s_nlong;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + tid, gs = (int64_t)gridDim.x * blockDim.x;
+  const bool b0 = blockIdx.x == 0;
   const int64_t P = A.P;
-  // skeleton entries beyond the preallocated buffers (aligned / rank scratch,
-  // or more pairs than half the pair table): the host redoes the round
-  if (A.off[P] > A.aligned_cap || 2 * A.off[P] > A.ptab_mask + 1) {
-    if (tid == 0) A.counts[3] = 1;
+  const int64_t nsk = A.off[P];
+  // skeleton entries beyond the preallocated buffers: the host redoes the round
+  // (uniform over the grid: every thread reads the same values)
+  if (nsk > A.aligned_cap || 2 * nsk > A.ptab_cap) {
+    if (gt == 0) A.counts[3] = 1;
     return;
   }
-  if (tid == 0) s_nlong = 0;
+  int64_t pm = 64;  // pair table in use: load factor <= 1/2
+  while (pm < 2 * nsk) pm <<= 1;
+  const uint64_t pmask = (uint64_t)pm - 1;
+  QS_TS(0);
   // 0. reset what the previous round touched; clear the tables
   const int32_t prevn = A.touched_n[1];
-  for (int i = tid; i < prevn; i += nt) {
+  for (int64_t i = gt; i < prevn; i += gs) {
     const int32_t s = A.prev_touched[i];
     A.g[s] = 0;
     A.a[s] = 0;
@@ -261,56 +419,41 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
     A.prio[s] = 0.0;
     A.dom[s] = 0;
   }
-  for (int64_t i = tid; i <= A.btab_mask; i += nt) {
+  for (int64_t i = gt; i <= A.btab_mask; i += gs) {
     A.btab_key[i] = QS_EMPTY;
     A.btab_min[i] = 0x7fffffff;
   }
-  for (int64_t i = tid; i <= A.ptab_mask; i += nt) {
+  for (int64_t i = gt; i < pm; i += gs) {
     A.ptab_key[i] = QS_EMPTY;
     A.ptab_cnt[i] = 0;
   }
-  if (tid == 0) A.touched_n[0] = 0;
-  __syncthreads();
-  // 1. counters g (pending) and a (active), once per distinct segment (83-89)
+  if (gt == 0) A.touched_n[0] = 0;
+  qs_gsync();
+  QS_TS(1);
+  // 1. counters g (pending) and a (active), once per distinct segment (83-89),
+  // and the touched list (prio's bit pattern doubles as the "listed" flag)
   for (int pass = 0; pass < 2; pass++) {
     const int64_t n = pass == 0 ? P : A.A;
     const int64_t *off = pass == 0 ? A.off : A.aoff;
     const int32_t *sk_ = pass == 0 ? A.sk : A.ask;
     int32_t *cnt = pass == 0 ? A.g : A.a;
-    for (int64_t i = tid; i < n; i += nt) {
-      const int64_t b = off[i], e = off[i + 1];
-      for (int64_t j = b; j < e; j++) {
-        const int32_t s = sk_[j];
-        bool dup = false;
-        for (int64_t q = b; q < j && !dup; q++) dup = sk_[q] == s;
-        if (!dup) atomicAdd(&cnt[s], 1);
-      }
-    }
-    __syncthreads();
-  }
-  // touched list: every segment appearing in pending or active skeletons
-  // (marked through prio = -1 as a temporary flag, then compacted)
-  for (int pass = 0; pass < 2; pass++) {
-    const int64_t n = pass == 0 ? P : A.A;
-    const int64_t *off = pass == 0 ? A.off : A.aoff;
-    const int32_t *sk_ = pass == 0 ? A.sk : A.ask;
-    for (int64_t i = tid; i < n; i += nt) {
-      for (int64_t j = off[i]; j < off[i + 1]; j++) {
-        const int32_t s = sk_[j];
-        if (atomicCAS((unsigned long long *)&A.prio[s], 0ull, 0xFFF0000000000001ull) == 0ull) {
-          const int32_t p = atomicAdd(&A.touched_n[0], 1);
-          A.touched[p] = s;
-        }
-      }
+    for (int64_t i = gt; i < n; i += gs) {
+      qs_distinct(sk_, off[i], off[i + 1], [&](int32_t s) {
+        atomicAdd(&cnt[s], 1);
+        unsigned long long *f = (unsigned long long *)&A.prio[s];
+        if (__ldcg(f) == 0ull && atomicCAS(f, 0ull, 0xFFF0000000000001ull) == 0ull)
+          A.touched[atomicAdd(&A.touched_n[0], 1)] = s;
+      });
     }
   }
-  __syncthreads();
-  // 2. front alignment + order-sensitive signature (109-143)
-  for (int64_t i = tid; i < P; i += nt) {
+  qs_gsync();
+  QS_TS(2);
+  // 2. front alignment + order-sensitive signature (109-143), bucket insert
+  for (int64_t i = gt; i < P; i += gs) {
     const int64_t b = A.off[i];
     const int k = (int)(A.off[i + 1] - b);
-    if (k > QS_MAXK) {  // aligned below by the whole block
-      A.longl[atomicAdd(&s_nlong, 1)] = (int32_t)i;
+    if (k > QS_MAXK) {  // aligned below by a whole block
+      A.longl[atomicAdd((unsigned long long *)&A.counts[4], 1ull)] = (int32_t)i;
       continue;
     }
     int32_t s[QS_MAXK], al[QS_MAXK];
@@ -332,194 +475,202 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
         ord[q] = j;
       }
       const int f = (int)(c.front < k ? c.front : k);
-      uint64_t chosen = 0;
+      uint32_t chosen = 0;
       int w = 0;
       for (int q = 0; q < f; q++) {
         al[w++] = s[ord[q]];
-        chosen |= 1ull << ord[q];
+        chosen |= 1u << ord[q];
       }
       for (int j = 0; j < k; j++)
-        if (!((chosen >> j) & 1ull)) al[w++] = s[j];
+        if (!((chosen >> j) & 1u)) al[w++] = s[j];
     }
     for (int j = 0; j < k; j++) A.aligned[b + j] = al[j];
     int sl = 0;
     if (k > 0) {
-      double pa[QS_MAXK];
-      for (int j = 0; j < k; j++) {
-        pa[j] = qpri0(c, A.g, A.a, al[j]);
+      for (int j = 0; j < k; j++) {  // ranks over the aligned order (p by position)
+        p[j] = qpri0(c, A.g, A.a, al[j]);
         int q = j;
-        while (q > 0 && qrank_before(pa[j], al[j], j, pa[ord[q - 1]], al[ord[q - 1]], ord[q - 1])) {
+        while (q > 0 && qrank_before(p[j], al[j], j, p[ord[q - 1]], al[ord[q - 1]], ord[q - 1])) {
           ord[q] = ord[q - 1];
           q--;
         }
         ord[q] = j;
       }
       const int kk = (int)(c.kappa < k ? c.kappa : k);
-      uint64_t chosen = 0;
-      for (int q = 0; q < kk; q++) chosen |= 1ull << ord[q];
+      uint32_t chosen = 0;
+      for (int q = 0; q < kk; q++) chosen |= 1u << ord[q];
       for (int j = 0; j < k; j++)
-        if ((chosen >> j) & 1ull) A.sig[i * c.kappa + sl++] = al[j];
+        if ((chosen >> j) & 1u) A.sig[i * c.kappa + sl++] = al[j];
     }
     A.siglen[i] = sl;
     qs_bucket_insert(A, c, i, sl);  // 3.
   }
-  __syncthreads();
-  for (int t = 0; t < s_nlong; t++) {  // skeletons longer than QS_MAXK
-    const int64_t i = A.longl[t];
-    const int64_t b = A.off[i];
-    const int sl = align_long_block(A.sk + b, (int)(A.off[i + 1] - b), A.reo[i] != 0, A.g, A.a, c.wg, c.wa,
-                                    c.front, c.kappa, A.aligned + b, A.sig + i * c.kappa, A.rk);
-    if (tid == 0) {
-      A.siglen[i] = sl;
-      qs_bucket_insert(A, c, i, sl);
-    }
-  }
-  __syncthreads();
-  // 4. bucket creation order = order of first members: scan of "is first" flags
-  for (int64_t i = tid; i < P; i += nt) A.bidx[i] = A.btab_min[A.slot_of[i]] == (int32_t)i ? 1 : 0;
-  __syncthreads();
-  const int32_t nb = block_exscan(A.bidx, (int)P, swarp);
-  if (tid == 0) s_nb = nb;
-  for (int64_t i = tid; i < P; i += nt) {
-    const int32_t first = A.btab_min[A.slot_of[i]];
-    A.bucket[i] = first;  // temporarily: first member index
-  }
-  __syncthreads();
-  for (int64_t i = tid; i < P; i += nt) A.bucket[i] = A.bidx[A.bucket[i]];
-  for (int b = tid; b < nb; b += nt) scnt[b] = 0;
-  __syncthreads();
-  // 5. rank inside the bucket, in pending order: warp 0 walks P in order
-  if (tid < 32) {
-    const int lane = tid;
-    for (int64_t base = 0; base < P; base += 32) {
-      const int64_t i = base + lane;
-      const int32_t b = i < P ? A.bucket[i] : -1 - lane;
-      const unsigned peers = __match_any_sync(0xffffffffu, b);
-      const int32_t before = __popc(peers & ((1u << lane) - 1u));
-      int32_t r = 0;
-      if (i < P) r = scnt[b] + before;
-      __syncwarp();
-      if (i < P) {
-        A.rank[i] = r;
-        if (lane == 31 - __clz(peers)) scnt[b] = r + 1;  // highest lane of the group
+  qs_gsync();
+  const int64_t nlong = (int64_t)__ldcg((const unsigned long long *)&A.counts[4]);
+  if (nlong > 0) {  // skeletons longer than QS_MAXK: one block each
+    for (int64_t t = blockIdx.x; t < nlong; t += gridDim.x) {
+      const int64_t i = A.longl[t];
+      const int64_t b = A.off[i];
+      const int sl = align_long_block(A.sk + b, (int)(A.off[i + 1] - b), A.reo[i] != 0, A.g, A.a, c.wg, c.wa,
+                                      c.front, c.kappa, A.aligned + b, A.sig + i * c.kappa, A.rk + b);
+      __threadfence();  // the block's aligned / sig writes, before thread 0 publishes
+      __syncthreads();
+      if (tid == 0) {
+        A.siglen[i] = sl;
+        qs_bucket_insert(A, c, i, sl);
       }
-      __syncwarp();
+      __syncthreads();
     }
+    qs_gsync();
   }
-  __syncthreads();
-  for (int b = tid; b < nb; b += nt) {
-    A.bsize[b] = scnt[b];
-    A.nsegs[b] = 0;
-    A.isum[b] = 0;
+  QS_TS(3);
+  // 4. (block 0) bucket creation order = order of first members; in-bucket
+  // ranks in pending order (211-223)
+  if (b0) {
+    for (int64_t i = tid; i < P; i += blockDim.x) {
+      const int32_t first = qs_ld(&A.btab_min[qs_ld(&A.slot_of[i])]);
+      sbk[i] = first;
+      scnt[i] = first == (int32_t)i ? 1 : 0;
+    }
+    __syncthreads();
+    const int32_t nb = block_exscan(scnt, (int)P, swarp);
+    for (int64_t i = tid; i < P; i += blockDim.x) sbk[i] = scnt[sbk[i]];
+    __syncthreads();
+    for (int b = tid; b < nb; b += blockDim.x) scnt[b] = 0;
+    __syncthreads();
+    if (tid < 32) {  // warp 0 walks P in order
+      const int lane = tid;
+      for (int64_t base = 0; base < P; base += 32) {
+        const int64_t i = base + lane;
+        const int32_t b = i < P ? sbk[i] : -1 - lane;
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        const int32_t before = __popc(peers & ((1u << lane) - 1u));
+        const int32_t r = i < P ? scnt[b] + before : 0;
+        __syncwarp();
+        if (i < P) {
+          A.rank[i] = r;
+          if (lane == 31 - __clz(peers)) scnt[b] = r + 1;  // highest lane of the group
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int64_t i = tid; i < P; i += blockDim.x) A.bucket[i] = sbk[i];
+    for (int b = tid; b < nb; b += blockDim.x) {
+      A.bsize[b] = scnt[b];
+      A.nsegs[b] = 0;
+      A.isum[b] = 0;
+    }
+    if (tid == 0) A.counts[2] = nb;
   }
-  __syncthreads();
+  qs_gsync();
+  QS_TS(4);
   // 7. distinct (bucket, segment) pairs; provisional = first hot_cap members (146-171)
   const int64_t hot_cap = c.budget - c.cold;
-  for (int64_t i = tid; i < P; i += nt) {
-    const int64_t b0 = A.off[i], e0 = A.off[i + 1];
+  for (int64_t i = gt; i < P; i += gs) {
     const int32_t bk = A.bucket[i];
     const int prov = A.rank[i] < hot_cap ? 1 : 0;
-    for (int64_t j = b0; j < e0; j++) {
-      const int32_t s = A.sk[j];
-      bool dup = false;
-      for (int64_t q = b0; q < j && !dup; q++) dup = A.sk[q] == s;
-      if (dup) continue;
+    qs_distinct(A.sk, A.off[i], A.off[i + 1], [&](int32_t s) {
       const uint64_t key = ((uint64_t)(uint32_t)bk << 32) | (uint32_t)s;
-      uint64_t pos = qmix64(key) & (uint64_t)A.ptab_mask;
+      uint64_t pos = qmix64(key) & pmask;
       for (;;) {
-        const unsigned long long prev = atomicCAS((unsigned long long *)&A.ptab_key[pos], QS_EMPTY, key);
-        if (prev == QS_EMPTY) atomicAdd(&A.nsegs[bk], 1);
+        unsigned long long *slot = (unsigned long long *)&A.ptab_key[pos];
+        unsigned long long prev = __ldcg(slot);
+        if (prev == QS_EMPTY) {
+          prev = atomicCAS(slot, QS_EMPTY, key);
+          if (prev == QS_EMPTY) {
+            atomicAdd(&A.nsegs[bk], 1);
+            A.plist[atomicAdd((unsigned long long *)&A.counts[5], 1ull)] = (int32_t)pos;
+          }
+        }
         if (prev == QS_EMPTY || prev == key) {
           if (prov) atomicAdd(&A.ptab_cnt[pos], 1);
           break;
         }
-        pos = (pos + 1) & (uint64_t)A.ptab_mask;
+        pos = (pos + 1) & pmask;
       }
-    }
+    });
   }
-  __syncthreads();
-  // 8. utility terms, summed exactly (integral by construction)
-  for (int64_t p = tid; p <= A.ptab_mask; p += nt) {
-    const uint64_t key = A.ptab_key[p];
-    if (key == QS_EMPTY) continue;
+  qs_gsync();
+  QS_TS(5);
+  // 8. utility terms of the distinct pairs, summed exactly (integral weights)
+  const int64_t npairs = (int64_t)__ldcg((const unsigned long long *)&A.counts[5]);
+  for (int64_t t = gt; t < npairs; t += gs) {
+    const int32_t pos = A.plist[t];
+    const uint64_t key = __ldcg((const unsigned long long *)&A.ptab_key[pos]);
     const int32_t bk = (int32_t)(key >> 32), s = (int32_t)(key & 0xffffffffu);
     const double t1 = __dmul_rn(c.wg, (double)A.g[s]);
     const double t2 = __dmul_rn(c.wa, (double)A.a[s]);
-    const double t3 = __dmul_rn(c.wn, (double)A.ptab_cnt[p]);
+    const double t3 = __dmul_rn(c.wn, (double)qs_ld(&A.ptab_cnt[pos]));
     atomicAdd((unsigned long long *)&A.isum[bk], (unsigned long long)(long long)__dadd_rn(__dadd_rn(t1, t2), t3));
   }
-  __syncthreads();
-  // 9. scores, and the (-score, creation order) sort keys
-  for (int b = tid; b < nb; b += nt) {
-    const int32_t ns = A.nsegs[b];
-    const double util = ns > 0 ? __ddiv_rn((double)A.isum[b], (double)ns) : 0.0;
-    const double sc = __dadd_rn(__dmul_rn(c.alpha, (double)A.bsize[b]), __dmul_rn(c.beta, util));
-    A.score[b] = sc;
-    sk[b] = {qord(-sc), (uint64_t)b};
-    sv[b] = b;
+  qs_gsync();
+  QS_TS(6);
+  // 9. (block 0) scores, the (-score, creation order) sort (234), hot-lane
+  // prefix sums of bucket sizes in that order (235-240)
+  const int32_t nb = (int32_t)__ldcg((const unsigned long long *)&A.counts[2]);
+  if (b0) {
+    for (int b = tid; b < nb; b += blockDim.x) {
+      const int32_t ns = qs_ld(&A.nsegs[b]);
+      const long long is = (long long)__ldcg((const unsigned long long *)&A.isum[b]);
+      const double util = ns > 0 ? __ddiv_rn((double)is, (double)ns) : 0.0;
+      const double sc = __dadd_rn(__dmul_rn(c.alpha, (double)A.bsize[b]), __dmul_rn(c.beta, util));
+      A.score[b] = sc;
+      sk[b] = {qord(-sc), (uint64_t)b};
+      sv[b] = b;
+    }
+    __syncthreads();
+    block_bitonic(sk, sv, nb);
+    for (int q = tid; q < nb; q += blockDim.x) scnt[q] = A.bsize[sv[q]];
+    __syncthreads();
+    block_exscan(scnt, nb, swarp);
+    for (int q = tid; q < nb; q += blockDim.x) {
+      const int32_t b = sv[q];
+      int64_t take = hot_cap - scnt[q];
+      take = take < 0 ? 0 : (take > A.bsize[b] ? A.bsize[b] : take);
+      A.nsegs[b] = (int32_t)take;                         // reuse: take
+      A.isum[b] = scnt[q] < hot_cap ? scnt[q] : hot_cap;  // reuse: base
+    }
   }
-  __syncthreads();
-  block_bitonic(sk, sv, nb);  // 234
-  // 10. hot lane by prefix sums of bucket sizes in sorted order (235-240)
-  for (int q = tid; q < nb; q += nt) scnt[q] = A.bsize[sv[q]];
-  __syncthreads();
-  block_exscan(scnt, nb, swarp);
-  for (int q = tid; q < nb; q += nt) {
-    const int32_t b = sv[q];
-    int64_t take = hot_cap - scnt[q];
-    take = take < 0 ? 0 : (take > A.bsize[b] ? A.bsize[b] : take);
-    A.nsegs[b] = (int32_t)take;                                        // reuse: take
-    A.isum[b] = scnt[q] < hot_cap ? scnt[q] : hot_cap;                 // reuse: base
-  }
-  __syncthreads();
-  for (int64_t i = tid; i < P; i += nt) {
+  qs_gsync();
+  QS_TS(7);
+  // 10. hot lane, and n_disp of its members (247-248)
+  for (int64_t i = gt; i < P; i += gs) {
     const int32_t b = A.bucket[i];
-    const bool h = A.rank[i] < A.nsegs[b];
-    A.bidx[i] = h ? 1 : 0;  // reuse: selected flag
-    if (h) A.hot[A.isum[b] + A.rank[i]] = i;
+    const bool h = A.rank[i] < qs_ld(&A.nsegs[b]);
+    A.bidx[i] = h ? 1 : 0;  // reuse: hot flag
+    if (h) {
+      A.hot[(int64_t)__ldcg((const unsigned long long *)&A.isum[b]) + A.rank[i]] = i;
+      qs_distinct(A.sk, A.off[i], A.off[i + 1], [&](int32_t s) { atomicAdd(&A.nd[s], 1); });
+    }
   }
-  __syncthreads();
-  // 11. cold lane: leftovers by (arrival, id), the oldest cold_quota (242-245)
+  qs_gsync();
+  QS_TS(8);
+  // 11. (block 0) cold lane: the oldest cold_quota leftovers by (arrival, id)
   const int64_t nh = hot_cap < P ? (hot_cap > 0 ? hot_cap : 0) : P;
   const int64_t nc = c.cold < P - nh ? c.cold : P - nh;
   if (nc > 0) {
-    for (int64_t i = tid; i < P; i += nt) {
-      const uint64_t sel = A.bidx[i] ? 1ull : 0ull;
-      // (selected, arrival) in hi (arrival order-preserving map, top bit for selected)
-      const uint64_t ar = qord(A.arrival[i]);
-      sk[i] = {sel ? ~0ull : ar, (uint64_t)A.ids[i] ^ 0x8000000000000000ull};
-      sv[i] = (int32_t)i;
-    }
-    __syncthreads();
-    block_bitonic(sk, sv, (int)P);
-    for (int64_t q = tid; q < nc; q += nt) A.cold[q] = sv[q];
-    __syncthreads();
+    if (b0) qs_cold_lane(A, c, P, nc, sk, sv, scnt, swarp);
+    qs_gsync();
   }
-  // 12. dispatch counters n over hot + cold, priorities over the domain (247-251)
-  for (int64_t q = tid; q < nh + nc; q += nt) {
-    const int64_t i = q < nh ? A.hot[q] : A.cold[q - nh];
-    const int64_t b0 = A.off[i], e0 = A.off[i + 1];
-    for (int64_t j = b0; j < e0; j++) {
-      const int32_t s = A.sk[j];
-      bool dup = false;
-      for (int64_t r = b0; r < j && !dup; r++) dup = A.sk[r] == s;
-      if (!dup) atomicAdd(&A.nd[s], 1);
-    }
-  }
-  __syncthreads();
-  const int32_t nt_ = A.touched_n[0];
-  for (int i = tid; i < nt_; i += nt) {
+  QS_TS(9);
+  // 12. priorities over the domain (249-251)
+  const int32_t ntouch = qs_ld(&A.touched_n[0]);
+  for (int64_t i = gt; i < ntouch; i += gs) {
     const int32_t s = A.touched[i];
-    const bool in = A.g[s] > 0 || A.a[s] > 0 || A.nd[s] > 0;
+    const int32_t g = A.g[s], a = A.a[s], n = qs_ld(&A.nd[s]);
+    const bool in = g > 0 || a > 0 || n > 0;
     A.dom[s] = in ? 1 : 0;
-    A.prio[s] = in ? __dadd_rn(qpri0(c, A.g, A.a, s), __dmul_rn(c.wn, (double)A.nd[s])) : 0.0;
+    A.prio[s] = in ? __dadd_rn(__dadd_rn(__dmul_rn(c.wg, (double)g), __dmul_rn(c.wa, (double)a)),
+                               __dmul_rn(c.wn, (double)n))
+                   : 0.0;
   }
-  if (tid == 0) {
+  if (gt == 0) {
     A.counts[0] = nh;
     A.counts[1] = nc;
-    A.counts[2] = s_nb;
-    A.touched_n[1] = nt_;  // this round's list is the next round's reset list
+    A.touched_n[1] = ntouch;  // this round's list is the next round's reset list
   }
+  QS_TS(10);
 }
 
 }  // namespace qsmall

@@ -57,6 +57,32 @@ class DeviceScheduler:
         max_p = (1 if on else 0) if isinstance(on, bool) else int(on)
         check(self._L.prism_qas_set_small(self._h, max_p))
 
+    _TUNE = {"max_p": 0, "grid": 1, "per_cta": 2}
+
+    def tune(self, **kw) -> None:
+        """One-launch round shape: max_p, grid (CTAs, 0 = auto), per_cta."""
+        self._L.prism_qas_tune.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p]
+        for k, v in kw.items():
+            check(self._L.prism_qas_tune(self._h, self._TUNE[k], int(v), None))
+
+    def last_grid(self) -> int:
+        """CTAs of the last one-launch round."""
+        out = C.c_int64(0)
+        self._L.prism_qas_tune.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p]
+        check(self._L.prism_qas_tune(self._h, 3, 0, C.addressof(out)))
+        return int(out.value)
+
+    def profile(self, on: bool) -> None:
+        self._L.prism_qas_profile.argtypes = [C.c_void_p, C.c_int32]
+        check(self._L.prism_qas_profile(self._h, 1 if on else 0))
+
+    def small_timeline(self) -> list[int]:
+        """ns from kernel start to the end of each one-CTA phase (last profiled round)."""
+        out = np.zeros(11, np.int64)
+        self._L.prism_qas_small_timeline.argtypes = [C.c_void_p, C.c_void_p, C.c_int32]
+        check(self._L.prism_qas_small_timeline(self._h, out.ctypes.data, 11))
+        return [int(x) for x in out]
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             self._L.prism_qas_destroy(self._h)

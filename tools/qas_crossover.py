@@ -35,20 +35,32 @@ def round_inputs(P, nseg, rng):
 def main():
     rng = np.random.default_rng(0)
     ds = DeviceScheduler()
-    for P in (64, 256, 512, 1024, 1536, 2048, 3072, 4096):
+    def timed(m, cfg, n=40):
+        for _ in range(5):
+            ds.round_arrays(m, cfg)
+        t0 = time.perf_counter()
+        for _ in range(n):
+            ds.round_arrays(m, cfg)
+        return round((time.perf_counter() - t0) / n * 1e6, 1)
+
+    for P in (64, 256, 512, 1024, 2048, 3072, 4096):
         pend, act = round_inputs(P, 981, rng)
-        cfg = SchedulerConfig(dispatch_budget=min(P, 512), cold_quota=min(P, 8))
+        cfg = SchedulerConfig(dispatch_budget=min(P, 4096), cold_quota=min(P, 64))
         m = marshal_round(pend, act)
         out = {"P": P}
-        for name, cut in (("one_cta", 4096), ("multi", 0)):
-            ds.set_small(cut)
-            for _ in range(5):
-                ds.round_arrays(m, cfg)
-            n = 40
-            t0 = time.perf_counter()
-            for _ in range(n):
-                ds.round_arrays(m, cfg)
-            out[name + "_us"] = round((time.perf_counter() - t0) / n * 1e6, 1)
+        ds.set_small(0)
+        out["multi_us"] = timed(m, cfg)
+        ds.set_small(4096)
+        for G in (1, 8, 32, 74, 148, 0):
+            ds.tune(grid=G)
+            out[f"grid{G or 'auto'}_us"] = timed(m, cfg)
+        ds.tune(grid=0)
+        ds.profile(True)
+        ds.round_arrays(m, cfg)
+        ts = ds.small_timeline()
+        ds.profile(False)
+        out["auto_grid"] = ds.last_grid()
+        out["auto_phases_us"] = [round((b - a) / 1e3, 1) for a, b in zip(ts, ts[1:])]
         print(json.dumps(out), flush=True)
 
 
