@@ -25,7 +25,12 @@ namespace cg = cooperative_groups;
 constexpr int COOP_TPB = 512;
 constexpr int COOP_ROUNDS = 14;
 constexpr int CHUNK = 4096;  // bitonic chunk per CTA (shared memory)
-constexpr size_t COOP_SMEM = (sizeof(Key3) + sizeof(uint64_t)) * CHUNK;
+// sample select (coop_sample_select)
+constexpr int SS_SAMP = 8192;  // samples at most
+constexpr int SS_SPL = 1536;   // splitters (selected samples) at most
+constexpr int SS_U = 2048;     // undecided samples kept as a list (more: flags only)
+constexpr size_t COOP_SORT_SMEM = (sizeof(Key3) + sizeof(uint64_t)) * CHUNK;
+constexpr size_t COOP_SMEM = COOP_SORT_SMEM;
 
 struct CoopState {
   unsigned long long cand;  // gathered candidates
@@ -34,6 +39,18 @@ struct CoopState {
   unsigned long long hist_n[COOP_ROUNDS + 2][256];
   unsigned long long hist_w[COOP_ROUNDS + 2][256];
   long long prot_n;  // protection: number protected
+  // sample-select (coop_sample_select)
+  unsigned long long ss_ns;     // samples
+  unsigned long long ss_n;      // items <= tau
+  unsigned long long ss_mass;   // their weight
+  unsigned long long ss_cand;   // all candidates
+  unsigned int ss_cnt[SS_SPL];  // per-bucket counts
+  unsigned int ss_cur[SS_SPL];  // per-bucket scatter cursors
+  unsigned int ss_off[SS_SPL + 4];  // bucket offsets
+  int ss_ok;                    // the sample select produced the sorted prefix
+  unsigned long long ss_dbg[24];  // diagnostics: [0] max bucket, [1] rounds, [2+3r..] (undecided, selected, shift)
+  int ss_nb;                    // diagnostics: splitters of the last sample select
+  int ss_fail;                  // diagnostics: why it fell back (0: it did not)
   int nts;
   // ---- not cleared per launch (the host clears up to offsetof(ts))
   unsigned long long ts[40];  // phase timeline (%globaltimer ns), CTA 0 thread 0
@@ -58,20 +75,38 @@ struct CoopBufs {
   int64_t *out_ids;  // protection: ids of the protected nodes (may be null)
 };
 
+__device__ inline Key3 shfl_key(const Key3 &k, int o) {
+  return {__shfl_xor_sync(0xffffffffu, k.w0, o), __shfl_xor_sync(0xffffffffu, k.w1, o),
+          __shfl_xor_sync(0xffffffffu, k.w2, o)};
+}
+
+// block min/max of Key3 (warp shuffles, then the warp results): written to
+// *gmin / *gmax by thread 0; smin/smax hold >= 32 entries of scratch
 __device__ inline void block_minmax(Key3 lo, Key3 hi, Key3 *smin, Key3 *smax, Key3 *gmin, Key3 *gmax) {
-  smin[threadIdx.x] = lo;
-  smax[threadIdx.x] = hi;
-  __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      if (key_less(smin[threadIdx.x + s], smin[threadIdx.x])) smin[threadIdx.x] = smin[threadIdx.x + s];
-      if (key_less(smax[threadIdx.x], smax[threadIdx.x + s])) smax[threadIdx.x] = smax[threadIdx.x + s];
-    }
-    __syncthreads();
+  for (int o = 16; o > 0; o >>= 1) {
+    const Key3 a = shfl_key(lo, o), b = shfl_key(hi, o);
+    if (key_less(a, lo)) lo = a;
+    if (key_less(hi, b)) hi = b;
   }
-  if (threadIdx.x == 0) {
-    *gmin = smin[0];
-    *gmax = smax[0];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    smin[wid] = lo;
+    smax[wid] = hi;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    lo = lane < nw ? smin[lane] : Key3{~0ull, ~0ull, ~0ull};
+    hi = lane < nw ? smax[lane] : Key3{0, 0, 0};
+    for (int o = 16; o > 0; o >>= 1) {
+      const Key3 a = shfl_key(lo, o), b = shfl_key(hi, o);
+      if (key_less(a, lo)) lo = a;
+      if (key_less(hi, b)) hi = b;
+    }
+    if (lane == 0) {
+      *gmin = lo;
+      *gmax = hi;
+    }
   }
   __syncthreads();
 }
@@ -379,30 +414,811 @@ __device__ void coop_sort(cg::grid_group &grid, const CoopBufs &B, int64_t n, Ke
   grid.sync();
 }
 
-// the eviction-order build after keys / subtree maxima / gather (full-
-// occupancy kernels k_build_keys, k_propagate, k_gather, which leave the
-// candidate count in st->cand): selection of the consumable prefix + its sort
-// + list ready -- one cooperative launch, no host round trip.
+// ------------------------------------------------------------ sample select
+// The smallest-key prefix of weight >= W of the candidates defined over the
+// slots [0, hw) by cand(s, key, val, w), sorted, into (kout, vout) -- without
+// materialising the candidates:
+//   1. one slot at a hashed offset in every m-slot window is sampled (m: the
+//      power of two that keeps the sample <= SS_SAMP);
+//   2. CTA 0 selects the sample prefix whose mass, scaled by m, reaches 1.25 W
+//      plus three samples of slack (radix rounds over the undecided samples,
+//      then an exact sort of the last few) and sorts it: the splitters; tau =
+//      the largest;
+//   3. one pass over all slots keeps the candidates with key <= tau -- exactly
+//      a prefix of the order, whatever the sample looked like -- each with its
+//      bucket (#splitters below it: buckets of ~m candidates);
+//   4. bucket offsets by a scan, a scatter into bucket order, and one shared-
+//      memory bitonic sort per bucket.
+// Returns false (nothing written to kout/vout) when the sample cannot promise
+// the prefix, the pass shows it fell short (mass < W and not every candidate
+// kept) or a bucket overflows shared memory; the caller then runs the
+// materialising selection.  Uniform over the grid.
+__device__ inline void bitonic_smem(Key3 *sk, uint64_t *sv, int m) {
+  for (int size = 2; size <= m; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int p = threadIdx.x; p < (m >> 1); p += blockDim.x) {
+        const int i = 2 * stride * (p / stride) + (p % stride), j = i + stride;
+        const bool up = (i & size) == 0;
+        if (up ? key_less(sk[j], sk[i]) : key_less(sk[i], sk[j])) {
+          const Key3 tk = sk[i];
+          sk[i] = sk[j];
+          sk[j] = tk;
+          const uint64_t tv = sv[i];
+          sv[i] = sv[j];
+          sv[j] = tv;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ inline void bitonic_keys(Key3 *sk, int m) {
+  for (int size = 2; size <= m; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int p = threadIdx.x; p < (m >> 1); p += blockDim.x) {
+        const int i = 2 * stride * (p / stride) + (p % stride), j = i + stride;
+        const bool up = (i & size) == 0;
+        if (up ? key_less(sk[j], sk[i]) : key_less(sk[i], sk[j])) {
+          const Key3 tk = sk[i];
+          sk[i] = sk[j];
+          sk[j] = tk;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// exclusive scan of a[0..n) in shared memory, returns the total
+__device__ inline unsigned long long block_exscan_u64(unsigned long long *a, int n, unsigned long long *warp_tot) {
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int b = threadIdx.x * per, e = min(b + per, n);
+  unsigned long long s = 0;
+  for (int i = b; i < e; i++) s += a[i];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long x = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    unsigned long long t = lane < nw ? warp_tot[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nw) warp_tot[lane] = t;  // inclusive warp prefix
+  }
+  __syncthreads();
+  unsigned long long run = x - s + (wid ? warp_tot[wid - 1] : 0);
+  const unsigned long long total = warp_tot[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  for (int i = b; i < e; i++) {
+    const unsigned long long v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  __syncthreads();
+  return total;
+}
+
+// block-wide reservation of c items per thread at *ctr (one global atomic per
+// CTA); returns this thread's first position.  Every thread calls it.
+__device__ inline unsigned long long block_reserve(unsigned c, unsigned long long *ctr, unsigned *s_w,
+                                                   unsigned long long *s_base) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned x = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[wid] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned run = 0;
+    for (int q = 0; q < nw; q++) {
+      const unsigned t = s_w[q];
+      s_w[q] = run;
+      run += t;
+    }
+    *s_base = run ? atomicAdd(ctr, (unsigned long long)run) : 0ull;
+  }
+  __syncthreads();
+  const unsigned long long pos = *s_base + s_w[wid] + (x - c);
+  __syncthreads();
+  return pos;
+}
+
+// ascending rank sort of n unique keys (+ values) in shared memory, written to
+// (ko, vo) -- items are ranked against all keys (broadcast reads, no
+// barriers), with tpi = blockDim / n threads (a power of two <= 32) per item
+// splitting the comparisons; for the small sets of the sample select
+__device__ inline void block_rank_sort(const Key3 *k, const uint64_t *v, int n, Key3 *ko, uint64_t *vo) {
+  int tpi = 1;
+  while (tpi < 32 && 2 * tpi * n <= (int)blockDim.x) tpi <<= 1;
+  const int sub = threadIdx.x & (tpi - 1);
+  const int per = (int)blockDim.x / tpi;
+  for (int i0 = 0; i0 < n; i0 += per) {  // uniform trip count (shuffles below)
+    const int i = i0 + (int)threadIdx.x / tpi;
+    const bool ok = i < n;
+    const Key3 x = ok ? k[i] : Key3{0, 0, 0};
+    int r = 0;
+    if (ok) {
+#pragma unroll 4
+      for (int j = sub; j < n; j += tpi) r += key_less(k[j], x) ? 1 : 0;
+    }
+    for (int o = 1; o < tpi; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (ok && sub == 0) {
+      ko[r] = x;
+      if (vo) vo[r] = v[i];
+    }
+  }
+}
+
+// ascending bitonic sort of blockDim.x (a power of two) items held one per
+// thread: thread t ends with the t-th smallest.  Strides below 32 exchange by
+// warp shuffles, larger ones through (sx, sv) in shared memory.
+__device__ inline void block_sort_reg(Key3 &key, uint64_t &val, Key3 *sx, uint64_t *svx) {
+  const int tid = threadIdx.x, N = blockDim.x;
+  for (int size = 2; size <= N; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      Key3 pk;
+      uint64_t pv;
+      if (stride >= 32) {
+        sx[tid] = key;
+        svx[tid] = val;
+        __syncthreads();
+        pk = sx[tid ^ stride];
+        pv = svx[tid ^ stride];
+        __syncthreads();
+      } else {
+        pk = shfl_key(key, stride);
+        pv = __shfl_xor_sync(0xffffffffu, val, stride);
+      }
+      const bool up = (tid & size) == 0, lower = (tid & stride) == 0;
+      const bool pless = key_less(pk, key);
+      if ((lower == up) ? pless : (!pless && key_less(key, pk))) {
+        key = pk;
+        val = pv;
+      }
+    }
+  }
+}
+
+// sort n <= blockDim.x keys (+ values) from (k, v) into (ko, vo) with the
+// register bitonic sort (ko/vo may alias k/v; sx/svx: blockDim.x scratch)
+__device__ inline void block_sort_small(const Key3 *k, const uint64_t *v, int n, Key3 *ko, uint64_t *vo, Key3 *sx,
+                                        uint64_t *svx) {
+  Key3 key = threadIdx.x < n ? k[threadIdx.x] : Key3{~0ull, ~0ull, ~0ull};
+  uint64_t val = (threadIdx.x < n && v) ? v[threadIdx.x] : 0ull;
+  __syncthreads();
+  block_sort_reg(key, val, sx, svx);
+  if (threadIdx.x < n) {
+    ko[threadIdx.x] = key;
+    if (vo) vo[threadIdx.x] = val;
+  }
+  __syncthreads();
+}
+
+// one radix round of CTA 0's sample selection over the undecided samples:
+// digit below the highest bit where the undecided keys differ, the weight
+// histogram, the crossing digit; lower digits join the selected keys, higher
+// ones are dropped, the crossing digit's samples stay undecided.  The
+// undecided set is either the list idx[0..nU) or (idx null) every sample with
+// flag 0 among ns; the next set is written as a list when it fits cap_nxt,
+// else kept in the flags only.  Global sample loads are batched SR_B per
+// thread (the sample lives in L2).
+struct SampleRound {
+  int nU_next;
+  bool listed;
+  long long below;
+  bool overflow;
+};
+constexpr int SR_B = 4;
+
+__device__ inline SampleRound sample_round(const Key3 *sk, const int64_t *sw, const int *idx, int nU, int ns,
+                                           uint8_t *flag, long long need, Key3 *selk, int *s_nsel, int *nxt,
+                                           int cap_nxt, Key3 *smin, Key3 *smax, unsigned *s_hn,
+                                           unsigned *s_hw, int *s_misc, long long *s_ll) {
+  const int lane = threadIdx.x & 31;
+  const int n = idx ? nU : ns;
+  const int step = SR_B * blockDim.x;
+  auto item = [&](int q) -> int {  // sample index of undecided position q, or -1
+    if (q >= n) return -1;
+    const int i = idx ? idx[q] : q;
+    return (idx || flag[i] == 0) ? i : -1;
+  };
+  Key3 lo = {~0ull, ~0ull, ~0ull}, hi = {0, 0, 0};
+  for (int q0 = threadIdx.x; q0 < n; q0 += step) {
+    Key3 kk[SR_B];
+    int ii[SR_B];
+#pragma unroll
+    for (int u = 0; u < SR_B; u++) {
+      ii[u] = item(q0 + u * blockDim.x);
+      if (ii[u] >= 0) kk[u] = sk[ii[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < SR_B; u++)
+      if (ii[u] >= 0) {
+        if (key_less(kk[u], lo)) lo = kk[u];
+        if (key_less(hi, kk[u])) hi = kk[u];
+      }
+  }
+  block_minmax(lo, hi, smin, smax, &smin[32], &smax[32]);
+  const Key3 gmin = smin[32], gmax = smax[32];
+  const Key3 xx = {gmin.w0 ^ gmax.w0, gmin.w1 ^ gmax.w1, gmin.w2 ^ gmax.w2};
+  const int hb = chighbit(xx);
+  const int shift = hb < 7 ? 0 : hb - 7;
+  for (int d = threadIdx.x; d < 256; d += blockDim.x) {
+    s_hn[d] = 0;
+    s_hw[d] = 0;
+  }
+  if (threadIdx.x == 0) s_misc[1] = 0;  // next-list count
+  __syncthreads();
+  {  // per-thread run-length aggregation (samples crowd few digits), warp-aggregated flushes
+    uint32_t cd = 256u;
+    unsigned cn = 0, cw = 0;
+    auto flush = [&]() {
+      const uint32_t d0 = __shfl_sync(0xffffffffu, cd, 0);
+      const unsigned same = __ballot_sync(0xffffffffu, cd == d0);
+      if (same == 0xffffffffu) {  // the common case: one digit across the warp
+        unsigned a = cn, b = cw;
+        for (int o = 16; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        if (lane == 0 && d0 < 256u && a) {
+          atomicAdd(&s_hn[d0], a);
+          atomicAdd(&s_hw[d0], b);
+        }
+      } else if (cd < 256u && cn) {
+        atomicAdd(&s_hn[cd], cn);
+        atomicAdd(&s_hw[cd], cw);
+      }
+    };
+    for (int q0 = threadIdx.x; q0 - (int)threadIdx.x < n; q0 += step) {  // warp-uniform trip count
+      uint32_t dd[SR_B];
+      unsigned ww[SR_B];
+#pragma unroll
+      for (int u = 0; u < SR_B; u++) {
+        const int i = item(q0 + u * blockDim.x);
+        dd[u] = i >= 0 ? cdigit(sk[i], shift) : 256u;
+        ww[u] = i >= 0 ? (unsigned)sw[i] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < SR_B; u++) {
+        if (dd[u] == 256u) continue;
+        if (dd[u] != cd) {
+          if (cd < 256u && cn) {
+            atomicAdd(&s_hn[cd], cn);
+            atomicAdd(&s_hw[cd], cw);
+          }
+          cd = dd[u];
+          cn = 0;
+          cw = 0;
+        }
+        cn++;
+        cw += ww[u];
+      }
+    }
+    flush();
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // crossing digit: the first whose cumulative weight reaches need
+    unsigned long long w8[8], run = 0;
+    for (int q = 0; q < 8; q++) {
+      run += s_hw[8 * lane + q];
+      w8[q] = run;
+    }
+    unsigned long long pre = run;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += y;
+    }
+    const unsigned long long before = pre - run;
+    int dl = 256;
+    for (int q = 0; q < 8; q++)
+      if ((long long)(before + w8[q]) >= need) {
+        dl = 8 * lane + q;
+        break;
+      }
+    const unsigned msk = __ballot_sync(0xffffffffu, dl < 256);
+    const int src = __ffs(msk) - 1;  // need <= mass of the undecided: some digit crosses
+    const int dstar = __shfl_sync(0xffffffffu, dl, src);
+    unsigned long long bb = 0;
+    if (lane == src) bb = before + ((dstar - 8 * src) ? w8[dstar - 8 * src - 1] : 0);
+    bb = __shfl_sync(0xffffffffu, bb, src);
+    if (lane == 0) {
+      s_misc[0] = dstar;
+      *s_ll = (long long)bb;
+    }
+  }
+  __syncthreads();
+  const int dstar = s_misc[0];
+  const int nnext = (int)s_hn[dstar];
+  const bool list = nnext <= cap_nxt;
+  bool ovf = false;
+  for (int q0 = threadIdx.x; q0 - (int)threadIdx.x < n; q0 += step) {  // warp-uniform trip count
+    Key3 kk[SR_B];
+    int ii[SR_B];
+#pragma unroll
+    for (int u = 0; u < SR_B; u++) {
+      ii[u] = item(q0 + u * blockDim.x);
+      if (ii[u] >= 0) kk[u] = sk[ii[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < SR_B; u++) {  // warp-aggregated appends (one atomic per warp and list)
+      const int i = ii[u];
+      const int d = i >= 0 ? (int)cdigit(kk[u], shift) : -1;
+      const bool below = i >= 0 && d < dstar, mid = i >= 0 && d == dstar;
+      if (i >= 0 && d > dstar) flag[i] = 2;
+      if (below) flag[i] = 1;
+      const unsigned mb = __ballot_sync(0xffffffffu, below), mm = __ballot_sync(0xffffffffu, mid && list);
+      int pb = 0, pm = 0;
+      if (lane == 0) {
+        if (mb) pb = atomicAdd(s_nsel, __popc(mb));
+        if (mm) pm = atomicAdd(&s_misc[1], __popc(mm));
+      }
+      pb = __shfl_sync(0xffffffffu, pb, 0) + __popc(mb & ((1u << lane) - 1u));
+      pm = __shfl_sync(0xffffffffu, pm, 0) + __popc(mm & ((1u << lane) - 1u));
+      if (below) {
+        if (pb < SS_SPL) selk[pb] = kk[u];
+        else ovf = true;
+      }
+      if (mid && list) nxt[pm] = i;
+    }
+  }
+  ovf = __syncthreads_or(ovf);
+  SampleRound r{nnext, list, *s_ll, ovf};
+  __syncthreads();
+  return r;
+}
+
+// candidate gather over the slots (the materialising path): cand(s) for every
+// slot s < hw into (B.k0, B.v0, B.w0); the count lands in st->cand
+template <class Cand>
+__device__ void coop_gather(const CoopBufs &B, int32_t hw, Cand cand) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t s0 = (int64_t)blockIdx.x * blockDim.x; s0 < hw; s0 += gsz) {
+    const int64_t s = s0 + threadIdx.x;
+    Key3 k;
+    uint64_t v;
+    int64_t w = 0;
+    const bool take = s < hw && cand((int32_t)s, k, v, w);
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (!m) continue;
+    unsigned long long b = 0;
+    if (lane == 0) b = atomicAdd(&B.st->cand, (unsigned long long)__popc(m));
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (take) {
+      const int64_t p = (int64_t)b + __popc(m & ((1u << lane) - 1u));
+      B.k0[p] = k;
+      B.v0[p] = v;
+      B.w0[p] = w;
+    }
+  }
+}
+
+// eviction-order candidate of slot s (after k_build_keys / k_propagate): every
+// live node whose subtree holds no blocked node, keyed (subtree max, deeper first)
+struct EvictCand {
+  DT T;
+  __device__ int32_t hw() const { return T.ctrl->hw; }
+  __device__ bool operator()(int32_t s, Key3 &k, uint64_t &v, int64_t &w) const {
+    const int32_t e = __ldg(&T.eff[s]);
+    if (e < 0) return false;
+    k = composite(T.kw[e], __ldg(&T.dend[s]));
+    v = ((uint64_t)__ldg(&T.kver[s]) << 32) | (uint32_t)s;
+    w = __ldg(&T.elen[s]);
+    return true;
+  }
+};
+
+// set_protection candidate (kvcache.py:370-381): live nodes holding a REUSABLE
+// anchor, keyed (-P-hat[seg], seg or -1, node_id); visiting a slot clears its
+// previous protection flag
+struct ProtCand {
+  DT T;
+  __device__ int32_t hw() const { return T.ctrl->hw; }
+  __device__ bool operator()(int32_t s, Key3 &k, uint64_t &v, int64_t &w) const {
+    T.prot[s] = 0;
+    if (s == ROOT || T.nid[s] < 0 || T.par[s] < 0 || !T.hasanc[s] || T.akind[s] != K_REUSABLE) return false;
+    const int32_t sg = T.seg[s];
+    const int32_t sv = sg == SEG_NONE ? -1 : sg;
+    k = {0, 0, 0};
+    shl_or(k, 64, ord_f64(-pri_of(T, sg)));
+    shl_or(k, 32, (uint64_t)((uint32_t)sv ^ 0x80000000u));
+    shl_or(k, 40, (uint64_t)T.nid[s] & ((1ull << 40) - 1));
+    v = (uint64_t)(uint32_t)s;
+    w = 1;
+    return true;
+  }
+};
+
+// ------------------------------------------------------------ sample select
+// The smallest-key prefix of weight >= W of the candidates cand(s) over the
+// slots [0, hw), sorted into (kout, vout), without materialising the
+// candidates -- five full-occupancy launches in stream order (no host round
+// trip), then the cooperative kernel finalises (or, when st->ss_ok is 0, runs
+// the materialising radix selection):
+//   k_ss_sample  one slot at a hashed offset in every m-slot window (m: the
+//                power of two that keeps the sample <= SS_SAMP);
+//   k_ss_select  one CTA: the sample prefix whose mass, scaled by m, reaches
+//                1.25 W + three samples of slack (radix rounds over the
+//                undecided samples, an exact sort of the last few), sorted:
+//                the splitters, tau = the largest;
+//   k_ss_filter  every slot: keep key <= tau -- exactly a prefix of the order,
+//                whatever the sample looked like -- with its bucket
+//                (#splitters below it; buckets of ~m candidates);
+//   k_ss_scatter bucket offsets; enough mass (or every candidate) and every
+//                bucket <= SS_BMAX? (st->ss_ok); scatter into bucket order;
+//   k_ss_sort    one CTA per bucket sorts it in shared memory.
+constexpr int SS_TPB = 256;
+constexpr int SS_SEL_TPB = 512;
+constexpr int SS_BMAX = 1024;  // largest bucket sorted in shared memory
+constexpr size_t SS_SEL_SMEM = 2 * sizeof(Key3) * SS_SPL + 8 * SS_U + 2 * (sizeof(Key3) + 8) * SS_SEL_TPB + SS_SAMP;
+constexpr size_t SS_FILTER_SMEM = sizeof(Key3) * SS_SPL + 4 * SS_SPL;
+constexpr size_t SS_SORT_SMEM = (sizeof(Key3) + 8) * SS_BMAX;
+
+__device__ inline int64_t ss_period(int32_t hw) {
+  int64_t m = 8;
+  while ((int64_t)hw > m * SS_SAMP) m <<= 1;
+  return m;
+}
+
+template <class Cand>
+__global__ void __launch_bounds__(SS_TPB) k_ss_sample(Cand cand, CoopBufs B, int64_t W, int64_t min_cand) {
+  __shared__ unsigned s_w[32];
+  __shared__ unsigned long long s_base;
+  const int32_t hw = cand.hw();
+  if (W <= 0 || hw <= min_cand) return;  // nothing sampled: k_ss_select gives up
+  const int64_t m = ss_period(hw), nsamp = ((int64_t)hw + m - 1) / m;
+  const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x; j0 < nsamp; j0 += gsz) {
+    const int64_t j = j0 + threadIdx.x;
+    Key3 k;
+    uint64_t v;
+    int64_t w;
+    // (a fixed offset in the window would alias with periodic slot layouts)
+    const int64_t s = j * m + (int64_t)(mix64((uint64_t)j ^ 0x9E3779B97F4A7C15ull) & (uint64_t)(m - 1));
+    const bool take = j < nsamp && s < hw && cand((int32_t)s, k, v, w);
+    const unsigned long long p = block_reserve(take ? 1u : 0u, &B.st->ss_ns, s_w, &s_base);
+    if (take) {
+      B.k1[p] = k;
+      B.w1[p] = w;
+    }
+  }
+}
+
+template <class Cand>
+__global__ void __launch_bounds__(SS_SEL_TPB) k_ss_select(Cand cand, CoopBufs B, int64_t W) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ Key3 smin[33], smax[33];
+  __shared__ unsigned s_hn[256];
+  __shared__ unsigned s_hw[256];
+  __shared__ unsigned long long s_u64[32];
+  __shared__ int s_misc[4];
+  __shared__ long long s_ll;
+  __shared__ int s_nsel;
+  CoopState *st = B.st;
+  const int lane = threadIdx.x & 31;
+  const int64_t m = ss_period(cand.hw());
+  Key3 *spl = reinterpret_cast<Key3 *>(dsm);          // [SS_SPL] sorted splitters
+  Key3 *selk = spl + SS_SPL;                          // [SS_SPL] selected sample keys, unsorted
+  int *ua = reinterpret_cast<int *>(selk + SS_SPL);   // [SS_U] undecided lists (ping-pong)
+  int *ub = ua + SS_U;
+  Key3 *fk = reinterpret_cast<Key3 *>(ub + SS_U);     // [blockDim] the last undecided; sort scratch
+  uint64_t *fw = reinterpret_cast<uint64_t *>(fk + SS_SEL_TPB);
+  Key3 *fk2 = reinterpret_cast<Key3 *>(fw + SS_SEL_TPB);
+  uint64_t *fw2 = reinterpret_cast<uint64_t *>(fk2 + SS_SEL_TPB);
+  uint8_t *flag = reinterpret_cast<uint8_t *>(fw2 + SS_SEL_TPB);  // [SS_SAMP] 0 undecided, 1 selected, 2 above
+  const int ns = (int)st->ss_ns;
+  unsigned long long x = 0;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+    x += (unsigned long long)B.w1[i];
+    flag[i] = 0;
+  }
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if (lane == 0) s_u64[threadIdx.x >> 5] = x;
+  if (threadIdx.x == 0) s_nsel = 0;
+  __syncthreads();
+  unsigned long long tot = 0;
+  for (int q = 0; q < (int)(blockDim.x >> 5); q++) tot += s_u64[q];
+  __syncthreads();
+  // target sample mass: (1.25 W + 3 average samples of slack) / m
+  long long need =
+      ns > 0 ? (long long)(((double)W * 1.25 + 3.0 * (double)m * ((double)tot / ns)) / (double)m) + 1 : 1;
+  int fail = (ns == 0 || (unsigned long long)need > tot) ? 1 : 0;  // (nearly) everything: sort it all
+  int nU = ns;
+  const int *cur = nullptr;  // null: the undecided set is in the flags
+  for (int r = 0; !fail && nU > (int)blockDim.x && r < 48; r++) {
+    int *nxt = (cur == ua) ? ub : ua;
+    const SampleRound R = sample_round(B.k1, B.w1, cur, nU, ns, flag, need, selk, &s_nsel, nxt, SS_U, smin, smax,
+                                       s_hn, s_hw, s_misc, &s_ll);
+    if (R.overflow) fail = 2;
+    need -= R.below;
+    nU = R.nU_next;
+    cur = R.listed ? nxt : nullptr;
+    if (threadIdx.x == 0) {
+      st->ss_dbg[1] = r + 1;
+      if (r < 3) {
+        st->ss_dbg[2 + 3 * r] = nU;
+        st->ss_dbg[3 + 3 * r] = s_nsel;
+        st->ss_dbg[4 + 3 * r] = (unsigned long long)need;
+      }
+    }
+  }
+  if (!fail && nU > (int)blockDim.x) fail = 2;
+  if (!fail) {  // the last undecided samples (<= blockDim): exact sort, then the crossing one
+    if (!cur) {
+      if (threadIdx.x == 0) s_misc[2] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < ns; i += blockDim.x)
+        if (flag[i] == 0) ua[atomicAdd(&s_misc[2], 1)] = i;
+      __syncthreads();
+      cur = ua;
+    }
+    for (int q = threadIdx.x; q < nU; q += blockDim.x) {
+      const int i = cur[q];
+      fk[q] = B.k1[i];
+      fw[q] = (uint64_t)B.w1[i];
+    }
+    __syncthreads();
+    block_sort_small(fk, fw, nU, fk2, fw2, fk, fw);
+    if (threadIdx.x == 0) {
+      long long run = 0;
+      int c = nU - 1;
+      for (int q = 0; q < nU; q++) {
+        run += (long long)fw2[q];
+        if (run >= need) {
+          c = q;
+          break;
+        }
+      }
+      s_misc[3] = c;
+    }
+    __syncthreads();
+    const int c = s_misc[3], base = s_nsel;
+    if (base + c + 1 > SS_SPL) fail = 3;
+    else
+      for (int q = threadIdx.x; q <= c; q += blockDim.x) selk[base + q] = fk2[q];
+    __syncthreads();
+    if (threadIdx.x == 0) s_nsel = base + c + 1;
+    __syncthreads();
+  }
+  int nb = 0;
+  if (!fail) {  // splitters: the selected samples, sorted exactly
+    nb = s_nsel;
+    if (nb <= (int)blockDim.x) {
+      block_sort_small(selk, nullptr, nb, spl, nullptr, fk, fw);
+    } else {
+      block_rank_sort(selk, nullptr, nb, spl, nullptr);
+      __syncthreads();
+    }
+    for (int q = threadIdx.x; q < nb; q += blockDim.x) B.kt[q] = spl[q];
+  }
+  if (threadIdx.x == 0) {
+    st->ss_nb = fail ? 0 : nb;
+    st->ss_fail = fail;
+  }
+}
+
+template <class Cand>
+__global__ void __launch_bounds__(SS_TPB) k_ss_filter(Cand cand, CoopBufs B) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ unsigned s_w[32];
+  __shared__ unsigned long long s_base;
+  CoopState *st = B.st;
+  const int nb = st->ss_nb;
+  if (nb <= 0) return;
+  Key3 *spl = reinterpret_cast<Key3 *>(dsm);
+  unsigned *hcnt = reinterpret_cast<unsigned *>(spl + SS_SPL);
+  for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+    spl[q] = B.kt[q];
+    hcnt[q] = 0;
+  }
+  __syncthreads();
+  const Key3 tau = spl[nb - 1];
+  const int32_t hw = cand.hw();
+  const int lane = threadIdx.x & 31;
+  const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long ccount = 0, mass = 0;  // per thread: candidates seen, weight kept
+  for (int64_t s0 = (int64_t)blockIdx.x * blockDim.x; s0 < hw; s0 += UNR * gsz) {
+    Key3 k[UNR];
+    uint64_t v[UNR];
+    int64_t w[UNR];
+    int bk[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {  // UNR independent candidates in flight
+      const int64_t s = s0 + u * gsz + threadIdx.x;
+      w[u] = 0;
+      const bool c = s < hw && cand((int32_t)s, k[u], v[u], w[u]);
+      ccount += c ? 1 : 0;
+      bk[u] = (c && !key_less(tau, k[u])) ? 0 : -1;
+    }
+    unsigned nt = 0;
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+      if (bk[u] == 0) {
+        int lo = 0, hi = nb - 1;  // first splitter >= k (exists: spl[nb-1] = tau >= k)
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (key_less(spl[mid], k[u])) lo = mid + 1;
+          else hi = mid;
+        }
+        bk[u] = lo;
+        nt++;
+        mass += (unsigned long long)w[u];
+        atomicAdd(&hcnt[lo], 1u);
+      }
+    }
+    unsigned long long p = block_reserve(nt, &st->ss_n, s_w, &s_base);
+#pragma unroll
+    for (int u = 0; u < UNR; u++)
+      if (bk[u] >= 0) {
+        B.k0[p] = k[u];
+        B.v0[p] = v[u];
+        B.w0[p] = bk[u];
+        p++;
+      }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    ccount += __shfl_xor_sync(0xffffffffu, ccount, o);
+    mass += __shfl_xor_sync(0xffffffffu, mass, o);
+  }
+  if (lane == 0) {
+    if (ccount) atomicAdd(&st->ss_cand, ccount);
+    if (mass) atomicAdd(&st->ss_mass, mass);
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < nb; q += blockDim.x)
+    if (hcnt[q]) atomicAdd(&st->ss_cnt[q], hcnt[q]);
+}
+
+__global__ void __launch_bounds__(SS_TPB) k_ss_scatter(CoopBufs B, int64_t W) {
+  __shared__ unsigned s_off[SS_SPL + 1];
+  __shared__ unsigned long long s_tot[32];
+  CoopState *st = B.st;
+  const int nb = st->ss_nb;
+  if (nb <= 0) return;
+  const int64_t n = (int64_t)st->ss_n, ncand = (int64_t)st->ss_cand;
+  // bucket offsets (every CTA; one warp-scan pass over <= SS_SPL counts)
+  bool fits = true;
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int per = (nb + blockDim.x - 1) / blockDim.x, b0 = threadIdx.x * per, b1 = min(b0 + per, nb);
+    unsigned sum = 0;
+    for (int b = b0; b < b1; b++) {
+      const unsigned c = st->ss_cnt[b];
+      fits = fits && c <= (unsigned)SS_BMAX;
+      sum += c;
+    }
+    unsigned x = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_tot[wid] = x;
+    __syncthreads();
+    unsigned before = 0;
+    for (int q = 0; q < wid; q++) before += (unsigned)s_tot[q];
+    unsigned run = before + x - sum;
+    for (int b = b0; b < b1; b++) {
+      s_off[b] = run;
+      run += st->ss_cnt[b];
+    }
+    if (threadIdx.x == 0) s_off[nb] = (unsigned)n;
+    (void)nw;
+  }
+  fits = __syncthreads_and(fits);
+  const bool ok = fits && ((int64_t)st->ss_mass >= W || n == ncand);
+  if (blockIdx.x == 0) {
+    for (int b = threadIdx.x; b <= nb; b += blockDim.x) st->ss_off[b] = s_off[b];
+    if (threadIdx.x == 0) {
+      st->ss_ok = ok ? 1 : 0;
+      if (!ok) st->ss_fail = fits ? 5 : 4;
+    }
+  }
+  if (!ok) return;
+  // scatter into bucket order (warp-aggregated cursors)
+  const int lane = threadIdx.x & 31;
+  const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += gsz) {
+    const int64_t i = i0 + threadIdx.x;
+    const int b = i < n ? (int)B.w0[i] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, b);
+    const int leader = __ffs(peers) - 1;
+    unsigned base = 0;
+    if (b >= 0 && lane == leader) base = atomicAdd(&st->ss_cur[b], (unsigned)__popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    if (b >= 0) {
+      const unsigned p = s_off[b] + base + __popc(peers & ((1u << lane) - 1u));
+      B.ks[p] = B.k0[i];
+      B.vs[p] = B.v0[i];
+    }
+  }
+}
+
+// one CTA per bucket: rank sort (no barriers) up to blockDim items, bitonic above
+__global__ void __launch_bounds__(SS_TPB) k_ss_sort(CoopBufs B, Key3 *kout, uint64_t *vout) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  CoopState *st = B.st;
+  const int b = blockIdx.x;
+  if (!st->ss_ok || b >= st->ss_nb) return;
+  const int b0 = (int)st->ss_off[b], m0 = (int)(st->ss_off[b + 1] - st->ss_off[b]);
+  if (m0 == 0) return;
+  Key3 *sk = reinterpret_cast<Key3 *>(dsm);
+  uint64_t *sv = reinterpret_cast<uint64_t *>(sk + SS_BMAX);
+  if (m0 <= (int)blockDim.x) {
+    for (int i = threadIdx.x; i < m0; i += blockDim.x) {
+      sk[i] = B.ks[b0 + i];
+      sv[i] = B.vs[b0 + i];
+    }
+    __syncthreads();
+    block_rank_sort(sk, sv, m0, kout + b0, vout + b0);
+    return;
+  }
+  int mp = 1;
+  while (mp < m0) mp <<= 1;
+  for (int i = threadIdx.x; i < mp; i += blockDim.x) {
+    if (i < m0) {
+      sk[i] = B.ks[b0 + i];
+      sv[i] = B.vs[b0 + i];
+    } else {
+      sk[i] = {~0ull, ~0ull, ~0ull};
+      sv[i] = 0;
+    }
+  }
+  __syncthreads();
+  bitonic_smem(sk, sv, mp);
+  for (int i = threadIdx.x; i < m0; i += blockDim.x) {
+    kout[b0 + i] = sk[i];
+    vout[b0 + i] = sv[i];
+  }
+}
+
+// the eviction-order build after keys / subtree maxima (full-occupancy
+// kernels k_build_keys, k_propagate) and the sample select: the prefix of the
+// order with >= W tokens sorted into the list -- finalised here when the
+// sample select succeeded (st->ss_ok), else by the materialising radix
+// selection (everything when W <= 0) -- one cooperative launch, no host round trip.
 __global__ void __launch_bounds__(COOP_TPB) k_build_coop(DT T, CoopBufs B, int64_t W, int64_t min_cand,
-                                                         int64_t small) {
+                                                         int64_t small, int32_t sampled) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ Key3 smin[COOP_TPB + 1], smax[COOP_TPB + 1];
   cg::grid_group grid = cg::this_grid();
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gsz = (int64_t)gridDim.x * blockDim.x;
-  const int64_t n = (int64_t)B.st->cand;
+  const int32_t hw = T.ctrl->hw;
+  const EvictCand cand{T};
   coop_mark(B.st);
-  int64_t nsel = n;
-  if (W > 0 && n > min_cand) {
-    nsel = coop_select(grid, B, n, W, small, smin, smax);
-  } else {  // sort everything: move candidates to the selected buffer
-    for (int64_t i = gtid; i < n; i += gsz) {
-      B.ks[i] = B.k0[i];
-      B.vs[i] = B.v0[i];
-    }
+  int64_t nsel = 0, n = 0;
+  const bool fast = sampled && B.st->ss_ok;
+  if (fast) {
+    nsel = (int64_t)B.st->ss_n;
+    n = (int64_t)B.st->ss_cand;
+  } else {
+    coop_gather(B, hw, cand);
     grid.sync();
+    n = (int64_t)B.st->cand;
+    nsel = n;
+    if (W > 0 && n > min_cand) {
+      nsel = coop_select(grid, B, n, W, small, smin, smax);
+    } else {  // sort everything: move candidates to the selected buffer
+      for (int64_t i = gtid; i < n; i += gsz) {
+        B.ks[i] = B.k0[i];
+        B.vs[i] = B.v0[i];
+      }
+      grid.sync();
+    }
+    coop_mark(B.st);
+    coop_sort(grid, B, nsel, T.Lk, T.Lv, dsm);
   }
-  coop_mark(B.st);
-  coop_sort(grid, B, nsel, T.Lk, T.Lv, dsm);
   coop_mark(B.st);
   if (gtid == 0) {
     Ctrl *c = T.ctrl;
@@ -414,64 +1230,55 @@ __global__ void __launch_bounds__(COOP_TPB) k_build_coop(DT T, CoopBufs B, int64
     c->builds++;
     for (int i = 0; i < B.st->nts; i++) B.st->ts_build[i] = B.st->ts[i];
     B.st->nts_build = B.st->nts;
-    B.st->ts_build[39] = (unsigned long long)nsel;  // selected-prefix size, for diagnostics
+    for (int i = 0; i < 12; i++) B.st->ts_build[21 + i] = B.st->ss_dbg[i];
+    B.st->ts_build[33] = B.st->ss_ns;  // diagnostics of the sample select
+    B.st->ts_build[34] = (unsigned long long)B.st->ss_nb;
+    B.st->ts_build[35] = (unsigned long long)B.st->ss_fail;
+    B.st->ts_build[36] = B.st->ss_mass;
+    B.st->ts_build[37] = (unsigned long long)W;
+    B.st->ts_build[38] = fast ? 1ull : 0ull;        // sampled path taken
+    B.st->ts_build[39] = (unsigned long long)nsel;  // selected-prefix size
   }
 }
 
-// set_protection (kvcache.py:364-383): top-f reusable anchors by (-P-hat, seg or -1, id)
+// set_protection (kvcache.py:364-383): top-f reusable anchors by (-P-hat, seg
+// or -1, id) -- from the sample select when it succeeded, else materialised
 __global__ void __launch_bounds__(COOP_TPB) k_protect_coop(DT T, CoopBufs B, int64_t f, int64_t min_cand,
-                                                           int64_t small) {
+                                                           int64_t small, int32_t sampled) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ Key3 smin[COOP_TPB + 1], smax[COOP_TPB + 1];
   cg::grid_group grid = cg::this_grid();
   const int32_t hw = T.ctrl->hw;
   const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
-  const int lane = threadIdx.x & 31;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < hw; base += gsz) {
-    const int64_t s = base + threadIdx.x;
-    bool take = false;
-    if (s < hw) {
-      T.prot[s] = 0;  // previous protection is cleared
-      take = s != ROOT && T.nid[s] >= 0 && T.par[s] >= 0 && T.hasanc[s] && T.akind[s] == K_REUSABLE;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, take);
-    if (!m) continue;
-    unsigned long long b = 0;
-    if (lane == 0) b = atomicAdd(&B.st->cand, (unsigned long long)__popc(m));
-    b = __shfl_sync(0xffffffffu, b, 0);
-    if (take) {
-      const int64_t pos = (int64_t)b + __popc(m & ((1u << lane) - 1));
-      const int32_t sg = T.seg[s];
-      const int32_t sv = sg == SEG_NONE ? -1 : sg;
-      Key3 k = {0, 0, 0};
-      shl_or(k, 64, ord_f64(-pri_of(T, sg)));
-      shl_or(k, 32, (uint64_t)((uint32_t)sv ^ 0x80000000u));
-      shl_or(k, 40, (uint64_t)T.nid[s] & ((1ull << 40) - 1));
-      B.k0[pos] = k;
-      B.v0[pos] = (uint64_t)(uint32_t)s;
-      B.w0[pos] = 1;
-    }
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const ProtCand cand{T};
+  int64_t n = 0, nsel = 0;
+  const bool fast = sampled && B.st->ss_ok;
+  if (fast) {
+    n = (int64_t)B.st->ss_cand;
+  } else {
+    coop_gather(B, hw, cand);
+    grid.sync();
+    n = (int64_t)B.st->cand;
   }
-  grid.sync();
-  const int64_t n = (int64_t)B.st->cand;
   const int64_t nf = f < n ? f : n;
   if (nf <= 0) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) B.st->prot_n = 0;
+    if (gtid == 0) B.st->prot_n = 0;
     return;
   }
-  int64_t nsel = n;
-  if (n > min_cand) {
-    nsel = coop_select(grid, B, n, nf, small, smin, smax);
-  } else {
-    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t i = gtid; i < n; i += gsz) {
-      B.ks[i] = B.k0[i];
-      B.vs[i] = B.v0[i];
+  if (!fast) {
+    nsel = n;
+    if (n > min_cand) {
+      nsel = coop_select(grid, B, n, nf, small, smin, smax);
+    } else {
+      for (int64_t i = gtid; i < n; i += gsz) {
+        B.ks[i] = B.k0[i];
+        B.vs[i] = B.v0[i];
+      }
+      grid.sync();
     }
-    grid.sync();
+    coop_sort(grid, B, nsel, T.Lk, T.Lv, dsm);  // Lk/Lv as scratch: no list survives a call
   }
-  coop_sort(grid, B, nsel, T.Lk, T.Lv, dsm);  // Lk/Lv as scratch: no list survives a call
-  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (int64_t i = gtid; i < nf; i += gsz) {
     const int32_t s = (int32_t)(T.Lv[i] & 0xffffffffu);
     T.prot[s] = 1;

@@ -124,6 +124,7 @@ struct prism_tree {
   int64_t list_slack_tokens = 4096;    // parallel commit: demand + 25% + this
   int64_t sel_min_candidates = 4096;   // below this many candidates, sort them all
   int64_t use_coop = 1;                // cooperative single-kernel build / protection
+  int64_t use_sample = 1;              // sample select before the materialising selection
 };
 
 enum { PH_COMMIT = 0, PH_BUILD = 1, PH_PROTECT = 2, PH_PREMATCH = 3, PH_RELEASE = 4, PH_NOTE = 5, PH_MAINT = 6 };
@@ -173,7 +174,10 @@ int alloc_scratch(prism_tree *t, int64_t S) {
     if (*b) CK(cudaFree(*b));
   CK(dalloc(&t->kt, S));
   CK(dalloc(&t->vt, S));
-  if (!t->cst) CK(dalloc(&t->cst, 1));
+  if (!t->cst) {
+    CK(dalloc(&t->cst, 1));
+    CK(cudaMemset(t->cst, 0, sizeof(CoopState)));
+  }
   CK(dalloc(&t->ck, S));
   CK(dalloc(&t->cv, S));
   CK(dalloc(&t->cw, S));
@@ -330,6 +334,27 @@ int coop_grid(prism_tree *t) {
   return t->coop_grid;
 }
 
+// the sample-select launches (coop.cuh) ahead of the cooperative finaliser
+template <class Cand>
+int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, int64_t min_cand) {
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_ss_select<EvictCand>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SEL_SMEM));
+    CK(cudaFuncSetAttribute(k_ss_select<ProtCand>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SEL_SMEM));
+    attr = true;
+  }
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev));
+  cudaStream_t st = t->st;
+  k_ss_sample<Cand><<<SS_SAMP / SS_TPB, SS_TPB, 0, st>>>(cand, B, W, min_cand);
+  k_ss_select<Cand><<<1, SS_SEL_TPB, SS_SEL_SMEM, st>>>(cand, B, W);
+  k_ss_filter<Cand><<<4 * sms, SS_TPB, SS_FILTER_SMEM, st>>>(cand, B);
+  k_ss_scatter<<<2 * sms, SS_TPB, 0, st>>>(B, W);
+  k_ss_sort<<<SS_SPL, SS_TPB, SS_SORT_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
+  CK(cudaGetLastError());
+  return PRISM_OK;
+}
+
 CoopBufs coop_bufs(prism_tree *t) {
   return CoopBufs{t->ck, t->ck2, t->ks, t->kt, t->cv, t->cv2, t->vs, t->vt, t->cw, t->cw2, t->bmin, t->bmax,
                   t->cst, t->d_prot_ids};
@@ -349,12 +374,16 @@ int build_list(prism_tree *t, int64_t W) {
     const int64_t S = t->d.S;
     k_build_keys<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1);
     k_propagate<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1);
-    k_gather<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1, t->ck, t->cv, t->cw, (int64_t *)&t->cst->cand);
     CoopBufs B = coop_bufs(t);
     int64_t minc = t->sel_min_candidates, small = std::min<int64_t>(SEL_SMALL, t->sel_min_candidates);
-    void *args[] = {(void *)&t->d, (void *)&B, (void *)&W, (void *)&minc, (void *)&small};
+    int32_t sampled = (t->use_sample && W > 0) ? 1 : 0;
+    if (sampled) {
+      int rc = sample_select(t, EvictCand{t->d}, B, W, minc);
+      if (rc) return rc;
+    }
+    void *args[] = {(void *)&t->d, (void *)&B, (void *)&W, (void *)&minc, (void *)&small, (void *)&sampled};
     CK(cudaLaunchCooperativeKernel((void *)k_build_coop, grid, COOP_TPB, args, COOP_SMEM, t->st));
-    t->launches[PH_BUILD] += 4;
+    t->launches[PH_BUILD] += 3 + (sampled ? 5 : 0);
     prof_end(t, PH_BUILD);
     return PRISM_OK;
   }
@@ -983,7 +1012,13 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out) {
     CoopBufs B = coop_bufs(t);
     int64_t minc = t->sel_min_candidates, small = std::min<int64_t>(SEL_SMALL, t->sel_min_candidates);
     int64_t ff = f;
-    void *args[] = {(void *)&t->d, (void *)&B, (void *)&ff, (void *)&minc, (void *)&small};
+    int32_t sampled = (t->use_sample && f > 0) ? 1 : 0;
+    if (sampled) {
+      rc = sample_select(t, ProtCand{t->d}, B, ff, minc);
+      if (rc) return rc;
+      t->launches[PH_PROTECT] += 5;
+    }
+    void *args[] = {(void *)&t->d, (void *)&B, (void *)&ff, (void *)&minc, (void *)&small, (void *)&sampled};
     CK(cudaLaunchCooperativeKernel((void *)k_protect_coop, grid, COOP_TPB, args, COOP_SMEM, t->st));
     t->launches[PH_PROTECT] += 1;
     prof_end(t, PH_PROTECT);
@@ -1416,7 +1451,8 @@ int64_t prism_compactions(prism_tree *t) { return t->compactions; }
 
 // phase timeline of the last cooperative list build: out[0..n) %globaltimer
 // ns stamps (start, after each selection round, after the chunk sort, after
-// each merge round, end); out[39] = selected-prefix size
+// each merge round, end); out[38] = 1 if the sample select produced it,
+// out[39] = selected-prefix size
 int prism_coop_timeline(prism_tree *t, uint64_t *out, int32_t *n) {
   cudaSetDevice(t->dev);
   CK(cudaMemcpyAsync(out, t->cst->ts_build, 40 * sizeof(uint64_t), cudaMemcpyDeviceToHost, t->st));
@@ -1426,13 +1462,15 @@ int prism_coop_timeline(prism_tree *t, uint64_t *out, int32_t *n) {
 }
 
 // 0: list_min_tokens, 1: list_slack_tokens, 2: sel_min_candidates (tests use
-// tiny values to force partial eviction lists and their rebuild/resume path)
+// tiny values to force partial eviction lists and their rebuild/resume path),
+// 3: cooperative kernels, 4: sample select (coop.cuh) before the radix selection
 int prism_tune(prism_tree *t, int32_t key, int64_t value) {
   switch (key) {
     case 0: t->list_min_tokens = std::max<int64_t>(value, 1); break;
     case 1: t->list_slack_tokens = std::max<int64_t>(value, 0); break;
     case 2: t->sel_min_candidates = std::max<int64_t>(value, 0); break;
     case 3: t->use_coop = value ? 1 : 0; break;
+    case 4: t->use_sample = value ? 1 : 0; break;
     default: return fail(PRISM_INVALID, "unknown tunable");
   }
   return PRISM_OK;

@@ -844,7 +844,7 @@ __global__ void k_propagate(DT T, int32_t hw) {
   if (!blocked) kv = T.kw[s];
   int32_t p = T.par[s];
   while (p > 0) {
-    int32_t cur = atomicAdd(&T.eff[p], 0);
+    int32_t cur = __ldcg(&T.eff[p]);  // L2-coherent read; CAS only to raise
     for (;;) {
       if (cur == EFF_BLOCKED) return;
       if (!blocked && cur >= 0 && !key_less(T.kw[cur], kv)) return;

@@ -212,7 +212,8 @@ class DeviceRadixCache:
             self._last = (int(self._op[1]), int(self._op[2]))
         self._dirty()
 
-    TUNABLES = {"list_min_tokens": 0, "list_slack_tokens": 1, "sel_min_candidates": 2, "use_coop": 3}
+    TUNABLES = {"list_min_tokens": 0, "list_slack_tokens": 1, "sel_min_candidates": 2, "use_coop": 3,
+                "use_sample": 4}
 
     def tune(self, **kw) -> None:
         """Eviction-list prefix sizing (semantics-free; tests force tiny prefixes)."""

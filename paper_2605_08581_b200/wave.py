@@ -168,7 +168,10 @@ class WaveEngine:
         n = np.zeros(1, dtype=np.int32)
         check(self.L.prism_coop_timeline(self.t, out.ctypes.data, n.ctypes.data))
         ts = out[: n[0]].astype(np.int64)
-        return {"phases_us": (np.diff(ts) / 1e3).round(1).tolist(), "selected": int(out[39])}
+        return {"phases_us": (np.diff(ts) / 1e3).round(1).tolist(), "selected": int(out[39]),
+                "sampled": int(out[38]), "samples": int(out[33]), "splitters": int(out[34]),
+                "fallback_reason": int(out[35]), "kept_mass": int(out[36]), "W": int(out[37]),
+                "dbg": out[21:33].astype(np.int64).tolist()}
 
     def cache_view(self):
         """The reference RadixCache API over this engine's tree (tests/debug)."""

@@ -54,7 +54,7 @@ def _pending_arrays(reqs):
 
 
 def run_case(seed, policy, mode, nseg=40, hot=6, kmin=2, kmax=5, suffixes=(2, 4), sys=8, chunk=4, cap=600,
-             wave=24, nwaves=8, protect=3, cold=2, tiny=False, coop=1):
+             wave=24, nwaves=8, protect=3, cold=2, tiny=False, coop=1, sample=1):
     import torch
 
     from paper_2605_08581_b200.wave import DevicePending, WaveEngine
@@ -64,7 +64,7 @@ def run_case(seed, policy, mode, nseg=40, hot=6, kmin=2, kmax=5, suffixes=(2, 4)
     scfg = SchedulerConfig(dispatch_budget=wave, cold_quota=cold)
     eng = WaveEngine(cfg, scfg, nseg, sys, chunk, device=0)
     eng.set_commit_mode(mode)
-    eng.tune(use_coop=coop)
+    eng.tune(use_coop=coop, use_sample=sample)
     if tiny:  # minimal selected prefixes of the eviction order
         eng.tune(list_min_tokens=1, list_slack_tokens=0, sel_min_candidates=0)
     ora = OracleRadixCache(cfg)
@@ -139,6 +139,53 @@ def test_ordered_commit_matches_oracle(policy):
     dict(tiny=True, cap=150, wave=32, nwaves=10),      # ... with capacity stops
     dict(coop=0),                                      # multi-kernel build / protection
     dict(coop=0, tiny=True),
+    dict(sample=0),                                    # materialising radix selection only
+    dict(sample=0, tiny=True),
 ])
 def test_parallel_commit_variants(variant):
     run_case(5, CachePolicy.DART, mode=0, **variant)
+
+
+def _mu_pool(rng, first, n, k=6, chunk=8, slot0=20, others=200_000, suffix=8):
+    sk = np.empty((n, k), dtype=np.int32)
+    sk[:, 0] = rng.integers(0, slot0, size=n)
+    sk[:, 1:] = slot0 + rng.integers(0, others, size=(n, k - 1))
+    ids = np.arange(first, first + n, dtype=np.int64)
+    return (ids, ids.astype(np.float64) * 1e-3, np.arange(n + 1, dtype=np.int64) * k, sk.reshape(-1),
+            np.ones(n, np.uint8), np.full(n, suffix, np.int32))
+
+
+@pytest.mark.parametrize("protect", [20, 3000])
+def test_sampled_selection_at_scale(protect):
+    """~150K-node tree, every wave evicts: the sampled eviction-prefix / top-f
+    selection (coop.cuh) commits exactly what the materialising radix selection
+    commits -- hits, leaf ids, the whole victim log and the final tree."""
+    import torch
+
+    from paper_2605_08581_b200.wave import DevicePending, WaveEngine
+
+    dev = torch.device("cuda", 0)
+    runs = []
+    for sample in (1, 0):
+        rng = np.random.default_rng(5)
+        cfg = CacheConfig(capacity_tokens=1_000_000, policy=CachePolicy.DART, protect_budget=protect)
+        eng = WaveEngine(cfg, SchedulerConfig(dispatch_budget=2048, cold_quota=16), 20 + 200_000, 12, 8, device=0)
+        eng.tune(use_sample=sample)
+        nid, prev, out, sampled = 0, 0, [], 0
+        for w in range(30):
+            pend = DevicePending.from_host(*_mu_pool(rng, nid, 2048), dev)
+            nid += 2048
+            eng.release(eng.leaf_slots, prev)
+            nm, prev = eng.step(pend)
+            out.append((eng.members[:nm].cpu().tolist(), eng.hits[:prev].cpu().tolist(),
+                        eng.leaf_ids[:prev].cpu().tolist()))
+            sampled += eng.build_timeline()["sampled"]
+        view = eng.cache_view()
+        runs.append((out, view.victim_log(), view.debug_nodes(), eng.stats()["live_nodes"], sampled))
+        eng.close()
+    (o1, v1, d1, n1, s1), (o0, v0, d0, n0, s0) = runs
+    assert n1 > 100_000 and len(v1) > 10_000
+    assert s1 > 0 and s0 == 0  # the sampled path ran (and only where enabled)
+    assert o1 == o0
+    assert v1 == v0
+    assert d1 == d0

@@ -1,0 +1,84 @@
+"""Per-phase diagnostics of the bench wave (run on a GPU box).
+
+    python tools/diag_wave.py [--steps 5]
+
+Prints, per timed wave: the wave's CUDA-event time, host wall time, the
+live per-phase device profile, the one-launch QAS round timeline and the
+cooperative eviction-list build timeline.  Diagnostics only (not a bench).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--wave", type=int, default=4096)
+    ap.add_argument("--paths", type=int, default=125_000)
+    args = ap.parse_args()
+    import torch
+
+    from paper_2605_08581_b200.types import CacheConfig, CachePolicy, SchedulerConfig
+    from paper_2605_08581_b200.wave import DevicePending, WaveEngine
+
+    B = args.wave
+    eng = WaveEngine(CacheConfig(capacity_tokens=16_000_000, policy=CachePolicy.DART, protect_budget=20),
+                     SchedulerConfig(dispatch_budget=B, cold_quota=64), bench.NSEG, bench.SYS_LEN, bench.CHUNK,
+                     device=0, initial_slots=1 << 21, initial_arena_tokens=1 << 26)
+    L = eng.L
+    L.prism_qas_small_timeline.argtypes = [C.c_void_p, C.c_void_p, C.c_int32]
+    rng = np.random.default_rng(0)
+
+    def dev(pool):
+        return DevicePending.from_host(pool["ids"], pool["arrival"], pool["sk_off"], pool["sk"],
+                                       pool["reorderable"], pool["suffix"], torch.device("cuda", 0))
+
+    nid, prev = 0, 0
+    while nid < args.paths:
+        n = min(B, args.paths - nid)
+        eng.release(eng.leaf_slots, prev)
+        _, prev = eng.step(dev(bench.make_pool(nid, n, rng)))
+        nid += n
+    pools = [dev(bench.make_pool(nid + s * B, B, rng)) for s in range(args.steps + 2)]
+    for s in range(2):
+        eng.release(eng.leaf_slots, prev)
+        _, prev = eng.step(pools[s])
+    torch.cuda.synchronize()
+    eng.profile(True)
+    for s in range(2, args.steps + 2):
+        p0 = eng.profile_read()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0.record(eng.stream)
+        eng.release(eng.leaf_slots, prev)
+        nm, prev = eng.step(pools[s])
+        e1.record(eng.stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e6
+        p1 = eng.profile_read()
+        ph = {k: round((p1[k]["ms"] - p0[k]["ms"]) * 1000, 1) for k in ("qas", "protect", "build", "commit",
+                                                                         "prematch", "release")}
+        ts = np.zeros(11, dtype=np.int64)
+        L.prism_qas_small_timeline(eng.q, ts.ctypes.data, 11)
+        print(f"wave {s}: event {e0.elapsed_time(e1) * 1000:.1f} us, wall {wall:.1f} us, phases(us) {ph}")
+        print("  qas one-launch phases (us):", (np.diff(ts) / 1e3).round(1).tolist())
+        print("  build:", eng.build_timeline())
+    eng.close()
+
+
+if __name__ == "__main__":
+    main()
