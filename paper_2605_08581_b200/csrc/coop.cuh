@@ -436,8 +436,9 @@ __device__ void coop_sort(cg::grid_group &grid, const CoopBufs &B, int64_t n, Ke
 __device__ inline void bitonic_smem(Key3 *sk, uint64_t *sv, int m) {
   for (int size = 2; size <= m; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const int lg = __ffs(stride) - 1;
       for (int p = threadIdx.x; p < (m >> 1); p += blockDim.x) {
-        const int i = 2 * stride * (p / stride) + (p % stride), j = i + stride;
+        const int i = ((p >> lg) << (lg + 1)) | (p & (stride - 1)), j = i + stride;
         const bool up = (i & size) == 0;
         if (up ? key_less(sk[j], sk[i]) : key_less(sk[i], sk[j])) {
           const Key3 tk = sk[i];
@@ -456,8 +457,9 @@ __device__ inline void bitonic_smem(Key3 *sk, uint64_t *sv, int m) {
 __device__ inline void bitonic_keys(Key3 *sk, int m) {
   for (int size = 2; size <= m; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const int lg = __ffs(stride) - 1;
       for (int p = threadIdx.x; p < (m >> 1); p += blockDim.x) {
-        const int i = 2 * stride * (p / stride) + (p % stride), j = i + stride;
+        const int i = ((p >> lg) << (lg + 1)) | (p & (stride - 1)), j = i + stride;
         const bool up = (i & size) == 0;
         if (up ? key_less(sk[j], sk[i]) : key_less(sk[i], sk[j])) {
           const Key3 tk = sk[i];
@@ -623,7 +625,8 @@ constexpr int SR_B = 4;
 __device__ inline SampleRound sample_round(const Key3 *sk, const int64_t *sw, const int *idx, int nU, int ns,
                                            uint8_t *flag, long long need, Key3 *selk, int *s_nsel, int *nxt,
                                            int cap_nxt, Key3 *smin, Key3 *smax, unsigned *s_hn,
-                                           unsigned *s_hw, int *s_misc, long long *s_ll) {
+                                           unsigned *s_hw, int *s_misc, long long *s_ll, Key3 &gmin, Key3 &gmax,
+                                           bool have_mm) {
   const int lane = threadIdx.x & 31;
   const int n = idx ? nU : ns;
   const int step = SR_B * blockDim.x;
@@ -633,23 +636,28 @@ __device__ inline SampleRound sample_round(const Key3 *sk, const int64_t *sw, co
     return (idx || flag[i] == 0) ? i : -1;
   };
   Key3 lo = {~0ull, ~0ull, ~0ull}, hi = {0, 0, 0};
-  for (int q0 = threadIdx.x; q0 < n; q0 += step) {
-    Key3 kk[SR_B];
-    int ii[SR_B];
+  if (!have_mm) {  // (later rounds get the min/max from the previous classification)
+    for (int q0 = threadIdx.x; q0 < n; q0 += step) {
+      Key3 kk[SR_B];
+      int ii[SR_B];
 #pragma unroll
-    for (int u = 0; u < SR_B; u++) {
-      ii[u] = item(q0 + u * blockDim.x);
-      if (ii[u] >= 0) kk[u] = sk[ii[u]];
-    }
-#pragma unroll
-    for (int u = 0; u < SR_B; u++)
-      if (ii[u] >= 0) {
-        if (key_less(kk[u], lo)) lo = kk[u];
-        if (key_less(hi, kk[u])) hi = kk[u];
+      for (int u = 0; u < SR_B; u++) {
+        ii[u] = item(q0 + u * blockDim.x);
+        if (ii[u] >= 0) kk[u] = sk[ii[u]];
       }
+#pragma unroll
+      for (int u = 0; u < SR_B; u++)
+        if (ii[u] >= 0) {
+          if (key_less(kk[u], lo)) lo = kk[u];
+          if (key_less(hi, kk[u])) hi = kk[u];
+        }
+    }
+    block_minmax(lo, hi, smin, smax, &smin[32], &smax[32]);
+    gmin = smin[32];
+    gmax = smax[32];
+    lo = {~0ull, ~0ull, ~0ull};
+    hi = {0, 0, 0};
   }
-  block_minmax(lo, hi, smin, smax, &smin[32], &smax[32]);
-  const Key3 gmin = smin[32], gmax = smax[32];
   const Key3 xx = {gmin.w0 ^ gmax.w0, gmin.w1 ^ gmax.w1, gmin.w2 ^ gmax.w2};
   const int hb = chighbit(xx);
   const int shift = hb < 7 ? 0 : hb - 7;
@@ -770,8 +778,15 @@ __device__ inline SampleRound sample_round(const Key3 *sk, const int64_t *sw, co
         else ovf = true;
       }
       if (mid && list) nxt[pm] = i;
+      if (mid) {  // min/max of the next undecided set
+        if (key_less(kk[u], lo)) lo = kk[u];
+        if (key_less(hi, kk[u])) hi = kk[u];
+      }
     }
   }
+  block_minmax(lo, hi, smin, smax, &smin[32], &smax[32]);
+  gmin = smin[32];
+  gmax = smax[32];
   ovf = __syncthreads_or(ovf);
   SampleRound r{nnext, list, *s_ll, ovf};
   __syncthreads();
@@ -861,7 +876,9 @@ struct ProtCand {
 constexpr int SS_TPB = 256;
 constexpr int SS_SEL_TPB = 512;
 constexpr int SS_BMAX = 1024;  // largest bucket sorted in shared memory
-constexpr size_t SS_SEL_SMEM = 2 * sizeof(Key3) * SS_SPL + 8 * SS_U + 2 * (sizeof(Key3) + 8) * SS_SEL_TPB + SS_SAMP;
+constexpr int SS_SUB = 2048;  // sub-sample the selection rounds run on
+constexpr size_t SS_SEL_SMEM =
+    2 * sizeof(Key3) * SS_SPL + 8 * SS_U + 2 * (sizeof(Key3) + 8) * SS_SEL_TPB + (sizeof(Key3) + 9) * SS_SUB;
 constexpr size_t SS_FILTER_SMEM = sizeof(Key3) * SS_SPL + 4 * SS_SPL;
 constexpr size_t SS_SORT_SMEM = (sizeof(Key3) + 8) * SS_BMAX;
 
@@ -916,31 +933,41 @@ __global__ void __launch_bounds__(SS_SEL_TPB) k_ss_select(Cand cand, CoopBufs B,
   uint64_t *fw = reinterpret_cast<uint64_t *>(fk + SS_SEL_TPB);
   Key3 *fk2 = reinterpret_cast<Key3 *>(fw + SS_SEL_TPB);
   uint64_t *fw2 = reinterpret_cast<uint64_t *>(fk2 + SS_SEL_TPB);
-  uint8_t *flag = reinterpret_cast<uint8_t *>(fw2 + SS_SEL_TPB);  // [SS_SAMP] 0 undecided, 1 selected, 2 above
+  Key3 *subk = reinterpret_cast<Key3 *>(fw2 + SS_SEL_TPB);  // [SS_SUB] the sub-sample the rounds run on
+  int64_t *subw = reinterpret_cast<int64_t *>(subk + SS_SUB);
+  uint8_t *flag = reinterpret_cast<uint8_t *>(subw + SS_SUB);  // [SS_SUB] 0 undecided, 1 selected, 2 above
+  coop_mark(st);
   const int ns = (int)st->ss_ns;
+  // tau comes from every q-th sample (<= SS_SUB of them, in shared memory);
+  // the splitters are then all samples <= tau
+  const int q = (ns + SS_SUB - 1) / SS_SUB > 0 ? (ns + SS_SUB - 1) / SS_SUB : 1;
+  const int nsub = (ns + q - 1) / q;
   unsigned long long x = 0;
-#pragma unroll 4
-  for (int i = threadIdx.x; i < ns; i += blockDim.x) {
-    x += (unsigned long long)B.w1[i];
-    flag[i] = 0;
+  for (int j = threadIdx.x; j < nsub; j += blockDim.x) {
+    subk[j] = B.k1[j * q];
+    subw[j] = B.w1[j * q];
+    x += (unsigned long long)subw[j];
+    flag[j] = 0;
   }
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   if (lane == 0) s_u64[threadIdx.x >> 5] = x;
   if (threadIdx.x == 0) s_nsel = 0;
   __syncthreads();
   unsigned long long tot = 0;
-  for (int q = 0; q < (int)(blockDim.x >> 5); q++) tot += s_u64[q];
+  for (int w = 0; w < (int)(blockDim.x >> 5); w++) tot += s_u64[w];
   __syncthreads();
-  // target sample mass: (1.25 W + 3 average samples of slack) / m
-  long long need =
-      ns > 0 ? (long long)(((double)W * 1.25 + 3.0 * (double)m * ((double)tot / ns)) / (double)m) + 1 : 1;
-  int fail = (ns == 0 || (unsigned long long)need > tot) ? 1 : 0;  // (nearly) everything: sort it all
-  int nU = ns;
+  // target sub-sample mass: (1.25 W + 3 average sub-samples of slack) / (m q)
+  coop_mark(st);
+  const double mq = (double)m * q;
+  long long need = nsub > 0 ? (long long)(((double)W * 1.25 + 3.0 * mq * ((double)tot / nsub)) / mq) + 1 : 1;
+  int fail = (nsub == 0 || (unsigned long long)need > tot) ? 1 : 0;  // (nearly) everything: sort it all
+  int nU = nsub;
   const int *cur = nullptr;  // null: the undecided set is in the flags
+  Key3 gmin, gmax;
   for (int r = 0; !fail && nU > (int)blockDim.x && r < 48; r++) {
     int *nxt = (cur == ua) ? ub : ua;
-    const SampleRound R = sample_round(B.k1, B.w1, cur, nU, ns, flag, need, selk, &s_nsel, nxt, SS_U, smin, smax,
-                                       s_hn, s_hw, s_misc, &s_ll);
+    const SampleRound R = sample_round(subk, subw, cur, nU, nsub, flag, need, selk, &s_nsel, nxt, SS_U, smin, smax,
+                                       s_hn, s_hw, s_misc, &s_ll, gmin, gmax, r > 0);
     if (R.overflow) fail = 2;
     need -= R.below;
     nU = R.nU_next;
@@ -954,43 +981,61 @@ __global__ void __launch_bounds__(SS_SEL_TPB) k_ss_select(Cand cand, CoopBufs B,
       }
     }
   }
+  coop_mark(st);
   if (!fail && nU > (int)blockDim.x) fail = 2;
   if (!fail) {  // the last undecided samples (<= blockDim): exact sort, then the crossing one
     if (!cur) {
       if (threadIdx.x == 0) s_misc[2] = 0;
       __syncthreads();
-      for (int i = threadIdx.x; i < ns; i += blockDim.x)
+      for (int i = threadIdx.x; i < nsub; i += blockDim.x)
         if (flag[i] == 0) ua[atomicAdd(&s_misc[2], 1)] = i;
       __syncthreads();
       cur = ua;
     }
-    for (int q = threadIdx.x; q < nU; q += blockDim.x) {
-      const int i = cur[q];
-      fk[q] = B.k1[i];
-      fw[q] = (uint64_t)B.w1[i];
+    for (int j = threadIdx.x; j < nU; j += blockDim.x) {
+      const int i = cur[j];
+      fk[j] = subk[i];
+      fw[j] = (uint64_t)subw[i];
     }
     __syncthreads();
     block_sort_small(fk, fw, nU, fk2, fw2, fk, fw);
+    coop_mark(st);
     if (threadIdx.x == 0) {
       long long run = 0;
       int c = nU - 1;
-      for (int q = 0; q < nU; q++) {
-        run += (long long)fw2[q];
+      for (int j = 0; j < nU; j++) {
+        run += (long long)fw2[j];
         if (run >= need) {
-          c = q;
+          c = j;
           break;
         }
       }
       s_misc[3] = c;
+      s_nsel = 0;
     }
     __syncthreads();
-    const int c = s_misc[3], base = s_nsel;
-    if (base + c + 1 > SS_SPL) fail = 3;
-    else
-      for (int q = threadIdx.x; q <= c; q += blockDim.x) selk[base + q] = fk2[q];
-    __syncthreads();
-    if (threadIdx.x == 0) s_nsel = base + c + 1;
-    __syncthreads();
+    const Key3 tau = fk2[s_misc[3]];
+    // splitters: every sample <= tau (warp-aggregated appends)
+    bool ovf = false;
+    for (int i0 = 0; i0 < ns; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
+      Key3 k = {0, 0, 0};
+      bool t = false;
+      if (i < ns) {
+        k = B.k1[i];
+        t = !key_less(tau, k);
+      }
+      const unsigned mt = __ballot_sync(0xffffffffu, t);
+      int p = 0;
+      if (lane == 0 && mt) p = atomicAdd(&s_nsel, __popc(mt));
+      p = __shfl_sync(0xffffffffu, p, 0) + __popc(mt & ((1u << lane) - 1u));
+      if (t) {
+        if (p < SS_SPL) selk[p] = k;
+        else ovf = true;
+      }
+    }
+    if (__syncthreads_or(ovf)) fail = 3;
+    coop_mark(st);
   }
   int nb = 0;
   if (!fail) {  // splitters: the selected samples, sorted exactly
@@ -1002,6 +1047,7 @@ __global__ void __launch_bounds__(SS_SEL_TPB) k_ss_select(Cand cand, CoopBufs B,
       __syncthreads();
     }
     for (int q = threadIdx.x; q < nb; q += blockDim.x) B.kt[q] = spl[q];
+    coop_mark(st);
   }
   if (threadIdx.x == 0) {
     st->ss_nb = fail ? 0 : nb;
