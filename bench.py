@@ -62,6 +62,8 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=-1)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baseline/e2e)")
+    ap.add_argument("--profile-steps", type=int, default=3,
+                    help="extra waves AFTER the timed region with the per-phase device profile on (roofline)")
     return ap.parse_args()
 
 
@@ -299,8 +301,9 @@ def run_ours(args) -> None:
     st0 = engine.stats()
 
     nsteps = args.warmup + args.steps
-    pools = [make_pool(next_id + s * B, B, rng) for s in range(nsteps)]
-    next_id += nsteps * B
+    nprof = max(args.profile_steps, 1)
+    pools = [make_pool(next_id + s * B, B, rng) for s in range(nsteps + nprof)]
+    next_id += (nsteps + nprof) * B
     dpools = [to_dev(p) for p in pools]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
@@ -320,8 +323,7 @@ def run_ours(args) -> None:
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    engine.profile(True)
-    prof0 = engine.profile_read()
+    prof0 = engine.profile_read()  # (launch counters; the profile itself stays off while timing)
     st1 = engine.stats()
     clocks = Clocks(local)
     clocks.start()
@@ -346,7 +348,6 @@ def run_ours(args) -> None:
     clk = clocks.stop()
     prof1 = engine.profile_read()
     st2 = engine.stats()
-    engine.profile(False)
     ms = sum(a.elapsed_time(b) for a, b in evs)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -404,20 +405,35 @@ def run_ours(args) -> None:
                "d2h_bytes_per_step": d2h // e2e_steps, "api": "prism_wave_step via WaveEngine.step "
                "(pinned host pools copied in, hits + admission order copied out)"}
 
-    # ---- roofline of the dominant kernel, from the live profile over the timed region
-    d = {p: {k: prof1[p][k] - prof0[p][k] for k in ("ms", "calls", "launches")}
+    # ---- roofline of the dominant kernel: a few more waves of the same workload
+    # AFTER the timed region with the live per-phase profile on (its per-phase
+    # event syncs would otherwise sit inside the timed region)
+    gpu_launches = int(sum(prof1[p]["launches"] - prof0[p]["launches"]
+                           for p in ("commit", "build", "protect", "prematch", "release", "qas")))
+    torch.cuda.synchronize()
+    engine.profile(True)
+    prof2 = engine.profile_read()
+    st3 = engine.stats()
+    for s in range(nsteps, nsteps + nprof):
+        one_step(dpools[s])
+    torch.cuda.synchronize()
+    prof3 = engine.profile_read()
+    st4 = engine.stats()
+    engine.profile(False)
+    d = {p: {k: prof3[p][k] - prof2[p][k] for k in ("ms", "calls", "launches")}
          for p in ("commit", "build", "protect", "prematch", "release", "qas")}
-    victims = st2["victims"] - st1["victims"]
-    created = st2["next_id"] - st1["next_id"]
-    chain = prof1["chain_nodes"] - prof0["chain_nodes"]
-    toks = prof1["inserted_tokens"] - prof0["inserted_tokens"]
-    live = st2["live_nodes"]
+    victims = st4["victims"] - st3["victims"]
+    created = st4["next_id"] - st3["next_id"]
+    chain = prof3["chain_nodes"] - prof2["chain_nodes"]
+    toks = prof3["inserted_tokens"] - prof2["inserted_tokens"]
+    live = st4["live_nodes"]
+    members_prof = nprof * B
     algo = {  # SURVEY.md 8(d) algorithmic bytes, per phase over the timed region
         "commit": 8 * toks + 32 * (chain + created + victims),
         "build": 16 * live * d["build"]["calls"],
         "protect": 16 * live * d["protect"]["calls"],
         "prematch": 4 * toks + 32 * chain,
-        "qas": members * (4 * K_SEG + 16),
+        "qas": members_prof * (4 * K_SEG + 16),
         "release": 0,
     }
     dom = max(("commit", "build", "protect", "prematch", "qas"), key=lambda p: d[p]["ms"])
@@ -438,8 +454,7 @@ def run_ours(args) -> None:
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": dom, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
                 "algorithmic_bytes_per_launch": per_launch_bytes, "launch_ms": per_launch_s * 1000.0,
-                "phase_ms": {p: round(d[p]["ms"], 3) for p in d}}
-    gpu_launches = int(sum(d[p]["launches"] for p in d))
+                "phase_ms": {p: round(d[p]["ms"], 3) for p in d}, "profiled_waves": nprof}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
@@ -465,9 +480,10 @@ def run_ours(args) -> None:
                 "l2": "flushed between timed steps (256 MiB write)",
                 "tree_nodes": st2["live_nodes"], "resident_tokens": st2["resident"],
                 "warm_start_s": round(warm_s, 2), "admitted_per_rank": admitted,
-                "members_per_rank": members, "victims": victims,
+                "members_per_rank": members, "victims": st2["victims"] - st1["victims"],
                 "fast_path_members": st2["fast_members"] - st1["fast_members"],
                 "slow_path_members": st2["slow_members"] - st1["slow_members"],
+                "profile": "per-phase device profile taken on extra waves after the timed region",
                 "commit": engine.wave_stats(),
                 "last_list_build": engine.build_timeline(),
             },
