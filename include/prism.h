@@ -205,6 +205,8 @@ int prism_set_protection_device(prism_tree *t, const double *d_pri, int32_t nseg
  * (engine.py:195-197). */
 int prism_note_active_device(prism_tree *t, const int32_t *d_a, const int32_t *d_nd, int32_t nseg);
 int32_t prism_tree_policy(prism_tree *t);
+/* The cudaStream_t (as void*) the tree launches on (tree mutations, builds). */
+void *prism_tree_stream(prism_tree *t);
 /* The cudaStream_t (as void*) the QAS instance launches on; prism_wave_step
  * completes on it, so events recorded there bracket a whole wave. */
 void *prism_qas_stream(prism_qas *q);

@@ -889,9 +889,11 @@ __device__ inline int64_t ss_period(int32_t hw) {
 }
 
 template <class Cand>
-__global__ void __launch_bounds__(SS_TPB) k_ss_sample(Cand cand, CoopBufs B, int64_t W, int64_t min_cand) {
+__global__ void __launch_bounds__(SS_TPB) k_ss_sample(Cand cand, CoopBufs B, int64_t W, const int64_t *dW,
+                                                      int64_t min_cand) {
   __shared__ unsigned s_w[32];
   __shared__ unsigned long long s_base;
+  if (dW) W = *dW;
   const int32_t hw = cand.hw();
   if (W <= 0 || hw <= min_cand) return;  // nothing sampled: k_ss_select gives up
   const int64_t m = ss_period(hw), nsamp = ((int64_t)hw + m - 1) / m;
@@ -913,8 +915,9 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_sample(Cand cand, CoopBufs B, int
 }
 
 template <class Cand>
-__global__ void __launch_bounds__(SS_SEL_TPB) k_ss_select(Cand cand, CoopBufs B, int64_t W) {
+__global__ void __launch_bounds__(SS_SEL_TPB) k_ss_select(Cand cand, CoopBufs B, int64_t W, const int64_t *dW) {
   extern __shared__ __align__(16) unsigned char dsm[];
+  if (dW) W = *dW;
   __shared__ Key3 smin[33], smax[33];
   __shared__ unsigned s_hn[256];
   __shared__ unsigned s_hw[256];
@@ -1127,9 +1130,10 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_filter(Cand cand, CoopBufs B) {
     if (hcnt[q]) atomicAdd(&st->ss_cnt[q], hcnt[q]);
 }
 
-__global__ void __launch_bounds__(SS_TPB) k_ss_scatter(CoopBufs B, int64_t W) {
+__global__ void __launch_bounds__(SS_TPB) k_ss_scatter(CoopBufs B, int64_t W, const int64_t *dW) {
   __shared__ unsigned s_off[SS_SPL + 1];
   __shared__ unsigned long long s_tot[32];
+  if (dW) W = *dW;
   CoopState *st = B.st;
   const int nb = st->ss_nb;
   if (nb <= 0) return;
@@ -1234,9 +1238,13 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_sort(CoopBufs B, Key3 *kout, uint
 // order with >= W tokens sorted into the list -- finalised here when the
 // sample select succeeded (st->ss_ok), else by the materialising radix
 // selection (everything when W <= 0) -- one cooperative launch, no host round trip.
-__global__ void __launch_bounds__(COOP_TPB) k_build_coop(DT T, CoopBufs B, int64_t W, int64_t min_cand,
-                                                         int64_t small, int32_t sampled) {
+__global__ void __launch_bounds__(COOP_TPB) k_build_coop(DT T, CoopBufs B, int64_t W, const int64_t *dW,
+                                                         int64_t min_cand, int64_t small, int32_t sampled) {
   extern __shared__ __align__(16) unsigned char dsm[];
+  if (dW) {
+    W = *dW;
+    if (W < 0) return;  // device-side control: no eviction this wave, no list
+  }
   __shared__ Key3 smin[COOP_TPB + 1], smax[COOP_TPB + 1];
   cg::grid_group grid = cg::this_grid();
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gsz = (int64_t)gridDim.x * blockDim.x;

@@ -114,8 +114,10 @@ struct prism_tree {
   int64_t prof_calls[8] = {};
   int64_t launches[8] = {};  // own kernel launches per phase (always counted)
   int64_t lib_calls = 0;     // CUB primitive invocations
-  // parallel wave commit scratch
+  // parallel wave commit scratch and device-side control
   WaveTmp wx{};
+  WaveCtl *wc = nullptr, *h_wc = nullptr;
+  int64_t *ds_part = nullptr;
   int64_t wx_cap = 0, wx_lt = 0, wx_T = 0;
   int64_t par_waves = 0, seq_waves = 0;
   int32_t last_fallback = 0;
@@ -336,7 +338,7 @@ int coop_grid(prism_tree *t) {
 
 // the sample-select launches (coop.cuh) ahead of the cooperative finaliser
 template <class Cand>
-int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, int64_t min_cand) {
+int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const int64_t *dW, int64_t min_cand) {
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(k_ss_select<EvictCand>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SEL_SMEM));
@@ -346,10 +348,10 @@ int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, int64_
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev));
   cudaStream_t st = t->st;
-  k_ss_sample<Cand><<<SS_SAMP / SS_TPB, SS_TPB, 0, st>>>(cand, B, W, min_cand);
-  k_ss_select<Cand><<<1, SS_SEL_TPB, SS_SEL_SMEM, st>>>(cand, B, W);
+  k_ss_sample<Cand><<<SS_SAMP / SS_TPB, SS_TPB, 0, st>>>(cand, B, W, dW, min_cand);
+  k_ss_select<Cand><<<1, SS_SEL_TPB, SS_SEL_SMEM, st>>>(cand, B, W, dW);
   k_ss_filter<Cand><<<4 * sms, SS_TPB, SS_FILTER_SMEM, st>>>(cand, B);
-  k_ss_scatter<<<2 * sms, SS_TPB, 0, st>>>(B, W);
+  k_ss_scatter<<<2 * sms, SS_TPB, 0, st>>>(B, W, dW);
   k_ss_sort<<<SS_SPL, SS_TPB, SS_SORT_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
   CK(cudaGetLastError());
   return PRISM_OK;
@@ -362,8 +364,9 @@ CoopBufs coop_bufs(prism_tree *t) {
 
 // ------------------------------------------------------------ eviction order
 // Build the eviction order of the current tree, but only the prefix whose
-// tokens reach W (W <= 0: the whole order).
-int build_list(prism_tree *t, int64_t W) {
+// tokens reach W (W <= 0: the whole order).  dW (cooperative path only): W is
+// read on the device instead (< 0: no list is built at all).
+int build_list(prism_tree *t, int64_t W, const int64_t *dW = nullptr) {
   if (t->use_coop) {  // one cooperative kernel, no host round trip
     int grid = coop_grid(t);
     if (grid < 0) return PRISM_FATAL;
@@ -372,16 +375,17 @@ int build_list(prism_tree *t, int64_t W) {
     // keys / subtree maxima / gather at full occupancy over the slot range
     // (each reads hw from the control block; the count lands in cst->cand)
     const int64_t S = t->d.S;
-    k_build_keys<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1);
-    k_propagate<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1);
+    k_build_keys<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1, dW);
+    k_propagate<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1, dW);
     CoopBufs B = coop_bufs(t);
     int64_t minc = t->sel_min_candidates, small = std::min<int64_t>(SEL_SMALL, t->sel_min_candidates);
-    int32_t sampled = (t->use_sample && W > 0) ? 1 : 0;
+    int32_t sampled = (t->use_sample && (dW || W > 0)) ? 1 : 0;
     if (sampled) {
-      int rc = sample_select(t, EvictCand{t->d}, B, W, minc);
+      int rc = sample_select(t, EvictCand{t->d}, B, W, dW, minc);
       if (rc) return rc;
     }
-    void *args[] = {(void *)&t->d, (void *)&B, (void *)&W, (void *)&minc, (void *)&small, (void *)&sampled};
+    void *args[] = {(void *)&t->d, (void *)&B, (void *)&W, (void *)&dW, (void *)&minc, (void *)&small,
+                    (void *)&sampled};
     CK(cudaLaunchCooperativeKernel((void *)k_build_coop, grid, COOP_TPB, args, COOP_SMEM, t->st));
     t->launches[PH_BUILD] += 3 + (sampled ? 5 : 0);
     prof_end(t, PH_BUILD);
@@ -574,151 +578,101 @@ int cub_scan(prism_tree *t, In in, Out out, int64_t n, bool inclusive) {
   return PRISM_OK;
 }
 
-// Parallel commit of a segment-structured wave (wave_par.cuh).  Returns
-// PRISM_OK with *applied = 1 when the wave was committed, *applied = 0 when an
-// exactness guard tripped (nothing was mutated; the caller runs k_commit).
+// Parallel commit of a segment-structured wave (wave_par.cuh), driven on the
+// device: plan -> scans -> plan verdict (k_wc_plan: fallback flags, capacity
+// headroom, eviction demand) -> the eviction-order prefix it needs (read on
+// the device) -> victim cuts + verdict (k_wc_cut) -> apply -> control block
+// (k_wc_finalize), one stream of launches with a single host round trip at
+// the end.  Returns PRISM_OK with *applied = 1 when the wave was committed,
+// *applied = 0 when an exactness guard tripped (nothing was mutated; the
+// caller runs the ordered commit k_commit).  Capacity maintenance and a
+// prefix that fell short are handled between attempts.
 int admit_wave_par(prism_tree *t, const WaveIn &W, int64_t levels, int64_t *hits, int32_t *leaf_slots,
                    int64_t *leaf_ids, int *applied) {
   *applied = 0;
   const int64_t B = W.B;
-  int rc = pull_ctrl(t);
-  if (rc) return rc;
-  Ctrl &C = *t->hctrl;
-  C.epoch++;
-  const uint32_t epoch = C.epoch;
-  rc = push_ctrl(t);
-  if (rc) return rc;
-  rc = wx_ensure(t, B, levels, 1);
-  if (rc) return rc;
-  WaveTmp &X = t->wx;
   cudaStream_t st = t->st;
-  prof_begin(t);
-  CK(cudaMemsetAsync(X.lt_key, 0xFF, sizeof(uint64_t) * (size_t)t->wx_lt, st));
-  CK(cudaMemsetAsync(X.lt_min, 0x7F, sizeof(int32_t) * (size_t)t->wx_lt, st));
-  CK(cudaMemsetAsync(X.flags, 0, sizeof(int32_t), st));
-  CK(cudaMemsetAsync(X.cnew + B, 0, sizeof(int64_t), st));
-  CK(cudaMemsetAsync(X.tail + B, 0, sizeof(int64_t), st));
-  CK(cudaMemsetAsync(X.misc, 0, sizeof(int64_t) * 8, st));
-  const int64_t big = INT64_MAX;
-  CK(cudaMemcpyAsync(X.misc + 1, &big, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  k_wp_plan<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, epoch);
-  k_wp_hits<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X);
-  CK(cudaGetLastError());
-  t->launches[PH_COMMIT] += 2;
-  int32_t flags = 0;
-  CK(cudaMemcpyAsync(&flags, X.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (flags) {
-    t->last_fallback = flags;
-    return PRISM_OK;
+  if (!t->wc) {
+    CK(dalloc(&t->wc, 1));
+    CK(cudaMallocHost(&t->h_wc, sizeof(WaveCtl)));
+    CK(dalloc(&t->ds_part, DS_BLOCKS));
   }
-  if ((rc = cub_scan(t, X.cnew, X.idb, B + 1, false))) return rc;
-  if ((rc = cub_scan(t, X.tail, X.arb, B + 1, false))) return rc;
-  if ((rc = cub_scan(t, X.miss, X.dem, B, true))) return rc;
-  int64_t tot[3];
-  CK(cudaMemcpyAsync(&tot[0], X.idb + B, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&tot[1], X.arb + B, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&tot[2], X.dem + B - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  const int64_t ncreate = tot[0], ntail = tot[1], nmiss = tot[2];
-  // capacity maintenance (semantics-free): slots, arena, child table
-  if ((int64_t)C.hw + ncreate + 2 > t->d.S) {
-    if ((rc = grow_slots(t, (int64_t)C.hw + ncreate + 2))) return rc;
-    if ((rc = wx_ensure(t, B, levels, 1))) return rc;
-  }
-  if (C.arena_top + ntail > t->d.acap) {
-    if ((rc = compact_arena(t, ntail))) return rc;
-  }
-  if ((C.hlive + C.htomb + ncreate + 64) * 2 > (int64_t)(t->d.hmask + 1)) {
-    if ((rc = rehash(t, ncreate + 64))) return rc;
-  }
-  if ((rc = pull_ctrl(t))) return rc;
-  prof_end(t, PH_COMMIT);
-  const int64_t R0 = C.resident, D = R0 + nmiss - t->d.capacity;
-  int64_t nv = 0, freed = 0, calls = 0;
-  if (D > 0) {
-    std::vector<int64_t> cut((size_t)B);
-    int64_t poison = 0;
-    for (int attempt = 0; attempt < 2; attempt++) {
-      // the victims are a prefix of the eviction order: select just enough of
-      // it (D tokens plus slack); the complete order if that falls short
-      if ((rc = build_list(t, attempt == 0 ? D + D / 4 + t->list_slack_tokens : 0))) return rc;
-      if ((rc = pull_ctrl(t))) return rc;
-      const int64_t Tn = C.L_n;
-      if (Tn == 0) {
-        t->last_fallback = WPF_CAPACITY;
-        return PRISM_OK;
-      }
-      if ((rc = wx_ensure(t, B, levels, Tn))) return rc;
-      prof_begin(t);
-      CK(cudaMemsetAsync(X.flags, 0, sizeof(int32_t), st));
-      CK(cudaMemcpyAsync(X.misc + 1, &big, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-      k_wp_vlen<<<blocks_for(Tn), TPB, 0, st>>>(t->d, 0, Tn, X, epoch);
-      if ((rc = cub_scan(t, X.vlen, X.F, Tn, true))) return rc;
-      k_wp_cuts<<<blocks_for(B), TPB, 0, st>>>(B, X.dem, R0, t->d.capacity, X.F, Tn, X.cut, X.flags);
-      CK(cudaGetLastError());
-      t->launches[PH_COMMIT] += 2;
-      CK(cudaMemcpyAsync(cut.data(), X.cut, sizeof(int64_t) * B, cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(&flags, X.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(&poison, X.misc + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  int32_t force_full = 0;
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev));
+  for (int attempt = 0; attempt < 8; attempt++) {
+    int rc = wx_ensure(t, B, levels, t->d.S);  // eviction-stream buffers for any prefix length
+    if (rc) return rc;
+    WaveTmp &X = t->wx;
+    WaveCtl *wc = t->wc;
+    prof_begin(t);
+    CK(cudaMemsetAsync(X.lt_key, 0xFF, sizeof(uint64_t) * (size_t)t->wx_lt, st));
+    CK(cudaMemsetAsync(X.lt_min, 0x7F, sizeof(int32_t) * (size_t)t->wx_lt, st));
+    CK(cudaMemsetAsync(X.flags, 0, sizeof(int32_t), st));
+    CK(cudaMemsetAsync(X.misc, 0, sizeof(int64_t) * 8, st));
+    CK(cudaMemsetAsync(X.misc + 1, 0x7F, sizeof(int64_t), st));  // poison index: "none"
+    k_wc_begin<<<1, 1, 0, st>>>(t->d, wc);
+    k_wp_plan<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
+    k_wp_hits<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X);
+    k_wp_scan3<<<1, 1024, 0, st>>>(B, X);
+    k_wc_plan<<<1, 1, 0, st>>>(t->d, B, X, wc, t->list_slack_tokens, force_full);
+    CK(cudaGetLastError());
+    t->launches[PH_COMMIT] += 5;
+    prof_end(t, PH_COMMIT);
+    const int64_t *dW = &wc->W;
+    if (t->use_coop) {
+      if ((rc = build_list(t, 0, dW))) return rc;
+    } else {  // the multi-kernel build sizes its passes on the host: one round trip for W
+      CK(cudaMemcpyAsync(t->h_wc, wc, sizeof(WaveCtl), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
-      prof_end(t, PH_COMMIT);
-      if (!(flags & WPF_CAPACITY) || !C.L_partial) break;
+      if (!t->h_wc->stop && t->h_wc->W >= 0 && (rc = build_list(t, t->h_wc->W))) return rc;
     }
-    nv = cut[B - 1];
-    if (flags || poison < nv) {
-      t->last_fallback = flags ? flags : WPF_VICTIM;
-      return PRISM_OK;
+    prof_begin(t);
+    k_wp_vlen<<<2 * sms, TPB, 0, st>>>(t->d, X, wc);
+    const int64_t *dn = &t->d.ctrl->L_n;
+    k_dscan_a<<<DS_BLOCKS, 256, 0, st>>>(X.vlen, dn, t->ds_part, wc);
+    k_dscan_b<<<1, 1024, 0, st>>>(t->ds_part, DS_BLOCKS, wc);
+    k_dscan_c<<<DS_BLOCKS, 256, 0, st>>>(X.vlen, dn, t->ds_part, X.F, wc);
+    k_wp_cuts<<<blocks_for(B), TPB, 0, st>>>(t->d, B, X, wc);
+    k_wc_cut<<<1, 32, 0, st>>>(t->d, B, X, wc);
+    k_wp_evict<<<2 * sms, TPB, 0, st>>>(t->d, wc);
+    k_wp_alloc<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
+    k_wp_label_reset<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
+    k_wp_create<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, W, X, wc);
+    k_wp_touch<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
+    k_wp_label<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc, hits, leaf_slots, leaf_ids);
+    k_wc_finalize<<<1, 1, 0, st>>>(t->d, B, X, wc);
+    CK(cudaGetLastError());
+    t->launches[PH_COMMIT] += 14;
+    CK(cudaMemcpyAsync(t->h_wc, wc, sizeof(WaveCtl), cudaMemcpyDeviceToHost, st));
+    if ((rc = pull_ctrl(t))) return rc;  // the wave's one host round trip
+    prof_end(t, PH_COMMIT);
+    const WaveCtl &H = *t->h_wc;
+    switch (H.stop) {
+      case WC_OK:
+        t->last_fallback = 0;
+        *applied = 1;
+        return PRISM_OK;
+      case WC_FALLBACK:
+        t->last_fallback = H.flags;
+        return PRISM_OK;
+      case WC_FULL:  // the selected prefix fell short: select the whole order
+        force_full = 1;
+        break;
+      case WC_MAINT: {  // semantics-free capacity maintenance, then the same wave again
+        Ctrl &C = *t->hctrl;
+        if ((int64_t)C.hw + H.ncreate + 2 > t->d.S && (rc = grow_slots(t, (int64_t)C.hw + H.ncreate + 2))) return rc;
+        if (C.arena_top + H.ntail > t->d.acap && (rc = compact_arena(t, H.ntail))) return rc;
+        if ((C.hlive + C.htomb + H.ncreate + 64) * 2 > (int64_t)(t->d.hmask + 1) && (rc = rehash(t, H.ncreate + 64)))
+          return rc;
+        if ((rc = pull_ctrl(t))) return rc;
+        break;
+      }
+      default:
+        return fail(PRISM_FATAL, "unexpected wave control stop " + std::to_string(H.stop));
     }
-    for (int64_t j = 0; j < B; j++) calls += cut[j] > (j ? cut[j - 1] : 0);
-    if (nv > 0) CK(cudaMemcpyAsync(&freed, X.F + nv - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
   }
-  // ---- apply (from here on the wave is committed)
-  prof_begin(t);
-  const int64_t id0 = C.next_id, clock0 = C.clock, arena0 = C.arena_top;
-  const int32_t ft0 = C.free_top, hw0 = C.hw;
-  const uint32_t vctr0 = C.vctr;
-  if (nv > 0) {
-    k_wp_evict<<<blocks_for(nv), TPB, 0, st>>>(t->d, 0, nv, C.vlog_count, ft0, vctr0, epoch);
-    t->launches[PH_COMMIT]++;
-  }
-  const int32_t ft1 = ft0 + (int32_t)nv;
-  k_wp_alloc<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, id0, ft1, hw0, vctr0 + (uint32_t)nv, epoch);
-  k_wp_label_reset<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X);
-  k_wp_create<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, W, X, arena0, clock0);
-  k_wp_touch<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, clock0);
-  k_wp_label<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, hits, leaf_slots, leaf_ids);
-  CK(cudaGetLastError());
-  t->launches[PH_COMMIT] += 5;
-  int64_t reused = 0, acct[2] = {0, 0};
-  CK(cudaMemcpyAsync(&reused, X.misc + 2, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(acct, X.misc + 3, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  prof_end(t, PH_COMMIT);
-  const int64_t from_free = std::min<int64_t>(ncreate, ft1);
-  C.free_top = ft1 - (int32_t)from_free;
-  C.hw = hw0 + (int32_t)(ncreate - from_free);
-  C.resident = R0 + nmiss - freed;
-  C.clock = clock0 + 2 * B;
-  C.next_id = id0 + ncreate;
-  C.arena_top = arena0 + ntail;
-  C.vlog_count += nv;
-  C.hlive += ncreate - nv;
-  C.htomb += nv - reused;
-  C.evict_calls += calls;
-  C.vctr = vctr0 + (uint32_t)(nv + ncreate);
-  C.n_admitted = (int32_t)B;
-  C.fast_members += B;
-  C.inserted_tokens += acct[0];
-  C.chain_nodes += acct[1];
-  C.status = ST_DONE;
-  C.L_valid = 0;
-  C.H_n = 0;
-  rc = push_ctrl(t);
-  if (rc) return rc;
-  *applied = 1;
-  return PRISM_OK;
+  return fail(PRISM_FATAL, "parallel wave commit did not converge");
 }
 
 template <class T>
@@ -1014,7 +968,7 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out) {
     int64_t ff = f;
     int32_t sampled = (t->use_sample && f > 0) ? 1 : 0;
     if (sampled) {
-      rc = sample_select(t, ProtCand{t->d}, B, ff, minc);
+      rc = sample_select(t, ProtCand{t->d}, B, ff, nullptr, minc);
       if (rc) return rc;
       t->launches[PH_PROTECT] += 5;
     }
@@ -1121,6 +1075,8 @@ int prism_note_active_device(prism_tree *t, const int32_t *d_a, const int32_t *d
   CK(cudaGetLastError());
   return PRISM_OK;
 }
+
+void *prism_tree_stream(prism_tree *t) { return (void *)t->st; }
 
 int32_t prism_tree_policy(prism_tree *t) { return t->d.policy; }
 

@@ -818,7 +818,8 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
 // ------------------------------------------------------------ eviction-order build
 
 // (hw < 0: read the high-water mark from the control block -- no host sync)
-__global__ void k_build_keys(DT T, int32_t hw) {
+__global__ void k_build_keys(DT T, int32_t hw, const int64_t *dW = nullptr) {
+  if (dW && *dW < 0) return;  // device-side control: no eviction this wave
   if (hw < 0) hw = T.ctrl->hw;
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= hw) return;
@@ -834,7 +835,8 @@ __global__ void k_build_keys(DT T, int32_t hw) {
 // eff[v] = slot of the maximum key in v's subtree (EFF_BLOCKED if any node of
 // the subtree can never be evicted): each node carries its own value upward
 // until an ancestor already holds something at least as large.
-__global__ void k_propagate(DT T, int32_t hw) {
+__global__ void k_propagate(DT T, int32_t hw, const int64_t *dW = nullptr) {
+  if (dW && *dW < 0) return;
   if (hw < 0) hw = T.ctrl->hw;
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= hw || s == ROOT || T.nid[s] < 0 || T.par[s] < 0) return;

@@ -504,6 +504,7 @@ struct prism_qas {
   X(int64_t, cv2) \
   X(int64_t, small) \
   X(int32_t, err) \
+  X(int64_t, tmp_tot) \
   /* fused wave step: dispatch order, serialized paths and anchors */ \
   X(int64_t, members) \
   X(int64_t, plen) \
@@ -1068,21 +1069,78 @@ namespace {
 constexpr uint64_t SEGMENT_TOKEN_BASE = 1000000ull;
 constexpr uint64_t SUFFIX_TOKEN_BASE = 2000000000ull;
 
-__global__ void q_members(int64_t nh, int64_t nc, const int64_t *__restrict__ hot, const int64_t *__restrict__ cold,
-                          int64_t *__restrict__ members) {
+// the wave's dispatch order (hot lane, then cold) with each member's path and
+// anchor counts, and the uint32 token-layout check of its private suffix
+// (workload.py:147-154), before anything is serialised
+__global__ void q_members_len(int64_t nh, int64_t nc, const int64_t *__restrict__ hot,
+                              const int64_t *__restrict__ cold, const int64_t *__restrict__ ids,
+                              const int64_t *__restrict__ off, const int32_t *__restrict__ suffix, int64_t sys,
+                              int64_t chunk, int64_t *__restrict__ members, int64_t *__restrict__ plen,
+                              int64_t *__restrict__ alen, int32_t *err) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nh) members[i] = hot[i];
-  else if (i < nh + nc) members[i] = cold[i - nh];
+  if (i >= nh + nc) return;
+  const int64_t m = i < nh ? hot[i] : cold[i - nh];
+  members[i] = m;
+  const int64_t k = off[m + 1] - off[m], sfx = suffix[m];
+  plen[i] = sys + k * chunk + sfx;
+  alen[i] = (sys > 0 ? 1 : 0) + k + (sfx > 0 ? 1 : 0);
+  if (SUFFIX_TOKEN_BASE + (uint64_t)ids[m] * (uint64_t)sfx + (uint64_t)sfx > 0xFFFFFFFFull) *err = 2;
 }
 
-__global__ void q_serial_len(int64_t B, const int64_t *__restrict__ members, const int64_t *__restrict__ off,
-                             const int32_t *__restrict__ suffix, int64_t sys, int64_t chunk,
-                             int64_t *__restrict__ plen, int64_t *__restrict__ alen) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= B) return;
-  const int64_t m = members[i], k = off[m + 1] - off[m];
-  plen[i] = sys + k * chunk + suffix[m];
-  alen[i] = (sys > 0 ? 1 : 0) + k + (suffix[m] > 0 ? 1 : 0);
+// exclusive scans plen -> poff and alen -> aoffs over B + 1 entries (the last
+// input entry is 0), one CTA
+__global__ void __launch_bounds__(1024) q_scan2(int64_t B, const int64_t *__restrict__ plen,
+                                                const int64_t *__restrict__ alen, int64_t *__restrict__ poff,
+                                                int64_t *__restrict__ aoffs, int64_t *__restrict__ tot) {
+  __shared__ int64_t s_w[2][32];
+  __shared__ int64_t s_carry[2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x < 2) s_carry[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t b0 = 0; b0 <= B; b0 += blockDim.x) {
+    const int64_t j = b0 + threadIdx.x;
+    const int64_t v0 = j < B ? plen[j] : 0, v1 = j < B ? alen[j] : 0;
+    int64_t x0 = v0, x1 = v1;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y0 = __shfl_up_sync(0xffffffffu, x0, o), y1 = __shfl_up_sync(0xffffffffu, x1, o);
+      if (lane >= o) {
+        x0 += y0;
+        x1 += y1;
+      }
+    }
+    if (lane == 31) {
+      s_w[0][wid] = x0;
+      s_w[1][wid] = x1;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      for (int a = 0; a < 2; a++) {
+        int64_t t = lane < nw ? s_w[a][lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int64_t y = __shfl_up_sync(0xffffffffu, t, o);
+          if (lane >= o) t += y;
+        }
+        if (lane < nw) s_w[a][lane] = t;
+      }
+    }
+    __syncthreads();
+    const int64_t i0 = s_carry[0] + x0 + (wid ? s_w[0][wid - 1] : 0);
+    const int64_t i1 = s_carry[1] + x1 + (wid ? s_w[1][wid - 1] : 0);
+    if (j <= B) {
+      poff[j] = i0 - v0;
+      aoffs[j] = i1 - v1;
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) {
+      s_carry[0] = i0;
+      s_carry[1] = i1;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    tot[0] = s_carry[0];
+    tot[1] = s_carry[1];
+  }
 }
 
 // one warp per member: token path and anchors
@@ -1104,8 +1162,7 @@ __global__ void q_serialize(int64_t B, const int64_t *__restrict__ members, cons
     const int64_t r = aligned[b + j / chunk];
     p[sys + j] = (uint32_t)(SEGMENT_TOKEN_BASE + (uint64_t)r * chunk + (uint64_t)(j % chunk));
   }
-  const uint64_t sb = SUFFIX_TOKEN_BASE + (uint64_t)ids[m] * (uint64_t)sfx;
-  if (lane == 0 && sb + sfx > 0xFFFFFFFFull) *err = 2;  // token layout must fit uint32
+  const uint64_t sb = SUFFIX_TOKEN_BASE + (uint64_t)ids[m] * (uint64_t)sfx;  // (checked by q_members_len)
   for (int64_t j = lane; j < sfx; j += 32) p[sys + k * chunk + j] = (uint32_t)(sb + j);
   if (lane == 0) {
     int64_t q = aoffs[w];
@@ -1134,14 +1191,7 @@ __global__ void q_serialize(int64_t B, const int64_t *__restrict__ members, cons
   }
 }
 
-int scan64(prism_qas *q, const int64_t *in, int64_t *out, int64_t n) {
-  size_t bytes = 0;
-  QCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)n, q->st));
-  if (ensure_tmp(q, bytes)) return PRISM_CUDA;
-  bytes = q->tmp_bytes;
-  QCK(cub::DeviceScan::ExclusiveSum(q->tmp, bytes, in, out, (int)n, q->st));
-  return PRISM_OK;
-}
+
 
 }  // namespace
 
@@ -1212,72 +1262,94 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
                     const prism_qas_config *cfg, int64_t sys_len, int64_t chunk, int64_t *members_out,
                     int64_t *hits, int32_t *leaf_slots, int64_t *leaf_ids, int64_t *n_members,
                     int64_t *n_admitted) {
+  if (cfg->cold_quota > cfg->dispatch_budget || cfg->signature_size < 1 ||
+      cfg->front_width < cfg->signature_size || cfg->signature_size > QMAXK)
+    return qfail(PRISM_INVALID, "invalid SchedulerConfig");
   cudaSetDevice(q->dev);
   cudaStream_t st = q->st;
+  const QCfg c{cfg->dispatch_budget, cfg->cold_quota, cfg->front_width, cfg->signature_size,
+               cfg->w_g, cfg->w_a, cfg->w_n, cfg->alpha_size, cfg->beta_util};
+  const QIn in{ids, arrival, sk_off, sk, reorderable, act_off, act_sk};
   int64_t nh = 0, nc = 0, nb = 0;
   if (q->prof_on) cudaEventRecord(q->e0, st);
-  int rc = prism_qas_round_device(q, P, ids, arrival, sk_off, sk, reorderable, A, act_off, act_sk, nseg, cfg, &nh,
-                                  &nc, &nb);  // (one-CTA rounds sync here for the bucket count / redo flag)
+  // QAS round (engine.py:189): one launch for the one-CTA/cooperative round
+  int rc = qas_run(q, in, P, A, nseg, c, &nh, &nc, &nb);
   if (rc) return rc;
-  if (q->prof_on) {
-    cudaEventRecord(q->e1, st);
-    cudaEventSynchronize(q->e1);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, q->e0, q->e1);
-    q->ms_round += ms;
-  }
-  const int64_t B = nh + nc;
-  *n_members = B;
-  *n_admitted = 0;
-  if (B == 0) return PRISM_OK;  // engine.py:190-191
-  // protection / active hand-off (engine.py:193-197)
-  const int32_t pol = prism_tree_policy(t);
-  QCK(cudaStreamSynchronize(st));
-  if (pol == 0) {
-    rc = prism_set_protection_device(t, q->prio, nseg, nullptr, nullptr);
-  } else if (pol == 2) {
-    rc = prism_note_active_device(t, q->a, q->nd, nseg);
-  }
-  if (rc) return rc;
-  // dispatch order and serialization (K1)
+  // dispatch order, path/anchor sizes and their offsets; ONE host round trip
+  // for the sizes, the one-launch round's redo flag and the layout check
   int64_t *members = members_out;
+  const int64_t Pc = std::max<int64_t>(P, 1);
   if (!members) {
-    QCK(grow(&q->members, q->members_cap, B));
+    QCK(grow(&q->members, q->members_cap, Pc));
     members = q->members;
   }
-  q_members<<<nblk(B), TPB, 0, st>>>(nh, nc, q->hot, q->cv2, members);
-  QCK(grow(&q->plen, q->plen_cap, B + 1));
-  QCK(grow(&q->poff, q->poff_cap, B + 1));
-  QCK(grow(&q->alen, q->alen_cap, B + 1));
-  QCK(grow(&q->aoffs, q->aoffs_cap, B + 1));
-  QCK(cudaMemsetAsync(q->plen + B, 0, sizeof(int64_t), st));
-  QCK(cudaMemsetAsync(q->alen + B, 0, sizeof(int64_t), st));
-  q_serial_len<<<nblk(B), TPB, 0, st>>>(B, members, sk_off, suffix, sys_len, chunk, q->plen, q->alen);
-  if ((rc = scan64(q, q->plen, q->poff, B + 1))) return rc;
-  if ((rc = scan64(q, q->alen, q->aoffs, B + 1))) return rc;
-  int64_t tot[2];
-  QCK(cudaMemcpyAsync(&tot[0], q->poff + B, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  QCK(cudaMemcpyAsync(&tot[1], q->aoffs + B, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  QCK(cudaMemsetAsync(q->err, 0, sizeof(int32_t), st));
-  QCK(cudaStreamSynchronize(st));
-  QCK(grow(&q->tok, q->tok_cap, std::max<int64_t>(tot[0], 1)));
-  QCK(grow(&q->a_off, q->a_off_cap, std::max<int64_t>(tot[1], 1)));
-  QCK(grow(&q->a_kind, q->a_kind_cap, std::max<int64_t>(tot[1], 1)));
-  QCK(grow(&q->a_seg, q->a_seg_cap, std::max<int64_t>(tot[1], 1)));
-  QCK(grow(&q->a_snap, q->a_snap_cap, 3 * std::max<int64_t>(tot[1], 1)));
-  q_serialize<<<nblk(B * 32), TPB, 0, st>>>(B, members, ids, sk_off, q->aligned, suffix, sys_len, chunk, q->g, q->a,
-                                            q->nd, q->poff, q->aoffs, q->tok, q->a_off, q->a_kind, q->a_seg,
-                                            q->a_snap, q->err);
-  QCK(cudaGetLastError());
-  q->launches += 3;
-  q->lib_calls += 2;
-  int32_t err = 0;
-  QCK(cudaMemcpyAsync(&err, q->err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  QCK(cudaStreamSynchronize(st));
-  if (err) return qfail(PRISM_INVALID, "token layout overflows uint32");
-  return prism_admit_wave_segmented(t, B, q->poff, q->tok, q->aoffs, q->a_off, q->a_kind, q->a_seg, q->a_snap,
-                                    members, sk_off, q->aligned, sys_len, chunk, q->commit_mode, hits, leaf_slots,
-                                    leaf_ids, n_admitted, (void *)st);
+  QCK(grow(&q->plen, q->plen_cap, Pc + 1));
+  QCK(grow(&q->poff, q->poff_cap, Pc + 1));
+  QCK(grow(&q->alen, q->alen_cap, Pc + 1));
+  QCK(grow(&q->aoffs, q->aoffs_cap, Pc + 1));
+  QCK(grow(&q->err, q->err_cap, 4));
+  QCK(grow(&q->tmp_tot, q->tmp_tot_cap, 2));
+  for (int pass = 0; pass < 2; pass++) {
+    const int64_t B = nh + nc;
+    if (B > 0) {
+      QCK(cudaMemsetAsync(q->err, 0, sizeof(int32_t), st));
+      q_members_len<<<nblk(B), TPB, 0, st>>>(nh, nc, q->hot, q->cv2, ids, sk_off, suffix, sys_len, chunk, members,
+                                             q->plen, q->alen, q->err);
+      q_scan2<<<1, 1024, 0, st>>>(B, q->plen, q->alen, q->poff, q->aoffs, q->tmp_tot);
+      q->launches += 2;
+    }
+    int64_t hb[6] = {0, 0, 0, 0, 0, 0};  // qcounts[2..3], tokens, anchors, err
+    if (nb < 0) QCK(cudaMemcpyAsync(hb, q->qcounts + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    if (B > 0) {
+      QCK(cudaMemcpyAsync(hb + 2, q->tmp_tot, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      QCK(cudaMemcpyAsync(hb + 4, q->err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    }
+    QCK(cudaStreamSynchronize(st));
+    if (nb < 0 && hb[1]) {  // the one-launch round overflowed its buffers: the multi-kernel round
+      if ((rc = qas_rerun_multi(q, in, P, A, nseg, c, &nh, &nc, &nb))) return rc;
+      continue;
+    }
+    if (q->prof_on) {
+      cudaEventRecord(q->e1, st);
+      cudaEventSynchronize(q->e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, q->e0, q->e1);
+      q->ms_round += ms;
+    }
+    *n_members = B;
+    *n_admitted = 0;
+    if (B == 0) return PRISM_OK;  // engine.py:190-191
+    if ((int32_t)hb[4]) return qfail(PRISM_INVALID, "token layout overflows uint32");
+    const int64_t ntok = hb[2], nanc = hb[3];
+    // protection / active hand-off (engine.py:193-197), ordered after the round
+    // on the tree's stream by an event (no host wait)
+    {
+      cudaEvent_t ev;
+      QCK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      QCK(cudaEventRecord(ev, st));
+      QCK(cudaStreamWaitEvent((cudaStream_t)prism_tree_stream(t), ev, 0));
+      QCK(cudaEventDestroy(ev));
+    }
+    const int32_t pol = prism_tree_policy(t);
+    if (pol == 0) rc = prism_set_protection_device(t, q->prio, nseg, nullptr, nullptr);
+    else if (pol == 2) rc = prism_note_active_device(t, q->a, q->nd, nseg);
+    if (rc) return rc;
+    // serialization (K1), then the admission on the tree's stream
+    QCK(grow(&q->tok, q->tok_cap, std::max<int64_t>(ntok, 1)));
+    QCK(grow(&q->a_off, q->a_off_cap, std::max<int64_t>(nanc, 1)));
+    QCK(grow(&q->a_kind, q->a_kind_cap, std::max<int64_t>(nanc, 1)));
+    QCK(grow(&q->a_seg, q->a_seg_cap, std::max<int64_t>(nanc, 1)));
+    QCK(grow(&q->a_snap, q->a_snap_cap, 3 * std::max<int64_t>(nanc, 1)));
+    q_serialize<<<nblk(B * 32), TPB, 0, st>>>(B, members, ids, sk_off, q->aligned, suffix, sys_len, chunk, q->g,
+                                              q->a, q->nd, q->poff, q->aoffs, q->tok, q->a_off, q->a_kind, q->a_seg,
+                                              q->a_snap, q->err);
+    QCK(cudaGetLastError());
+    q->launches += 1;
+    return prism_admit_wave_segmented(t, B, q->poff, q->tok, q->aoffs, q->a_off, q->a_kind, q->a_seg, q->a_snap,
+                                      members, sk_off, q->aligned, sys_len, chunk, q->commit_mode, hits, leaf_slots,
+                                      leaf_ids, n_admitted, (void *)st);
+  }
+  return qfail(PRISM_FATAL, "QAS round did not converge");
 }
 
 // rounds over <= max_p pending requests with integral weights run in one CTA

@@ -65,6 +65,20 @@ struct WaveTmp {
   int64_t *misc;                     // [8] device scalars
 };
 
+// device-side control of one parallel wave commit: the control-block snapshot
+// the wave starts from, its totals, and the stop decision -- so the whole
+// commit is one stream of launches with no host round trip in the middle
+enum { WC_OK = 0, WC_FALLBACK = 1, WC_MAINT = 2, WC_FULL = 3 };
+struct WaveCtl {
+  int64_t R0, id0, clock0, arena0, vbase;  // snapshot of the control block
+  int64_t ncreate, ntail, nmiss;           // totals of the plan
+  int64_t W;                               // eviction-prefix tokens to select (-1: no eviction)
+  int64_t nv, freed, calls;                // victims consumed, their tokens, evict calls
+  int32_t ft0, hw0;
+  uint32_t vctr0, epoch;
+  int32_t stop, flags;                     // WC_*; fallback reason (WPF_*)
+};
+
 __device__ inline int64_t wp_end(const WaveIn &W, int p, int k, int64_t n) {
   // end depth of piece p: [sys][seg 0..k-1][suffix]
   const int has_sys = W.sys > 0;
@@ -106,9 +120,10 @@ __device__ inline int32_t wp_table(const WaveTmp &X, uint64_t key, int32_t j, bo
 }
 
 // W1: per-member plan checks + skeleton-prefix ownership table
-__global__ void k_wp_plan(DT T, WaveIn W, WaveTmp X, uint32_t epoch) {
+__global__ void k_wp_plan(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= W.B) return;
+  const uint32_t epoch = wc->epoch;
   const int64_t m = W.members[j];
   const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
   const int32_t *s = W.aligned + W.sk_off[m];
@@ -208,71 +223,76 @@ __global__ void k_wp_hits(DT T, WaveIn W, WaveTmp X) {
 // eviction stream prefix: token length of each list entry; misc[1] = first
 // entry that a member's pin or guard would make non-evictable (list entries
 // with children are fine: the stream puts every descendant first)
-__global__ void k_wp_vlen(DT T, int64_t T0, int64_t Tn, WaveTmp X, uint32_t epoch) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= Tn) return;
-  const uint64_t v = T.Lv[T0 + i];
-  const int32_t s = (int32_t)(v & 0xffffffffu);
-  const bool valid = T.kver[s] == (uint32_t)(v >> 32) && T.nid[s] >= 0 && T.par[s] >= 0 && T.ref[s] == 0;
-  X.vlen[i] = valid ? T.elen[s] : 0;
-  if (!valid || T.wchild[s] == epoch) atomicMin((unsigned long long *)&X.misc[1], (unsigned long long)i);
+__global__ void k_wp_vlen(DT T, WaveTmp X, const WaveCtl *wc) {
+  if (wc->stop || wc->W < 0) return;
+  const int64_t Tn = T.ctrl->L_n;
+  const uint32_t epoch = wc->epoch;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Tn; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = T.Lv[i];
+    const int32_t s = (int32_t)(v & 0xffffffffu);
+    const bool valid = T.kver[s] == (uint32_t)(v >> 32) && T.nid[s] >= 0 && T.par[s] >= 0 && T.ref[s] == 0;
+    X.vlen[i] = valid ? T.elen[s] : 0;
+    if (!valid || T.wchild[s] == epoch) atomicMin((unsigned long long *)&X.misc[1], (unsigned long long)i);
+  }
 }
 
 // per member: number of list entries consumed through member j (first F >= D_j)
-__global__ void k_wp_cuts(int64_t B, const int64_t *__restrict__ dem, int64_t R0, int64_t cap,
-                          const int64_t *__restrict__ F, int64_t Tn, int64_t *__restrict__ cut,
-                          int32_t *flags) {
+__global__ void k_wp_cuts(DT T, int64_t B, WaveTmp X, const WaveCtl *wc) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= B) return;
-  const int64_t D = R0 + dem[j] - cap;  // dem = inclusive sum of missing
+  if (j >= B || wc->stop) return;
+  const int64_t D = wc->R0 + X.dem[j] - T.capacity;  // dem = inclusive sum of missing
   int64_t c = 0;
   if (D > 0) {
+    const int64_t Tn = T.ctrl->L_n;
     int64_t lo = 0, hi = Tn;  // first idx with F[idx] >= D
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
-      if (F[mid] >= D) hi = mid;
+      if (X.F[mid] >= D) hi = mid;
       else lo = mid + 1;
     }
     if (lo >= Tn) {
-      atomicOr(flags, WPF_CAPACITY);
+      atomicOr(X.flags, WPF_CAPACITY);
       c = Tn;
     } else {
       c = lo + 1;
     }
   }
-  cut[j] = c;
+  X.cut[j] = c;
 }
 
 // apply the consumed victims [0, nv) of the stream (stream order == victim order)
-__global__ void k_wp_evict(DT T, int64_t T0, int64_t nv, int64_t vbase, int32_t free_top0, uint32_t vctr0,
-                           uint32_t epoch) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nv) return;
-  const int32_t s = (int32_t)(T.Lv[T0 + i] & 0xffffffffu);
-  const int32_t p = T.par[s];
-  atomicSub(&T.nch[p], 1);
-  VRec rec;
-  rec.id = T.nid[s];
-  rec.eoff = T.eoff[s];
-  rec.ftok = T.ftok[s];
-  rec.elen = T.elen[s];
-  rec.seg = T.seg[s];
-  rec.kind = (int8_t)T.kind[s];
-  rec.pad[0] = rec.pad[1] = rec.pad[2] = 0;
-  T.ht[T.hslot[s]].key = HTOMB;
-  T.vlog[(vbase + i) % T.vcap] = rec;
-  T.nid[s] = -1;
-  T.par[s] = -1;
-  T.kver[s] = vctr0 + (uint32_t)i + 1;
-  T.wmod[s] = epoch;
-  T.freelist[free_top0 + i] = s;
+__global__ void k_wp_evict(DT T, const WaveCtl *wc) {
+  if (wc->stop) return;
+  const int64_t nv = wc->nv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = (int32_t)(T.Lv[i] & 0xffffffffu);
+    const int32_t p = T.par[s];
+    atomicSub(&T.nch[p], 1);
+    VRec rec;
+    rec.id = T.nid[s];
+    rec.eoff = T.eoff[s];
+    rec.ftok = T.ftok[s];
+    rec.elen = T.elen[s];
+    rec.seg = T.seg[s];
+    rec.kind = (int8_t)T.kind[s];
+    rec.pad[0] = rec.pad[1] = rec.pad[2] = 0;
+    T.ht[T.hslot[s]].key = HTOMB;
+    T.vlog[(wc->vbase + i) % T.vcap] = rec;
+    T.nid[s] = -1;
+    T.par[s] = -1;
+    T.kver[s] = wc->vctr0 + (uint32_t)i + 1;
+    T.wmod[s] = wc->epoch;
+    T.freelist[wc->ft0 + i] = s;
+  }
 }
 
 // W6a: slot of every new piece (free list LIFO, then the high-water mark)
-__global__ void k_wp_alloc(DT T, WaveIn W, WaveTmp X, int64_t id0, int32_t free_top, int32_t hw,
-                           uint32_t vctr0, uint32_t epoch) {
+__global__ void k_wp_alloc(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= W.B || X.cnew[j] == 0) return;
+  if (j >= W.B || wc->stop || X.cnew[j] == 0) return;
+  const int64_t id0 = wc->id0;
+  const int32_t free_top = wc->ft0 + (int32_t)wc->nv, hw = wc->hw0;
+  const uint32_t vctr0 = wc->vctr0 + (uint32_t)wc->nv, epoch = wc->epoch;
   const int P = X.npieces[j], p0 = X.p0[j];
   const int64_t g0 = X.idb[j];  // global index of this member's first new piece
   for (int p = p0; p < P; p++) {
@@ -303,10 +323,11 @@ __device__ inline int32_t wp_node(const WaveIn &W, const WaveTmp &X, int64_t j, 
 }
 
 // W6b: fields, child-table entries and tokens of the new pieces (warp per member)
-__global__ void k_wp_create(DT T, WaveIn W, WaveTmp X, int64_t arena0, int64_t clock0) {
+__global__ void k_wp_create(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = lane_id();
-  if (j >= W.B || X.cnew[j] == 0) return;
+  if (j >= W.B || wc->stop || X.cnew[j] == 0) return;
+  const int64_t arena0 = wc->arena0, clock0 = wc->clock0;
   const int64_t m = W.members[j];
   const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
   const int64_t n = W.poff[j + 1] - W.poff[j];
@@ -351,9 +372,10 @@ __global__ void k_wp_create(DT T, WaveIn W, WaveTmp X, int64_t arena0, int64_t c
 }
 
 // W7: touches of pre-existing nodes, pins, and last-writer label election
-__global__ void k_wp_touch(DT T, WaveIn W, WaveTmp X, int64_t clock0) {
+__global__ void k_wp_touch(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= W.B) return;
+  if (j >= W.B || wc->stop) return;
+  const int64_t clock0 = wc->clock0;
   const int P = X.npieces[j];
   const int own0 = X.cnew[j] ? X.p0[j] : P;
   const unsigned long long tick = (unsigned long long)(clock0 + 2 * j + 2);
@@ -369,17 +391,18 @@ __global__ void k_wp_touch(DT T, WaveIn W, WaveTmp X, int64_t clock0) {
   atomicAdd(&T.ref[ROOT], 1);  // _pin reaches the root (kvcache.py:344-348)
 }
 
-__global__ void k_wp_label_reset(DT T, WaveIn W, WaveTmp X) {
+__global__ void k_wp_label_reset(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= W.B) return;
+  if (j >= W.B || wc->stop) return;
   const int own0 = X.cnew[j] ? X.p0[j] : X.npieces[j];
   for (int p = 0; p < own0; p++) T.eff[wp_node(W, X, j, p)] = -1;
 }
 
 // W8: the elected (max-index) member writes kind/seg/anchor (kvcache.py:317-340)
-__global__ void k_wp_label(DT T, WaveIn W, WaveTmp X, int64_t *hits, int32_t *leaf_slots, int64_t *leaf_ids) {
+__global__ void k_wp_label(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc, int64_t *hits, int32_t *leaf_slots,
+                           int64_t *leaf_ids) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= W.B) return;
+  if (j >= W.B || wc->stop) return;
   const int64_t m = W.members[j];
   const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
   const int64_t n = W.poff[j + 1] - W.poff[j];
@@ -402,6 +425,226 @@ __global__ void k_wp_label(DT T, WaveIn W, WaveTmp X, int64_t *hits, int32_t *le
   if (hits) hits[j] = X.hit[j];
   if (leaf_slots) leaf_slots[j] = leaf;
   if (leaf_ids) leaf_ids[j] = T.nid[leaf];
+}
+
+
+// ------------------------------------------------------------ device-side control
+
+// epoch + control-block snapshot the wave commits from
+__global__ void k_wc_begin(DT T, WaveCtl *wc) {
+  Ctrl *C = T.ctrl;
+  C->epoch++;
+  WaveCtl w{};
+  w.epoch = C->epoch;
+  w.R0 = C->resident;
+  w.id0 = C->next_id;
+  w.clock0 = C->clock;
+  w.arena0 = C->arena_top;
+  w.vbase = C->vlog_count;
+  w.ft0 = C->free_top;
+  w.hw0 = C->hw;
+  w.vctr0 = C->vctr;
+  w.W = -1;
+  *wc = w;
+}
+
+// exclusive scans cnew -> idb, tail -> arb (B + 1 entries) and the inclusive
+// scan miss -> dem (B entries), one CTA
+__global__ void __launch_bounds__(1024) k_wp_scan3(int64_t B, WaveTmp X) {
+  __shared__ int64_t s_w[3][32];
+  __shared__ int64_t s_carry[3];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x < 3) s_carry[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t b0 = 0; b0 <= B; b0 += blockDim.x) {
+    const int64_t j = b0 + threadIdx.x;
+    int64_t v[3] = {j < B ? X.cnew[j] : 0, j < B ? X.tail[j] : 0, j < B ? X.miss[j] : 0};
+    int64_t x[3] = {v[0], v[1], v[2]};
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x[a], o);
+        if (lane >= o) x[a] += y;
+      }
+      if (lane == 31) s_w[a][wid] = x[a];
+    }
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        int64_t t = lane < nw ? s_w[a][lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int64_t y = __shfl_up_sync(0xffffffffu, t, o);
+          if (lane >= o) t += y;
+        }
+        if (lane < nw) s_w[a][lane] = t;
+      }
+    }
+    __syncthreads();
+    int64_t incl[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) incl[a] = s_carry[a] + x[a] + (wid ? s_w[a][wid - 1] : 0);
+    if (j <= B) {
+      X.idb[j] = incl[0] - v[0];
+      X.arb[j] = incl[1] - v[1];
+    }
+    if (j < B) X.dem[j] = incl[2];
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1)
+#pragma unroll
+      for (int a = 0; a < 3; a++) s_carry[a] = incl[a];
+    __syncthreads();
+  }
+}
+
+// plan verdict: fallback flags, capacity headroom (slots, arena, child table),
+// and the eviction demand -> the prefix of the order to select (-1: none)
+__global__ void k_wc_plan(DT T, int64_t B, WaveTmp X, WaveCtl *wc, int64_t slack, int32_t force_full) {
+  const int32_t flags = *X.flags;
+  if (flags) {
+    wc->stop = WC_FALLBACK;
+    wc->flags = flags;
+    wc->W = -1;
+    return;
+  }
+  const int64_t ncreate = X.idb[B], ntail = X.arb[B], nmiss = X.dem[B - 1];
+  wc->ncreate = ncreate;
+  wc->ntail = ntail;
+  wc->nmiss = nmiss;
+  const Ctrl *C = T.ctrl;
+  if ((int64_t)wc->hw0 + ncreate + 2 > (int64_t)T.S || wc->arena0 + ntail > T.acap ||
+      (C->hlive + C->htomb + ncreate + 64) * 2 > (int64_t)(T.hmask + 1)) {
+    wc->stop = WC_MAINT;
+    wc->W = -1;
+    return;
+  }
+  const int64_t D = wc->R0 + nmiss - T.capacity;
+  wc->W = D > 0 ? (force_full ? 0 : D + D / 4 + slack) : -1;
+}
+
+// the victims: nv = entries consumed through the last member, checks that the
+// prefix sufficed and that no consumed entry is pinned/guarded; the number of
+// evict calls (members whose cut advances) and the tokens freed
+__global__ void k_wc_cut(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
+  if (wc->stop) return;
+  const int lane = threadIdx.x;
+  int64_t calls = 0;
+  for (int64_t j = lane; j < B; j += 32) calls += X.cut[j] > (j ? X.cut[j - 1] : 0) ? 1 : 0;
+  for (int o = 16; o > 0; o >>= 1) calls += __shfl_xor_sync(0xffffffffu, calls, o);
+  if (lane) return;
+  const int64_t nv = X.cut[B - 1];
+  const int32_t flags = *X.flags;
+  const int64_t poison = X.misc[1];
+  if (flags & WPF_CAPACITY) {
+    if (T.ctrl->L_partial) {
+      wc->stop = WC_FULL;  // the selected prefix fell short: the whole order
+    } else {
+      wc->stop = WC_FALLBACK;
+      wc->flags = flags;
+    }
+    return;
+  }
+  if (flags || poison < nv) {
+    wc->stop = WC_FALLBACK;
+    wc->flags = flags ? flags : WPF_VICTIM;
+    return;
+  }
+  wc->nv = nv;
+  wc->calls = calls;
+  wc->freed = nv > 0 ? X.F[nv - 1] : 0;
+}
+
+// the control block after the committed wave (what the ordered commit leaves)
+__global__ void k_wc_finalize(DT T, int64_t B, WaveTmp X, const WaveCtl *wc) {
+  if (wc->stop) return;
+  Ctrl *C = T.ctrl;
+  const int64_t nv = wc->nv, ncreate = wc->ncreate;
+  const int32_t ft1 = wc->ft0 + (int32_t)nv;
+  const int64_t from_free = ncreate < ft1 ? ncreate : ft1;
+  const int64_t reused = X.misc[2];
+  C->free_top = ft1 - (int32_t)from_free;
+  C->hw = wc->hw0 + (int32_t)(ncreate - from_free);
+  C->resident = wc->R0 + wc->nmiss - wc->freed;
+  C->clock = wc->clock0 + 2 * B;
+  C->next_id = wc->id0 + ncreate;
+  C->arena_top = wc->arena0 + wc->ntail;
+  C->vlog_count += nv;
+  C->hlive += ncreate - nv;
+  C->htomb += nv - reused;
+  C->evict_calls += wc->calls;
+  C->vctr = wc->vctr0 + (uint32_t)(nv + ncreate);
+  C->n_admitted = (int32_t)B;
+  C->fast_members += B;
+  C->inserted_tokens += X.misc[3];
+  C->chain_nodes += X.misc[4];
+  C->status = ST_DONE;
+  C->L_valid = 0;
+  C->H_n = 0;
+}
+
+// inclusive scan of in[0..n) -> out with n read on the device (*dn), three
+// launches: per-block sums, a scan of the sums, per-block rescans; skipped
+// when skip && (*skip < 0 || stop)
+constexpr int DS_BLOCKS = 296;
+__global__ void __launch_bounds__(256) k_dscan_a(const int64_t *in, const int64_t *dn, int64_t *part,
+                                                 const WaveCtl *wc) {
+  if (wc && (wc->stop || wc->W < 0)) return;
+  const int64_t n = *dn, per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * per, b1 = b0 + per < n ? b0 + per : n;
+  int64_t s = 0;
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) s += in[i];
+  __shared__ int64_t sw[8];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += sw[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_dscan_b(int64_t *part, int nparts, const WaveCtl *wc) {
+  if (wc && (wc->stop || wc->W < 0)) return;
+  __shared__ int64_t s[1024];
+  const int i = threadIdx.x;
+  s[i] = i < nparts ? part[i] : 0;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+    const int64_t y = i >= o ? s[i - o] : 0;
+    __syncthreads();
+    s[i] += y;
+    __syncthreads();
+  }
+  if (i < nparts) part[i] = s[i] - (i < nparts ? part[i] : 0);  // exclusive
+}
+
+__global__ void __launch_bounds__(256) k_dscan_c(const int64_t *in, const int64_t *dn, const int64_t *part,
+                                                 int64_t *out, const WaveCtl *wc) {
+  if (wc && (wc->stop || wc->W < 0)) return;
+  __shared__ int64_t sw[8];
+  __shared__ int64_t carry;
+  const int64_t n = *dn, per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * per, b1 = b0 + per < n ? b0 + per : n;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = part[blockIdx.x];
+  __syncthreads();
+  for (int64_t t0 = b0; t0 < b1; t0 += blockDim.x) {
+    const int64_t i = t0 + threadIdx.x;
+    int64_t x = i < b1 ? in[i] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) sw[wid] = x;
+    __syncthreads();
+    int64_t before = carry;
+    for (int w = 0; w < wid; w++) before += sw[w];
+    if (i < b1) out[i] = before + x;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = before + x;
+    __syncthreads();
+  }
 }
 
 }  // namespace prism
