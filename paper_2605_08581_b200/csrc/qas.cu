@@ -458,6 +458,7 @@ struct prism_qas {
   X(uint32_t, sighash) \
   X(int32_t, longl) \
   X(int32_t, rk) \
+  X(int32_t, emap) \
   X(uint64_t, tkey) \
   X(int32_t, tmin) \
   X(int32_t, slot_of) \
@@ -624,6 +625,7 @@ int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, con
     QCK(grow(&q->tn, q->tn_cap, 2));
     QCK(grow(&q->aligned, q->aligned_cap, P * qsmall::QS_SKCAP));
     QCK(grow(&q->rk, q->rk_cap, q->aligned_cap));
+    QCK(grow(&q->emap, q->emap_cap, q->aligned_cap));
     QCK(grow(&q->longl, q->longl_cap, P));
     QCK(grow(&q->sig, q->sig_cap, P * c.kappa));
     QCK(grow(&q->siglen, q->siglen_cap, P));
@@ -689,7 +691,8 @@ int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, con
     qa.btab_mask = bt - 1;
     qa.longl = q->longl;
     qa.rk = q->rk;
-    qa.aligned_cap = std::min(q->aligned_cap, q->rk_cap);
+    qa.emap = q->emap;
+    qa.aligned_cap = std::min(std::min(q->aligned_cap, q->rk_cap), q->emap_cap);
     if (q->prof_on) QCK(grow(&q->qts, q->qts_cap, qsmall::QS_NTS));
     qa.ts = q->prof_on ? q->qts : nullptr;
     const qsmall::QsCfg qc{c.budget, c.cold, c.front, c.kappa, c.wg, c.wa, c.wn, c.alpha, c.beta};

@@ -66,6 +66,7 @@ struct QsArgs {
   int64_t ptab_cap, btab_mask;
   int32_t *longl;       // requests with skeletons longer than QS_MAXK
   int32_t *rk;          // rank scratch for them (aligned_cap ints)
+  int32_t *emap;        // pending skeleton entry -> its request (aligned_cap ints)
   int64_t aligned_cap;  // capacity of aligned / rk in skeleton entries
   unsigned long long *ts;  // QS_NTS phase stamps, or null
 };
@@ -231,7 +232,8 @@ __device__ inline void qs_bucket_insert(const QsArgs &A, const QsCfg &c, int64_t
   const uint64_t mine = ((uint64_t)h << 32) | (uint32_t)i;
   uint64_t pos = qmix64(h) & (uint64_t)A.btab_mask;
   for (;;) {
-    const unsigned long long prev = atomicCAS((unsigned long long *)&A.btab_key[pos], QS_EMPTY, mine);
+    unsigned long long prev = __ldcg((const unsigned long long *)&A.btab_key[pos]);
+    if (prev == QS_EMPTY) prev = atomicCAS((unsigned long long *)&A.btab_key[pos], QS_EMPTY, mine);
     bool same = prev == QS_EMPTY;
     if (!same && (uint32_t)(prev >> 32) == h) {
       const int64_t o = (int64_t)(prev & 0xffffffffu);
@@ -269,6 +271,14 @@ __device__ inline void qs_gsync() {
 
 __device__ inline int32_t qs_ld(const int32_t *p) { return __ldcg(p); }  // L2 (coherent across CTAs)
 
+// position of this thread within one sweep of gs = gridDim * blockDim items,
+// interleaved over the CTAs (item t of a sweep goes to CTA t % gridDim), so a
+// sweep of fewer items than threads still spreads over every SM
+__device__ inline int64_t qs_ilv(int64_t gs) {
+  (void)gs;
+  return (int64_t)threadIdx.x * gridDim.x + blockIdx.x;
+}
+
 // each distinct segment of skeleton [b, e) once (count_segments dedup, 83-89)
 template <class F>
 __device__ inline void qs_distinct(const int32_t *sk, int64_t b, int64_t e, F &&f) {
@@ -278,6 +288,29 @@ __device__ inline void qs_distinct(const int32_t *sk, int64_t b, int64_t e, F &&
     for (int64_t q = b; q < j && !dup; q++) dup = sk[q] == s;
     if (!dup) f(s);
   }
+}
+
+// skeleton entry e of a request starting at entry b: its segment, and whether
+// it is the segment's first occurrence in that skeleton (count_segments dedup)
+__device__ inline bool qs_first(const int32_t *sk, int64_t b, int64_t e, int32_t &s) {
+  s = sk[e];
+  for (int64_t q = b; q < e; q++)
+    if (sk[q] == s) return false;
+  return true;
+}
+
+// warp-aggregated append of c items at *ctr (int32 counter); returns this
+// lane's first position (every lane of the warp calls it)
+__device__ inline int qs_warp_reserve(int c, int32_t *ctr) {
+  const int lane = threadIdx.x & 31;
+  int x = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  int base = 0;
+  if (lane == 31 && x) base = atomicAdd(ctr, x);
+  return __shfl_sync(0xffffffffu, base, 31) + x - c;
 }
 
 // cold lane (242-245) in block 0: the nc smallest leftovers by (arrival, id),
@@ -428,28 +461,69 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
     A.ptab_cnt[i] = 0;
   }
   if (gt == 0) A.touched_n[0] = 0;
+  for (int64_t i0 = 0; i0 < P; i0 += gs) {  // entry -> request map of the pending skeletons
+    const int64_t i = i0 + qs_ilv(gs);
+    if (i < P)
+      for (int64_t e = A.off[i]; e < A.off[i + 1]; e++) A.emap[e] = (int32_t)i;
+  }
   qs_gsync();
   QS_TS(1);
   // 1. counters g (pending) and a (active), once per distinct segment (83-89),
   // and the touched list (prio's bit pattern doubles as the "listed" flag)
-  for (int pass = 0; pass < 2; pass++) {
+  // pending: one thread per skeleton entry (all probes of a request in flight)
+  for (int64_t e0 = 0; e0 < nsk; e0 += gs) {
+    const int64_t e = e0 + gt;
+    int32_t s = 0;
+    bool nt = false;
+    if (e < nsk && qs_first(A.sk, A.off[A.emap[e]], e, s)) {
+      atomicAdd(&A.g[s], 1);
+      unsigned long long *f = (unsigned long long *)&A.prio[s];
+      nt = __ldcg(f) == 0ull && atomicCAS(f, 0ull, 0xFFF0000000000001ull) == 0ull;
+    }
+    const int p = qs_warp_reserve(nt ? 1 : 0, &A.touched_n[0]);
+    if (nt) A.touched[p] = s;
+  }
+  for (int pass = 1; pass < 2; pass++) {  // active set: one thread per request
     const int64_t n = pass == 0 ? P : A.A;
     const int64_t *off = pass == 0 ? A.off : A.aoff;
     const int32_t *sk_ = pass == 0 ? A.sk : A.ask;
     int32_t *cnt = pass == 0 ? A.g : A.a;
-    for (int64_t i = gt; i < n; i += gs) {
-      qs_distinct(sk_, off[i], off[i + 1], [&](int32_t s) {
-        atomicAdd(&cnt[s], 1);
-        unsigned long long *f = (unsigned long long *)&A.prio[s];
-        if (__ldcg(f) == 0ull && atomicCAS(f, 0ull, 0xFFF0000000000001ull) == 0ull)
-          A.touched[atomicAdd(&A.touched_n[0], 1)] = s;
-      });
+    // requests interleaved over the CTAs (every SM gets a share); the touched
+    // list is appended once per warp and batch (a single counter otherwise
+    // serialises every first touch)
+    for (int64_t i0 = 0; i0 < n; i0 += gs) {
+      const int64_t i = i0 + qs_ilv(gs);
+      int32_t newt[QS_MAXK];
+      int nn = 0;
+      if (i < n) {
+        const int64_t b = off[i], e = off[i + 1];
+        qs_distinct(sk_, b, e, [&](int32_t s) {
+          atomicAdd(&cnt[s], 1);
+          unsigned long long *f = (unsigned long long *)&A.prio[s];
+          if (__ldcg(f) == 0ull && atomicCAS(f, 0ull, 0xFFF0000000000001ull) == 0ull) {
+            if (nn < QS_MAXK) newt[nn++] = s;
+            else A.touched[atomicAdd(&A.touched_n[0], 1)] = s;
+          }
+        });
+      }
+      const int lane = tid & 31;
+      int x = nn;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      int base = 0;
+      if (lane == 31 && x) base = atomicAdd(&A.touched_n[0], x);
+      base = __shfl_sync(0xffffffffu, base, 31) + x - nn;
+      for (int q = 0; q < nn; q++) A.touched[base + q] = newt[q];
     }
   }
   qs_gsync();
   QS_TS(2);
   // 2. front alignment + order-sensitive signature (109-143), bucket insert
-  for (int64_t i = gt; i < P; i += gs) {
+  for (int64_t i0 = 0; i0 < P; i0 += gs) {
+    const int64_t i = i0 + qs_ilv(gs);
+    if (i >= P) continue;
     const int64_t b = A.off[i];
     const int k = (int)(A.off[i + 1] - b);
     if (k > QS_MAXK) {  // aligned below by a whole block
@@ -567,29 +641,39 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   QS_TS(4);
   // 7. distinct (bucket, segment) pairs; provisional = first hot_cap members (146-171)
   const int64_t hot_cap = c.budget - c.cold;
-  for (int64_t i = gt; i < P; i += gs) {
-    const int32_t bk = A.bucket[i];
-    const int prov = A.rank[i] < hot_cap ? 1 : 0;
-    qs_distinct(A.sk, A.off[i], A.off[i + 1], [&](int32_t s) {
-      const uint64_t key = ((uint64_t)(uint32_t)bk << 32) | (uint32_t)s;
-      uint64_t pos = qmix64(key) & pmask;
-      for (;;) {
-        unsigned long long *slot = (unsigned long long *)&A.ptab_key[pos];
-        unsigned long long prev = __ldcg(slot);
-        if (prev == QS_EMPTY) {
-          prev = atomicCAS(slot, QS_EMPTY, key);
+  for (int64_t e0 = 0; e0 < nsk; e0 += gs) {  // one thread per skeleton entry
+    const int64_t e = e0 + gt;
+    int32_t s = 0, bk = 0;
+    bool np = false;
+    int32_t npos = 0;
+    if (e < nsk) {
+      const int64_t i = A.emap[e];
+      if (qs_first(A.sk, A.off[i], e, s)) {
+        bk = A.bucket[i];
+        const int prov = A.rank[i] < hot_cap ? 1 : 0;
+        const uint64_t key = ((uint64_t)(uint32_t)bk << 32) | (uint32_t)s;
+        uint64_t pos = qmix64(key) & pmask;
+        for (;;) {
+          unsigned long long *slot = (unsigned long long *)&A.ptab_key[pos];
+          unsigned long long prev = __ldcg(slot);
           if (prev == QS_EMPTY) {
-            atomicAdd(&A.nsegs[bk], 1);
-            A.plist[atomicAdd((unsigned long long *)&A.counts[5], 1ull)] = (int32_t)pos;
+            prev = atomicCAS(slot, QS_EMPTY, key);
+            if (prev == QS_EMPTY) {
+              np = true;
+              npos = (int32_t)pos;
+            }
           }
+          if (prev == QS_EMPTY || prev == key) {
+            if (prov) atomicAdd(&A.ptab_cnt[pos], 1);
+            break;
+          }
+          pos = (pos + 1) & pmask;
         }
-        if (prev == QS_EMPTY || prev == key) {
-          if (prov) atomicAdd(&A.ptab_cnt[pos], 1);
-          break;
-        }
-        pos = (pos + 1) & pmask;
+        if (np) atomicAdd(&A.nsegs[bk], 1);
       }
-    });
+    }
+    const int p = qs_warp_reserve(np ? 1 : 0, (int32_t *)&A.counts[5]);  // (low word of the zeroed int64)
+    if (np) A.plist[p] = npos;
   }
   qs_gsync();
   QS_TS(5);
