@@ -48,7 +48,8 @@ struct CoopState {
   unsigned int ss_cur[SS_SPL];  // per-bucket scatter cursors
   unsigned int ss_off[SS_SPL + 4];  // bucket offsets
   int ss_ok;                    // the sample select produced the sorted prefix
-  unsigned long long ss_dbg[24];  // diagnostics: [0] max bucket, [1] rounds, [2+3r..] (undecided, selected, shift)
+  unsigned long long ss_dbg[24];
+  unsigned long long ss_prof[8];  // diagnostics: k_ss_sort clock64 sums (load, sort, buckets, items)  // diagnostics: [0] max bucket, [1] rounds, [2+3r..] (undecided, selected, shift)
   int ss_nb;                    // diagnostics: splitters of the last sample select
   int ss_fail;                  // diagnostics: why it fell back (0: it did not)
   int nts;
@@ -606,6 +607,55 @@ __device__ inline void block_sort_small(const Key3 *k, const uint64_t *v, int n,
   __syncthreads();
 }
 
+// ascending sort of n unique keys (+ values) in shared memory: chunks of
+// MS_CH rank-sorted into (tk, tv) (broadcast reads, no barriers), then every
+// item's final position = its rank in its chunk + its lower bound in every
+// other chunk; written to (ko, vo), which may alias (k, v).  O(n * MS_CH)
+// compares instead of the O(n^2) of a plain rank sort, two barriers instead of
+// the O(log^2 n) of a bitonic network.
+constexpr int MS_CH = 128;
+__device__ inline void block_merge_sort(const Key3 *k, const uint64_t *v, int n, Key3 *tk, uint64_t *tv, Key3 *ko,
+                                        uint64_t *vo) {
+  const int nch = (n + MS_CH - 1) / MS_CH;
+  int tpi = 1;  // threads per item (a power of two <= 8): small sets use the whole block
+  while (tpi < 8 && 2 * tpi * n <= (int)blockDim.x) tpi <<= 1;
+  const int sub = threadIdx.x & (tpi - 1), per = (int)blockDim.x / tpi;
+  for (int i0 = 0; i0 < n; i0 += per) {  // uniform trip count (shuffles below)
+    const int i = i0 + (int)threadIdx.x / tpi;
+    const bool ok = i < n;
+    const int c0 = ok ? (i / MS_CH) * MS_CH : 0, c1 = ok ? min(c0 + MS_CH, n) : 0;
+    const Key3 x = ok ? k[i] : Key3{0, 0, 0};
+    int r = 0;
+#pragma unroll 4
+    for (int j = c0 + sub; j < c1; j += tpi) r += key_less(k[j], x) ? 1 : 0;
+    for (int o = 1; o < tpi; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (ok && sub == 0) {
+      tk[c0 + r] = x;
+      if (tv) tv[c0 + r] = v ? v[i] : 0ull;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int c = i / MS_CH;
+    const Key3 x = tk[i];
+    int pos = i - c * MS_CH;
+    for (int d = 0; d < nch; d++) {
+      if (d == c) continue;
+      int lo = d * MS_CH, hi = min(lo + MS_CH, n);
+      const int base = lo;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (key_less(tk[mid], x)) lo = mid + 1;
+        else hi = mid;
+      }
+      pos += lo - base;
+    }
+    ko[pos] = x;  // (ko may alias k: phase 1 read all of k before the barrier)
+    if (vo) vo[pos] = tv ? tv[i] : 0ull;
+  }
+  __syncthreads();
+}
+
 // one radix round of CTA 0's sample selection over the undecided samples:
 // digit below the highest bit where the undecided keys differ, the weight
 // histogram, the crossing digit; lower digits join the selected keys, higher
@@ -880,7 +930,7 @@ constexpr int SS_SUB = 2048;  // sub-sample the selection rounds run on
 constexpr size_t SS_SEL_SMEM =
     2 * sizeof(Key3) * SS_SPL + 8 * SS_U + 2 * (sizeof(Key3) + 8) * SS_SEL_TPB + (sizeof(Key3) + 9) * SS_SUB;
 constexpr size_t SS_FILTER_SMEM = sizeof(Key3) * SS_SPL + 4 * SS_SPL;
-constexpr size_t SS_SORT_SMEM = (sizeof(Key3) + 8) * SS_BMAX;
+constexpr size_t SS_SORT_SMEM = 2 * (sizeof(Key3) + 8) * SS_BMAX;
 
 __device__ inline int64_t ss_period(int32_t hw) {
   int64_t m = 8;
@@ -1001,13 +1051,13 @@ __global__ void __launch_bounds__(SS_SEL_TPB) k_ss_select(Cand cand, CoopBufs B,
       fw[j] = (uint64_t)subw[i];
     }
     __syncthreads();
-    block_sort_small(fk, fw, nU, fk2, fw2, fk, fw);
+    block_merge_sort(fk, fw, nU, fk2, fw2, fk, fw);
     coop_mark(st);
     if (threadIdx.x == 0) {
       long long run = 0;
       int c = nU - 1;
       for (int j = 0; j < nU; j++) {
-        run += (long long)fw2[j];
+        run += (long long)fw[j];
         if (run >= need) {
           c = j;
           break;
@@ -1017,7 +1067,7 @@ __global__ void __launch_bounds__(SS_SEL_TPB) k_ss_select(Cand cand, CoopBufs B,
       s_nsel = 0;
     }
     __syncthreads();
-    const Key3 tau = fk2[s_misc[3]];
+    const Key3 tau = fk[s_misc[3]];
     // splitters: every sample <= tau (warp-aggregated appends)
     bool ovf = false;
     for (int i0 = 0; i0 < ns; i0 += blockDim.x) {
@@ -1043,13 +1093,8 @@ __global__ void __launch_bounds__(SS_SEL_TPB) k_ss_select(Cand cand, CoopBufs B,
   int nb = 0;
   if (!fail) {  // splitters: the selected samples, sorted exactly
     nb = s_nsel;
-    if (nb <= (int)blockDim.x) {
-      block_sort_small(selk, nullptr, nb, spl, nullptr, fk, fw);
-    } else {
-      block_rank_sort(selk, nullptr, nb, spl, nullptr);
-      __syncthreads();
-    }
-    for (int q = threadIdx.x; q < nb; q += blockDim.x) B.kt[q] = spl[q];
+    block_merge_sort(selk, nullptr, nb, spl, nullptr, selk, nullptr);
+    for (int q = threadIdx.x; q < nb; q += blockDim.x) B.kt[q] = selk[q];
     coop_mark(st);
   }
   if (threadIdx.x == 0) {
@@ -1195,41 +1240,35 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_scatter(CoopBufs B, int64_t W, co
   }
 }
 
-// one CTA per bucket: rank sort (no barriers) up to blockDim items, bitonic above
+// the buckets over the CTAs, each sorted in shared memory (block_merge_sort)
 __global__ void __launch_bounds__(SS_TPB) k_ss_sort(CoopBufs B, Key3 *kout, uint64_t *vout) {
   extern __shared__ __align__(16) unsigned char dsm[];
   CoopState *st = B.st;
-  const int b = blockIdx.x;
-  if (!st->ss_ok || b >= st->ss_nb) return;
-  const int b0 = (int)st->ss_off[b], m0 = (int)(st->ss_off[b + 1] - st->ss_off[b]);
-  if (m0 == 0) return;
+  if (!st->ss_ok) return;
+  const int nb = st->ss_nb;
   Key3 *sk = reinterpret_cast<Key3 *>(dsm);
   uint64_t *sv = reinterpret_cast<uint64_t *>(sk + SS_BMAX);
-  if (m0 <= (int)blockDim.x) {
+  Key3 *tk = reinterpret_cast<Key3 *>(sv + SS_BMAX);
+  uint64_t *tv = reinterpret_cast<uint64_t *>(tk + SS_BMAX);
+  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int b0 = (int)st->ss_off[b], m0 = (int)(st->ss_off[b + 1] - st->ss_off[b]);
+    if (m0 == 0) continue;
+    const long long c0 = clock64();
     for (int i = threadIdx.x; i < m0; i += blockDim.x) {
       sk[i] = B.ks[b0 + i];
       sv[i] = B.vs[b0 + i];
     }
     __syncthreads();
-    block_rank_sort(sk, sv, m0, kout + b0, vout + b0);
-    return;
-  }
-  int mp = 1;
-  while (mp < m0) mp <<= 1;
-  for (int i = threadIdx.x; i < mp; i += blockDim.x) {
-    if (i < m0) {
-      sk[i] = B.ks[b0 + i];
-      sv[i] = B.vs[b0 + i];
-    } else {
-      sk[i] = {~0ull, ~0ull, ~0ull};
-      sv[i] = 0;
+    const long long c1 = clock64();
+    block_merge_sort(sk, sv, m0, tk, tv, kout + b0, vout + b0);
+    if (threadIdx.x == 0) {
+      const long long c2 = clock64();
+      atomicAdd(&st->ss_prof[0], (unsigned long long)(c1 - c0));
+      atomicAdd(&st->ss_prof[1], (unsigned long long)(c2 - c1));
+      atomicAdd(&st->ss_prof[2], 1ull);
+      atomicAdd(&st->ss_prof[3], (unsigned long long)m0);
+      atomicMax(&st->ss_prof[4], (unsigned long long)(c2 - c0));
     }
-  }
-  __syncthreads();
-  bitonic_smem(sk, sv, mp);
-  for (int i = threadIdx.x; i < m0; i += blockDim.x) {
-    kout[b0 + i] = sk[i];
-    vout[b0 + i] = sv[i];
   }
 }
 
@@ -1284,7 +1323,8 @@ __global__ void __launch_bounds__(COOP_TPB) k_build_coop(DT T, CoopBufs B, int64
     c->builds++;
     for (int i = 0; i < B.st->nts; i++) B.st->ts_build[i] = B.st->ts[i];
     B.st->nts_build = B.st->nts;
-    for (int i = 0; i < 12; i++) B.st->ts_build[21 + i] = B.st->ss_dbg[i];
+    for (int i = 0; i < 7; i++) B.st->ts_build[21 + i] = B.st->ss_dbg[i];
+    for (int i = 0; i < 5; i++) B.st->ts_build[28 + i] = B.st->ss_prof[i];
     B.st->ts_build[33] = B.st->ss_ns;  // diagnostics of the sample select
     B.st->ts_build[34] = (unsigned long long)B.st->ss_nb;
     B.st->ts_build[35] = (unsigned long long)B.st->ss_fail;

@@ -343,6 +343,7 @@ int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const 
   if (!attr) {
     CK(cudaFuncSetAttribute(k_ss_select<EvictCand>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SEL_SMEM));
     CK(cudaFuncSetAttribute(k_ss_select<ProtCand>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SEL_SMEM));
+    CK(cudaFuncSetAttribute(k_ss_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SORT_SMEM));
     attr = true;
   }
   int sms = 0;
@@ -352,7 +353,7 @@ int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const 
   k_ss_select<Cand><<<1, SS_SEL_TPB, SS_SEL_SMEM, st>>>(cand, B, W, dW);
   k_ss_filter<Cand><<<4 * sms, SS_TPB, SS_FILTER_SMEM, st>>>(cand, B);
   k_ss_scatter<<<2 * sms, SS_TPB, 0, st>>>(B, W, dW);
-  k_ss_sort<<<SS_SPL, SS_TPB, SS_SORT_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
+  k_ss_sort<<<sms, SS_TPB, SS_SORT_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
   CK(cudaGetLastError());
   return PRISM_OK;
 }
@@ -634,7 +635,7 @@ int admit_wave_par(prism_tree *t, const WaveIn &W, int64_t levels, int64_t *hits
     k_dscan_b<<<1, 1024, 0, st>>>(t->ds_part, DS_BLOCKS, wc);
     k_dscan_c<<<DS_BLOCKS, 256, 0, st>>>(X.vlen, dn, t->ds_part, X.F, wc);
     k_wp_cuts<<<blocks_for(B), TPB, 0, st>>>(t->d, B, X, wc);
-    k_wc_cut<<<1, 32, 0, st>>>(t->d, B, X, wc);
+    k_wc_cut<<<1, 1024, 0, st>>>(t->d, B, X, wc);
     k_wp_evict<<<2 * sms, TPB, 0, st>>>(t->d, wc);
     k_wp_alloc<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
     k_wp_label_reset<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);

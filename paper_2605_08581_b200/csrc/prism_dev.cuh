@@ -184,10 +184,13 @@ __device__ inline void shl_or(Key3 &a, int n, uint64_t v) {
   a.w2 = (a.w2 << n) | v;
 }
 
-__device__ inline bool key_less(const Key3 &a, const Key3 &b) {
-  if (a.w0 != b.w0) return a.w0 < b.w0;
-  if (a.w1 != b.w1) return a.w1 < b.w1;
-  return a.w2 < b.w2;
+// branch-free (lanes comparing different keys would otherwise diverge at every
+// word and reconverge per compare)
+__device__ __forceinline__ bool key_less(const Key3 &a, const Key3 &b) {
+  const bool l0 = a.w0 < b.w0, e0 = a.w0 == b.w0;
+  const bool l1 = a.w1 < b.w1, e1 = a.w1 == b.w1;
+  const bool l2 = a.w2 < b.w2;
+  return l0 | (e0 & (l1 | (e1 & l2)));
 }
 
 // order-preserving map of a double onto uint64 (-0.0 folded onto +0.0, so

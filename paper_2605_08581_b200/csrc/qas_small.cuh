@@ -186,7 +186,9 @@ __device__ inline int32_t block_exscan(int32_t *v, int n, int32_t *swarp) {
 struct QKey {
   uint64_t hi, lo;
 };
-__device__ inline bool qk_less(const QKey &x, const QKey &y) { return x.hi != y.hi ? x.hi < y.hi : x.lo < y.lo; }
+__device__ __forceinline__ bool qk_less(const QKey &x, const QKey &y) {  // branch-free
+  return (x.hi < y.hi) | ((x.hi == y.hi) & (x.lo < y.lo));
+}
 
 // bitonic sort of n <= QS_MAXP (key, value) pairs in shared memory
 __device__ inline void block_bitonic(QKey *k, int32_t *v, int n) {

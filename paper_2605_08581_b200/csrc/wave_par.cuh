@@ -525,13 +525,17 @@ __global__ void k_wc_plan(DT T, int64_t B, WaveTmp X, WaveCtl *wc, int64_t slack
 // the victims: nv = entries consumed through the last member, checks that the
 // prefix sufficed and that no consumed entry is pinned/guarded; the number of
 // evict calls (members whose cut advances) and the tokens freed
-__global__ void k_wc_cut(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
+__global__ void __launch_bounds__(1024) k_wc_cut(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
+  __shared__ int64_t s_calls[32];
   if (wc->stop) return;
-  const int lane = threadIdx.x;
   int64_t calls = 0;
-  for (int64_t j = lane; j < B; j += 32) calls += X.cut[j] > (j ? X.cut[j - 1] : 0) ? 1 : 0;
+  for (int64_t j = threadIdx.x; j < B; j += blockDim.x) calls += X.cut[j] > (j ? X.cut[j - 1] : 0) ? 1 : 0;
   for (int o = 16; o > 0; o >>= 1) calls += __shfl_xor_sync(0xffffffffu, calls, o);
-  if (lane) return;
+  if ((threadIdx.x & 31) == 0) s_calls[threadIdx.x >> 5] = calls;
+  __syncthreads();
+  if (threadIdx.x) return;
+  calls = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); w++) calls += s_calls[w];
   const int64_t nv = X.cut[B - 1];
   const int32_t flags = *X.flags;
   const int64_t poison = X.misc[1];
