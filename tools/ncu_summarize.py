@@ -16,13 +16,14 @@ import io
 import json
 import sys
 
-PHASE = [  # (phase, kernel-name substrings)
-    ("build", ("k_build_keys", "k_propagate", "k_gather", "k_list_ready")),
-    ("commit", ("k_wp_", "k_commit")),
+PHASE = [  # (phase, kernel-name substrings); first match wins
+    ("protect", ("k_prot_", "k_protect_coop", "<prism::ProtCand>")),
+    ("build", ("k_build_keys", "k_propagate", "k_gather", "k_list_ready", "k_build_coop", "<prism::EvictCand>")),
+    ("select", ("k_ss_",)),  # shared sample-select kernels (build and protection)
+    ("commit", ("k_wp_", "k_wc_", "k_dscan_", "k_commit")),
     ("prematch", ("k_prematch",)),
-    ("protect", ("k_prot_",)),
     ("release", ("k_release",)),
-    ("qas", ("q_",)),
+    ("qas", ("k_qas_small", "q_")),
 ]
 
 
@@ -48,6 +49,8 @@ def main():
     for r in rows:
         name = r["Kernel Name"]
         short = name.split("(")[0].replace("void ", "")[:90]
+        if "<" in name.split("(")[0]:  # keep template arguments (ProtCand / EvictCand instances)
+            short = name.split("(")[0].replace("void ", "")[:120]
         m, v = r["Metric Name"], r["Metric Value"].replace(",", "")
         try:
             v = float(v)
