@@ -637,11 +637,11 @@ int admit_wave_par(prism_tree *t, const WaveIn &W, int64_t levels, int64_t *hits
     k_wp_cuts<<<blocks_for(B), TPB, 0, st>>>(t->d, B, X, wc);
     k_wc_cut<<<1, 1024, 0, st>>>(t->d, B, X, wc);
     k_wp_evict<<<2 * sms, TPB, 0, st>>>(t->d, wc);
-    k_wp_alloc<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
-    k_wp_label_reset<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
+    k_wp_alloc<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
+    k_wp_label_reset<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
     k_wp_create<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, W, X, wc);
-    k_wp_touch<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
-    k_wp_label<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc, hits, leaf_slots, leaf_ids);
+    k_wp_touch<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
+    k_wp_label<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc, hits, leaf_slots, leaf_ids);
     k_wc_finalize<<<1, 1, 0, st>>>(t->d, B, X, wc);
     CK(cudaGetLastError());
     t->launches[PH_COMMIT] += 14;

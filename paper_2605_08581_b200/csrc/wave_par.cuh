@@ -287,15 +287,19 @@ __global__ void k_wp_evict(DT T, const WaveCtl *wc) {
 }
 
 // W6a: slot of every new piece (free list LIFO, then the high-water mark)
+// (member, piece)-parallel kernels: WP_PL threads per member, piece p on lane p % WP_PL
+constexpr int WP_PL = 16;
+
 __global__ void k_wp_alloc(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, j = t / WP_PL;
+  const int pl = (int)(t % WP_PL);
   if (j >= W.B || wc->stop || X.cnew[j] == 0) return;
   const int64_t id0 = wc->id0;
   const int32_t free_top = wc->ft0 + (int32_t)wc->nv, hw = wc->hw0;
   const uint32_t vctr0 = wc->vctr0 + (uint32_t)wc->nv, epoch = wc->epoch;
   const int P = X.npieces[j], p0 = X.p0[j];
   const int64_t g0 = X.idb[j];  // global index of this member's first new piece
-  for (int p = p0; p < P; p++) {
+  for (int p = p0 + pl; p < P; p += WP_PL) {
     const int64_t g = g0 + (p - p0);
     const int32_t s = g < free_top ? T.freelist[free_top - 1 - g] : (int32_t)(hw + (g - free_top));
     X.piece_slot[j * WP_MAXP + p] = s;
@@ -372,42 +376,60 @@ __global__ void k_wp_create(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
 }
 
 // W7: touches of pre-existing nodes, pins, and last-writer label election
+// piece-major (thread = piece p of member j, consecutive members in a warp) so
+// the members sharing an upper node (the system prompt, popular segments)
+// combine their touches/pins in one atomic per warp and node.  A node shared
+// inside the wave is "old" (pre-existing: match + insert touches) only for the
+// members after its creator, so the touches aggregate over the old peers.
 __global__ void k_wp_touch(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= W.B || wc->stop) return;
-  const int64_t clock0 = wc->clock0;
-  const int P = X.npieces[j];
-  const int own0 = X.cnew[j] ? X.p0[j] : P;
-  const unsigned long long tick = (unsigned long long)(clock0 + 2 * j + 2);
-  for (int p = 0; p < P; p++) {
-    const int32_t s = wp_node(W, X, j, p);
-    if (p < own0) {  // existed before this member: match + insert touches
-      atomicAdd(&T.hits[s], 2);
-      atomicMax((unsigned long long *)&T.last[s], tick);
+  if (wc->stop) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t j = t % W.B;
+  const int lane = threadIdx.x & 31;
+  const bool live = t < (int64_t)W.B * WP_PL;  // (threads past the grid's rows only vote)
+  const int P = live ? X.npieces[j] : 0;
+  const int own0 = live ? (X.cnew[j] ? X.p0[j] : P) : 0;
+  const unsigned long long base_tick = (unsigned long long)(wc->clock0 + 2);
+  for (int p = (int)(t / W.B); __any_sync(0xffffffffu, p < P); p += WP_PL) {  // rows of WP_PL pieces
+    const bool on = p < P;
+    const int32_t s = on ? wp_node(W, X, j, p) : -1 - lane;
+    const bool old = on && p < own0;
+    const unsigned peers = __match_any_sync(0xffffffffu, s);
+    const unsigned jall = __reduce_max_sync(peers, (unsigned)j);
+    const unsigned jold = __reduce_max_sync(peers, old ? (unsigned)j + 1u : 0u);  // 0: no old peer
+    const int nold = __popc(__ballot_sync(0xffffffffu, old) & peers);
+    if (on && lane == __ffs(peers) - 1) {
+      if (jold) {
+        atomicAdd(&T.hits[s], 2 * nold);
+        atomicMax((unsigned long long *)&T.last[s], base_tick + 2ull * (jold - 1));
+      }
+      atomicAdd(&T.ref[s], __popc(peers));
+      atomicMax(&T.eff[s], (int32_t)jall);
     }
-    atomicAdd(&T.ref[s], 1);
-    atomicMax(&T.eff[s], (int32_t)j);
   }
-  atomicAdd(&T.ref[ROOT], 1);  // _pin reaches the root (kvcache.py:344-348)
+  const unsigned m0 = __ballot_sync(0xffffffffu, live && t < (int64_t)W.B);
+  if (m0 && lane == __ffs(m0) - 1) atomicAdd(&T.ref[ROOT], __popc(m0));  // _pin reaches the root (kvcache.py:344-348)
 }
 
 __global__ void k_wp_label_reset(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, j = t / WP_PL;
+  const int pl = (int)(t % WP_PL);
   if (j >= W.B || wc->stop) return;
   const int own0 = X.cnew[j] ? X.p0[j] : X.npieces[j];
-  for (int p = 0; p < own0; p++) T.eff[wp_node(W, X, j, p)] = -1;
+  for (int p = pl; p < own0; p += WP_PL) T.eff[wp_node(W, X, j, p)] = -1;
 }
 
 // W8: the elected (max-index) member writes kind/seg/anchor (kvcache.py:317-340)
 __global__ void k_wp_label(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc, int64_t *hits, int32_t *leaf_slots,
                            int64_t *leaf_ids) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, j = t / WP_PL;
+  const int pl = (int)(t % WP_PL);
   if (j >= W.B || wc->stop) return;
   const int64_t m = W.members[j];
   const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
   const int64_t n = W.poff[j + 1] - W.poff[j];
   const int P = X.npieces[j];
-  for (int p = 0; p < P; p++) {
+  for (int p = pl; p < P; p += WP_PL) {
     const int32_t s = wp_node(W, X, j, p);
     if (T.eff[s] != (int32_t)j) continue;
     const int64_t a = W.aoffs[j] + p;
@@ -421,6 +443,7 @@ __global__ void k_wp_label(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc, int64_t
     T.snap[3 * (int64_t)s + 1] = W.a_snap[3 * a + 1];
     T.snap[3 * (int64_t)s + 2] = W.a_snap[3 * a + 2];
   }
+  if (pl) return;
   const int32_t leaf = P > 0 ? wp_node(W, X, j, P - 1) : ROOT;
   if (hits) hits[j] = X.hit[j];
   if (leaf_slots) leaf_slots[j] = leaf;
