@@ -614,11 +614,12 @@ int admit_wave_par(prism_tree *t, const WaveIn &W, int64_t levels, int64_t *hits
     CK(cudaMemsetAsync(X.misc + 1, 0x7F, sizeof(int64_t), st));  // poison index: "none"
     k_wc_begin<<<1, 1, 0, st>>>(t->d, wc);
     k_wp_plan<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
+    k_wp_levels<<<blocks_for(B * WP_PL), TPB, 0, st>>>(W, X);
     k_wp_hits<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X);
     k_wp_scan3<<<1, 1024, 0, st>>>(B, X);
     k_wc_plan<<<1, 1, 0, st>>>(t->d, B, X, wc, t->list_slack_tokens, force_full);
     CK(cudaGetLastError());
-    t->launches[PH_COMMIT] += 5;
+    t->launches[PH_COMMIT] += 6;
     prof_end(t, PH_COMMIT);
     const int64_t *dW = &wc->W;
     if (t->use_coop) {

@@ -32,6 +32,8 @@
 namespace prism {
 
 constexpr int WP_MAXP = 66;  // pieces per path: sys + 64 segments + suffix
+// (member, piece)-parallel kernels: WP_PL threads per member, piece p on thread p % WP_PL
+constexpr int WP_PL = 16;
 enum { WPF_OVERFLOW = 1, WPF_PARTIAL = 2, WPF_ALIGN = 4, WPF_COLLIDE = 8, WPF_VICTIM = 16, WPF_CAPACITY = 32,
        WPF_SHAPE = 64 };
 
@@ -126,7 +128,6 @@ __global__ void k_wp_plan(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   const uint32_t epoch = wc->epoch;
   const int64_t m = W.members[j];
   const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
-  const int32_t *s = W.aligned + W.sk_off[m];
   const int64_t n = W.poff[j + 1] - W.poff[j];
   const int64_t sfx = n - W.sys - (int64_t)k * W.chunk;
   const int P = (W.sys > 0) + k + (sfx > 0);
@@ -150,13 +151,49 @@ __global__ void k_wp_plan(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
     return;
   }
   X.pre[j] = hit_pre;
-  X.npieces[j] = P;
-  // skeleton-prefix levels: level L = sys piece plus the first L segments
-  uint64_t h = 0x51ED270B27ull;
+  X.npieces[j] = P;  // (the skeleton-prefix levels go into the table in k_wp_levels)
+}
+
+// W1b: skeleton-prefix ownership table -- level L = sys piece plus the first L
+// segments; the first owner of each prefix by atomicMin.  Level-major (thread
+// = level L of member j, consecutive members in a warp): every member shares
+// the low levels, so each warp inserts one key per distinct prefix.
+__global__ void k_wp_levels(WaveIn W, WaveTmp X) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t j = t % W.B;
+  const int lane = threadIdx.x & 31;
+  const bool live = t < (int64_t)W.B * WP_PL;
+  int k = 0;
+  const int32_t *s = nullptr;
+  if (live) {
+    const int64_t m = W.members[j];
+    k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
+    s = W.aligned + W.sk_off[m];
+  }
   const int lmin = W.sys > 0 ? 0 : 1;
-  for (int L = 0; L <= k; L++) {
-    if (L > 0) h = wp_hash_next(h, s[L - 1]);
-    if (L >= lmin) wp_table(X, wp_level_key(L, h), (int32_t)j, true);
+  for (int L = (int)(t / W.B); __any_sync(0xffffffffu, live && L <= k); L += WP_PL) {
+    const bool on = live && L <= k && L >= lmin;
+    uint64_t key = 0;
+    if (on) {
+      uint64_t h = 0x51ED270B27ull;
+      for (int q = 0; q < L; q++) h = wp_hash_next(h, s[q]);
+      key = wp_level_key(L, h);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, on ? key : ~0ull);
+    const unsigned jmin = __reduce_min_sync(peers, (unsigned)j);
+    if (on && lane == __ffs(peers) - 1) {
+      uint64_t h = mix64(key) & X.lt_mask;
+      for (;;) {
+        unsigned long long prev = __ldcg((const unsigned long long *)&X.lt_key[h]);
+        if (prev == (unsigned long long)HEMPTY)
+          prev = atomicCAS((unsigned long long *)&X.lt_key[h], (unsigned long long)HEMPTY, (unsigned long long)key);
+        if (prev == (unsigned long long)HEMPTY || prev == key) {
+          atomicMin(&X.lt_min[h], (int32_t)jmin);
+          break;
+        }
+        h = (h + 1) & X.lt_mask;
+      }
+    }
   }
 }
 
@@ -287,8 +324,6 @@ __global__ void k_wp_evict(DT T, const WaveCtl *wc) {
 }
 
 // W6a: slot of every new piece (free list LIFO, then the high-water mark)
-// (member, piece)-parallel kernels: WP_PL threads per member, piece p on lane p % WP_PL
-constexpr int WP_PL = 16;
 
 __global__ void k_wp_alloc(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, j = t / WP_PL;
