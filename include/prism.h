@@ -201,6 +201,10 @@ int prism_qas_round_device(prism_qas *q, int64_t P, const int64_t *ids, const do
  * (kvcache.py:364-383 fed by scheduler.py:247-251). out_ids may be NULL. */
 int prism_set_protection_device(prism_tree *t, const double *d_pri, int32_t nseg,
                                 int64_t *out_ids, int64_t *n_out);
+/* The same, queued on the tree's auxiliary stream after the work queued so
+ * far; the tree stream joins it before the next eviction-order build or API
+ * call (used by prism_wave_step to overlap protection with serialization). */
+int prism_set_protection_device_async(prism_tree *t, const double *d_pri, int32_t nseg);
 /* note_active_segments from dense DEVICE counters: active = a > 0 or n > 0
  * (engine.py:195-197). */
 int prism_note_active_device(prism_tree *t, const int32_t *d_a, const int32_t *d_nd, int32_t nseg);

@@ -62,6 +62,12 @@ inline unsigned blocks_for(int64_t n, int tpb = TPB) { return (unsigned)((n + tp
 struct prism_tree {
   int dev = 0;
   cudaStream_t st = nullptr;
+  // protection of the fused wave runs on st_aux, overlapped with the
+  // serialization / pre-match / commit plan on st; st joins it (join_aux)
+  // before anything reads the protected flags
+  cudaStream_t st_aux = nullptr;
+  cudaEvent_t ev_aux = nullptr, ev_main = nullptr;
+  int aux_pending = 0;
   DT d{};
   Ctrl *hctrl = nullptr;  // pinned
   int64_t protect_budget = 0;
@@ -147,6 +153,12 @@ inline void prof_end(prism_tree *t, int ph) {
 }  // namespace
 
 namespace {
+inline void join_aux(prism_tree *t) {
+  if (t->aux_pending) {
+    cudaStreamWaitEvent(t->st, t->ev_aux, 0);
+    t->aux_pending = 0;
+  }
+}
 
 // ----------------------------------------------------------------- slot arrays
 struct SlotField {
@@ -208,6 +220,7 @@ int alloc_slots(prism_tree *t, int32_t S) {
 }
 
 int grow_slots(prism_tree *t, int64_t need_total) {
+  join_aux(t);  // the auxiliary stream must not touch arrays being replaced
   int64_t S2 = (int64_t)t->d.S * 2;
   while (S2 < need_total) S2 *= 2;
   if (S2 > 0x7fffff00) return fail(PRISM_FATAL, "slot capacity overflow");
@@ -368,6 +381,7 @@ CoopBufs coop_bufs(prism_tree *t) {
 // tokens reach W (W <= 0: the whole order).  dW (cooperative path only): W is
 // read on the device instead (< 0: no list is built at all).
 int build_list(prism_tree *t, int64_t W, const int64_t *dW = nullptr) {
+  join_aux(t);  // the keys read the protected flags
   if (t->use_coop) {  // one cooperative kernel, no host round trip
     int grid = coop_grid(t);
     if (grid < 0) return PRISM_FATAL;
@@ -419,6 +433,7 @@ int build_list(prism_tree *t, int64_t W, const int64_t *dW = nullptr) {
 }
 
 int rehash(prism_tree *t, int64_t extra) {
+  join_aux(t);  // the auxiliary stream must not touch arrays being replaced
   int64_t live = t->hctrl->hlive + extra;
   const int64_t cap = (int64_t)(t->d.hmask + 1);
   const int64_t want = std::max<int64_t>(cap, next_pow2(4 * (live + 64)));  // never shrinks
@@ -441,6 +456,7 @@ int rehash(prism_tree *t, int64_t extra) {
 }
 
 int compact_arena(prism_tree *t, int64_t need) {
+  join_aux(t);  // the auxiliary stream must not touch arrays being replaced
   const int32_t hw = t->hctrl->hw;
   int64_t *len = nullptr, *off = nullptr;
   CK(dalloc(&len, hw + 1));
@@ -777,6 +793,10 @@ prism_tree *prism_tree_create(int64_t capacity_tokens, int32_t policy, int64_t p
   };
   if (cudaSetDevice(device) != cudaSuccess) return bad("cudaSetDevice");
   if (cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking) != cudaSuccess) return bad("stream");
+  if (cudaStreamCreateWithFlags(&t->st_aux, cudaStreamNonBlocking) != cudaSuccess) return bad("stream");
+  if (cudaEventCreateWithFlags(&t->ev_aux, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&t->ev_main, cudaEventDisableTiming) != cudaSuccess)
+    return bad("events");
   int64_t S = std::max<int64_t>(initial_slots > 0 ? initial_slots : 4096, 64);
   S = std::min<int64_t>(next_pow2(S), 1ll << 30);
   t->d.policy = policy;
@@ -842,12 +862,17 @@ void prism_tree_destroy(prism_tree *t) {
   cudaFreeHost(t->hctrl);
   cudaFreeHost(t->h_small);
   cudaFreeHost(t->h_res);
+  cudaStreamSynchronize(t->st_aux);
+  cudaStreamDestroy(t->st_aux);
+  cudaEventDestroy(t->ev_aux);
+  cudaEventDestroy(t->ev_main);
   cudaStreamDestroy(t->st);
   delete t;
 }
 
 int prism_match(prism_tree *t, const uint32_t *path, int64_t n, int64_t *hit, int32_t *visited_slots,
                 int64_t *visited_ids, int64_t *n_visited) {
+  join_aux(t);
   if (n < 0 || n > MAX_PATH) return fail(PRISM_INVALID, "path length out of range");
   cudaSetDevice(t->dev);
   int rc = ensure_buf(&t->d_path, t->path_cap, n);
@@ -882,6 +907,7 @@ int prism_match(prism_tree *t, const uint32_t *path, int64_t n, int64_t *hit, in
 
 // last-op details for the Python binding: [evicted, vbeg, vend, freed, status]
 int prism_last_op(prism_tree *t, int64_t *out) {
+  join_aux(t);
   out[0] = t->h_res->evicted;
   out[1] = t->h_res->vbeg;
   out[2] = t->h_res->vend;
@@ -893,6 +919,7 @@ int prism_last_op(prism_tree *t, int64_t *out) {
 int prism_insert(prism_tree *t, const uint32_t *path, int64_t n, int64_t na, const int32_t *a_off,
                  const int8_t *a_kind, const int32_t *a_seg, const int32_t *a_snap, int32_t *leaf_slot,
                  int64_t *leaf_id) {
+  join_aux(t);
   if (n < 0 || n > MAX_PATH) return fail(PRISM_INVALID, "path length out of range");
   int rc = validate_anchors(n, na, a_off, a_kind, a_seg);
   if (rc) return rc;
@@ -913,6 +940,7 @@ int prism_insert(prism_tree *t, const uint32_t *path, int64_t n, int64_t na, con
 }
 
 int prism_release(prism_tree *t, int64_t n, const int32_t *slots, const int64_t *ids) {
+  join_aux(t);
   if (n <= 0) return PRISM_OK;
   cudaSetDevice(t->dev);
   int32_t *ds = nullptr;
@@ -934,6 +962,7 @@ int prism_release(prism_tree *t, int64_t n, const int32_t *slots, const int64_t 
 }
 
 int prism_release_device(prism_tree *t, int64_t n, const int32_t *slots, const int64_t *ids, void *stream) {
+  join_aux(t);
   (void)ids;
   if (n <= 0) return PRISM_OK;
   cudaSetDevice(t->dev);
@@ -945,6 +974,7 @@ int prism_release_device(prism_tree *t, int64_t n, const int32_t *slots, const i
 }
 
 int prism_evict(prism_tree *t, int64_t k_free, int64_t *freed) {
+  join_aux(t);
   if (k_free < 0) return fail(PRISM_INVALID, "k_free must be >= 0");
   cudaSetDevice(t->dev);
   int rc = run_commit(t, one_op(t, OP_EVICT, 0, 0, k_free));
@@ -1029,6 +1059,7 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out) {
 
 int prism_set_protection(prism_tree *t, int64_t n, const int32_t *segs, const double *vals,
                          int64_t *out_ids, int64_t *n_out) {
+  join_aux(t);
   cudaSetDevice(t->dev);
   int32_t nseg = 0;
   for (int64_t i = 0; i < n; i++) {
@@ -1048,8 +1079,8 @@ int prism_set_protection(prism_tree *t, int64_t n, const int32_t *segs, const do
 }
 
 // set_protection from a dense device P-hat array (the QAS round's output)
-int prism_set_protection_device(prism_tree *t, const double *d_pri, int32_t nseg, int64_t *out_ids,
-                                int64_t *n_out) {
+static int prism_set_protection_device_impl(prism_tree *t, const double *d_pri, int32_t nseg,
+                                           int64_t *out_ids, int64_t *n_out) {
   cudaSetDevice(t->dev);
   if (nseg > t->d.npri) {
     CK(cudaFree(t->d.pri));
@@ -1060,9 +1091,33 @@ int prism_set_protection_device(prism_tree *t, const double *d_pri, int32_t nseg
   return protect_current(t, out_ids, n_out);
 }
 
+int prism_set_protection_device(prism_tree *t, const double *d_pri, int32_t nseg, int64_t *out_ids,
+                                int64_t *n_out) {
+  join_aux(t);
+  return prism_set_protection_device_impl(t, d_pri, nseg, out_ids, n_out);
+}
+
+// set_protection from a dense device P-hat array, on the auxiliary stream:
+// ordered after the tree stream's work so far, joined by the tree stream
+// before the next eviction-order build or API call (join_aux)
+int prism_set_protection_device_async(prism_tree *t, const double *d_pri, int32_t nseg) {
+  cudaSetDevice(t->dev);
+  join_aux(t);
+  CK(cudaEventRecord(t->ev_main, t->st));
+  CK(cudaStreamWaitEvent(t->st_aux, t->ev_main, 0));
+  std::swap(t->st, t->st_aux);
+  int rc = prism_set_protection_device_impl(t, d_pri, nseg, nullptr, nullptr);
+  std::swap(t->st, t->st_aux);
+  if (rc) return rc;
+  CK(cudaEventRecord(t->ev_aux, t->st_aux));
+  t->aux_pending = 1;
+  return PRISM_OK;
+}
+
 // LRU_ACTIVE hand-off (engine.py:195-197) from dense device counters:
 // active = segments with a count > 0 over the active set or the batch
 int prism_note_active_device(prism_tree *t, const int32_t *d_a, const int32_t *d_nd, int32_t nseg) {
+  join_aux(t);
   cudaSetDevice(t->dev);
   if (nseg > t->d.nact) {
     CK(cudaFree(t->d.act));
@@ -1083,6 +1138,7 @@ void *prism_tree_stream(prism_tree *t) { return (void *)t->st; }
 int32_t prism_tree_policy(prism_tree *t) { return t->d.policy; }
 
 int prism_note_active(prism_tree *t, int64_t n, const int32_t *segs) {
+  join_aux(t);
   cudaSetDevice(t->dev);
   int32_t nseg = 0;
   for (int64_t i = 0; i < n; i++) {
@@ -1111,6 +1167,7 @@ int prism_admit_wave_device(prism_tree *t, int64_t B, const int64_t *path_off, c
                             const int32_t *a_seg, const int32_t *a_snap, int64_t *hits,
                             int32_t *leaf_slots, int64_t *leaf_ids, int64_t *n_admitted_host,
                             void *stream) {
+  join_aux(t);
   cudaSetDevice(t->dev);
   if (B <= 0) {
     *n_admitted_host = 0;
@@ -1224,6 +1281,7 @@ int prism_admit_wave_segmented(prism_tree *t, int64_t B, const int64_t *path_off
 
 // out[3]: waves committed in parallel, waves committed in order, last fallback reason flags
 int prism_wave_stats(prism_tree *t, int64_t *out) {
+  join_aux(t);
   out[0] = t->par_waves;
   out[1] = t->seq_waves;
   out[2] = t->last_fallback;
@@ -1234,6 +1292,7 @@ int prism_admit_wave(prism_tree *t, int64_t B, const int64_t *path_off, const ui
                      const int64_t *anc_off, const int32_t *a_off, const int8_t *a_kind, const int32_t *a_seg,
                      const int32_t *a_snap, int64_t *hits, int32_t *leaf_slots, int64_t *leaf_ids,
                      int64_t *n_admitted) {
+  join_aux(t);
   cudaSetDevice(t->dev);
   if (B <= 0) {
     *n_admitted = 0;
@@ -1303,6 +1362,7 @@ int prism_admit_wave(prism_tree *t, int64_t B, const int64_t *path_off, const ui
 }
 
 int prism_stats(prism_tree *t, int64_t *out) {
+  join_aux(t);
   cudaSetDevice(t->dev);
   int rc = pull_ctrl(t);
   if (rc) return rc;
@@ -1328,6 +1388,7 @@ int prism_stats(prism_tree *t, int64_t *out) {
 
 int prism_victims(prism_tree *t, int64_t first, int64_t count, int64_t *ids, int8_t *kinds, int32_t *segs,
                   uint32_t *first_tok, int32_t *edge_len, int64_t *edge_off) {
+  join_aux(t);
   cudaSetDevice(t->dev);
   int rc = pull_ctrl(t);
   if (rc) return rc;
@@ -1356,6 +1417,7 @@ int prism_snapshot(prism_tree *t, int64_t cap, int64_t *hw_out, int64_t *node_id
                    int32_t *edge_len, int8_t *kind, int32_t *seg, int32_t *ref, int64_t *last, int32_t *hits,
                    int8_t *prot, int8_t *has_anchor, uint32_t *first_tok, int8_t *anchor_kind,
                    int32_t *anchor_seg, int32_t *anchor_off, int32_t *snap, int64_t *edge_off) {
+  join_aux(t);
   cudaSetDevice(t->dev);
   int rc = pull_ctrl(t);
   if (rc) return rc;
@@ -1387,6 +1449,7 @@ int prism_snapshot(prism_tree *t, int64_t cap, int64_t *hw_out, int64_t *node_id
 }
 
 int prism_arena_read(prism_tree *t, int64_t off, int64_t n, uint32_t *out) {
+  join_aux(t);
   cudaSetDevice(t->dev);
   if (off < 0 || n < 0 || off + n > t->d.acap) return fail(PRISM_INVALID, "arena range");
   if (n) CK(cudaMemcpyAsync(out, t->d.tok + off, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, t->st));
@@ -1395,6 +1458,7 @@ int prism_arena_read(prism_tree *t, int64_t off, int64_t n, uint32_t *out) {
 }
 
 int prism_evict_key(prism_tree *t, int32_t slot, uint64_t *key3) {
+  join_aux(t);
   cudaSetDevice(t->dev);
   Key3 *dk = nullptr;
   CK(dalloc(&dk, 1));
@@ -1412,6 +1476,7 @@ int64_t prism_compactions(prism_tree *t) { return t->compactions; }
 // each merge round, end); out[38] = 1 if the sample select produced it,
 // out[39] = selected-prefix size
 int prism_coop_timeline(prism_tree *t, uint64_t *out, int32_t *n) {
+  join_aux(t);
   cudaSetDevice(t->dev);
   CK(cudaMemcpyAsync(out, t->cst->ts_build, 40 * sizeof(uint64_t), cudaMemcpyDeviceToHost, t->st));
   CK(cudaMemcpyAsync(n, &t->cst->nts_build, sizeof(int32_t), cudaMemcpyDeviceToHost, t->st));
@@ -1448,6 +1513,7 @@ int prism_profile(prism_tree *t, int32_t enable) {
 // device ms [0..8), calls [8..16), own kernel launches [16..24); out[24] CUB calls;
 // out[25] chain nodes, out[26] inserted tokens (SURVEY.md 8(d) byte model)
 int prism_profile_read(prism_tree *t, double *out) {
+  join_aux(t);
   int rc = pull_ctrl(t);
   if (rc) return rc;
   for (int i = 0; i < 8; i++) {

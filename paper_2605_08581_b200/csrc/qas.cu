@@ -1334,7 +1334,7 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
       QCK(cudaEventDestroy(ev));
     }
     const int32_t pol = prism_tree_policy(t);
-    if (pol == 0) rc = prism_set_protection_device(t, q->prio, nseg, nullptr, nullptr);
+    if (pol == 0) rc = prism_set_protection_device_async(t, q->prio, nseg);  // overlaps the serialization
     else if (pol == 2) rc = prism_note_active_device(t, q->a, q->nd, nseg);
     if (rc) return rc;
     // serialization (K1), then the admission on the tree's stream
