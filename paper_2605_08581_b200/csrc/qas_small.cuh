@@ -19,6 +19,7 @@
 #pragma once
 #include <cooperative_groups.h>
 #include <cstdint>
+#include <cub/block/block_radix_sort.cuh>
 
 namespace qsmall {
 
@@ -599,43 +600,77 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
     }
     qs_gsync();
   }
+  // 3b. every request's bucket representative = its bucket's first member
+  // (final now that every insert is done), into bidx (scratch until phase 10)
+  for (int64_t i0 = 0; i0 < P; i0 += gs) {
+    const int64_t i = i0 + qs_ilv(gs);
+    if (i < P) A.bidx[i] = qs_ld(&A.btab_min[qs_ld(&A.slot_of[i])]);
+  }
+  qs_gsync();
   QS_TS(3);
   // 4. (block 0) bucket creation order = order of first members; in-bucket
-  // ranks in pending order (211-223)
+  // ranks in pending order (211-223): a stable block radix sort of the bucket
+  // ids (items in pending order) gives each request its position in its bucket
   if (b0) {
-    for (int64_t i = tid; i < P; i += blockDim.x) {
-      const int32_t first = qs_ld(&A.btab_min[qs_ld(&A.slot_of[i])]);
-      sbk[i] = first;
-      scnt[i] = first == (int32_t)i ? 1 : 0;
+    using BRS = cub::BlockRadixSort<unsigned, QS_TPB, QS_MAXP / QS_TPB, unsigned>;
+    constexpr int IPT = QS_MAXP / QS_TPB;
+    int32_t *bstart = scnt;  // [nb] first sorted position of each bucket
+    // bucket ids: exclusive count of first members before each first member
+    unsigned first[IPT], fl[IPT];
+    unsigned my = 0;
+#pragma unroll
+    for (int u = 0; u < IPT; u++) {
+      const int64_t i = (int64_t)tid * IPT + u;
+      first[u] = i < P ? (unsigned)qs_ld(&A.bidx[i]) : 0u;
+      fl[u] = (i < P && first[u] == (unsigned)i) ? 1u : 0u;
+      my += fl[u];
+    }
+    sbk[tid] = (int32_t)my;
+    __syncthreads();
+    const int32_t nb = block_exscan(sbk, QS_TPB, swarp);  // per-thread exclusive first-member counts
+    unsigned run = (unsigned)sbk[tid];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < IPT; u++) {  // sbk[first member] = its bucket id
+      const int64_t i = (int64_t)tid * IPT + u;
+      if (fl[u]) sbk[i] = (int32_t)run;
+      run += fl[u];
     }
     __syncthreads();
-    const int32_t nb = block_exscan(scnt, (int)P, swarp);
-    for (int64_t i = tid; i < P; i += blockDim.x) sbk[i] = scnt[sbk[i]];
+    unsigned key[IPT], val[IPT];
+#pragma unroll
+    for (int u = 0; u < IPT; u++) {
+      const int64_t i = (int64_t)tid * IPT + u;
+      key[u] = i < P ? (unsigned)sbk[first[u]] : (unsigned)QS_MAXP;  // padding sorts last
+      val[u] = (unsigned)i;
+    }
     __syncthreads();
-    for (int b = tid; b < nb; b += blockDim.x) scnt[b] = 0;
+    static_assert(sizeof(typename BRS::TempStorage) <= sizeof(QKey) * QS_MAXP, "radix-sort storage");
+    typename BRS::TempStorage &ts = *reinterpret_cast<typename BRS::TempStorage *>(sk);
+    BRS(ts).Sort(key, val, 0, 13);  // stable: pending order inside a bucket (ids < 2^13)
     __syncthreads();
-    if (tid < 32) {  // warp 0 walks P in order
-      const int lane = tid;
-      for (int64_t base = 0; base < P; base += 32) {
-        const int64_t i = base + lane;
-        const int32_t b = i < P ? sbk[i] : -1 - lane;
-        const unsigned peers = __match_any_sync(0xffffffffu, b);
-        const int32_t before = __popc(peers & ((1u << lane) - 1u));
-        const int32_t r = i < P ? scnt[b] + before : 0;
-        __syncwarp();
-        if (i < P) {
-          A.rank[i] = r;
-          if (lane == 31 - __clz(peers)) scnt[b] = r + 1;  // highest lane of the group
-        }
-        __syncwarp();
+    // thread tid now holds sorted positions tid*IPT + u; sv: the sorted keys
+#pragma unroll
+    for (int u = 0; u < IPT; u++) sv[tid * IPT + u] = (int32_t)key[u];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < IPT; u++) {
+      const int pos = tid * IPT + u;
+      if (pos < P && (pos == 0 || sv[pos - 1] != (int32_t)key[u])) bstart[key[u]] = pos;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < IPT; u++) {
+      const int pos = tid * IPT + u;
+      if (pos >= P) continue;
+      const int32_t b = (int32_t)key[u];
+      A.rank[val[u]] = pos - bstart[b];
+      A.bucket[val[u]] = b;
+      if (pos == (int)P - 1 || sv[pos + 1] != b) {  // last of its bucket
+        A.bsize[b] = pos - bstart[b] + 1;
+        A.nsegs[b] = 0;
+        A.isum[b] = 0;
       }
-    }
-    __syncthreads();
-    for (int64_t i = tid; i < P; i += blockDim.x) A.bucket[i] = sbk[i];
-    for (int b = tid; b < nb; b += blockDim.x) {
-      A.bsize[b] = scnt[b];
-      A.nsegs[b] = 0;
-      A.isum[b] = 0;
     }
     if (tid == 0) A.counts[2] = nb;
   }
