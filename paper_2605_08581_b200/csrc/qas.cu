@@ -632,7 +632,7 @@ int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, con
     int64_t bt = 64;
     while (bt < 2 * P) bt <<= 1;
     int64_t pt = 64;
-    while (pt < 2 * P * qsmall::QS_SKCAP) pt <<= 1;  // pairs: distinct (bucket, seg) <= nsk
+    while (pt < 4 * P * qsmall::QS_SKCAP) pt <<= 1;  // pairs: distinct (bucket, seg) <= nsk, load <= 1/4
     QCK(grow(&q->tkey, q->tkey_cap, bt));
     QCK(grow(&q->tmin, q->tmin_cap, bt));
     QCK(grow(&q->slot_of, q->slot_of_cap, P));
@@ -1301,6 +1301,7 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
       q_scan2<<<1, 1024, 0, st>>>(B, q->plen, q->alen, q->poff, q->aoffs, q->tmp_tot);
       q->launches += 2;
     }
+    if (q->prof_on) cudaEventRecord(q->e1, st);  // device time of the round + dispatch order only
     int64_t hb[6] = {0, 0, 0, 0, 0, 0};  // qcounts[2..3], tokens, anchors, err
     if (nb < 0) QCK(cudaMemcpyAsync(hb, q->qcounts + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     if (B > 0) {
@@ -1313,7 +1314,6 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
       continue;
     }
     if (q->prof_on) {
-      cudaEventRecord(q->e1, st);
       cudaEventSynchronize(q->e1);
       float ms = 0.f;
       cudaEventElapsedTime(&ms, q->e0, q->e1);

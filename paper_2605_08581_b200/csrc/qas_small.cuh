@@ -437,12 +437,12 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   const int64_t nsk = A.off[P];
   // skeleton entries beyond the preallocated buffers: the host redoes the round
   // (uniform over the grid: every thread reads the same values)
-  if (nsk > A.aligned_cap || 2 * nsk > A.ptab_cap) {
+  if (nsk > A.aligned_cap || 4 * nsk > A.ptab_cap) {
     if (gt == 0) A.counts[3] = 1;
     return;
   }
-  int64_t pm = 64;  // pair table in use: load factor <= 1/2
-  while (pm < 2 * nsk) pm <<= 1;
+  int64_t pm = 64;  // pair table in use
+  while (pm < 4 * nsk) pm <<= 1;  // load factor <= 1/4: short linear-probe tails
   const uint64_t pmask = (uint64_t)pm - 1;
   QS_TS(0);
   // 0. reset what the previous round touched; clear the tables
@@ -534,14 +534,17 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
       continue;
     }
     int32_t s[QS_MAXK], al[QS_MAXK];
-    double p[QS_MAXK];
+    double p[QS_MAXK], pa[QS_MAXK];  // priorities by skeleton / by aligned position
     int ord[QS_MAXK];
     for (int j = 0; j < k; j++) {
       s[j] = A.sk[b + j];
       p[j] = qpri0(c, A.g, A.a, s[j]);
     }
     if (!A.reo[i] || k == 0) {
-      for (int j = 0; j < k; j++) al[j] = s[j];
+      for (int j = 0; j < k; j++) {
+        al[j] = s[j];
+        pa[j] = p[j];
+      }
     } else {
       for (int j = 0; j < k; j++) {
         int q = j;
@@ -555,19 +558,22 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
       uint32_t chosen = 0;
       int w = 0;
       for (int q = 0; q < f; q++) {
+        pa[w] = p[ord[q]];
         al[w++] = s[ord[q]];
         chosen |= 1u << ord[q];
       }
       for (int j = 0; j < k; j++)
-        if (!((chosen >> j) & 1u)) al[w++] = s[j];
+        if (!((chosen >> j) & 1u)) {
+          pa[w] = p[j];
+          al[w++] = s[j];
+        }
     }
     for (int j = 0; j < k; j++) A.aligned[b + j] = al[j];
     int sl = 0;
     if (k > 0) {
-      for (int j = 0; j < k; j++) {  // ranks over the aligned order (p by position)
-        p[j] = qpri0(c, A.g, A.a, al[j]);
+      for (int j = 0; j < k; j++) {  // ranks over the aligned order (priorities carried along)
         int q = j;
-        while (q > 0 && qrank_before(p[j], al[j], j, p[ord[q - 1]], al[ord[q - 1]], ord[q - 1])) {
+        while (q > 0 && qrank_before(pa[j], al[j], j, pa[ord[q - 1]], al[ord[q - 1]], ord[q - 1])) {
           ord[q] = ord[q - 1];
           q--;
         }
@@ -716,14 +722,27 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   QS_TS(5);
   // 8. utility terms of the distinct pairs, summed exactly (integral weights)
   const int64_t npairs = (int64_t)__ldcg((const unsigned long long *)&A.counts[5]);
-  for (int64_t t = gt; t < npairs; t += gs) {
-    const int32_t pos = A.plist[t];
-    const uint64_t key = __ldcg((const unsigned long long *)&A.ptab_key[pos]);
-    const int32_t bk = (int32_t)(key >> 32), s = (int32_t)(key & 0xffffffffu);
-    const double t1 = __dmul_rn(c.wg, (double)A.g[s]);
-    const double t2 = __dmul_rn(c.wa, (double)A.a[s]);
-    const double t3 = __dmul_rn(c.wn, (double)qs_ld(&A.ptab_cnt[pos]));
-    atomicAdd((unsigned long long *)&A.isum[bk], (unsigned long long)(long long)__dadd_rn(__dadd_rn(t1, t2), t3));
+  for (int64_t t0 = 0; t0 < npairs; t0 += gs) {  // warp-combined per bucket (hot buckets collect many pairs)
+    const int64_t t = t0 + gt;
+    int32_t bk = -1 - (int32_t)(tid & 31);
+    unsigned long long v = 0;
+    if (t < npairs) {
+      const int32_t pos = A.plist[t];
+      const uint64_t key = __ldcg((const unsigned long long *)&A.ptab_key[pos]);
+      bk = (int32_t)(key >> 32);
+      const int32_t s = (int32_t)(key & 0xffffffffu);
+      const double t1 = __dmul_rn(c.wg, (double)A.g[s]);
+      const double t2 = __dmul_rn(c.wa, (double)A.a[s]);
+      const double t3 = __dmul_rn(c.wn, (double)qs_ld(&A.ptab_cnt[pos]));
+      v = (unsigned long long)(long long)__dadd_rn(__dadd_rn(t1, t2), t3);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, bk);
+    // exact 64-bit sum over the peers from three 24/24/16-bit partial sums
+    const unsigned long long s0 = __reduce_add_sync(peers, (unsigned)(v & 0xFFFFFFull));
+    const unsigned long long s1 = __reduce_add_sync(peers, (unsigned)((v >> 24) & 0xFFFFFFull));
+    const unsigned long long s2 = __reduce_add_sync(peers, (unsigned)(v >> 48));
+    if (t < npairs && (int)(tid & 31) == __ffs(peers) - 1)
+      atomicAdd((unsigned long long *)&A.isum[bk], s0 + (s1 << 24) + (s2 << 48));
   }
   qs_gsync();
   QS_TS(6);
@@ -756,14 +775,19 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   qs_gsync();
   QS_TS(7);
   // 10. hot lane, and n_disp of its members (247-248)
-  for (int64_t i = gt; i < P; i += gs) {
+  for (int64_t i0 = 0; i0 < P; i0 += gs) {
+    const int64_t i = i0 + qs_ilv(gs);
+    if (i >= P) continue;
     const int32_t b = A.bucket[i];
     const bool h = A.rank[i] < qs_ld(&A.nsegs[b]);
     A.bidx[i] = h ? 1 : 0;  // reuse: hot flag
-    if (h) {
-      A.hot[(int64_t)__ldcg((const unsigned long long *)&A.isum[b]) + A.rank[i]] = i;
-      qs_distinct(A.sk, A.off[i], A.off[i + 1], [&](int32_t s) { atomicAdd(&A.nd[s], 1); });
-    }
+    if (h) A.hot[(int64_t)__ldcg((const unsigned long long *)&A.isum[b]) + A.rank[i]] = i;
+  }
+  for (int64_t e = gt; e < nsk; e += gs) {  // n_disp of the hot members: one thread per skeleton entry
+    const int64_t i = A.emap[e];
+    const int32_t b = A.bucket[i];
+    int32_t s = 0;
+    if (A.rank[i] < qs_ld(&A.nsegs[b]) && qs_first(A.sk, A.off[i], e, s)) atomicAdd(&A.nd[s], 1);
   }
   qs_gsync();
   QS_TS(8);
