@@ -889,10 +889,21 @@ struct EvictCand {
 // previous protection flag
 struct ProtCand {
   DT T;
+  int32_t keys;  // also leave the eviction keys of the unprotected tree (kw / eff, as k_build_keys)
   __device__ int32_t hw() const { return T.ctrl->hw; }
   __device__ bool operator()(int32_t s, Key3 &k, uint64_t &v, int64_t &w) const {
     T.prot[s] = 0;
-    if (s == ROOT || T.nid[s] < 0 || T.par[s] < 0 || !T.hasanc[s] || T.akind[s] != K_REUSABLE) return false;
+    const bool live = s != ROOT && T.nid[s] >= 0 && T.par[s] >= 0;
+    if (keys) {
+      if (!live) {
+        T.eff[s] = EFF_DEAD;
+      } else {
+        const bool blocked = T.ref[s] > 0 || (T.policy == P_DART && T.kind[s] == K_SYSTEM);
+        T.kw[s] = make_key(T, s);  // (prot cleared above; the top-f get theirs in k_protect_coop)
+        T.eff[s] = blocked ? EFF_BLOCKED : s;
+      }
+    }
+    if (!live || !T.hasanc[s] || T.akind[s] != K_REUSABLE) return false;
     const int32_t sg = T.seg[s];
     const int32_t sv = sg == SEG_NONE ? -1 : sg;
     k = {0, 0, 0};
@@ -1338,14 +1349,14 @@ __global__ void __launch_bounds__(COOP_TPB) k_build_coop(DT T, CoopBufs B, int64
 // set_protection (kvcache.py:364-383): top-f reusable anchors by (-P-hat, seg
 // or -1, id) -- from the sample select when it succeeded, else materialised
 __global__ void __launch_bounds__(COOP_TPB) k_protect_coop(DT T, CoopBufs B, int64_t f, int64_t min_cand,
-                                                           int64_t small, int32_t sampled) {
+                                                           int64_t small, int32_t sampled, int32_t keys) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ Key3 smin[COOP_TPB + 1], smax[COOP_TPB + 1];
   cg::grid_group grid = cg::this_grid();
   const int32_t hw = T.ctrl->hw;
   const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const ProtCand cand{T};
+  const ProtCand cand{T, keys};
   int64_t n = 0, nsel = 0;
   const bool fast = sampled && B.st->ss_ok;
   if (fast) {
@@ -1376,6 +1387,7 @@ __global__ void __launch_bounds__(COOP_TPB) k_protect_coop(DT T, CoopBufs B, int
   for (int64_t i = gtid; i < nf; i += gsz) {
     const int32_t s = (int32_t)(T.Lv[i] & 0xffffffffu);
     T.prot[s] = 1;
+    if (keys) T.kw[s] = make_key(T, s);  // protected: class 2 (kvcache.py:405-406)
     if (B.out_ids) B.out_ids[i] = T.nid[s];
   }
   if (gtid == 0) B.st->prot_n = nf;

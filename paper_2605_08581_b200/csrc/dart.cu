@@ -68,6 +68,7 @@ struct prism_tree {
   cudaStream_t st_aux = nullptr;
   cudaEvent_t ev_aux = nullptr, ev_main = nullptr;
   int aux_pending = 0;
+  int keys_fresh = 0;  // the protection pass left the eviction keys (k_build_keys not needed)
   DT d{};
   Ctrl *hctrl = nullptr;  // pinned
   int64_t protect_budget = 0;
@@ -158,6 +159,12 @@ inline void join_aux(prism_tree *t) {
     cudaStreamWaitEvent(t->st, t->ev_aux, 0);
     t->aux_pending = 0;
   }
+}
+// public entry points: join the auxiliary stream; keys left by a protection
+// pass are only trusted by the build of the same fused wave
+inline void api_enter(prism_tree *t) {
+  join_aux(t);
+  t->keys_fresh = 0;
 }
 
 // ----------------------------------------------------------------- slot arrays
@@ -390,7 +397,8 @@ int build_list(prism_tree *t, int64_t W, const int64_t *dW = nullptr) {
     // keys / subtree maxima / gather at full occupancy over the slot range
     // (each reads hw from the control block; the count lands in cst->cand)
     const int64_t S = t->d.S;
-    k_build_keys<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1, dW);
+    if (!t->keys_fresh) k_build_keys<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1, dW);
+    t->keys_fresh = 0;  // consumed (the commit mutates the tree next)
     k_propagate<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1, dW);
     CoopBufs B = coop_bufs(t);
     int64_t minc = t->sel_min_candidates, small = std::min<int64_t>(SEL_SMALL, t->sel_min_candidates);
@@ -406,6 +414,7 @@ int build_list(prism_tree *t, int64_t W, const int64_t *dW = nullptr) {
     prof_end(t, PH_BUILD);
     return PRISM_OK;
   }
+  t->keys_fresh = 0;
   const int32_t hw = t->hctrl->hw;
   prof_begin(t);
   CK(cudaMemsetAsync(t->d_count, 0, 2 * sizeof(int64_t), t->st));
@@ -872,7 +881,7 @@ void prism_tree_destroy(prism_tree *t) {
 
 int prism_match(prism_tree *t, const uint32_t *path, int64_t n, int64_t *hit, int32_t *visited_slots,
                 int64_t *visited_ids, int64_t *n_visited) {
-  join_aux(t);
+  api_enter(t);
   if (n < 0 || n > MAX_PATH) return fail(PRISM_INVALID, "path length out of range");
   cudaSetDevice(t->dev);
   int rc = ensure_buf(&t->d_path, t->path_cap, n);
@@ -907,7 +916,7 @@ int prism_match(prism_tree *t, const uint32_t *path, int64_t n, int64_t *hit, in
 
 // last-op details for the Python binding: [evicted, vbeg, vend, freed, status]
 int prism_last_op(prism_tree *t, int64_t *out) {
-  join_aux(t);
+  api_enter(t);
   out[0] = t->h_res->evicted;
   out[1] = t->h_res->vbeg;
   out[2] = t->h_res->vend;
@@ -919,7 +928,7 @@ int prism_last_op(prism_tree *t, int64_t *out) {
 int prism_insert(prism_tree *t, const uint32_t *path, int64_t n, int64_t na, const int32_t *a_off,
                  const int8_t *a_kind, const int32_t *a_seg, const int32_t *a_snap, int32_t *leaf_slot,
                  int64_t *leaf_id) {
-  join_aux(t);
+  api_enter(t);
   if (n < 0 || n > MAX_PATH) return fail(PRISM_INVALID, "path length out of range");
   int rc = validate_anchors(n, na, a_off, a_kind, a_seg);
   if (rc) return rc;
@@ -940,7 +949,7 @@ int prism_insert(prism_tree *t, const uint32_t *path, int64_t n, int64_t na, con
 }
 
 int prism_release(prism_tree *t, int64_t n, const int32_t *slots, const int64_t *ids) {
-  join_aux(t);
+  api_enter(t);
   if (n <= 0) return PRISM_OK;
   cudaSetDevice(t->dev);
   int32_t *ds = nullptr;
@@ -962,7 +971,7 @@ int prism_release(prism_tree *t, int64_t n, const int32_t *slots, const int64_t 
 }
 
 int prism_release_device(prism_tree *t, int64_t n, const int32_t *slots, const int64_t *ids, void *stream) {
-  join_aux(t);
+  api_enter(t);
   (void)ids;
   if (n <= 0) return PRISM_OK;
   cudaSetDevice(t->dev);
@@ -974,7 +983,7 @@ int prism_release_device(prism_tree *t, int64_t n, const int32_t *slots, const i
 }
 
 int prism_evict(prism_tree *t, int64_t k_free, int64_t *freed) {
-  join_aux(t);
+  api_enter(t);
   if (k_free < 0) return fail(PRISM_INVALID, "k_free must be >= 0");
   cudaSetDevice(t->dev);
   int rc = run_commit(t, one_op(t, OP_EVICT, 0, 0, k_free));
@@ -986,7 +995,7 @@ int prism_evict(prism_tree *t, int64_t k_free, int64_t *freed) {
 }
 
 // top-f reusable anchors by (-P-hat, segment, id) with the current t->d.pri
-static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out) {
+static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out, int32_t keys = 0) {
   int rc;
   if (t->use_coop) {  // one cooperative kernel; no host round trip unless ids are wanted
     int grid = coop_grid(t);
@@ -1000,11 +1009,12 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out) {
     int64_t ff = f;
     int32_t sampled = (t->use_sample && f > 0) ? 1 : 0;
     if (sampled) {
-      rc = sample_select(t, ProtCand{t->d}, B, ff, nullptr, minc);
+      rc = sample_select(t, ProtCand{t->d, keys}, B, ff, nullptr, minc);
       if (rc) return rc;
       t->launches[PH_PROTECT] += 5;
     }
-    void *args[] = {(void *)&t->d, (void *)&B, (void *)&ff, (void *)&minc, (void *)&small, (void *)&sampled};
+    void *args[] = {(void *)&t->d, (void *)&B, (void *)&ff, (void *)&minc, (void *)&small, (void *)&sampled,
+                    (void *)&keys};
     CK(cudaLaunchCooperativeKernel((void *)k_protect_coop, grid, COOP_TPB, args, COOP_SMEM, t->st));
     t->launches[PH_PROTECT] += 1;
     prof_end(t, PH_PROTECT);
@@ -1059,7 +1069,7 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out) {
 
 int prism_set_protection(prism_tree *t, int64_t n, const int32_t *segs, const double *vals,
                          int64_t *out_ids, int64_t *n_out) {
-  join_aux(t);
+  api_enter(t);
   cudaSetDevice(t->dev);
   int32_t nseg = 0;
   for (int64_t i = 0; i < n; i++) {
@@ -1080,7 +1090,7 @@ int prism_set_protection(prism_tree *t, int64_t n, const int32_t *segs, const do
 
 // set_protection from a dense device P-hat array (the QAS round's output)
 static int prism_set_protection_device_impl(prism_tree *t, const double *d_pri, int32_t nseg,
-                                           int64_t *out_ids, int64_t *n_out) {
+                                           int64_t *out_ids, int64_t *n_out, int32_t keys = 0) {
   cudaSetDevice(t->dev);
   if (nseg > t->d.npri) {
     CK(cudaFree(t->d.pri));
@@ -1088,12 +1098,12 @@ static int prism_set_protection_device_impl(prism_tree *t, const double *d_pri, 
   }
   if (nseg) CK(cudaMemcpyAsync(t->d.pri, d_pri, sizeof(double) * nseg, cudaMemcpyDeviceToDevice, t->st));
   t->d.npri = nseg;
-  return protect_current(t, out_ids, n_out);
+  return protect_current(t, out_ids, n_out, keys);
 }
 
 int prism_set_protection_device(prism_tree *t, const double *d_pri, int32_t nseg, int64_t *out_ids,
                                 int64_t *n_out) {
-  join_aux(t);
+  api_enter(t);
   return prism_set_protection_device_impl(t, d_pri, nseg, out_ids, n_out);
 }
 
@@ -1102,22 +1112,25 @@ int prism_set_protection_device(prism_tree *t, const double *d_pri, int32_t nseg
 // before the next eviction-order build or API call (join_aux)
 int prism_set_protection_device_async(prism_tree *t, const double *d_pri, int32_t nseg) {
   cudaSetDevice(t->dev);
-  join_aux(t);
+  api_enter(t);
   CK(cudaEventRecord(t->ev_main, t->st));
   CK(cudaStreamWaitEvent(t->st_aux, t->ev_main, 0));
   std::swap(t->st, t->st_aux);
-  int rc = prism_set_protection_device_impl(t, d_pri, nseg, nullptr, nullptr);
+  // the pass over every node also leaves the eviction keys (cooperative path)
+  const int32_t keys = t->use_coop ? 1 : 0;
+  int rc = prism_set_protection_device_impl(t, d_pri, nseg, nullptr, nullptr, keys);
   std::swap(t->st, t->st_aux);
   if (rc) return rc;
   CK(cudaEventRecord(t->ev_aux, t->st_aux));
   t->aux_pending = 1;
+  t->keys_fresh = keys;
   return PRISM_OK;
 }
 
 // LRU_ACTIVE hand-off (engine.py:195-197) from dense device counters:
 // active = segments with a count > 0 over the active set or the batch
 int prism_note_active_device(prism_tree *t, const int32_t *d_a, const int32_t *d_nd, int32_t nseg) {
-  join_aux(t);
+  api_enter(t);
   cudaSetDevice(t->dev);
   if (nseg > t->d.nact) {
     CK(cudaFree(t->d.act));
@@ -1138,7 +1151,7 @@ void *prism_tree_stream(prism_tree *t) { return (void *)t->st; }
 int32_t prism_tree_policy(prism_tree *t) { return t->d.policy; }
 
 int prism_note_active(prism_tree *t, int64_t n, const int32_t *segs) {
-  join_aux(t);
+  api_enter(t);
   cudaSetDevice(t->dev);
   int32_t nseg = 0;
   for (int64_t i = 0; i < n; i++) {
@@ -1167,7 +1180,7 @@ int prism_admit_wave_device(prism_tree *t, int64_t B, const int64_t *path_off, c
                             const int32_t *a_seg, const int32_t *a_snap, int64_t *hits,
                             int32_t *leaf_slots, int64_t *leaf_ids, int64_t *n_admitted_host,
                             void *stream) {
-  join_aux(t);
+  api_enter(t);
   cudaSetDevice(t->dev);
   if (B <= 0) {
     *n_admitted_host = 0;
@@ -1281,7 +1294,7 @@ int prism_admit_wave_segmented(prism_tree *t, int64_t B, const int64_t *path_off
 
 // out[3]: waves committed in parallel, waves committed in order, last fallback reason flags
 int prism_wave_stats(prism_tree *t, int64_t *out) {
-  join_aux(t);
+  api_enter(t);
   out[0] = t->par_waves;
   out[1] = t->seq_waves;
   out[2] = t->last_fallback;
@@ -1292,7 +1305,7 @@ int prism_admit_wave(prism_tree *t, int64_t B, const int64_t *path_off, const ui
                      const int64_t *anc_off, const int32_t *a_off, const int8_t *a_kind, const int32_t *a_seg,
                      const int32_t *a_snap, int64_t *hits, int32_t *leaf_slots, int64_t *leaf_ids,
                      int64_t *n_admitted) {
-  join_aux(t);
+  api_enter(t);
   cudaSetDevice(t->dev);
   if (B <= 0) {
     *n_admitted = 0;
@@ -1362,7 +1375,7 @@ int prism_admit_wave(prism_tree *t, int64_t B, const int64_t *path_off, const ui
 }
 
 int prism_stats(prism_tree *t, int64_t *out) {
-  join_aux(t);
+  api_enter(t);
   cudaSetDevice(t->dev);
   int rc = pull_ctrl(t);
   if (rc) return rc;
@@ -1388,7 +1401,7 @@ int prism_stats(prism_tree *t, int64_t *out) {
 
 int prism_victims(prism_tree *t, int64_t first, int64_t count, int64_t *ids, int8_t *kinds, int32_t *segs,
                   uint32_t *first_tok, int32_t *edge_len, int64_t *edge_off) {
-  join_aux(t);
+  api_enter(t);
   cudaSetDevice(t->dev);
   int rc = pull_ctrl(t);
   if (rc) return rc;
@@ -1417,7 +1430,7 @@ int prism_snapshot(prism_tree *t, int64_t cap, int64_t *hw_out, int64_t *node_id
                    int32_t *edge_len, int8_t *kind, int32_t *seg, int32_t *ref, int64_t *last, int32_t *hits,
                    int8_t *prot, int8_t *has_anchor, uint32_t *first_tok, int8_t *anchor_kind,
                    int32_t *anchor_seg, int32_t *anchor_off, int32_t *snap, int64_t *edge_off) {
-  join_aux(t);
+  api_enter(t);
   cudaSetDevice(t->dev);
   int rc = pull_ctrl(t);
   if (rc) return rc;
@@ -1449,7 +1462,7 @@ int prism_snapshot(prism_tree *t, int64_t cap, int64_t *hw_out, int64_t *node_id
 }
 
 int prism_arena_read(prism_tree *t, int64_t off, int64_t n, uint32_t *out) {
-  join_aux(t);
+  api_enter(t);
   cudaSetDevice(t->dev);
   if (off < 0 || n < 0 || off + n > t->d.acap) return fail(PRISM_INVALID, "arena range");
   if (n) CK(cudaMemcpyAsync(out, t->d.tok + off, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, t->st));
@@ -1458,7 +1471,7 @@ int prism_arena_read(prism_tree *t, int64_t off, int64_t n, uint32_t *out) {
 }
 
 int prism_evict_key(prism_tree *t, int32_t slot, uint64_t *key3) {
-  join_aux(t);
+  api_enter(t);
   cudaSetDevice(t->dev);
   Key3 *dk = nullptr;
   CK(dalloc(&dk, 1));
@@ -1476,7 +1489,7 @@ int64_t prism_compactions(prism_tree *t) { return t->compactions; }
 // each merge round, end); out[38] = 1 if the sample select produced it,
 // out[39] = selected-prefix size
 int prism_coop_timeline(prism_tree *t, uint64_t *out, int32_t *n) {
-  join_aux(t);
+  api_enter(t);
   cudaSetDevice(t->dev);
   CK(cudaMemcpyAsync(out, t->cst->ts_build, 40 * sizeof(uint64_t), cudaMemcpyDeviceToHost, t->st));
   CK(cudaMemcpyAsync(n, &t->cst->nts_build, sizeof(int32_t), cudaMemcpyDeviceToHost, t->st));
@@ -1513,7 +1526,7 @@ int prism_profile(prism_tree *t, int32_t enable) {
 // device ms [0..8), calls [8..16), own kernel launches [16..24); out[24] CUB calls;
 // out[25] chain nodes, out[26] inserted tokens (SURVEY.md 8(d) byte model)
 int prism_profile_read(prism_tree *t, double *out) {
-  join_aux(t);
+  api_enter(t);
   int rc = pull_ctrl(t);
   if (rc) return rc;
   for (int i = 0; i < 8; i++) {

@@ -839,8 +839,11 @@ __global__ void k_propagate(DT T, int32_t hw, const int64_t *dW = nullptr) {
   if (dW && *dW < 0) return;
   if (hw < 0) hw = T.ctrl->hw;
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= hw || s == ROOT || T.nid[s] < 0 || T.par[s] < 0) return;
-  const bool blocked = T.ref[s] > 0 || (T.policy == P_DART && T.kind[s] == K_SYSTEM);
+  if (s >= hw) return;
+  // k_build_keys left eff[s] = s (evictable so far), EFF_BLOCKED, or EFF_DEAD (root / free)
+  const int32_t e0 = __ldcg(&T.eff[s]);
+  if (e0 == EFF_DEAD) return;
+  const bool blocked = e0 == EFF_BLOCKED;
   const int32_t val = blocked ? EFF_BLOCKED : s;
   Key3 kv;
   if (!blocked) kv = T.kw[s];
@@ -976,10 +979,18 @@ __global__ void k_release_seq(DT T, int64_t n, const int32_t *__restrict__ slots
 }
 
 // batched release of valid pins: one warp per leaf, atomic decrements
+// the lanes of a warp climb their chains in lock step; lanes standing on the
+// same node (the shared upper levels: system prompt, popular segments, the
+// root) release it with one combined atomic
 __global__ void k_release_par(DT T, int64_t n, const int32_t *__restrict__ slots) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  for (int32_t x = slots[i]; x >= 0; x = T.par[x]) atomicSub(&T.ref[x], 1);
+  const int lane = threadIdx.x & 31;
+  int32_t x = i < n ? slots[i] : -1;
+  while (__any_sync(0xffffffffu, x >= 0)) {
+    const unsigned peers = __match_any_sync(0xffffffffu, x);
+    if (x >= 0 && lane == __ffs(peers) - 1) atomicSub(&T.ref[x], __popc(peers));
+    if (x >= 0) x = T.par[x];
+  }
 }
 
 // ------------------------------------------------------------ maintenance

@@ -21,6 +21,7 @@
 
 #include "../../include/prism.h"
 #include "qas_small.cuh"
+#include "scan.cuh"
 #include "select.cuh"
 
 namespace {
@@ -1091,59 +1092,16 @@ __global__ void q_members_len(int64_t nh, int64_t nc, const int64_t *__restrict_
 }
 
 // exclusive scans plen -> poff and alen -> aoffs over B + 1 entries (the last
-// input entry is 0), one CTA
+// input entry is 0) and their totals, one CTA
 __global__ void __launch_bounds__(1024) q_scan2(int64_t B, const int64_t *__restrict__ plen,
                                                 const int64_t *__restrict__ alen, int64_t *__restrict__ poff,
                                                 int64_t *__restrict__ aoffs, int64_t *__restrict__ tot) {
-  __shared__ int64_t s_w[2][32];
-  __shared__ int64_t s_carry[2];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if (threadIdx.x < 2) s_carry[threadIdx.x] = 0;
-  __syncthreads();
-  for (int64_t b0 = 0; b0 <= B; b0 += blockDim.x) {
-    const int64_t j = b0 + threadIdx.x;
-    const int64_t v0 = j < B ? plen[j] : 0, v1 = j < B ? alen[j] : 0;
-    int64_t x0 = v0, x1 = v1;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t y0 = __shfl_up_sync(0xffffffffu, x0, o), y1 = __shfl_up_sync(0xffffffffu, x1, o);
-      if (lane >= o) {
-        x0 += y0;
-        x1 += y1;
-      }
-    }
-    if (lane == 31) {
-      s_w[0][wid] = x0;
-      s_w[1][wid] = x1;
-    }
-    __syncthreads();
-    if (wid == 0) {
-      for (int a = 0; a < 2; a++) {
-        int64_t t = lane < nw ? s_w[a][lane] : 0;
-        for (int o = 1; o < 32; o <<= 1) {
-          const int64_t y = __shfl_up_sync(0xffffffffu, t, o);
-          if (lane >= o) t += y;
-        }
-        if (lane < nw) s_w[a][lane] = t;
-      }
-    }
-    __syncthreads();
-    const int64_t i0 = s_carry[0] + x0 + (wid ? s_w[0][wid - 1] : 0);
-    const int64_t i1 = s_carry[1] + x1 + (wid ? s_w[1][wid - 1] : 0);
-    if (j <= B) {
-      poff[j] = i0 - v0;
-      aoffs[j] = i1 - v1;
-    }
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) {
-      s_carry[0] = i0;
-      s_carry[1] = i1;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    tot[0] = s_carry[0];
-    tot[1] = s_carry[1];
-  }
+  prism::block_scan4<2, 8>(
+      B + 1, [&](int a, int64_t i) -> int64_t { return i >= B ? 0 : (a == 0 ? plen[i] : alen[i]); },
+      [&](int a, int64_t i, int64_t ex, int64_t) {
+        (a == 0 ? poff : aoffs)[i] = ex;
+        if (i == B) tot[a] = ex;
+      });
 }
 
 // one warp per member: token path and anchors

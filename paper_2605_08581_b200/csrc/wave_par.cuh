@@ -28,6 +28,7 @@
 // consumed victim on any member's pre-wave chain, enough evictable tokens.
 #pragma once
 #include "dart_kernels.cuh"
+#include "scan.cuh"
 
 namespace prism {
 
@@ -509,50 +510,17 @@ __global__ void k_wc_begin(DT T, WaveCtl *wc) {
 // exclusive scans cnew -> idb, tail -> arb (B + 1 entries) and the inclusive
 // scan miss -> dem (B entries), one CTA
 __global__ void __launch_bounds__(1024) k_wp_scan3(int64_t B, WaveTmp X) {
-  __shared__ int64_t s_w[3][32];
-  __shared__ int64_t s_carry[3];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if (threadIdx.x < 3) s_carry[threadIdx.x] = 0;
-  __syncthreads();
-  for (int64_t b0 = 0; b0 <= B; b0 += blockDim.x) {
-    const int64_t j = b0 + threadIdx.x;
-    int64_t v[3] = {j < B ? X.cnew[j] : 0, j < B ? X.tail[j] : 0, j < B ? X.miss[j] : 0};
-    int64_t x[3] = {v[0], v[1], v[2]};
-#pragma unroll
-    for (int a = 0; a < 3; a++) {
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t y = __shfl_up_sync(0xffffffffu, x[a], o);
-        if (lane >= o) x[a] += y;
-      }
-      if (lane == 31) s_w[a][wid] = x[a];
-    }
-    __syncthreads();
-    if (wid == 0) {
-#pragma unroll
-      for (int a = 0; a < 3; a++) {
-        int64_t t = lane < nw ? s_w[a][lane] : 0;
-        for (int o = 1; o < 32; o <<= 1) {
-          const int64_t y = __shfl_up_sync(0xffffffffu, t, o);
-          if (lane >= o) t += y;
-        }
-        if (lane < nw) s_w[a][lane] = t;
-      }
-    }
-    __syncthreads();
-    int64_t incl[3];
-#pragma unroll
-    for (int a = 0; a < 3; a++) incl[a] = s_carry[a] + x[a] + (wid ? s_w[a][wid - 1] : 0);
-    if (j <= B) {
-      X.idb[j] = incl[0] - v[0];
-      X.arb[j] = incl[1] - v[1];
-    }
-    if (j < B) X.dem[j] = incl[2];
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1)
-#pragma unroll
-      for (int a = 0; a < 3; a++) s_carry[a] = incl[a];
-    __syncthreads();
-  }
+  block_scan4<3, 8>(
+      B + 1,
+      [&](int a, int64_t i) -> int64_t {
+        if (i >= B) return 0;
+        return a == 0 ? X.cnew[i] : (a == 1 ? X.tail[i] : X.miss[i]);
+      },
+      [&](int a, int64_t i, int64_t ex, int64_t in) {
+        if (a == 0) X.idb[i] = ex;
+        else if (a == 1) X.arb[i] = ex;
+        else if (i < B) X.dem[i] = in;
+      });
 }
 
 // plan verdict: fallback flags, capacity headroom (slots, arena, child table),
