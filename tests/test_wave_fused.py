@@ -28,7 +28,7 @@ from paper_2605_08581_b200.types import (
 pytestmark = pytest.mark.gpu
 
 
-def _requests(rng, first_id, n, nseg, hot, kmin, kmax, suffixes, sys, chunk, zipf=1.3):
+def _requests(rng, first_id, n, nseg, hot, kmin, kmax, suffixes, sys, chunk, zipf=1.3, reo=1.0):
     reqs = []
     for i in range(n):
         k = int(rng.integers(kmin, kmax + 1))
@@ -40,7 +40,8 @@ def _requests(rng, first_id, n, nseg, hot, kmin, kmax, suffixes, sys, chunk, zip
             if c not in sk:
                 sk.append(c)
         sfx = int(rng.choice(suffixes))
-        reqs.append(Request(first_id + i, float(first_id + i) * 0.01, sk, True, [], sys, k * chunk, sfx))
+        reqs.append(Request(first_id + i, float(first_id + i) * 0.01, sk, bool(rng.random() < reo), [], sys, k * chunk,
+                            sfx))
     return reqs
 
 
@@ -49,12 +50,13 @@ def _pending_arrays(reqs):
     off = np.zeros(P + 1, np.int64)
     np.cumsum([len(r.skeleton) for r in reqs], out=off[1:])
     return (np.array([r.id for r in reqs], np.int64), np.array([r.arrival_time for r in reqs], np.float64), off,
-            np.array([s for r in reqs for s in r.skeleton], np.int32), np.ones(P, np.uint8),
+            np.array([s for r in reqs for s in r.skeleton], np.int32),
+            np.array([1 if r.reorderable else 0 for r in reqs], np.uint8),
             np.array([r.suffix_len for r in reqs], np.int32))
 
 
 def run_case(seed, policy, mode, nseg=40, hot=6, kmin=2, kmax=5, suffixes=(2, 4), sys=8, chunk=4, cap=600,
-             wave=24, nwaves=8, protect=3, cold=2, tiny=False, coop=1, sample=1):
+             wave=24, nwaves=8, protect=3, cold=2, tiny=False, coop=1, sample=1, reo=1.0):
     import torch
 
     from paper_2605_08581_b200.wave import DevicePending, WaveEngine
@@ -74,7 +76,8 @@ def run_case(seed, policy, mode, nseg=40, hot=6, kmin=2, kmax=5, suffixes=(2, 4)
     ora_prev = []
     next_id = 0
     for w in range(nwaves):
-        reqs = _requests(rng, next_id, wave + int(rng.integers(0, 6)), nseg, hot, kmin, kmax, suffixes, sys, chunk)
+        reqs = _requests(rng, next_id, wave + int(rng.integers(0, 6)), nseg, hot, kmin, kmax, suffixes, sys, chunk,
+                         reo=reo)
         next_id += len(reqs)
         pend = DevicePending.from_host(*_pending_arrays(reqs), torch.device("cuda", 0))
         eng.release(eng.leaf_slots, dev_prev)
@@ -141,6 +144,11 @@ def test_ordered_commit_matches_oracle(policy):
     dict(coop=0, tiny=True),
     dict(sample=0),                                    # materialising radix selection only
     dict(sample=0, tiny=True),
+    dict(reo=0.0),                                     # non-reorderable skeletons (no front-alignment)
+    dict(reo=0.5, kmin=1, kmax=6),                     # mixed
+    dict(nseg=300, hot=8, kmin=20, kmax=40, suffixes=(0, 8), wave=16, nwaves=6, cap=6000),  # agent-like deep paths
+    dict(nseg=300, hot=8, kmin=20, kmax=40, suffixes=(8,), wave=24, nwaves=8, cap=900, reo=0.0),  # ... evicting
+    dict(cap=260, wave=48, nwaves=12, protect=8),      # eviction stress: most of the tree turns over per wave
 ])
 def test_parallel_commit_variants(variant):
     run_case(5, CachePolicy.DART, mode=0, **variant)
