@@ -523,70 +523,63 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   }
   qs_gsync();
   QS_TS(2);
-  // 2. front alignment + order-sensitive signature (109-143), bucket insert
-  for (int64_t i0 = 0; i0 < P; i0 += gs) {
-    const int64_t i = i0 + qs_ilv(gs);
-    if (i >= P) continue;
-    const int64_t b = A.off[i];
-    const int k = (int)(A.off[i + 1] - b);
-    if (k > QS_MAXK) {  // aligned below by a whole block
-      A.longl[atomicAdd((unsigned long long *)&A.counts[4], 1ull)] = (int32_t)i;
-      continue;
-    }
-    int32_t s[QS_MAXK], al[QS_MAXK];
-    double p[QS_MAXK], pa[QS_MAXK];  // priorities by skeleton / by aligned position
-    int ord[QS_MAXK];
-    for (int j = 0; j < k; j++) {
-      s[j] = A.sk[b + j];
-      p[j] = qpri0(c, A.g, A.a, s[j]);
-    }
-    if (!A.reo[i] || k == 0) {
-      for (int j = 0; j < k; j++) {
-        al[j] = s[j];
-        pa[j] = p[j];
-      }
-    } else {
-      for (int j = 0; j < k; j++) {
-        int q = j;
-        while (q > 0 && qrank_before(p[j], s[j], j, p[ord[q - 1]], s[ord[q - 1]], ord[q - 1])) {
-          ord[q] = ord[q - 1];
-          q--;
-        }
-        ord[q] = j;
+  // 2. front alignment + order-sensitive signature (109-143), bucket insert:
+  // 16 lanes per request, lane q holding skeleton entry q in registers; ranks
+  // by shuffles over the group (no per-thread arrays, no local memory)
+  {
+    const int gl = tid & 15, gb = tid & 16;  // lane in the group, the group's first lane in the warp
+    const int64_t ng = gs >> 4;
+    for (int64_t g0 = 0; g0 < P; g0 += ng) {
+      const int64_t i = g0 + (gt >> 4);
+      const bool vi = i < P;
+      const int64_t b = vi ? A.off[i] : 0;
+      const int k = vi ? (int)(A.off[i + 1] - b) : 0;
+      const bool lng = k > QS_MAXK;
+      if (vi && lng && gl == 0) A.longl[atomicAdd((unsigned long long *)&A.counts[4], 1ull)] = (int32_t)i;
+      const bool on = vi && !lng && gl < k;
+      const int32_t sj = on ? A.sk[b + gl] : 0;
+      const double pj = on ? qpri0(c, A.g, A.a, sj) : 0.0;
+      const bool reo = vi && A.reo[i];
+      // 2a. rank by (-pri, seg, skeleton index); front_align: the top-f to the
+      // front in rank order, the rest stable
+      int r = 0;
+#pragma unroll
+      for (int q = 0; q < QS_MAXK; q++) {
+        const double pq = __shfl_sync(0xffffffffu, pj, q, 16);
+        const int32_t sq = __shfl_sync(0xffffffffu, sj, q, 16);
+        r += (q < k && qrank_before(pq, sq, q, pj, sj, gl)) ? 1 : 0;
       }
       const int f = (int)(c.front < k ? c.front : k);
-      uint32_t chosen = 0;
-      int w = 0;
-      for (int q = 0; q < f; q++) {
-        pa[w] = p[ord[q]];
-        al[w++] = s[ord[q]];
-        chosen |= 1u << ord[q];
-      }
-      for (int j = 0; j < k; j++)
-        if (!((chosen >> j) & 1u)) {
-          pa[w] = p[j];
-          al[w++] = s[j];
-        }
-    }
-    for (int j = 0; j < k; j++) A.aligned[b + j] = al[j];
-    int sl = 0;
-    if (k > 0) {
-      for (int j = 0; j < k; j++) {  // ranks over the aligned order (priorities carried along)
-        int q = j;
-        while (q > 0 && qrank_before(pa[j], al[j], j, pa[ord[q - 1]], al[ord[q - 1]], ord[q - 1])) {
-          ord[q] = ord[q - 1];
-          q--;
-        }
-        ord[q] = j;
-      }
+      const bool fronted = reo && r < f;
+      const unsigned rest = (__ballot_sync(0xffffffffu, on && !fronted) >> gb) & 0xFFFFu;
+      const int pos = !reo ? gl : (fronted ? r : f + __popc(rest & ((1u << gl) - 1u)));
+      if (on) A.aligned[b + pos] = sj;
+      // 2b. signature: the top-kappa by (-pri, seg, aligned position), emitted in aligned order
       const int kk = (int)(c.kappa < k ? c.kappa : k);
-      uint32_t chosen = 0;
-      for (int q = 0; q < kk; q++) chosen |= 1u << ord[q];
-      for (int j = 0; j < k; j++)
-        if ((chosen >> j) & 1u) A.sig[i * c.kappa + sl++] = al[j];
+      int r2 = 0;
+#pragma unroll
+      for (int q = 0; q < QS_MAXK; q++) {
+        const double pq = __shfl_sync(0xffffffffu, pj, q, 16);
+        const int32_t sq = __shfl_sync(0xffffffffu, sj, q, 16);
+        const int posq = __shfl_sync(0xffffffffu, pos, q, 16);
+        r2 += (q < k && qrank_before(pq, sq, posq, pj, sj, pos)) ? 1 : 0;
+      }
+      const bool chosen = on && r2 < kk;
+      int before = 0;  // chosen entries ahead of mine in aligned order
+#pragma unroll
+      for (int q = 0; q < QS_MAXK; q++) {
+        const int posq = __shfl_sync(0xffffffffu, pos, q, 16);
+        const bool cq = __shfl_sync(0xffffffffu, chosen, q, 16);
+        before += (cq && posq < pos) ? 1 : 0;
+      }
+      if (chosen) A.sig[i * c.kappa + before] = sj;
+      __syncwarp();
+      if (vi && !lng && gl == 0) {
+        const int sl = k > 0 ? kk : 0;
+        A.siglen[i] = sl;
+        qs_bucket_insert(A, c, i, sl);  // 3.
+      }
     }
-    A.siglen[i] = sl;
-    qs_bucket_insert(A, c, i, sl);  // 3.
   }
   qs_gsync();
   const int64_t nlong = (int64_t)__ldcg((const unsigned long long *)&A.counts[4]);
