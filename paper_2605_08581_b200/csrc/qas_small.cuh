@@ -326,16 +326,12 @@ __device__ inline void qs_cold_lane(const QsArgs &A, const QsCfg &c, int64_t P, 
   __shared__ int32_t hist[256];
   __shared__ int32_t s_need, s_digit, s_done;
   const int tid = threadIdx.x, nt = blockDim.x;
-  for (int64_t i = tid; i < P; i += nt) tmp[i] = qs_ld(&A.bidx[i]) ? 0 : 1;  // bidx: hot flag
-  __syncthreads();
-  int32_t *lf = tmp + QS_MAXP;  // (sbk, free here) leftover flags kept for the fill
-  for (int64_t i = tid; i < P; i += nt) lf[i] = tmp[i];
-  const int m = block_exscan(tmp, (int)P, swarp);
-  for (int64_t i = tid; i < P; i += nt) {
-    if (lf[i]) {
-      sk[tmp[i]] = {qord(A.arrival[i]), (uint64_t)A.ids[i] ^ 0x8000000000000000ull};
-      sv[tmp[i]] = (int32_t)i;
-    }
+  // the leftovers, listed by the hot-lane phase (any order: the keys are distinct)
+  const int m = (int)__ldcg((const unsigned long long *)&A.counts[6]);
+  for (int q = tid; q < m; q += nt) {
+    const int32_t i = qs_ld(&A.longl[q]);
+    sk[q] = {qord(A.arrival[i]), (uint64_t)A.ids[i] ^ 0x8000000000000000ull};
+    sv[q] = i;
   }
   __syncthreads();
   int n = m;
@@ -412,10 +408,14 @@ __device__ inline void qs_cold_lane(const QsArgs &A, const QsCfg &c, int64_t P, 
   }
   block_bitonic(sk, sv, n);
   for (int q = tid; q < nc; q += nt) A.cold[q] = sv[q];
-  // n_disp of the cold members (247-248)
-  for (int q = tid; q < nc; q += nt) {
-    const int64_t i = sv[q];
-    qs_distinct(A.sk, A.off[i], A.off[i + 1], [&](int32_t s) { atomicAdd(&A.nd[s], 1); });
+  // n_disp of the cold members (247-248): one thread per (member, skeleton entry)
+  for (int64_t t = tid; t < nc * QS_MAXK; t += nt) {
+    const int64_t i = sv[t / QS_MAXK];
+    const int64_t b = A.off[i], e = A.off[i + 1];
+    for (int64_t x = b + t % QS_MAXK; x < e; x += QS_MAXK) {
+      int32_t s = 0;
+      if (qs_first(A.sk, b, x, s)) atomicAdd(&A.nd[s], 1);
+    }
   }
 }
 
@@ -775,6 +775,7 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
     const bool h = A.rank[i] < qs_ld(&A.nsegs[b]);
     A.bidx[i] = h ? 1 : 0;  // reuse: hot flag
     if (h) A.hot[(int64_t)__ldcg((const unsigned long long *)&A.isum[b]) + A.rank[i]] = i;
+    else A.longl[atomicAdd((unsigned long long *)&A.counts[6], 1ull)] = (int32_t)i;  // leftover (cold lane)
   }
   for (int64_t e = gt; e < nsk; e += gs) {  // n_disp of the hot members: one thread per skeleton entry
     const int64_t i = A.emap[e];
