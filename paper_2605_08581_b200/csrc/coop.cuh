@@ -613,7 +613,7 @@ __device__ inline void block_sort_small(const Key3 *k, const uint64_t *v, int n,
 // other chunk; written to (ko, vo), which may alias (k, v).  O(n * MS_CH)
 // compares instead of the O(n^2) of a plain rank sort, two barriers instead of
 // the O(log^2 n) of a bitonic network.
-constexpr int MS_CH = 128;
+constexpr int MS_CH = 64;
 __device__ inline void block_merge_sort(const Key3 *k, const uint64_t *v, int n, Key3 *tk, uint64_t *tv, Key3 *ko,
                                         uint64_t *vo) {
   const int nch = (n + MS_CH - 1) / MS_CH;

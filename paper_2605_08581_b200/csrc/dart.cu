@@ -373,7 +373,7 @@ int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const 
   k_ss_select<Cand><<<1, SS_SEL_TPB, SS_SEL_SMEM, st>>>(cand, B, W, dW);
   k_ss_filter<Cand><<<4 * sms, SS_TPB, SS_FILTER_SMEM, st>>>(cand, B);
   k_ss_scatter<<<2 * sms, SS_TPB, 0, st>>>(B, W, dW);
-  k_ss_sort<<<sms, SS_TPB, SS_SORT_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
+  k_ss_sort<<<3 * sms, SS_TPB, SS_SORT_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
   CK(cudaGetLastError());
   return PRISM_OK;
 }
