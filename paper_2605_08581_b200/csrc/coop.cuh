@@ -48,6 +48,7 @@ struct CoopState {
   unsigned int ss_cur[SS_SPL];  // per-bucket scatter cursors
   unsigned int ss_off[SS_SPL + 4];  // bucket offsets
   int ss_ok;                    // the sample select produced the sorted prefix
+  unsigned long long tf_n;      // top-f protection: candidates with a positive P-hat
   unsigned long long ss_dbg[24];
   unsigned long long ss_prof[8];  // diagnostics: k_ss_sort clock64 sums (load, sort, buckets, items)  // diagnostics: [0] max bucket, [1] rounds, [2+3r..] (undecided, selected, shift)
   int ss_nb;                    // diagnostics: splitters of the last sample select
@@ -1346,8 +1347,108 @@ __global__ void __launch_bounds__(COOP_TPB) k_build_coop(DT T, CoopBufs B, int64
   }
 }
 
+// ------------------------------------------------------------ small top-f
+// set_protection for a small budget f (kvcache.py:364-383): the keys are
+// (-P-hat, seg, id), so when at least f reusable anchors carry a positive
+// P-hat -- the pending round's segments, a few thousand nodes -- the top f are
+// among those.  k_tf_scan visits every slot once (clearing the previous flags,
+// leaving the eviction keys when asked) and lists them; every slice of the
+// list keeps its f smallest (k_tf_local), one CTA merges those (k_tf_merge).
+// Otherwise ss_ok stays 0 and k_protect_coop runs the materialising selection.
+constexpr int TF_MAX = 64;     // budgets up to this use the small top-f path
+constexpr int TF_SLICE = 256;  // list items per slice of k_tf_local (shared-memory sort)
+constexpr size_t TF_SMEM = 2 * (sizeof(Key3) + 8) * TF_SLICE;
+constexpr int TF_MERGE_MAX = 3072;  // per-slice winners merged by one CTA
+constexpr size_t TF_MERGE_SMEM = 2 * (sizeof(Key3) + 8) * TF_MERGE_MAX;
+
+__global__ void __launch_bounds__(SS_TPB) k_tf_scan(ProtCand cand, CoopBufs B) {
+  __shared__ unsigned s_w[32];
+  __shared__ unsigned long long s_base;
+  const int32_t hw = cand.hw();
+  const int lane = threadIdx.x & 31;
+  const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long ccount = 0;
+  for (int64_t s0 = (int64_t)blockIdx.x * blockDim.x; s0 < hw; s0 += UNR * gsz) {
+    Key3 k[UNR];
+    uint64_t v[UNR];
+    bool pos[UNR];
+    unsigned nt = 0;
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+      const int64_t s = s0 + u * gsz + threadIdx.x;
+      int64_t w = 0;
+      const bool c = s < hw && cand((int32_t)s, k[u], v[u], w);
+      ccount += c ? 1 : 0;
+      pos[u] = c && pri_of(cand.T, cand.T.seg[(int32_t)s]) > 0.0;
+      nt += pos[u] ? 1 : 0;
+    }
+    unsigned long long p = block_reserve(nt, &B.st->tf_n, s_w, &s_base);
+#pragma unroll
+    for (int u = 0; u < UNR; u++)
+      if (pos[u]) {
+        B.k1[p] = k[u];
+        B.v1[p] = v[u];
+        p++;
+      }
+  }
+  for (int o = 16; o > 0; o >>= 1) ccount += __shfl_xor_sync(0xffffffffu, ccount, o);
+  if (lane == 0 && ccount) atomicAdd(&B.st->ss_cand, ccount);
+}
+
+// every CTA: the f smallest keys of its TF_SLICE-item slices of the list -> B.ks/vs[slice * f ..]
+__global__ void __launch_bounds__(SS_TPB) k_tf_local(CoopBufs B, int64_t f) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int64_t n = (int64_t)B.st->tf_n;
+  if (n < f) return;
+  Key3 *sk = reinterpret_cast<Key3 *>(dsm);
+  uint64_t *sv = reinterpret_cast<uint64_t *>(sk + TF_SLICE);
+  Key3 *tk = reinterpret_cast<Key3 *>(sv + TF_SLICE);
+  uint64_t *tv = reinterpret_cast<uint64_t *>(tk + TF_SLICE);
+  for (int64_t c = blockIdx.x; c * TF_SLICE < n; c += gridDim.x) {
+    const int64_t b0 = c * TF_SLICE;
+    const int m = (int)(n - b0 < TF_SLICE ? n - b0 : TF_SLICE);
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      sk[i] = B.k1[b0 + i];
+      sv[i] = B.v1[b0 + i];
+    }
+    __syncthreads();
+    block_merge_sort(sk, sv, m, tk, tv, sk, sv);
+    const int keep = (int)(f < m ? f : m);
+    for (int i = threadIdx.x; i < f; i += blockDim.x) {
+      B.ks[c * f + i] = i < keep ? sk[i] : Key3{~0ull, ~0ull, ~0ull};
+      B.vs[c * f + i] = i < keep ? sv[i] : 0ull;
+    }
+    __syncthreads();
+  }
+}
+
+// one CTA: the f smallest of the per-slice winners -> T.Lk/Lv[0..f), ss_ok
+__global__ void __launch_bounds__(SS_SEL_TPB) k_tf_merge(DT T, CoopBufs B, int64_t f) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int64_t n = (int64_t)B.st->tf_n;
+  if (n < f || f <= 0) return;  // ss_ok stays 0: the materialising path decides
+  const int64_t nsl = (n + TF_SLICE - 1) / TF_SLICE;
+  const int64_t m = nsl * f;
+  if (m > TF_MERGE_MAX) return;  // too many winners for one CTA: the materialising path
+  Key3 *sk = reinterpret_cast<Key3 *>(dsm);
+  uint64_t *sv = reinterpret_cast<uint64_t *>(sk + TF_MERGE_MAX);
+  Key3 *tk = reinterpret_cast<Key3 *>(sv + TF_MERGE_MAX);
+  uint64_t *tv = reinterpret_cast<uint64_t *>(tk + TF_MERGE_MAX);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    sk[i] = B.ks[i];
+    sv[i] = B.vs[i];
+  }
+  __syncthreads();
+  block_merge_sort(sk, sv, (int)m, tk, tv, sk, sv);
+  for (int i = threadIdx.x; i < f; i += blockDim.x) {
+    T.Lk[i] = sk[i];
+    T.Lv[i] = sv[i];
+  }
+  if (threadIdx.x == 0) B.st->ss_ok = 1;
+}
+
 // set_protection (kvcache.py:364-383): top-f reusable anchors by (-P-hat, seg
-// or -1, id) -- from the sample select when it succeeded, else materialised
+// or -1, id) -- from the small top-f / sample select when it succeeded, else materialised
 __global__ void __launch_bounds__(COOP_TPB) k_protect_coop(DT T, CoopBufs B, int64_t f, int64_t min_cand,
                                                            int64_t small, int32_t sampled, int32_t keys) {
   extern __shared__ __align__(16) unsigned char dsm[];

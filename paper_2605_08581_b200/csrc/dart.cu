@@ -1008,7 +1008,20 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out, int3
     int64_t minc = t->sel_min_candidates, small = std::min<int64_t>(SEL_SMALL, t->sel_min_candidates);
     int64_t ff = f;
     int32_t sampled = (t->use_sample && f > 0) ? 1 : 0;
-    if (sampled) {
+    if (sampled && f <= TF_MAX) {  // small budget: the positive-P-hat list and its top f
+      int sms = 0;
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev));
+      static bool tf_attr = false;
+      if (!tf_attr) {
+        CK(cudaFuncSetAttribute(k_tf_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TF_MERGE_SMEM));
+        tf_attr = true;
+      }
+      k_tf_scan<<<4 * sms, SS_TPB, 0, t->st>>>(ProtCand{t->d, keys}, B);
+      k_tf_local<<<2 * sms, SS_TPB, TF_SMEM, t->st>>>(B, ff);
+      k_tf_merge<<<1, SS_SEL_TPB, TF_MERGE_SMEM, t->st>>>(t->d, B, ff);
+      CK(cudaGetLastError());
+      t->launches[PH_PROTECT] += 3;
+    } else if (sampled) {
       rc = sample_select(t, ProtCand{t->d, keys}, B, ff, nullptr, minc);
       if (rc) return rc;
       t->launches[PH_PROTECT] += 5;
