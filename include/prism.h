@@ -211,6 +211,23 @@ int prism_note_active_device(prism_tree *t, const int32_t *d_a, const int32_t *d
 int32_t prism_tree_policy(prism_tree *t);
 /* The cudaStream_t (as void*) the tree launches on (tree mutations, builds). */
 void *prism_tree_stream(prism_tree *t);
+/* 1 when the tree's part of the fused wave is capturable (cooperative build, no live profile). */
+int32_t prism_tree_graphable(prism_tree *t);
+/* The fused wave's commit split for CUDA-graph capture by prism_wave_step:
+ * prepare (allocations, never inside a capture) -> enqueue (pre-match + one
+ * device-driven parallel-commit attempt, ordered after and joined back into
+ * `stream`, no host wait; capturable) -> finish (after `stream` completed:
+ * *applied = 1 when the attempt committed the wave; otherwise the caller
+ * re-runs prism_admit_wave_segmented).  key: fingerprint of everything a
+ * capture bakes in (device layout, scratch pointers, tunables). */
+int prism_wave_commit_prepare(prism_tree *t, int64_t B);
+int prism_wave_commit_enqueue(prism_tree *t, int64_t B, const int64_t *path_off, const uint32_t *tokens,
+                              const int64_t *anc_off, const int8_t *a_kind, const int32_t *a_seg,
+                              const int32_t *a_snap, const int64_t *members, const int64_t *sk_off,
+                              const int32_t *aligned, int64_t sys_len, int64_t chunk, int64_t *hits,
+                              int32_t *leaf_slots, int64_t *leaf_ids, void *stream);
+int prism_wave_commit_finish(prism_tree *t, int64_t B, int32_t *applied);
+uint64_t prism_wave_commit_key(prism_tree *t);
 /* The cudaStream_t (as void*) the QAS instance launches on; prism_wave_step
  * completes on it, so events recorded there bracket a whole wave. */
 void *prism_qas_stream(prism_qas *q);
@@ -225,6 +242,9 @@ int prism_qas_set_small(prism_qas *q, int32_t max_p);
  * 1 = CTAs of the cooperative grid (0: auto), 2 = pending requests per CTA
  * for the auto grid; key 3 writes the last round's CTA count to *out. */
 int prism_qas_tune(prism_qas *q, int32_t key, int64_t value, int64_t *out);
+/*   key 4: 1 (default) the fused wave's tail (protection, serialization,
+ *          pre-match, commit) replayed as a CUDA graph for repeated wave
+ *          shapes, 0 plain launches; key 5: out[0..1] = graph captures, replays */
 /* out[4]: own kernel launches, CUB primitive calls, rounds so far, and the
  * device microseconds of those rounds when profiling is on. */
 int prism_qas_counts(prism_qas *q, int64_t *out);

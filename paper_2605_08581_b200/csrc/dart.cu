@@ -67,6 +67,7 @@ struct prism_tree {
   // before anything reads the protected flags
   cudaStream_t st_aux = nullptr;
   cudaEvent_t ev_aux = nullptr, ev_main = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;  // caller stream <-> tree stream (graph-capturable)
   int aux_pending = 0;
   int keys_fresh = 0;  // the protection pass left the eviction keys (k_build_keys not needed)
   DT d{};
@@ -125,6 +126,7 @@ struct prism_tree {
   WaveTmp wx{};
   WaveCtl *wc = nullptr, *h_wc = nullptr;
   int64_t *ds_part = nullptr;
+  int sms = 0;
   int64_t wx_cap = 0, wx_lt = 0, wx_T = 0;
   int64_t par_waves = 0, seq_waves = 0;
   int32_t last_fallback = 0;
@@ -613,91 +615,129 @@ int cub_scan(prism_tree *t, In in, Out out, int64_t n, bool inclusive) {
 // *applied = 0 when an exactness guard tripped (nothing was mutated; the
 // caller runs the ordered commit k_commit).  Capacity maintenance and a
 // prefix that fell short are handled between attempts.
-int admit_wave_par(prism_tree *t, const WaveIn &W, int64_t levels, int64_t *hits, int32_t *leaf_slots,
-                   int64_t *leaf_ids, int *applied) {
-  *applied = 0;
-  const int64_t B = W.B;
-  cudaStream_t st = t->st;
+// buffers of the device-driven commit for a wave of B members
+int wave_par_prepare(prism_tree *t, int64_t B, int64_t levels) {
   if (!t->wc) {
     CK(dalloc(&t->wc, 1));
     CK(cudaMallocHost(&t->h_wc, sizeof(WaveCtl)));
     CK(dalloc(&t->ds_part, DS_BLOCKS));
   }
-  int32_t force_full = 0;
-  int sms = 0;
-  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev));
-  for (int attempt = 0; attempt < 8; attempt++) {
-    int rc = wx_ensure(t, B, levels, t->d.S);  // eviction-stream buffers for any prefix length
-    if (rc) return rc;
-    WaveTmp &X = t->wx;
-    WaveCtl *wc = t->wc;
-    prof_begin(t);
-    CK(cudaMemsetAsync(X.lt_key, 0xFF, sizeof(uint64_t) * (size_t)t->wx_lt, st));
-    CK(cudaMemsetAsync(X.lt_min, 0x7F, sizeof(int32_t) * (size_t)t->wx_lt, st));
-    CK(cudaMemsetAsync(X.flags, 0, sizeof(int32_t), st));
-    CK(cudaMemsetAsync(X.misc, 0, sizeof(int64_t) * 8, st));
-    CK(cudaMemsetAsync(X.misc + 1, 0x7F, sizeof(int64_t), st));  // poison index: "none"
-    k_wc_begin<<<1, 1, 0, st>>>(t->d, wc);
-    k_wp_plan<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
-    k_wp_levels<<<blocks_for(B * WP_PL), TPB, 0, st>>>(W, X);
-    k_wp_hits<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X);
-    k_wp_scan3<<<1, 1024, 0, st>>>(B, X);
-    k_wc_plan<<<1, 1, 0, st>>>(t->d, B, X, wc, t->list_slack_tokens, force_full);
-    CK(cudaGetLastError());
-    t->launches[PH_COMMIT] += 6;
-    prof_end(t, PH_COMMIT);
-    const int64_t *dW = &wc->W;
-    if (t->use_coop) {
-      if ((rc = build_list(t, 0, dW))) return rc;
-    } else {  // the multi-kernel build sizes its passes on the host: one round trip for W
-      CK(cudaMemcpyAsync(t->h_wc, wc, sizeof(WaveCtl), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      if (!t->h_wc->stop && t->h_wc->W >= 0 && (rc = build_list(t, t->h_wc->W))) return rc;
-    }
-    prof_begin(t);
-    k_wp_vlen<<<2 * sms, TPB, 0, st>>>(t->d, X, wc);
-    const int64_t *dn = &t->d.ctrl->L_n;
-    k_dscan_a<<<DS_BLOCKS, 256, 0, st>>>(X.vlen, dn, t->ds_part, wc);
-    k_dscan_b<<<1, 1024, 0, st>>>(t->ds_part, DS_BLOCKS, wc);
-    k_dscan_c<<<DS_BLOCKS, 256, 0, st>>>(X.vlen, dn, t->ds_part, X.F, wc);
-    k_wp_cuts<<<blocks_for(B), TPB, 0, st>>>(t->d, B, X, wc);
-    k_wc_cut<<<1, 1024, 0, st>>>(t->d, B, X, wc);
-    k_wp_evict<<<2 * sms, TPB, 0, st>>>(t->d, wc);
-    k_wp_alloc<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
-    k_wp_label_reset<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
-    k_wp_create<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, W, X, wc);
-    k_wp_touch<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
-    k_wp_label<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc, hits, leaf_slots, leaf_ids);
-    k_wc_finalize<<<1, 1, 0, st>>>(t->d, B, X, wc);
-    CK(cudaGetLastError());
-    t->launches[PH_COMMIT] += 14;
+  if (!t->sms) CK(cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, t->dev));
+  return wx_ensure(t, B, levels, t->d.S);  // eviction-stream buffers for any prefix length
+}
+
+// one attempt of the device-driven commit, enqueued on the tree stream with
+// no host wait (cooperative build path); ends by copying the verdict and the
+// control block to pinned host memory.  Capturable in a CUDA graph.
+int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *leaf_slots, int64_t *leaf_ids,
+                     int32_t force_full) {
+  const int64_t B = W.B;
+  cudaStream_t st = t->st;
+  const int sms = t->sms;
+  WaveTmp &X = t->wx;
+  WaveCtl *wc = t->wc;
+  int rc;
+  prof_begin(t);
+  CK(cudaMemsetAsync(X.lt_key, 0xFF, sizeof(uint64_t) * (size_t)t->wx_lt, st));
+  CK(cudaMemsetAsync(X.lt_min, 0x7F, sizeof(int32_t) * (size_t)t->wx_lt, st));
+  CK(cudaMemsetAsync(X.flags, 0, sizeof(int32_t), st));
+  CK(cudaMemsetAsync(X.misc, 0, sizeof(int64_t) * 8, st));
+  CK(cudaMemsetAsync(X.misc + 1, 0x7F, sizeof(int64_t), st));  // poison index: "none"
+  k_wc_begin<<<1, 1, 0, st>>>(t->d, wc);
+  k_wp_plan<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
+  k_wp_levels<<<blocks_for(B * WP_PL), TPB, 0, st>>>(W, X);
+  k_wp_hits<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X);
+  k_wp_scan3<<<1, 1024, 0, st>>>(B, X);
+  k_wc_plan<<<1, 1, 0, st>>>(t->d, B, X, wc, t->list_slack_tokens, force_full);
+  CK(cudaGetLastError());
+  t->launches[PH_COMMIT] += 6;
+  prof_end(t, PH_COMMIT);
+  const int64_t *dW = &wc->W;
+  if (t->use_coop) {
+    if ((rc = build_list(t, 0, dW))) return rc;
+  } else {  // the multi-kernel build sizes its passes on the host: one round trip for W
     CK(cudaMemcpyAsync(t->h_wc, wc, sizeof(WaveCtl), cudaMemcpyDeviceToHost, st));
-    if ((rc = pull_ctrl(t))) return rc;  // the wave's one host round trip
-    prof_end(t, PH_COMMIT);
-    const WaveCtl &H = *t->h_wc;
-    switch (H.stop) {
-      case WC_OK:
-        t->last_fallback = 0;
-        *applied = 1;
-        return PRISM_OK;
-      case WC_FALLBACK:
-        t->last_fallback = H.flags;
-        return PRISM_OK;
-      case WC_FULL:  // the selected prefix fell short: select the whole order
-        force_full = 1;
-        break;
-      case WC_MAINT: {  // semantics-free capacity maintenance, then the same wave again
-        Ctrl &C = *t->hctrl;
-        if ((int64_t)C.hw + H.ncreate + 2 > t->d.S && (rc = grow_slots(t, (int64_t)C.hw + H.ncreate + 2))) return rc;
-        if (C.arena_top + H.ntail > t->d.acap && (rc = compact_arena(t, H.ntail))) return rc;
-        if ((C.hlive + C.htomb + H.ncreate + 64) * 2 > (int64_t)(t->d.hmask + 1) && (rc = rehash(t, H.ncreate + 64)))
-          return rc;
-        if ((rc = pull_ctrl(t))) return rc;
-        break;
-      }
-      default:
-        return fail(PRISM_FATAL, "unexpected wave control stop " + std::to_string(H.stop));
+    CK(cudaStreamSynchronize(st));
+    if (!t->h_wc->stop && t->h_wc->W >= 0 && (rc = build_list(t, t->h_wc->W))) return rc;
+  }
+  prof_begin(t);
+  k_wp_vlen<<<2 * sms, TPB, 0, st>>>(t->d, X, wc);
+  const int64_t *dn = &t->d.ctrl->L_n;
+  k_dscan_a<<<DS_BLOCKS, 256, 0, st>>>(X.vlen, dn, t->ds_part, wc);
+  k_dscan_b<<<1, 1024, 0, st>>>(t->ds_part, DS_BLOCKS, wc);
+  k_dscan_c<<<DS_BLOCKS, 256, 0, st>>>(X.vlen, dn, t->ds_part, X.F, wc);
+  k_wp_cuts<<<blocks_for(B), TPB, 0, st>>>(t->d, B, X, wc);
+  k_wc_cut<<<1, 1024, 0, st>>>(t->d, B, X, wc);
+  k_wp_evict<<<2 * sms, TPB, 0, st>>>(t->d, wc);
+  k_wp_alloc<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
+  k_wp_label_reset<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
+  k_wp_create<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, W, X, wc);
+  k_wp_touch<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
+  k_wp_label<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc, hits, leaf_slots, leaf_ids);
+  k_wc_finalize<<<1, 1, 0, st>>>(t->d, B, X, wc);
+  CK(cudaGetLastError());
+  t->launches[PH_COMMIT] += 14;
+  CK(cudaMemcpyAsync(t->h_wc, wc, sizeof(WaveCtl), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(t->hctrl, t->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  return PRISM_OK;
+}
+
+// the verdict of a completed attempt (h_wc / hctrl current): *applied = 1
+// committed; *again = 1 retry (maintenance done / whole order needed,
+// *force_full set); neither: an exactness guard tripped (ordered commit)
+int wave_par_verdict(prism_tree *t, int *applied, int *again, int32_t *force_full) {
+  *applied = *again = 0;
+  const WaveCtl &H = *t->h_wc;
+  int rc;
+  switch (H.stop) {
+    case WC_OK:
+      t->last_fallback = 0;
+      *applied = 1;
+      return PRISM_OK;
+    case WC_FALLBACK:
+      t->last_fallback = H.flags;
+      return PRISM_OK;
+    case WC_FULL:  // the selected prefix fell short: select the whole order
+      *force_full = 1;
+      *again = 1;
+      return PRISM_OK;
+    case WC_MAINT: {  // semantics-free capacity maintenance, then the same wave again
+      Ctrl &C = *t->hctrl;
+      if ((int64_t)C.hw + H.ncreate + 2 > t->d.S && (rc = grow_slots(t, (int64_t)C.hw + H.ncreate + 2))) return rc;
+      if (C.arena_top + H.ntail > t->d.acap && (rc = compact_arena(t, H.ntail))) return rc;
+      if ((C.hlive + C.htomb + H.ncreate + 64) * 2 > (int64_t)(t->d.hmask + 1) && (rc = rehash(t, H.ncreate + 64)))
+        return rc;
+      if ((rc = pull_ctrl(t))) return rc;
+      *again = 1;
+      return PRISM_OK;
     }
+    default:
+      return fail(PRISM_FATAL, "unexpected wave control stop " + std::to_string(H.stop));
+  }
+}
+
+// Parallel commit of a segment-structured wave (wave_par.cuh), driven on the
+// device: plan -> scans -> plan verdict (k_wc_plan: fallback flags, capacity
+// headroom, eviction demand) -> the eviction-order prefix it needs (read on
+// the device) -> victim cuts + verdict (k_wc_cut) -> apply -> control block
+// (k_wc_finalize), one stream of launches with a single host round trip at
+// the end.  Returns PRISM_OK with *applied = 1 when the wave was committed,
+// *applied = 0 when an exactness guard tripped (nothing was mutated; the
+// caller runs the ordered commit k_commit).  Capacity maintenance and a
+// prefix that fell short are handled between attempts.
+int admit_wave_par(prism_tree *t, const WaveIn &W, int64_t levels, int64_t *hits, int32_t *leaf_slots,
+                   int64_t *leaf_ids, int *applied) {
+  *applied = 0;
+  int32_t force_full = 0;
+  for (int attempt = 0; attempt < 8; attempt++) {
+    int rc = wave_par_prepare(t, W.B, levels);
+    if (rc) return rc;
+    if ((rc = wave_par_enqueue(t, W, hits, leaf_slots, leaf_ids, force_full))) return rc;
+    CK(cudaStreamSynchronize(t->st));  // the wave's one host round trip
+    prof_end(t, PH_COMMIT);
+    int again = 0;
+    if ((rc = wave_par_verdict(t, applied, &again, &force_full))) return rc;
+    if (!again) return PRISM_OK;
   }
   return fail(PRISM_FATAL, "parallel wave commit did not converge");
 }
@@ -804,7 +844,9 @@ prism_tree *prism_tree_create(int64_t capacity_tokens, int32_t policy, int64_t p
   if (cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking) != cudaSuccess) return bad("stream");
   if (cudaStreamCreateWithFlags(&t->st_aux, cudaStreamNonBlocking) != cudaSuccess) return bad("stream");
   if (cudaEventCreateWithFlags(&t->ev_aux, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&t->ev_main, cudaEventDisableTiming) != cudaSuccess)
+      cudaEventCreateWithFlags(&t->ev_main, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&t->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&t->ev_out, cudaEventDisableTiming) != cudaSuccess)
     return bad("events");
   int64_t S = std::max<int64_t>(initial_slots > 0 ? initial_slots : 4096, 64);
   S = std::min<int64_t>(next_pow2(S), 1ll << 30);
@@ -875,6 +917,8 @@ void prism_tree_destroy(prism_tree *t) {
   cudaStreamDestroy(t->st_aux);
   cudaEventDestroy(t->ev_aux);
   cudaEventDestroy(t->ev_main);
+  cudaEventDestroy(t->ev_in);
+  cudaEventDestroy(t->ev_out);
   cudaStreamDestroy(t->st);
   delete t;
 }
@@ -1161,6 +1205,10 @@ int prism_note_active_device(prism_tree *t, const int32_t *d_a, const int32_t *d
 
 void *prism_tree_stream(prism_tree *t) { return (void *)t->st; }
 
+// the tree's part of the fused wave can be captured in a CUDA graph: the
+// cooperative (host-sync-free) build and no live profile
+int32_t prism_tree_graphable(prism_tree *t) { return (t->use_coop && !t->prof_on) ? 1 : 0; }
+
 int32_t prism_tree_policy(prism_tree *t) { return t->d.policy; }
 
 int prism_note_active(prism_tree *t, int64_t n, const int32_t *segs) {
@@ -1303,6 +1351,76 @@ int prism_admit_wave_segmented(prism_tree *t, int64_t B, const int64_t *path_off
   t->seq_waves++;
   return prism_admit_wave_device(t, B, path_off, tokens, anc_off, a_off, a_kind, a_seg, a_snap, hits, leaf_slots,
                                  leaf_ids, n_admitted_host, stream);
+}
+
+// ---- the fused wave's commit split for CUDA-graph capture (prism_wave_step):
+// prepare (allocations, outside any capture) -> enqueue (pre-match + one
+// device-driven attempt, ordered after and joined back into `stream`, no host
+// wait) -> finish (after the stream completed: the verdict; a wave that did
+// not commit is re-run by the regular path, which also covers maintenance).
+int prism_wave_commit_prepare(prism_tree *t, int64_t B) {
+  cudaSetDevice(t->dev);
+  if (B > t->pm_cap || !t->d_pm_meta) {
+    if (t->d_pm_meta) {
+      CK(cudaFree(t->d_pm_meta));
+      CK(cudaFree(t->d_pm_chain));
+    }
+    t->pm_cap = std::max<int64_t>(next_pow2(B), 64);
+    CK(dalloc(&t->d_pm_meta, 4 * t->pm_cap));
+    CK(dalloc(&t->d_pm_chain, PM_MAX * t->pm_cap));
+  }
+  return wave_par_prepare(t, B, B * WP_MAXP);
+}
+
+int prism_wave_commit_enqueue(prism_tree *t, int64_t B, const int64_t *path_off, const uint32_t *tokens,
+                              const int64_t *anc_off, const int8_t *a_kind, const int32_t *a_seg,
+                              const int32_t *a_snap, const int64_t *members, const int64_t *sk_off,
+                              const int32_t *aligned, int64_t sys_len, int64_t chunk, int64_t *hits,
+                              int32_t *leaf_slots, int64_t *leaf_ids, void *stream) {
+  CK(cudaEventRecord(t->ev_in, (cudaStream_t)stream));
+  CK(cudaStreamWaitEvent(t->st, t->ev_in, 0));
+  k_prematch<<<blocks_for(B * 32), TPB, 0, t->st>>>(t->d, B, path_off, tokens, t->d_pm_meta, t->d_pm_chain);
+  t->launches[PH_PREMATCH]++;
+  WaveIn W{B, sys_len, chunk, path_off, tokens, anc_off, a_kind, a_seg, a_snap, members, sk_off, aligned,
+           t->d_pm_meta, t->d_pm_chain};
+  int rc = wave_par_enqueue(t, W, hits, leaf_slots, leaf_ids, 0);
+  if (rc) return rc;
+  CK(cudaEventRecord(t->ev_out, t->st));
+  CK(cudaStreamWaitEvent((cudaStream_t)stream, t->ev_out, 0));
+  return PRISM_OK;
+}
+
+// *applied = 1: the enqueued attempt committed the wave
+int prism_wave_commit_finish(prism_tree *t, int64_t B, int32_t *applied) {
+  int ap = 0, again = 0;
+  int32_t ff = 0;
+  int rc = wave_par_verdict(t, &ap, &again, &ff);
+  if (rc) return rc;
+  *applied = ap;
+  if (ap) t->par_waves++;
+  (void)B;
+  return PRISM_OK;
+}
+
+// fingerprint of everything a captured commit bakes in (device layout, scratch
+// pointers, tunables): a graph is reused only while it is unchanged
+uint64_t prism_wave_commit_key(prism_tree *t) {
+  auto mixin = [](uint64_t h, const void *p, size_t n) {
+    const unsigned char *c = (const unsigned char *)p;
+    for (size_t i = 0; i < n; i++) h = (h ^ c[i]) * 0x100000001B3ull;
+    return h;
+  };
+  uint64_t h = 0xCBF29CE484222325ull;
+  h = mixin(h, &t->d, sizeof(DT));
+  h = mixin(h, &t->wx, sizeof(WaveTmp));
+  const void *ptrs[] = {t->wc, t->ds_part, t->cst, t->d_pm_meta, t->d_pm_chain, t->ck, t->ck2, t->ks, t->kt,
+                        t->cv, t->cv2, t->vs, t->vt, t->cw, t->cw2, t->bmin, t->bmax, t->d_prot_ids,
+                        t->hctrl, t->h_wc, t->st, t->st_aux};
+  h = mixin(h, ptrs, sizeof(ptrs));
+  const int64_t knobs[] = {t->wx_lt, t->list_slack_tokens, t->sel_min_candidates, t->use_coop, t->use_sample,
+                           t->protect_budget, t->sms, t->prof_on};
+  h = mixin(h, knobs, sizeof(knobs));
+  return h;
 }
 
 // out[3]: waves committed in parallel, waves committed in order, last fallback reason flags

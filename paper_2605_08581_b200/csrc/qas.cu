@@ -460,6 +460,9 @@ struct prism_qas {
   X(int32_t, longl) \
   X(int32_t, rk) \
   X(int32_t, emap) \
+  X(int64_t, gids) \
+  X(int64_t, goff) \
+  X(int32_t, gsfx) \
   X(uint64_t, tkey) \
   X(int32_t, tmin) \
   X(int32_t, slot_of) \
@@ -552,6 +555,12 @@ struct prism_qas {
   int prof_on = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   double ms_round = 0.0;  // QAS round + serialization device time (events on q->st)
+  // the fused wave's tail as a CUDA graph (prism_wave_step)
+  cudaEvent_t ev_t = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  uint64_t gkey = 0, gkey_seen = 0;
+  int32_t use_graph = 1;
+  int64_t graph_captures = 0, graph_replays = 0, graph_kernels = 0;
 };
 
 namespace {
@@ -978,6 +987,8 @@ void prism_qas_destroy(prism_qas *q) {
 #undef QPTR
   for (void *p : bufs)
     if (p) cudaFree(p);
+  if (q->gexec) cudaGraphExecDestroy(q->gexec);
+  if (q->ev_t) cudaEventDestroy(q->ev_t);
   if (q->e0) cudaEventDestroy(q->e0);
   if (q->e1) cudaEventDestroy(q->e1);
   cudaStreamDestroy(q->st);
@@ -1282,25 +1293,105 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
     if (B == 0) return PRISM_OK;  // engine.py:190-191
     if ((int32_t)hb[4]) return qfail(PRISM_INVALID, "token layout overflows uint32");
     const int64_t ntok = hb[2], nanc = hb[3];
-    // protection / active hand-off (engine.py:193-197), ordered after the round
-    // on the tree's stream by an event (no host wait)
-    {
-      cudaEvent_t ev;
-      QCK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      QCK(cudaEventRecord(ev, st));
-      QCK(cudaStreamWaitEvent((cudaStream_t)prism_tree_stream(t), ev, 0));
-      QCK(cudaEventDestroy(ev));
-    }
-    const int32_t pol = prism_tree_policy(t);
-    if (pol == 0) rc = prism_set_protection_device_async(t, q->prio, nseg);  // overlaps the serialization
-    else if (pol == 2) rc = prism_note_active_device(t, q->a, q->nd, nseg);
-    if (rc) return rc;
-    // serialization (K1), then the admission on the tree's stream
     QCK(grow(&q->tok, q->tok_cap, std::max<int64_t>(ntok, 1)));
     QCK(grow(&q->a_off, q->a_off_cap, std::max<int64_t>(nanc, 1)));
     QCK(grow(&q->a_kind, q->a_kind_cap, std::max<int64_t>(nanc, 1)));
     QCK(grow(&q->a_seg, q->a_seg_cap, std::max<int64_t>(nanc, 1)));
     QCK(grow(&q->a_snap, q->a_snap_cap, 3 * std::max<int64_t>(nanc, 1)));
+    if (!q->ev_t) QCK(cudaEventCreateWithFlags(&q->ev_t, cudaEventDisableTiming));
+    const int32_t pol = prism_tree_policy(t);
+    // the rest of the wave is one stream of launches (protection on the tree's
+    // auxiliary stream, serialization here, pre-match + commit on the tree
+    // stream) with one host wait at the end; repeated waves of the same shape
+    // replay it as a CUDA graph
+    const bool graph = q->use_graph && !q->prof_on && pol == 0 && q->commit_mode == 0 && chunk > 0 &&
+                       prism_tree_graphable(t);
+    if (graph) {
+      if ((rc = prism_wave_commit_prepare(t, B))) return rc;
+      // the graph reads fixed copies of the caller's per-wave arrays
+      QCK(grow(&q->gids, q->gids_cap, Pc));
+      QCK(grow(&q->goff, q->goff_cap, Pc + 1));
+      QCK(grow(&q->gsfx, q->gsfx_cap, Pc));
+      QCK(cudaMemcpyAsync(q->gids, ids, sizeof(int64_t) * P, cudaMemcpyDeviceToDevice, st));
+      QCK(cudaMemcpyAsync(q->goff, sk_off, sizeof(int64_t) * (P + 1), cudaMemcpyDeviceToDevice, st));
+      QCK(cudaMemcpyAsync(q->gsfx, suffix, sizeof(int32_t) * P, cudaMemcpyDeviceToDevice, st));
+      auto tail = [&]() -> int {
+        int r;
+        QCK(cudaEventRecord(q->ev_t, st));
+        QCK(cudaStreamWaitEvent((cudaStream_t)prism_tree_stream(t), q->ev_t, 0));
+        if ((r = prism_set_protection_device_async(t, q->prio, nseg))) return r;  // overlaps serialization
+        q_serialize<<<nblk(B * 32), TPB, 0, st>>>(B, members, q->gids, q->goff, q->aligned, q->gsfx, sys_len, chunk,
+                                                  q->g, q->a, q->nd, q->poff, q->aoffs, q->tok, q->a_off, q->a_kind,
+                                                  q->a_seg, q->a_snap, q->err);
+        QCK(cudaGetLastError());
+        return prism_wave_commit_enqueue(t, B, q->poff, q->tok, q->aoffs, q->a_kind, q->a_seg, q->a_snap, members,
+                                         q->goff, q->aligned, sys_len, chunk, hits, leaf_slots, leaf_ids,
+                                         (void *)st);
+      };
+      uint64_t key = prism_wave_commit_key(t);
+      const void *ptrs[] = {members, hits, leaf_slots, leaf_ids, q->gids, q->goff, q->gsfx, q->aligned, q->g,
+                            q->a, q->nd, q->prio, q->poff, q->aoffs, q->tok, q->a_off, q->a_kind, q->a_seg,
+                            q->a_snap, q->err};
+      const int64_t dims[] = {B, sys_len, chunk, nseg};
+      for (const unsigned char *c = (const unsigned char *)ptrs; c < (const unsigned char *)(ptrs + 20); c++)
+        key = (key ^ *c) * 0x100000001B3ull;
+      for (const unsigned char *c = (const unsigned char *)dims; c < (const unsigned char *)(dims + 4); c++)
+        key = (key ^ *c) * 0x100000001B3ull;
+      if (q->gexec && key == q->gkey) {
+        QCK(cudaGraphLaunch(q->gexec, st));
+        q->graph_replays++;
+        q->launches += q->graph_kernels;
+      } else if (key == q->gkey_seen) {  // second wave of this shape: capture it
+        if (q->gexec) {
+          cudaGraphExecDestroy(q->gexec);
+          q->gexec = nullptr;
+        }
+        QCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+        const int r = tail();
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(st, &g);
+        if (r) return r;
+        if (ce != cudaSuccess || !g) return qfail(PRISM_CUDA, std::string("wave capture: ") + cudaGetErrorString(ce));
+        size_t nn = 0;  // kernel nodes: what one replay launches (launch accounting)
+        QCK(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        QCK(cudaGraphGetNodes(g, nodes.data(), &nn));
+        q->graph_kernels = 0;
+        for (auto nd : nodes) {
+          cudaGraphNodeType ty;
+          QCK(cudaGraphNodeGetType(nd, &ty));
+          q->graph_kernels += ty == cudaGraphNodeTypeKernel ? 1 : 0;
+        }
+        QCK(cudaGraphInstantiate(&q->gexec, g, 0));
+        cudaGraphDestroy(g);
+        q->gkey = key;
+        QCK(cudaGraphLaunch(q->gexec, st));
+        q->graph_captures++;
+      } else {  // first wave of this shape: plain launches
+        q->gkey_seen = key;
+        if ((rc = tail())) return rc;
+      }
+      QCK(cudaStreamSynchronize(st));
+      int32_t applied = 0;
+      if ((rc = prism_wave_commit_finish(t, B, &applied))) return rc;
+      if (applied) {
+        *n_admitted = B;
+        return PRISM_OK;
+      }
+      // not committed in parallel (maintenance / whole order / exactness guard):
+      // the regular path re-runs the commit on the already-serialized wave
+      return prism_admit_wave_segmented(t, B, q->poff, q->tok, q->aoffs, q->a_off, q->a_kind, q->a_seg, q->a_snap,
+                                        members, q->goff, q->aligned, sys_len, chunk, q->commit_mode, hits,
+                                        leaf_slots, leaf_ids, n_admitted, (void *)st);
+    }
+    // protection / active hand-off (engine.py:193-197), ordered after the round
+    // on the tree's stream by an event (no host wait)
+    QCK(cudaEventRecord(q->ev_t, st));
+    QCK(cudaStreamWaitEvent((cudaStream_t)prism_tree_stream(t), q->ev_t, 0));
+    if (pol == 0) rc = prism_set_protection_device_async(t, q->prio, nseg);  // overlaps the serialization
+    else if (pol == 2) rc = prism_note_active_device(t, q->a, q->nd, nseg);
+    if (rc) return rc;
+    // serialization (K1), then the admission on the tree's stream
     q_serialize<<<nblk(B * 32), TPB, 0, st>>>(B, members, ids, sk_off, q->aligned, suffix, sys_len, chunk, q->g,
                                               q->a, q->nd, q->poff, q->aoffs, q->tok, q->a_off, q->a_kind, q->a_seg,
                                               q->a_snap, q->err);
@@ -1338,6 +1429,15 @@ int prism_qas_tune(prism_qas *q, int32_t key, int64_t value, int64_t *out) {
       return PRISM_OK;
     case 3:
       if (out) *out = q->last_small_grid;
+      return PRISM_OK;
+    case 4:  // the fused wave's tail as a CUDA graph (1, default) or plain launches (0)
+      q->use_graph = value ? 1 : 0;
+      return PRISM_OK;
+    case 5:  // read-only: graph captures, graph replays
+      if (out) {
+        out[0] = q->graph_captures;
+        out[1] = q->graph_replays;
+      }
       return PRISM_OK;
     default:
       return qfail(PRISM_INVALID, "unknown QAS tunable");

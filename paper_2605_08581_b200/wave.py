@@ -145,6 +145,17 @@ class WaveEngine:
         """Last round's pending demand counters g (int32 [nseg]) into dst."""
         check(self.L.prism_qas_counters(self.q, dst.data_ptr(), self.nseg))
 
+    def set_graph(self, enable: bool) -> None:
+        """Replay the wave's tail (protection, serialization, commit) as a CUDA graph."""
+        self.L.prism_qas_tune.argtypes = [_p, C.c_int32, _i64, _p]
+        check(self.L.prism_qas_tune(self.q, 4, 1 if enable else 0, None))
+
+    def graph_stats(self) -> dict:
+        self.L.prism_qas_tune.argtypes = [_p, C.c_int32, _i64, _p]
+        out = np.zeros(2, dtype=np.int64)
+        check(self.L.prism_qas_tune(self.q, 5, 0, out.ctypes.data))
+        return {"captures": int(out[0]), "replays": int(out[1])}
+
     def set_commit_mode(self, mode: int) -> None:
         """0: exact parallel wave commit with ordered fallback; 1: ordered only."""
         check(self.L.prism_qas_set_commit_mode(self.q, mode))

@@ -197,3 +197,35 @@ def test_sampled_selection_at_scale(protect):
     assert o1 == o0
     assert v1 == v0
     assert d1 == d0
+
+
+def test_graph_replay_matches_plain_launches():
+    """The wave tail replayed as a CUDA graph (fixed wave shape: captured on the
+    second wave, replayed after) commits exactly what plain launches commit."""
+    import torch
+
+    from paper_2605_08581_b200.wave import DevicePending, WaveEngine
+
+    dev = torch.device("cuda", 0)
+    runs = []
+    for graph in (True, False):
+        rng = np.random.default_rng(9)
+        cfg = CacheConfig(capacity_tokens=400_000, policy=CachePolicy.DART, protect_budget=20)
+        eng = WaveEngine(cfg, SchedulerConfig(dispatch_budget=1024, cold_quota=16), 20 + 200_000, 12, 8, device=0)
+        eng.set_graph(graph)
+        nid, prev, out = 0, 0, []
+        for w in range(40):
+            pend = DevicePending.from_host(*_mu_pool(rng, nid, 1024), dev)
+            nid += 1024
+            eng.release(eng.leaf_slots, prev)
+            nm, prev = eng.step(pend)
+            out.append((eng.members[:nm].cpu().tolist(), eng.hits[:prev].cpu().tolist(),
+                        eng.leaf_ids[:prev].cpu().tolist()))
+        view = eng.cache_view()
+        runs.append((out, view.victim_log(), view.debug_nodes(), eng.graph_stats()))
+        eng.close()
+    (o1, v1, d1, g1), (o0, v0, d0, g0) = runs
+    assert g1["replays"] > 10 and g0["replays"] == 0, (g1, g0)
+    assert o1 == o0
+    assert v1 == v0
+    assert d1 == d0
