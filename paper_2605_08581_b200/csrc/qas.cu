@@ -533,7 +533,6 @@ struct prism_qas {
   X(prism::Key3, sbmax) \
   /* one-CTA rounds */ \
   X(int32_t, touched) \
-  X(int32_t, touched2) \
   X(int32_t, tn) \
   X(int64_t, qcounts) \
   X(int32_t, plist) \
@@ -596,8 +595,15 @@ int qas_rerun_multi(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t n
 }
 
 // the full round; outputs stay in q's device buffers
-int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, const QCfg &c, int64_t *nhot, int64_t *ncold,
-            int64_t *nbuckets) {
+bool qas_small_eligible(const prism_qas *q, int64_t P, const QCfg &c) {
+  const bool integral = c.wg == std::floor(c.wg) && c.wa == std::floor(c.wa) && c.wn == std::floor(c.wn) &&
+                        std::fabs(c.wg) < 1e9 && std::fabs(c.wa) < 1e9 && std::fabs(c.wn) < 1e9;
+  return P > 0 && P <= q->small_max_p && integral && c.kappa <= QMAXK;
+}
+
+// buffers (and the counter reset when they are fresh) of a one-launch round;
+// returns the grid (no kernel launched)
+int qas_small_prepare(prism_qas *q, int64_t P, int32_t nseg, const QCfg &c, int64_t *G_out) {
   cudaStream_t st = q->st;
   const int32_t S1 = std::max(nseg, 1);
   const int64_t gcap0 = q->g_cap;
@@ -606,130 +612,145 @@ int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, con
   QCK(grow(&q->nd, q->nd_cap, S1));
   QCK(grow(&q->prio, q->prio_cap, S1));
   QCK(grow(&q->dom, q->dom_cap, S1));
-  QCK(grow(&q->err, q->err_cap, 1));
+  QCK(grow(&q->err, q->err_cap, 4));
   QCK(grow(&q->small, q->small_cap, 8));
   if (q->g_cap != gcap0) q->full_reset = true;  // fresh (uninitialised) counter arrays
-  // ---- one-CTA round for small pending sets with integral weights (qas_small.cuh)
-  const bool integral = c.wg == std::floor(c.wg) && c.wa == std::floor(c.wa) && c.wn == std::floor(c.wn) &&
-                        std::fabs(c.wg) < 1e9 && std::fabs(c.wa) < 1e9 && std::fabs(c.wn) < 1e9;
-  if (P > 0 && P <= q->small_max_p && integral && c.kappa <= QMAXK) {
-    // touched-segment lists: a grown list loses the previous round's entries, so
-    // growing either one forces a full counter reset this round
-    const int64_t tneed = (int64_t)S1 + 1;  // distinct touched segments <= nseg
-    if (tneed > q->touched_cap || tneed > q->touched2_cap || !q->touched || !q->touched2) {
-      const int64_t cap = std::max<int64_t>(tneed, std::max(q->touched_cap, q->touched2_cap));
-      QCK(grow(&q->touched, q->touched_cap, cap));
-      QCK(grow(&q->touched2, q->touched2_cap, cap));
-      q->full_reset = true;
-    }
-    if (q->full_reset) {
-      QCK(cudaMemsetAsync(q->g, 0, sizeof(int32_t) * q->g_cap, st));
-      QCK(cudaMemsetAsync(q->a, 0, sizeof(int32_t) * q->a_cap, st));
-      QCK(cudaMemsetAsync(q->nd, 0, sizeof(int32_t) * q->nd_cap, st));
-      QCK(cudaMemsetAsync(q->prio, 0, sizeof(double) * q->prio_cap, st));
-      QCK(cudaMemsetAsync(q->dom, 0, (size_t)q->dom_cap, st));
-      QCK(grow(&q->tn, q->tn_cap, 2));
-      QCK(cudaMemsetAsync(q->tn, 0, 2 * sizeof(int32_t), st));
-      q->full_reset = false;
-    }
-    QCK(grow(&q->tn, q->tn_cap, 2));
-    QCK(grow(&q->aligned, q->aligned_cap, P * qsmall::QS_SKCAP));
-    QCK(grow(&q->rk, q->rk_cap, q->aligned_cap));
-    QCK(grow(&q->emap, q->emap_cap, q->aligned_cap));
-    QCK(grow(&q->longl, q->longl_cap, P));
-    QCK(grow(&q->sig, q->sig_cap, P * c.kappa));
-    QCK(grow(&q->siglen, q->siglen_cap, P));
-    int64_t bt = 64;
-    while (bt < 2 * P) bt <<= 1;
-    int64_t pt = 64;
-    while (pt < 4 * P * qsmall::QS_SKCAP) pt <<= 1;  // pairs: distinct (bucket, seg) <= nsk, load <= 1/4
-    QCK(grow(&q->tkey, q->tkey_cap, bt));
-    QCK(grow(&q->tmin, q->tmin_cap, bt));
-    QCK(grow(&q->slot_of, q->slot_of_cap, P));
-    QCK(grow(&q->bmin, q->bmin_cap, P));
-    QCK(grow(&q->bstart, q->bstart_cap, P));
-    QCK(grow(&q->bend, q->bend_cap, P));
-    QCK(grow(&q->score, q->score_cap, P));
-    QCK(grow(&q->take, q->take_cap, P));
-    QCK(grow(&q->rank, q->rank_cap, P));
-    QCK(grow(&q->bucket, q->bucket_cap, P));
-    QCK(grow(&q->hot, q->hot_cap, P));
-    QCK(grow(&q->cv2, q->cv2_cap, P));
-    QCK(grow(&q->pk, q->pk_cap, pt));
-    QCK(grow(&q->pv, q->pv_cap, pt));
-    QCK(grow(&q->plist, q->plist_cap, pt / 2));
-    QCK(grow(&q->qcounts, q->qcounts_cap, 8));
-    QCK(cudaMemsetAsync(q->qcounts, 0, 8 * sizeof(int64_t), st));
-    qsmall::QsArgs qa{};
-    qa.P = P;
-    qa.A = A;
-    qa.ids = in.ids;
-    qa.arrival = in.arrival;
-    qa.off = in.off;
-    qa.sk = in.sk;
-    qa.reo = in.reo;
-    qa.aoff = in.aoff;
-    qa.ask = in.ask;
-    qa.g = q->g;
-    qa.a = q->a;
-    qa.nd = q->nd;
-    qa.prio = q->prio;
-    qa.dom = q->dom;
-    qa.touched = q->touched;
-    qa.touched_n = q->tn;
-    qa.prev_touched = q->touched2;
-    qa.aligned = q->aligned;
-    qa.sig = q->sig;
-    qa.siglen = q->siglen;
-    qa.rank = q->rank;
-    qa.bucket = q->bucket;
-    qa.hot = q->hot;
-    qa.cold = q->cv2;
-    qa.score = q->score;
-    qa.counts = q->qcounts;
-    qa.btab_key = q->tkey;
-    qa.btab_min = q->tmin;
-    qa.slot_of = q->slot_of;
-    qa.bidx = q->bmin;
-    qa.bsize = q->bstart;
-    qa.nsegs = q->bend;
-    qa.isum = (long long *)q->take;
-    qa.ptab_key = q->pk;
-    qa.ptab_cnt = q->pv;
-    qa.plist = q->plist;
-    qa.ptab_cap = std::min(q->pk_cap, q->pv_cap);
-    qa.btab_mask = bt - 1;
-    qa.longl = q->longl;
-    qa.rk = q->rk;
-    qa.emap = q->emap;
-    qa.aligned_cap = std::min(std::min(q->aligned_cap, q->rk_cap), q->emap_cap);
-    if (q->prof_on) QCK(grow(&q->qts, q->qts_cap, qsmall::QS_NTS));
-    qa.ts = q->prof_on ? q->qts : nullptr;
-    const qsmall::QsCfg qc{c.budget, c.cold, c.front, c.kappa, c.wg, c.wa, c.wn, c.alpha, c.beta};
-    if (!q->small_coresident) {
-      QCK(cudaFuncSetAttribute(qsmall::k_qas_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)qsmall::QS_SMEM));
-      int nsm = 0, occ = 0;
-      QCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, q->dev));
-      QCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, qsmall::k_qas_small, qsmall::QS_TPB,
-                                                        qsmall::QS_SMEM));
-      q->small_coresident = std::max(1, nsm * occ);
-    }
-    // grid: one CTA for small sets (no grid barriers), else ~one CTA per
-    // small_per_cta pending requests, up to every SM
-    int64_t G = q->small_grid > 0 ? q->small_grid : (P + q->small_per_cta - 1) / q->small_per_cta;
-    G = std::max<int64_t>(1, std::min<int64_t>(G, q->small_coresident));
-    if (G == 1) {
-      qsmall::k_qas_small<<<1, qsmall::QS_TPB, qsmall::QS_SMEM, st>>>(qa, qc);
-    } else {
-      void *args[] = {(void *)&qa, (void *)&qc};
-      QCK(cudaLaunchCooperativeKernel((void *)qsmall::k_qas_small, dim3((unsigned)G), dim3(qsmall::QS_TPB), args,
-                                      qsmall::QS_SMEM, st));
-    }
-    QCK(cudaGetLastError());
+  // the touched-segment list (this round's list, read back next round to reset
+  // the counters: phase 0 consumes it before phase 1 rewrites it); growing it
+  // loses the previous round's entries, so that forces a full counter reset
+  const int64_t tneed = (int64_t)S1 + 1;  // distinct touched segments <= nseg
+  if (tneed > q->touched_cap || !q->touched) {
+    QCK(grow(&q->touched, q->touched_cap, tneed));
+    q->full_reset = true;
+  }
+  QCK(grow(&q->tn, q->tn_cap, 2));
+  if (q->full_reset) {
+    QCK(cudaMemsetAsync(q->g, 0, sizeof(int32_t) * q->g_cap, st));
+    QCK(cudaMemsetAsync(q->a, 0, sizeof(int32_t) * q->a_cap, st));
+    QCK(cudaMemsetAsync(q->nd, 0, sizeof(int32_t) * q->nd_cap, st));
+    QCK(cudaMemsetAsync(q->prio, 0, sizeof(double) * q->prio_cap, st));
+    QCK(cudaMemsetAsync(q->dom, 0, (size_t)q->dom_cap, st));
+    QCK(cudaMemsetAsync(q->tn, 0, 2 * sizeof(int32_t), st));
+    q->full_reset = false;
+  }
+  QCK(grow(&q->aligned, q->aligned_cap, P * qsmall::QS_SKCAP));
+  QCK(grow(&q->rk, q->rk_cap, q->aligned_cap));
+  QCK(grow(&q->emap, q->emap_cap, q->aligned_cap));
+  QCK(grow(&q->longl, q->longl_cap, P));
+  QCK(grow(&q->sig, q->sig_cap, P * c.kappa));
+  QCK(grow(&q->siglen, q->siglen_cap, P));
+  int64_t bt = 64;
+  while (bt < 2 * P) bt <<= 1;
+  int64_t pt = 64;
+  while (pt < 4 * P * qsmall::QS_SKCAP) pt <<= 1;  // pairs: distinct (bucket, seg) <= nsk, load <= 1/4
+  QCK(grow(&q->tkey, q->tkey_cap, bt));
+  QCK(grow(&q->tmin, q->tmin_cap, bt));
+  QCK(grow(&q->slot_of, q->slot_of_cap, P));
+  QCK(grow(&q->bmin, q->bmin_cap, P));
+  QCK(grow(&q->bstart, q->bstart_cap, P));
+  QCK(grow(&q->bend, q->bend_cap, P));
+  QCK(grow(&q->score, q->score_cap, P));
+  QCK(grow(&q->take, q->take_cap, P));
+  QCK(grow(&q->rank, q->rank_cap, P));
+  QCK(grow(&q->bucket, q->bucket_cap, P));
+  QCK(grow(&q->hot, q->hot_cap, P));
+  QCK(grow(&q->cv2, q->cv2_cap, P));
+  QCK(grow(&q->pk, q->pk_cap, pt));
+  QCK(grow(&q->pv, q->pv_cap, pt));
+  QCK(grow(&q->plist, q->plist_cap, pt / 2));
+  QCK(grow(&q->qcounts, q->qcounts_cap, 8));
+  if (q->prof_on) QCK(grow(&q->qts, q->qts_cap, qsmall::QS_NTS));
+  if (!q->small_coresident) {
+    QCK(cudaFuncSetAttribute(qsmall::k_qas_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)qsmall::QS_SMEM));
+    int nsm = 0, occ = 0;
+    QCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, q->dev));
+    QCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, qsmall::k_qas_small, qsmall::QS_TPB,
+                                                      qsmall::QS_SMEM));
+    q->small_coresident = std::max(1, nsm * occ);
+  }
+  // grid: one CTA for small sets (no grid barriers), else ~one CTA per
+  // small_per_cta pending requests, up to every SM
+  int64_t G = q->small_grid > 0 ? q->small_grid : (P + q->small_per_cta - 1) / q->small_per_cta;
+  *G_out = std::max<int64_t>(1, std::min<int64_t>(G, q->small_coresident));
+  return PRISM_OK;
+}
+
+// the one-launch round itself (capturable): counters reset, the kernel
+int qas_small_launch(prism_qas *q, const QIn &in, int64_t P, int64_t A, int64_t bt_mask, const QCfg &c, int64_t G) {
+  cudaStream_t st = q->st;
+  QCK(cudaMemsetAsync(q->qcounts, 0, 8 * sizeof(int64_t), st));
+  qsmall::QsArgs qa{};
+  qa.P = P;
+  qa.A = A;
+  qa.ids = in.ids;
+  qa.arrival = in.arrival;
+  qa.off = in.off;
+  qa.sk = in.sk;
+  qa.reo = in.reo;
+  qa.aoff = in.aoff;
+  qa.ask = in.ask;
+  qa.g = q->g;
+  qa.a = q->a;
+  qa.nd = q->nd;
+  qa.prio = q->prio;
+  qa.dom = q->dom;
+  qa.touched = q->touched;
+  qa.touched_n = q->tn;
+  qa.prev_touched = q->touched;
+  qa.aligned = q->aligned;
+  qa.sig = q->sig;
+  qa.siglen = q->siglen;
+  qa.rank = q->rank;
+  qa.bucket = q->bucket;
+  qa.hot = q->hot;
+  qa.cold = q->cv2;
+  qa.score = q->score;
+  qa.counts = q->qcounts;
+  qa.btab_key = q->tkey;
+  qa.btab_min = q->tmin;
+  qa.slot_of = q->slot_of;
+  qa.bidx = q->bmin;
+  qa.bsize = q->bstart;
+  qa.nsegs = q->bend;
+  qa.isum = (long long *)q->take;
+  qa.ptab_key = q->pk;
+  qa.ptab_cnt = q->pv;
+  qa.plist = q->plist;
+  qa.ptab_cap = std::min(q->pk_cap, q->pv_cap);
+  qa.btab_mask = bt_mask;
+  qa.longl = q->longl;
+  qa.rk = q->rk;
+  qa.emap = q->emap;
+  qa.aligned_cap = std::min(std::min(q->aligned_cap, q->rk_cap), q->emap_cap);
+  qa.ts = q->prof_on ? q->qts : nullptr;
+  const qsmall::QsCfg qc{c.budget, c.cold, c.front, c.kappa, c.wg, c.wa, c.wn, c.alpha, c.beta};
+  if (G == 1) {
+    qsmall::k_qas_small<<<1, qsmall::QS_TPB, qsmall::QS_SMEM, st>>>(qa, qc);
+  } else {
+    void *args[] = {(void *)&qa, (void *)&qc};
+    QCK(cudaLaunchCooperativeKernel((void *)qsmall::k_qas_small, dim3((unsigned)G), dim3(qsmall::QS_TPB), args,
+                                    qsmall::QS_SMEM, st));
+  }
+  QCK(cudaGetLastError());
+  return PRISM_OK;
+}
+
+int64_t qas_small_btmask(int64_t P) {
+  int64_t bt = 64;
+  while (bt < 2 * P) bt <<= 1;
+  return bt - 1;
+}
+
+int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, const QCfg &c, int64_t *nhot, int64_t *ncold,
+            int64_t *nbuckets) {
+  // ---- one-launch round for small pending sets with integral weights (qas_small.cuh)
+  if (qas_small_eligible(q, P, c)) {
+    int64_t G = 1;
+    int rc = qas_small_prepare(q, P, nseg, c, &G);
+    if (rc) return rc;
+    if ((rc = qas_small_launch(q, in, P, A, qas_small_btmask(P), c, G))) return rc;
     q->last_small_grid = G;
-    std::swap(q->touched, q->touched2);  // this round's list resets the next round
-    std::swap(q->touched_cap, q->touched2_cap);
     const int64_t hot_cap = c.budget - c.cold;
     *nhot = std::min<int64_t>(std::max<int64_t>(hot_cap, 0), P);
     *ncold = std::min<int64_t>(c.cold, P - *nhot);
@@ -739,6 +760,16 @@ int qas_run(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nseg, con
     q->small_rounds++;
     return PRISM_OK;
   }
+  const int32_t S1 = std::max(nseg, 1);
+  const int64_t gcap0 = q->g_cap;
+  QCK(grow(&q->g, q->g_cap, S1));
+  QCK(grow(&q->a, q->a_cap, S1));
+  QCK(grow(&q->nd, q->nd_cap, S1));
+  QCK(grow(&q->prio, q->prio_cap, S1));
+  QCK(grow(&q->dom, q->dom_cap, S1));
+  QCK(grow(&q->err, q->err_cap, 4));
+  QCK(grow(&q->small, q->small_cap, 8));
+  if (q->g_cap != gcap0) q->full_reset = true;
   return qas_run_multi(q, in, P, A, nseg, c, nhot, ncold, nbuckets);
 }
 
