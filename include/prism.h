@@ -45,6 +45,7 @@ extern "C" {
 typedef struct prism_tree prism_tree;
 
 const char *prism_last_error(void);
+void prism_set_last_error(const char *msg);
 int prism_device_count(void);
 
 /* RadixCache.__init__(CacheConfig) -- kvcache.py:120-131, CacheConfig kvcache.py:66-76.
@@ -225,7 +226,7 @@ int prism_wave_commit_enqueue(prism_tree *t, int64_t B, const int64_t *path_off,
                               const int64_t *anc_off, const int8_t *a_kind, const int32_t *a_seg,
                               const int32_t *a_snap, const int64_t *members, const int64_t *sk_off,
                               const int32_t *aligned, int64_t sys_len, int64_t chunk, int64_t *hits,
-                              int32_t *leaf_slots, int64_t *leaf_ids, void *stream);
+                              int32_t *leaf_slots, int64_t *leaf_ids, void *stream, const int32_t *abort);
 int prism_wave_commit_finish(prism_tree *t, int64_t B, int32_t *applied);
 uint64_t prism_wave_commit_key(prism_tree *t);
 /* The cudaStream_t (as void*) the QAS instance launches on; prism_wave_step

@@ -626,9 +626,9 @@ __device__ inline void block_merge_sort(const Key3 *k, const uint64_t *v, int n,
     const bool ok = i < n;
     const int c0 = ok ? (i / MS_CH) * MS_CH : 0, c1 = ok ? min(c0 + MS_CH, n) : 0;
     const Key3 x = ok ? k[i] : Key3{0, 0, 0};
-    int r = 0;
+    int r = 0;  // (ties by position: equal keys, e.g. padding, keep a permutation -- a stable sort)
 #pragma unroll 4
-    for (int j = c0 + sub; j < c1; j += tpi) r += key_less(k[j], x) ? 1 : 0;
+    for (int j = c0 + sub; j < c1; j += tpi) r += (key_less(k[j], x) || (j < i && !key_less(x, k[j]))) ? 1 : 0;
     for (int o = 1; o < tpi; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
     if (ok && sub == 0) {
       tk[c0 + r] = x;
@@ -644,9 +644,10 @@ __device__ inline void block_merge_sort(const Key3 *k, const uint64_t *v, int n,
       if (d == c) continue;
       int lo = d * MS_CH, hi = min(lo + MS_CH, n);
       const int base = lo;
+      const bool before = d < c;  // equal keys of earlier chunks precede
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (key_less(tk[mid], x)) lo = mid + 1;
+        if (before ? !key_less(x, tk[mid]) : key_less(tk[mid], x)) lo = mid + 1;
         else hi = mid;
       }
       pos += lo - base;

@@ -630,7 +630,7 @@ int wave_par_prepare(prism_tree *t, int64_t B, int64_t levels) {
 // no host wait (cooperative build path); ends by copying the verdict and the
 // control block to pinned host memory.  Capturable in a CUDA graph.
 int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *leaf_slots, int64_t *leaf_ids,
-                     int32_t force_full) {
+                     int32_t force_full, const int32_t *abort = nullptr) {
   const int64_t B = W.B;
   cudaStream_t st = t->st;
   const int sms = t->sms;
@@ -643,7 +643,7 @@ int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *lea
   CK(cudaMemsetAsync(X.flags, 0, sizeof(int32_t), st));
   CK(cudaMemsetAsync(X.misc, 0, sizeof(int64_t) * 8, st));
   CK(cudaMemsetAsync(X.misc + 1, 0x7F, sizeof(int64_t), st));  // poison index: "none"
-  k_wc_begin<<<1, 1, 0, st>>>(t->d, wc);
+  k_wc_begin<<<1, 1, 0, st>>>(t->d, wc, abort);
   k_wp_plan<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_levels<<<blocks_for(B * WP_PL), TPB, 0, st>>>(W, X);
   k_wp_hits<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X);
@@ -696,6 +696,8 @@ int wave_par_verdict(prism_tree *t, int *applied, int *again, int32_t *force_ful
       return PRISM_OK;
     case WC_FALLBACK:
       t->last_fallback = H.flags;
+      return PRISM_OK;
+    case WC_ABORT:  // the caller's stage failed; it re-runs the wave
       return PRISM_OK;
     case WC_FULL:  // the selected prefix fell short: select the whole order
       *force_full = 1;
@@ -815,6 +817,7 @@ int validate_anchors(int64_t n, int64_t na, const int32_t *a_off, const int8_t *
 extern "C" {
 
 const char *prism_last_error(void) { return g_err.c_str(); }
+void prism_set_last_error(const char *msg) { g_err = msg ? msg : ""; }
 
 int prism_device_count(void) {
   int n = 0;
@@ -1376,14 +1379,14 @@ int prism_wave_commit_enqueue(prism_tree *t, int64_t B, const int64_t *path_off,
                               const int64_t *anc_off, const int8_t *a_kind, const int32_t *a_seg,
                               const int32_t *a_snap, const int64_t *members, const int64_t *sk_off,
                               const int32_t *aligned, int64_t sys_len, int64_t chunk, int64_t *hits,
-                              int32_t *leaf_slots, int64_t *leaf_ids, void *stream) {
+                              int32_t *leaf_slots, int64_t *leaf_ids, void *stream, const int32_t *abort) {
   CK(cudaEventRecord(t->ev_in, (cudaStream_t)stream));
   CK(cudaStreamWaitEvent(t->st, t->ev_in, 0));
-  k_prematch<<<blocks_for(B * 32), TPB, 0, t->st>>>(t->d, B, path_off, tokens, t->d_pm_meta, t->d_pm_chain);
+  k_prematch<<<blocks_for(B * 32), TPB, 0, t->st>>>(t->d, B, path_off, tokens, t->d_pm_meta, t->d_pm_chain, abort);
   t->launches[PH_PREMATCH]++;
   WaveIn W{B, sys_len, chunk, path_off, tokens, anc_off, a_kind, a_seg, a_snap, members, sk_off, aligned,
            t->d_pm_meta, t->d_pm_chain};
-  int rc = wave_par_enqueue(t, W, hits, leaf_slots, leaf_ids, 0);
+  int rc = wave_par_enqueue(t, W, hits, leaf_slots, leaf_ids, 0, abort);
   if (rc) return rc;
   CK(cudaEventRecord(t->ev_out, t->st));
   CK(cudaStreamWaitEvent((cudaStream_t)stream, t->ev_out, 0));

@@ -113,9 +113,9 @@ __device__ inline WalkOut warp_walk(const DT &T, const uint32_t *p, int64_t n, i
 
 __global__ void k_prematch(DT T, int64_t B, const int64_t *__restrict__ poff,
                            const uint32_t *__restrict__ tok, int32_t *__restrict__ pm_meta,
-                           int32_t *__restrict__ pm_chain) {
+                           int32_t *__restrict__ pm_chain, const int32_t *abort = nullptr) {
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= B) return;
+  if (w >= B || (abort && *abort)) return;
   const int64_t b = poff[w], n = poff[w + 1] - b;
   const WalkOut r = warp_walk(T, tok + b, n, pm_chain + w * PM_MAX, PM_MAX);
   if (lane_id() == 0) {

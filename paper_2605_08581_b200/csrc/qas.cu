@@ -34,6 +34,7 @@ inline unsigned nblk(int64_t n) { return (unsigned)((n + TPB - 1) / TPB); }
 thread_local std::string q_err;
 int qfail(int code, const std::string &m) {
   q_err = m;
+  prism_set_last_error(m.c_str());  // one last-error for the whole library
   return code;
 }
 #define QCK(x)                                                                                \
@@ -463,6 +464,9 @@ struct prism_qas {
   X(int64_t, gids) \
   X(int64_t, goff) \
   X(int32_t, gsfx) \
+  X(double, garr) \
+  X(uint8_t, greo) \
+  X(int32_t, gsk) \
   X(uint64_t, tkey) \
   X(int32_t, tmin) \
   X(int32_t, slot_of) \
@@ -560,6 +564,7 @@ struct prism_qas {
   uint64_t gkey = 0, gkey_seen = 0;
   int32_t use_graph = 1;
   int64_t graph_captures = 0, graph_replays = 0, graph_kernels = 0;
+  int64_t *hres = nullptr;  // pinned: the fused wave's stage results
 };
 
 namespace {
@@ -1019,6 +1024,7 @@ void prism_qas_destroy(prism_qas *q) {
   for (void *p : bufs)
     if (p) cudaFree(p);
   if (q->gexec) cudaGraphExecDestroy(q->gexec);
+  if (q->hres) cudaFreeHost(q->hres);
   if (q->ev_t) cudaEventDestroy(q->ev_t);
   if (q->e0) cudaEventDestroy(q->e0);
   if (q->e1) cudaEventDestroy(q->e1);
@@ -1115,6 +1121,36 @@ namespace {
 constexpr uint64_t SEGMENT_TOKEN_BASE = 1000000ull;
 constexpr uint64_t SUFFIX_TOKEN_BASE = 2000000000ull;
 
+// the fused wave's per-call inputs copied into fixed buffers (a CUDA graph of
+// the wave reads those); abort when the skeletons exceed the staged capacity
+__global__ void q_stage(int64_t P, const int64_t *__restrict__ ids, const double *__restrict__ arr,
+                        const int64_t *__restrict__ off, const int32_t *__restrict__ sk,
+                        const uint8_t *__restrict__ reo, const int32_t *__restrict__ sfx, int64_t *__restrict__ gids,
+                        double *__restrict__ garr, int64_t *__restrict__ goff, int32_t *__restrict__ gsk,
+                        uint8_t *__restrict__ greo, int32_t *__restrict__ gsfx, int64_t skcap, int32_t *abort) {
+  const int64_t nsk = off[P];
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = gt; i <= P; i += gs) {
+    goff[i] = off[i];
+    if (i < P) {
+      gids[i] = ids[i];
+      garr[i] = arr[i];
+      greo[i] = reo[i];
+      gsfx[i] = sfx[i];
+    }
+  }
+  const int64_t n = nsk < skcap ? nsk : skcap;
+  for (int64_t e = gt; e < n; e += gs) gsk[e] = sk[e];
+  if (gt == 0) *abort = nsk > skcap ? 1 : 0;
+}
+
+// the fused wave's stage verdict: the one-launch round overflowed (redo), the
+// layout check failed, or the paths / anchors exceed the serialization buffers
+__global__ void q_capcheck(const int64_t *__restrict__ qcounts, const int64_t *__restrict__ tot, int64_t tok_cap,
+                           int64_t anc_cap, const int32_t *err, int32_t *abort) {
+  if (qcounts[3] || *err || tot[0] > tok_cap || tot[1] > anc_cap) *abort = 1;
+}
+
 // the wave's dispatch order (hot lane, then cold) with each member's path and
 // anchor counts, and the uint32 token-layout check of its private suffix
 // (workload.py:147-154), before anything is serialised
@@ -1154,7 +1190,9 @@ __global__ void q_serialize(int64_t B, const int64_t *__restrict__ members, cons
                             const int32_t *__restrict__ nd, const int64_t *__restrict__ poff,
                             const int64_t *__restrict__ aoffs, uint32_t *__restrict__ tok,
                             int32_t *__restrict__ a_off, int8_t *__restrict__ a_kind, int32_t *__restrict__ a_seg,
-                            int32_t *__restrict__ a_snap, int32_t *__restrict__ err) {
+                            int32_t *__restrict__ a_snap, int32_t *__restrict__ err,
+                            const int32_t *abort = nullptr) {
+  if (abort && *abort) return;  // (the fused wave's stage failed: sizes may exceed the buffers)
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= B) return;
@@ -1259,6 +1297,171 @@ int prism_qas_round_device(prism_qas *q, int64_t P, const int64_t *ids, const do
   return PRISM_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// The whole fused wave -- QAS round, dispatch order, protection (tree's
+// auxiliary stream), serialization, pre-match and the device-driven commit --
+// as ONE stream of launches with one host wait at the end; captured once per
+// wave shape and replayed as a CUDA graph.  The per-call inputs are staged
+// into fixed buffers first.  *handled = false: the stage failed on the device
+// (buffers too small, the one-launch round overflowed, layout check) and
+// nothing was committed -- the caller runs the regular path.
+int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, const double *arrival,
+                    const int64_t *sk_off, const int32_t *sk, const uint8_t *reorderable, const int32_t *suffix,
+                    int32_t nseg, const QCfg &c, int64_t sys_len, int64_t chunk, int64_t *members_out, int64_t *hits,
+                    int32_t *leaf_slots, int64_t *leaf_ids, int64_t *n_members, int64_t *n_admitted, bool *handled) {
+  *handled = false;
+  cudaStream_t st = q->st;
+  int64_t G = 1;
+  int rc = qas_small_prepare(q, P, nseg, c, &G);
+  if (rc) return rc;
+  const int64_t hot_cap = c.budget - c.cold;
+  const int64_t nh = std::min<int64_t>(std::max<int64_t>(hot_cap, 0), P);
+  const int64_t nc = std::min<int64_t>(c.cold, P - nh);
+  const int64_t B = nh + nc;
+  if (B == 0) return PRISM_OK;
+  int64_t *members = members_out;
+  if (!members) {
+    QCK(grow(&q->members, q->members_cap, P));
+    members = q->members;
+  }
+  QCK(grow(&q->plen, q->plen_cap, P + 1));
+  QCK(grow(&q->poff, q->poff_cap, P + 1));
+  QCK(grow(&q->alen, q->alen_cap, P + 1));
+  QCK(grow(&q->aoffs, q->aoffs_cap, P + 1));
+  QCK(grow(&q->tmp_tot, q->tmp_tot_cap, 2));
+  QCK(grow(&q->gids, q->gids_cap, P));
+  QCK(grow(&q->goff, q->goff_cap, P + 1));
+  QCK(grow(&q->gsfx, q->gsfx_cap, P));
+  QCK(grow(&q->garr, q->garr_cap, P));
+  QCK(grow(&q->greo, q->greo_cap, P));
+  QCK(grow(&q->gsk, q->gsk_cap, P * qsmall::QS_SKCAP));
+  // serialization buffers: every anchor a <= QS_SKCAP-segment skeleton can
+  // have; paths sized from the last overflow (the stage aborts, never overflows)
+  const int64_t nanc_cap = P * (qsmall::QS_SKCAP + 2);
+  QCK(grow(&q->a_off, q->a_off_cap, nanc_cap));
+  QCK(grow(&q->a_kind, q->a_kind_cap, nanc_cap));
+  QCK(grow(&q->a_seg, q->a_seg_cap, nanc_cap));
+  QCK(grow(&q->a_snap, q->a_snap_cap, 3 * nanc_cap));
+  QCK(grow(&q->tok, q->tok_cap, std::max<int64_t>(P * (sys_len + 16 * chunk + 64), 1)));
+  if (!q->hres) QCK(cudaMallocHost(&q->hres, 8 * sizeof(int64_t)));
+  if (!q->ev_t) QCK(cudaEventCreateWithFlags(&q->ev_t, cudaEventDisableTiming));
+  if ((rc = prism_wave_commit_prepare(t, B))) return rc;
+  int32_t *abort = q->err + 1;
+  q_stage<<<nblk(P * 8), TPB, 0, st>>>(P, ids, arrival, sk_off, sk, reorderable, suffix, q->gids, q->garr, q->goff,
+                                       q->gsk, q->greo, q->gsfx, q->gsk_cap, abort);
+  QCK(cudaGetLastError());
+  const QIn gin{q->gids, q->garr, q->goff, q->gsk, q->greo, nullptr, nullptr};
+  const int64_t btmask = qas_small_btmask(P);
+  const int64_t tok_cap = q->tok_cap, anc_cap = std::min(q->a_off_cap, q->a_snap_cap / 3);
+  auto body = [&]() -> int {
+    int r;
+    if ((r = qas_small_launch(q, gin, P, 0, btmask, c, G))) return r;
+    QCK(cudaMemsetAsync(q->err, 0, sizeof(int32_t), st));
+    q_members_len<<<nblk(B), TPB, 0, st>>>(nh, nc, q->hot, q->cv2, q->gids, q->goff, q->gsfx, sys_len, chunk,
+                                           members, q->plen, q->alen, q->err);
+    q_scan2<<<1, 1024, 0, st>>>(B, q->plen, q->alen, q->poff, q->aoffs, q->tmp_tot);
+    q_capcheck<<<1, 1, 0, st>>>(q->qcounts, q->tmp_tot, tok_cap, anc_cap, q->err, abort);
+    QCK(cudaEventRecord(q->ev_t, st));
+    QCK(cudaStreamWaitEvent((cudaStream_t)prism_tree_stream(t), q->ev_t, 0));
+    if ((r = prism_set_protection_device_async(t, q->prio, nseg))) return r;  // overlaps serialization
+    q_serialize<<<nblk(B * 32), TPB, 0, st>>>(B, members, q->gids, q->goff, q->aligned, q->gsfx, sys_len, chunk, q->g,
+                                              q->a, q->nd, q->poff, q->aoffs, q->tok, q->a_off, q->a_kind, q->a_seg,
+                                              q->a_snap, q->err, abort);
+    QCK(cudaGetLastError());
+    if ((r = prism_wave_commit_enqueue(t, B, q->poff, q->tok, q->aoffs, q->a_kind, q->a_seg, q->a_snap, members,
+                                       q->goff, q->aligned, sys_len, chunk, hits, leaf_slots, leaf_ids, (void *)st,
+                                       abort)))
+      return r;
+    QCK(cudaMemcpyAsync(q->hres, q->qcounts + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    QCK(cudaMemcpyAsync(q->hres + 2, q->tmp_tot, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    QCK(cudaMemcpyAsync(q->hres + 4, q->err, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    return PRISM_OK;
+  };
+  uint64_t key = prism_wave_commit_key(t);
+  {
+    const void *ptrs[] = {members, hits, leaf_slots, leaf_ids, q->gids, q->goff, q->gsfx, q->garr, q->greo, q->gsk,
+                          q->aligned, q->g, q->a, q->nd, q->prio, q->dom, q->poff, q->aoffs, q->plen, q->alen,
+                          q->tok, q->a_off, q->a_kind, q->a_seg, q->a_snap, q->err, q->tmp_tot, q->qcounts, q->hres,
+                          q->touched, q->tn, q->rk, q->emap, q->longl, q->sig, q->siglen, q->tkey, q->tmin,
+                          q->slot_of, q->bmin, q->bstart, q->bend, q->score, q->take, q->rank, q->bucket, q->hot,
+                          q->cv2, q->pk, q->pv, q->plist};
+    const int64_t dims[] = {P, B, G, btmask, nseg, sys_len, chunk, tok_cap, anc_cap, q->pk_cap, q->pv_cap,
+                            q->aligned_cap, q->rk_cap, q->emap_cap, (int64_t)q->prof_on};
+    const double cw[] = {c.wg, c.wa, c.wn, c.alpha, c.beta, (double)c.budget, (double)c.cold, (double)c.front,
+                         (double)c.kappa};
+    auto mixin = [&](const void *p, size_t n) {
+      for (size_t i = 0; i < n; i++) key = (key ^ ((const unsigned char *)p)[i]) * 0x100000001B3ull;
+    };
+    mixin(ptrs, sizeof(ptrs));
+    mixin(dims, sizeof(dims));
+    mixin(cw, sizeof(cw));
+  }
+  if (q->gexec && key == q->gkey) {
+    QCK(cudaGraphLaunch(q->gexec, st));
+    q->graph_replays++;
+    q->launches += q->graph_kernels;
+  } else if (key == q->gkey_seen) {  // second wave of this shape: capture it
+    if (q->gexec) {
+      cudaGraphExecDestroy(q->gexec);
+      q->gexec = nullptr;
+    }
+    QCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    const int r = body();
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(st, &g);
+    if (r) return r;
+    if (ce != cudaSuccess || !g) return qfail(PRISM_CUDA, std::string("wave capture: ") + cudaGetErrorString(ce));
+    size_t nn = 0;  // kernel nodes: what one replay launches (launch accounting)
+    QCK(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    QCK(cudaGraphGetNodes(g, nodes.data(), &nn));
+    q->graph_kernels = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType ty;
+      QCK(cudaGraphNodeGetType(nd, &ty));
+      q->graph_kernels += ty == cudaGraphNodeTypeKernel ? 1 : 0;
+    }
+    QCK(cudaGraphInstantiate(&q->gexec, g, 0));
+    cudaGraphDestroy(g);
+    q->gkey = key;
+    QCK(cudaGraphLaunch(q->gexec, st));
+    q->graph_captures++;
+    q->launches += q->graph_kernels;
+  } else {  // first wave of this shape: plain launches
+    q->gkey_seen = key;
+    if ((rc = body())) return rc;
+    q->launches += 4;
+  }
+  QCK(cudaStreamSynchronize(st));
+  const int64_t *H = q->hres;
+  const int32_t *herr = reinterpret_cast<const int32_t *>(H + 4);
+  if (herr[1]) {  // stage aborted: nothing committed; size the buffers, the regular path redoes the wave
+    if (H[2] > tok_cap) QCK(grow(&q->tok, q->tok_cap, H[2] + H[2] / 4));
+    return PRISM_OK;
+  }
+  q->last_small_grid = G;
+  q->rounds++;
+  q->small_rounds++;
+  int32_t applied = 0;
+  if ((rc = prism_wave_commit_finish(t, B, &applied))) return rc;
+  *handled = true;
+  *n_members = B;
+  if (applied) {
+    *n_admitted = B;
+    return PRISM_OK;
+  }
+  // not committed in parallel (maintenance / whole order / exactness guard):
+  // the regular path re-runs the commit on the already-serialized wave
+  return prism_admit_wave_segmented(t, B, q->poff, q->tok, q->aoffs, q->a_off, q->a_kind, q->a_seg, q->a_snap,
+                                    members, q->goff, q->aligned, sys_len, chunk, q->commit_mode, hits, leaf_slots,
+                                    leaf_ids, n_admitted, (void *)st);
+}
+}  // namespace
+
+extern "C" {
+
 int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, const double *arrival,
                     const int64_t *sk_off, const int32_t *sk, const uint8_t *reorderable, const int32_t *suffix,
                     int64_t A, const int64_t *act_off, const int32_t *act_sk, int32_t nseg,
@@ -1274,6 +1477,13 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
                cfg->w_g, cfg->w_a, cfg->w_n, cfg->alpha_size, cfg->beta_util};
   const QIn in{ids, arrival, sk_off, sk, reorderable, act_off, act_sk};
   int64_t nh = 0, nc = 0, nb = 0;
+  if (q->use_graph && !q->prof_on && A == 0 && q->commit_mode == 0 && chunk > 0 && qas_small_eligible(q, P, c) &&
+      prism_tree_policy(t) == 0 && prism_tree_graphable(t)) {
+    bool handled = false;
+    int rc = wave_step_graph(t, q, P, ids, arrival, sk_off, sk, reorderable, suffix, nseg, c, sys_len, chunk,
+                             members_out, hits, leaf_slots, leaf_ids, n_members, n_admitted, &handled);
+    if (rc || handled) return rc;
+  }
   if (q->prof_on) cudaEventRecord(q->e0, st);
   // QAS round (engine.py:189): one launch for the one-CTA/cooperative round
   int rc = qas_run(q, in, P, A, nseg, c, &nh, &nc, &nb);
@@ -1331,90 +1541,6 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
     QCK(grow(&q->a_snap, q->a_snap_cap, 3 * std::max<int64_t>(nanc, 1)));
     if (!q->ev_t) QCK(cudaEventCreateWithFlags(&q->ev_t, cudaEventDisableTiming));
     const int32_t pol = prism_tree_policy(t);
-    // the rest of the wave is one stream of launches (protection on the tree's
-    // auxiliary stream, serialization here, pre-match + commit on the tree
-    // stream) with one host wait at the end; repeated waves of the same shape
-    // replay it as a CUDA graph
-    const bool graph = q->use_graph && !q->prof_on && pol == 0 && q->commit_mode == 0 && chunk > 0 &&
-                       prism_tree_graphable(t);
-    if (graph) {
-      if ((rc = prism_wave_commit_prepare(t, B))) return rc;
-      // the graph reads fixed copies of the caller's per-wave arrays
-      QCK(grow(&q->gids, q->gids_cap, Pc));
-      QCK(grow(&q->goff, q->goff_cap, Pc + 1));
-      QCK(grow(&q->gsfx, q->gsfx_cap, Pc));
-      QCK(cudaMemcpyAsync(q->gids, ids, sizeof(int64_t) * P, cudaMemcpyDeviceToDevice, st));
-      QCK(cudaMemcpyAsync(q->goff, sk_off, sizeof(int64_t) * (P + 1), cudaMemcpyDeviceToDevice, st));
-      QCK(cudaMemcpyAsync(q->gsfx, suffix, sizeof(int32_t) * P, cudaMemcpyDeviceToDevice, st));
-      auto tail = [&]() -> int {
-        int r;
-        QCK(cudaEventRecord(q->ev_t, st));
-        QCK(cudaStreamWaitEvent((cudaStream_t)prism_tree_stream(t), q->ev_t, 0));
-        if ((r = prism_set_protection_device_async(t, q->prio, nseg))) return r;  // overlaps serialization
-        q_serialize<<<nblk(B * 32), TPB, 0, st>>>(B, members, q->gids, q->goff, q->aligned, q->gsfx, sys_len, chunk,
-                                                  q->g, q->a, q->nd, q->poff, q->aoffs, q->tok, q->a_off, q->a_kind,
-                                                  q->a_seg, q->a_snap, q->err);
-        QCK(cudaGetLastError());
-        return prism_wave_commit_enqueue(t, B, q->poff, q->tok, q->aoffs, q->a_kind, q->a_seg, q->a_snap, members,
-                                         q->goff, q->aligned, sys_len, chunk, hits, leaf_slots, leaf_ids,
-                                         (void *)st);
-      };
-      uint64_t key = prism_wave_commit_key(t);
-      const void *ptrs[] = {members, hits, leaf_slots, leaf_ids, q->gids, q->goff, q->gsfx, q->aligned, q->g,
-                            q->a, q->nd, q->prio, q->poff, q->aoffs, q->tok, q->a_off, q->a_kind, q->a_seg,
-                            q->a_snap, q->err};
-      const int64_t dims[] = {B, sys_len, chunk, nseg};
-      for (const unsigned char *c = (const unsigned char *)ptrs; c < (const unsigned char *)(ptrs + 20); c++)
-        key = (key ^ *c) * 0x100000001B3ull;
-      for (const unsigned char *c = (const unsigned char *)dims; c < (const unsigned char *)(dims + 4); c++)
-        key = (key ^ *c) * 0x100000001B3ull;
-      if (q->gexec && key == q->gkey) {
-        QCK(cudaGraphLaunch(q->gexec, st));
-        q->graph_replays++;
-        q->launches += q->graph_kernels;
-      } else if (key == q->gkey_seen) {  // second wave of this shape: capture it
-        if (q->gexec) {
-          cudaGraphExecDestroy(q->gexec);
-          q->gexec = nullptr;
-        }
-        QCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
-        const int r = tail();
-        cudaGraph_t g = nullptr;
-        const cudaError_t ce = cudaStreamEndCapture(st, &g);
-        if (r) return r;
-        if (ce != cudaSuccess || !g) return qfail(PRISM_CUDA, std::string("wave capture: ") + cudaGetErrorString(ce));
-        size_t nn = 0;  // kernel nodes: what one replay launches (launch accounting)
-        QCK(cudaGraphGetNodes(g, nullptr, &nn));
-        std::vector<cudaGraphNode_t> nodes(nn);
-        QCK(cudaGraphGetNodes(g, nodes.data(), &nn));
-        q->graph_kernels = 0;
-        for (auto nd : nodes) {
-          cudaGraphNodeType ty;
-          QCK(cudaGraphNodeGetType(nd, &ty));
-          q->graph_kernels += ty == cudaGraphNodeTypeKernel ? 1 : 0;
-        }
-        QCK(cudaGraphInstantiate(&q->gexec, g, 0));
-        cudaGraphDestroy(g);
-        q->gkey = key;
-        QCK(cudaGraphLaunch(q->gexec, st));
-        q->graph_captures++;
-      } else {  // first wave of this shape: plain launches
-        q->gkey_seen = key;
-        if ((rc = tail())) return rc;
-      }
-      QCK(cudaStreamSynchronize(st));
-      int32_t applied = 0;
-      if ((rc = prism_wave_commit_finish(t, B, &applied))) return rc;
-      if (applied) {
-        *n_admitted = B;
-        return PRISM_OK;
-      }
-      // not committed in parallel (maintenance / whole order / exactness guard):
-      // the regular path re-runs the commit on the already-serialized wave
-      return prism_admit_wave_segmented(t, B, q->poff, q->tok, q->aoffs, q->a_off, q->a_kind, q->a_seg, q->a_snap,
-                                        members, q->goff, q->aligned, sys_len, chunk, q->commit_mode, hits,
-                                        leaf_slots, leaf_ids, n_admitted, (void *)st);
-    }
     // protection / active hand-off (engine.py:193-197), ordered after the round
     // on the tree's stream by an event (no host wait)
     QCK(cudaEventRecord(q->ev_t, st));

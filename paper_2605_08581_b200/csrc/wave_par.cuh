@@ -71,7 +71,7 @@ struct WaveTmp {
 // device-side control of one parallel wave commit: the control-block snapshot
 // the wave starts from, its totals, and the stop decision -- so the whole
 // commit is one stream of launches with no host round trip in the middle
-enum { WC_OK = 0, WC_FALLBACK = 1, WC_MAINT = 2, WC_FULL = 3 };
+enum { WC_OK = 0, WC_FALLBACK = 1, WC_MAINT = 2, WC_FULL = 3, WC_ABORT = 4 };
 struct WaveCtl {
   int64_t R0, id0, clock0, arena0, vbase;  // snapshot of the control block
   int64_t ncreate, ntail, nmiss;           // totals of the plan
@@ -125,7 +125,7 @@ __device__ inline int32_t wp_table(const WaveTmp &X, uint64_t key, int32_t j, bo
 // W1: per-member plan checks + skeleton-prefix ownership table
 __global__ void k_wp_plan(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= W.B) return;
+  if (j >= W.B || wc->stop) return;
   const uint32_t epoch = wc->epoch;
   const int64_t m = W.members[j];
   const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
@@ -490,10 +490,11 @@ __global__ void k_wp_label(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc, int64_t
 // ------------------------------------------------------------ device-side control
 
 // epoch + control-block snapshot the wave commits from
-__global__ void k_wc_begin(DT T, WaveCtl *wc) {
+__global__ void k_wc_begin(DT T, WaveCtl *wc, const int32_t *abort) {
   Ctrl *C = T.ctrl;
   C->epoch++;
   WaveCtl w{};
+  if (abort && *abort) w.stop = WC_ABORT;  // the caller's stage of the wave failed: touch nothing
   w.epoch = C->epoch;
   w.R0 = C->resident;
   w.id0 = C->next_id;
@@ -526,6 +527,10 @@ __global__ void __launch_bounds__(1024) k_wp_scan3(int64_t B, WaveTmp X) {
 // plan verdict: fallback flags, capacity headroom (slots, arena, child table),
 // and the eviction demand -> the prefix of the order to select (-1: none)
 __global__ void k_wc_plan(DT T, int64_t B, WaveTmp X, WaveCtl *wc, int64_t slack, int32_t force_full) {
+  if (wc->stop) {  // aborted before the plan
+    wc->W = -1;
+    return;
+  }
   const int32_t flags = *X.flags;
   if (flags) {
     wc->stop = WC_FALLBACK;
