@@ -506,6 +506,7 @@ def run_ours(args) -> None:
                 "slow_path_members": st2["slow_members"] - st1["slow_members"],
                 "profile": "per-phase device profile taken on extra waves after the timed region",
                 "commit": engine.wave_stats(),
+                "cuda_graph": engine.graph_stats(),
                 "last_list_build": engine.build_timeline(),
             },
             "roofline": roofline,

@@ -938,7 +938,8 @@ struct ProtCand {
 //   k_ss_sort    one CTA per bucket sorts it in shared memory.
 constexpr int SS_TPB = 256;
 constexpr int SS_SEL_TPB = 512;
-constexpr int SS_BMAX = 1024;  // largest bucket sorted in shared memory
+constexpr int SS_BMAX = 1024;  // buckets up to this size: k_ss_sort (merge sort, several CTAs per SM)
+constexpr int SS_BBIG = CHUNK; // larger ones up to this: k_ss_sort_big (in-place bitonic); beyond: fallback
 constexpr int SS_SUB = 2048;  // sub-sample the selection rounds run on
 constexpr size_t SS_SEL_SMEM =
     2 * sizeof(Key3) * SS_SPL + 8 * SS_U + 2 * (sizeof(Key3) + 8) * SS_SEL_TPB + (sizeof(Key3) + 9) * SS_SUB;
@@ -1204,7 +1205,7 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_scatter(CoopBufs B, int64_t W, co
     unsigned sum = 0;
     for (int b = b0; b < b1; b++) {
       const unsigned c = st->ss_cnt[b];
-      fits = fits && c <= (unsigned)SS_BMAX;
+      fits = fits && c <= (unsigned)SS_BBIG;
       sum += c;
     }
     unsigned x = sum;
@@ -1265,7 +1266,7 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_sort(CoopBufs B, Key3 *kout, uint
   uint64_t *tv = reinterpret_cast<uint64_t *>(tk + SS_BMAX);
   for (int b = blockIdx.x; b < nb; b += gridDim.x) {
     const int b0 = (int)st->ss_off[b], m0 = (int)(st->ss_off[b + 1] - st->ss_off[b]);
-    if (m0 == 0) continue;
+    if (m0 == 0 || m0 > SS_BMAX) continue;  // (big buckets: k_ss_sort_big)
     const long long c0 = clock64();
     for (int i = threadIdx.x; i < m0; i += blockDim.x) {
       sk[i] = B.ks[b0 + i];
@@ -1284,6 +1285,39 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_sort(CoopBufs B, Key3 *kout, uint
     }
   }
 }
+
+// the rare buckets above SS_BMAX (geometric sizes): in-place bitonic in shared memory
+__global__ void __launch_bounds__(512) k_ss_sort_big(CoopBufs B, Key3 *kout, uint64_t *vout) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  CoopState *st = B.st;
+  if (!st->ss_ok) return;
+  const int nb = st->ss_nb;
+  Key3 *sk = reinterpret_cast<Key3 *>(dsm);
+  uint64_t *sv = reinterpret_cast<uint64_t *>(sk + SS_BBIG);
+  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int b0 = (int)st->ss_off[b], m0 = (int)(st->ss_off[b + 1] - st->ss_off[b]);
+    if (m0 <= SS_BMAX) continue;
+    int mp = 1;
+    while (mp < m0) mp <<= 1;
+    for (int i = threadIdx.x; i < mp; i += blockDim.x) {
+      if (i < m0) {
+        sk[i] = B.ks[b0 + i];
+        sv[i] = B.vs[b0 + i];
+      } else {
+        sk[i] = {~0ull, ~0ull, ~0ull};
+        sv[i] = 0;
+      }
+    }
+    __syncthreads();
+    bitonic_smem(sk, sv, mp);
+    for (int i = threadIdx.x; i < m0; i += blockDim.x) {
+      kout[b0 + i] = sk[i];
+      vout[b0 + i] = sv[i];
+    }
+    __syncthreads();
+  }
+}
+constexpr size_t SS_BIG_SMEM = (sizeof(Key3) + 8) * SS_BBIG;
 
 // the eviction-order build after keys / subtree maxima (full-occupancy
 // kernels k_build_keys, k_propagate) and the sample select: the prefix of the
@@ -1423,24 +1457,46 @@ __global__ void __launch_bounds__(SS_TPB) k_tf_local(CoopBufs B, int64_t f) {
   }
 }
 
-// one CTA: the f smallest of the per-slice winners -> T.Lk/Lv[0..f), ss_ok
+// one CTA: the f smallest of the per-slice winners -> T.Lk/Lv[0..f), ss_ok.
+// Every slice holding f items bounds the answer by its f-th smallest key, so
+// only the winners up to the smallest such bound are gathered and sorted.
 __global__ void __launch_bounds__(SS_SEL_TPB) k_tf_merge(DT T, CoopBufs B, int64_t f) {
   extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ Key3 smin[33], smax[33];
+  __shared__ int s_n;
   const int64_t n = (int64_t)B.st->tf_n;
   if (n < f || f <= 0) return;  // ss_ok stays 0: the materialising path decides
   const int64_t nsl = (n + TF_SLICE - 1) / TF_SLICE;
-  const int64_t m = nsl * f;
-  if (m > TF_MERGE_MAX) return;  // too many winners for one CTA: the materialising path
   Key3 *sk = reinterpret_cast<Key3 *>(dsm);
   uint64_t *sv = reinterpret_cast<uint64_t *>(sk + TF_MERGE_MAX);
   Key3 *tk = reinterpret_cast<Key3 *>(sv + TF_MERGE_MAX);
   uint64_t *tv = reinterpret_cast<uint64_t *>(tk + TF_MERGE_MAX);
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    sk[i] = B.ks[i];
-    sv[i] = B.vs[i];
+  // the bound: the smallest f-th key over the slices (padding keys are maximal)
+  Key3 lo = {~0ull, ~0ull, ~0ull}, hi = {0, 0, 0};
+  for (int64_t c = threadIdx.x; c < nsl; c += blockDim.x) {
+    const Key3 x = B.ks[c * f + f - 1];
+    if (key_less(x, lo)) lo = x;
   }
+  block_minmax(lo, hi, smin, smax, &smin[32], &smax[32]);
+  const Key3 bound = smin[32];
+  if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
-  block_merge_sort(sk, sv, (int)m, tk, tv, sk, sv);
+  bool ovf = false;
+  for (int64_t i = threadIdx.x; i < nsl * f; i += blockDim.x) {
+    const Key3 x = B.ks[i];
+    if (!key_less(bound, x)) {  // x <= bound
+      const int p = atomicAdd(&s_n, 1);
+      if (p < TF_MERGE_MAX) {
+        sk[p] = x;
+        sv[p] = B.vs[i];
+      } else {
+        ovf = true;
+      }
+    }
+  }
+  if (__syncthreads_or(ovf)) return;  // (ss_ok stays 0)
+  const int m = s_n;
+  block_merge_sort(sk, sv, m, tk, tv, sk, sv);
   for (int i = threadIdx.x; i < f; i += blockDim.x) {
     T.Lk[i] = sk[i];
     T.Lv[i] = sv[i];

@@ -366,6 +366,7 @@ int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const 
     CK(cudaFuncSetAttribute(k_ss_select<EvictCand>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SEL_SMEM));
     CK(cudaFuncSetAttribute(k_ss_select<ProtCand>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SEL_SMEM));
     CK(cudaFuncSetAttribute(k_ss_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SORT_SMEM));
+    CK(cudaFuncSetAttribute(k_ss_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_BIG_SMEM));
     attr = true;
   }
   int sms = 0;
@@ -376,6 +377,7 @@ int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const 
   k_ss_filter<Cand><<<4 * sms, SS_TPB, SS_FILTER_SMEM, st>>>(cand, B);
   k_ss_scatter<<<2 * sms, SS_TPB, 0, st>>>(B, W, dW);
   k_ss_sort<<<3 * sms, SS_TPB, SS_SORT_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
+  k_ss_sort_big<<<sms, 512, SS_BIG_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
   CK(cudaGetLastError());
   return PRISM_OK;
 }
@@ -412,7 +414,7 @@ int build_list(prism_tree *t, int64_t W, const int64_t *dW = nullptr) {
     void *args[] = {(void *)&t->d, (void *)&B, (void *)&W, (void *)&dW, (void *)&minc, (void *)&small,
                     (void *)&sampled};
     CK(cudaLaunchCooperativeKernel((void *)k_build_coop, grid, COOP_TPB, args, COOP_SMEM, t->st));
-    t->launches[PH_BUILD] += 3 + (sampled ? 5 : 0);
+    t->launches[PH_BUILD] += 3 + (sampled ? 6 : 0);
     prof_end(t, PH_BUILD);
     return PRISM_OK;
   }
