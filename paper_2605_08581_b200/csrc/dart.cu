@@ -663,11 +663,9 @@ int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *lea
     if (!t->h_wc->stop && t->h_wc->W >= 0 && (rc = build_list(t, t->h_wc->W))) return rc;
   }
   prof_begin(t);
-  k_wp_vlen<<<2 * sms, TPB, 0, st>>>(t->d, X, wc);
-  const int64_t *dn = &t->d.ctrl->L_n;
-  k_dscan_a<<<DS_BLOCKS, 256, 0, st>>>(X.vlen, dn, t->ds_part, wc);
+  k_vscan_a<<<DS_BLOCKS, 256, 0, st>>>(t->d, X, t->ds_part, wc);
   k_dscan_b<<<1, 1024, 0, st>>>(t->ds_part, DS_BLOCKS, wc);
-  k_dscan_c<<<DS_BLOCKS, 256, 0, st>>>(X.vlen, dn, t->ds_part, X.F, wc);
+  k_vscan_c<<<DS_BLOCKS, 256, 0, st>>>(t->d, X, t->ds_part, wc);
   k_wp_cuts<<<blocks_for(B), TPB, 0, st>>>(t->d, B, X, wc);
   k_wc_cut<<<1, 1024, 0, st>>>(t->d, B, X, wc);
   k_wp_evict<<<2 * sms, TPB, 0, st>>>(t->d, wc);
@@ -678,7 +676,7 @@ int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *lea
   k_wp_label<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc, hits, leaf_slots, leaf_ids);
   k_wc_finalize<<<1, 1, 0, st>>>(t->d, B, X, wc);
   CK(cudaGetLastError());
-  t->launches[PH_COMMIT] += 14;
+  t->launches[PH_COMMIT] += 13;
   CK(cudaMemcpyAsync(t->h_wc, wc, sizeof(WaveCtl), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(t->hctrl, t->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
   return PRISM_OK;

@@ -511,17 +511,16 @@ __global__ void k_wc_begin(DT T, WaveCtl *wc, const int32_t *abort) {
 // exclusive scans cnew -> idb, tail -> arb (B + 1 entries) and the inclusive
 // scan miss -> dem (B entries), one CTA
 __global__ void __launch_bounds__(1024) k_wp_scan3(int64_t B, WaveTmp X) {
-  block_scan4<3, 8>(
-      B + 1,
-      [&](int a, int64_t i) -> int64_t {
-        if (i >= B) return 0;
-        return a == 0 ? X.cnew[i] : (a == 1 ? X.tail[i] : X.miss[i]);
-      },
-      [&](int a, int64_t i, int64_t ex, int64_t in) {
-        if (a == 0) X.idb[i] = ex;
-        else if (a == 1) X.arb[i] = ex;
-        else if (i < B) X.dem[i] = in;
-      });
+  // three single-sequence scans (one at a time keeps the tile in registers)
+  block_scan4<1, 8>(
+      B + 1, [&](int, int64_t i) -> int64_t { return i < B ? X.cnew[i] : 0; },
+      [&](int, int64_t i, int64_t ex, int64_t) { X.idb[i] = ex; });
+  block_scan4<1, 8>(
+      B + 1, [&](int, int64_t i) -> int64_t { return i < B ? X.tail[i] : 0; },
+      [&](int, int64_t i, int64_t ex, int64_t) { X.arb[i] = ex; });
+  block_scan4<1, 8>(
+      B, [&](int, int64_t i) -> int64_t { return X.miss[i]; },
+      [&](int, int64_t i, int64_t, int64_t in) { X.dem[i] = in; });
 }
 
 // plan verdict: fallback flags, capacity headroom (slots, arena, child table),
@@ -676,6 +675,66 @@ __global__ void __launch_bounds__(256) k_dscan_c(const int64_t *in, const int64_
     int64_t before = carry;
     for (int w = 0; w < wid; w++) before += sw[w];
     if (i < b1) out[i] = before + x;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = before + x;
+    __syncthreads();
+  }
+}
+
+
+// the eviction stream's token lengths fused into the device-sized scan: entry
+// i of the list counts elen when it is still the node it was listed as and
+// evictable by the wave's members, else 0 (and marks the first such entry:
+// misc[1], the victim guard).  k_vscan_a: per-block sums (+ the guard),
+// k_dscan_b: their scan, k_vscan_c: the inclusive prefix F.
+__device__ __forceinline__ int64_t wp_vlen(const DT &T, const WaveTmp &X, int64_t i, uint32_t epoch, bool mark) {
+  const uint64_t v = T.Lv[i];
+  const int32_t s = (int32_t)(v & 0xffffffffu);
+  const bool valid = T.kver[s] == (uint32_t)(v >> 32) && T.nid[s] >= 0 && T.par[s] >= 0 && T.ref[s] == 0;
+  if (mark && (!valid || T.wchild[s] == epoch)) atomicMin((unsigned long long *)&X.misc[1], (unsigned long long)i);
+  return valid ? T.elen[s] : 0;
+}
+
+__global__ void __launch_bounds__(256) k_vscan_a(DT T, WaveTmp X, int64_t *part, const WaveCtl *wc) {
+  if (wc->stop || wc->W < 0) return;
+  const int64_t n = T.ctrl->L_n, per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * per, b1 = b0 + per < n ? b0 + per : n;
+  const uint32_t epoch = wc->epoch;
+  int64_t s = 0;
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) s += wp_vlen(T, X, i, epoch, true);
+  __shared__ int64_t sw[8];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += sw[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_vscan_c(DT T, WaveTmp X, const int64_t *part, const WaveCtl *wc) {
+  if (wc->stop || wc->W < 0) return;
+  __shared__ int64_t sw[8];
+  __shared__ int64_t carry;
+  const int64_t n = T.ctrl->L_n, per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * per, b1 = b0 + per < n ? b0 + per : n;
+  const uint32_t epoch = wc->epoch;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = part[blockIdx.x];
+  __syncthreads();
+  for (int64_t t0 = b0; t0 < b1; t0 += blockDim.x) {
+    const int64_t i = t0 + threadIdx.x;
+    int64_t x = i < b1 ? wp_vlen(T, X, i, epoch, false) : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) sw[wid] = x;
+    __syncthreads();
+    int64_t before = carry;
+    for (int w = 0; w < wid; w++) before += sw[w];
+    if (i < b1) X.F[i] = before + x;
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) carry = before + x;
     __syncthreads();
