@@ -276,7 +276,7 @@ def run_ours(args) -> None:
     engine = WaveEngine(
         CacheConfig(capacity_tokens=args.capacity, policy=CachePolicy.DART, protect_budget=args.protect),
         SchedulerConfig(dispatch_budget=B, cold_quota=args.cold_quota),
-        NSEG, SYS_LEN, CHUNK, device=local, initial_slots=1 << 21, initial_arena_tokens=1 << 26,
+        NSEG, SYS_LEN, CHUNK, device=local, initial_slots=1 << 21, initial_arena_tokens=1 << 28,
     )
     rng = np.random.default_rng(args.seed + 1000 * rank)  # shard = independent sub-trace
     stream = engine.stream
@@ -364,45 +364,35 @@ def run_ours(args) -> None:
     e2e_steps = args.steps if args.e2e_steps < 0 else args.e2e_steps
     e2e = None
     if e2e_steps > 0 and not args.profile_only:
-        hpools = [make_pool(next_id + s * B, B, rng) for s in range(e2e_steps)]
-        next_id += e2e_steps * B
+        ew = max(args.warmup, 3)  # untimed: the first waves of the host-buffer shape capture its graph
+        hpools = [make_pool(next_id + s * B, B, rng) for s in range(e2e_steps + ew)]
+        next_id += (e2e_steps + ew) * B
         pinned = [{k: torch.from_numpy(v).pin_memory() for k, v in p.items()} for p in hpools]
-        # double-buffered inputs: step s+1's host->device copy runs on a copy
-        # stream while step s computes (the API call blocks until its wave ends)
-        dbufs = [{k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in pinned[0].items()}
-                 for _ in range(2)]
-        cstream = torch.cuda.Stream(device=dev)
-        ev_in = [torch.cuda.Event() for _ in range(2)]
-        out_hits = torch.empty(B, dtype=torch.int64).pin_memory()
-        out_mem = torch.empty(B, dtype=torch.int64).pin_memory()
+        out_mem = np.empty(B, dtype=np.int64)
+        out_hits = np.empty(B, dtype=np.int64)
         h2d = sum(v.numel() * v.element_size() for v in pinned[0].values())
+        for s in range(ew):
+            _, prev = engine.step_host(pinned[e2e_steps + s], out_mem, out_hits, release_n=prev)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        cstream.wait_event(e0)
-
-        def prefetch(s):
-            with torch.cuda.stream(cstream):
-                for k, buf in dbufs[s % 2].items():
-                    buf.copy_(pinned[s][k], non_blocking=True)
-                ev_in[s % 2].record(cstream)
-
-        prefetch(0)
         adm2 = 0
         d2h = 0
+        wall = []
         for s in range(e2e_steps):
-            if s + 1 < e2e_steps:
-                prefetch(s + 1)  # (its buffer's last reader, step s-1, has completed)
-            stream.wait_event(ev_in[s % 2])
-            db = dbufs[s % 2]
-            pend = DevicePending(db["ids"], db["arrival"], db["sk_off"], db["sk"], db["reorderable"], db["suffix"])
-            nm, na = one_step(pend)
-            with torch.cuda.stream(stream):
-                out_hits[:na].copy_(engine.hits[:na], non_blocking=True)
-                out_mem[:nm].copy_(engine.members[:nm], non_blocking=True)
+            # host pinned inputs read in place by the wave, results back in host arrays,
+            # the previous wave's pins released by the same call
+            tw = time.perf_counter()
+            nm, na = engine.step_host(pinned[s], out_mem, out_hits, release_n=prev)
+            wall.append((time.perf_counter() - tw) * 1e3)
+            prev = na
+            if demand is not None:
+                with torch.cuda.stream(stream):
+                    engine.demand_counters(demand)
+                    dist.all_reduce(demand)
             d2h += 8 * (na + nm)
             adm2 += na
         e1.record(stream)
@@ -416,9 +406,10 @@ def run_ours(args) -> None:
             dist.all_reduce(c)
             adm2 = int(c.item())
         e2e = {"value": adm2 / (ms2 / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h // e2e_steps, "api": "prism_wave_step via WaveEngine.step "
-               "(pinned host pools copied in on a copy stream, double-buffered; hits + admission order "
-               "copied out after each wave)"}
+               "d2h_bytes_per_step": d2h // e2e_steps, "api": "prism_wave_step_host via WaveEngine.step_host "
+               "(pinned host pending arrays read in place by the wave's staging kernel; admission order + hits "
+               "copied to host inside the wave; the previous wave's pins released by the same call)",
+               "host_ms_per_call": {"median": round(statistics.median(wall), 4), "max": round(max(wall), 4)}}
 
     # ---- roofline of the dominant kernel: a few more waves of the same workload
     # AFTER the timed region with the live per-phase profile on (its per-phase

@@ -115,6 +115,10 @@ struct prism_tree {
   int64_t *d_prot_ids = nullptr;
   int64_t prot_cap = 0;
   int64_t compactions = 0;
+  uint32_t *tok_spare = nullptr;  // spare token arena (compaction target)
+  int64_t spare_cap = 0;
+  int64_t *cmp_len = nullptr, *cmp_off = nullptr;
+  int64_t cmp_cap = 0;
   // live device-time profile per phase (CUDA events on the tree stream)
   int prof_on = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -468,12 +472,20 @@ int rehash(prism_tree *t, int64_t extra) {
   return push_ctrl(t);
 }
 
+// compaction of the token arena: live edges packed into the spare arena (kept
+// allocated at the same capacity, so a steady-state compaction is two kernels
+// and a scan, no allocation), then the two swap
 int compact_arena(prism_tree *t, int64_t need) {
   join_aux(t);  // the auxiliary stream must not touch arrays being replaced
   const int32_t hw = t->hctrl->hw;
-  int64_t *len = nullptr, *off = nullptr;
-  CK(dalloc(&len, hw + 1));
-  CK(dalloc(&off, hw + 1));
+  if (hw + 1 > t->cmp_cap) {
+    if (t->cmp_len) CK(cudaFree(t->cmp_len));
+    if (t->cmp_off) CK(cudaFree(t->cmp_off));
+    t->cmp_cap = next_pow2(hw + 1);
+    CK(dalloc(&t->cmp_len, t->cmp_cap));
+    CK(dalloc(&t->cmp_off, t->cmp_cap));
+  }
+  int64_t *len = t->cmp_len, *off = t->cmp_off;
   k_compact_len<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw, len);
   size_t bytes = 0;
   CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, len, off, (int)hw, t->st));
@@ -488,14 +500,22 @@ int compact_arena(prism_tree *t, int64_t need) {
   const int64_t live = h2[0] + h2[1];
   int64_t cap = t->d.acap;
   while (live + need > cap / 2) cap *= 2;
-  uint32_t *na = nullptr;
-  CK(dalloc(&na, cap));
+  if (cap != t->d.acap || !t->tok_spare || t->spare_cap != cap) {  // (re)size the spare
+    if (t->tok_spare) CK(cudaFree(t->tok_spare));
+    CK(dalloc(&t->tok_spare, cap));
+    t->spare_cap = cap;
+  }
+  uint32_t *na = t->tok_spare;
   k_compact_copy<<<blocks_for((int64_t)hw * 32), TPB, 0, t->st>>>(t->d, hw, off, na);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(t->st));
-  CK(cudaFree(t->d.tok));
-  CK(cudaFree(len));
-  CK(cudaFree(off));
+  if (cap == t->d.acap) {  // keep the old arena as the next spare
+    t->tok_spare = t->d.tok;
+  } else {
+    CK(cudaFree(t->d.tok));
+    t->tok_spare = nullptr;
+    t->spare_cap = 0;
+  }
   t->d.tok = na;
   t->d.acap = cap;
   t->hctrl->arena_top = live;
@@ -897,6 +917,9 @@ void prism_tree_destroy(prism_tree *t) {
   cudaSetDevice(t->dev);
   cudaStreamSynchronize(t->st);
   for (auto &f : slot_fields(t)) cudaFree(*f.ptr);
+  if (t->tok_spare) cudaFree(t->tok_spare);
+  if (t->cmp_len) cudaFree(t->cmp_len);
+  if (t->cmp_off) cudaFree(t->cmp_off);
   void *bufs[] = {t->d.ht,     t->d.tok,     t->d.Hk,      t->d.Hv,     t->d.vlog,    t->d.pri,
                   t->d.act,    t->d.ctrl,    t->ck,        t->cv,       t->d_count,   t->cub_tmp,
                   t->d_path,   t->d_aoff,    t->d_akind,   t->d_aseg,   t->d_asnap,   t->d_res,

@@ -560,11 +560,19 @@ struct prism_qas {
   double ms_round = 0.0;  // QAS round + serialization device time (events on q->st)
   // the fused wave's tail as a CUDA graph (prism_wave_step)
   cudaEvent_t ev_t = nullptr;
-  cudaGraphExec_t gexec = nullptr;
-  uint64_t gkey = 0, gkey_seen = 0;
+  uint64_t gkey_seen = 0;  // the last wave shape run without a graph (captured when it repeats)
+  struct GEnt {
+    uint64_t key = 0;
+    cudaGraphExec_t exec = nullptr;
+    int64_t kernels = 0, last = 0;
+  } gcache[4];
+  int64_t gtick = 0;
   int32_t use_graph = 1;
-  int64_t graph_captures = 0, graph_replays = 0, graph_kernels = 0;
+  int64_t graph_captures = 0, graph_replays = 0;
   int64_t *hres = nullptr;  // pinned: the fused wave's stage results
+  int64_t *hout_mem = nullptr, *hout_hit = nullptr;  // pinned: a wave's dispatch order and hits
+  int64_t hout_cap = 0;
+  int32_t hout_ready = 0;
 };
 
 namespace {
@@ -1023,8 +1031,11 @@ void prism_qas_destroy(prism_qas *q) {
 #undef QPTR
   for (void *p : bufs)
     if (p) cudaFree(p);
-  if (q->gexec) cudaGraphExecDestroy(q->gexec);
+  for (auto &e : q->gcache)
+    if (e.exec) cudaGraphExecDestroy(e.exec);
   if (q->hres) cudaFreeHost(q->hres);
+  if (q->hout_mem) cudaFreeHost(q->hout_mem);
+  if (q->hout_hit) cudaFreeHost(q->hout_hit);
   if (q->ev_t) cudaEventDestroy(q->ev_t);
   if (q->e0) cudaEventDestroy(q->e0);
   if (q->e1) cudaEventDestroy(q->e1);
@@ -1310,7 +1321,8 @@ namespace {
 int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, const double *arrival,
                     const int64_t *sk_off, const int32_t *sk, const uint8_t *reorderable, const int32_t *suffix,
                     int32_t nseg, const QCfg &c, int64_t sys_len, int64_t chunk, int64_t *members_out, int64_t *hits,
-                    int32_t *leaf_slots, int64_t *leaf_ids, int64_t *n_members, int64_t *n_admitted, bool *handled) {
+                    int32_t *leaf_slots, int64_t *leaf_ids, int64_t *n_members, int64_t *n_admitted, bool *handled,
+                    bool host_out) {
   *handled = false;
   cudaStream_t st = q->st;
   int64_t G = 1;
@@ -1346,6 +1358,13 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
   QCK(grow(&q->a_snap, q->a_snap_cap, 3 * nanc_cap));
   QCK(grow(&q->tok, q->tok_cap, std::max<int64_t>(P * (sys_len + 16 * chunk + 64), 1)));
   if (!q->hres) QCK(cudaMallocHost(&q->hres, 8 * sizeof(int64_t)));
+  if (host_out && q->hout_cap < P) {
+    if (q->hout_mem) cudaFreeHost(q->hout_mem);
+    if (q->hout_hit) cudaFreeHost(q->hout_hit);
+    QCK(cudaMallocHost(&q->hout_mem, sizeof(int64_t) * P));
+    QCK(cudaMallocHost(&q->hout_hit, sizeof(int64_t) * P));
+    q->hout_cap = P;
+  }
   if (!q->ev_t) QCK(cudaEventCreateWithFlags(&q->ev_t, cudaEventDisableTiming));
   if ((rc = prism_wave_commit_prepare(t, B))) return rc;
   int32_t *abort = q->err + 1;
@@ -1374,6 +1393,10 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
                                        q->goff, q->aligned, sys_len, chunk, hits, leaf_slots, leaf_ids, (void *)st,
                                        abort)))
       return r;
+    if (host_out) {  // the wave's results straight to pinned host memory (fixed buffers)
+      QCK(cudaMemcpyAsync(q->hout_mem, members, sizeof(int64_t) * B, cudaMemcpyDeviceToHost, st));
+      QCK(cudaMemcpyAsync(q->hout_hit, hits, sizeof(int64_t) * B, cudaMemcpyDeviceToHost, st));
+    }
     QCK(cudaMemcpyAsync(q->hres, q->qcounts + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     QCK(cudaMemcpyAsync(q->hres + 2, q->tmp_tot, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     QCK(cudaMemcpyAsync(q->hres + 4, q->err, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -1386,7 +1409,8 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
                           q->tok, q->a_off, q->a_kind, q->a_seg, q->a_snap, q->err, q->tmp_tot, q->qcounts, q->hres,
                           q->touched, q->tn, q->rk, q->emap, q->longl, q->sig, q->siglen, q->tkey, q->tmin,
                           q->slot_of, q->bmin, q->bstart, q->bend, q->score, q->take, q->rank, q->bucket, q->hot,
-                          q->cv2, q->pk, q->pv, q->plist};
+                          q->cv2, q->pk, q->pv, q->plist, host_out ? q->hout_mem : nullptr,
+                          host_out ? q->hout_hit : nullptr};
     const int64_t dims[] = {P, B, G, btmask, nseg, sys_len, chunk, tok_cap, anc_cap, q->pk_cap, q->pv_cap,
                             q->aligned_cap, q->rk_cap, q->emap_cap, (int64_t)q->prof_on};
     const double cw[] = {c.wg, c.wa, c.wn, c.alpha, c.beta, (double)c.budget, (double)c.cold, (double)c.front,
@@ -1398,14 +1422,21 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
     mixin(dims, sizeof(dims));
     mixin(cw, sizeof(cw));
   }
-  if (q->gexec && key == q->gkey) {
-    QCK(cudaGraphLaunch(q->gexec, st));
+  prism_qas::GEnt *hit = nullptr;
+  for (auto &e : q->gcache)
+    if (e.exec && e.key == key) hit = &e;
+  if (hit) {  // a wave of a known shape: replay
+    QCK(cudaGraphLaunch(hit->exec, st));
+    hit->last = ++q->gtick;
     q->graph_replays++;
-    q->launches += q->graph_kernels;
-  } else if (key == q->gkey_seen) {  // second wave of this shape: capture it
-    if (q->gexec) {
-      cudaGraphExecDestroy(q->gexec);
-      q->gexec = nullptr;
+    q->launches += hit->kernels;
+  } else if (key == q->gkey_seen) {  // second wave of this shape: capture it (LRU slot)
+    prism_qas::GEnt *slot = &q->gcache[0];
+    for (auto &e : q->gcache)
+      if (!e.exec || e.last < slot->last) slot = &e;
+    if (slot->exec) {
+      cudaGraphExecDestroy(slot->exec);
+      slot->exec = nullptr;
     }
     QCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
     const int r = body();
@@ -1417,18 +1448,19 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
     QCK(cudaGraphGetNodes(g, nullptr, &nn));
     std::vector<cudaGraphNode_t> nodes(nn);
     QCK(cudaGraphGetNodes(g, nodes.data(), &nn));
-    q->graph_kernels = 0;
+    slot->kernels = 0;
     for (auto nd : nodes) {
       cudaGraphNodeType ty;
       QCK(cudaGraphNodeGetType(nd, &ty));
-      q->graph_kernels += ty == cudaGraphNodeTypeKernel ? 1 : 0;
+      slot->kernels += ty == cudaGraphNodeTypeKernel ? 1 : 0;
     }
-    QCK(cudaGraphInstantiate(&q->gexec, g, 0));
+    QCK(cudaGraphInstantiate(&slot->exec, g, 0));
     cudaGraphDestroy(g);
-    q->gkey = key;
-    QCK(cudaGraphLaunch(q->gexec, st));
+    slot->key = key;
+    slot->last = ++q->gtick;
+    QCK(cudaGraphLaunch(slot->exec, st));
     q->graph_captures++;
-    q->launches += q->graph_kernels;
+    q->launches += slot->kernels;
   } else {  // first wave of this shape: plain launches
     q->gkey_seen = key;
     if ((rc = body())) return rc;
@@ -1450,6 +1482,7 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
   *n_members = B;
   if (applied) {
     *n_admitted = B;
+    q->hout_ready = host_out ? 1 : 0;  // results already in the pinned output buffers
     return PRISM_OK;
   }
   // not committed in parallel (maintenance / whole order / exactness guard):
@@ -1458,6 +1491,11 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
                                     members, q->goff, q->aligned, sys_len, chunk, q->commit_mode, hits, leaf_slots,
                                     leaf_ids, n_admitted, (void *)st);
 }
+int wave_step_impl(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, const double *arrival,
+                   const int64_t *sk_off, const int32_t *sk, const uint8_t *reorderable, const int32_t *suffix,
+                   int64_t A, const int64_t *act_off, const int32_t *act_sk, int32_t nseg,
+                   const prism_qas_config *cfg, int64_t sys_len, int64_t chunk, int64_t *members_out, int64_t *hits,
+                   int32_t *leaf_slots, int64_t *leaf_ids, int64_t *n_members, int64_t *n_admitted, bool host_out);
 }  // namespace
 
 extern "C" {
@@ -1468,6 +1506,49 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
                     const prism_qas_config *cfg, int64_t sys_len, int64_t chunk, int64_t *members_out,
                     int64_t *hits, int32_t *leaf_slots, int64_t *leaf_ids, int64_t *n_members,
                     int64_t *n_admitted) {
+  q->hout_ready = 0;
+  return wave_step_impl(t, q, P, ids, arrival, sk_off, sk, reorderable, suffix, A, act_off, act_sk, nseg, cfg,
+                        sys_len, chunk, members_out, hits, leaf_slots, leaf_ids, n_members, n_admitted, false);
+}
+
+// The fused wave from host memory to host memory: the pending arrays may be
+// pinned host buffers (read in place by the staging kernel), the previous
+// wave's pins are released first, and the dispatch order and hits land in
+// h_members / h_hits (copied inside the wave's graph to fixed pinned buffers).
+int prism_wave_step_host(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, const double *arrival,
+                         const int64_t *sk_off, const int32_t *sk, const uint8_t *reorderable, const int32_t *suffix,
+                         int32_t nseg, const prism_qas_config *cfg, int64_t sys_len, int64_t chunk,
+                         int64_t release_n, const int32_t *release_slots, int64_t *members_out, int64_t *hits,
+                         int32_t *leaf_slots, int64_t *leaf_ids, int64_t *h_members, int64_t *h_hits,
+                         int64_t *n_members, int64_t *n_admitted) {
+  cudaSetDevice(q->dev);
+  q->hout_ready = 0;
+  int rc;
+  if (release_n > 0 && (rc = prism_release_device(t, release_n, release_slots, nullptr, (void *)q->st))) return rc;
+  if ((rc = wave_step_impl(t, q, P, ids, arrival, sk_off, sk, reorderable, suffix, 0, nullptr, nullptr, nseg, cfg,
+                           sys_len, chunk, members_out, hits, leaf_slots, leaf_ids, n_members, n_admitted, true)))
+    return rc;
+  if (q->hout_ready) {
+    memcpy(h_members, q->hout_mem, sizeof(int64_t) * (size_t)*n_members);
+    memcpy(h_hits, q->hout_hit, sizeof(int64_t) * (size_t)*n_admitted);
+  } else {  // (first wave of a shape / regular path)
+    if (*n_members)
+      QCK(cudaMemcpyAsync(h_members, members_out, sizeof(int64_t) * *n_members, cudaMemcpyDeviceToHost, q->st));
+    if (*n_admitted)
+      QCK(cudaMemcpyAsync(h_hits, hits, sizeof(int64_t) * *n_admitted, cudaMemcpyDeviceToHost, q->st));
+    QCK(cudaStreamSynchronize(q->st));
+  }
+  return PRISM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+int wave_step_impl(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, const double *arrival,
+                   const int64_t *sk_off, const int32_t *sk, const uint8_t *reorderable, const int32_t *suffix,
+                   int64_t A, const int64_t *act_off, const int32_t *act_sk, int32_t nseg,
+                   const prism_qas_config *cfg, int64_t sys_len, int64_t chunk, int64_t *members_out, int64_t *hits,
+                   int32_t *leaf_slots, int64_t *leaf_ids, int64_t *n_members, int64_t *n_admitted, bool host_out) {
   if (cfg->cold_quota > cfg->dispatch_budget || cfg->signature_size < 1 ||
       cfg->front_width < cfg->signature_size || cfg->signature_size > QMAXK)
     return qfail(PRISM_INVALID, "invalid SchedulerConfig");
@@ -1481,7 +1562,7 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
       prism_tree_policy(t) == 0 && prism_tree_graphable(t)) {
     bool handled = false;
     int rc = wave_step_graph(t, q, P, ids, arrival, sk_off, sk, reorderable, suffix, nseg, c, sys_len, chunk,
-                             members_out, hits, leaf_slots, leaf_ids, n_members, n_admitted, &handled);
+                             members_out, hits, leaf_slots, leaf_ids, n_members, n_admitted, &handled, host_out);
     if (rc || handled) return rc;
   }
   if (q->prof_on) cudaEventRecord(q->e0, st);
@@ -1560,6 +1641,9 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
   }
   return qfail(PRISM_FATAL, "QAS round did not converge");
 }
+}  // namespace
+
+extern "C" {
 
 // rounds over <= max_p pending requests with integral weights run in one CTA
 // (qas_small.cuh); 0: always the multi-kernel round; 1: the default cutoff

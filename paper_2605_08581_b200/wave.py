@@ -29,6 +29,8 @@ def _bind(lib):
     sig = {
         "prism_wave_step": (C.c_int, [_p, _p, _i64, _p, _p, _p, _p, _p, _p, _i64, _p, _p, C.c_int32, _p,
                                       _i64, _i64, _p, _p, _p, _p, _p, _p]),
+        "prism_wave_step_host": (C.c_int, [_p, _p, _i64, _p, _p, _p, _p, _p, _p, C.c_int32, _p, _i64, _i64, _i64,
+                                           _p, _p, _p, _p, _p, _p, _p, _p, _p]),
         "prism_qas_stream": (_p, [_p]),
         "prism_qas_counters": (C.c_int, [_p, _p, C.c_int32]),
         "prism_set_protection_device": (C.c_int, [_p, _p, C.c_int32, _p, _p]),
@@ -132,6 +134,25 @@ class WaveEngine:
             self._act_off.data_ptr(), self._act_sk.data_ptr(), self.nseg, C.addressof(self._cfg),
             self.sys_len, self.chunk, self.members.data_ptr(), self.hits.data_ptr(), self.leaf_slots.data_ptr(),
             self.leaf_ids.data_ptr(), self._nm.ctypes.data, self._na.ctypes.data,
+        ))
+        return int(self._nm[0]), int(self._na[0])
+
+    def step_host(self, pool: dict, out_members: np.ndarray, out_hits: np.ndarray, release_n: int = 0) -> tuple[int, int]:
+        """One wave from host memory to host memory (the end-to-end entry point).
+
+        ``pool`` maps ids / arrival / sk_off / sk / reorderable / suffix to
+        pinned host tensors (read in place by the device); the previous wave's
+        ``release_n`` pins (``self.leaf_slots``) are dropped first; the dispatch
+        order and the hits come back in ``out_members`` / ``out_hits`` (int64)."""
+        P = int(pool["ids"].shape[0])
+        if P > self.members.shape[0]:
+            raise ValueError("pending set larger than the engine's dispatch buffers")
+        check(self.L.prism_wave_step_host(
+            self.t, self.q, P, pool["ids"].data_ptr(), pool["arrival"].data_ptr(), pool["sk_off"].data_ptr(),
+            pool["sk"].data_ptr(), pool["reorderable"].data_ptr(), pool["suffix"].data_ptr(), self.nseg,
+            C.addressof(self._cfg), self.sys_len, self.chunk, release_n, self.leaf_slots.data_ptr(),
+            self.members.data_ptr(), self.hits.data_ptr(), self.leaf_slots.data_ptr(), self.leaf_ids.data_ptr(),
+            out_members.ctypes.data, out_hits.ctypes.data, self._nm.ctypes.data, self._na.ctypes.data,
         ))
         return int(self._nm[0]), int(self._na[0])
 

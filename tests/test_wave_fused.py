@@ -229,3 +229,37 @@ def test_graph_replay_matches_plain_launches():
     assert o1 == o0
     assert v1 == v0
     assert d1 == d0
+
+
+def test_step_host_matches_device_step():
+    """prism_wave_step_host (pinned host inputs read in place, results copied
+    to host inside the wave, release folded in) == prism_wave_step."""
+    import torch
+
+    from paper_2605_08581_b200.wave import DevicePending, WaveEngine
+
+    dev = torch.device("cuda", 0)
+    outs = []
+    for host in (True, False):
+        rng = np.random.default_rng(13)
+        cfg = CacheConfig(capacity_tokens=200_000, policy=CachePolicy.DART, protect_budget=10)
+        eng = WaveEngine(cfg, SchedulerConfig(dispatch_budget=512, cold_quota=8), 20 + 200_000, 12, 8, device=0)
+        nid, prev, out = 0, 0, []
+        om, oh = np.empty(512, np.int64), np.empty(512, np.int64)
+        for w in range(30):
+            arrs = _mu_pool(rng, nid, 512)
+            nid += 512
+            if host:
+                names = ("ids", "arrival", "sk_off", "sk", "reorderable", "suffix")
+                pool = {k: torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for k, a in zip(names, arrs)}
+                nm, na = eng.step_host(pool, om, oh, release_n=prev)
+                out.append((om[:nm].tolist(), oh[:na].tolist(), eng.leaf_ids[:na].cpu().tolist()))
+            else:
+                eng.release(eng.leaf_slots, prev)
+                nm, na = eng.step(DevicePending.from_host(*arrs, dev))
+                out.append((eng.members[:nm].cpu().tolist(), eng.hits[:na].cpu().tolist(),
+                            eng.leaf_ids[:na].cpu().tolist()))
+            prev = na
+        outs.append((out, eng.cache_view().victim_log()))
+        eng.close()
+    assert outs[0] == outs[1]
