@@ -456,23 +456,6 @@ __device__ inline void bitonic_smem(Key3 *sk, uint64_t *sv, int m) {
   }
 }
 
-__device__ inline void bitonic_keys(Key3 *sk, int m) {
-  for (int size = 2; size <= m; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      const int lg = __ffs(stride) - 1;
-      for (int p = threadIdx.x; p < (m >> 1); p += blockDim.x) {
-        const int i = ((p >> lg) << (lg + 1)) | (p & (stride - 1)), j = i + stride;
-        const bool up = (i & size) == 0;
-        if (up ? key_less(sk[j], sk[i]) : key_less(sk[i], sk[j])) {
-          const Key3 tk = sk[i];
-          sk[i] = sk[j];
-          sk[j] = tk;
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
 
 // exclusive scan of a[0..n) in shared memory, returns the total
 __device__ inline unsigned long long block_exscan_u64(unsigned long long *a, int n, unsigned long long *warp_tot) {
@@ -535,77 +518,6 @@ __device__ inline unsigned long long block_reserve(unsigned c, unsigned long lon
   const unsigned long long pos = *s_base + s_w[wid] + (x - c);
   __syncthreads();
   return pos;
-}
-
-// ascending rank sort of n unique keys (+ values) in shared memory, written to
-// (ko, vo) -- items are ranked against all keys (broadcast reads, no
-// barriers), with tpi = blockDim / n threads (a power of two <= 32) per item
-// splitting the comparisons; for the small sets of the sample select
-__device__ inline void block_rank_sort(const Key3 *k, const uint64_t *v, int n, Key3 *ko, uint64_t *vo) {
-  int tpi = 1;
-  while (tpi < 32 && 2 * tpi * n <= (int)blockDim.x) tpi <<= 1;
-  const int sub = threadIdx.x & (tpi - 1);
-  const int per = (int)blockDim.x / tpi;
-  for (int i0 = 0; i0 < n; i0 += per) {  // uniform trip count (shuffles below)
-    const int i = i0 + (int)threadIdx.x / tpi;
-    const bool ok = i < n;
-    const Key3 x = ok ? k[i] : Key3{0, 0, 0};
-    int r = 0;
-    if (ok) {
-#pragma unroll 4
-      for (int j = sub; j < n; j += tpi) r += key_less(k[j], x) ? 1 : 0;
-    }
-    for (int o = 1; o < tpi; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-    if (ok && sub == 0) {
-      ko[r] = x;
-      if (vo) vo[r] = v[i];
-    }
-  }
-}
-
-// ascending bitonic sort of blockDim.x (a power of two) items held one per
-// thread: thread t ends with the t-th smallest.  Strides below 32 exchange by
-// warp shuffles, larger ones through (sx, sv) in shared memory.
-__device__ inline void block_sort_reg(Key3 &key, uint64_t &val, Key3 *sx, uint64_t *svx) {
-  const int tid = threadIdx.x, N = blockDim.x;
-  for (int size = 2; size <= N; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      Key3 pk;
-      uint64_t pv;
-      if (stride >= 32) {
-        sx[tid] = key;
-        svx[tid] = val;
-        __syncthreads();
-        pk = sx[tid ^ stride];
-        pv = svx[tid ^ stride];
-        __syncthreads();
-      } else {
-        pk = shfl_key(key, stride);
-        pv = __shfl_xor_sync(0xffffffffu, val, stride);
-      }
-      const bool up = (tid & size) == 0, lower = (tid & stride) == 0;
-      const bool pless = key_less(pk, key);
-      if ((lower == up) ? pless : (!pless && key_less(key, pk))) {
-        key = pk;
-        val = pv;
-      }
-    }
-  }
-}
-
-// sort n <= blockDim.x keys (+ values) from (k, v) into (ko, vo) with the
-// register bitonic sort (ko/vo may alias k/v; sx/svx: blockDim.x scratch)
-__device__ inline void block_sort_small(const Key3 *k, const uint64_t *v, int n, Key3 *ko, uint64_t *vo, Key3 *sx,
-                                        uint64_t *svx) {
-  Key3 key = threadIdx.x < n ? k[threadIdx.x] : Key3{~0ull, ~0ull, ~0ull};
-  uint64_t val = (threadIdx.x < n && v) ? v[threadIdx.x] : 0ull;
-  __syncthreads();
-  block_sort_reg(key, val, sx, svx);
-  if (threadIdx.x < n) {
-    ko[threadIdx.x] = key;
-    if (vo) vo[threadIdx.x] = val;
-  }
-  __syncthreads();
 }
 
 // ascending sort of n unique keys (+ values) in shared memory: chunks of

@@ -258,22 +258,6 @@ __global__ void k_wp_hits(DT T, WaveIn W, WaveTmp X) {
   X.miss[j] = n - hit;
 }
 
-// eviction stream prefix: token length of each list entry; misc[1] = first
-// entry that a member's pin or guard would make non-evictable (list entries
-// with children are fine: the stream puts every descendant first)
-__global__ void k_wp_vlen(DT T, WaveTmp X, const WaveCtl *wc) {
-  if (wc->stop || wc->W < 0) return;
-  const int64_t Tn = T.ctrl->L_n;
-  const uint32_t epoch = wc->epoch;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Tn; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t v = T.Lv[i];
-    const int32_t s = (int32_t)(v & 0xffffffffu);
-    const bool valid = T.kver[s] == (uint32_t)(v >> 32) && T.nid[s] >= 0 && T.par[s] >= 0 && T.ref[s] == 0;
-    X.vlen[i] = valid ? T.elen[s] : 0;
-    if (!valid || T.wchild[s] == epoch) atomicMin((unsigned long long *)&X.misc[1], (unsigned long long)i);
-  }
-}
-
 // per member: number of list entries consumed through member j (first F >= D_j)
 __global__ void k_wp_cuts(DT T, int64_t B, WaveTmp X, const WaveCtl *wc) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -616,27 +600,8 @@ __global__ void k_wc_finalize(DT T, int64_t B, WaveTmp X, const WaveCtl *wc) {
   C->H_n = 0;
 }
 
-// inclusive scan of in[0..n) -> out with n read on the device (*dn), three
-// launches: per-block sums, a scan of the sums, per-block rescans; skipped
-// when skip && (*skip < 0 || stop)
+// device-sized scans: k_dscan_b scans the per-block sums of k_vscan_a (below)
 constexpr int DS_BLOCKS = 296;
-__global__ void __launch_bounds__(256) k_dscan_a(const int64_t *in, const int64_t *dn, int64_t *part,
-                                                 const WaveCtl *wc) {
-  if (wc && (wc->stop || wc->W < 0)) return;
-  const int64_t n = *dn, per = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t b0 = blockIdx.x * per, b1 = b0 + per < n ? b0 + per : n;
-  int64_t s = 0;
-  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) s += in[i];
-  __shared__ int64_t sw[8];
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t t = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += sw[w];
-    part[blockIdx.x] = t;
-  }
-}
 
 __global__ void __launch_bounds__(1024) k_dscan_b(int64_t *part, int nparts, const WaveCtl *wc) {
   if (wc && (wc->stop || wc->W < 0)) return;
@@ -653,33 +618,6 @@ __global__ void __launch_bounds__(1024) k_dscan_b(int64_t *part, int nparts, con
   if (i < nparts) part[i] = s[i] - (i < nparts ? part[i] : 0);  // exclusive
 }
 
-__global__ void __launch_bounds__(256) k_dscan_c(const int64_t *in, const int64_t *dn, const int64_t *part,
-                                                 int64_t *out, const WaveCtl *wc) {
-  if (wc && (wc->stop || wc->W < 0)) return;
-  __shared__ int64_t sw[8];
-  __shared__ int64_t carry;
-  const int64_t n = *dn, per = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t b0 = blockIdx.x * per, b1 = b0 + per < n ? b0 + per : n;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = part[blockIdx.x];
-  __syncthreads();
-  for (int64_t t0 = b0; t0 < b1; t0 += blockDim.x) {
-    const int64_t i = t0 + threadIdx.x;
-    int64_t x = i < b1 ? in[i] : 0;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) sw[wid] = x;
-    __syncthreads();
-    int64_t before = carry;
-    for (int w = 0; w < wid; w++) before += sw[w];
-    if (i < b1) out[i] = before + x;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = before + x;
-    __syncthreads();
-  }
-}
 
 
 // the eviction stream's token lengths fused into the device-sized scan: entry
