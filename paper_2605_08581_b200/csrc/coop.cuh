@@ -1370,48 +1370,62 @@ __global__ void __launch_bounds__(SS_TPB) k_tf_local(CoopBufs B, int64_t f) {
 }
 
 // one CTA: the f smallest of the per-slice winners -> T.Lk/Lv[0..f), ss_ok.
-// Every slice holding f items bounds the answer by its f-th smallest key, so
-// only the winners up to the smallest such bound are gathered and sorted.
+// The slices' sorted top-f lists are merged pairwise in a tree: an item's
+// place in the merge of lists A and B is its index plus its rank in the other
+// list (a binary search over f), and only places < f are kept.
 __global__ void __launch_bounds__(SS_SEL_TPB) k_tf_merge(DT T, CoopBufs B, int64_t f) {
   extern __shared__ __align__(16) unsigned char dsm[];
-  __shared__ Key3 smin[33], smax[33];
-  __shared__ int s_n;
   const int64_t n = (int64_t)B.st->tf_n;
   if (n < f || f <= 0) return;  // ss_ok stays 0: the materialising path decides
-  const int64_t nsl = (n + TF_SLICE - 1) / TF_SLICE;
-  Key3 *sk = reinterpret_cast<Key3 *>(dsm);
-  uint64_t *sv = reinterpret_cast<uint64_t *>(sk + TF_MERGE_MAX);
-  Key3 *tk = reinterpret_cast<Key3 *>(sv + TF_MERGE_MAX);
-  uint64_t *tv = reinterpret_cast<uint64_t *>(tk + TF_MERGE_MAX);
-  // the bound: the smallest f-th key over the slices (padding keys are maximal)
-  Key3 lo = {~0ull, ~0ull, ~0ull}, hi = {0, 0, 0};
-  for (int64_t c = threadIdx.x; c < nsl; c += blockDim.x) {
-    const Key3 x = B.ks[c * f + f - 1];
-    if (key_less(x, lo)) lo = x;
+  const int nsl = (int)((n + TF_SLICE - 1) / TF_SLICE);
+  const int F = (int)f;
+  if ((int64_t)nsl * F > TF_MERGE_MAX) return;  // too many lists for one CTA: the materialising path
+  Key3 *ak = reinterpret_cast<Key3 *>(dsm);
+  uint64_t *av = reinterpret_cast<uint64_t *>(ak + TF_MERGE_MAX);
+  Key3 *bk = reinterpret_cast<Key3 *>(av + TF_MERGE_MAX);
+  uint64_t *bv = reinterpret_cast<uint64_t *>(bk + TF_MERGE_MAX);
+  for (int i = threadIdx.x; i < nsl * F; i += blockDim.x) {
+    ak[i] = B.ks[i];
+    av[i] = B.vs[i];
   }
-  block_minmax(lo, hi, smin, smax, &smin[32], &smax[32]);
-  const Key3 bound = smin[32];
-  if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
-  bool ovf = false;
-  for (int64_t i = threadIdx.x; i < nsl * f; i += blockDim.x) {
-    const Key3 x = B.ks[i];
-    if (!key_less(bound, x)) {  // x <= bound
-      const int p = atomicAdd(&s_n, 1);
-      if (p < TF_MERGE_MAX) {
-        sk[p] = x;
-        sv[p] = B.vs[i];
-      } else {
-        ovf = true;
+  int L = nsl;
+  while (L > 1) {
+    const int pairs = L >> 1;
+    for (int t = threadIdx.x; t < pairs * 2 * F; t += blockDim.x) {
+      const int p = t / (2 * F), side = (t / F) & 1, i = t % F;
+      const Key3 *A = ak + (2 * p) * F, *Bl = ak + (2 * p + 1) * F;
+      const Key3 x = side ? Bl[i] : A[i];
+      const Key3 *O = side ? A : Bl;  // the other list
+      int lo = 0, hi = F;  // A's items go before equal B items (stable)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (side ? !key_less(x, O[mid]) : key_less(O[mid], x)) lo = mid + 1;
+        else hi = mid;
+      }
+      const int pos = i + lo;
+      if (pos < F) {
+        bk[p * F + pos] = x;
+        bv[p * F + pos] = side ? av[(2 * p + 1) * F + i] : av[(2 * p) * F + i];
       }
     }
+    if (L & 1)
+      for (int i = threadIdx.x; i < F; i += blockDim.x) {
+        bk[pairs * F + i] = ak[(L - 1) * F + i];
+        bv[pairs * F + i] = av[(L - 1) * F + i];
+      }
+    __syncthreads();
+    Key3 *tk = ak;
+    ak = bk;
+    bk = tk;
+    uint64_t *tv = av;
+    av = bv;
+    bv = tv;
+    L = pairs + (L & 1);
   }
-  if (__syncthreads_or(ovf)) return;  // (ss_ok stays 0)
-  const int m = s_n;
-  block_merge_sort(sk, sv, m, tk, tv, sk, sv);
-  for (int i = threadIdx.x; i < f; i += blockDim.x) {
-    T.Lk[i] = sk[i];
-    T.Lv[i] = sv[i];
+  for (int i = threadIdx.x; i < F; i += blockDim.x) {
+    T.Lk[i] = ak[i];
+    T.Lv[i] = av[i];
   }
   if (threadIdx.x == 0) B.st->ss_ok = 1;
 }
