@@ -530,6 +530,11 @@ int run_commit(prism_tree *t, CommitArgs a) {
     CK(cudaFuncSetAttribute(k_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)COMMIT_SMEM));
     attr_set = true;
   }
+  // a rebuild that made no progress (the prefix held only entries the stopped
+  // call may not evict, e.g. its own guarded path) is retried with a doubled
+  // prefix, then the whole order: any prefix gives the same victims
+  int64_t last_hint = -1, last_freed = -1, lastW = 0;
+  int stalls = 0;
   for (int iter = 0; iter < 1000000; iter++) {
     prof_begin(t);
     k_commit<<<1, 32, COMMIT_SMEM, t->st>>>(t->d, a);
@@ -546,11 +551,19 @@ int run_commit(prism_tree *t, CommitArgs a) {
       case ST_CAPACITY:
         return PRISM_OK;
       case ST_NEED_BUILD:
-      case ST_NEED_REBUILD:
+      case ST_NEED_REBUILD: {
         // a prefix of the eviction order with 4x the tokens the stopped call
         // still needs; a call that exhausts it resumes after a rebuild
-        rc = build_list(t, std::max<int64_t>(4 * c.need_hint, t->list_min_tokens));
+        int64_t W = std::max<int64_t>(4 * c.need_hint, t->list_min_tokens);
+        const bool stalled = c.status == ST_NEED_REBUILD && c.need_hint == last_hint && c.resume_freed == last_freed;
+        stalls = stalled ? stalls + 1 : 0;
+        if (stalls) W = stalls > 8 || lastW <= 0 ? 0 : std::max(W, 2 * lastW);
+        last_hint = c.need_hint;
+        last_freed = c.resume_freed;
+        lastW = W;
+        rc = build_list(t, W);
         break;
+      }
       case ST_NEED_SLOTS:
         rc = grow_slots(t, (int64_t)c.hw + 2 + MAX_ANCH);
         break;
