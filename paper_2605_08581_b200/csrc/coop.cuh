@@ -1315,18 +1315,68 @@ __global__ void __launch_bounds__(SS_TPB) k_tf_scan(ProtCand cand, CoopBufs B) {
   const int lane = threadIdx.x & 31;
   const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
   unsigned long long ccount = 0;
+  const DT &T = cand.T;
+  const int32_t pol = T.policy;
+  // ProtCand's visit, restated so that every load of the UNR slots is issued
+  // before the first store (stores to prot / kw / eff would otherwise order
+  // the next slot's loads behind them: one memory round trip per slot)
   for (int64_t s0 = (int64_t)blockIdx.x * blockDim.x; s0 < hw; s0 += UNR * gsz) {
+    int64_t nid[UNR], last[UNR];
+    int32_t par[UNR], ref[UNR], seg[UNR], hits[UNR];
+    uint8_t kind[UNR], ha[UNR], ak[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+      const int64_t s = s0 + u * gsz + threadIdx.x;
+      const bool in = s < hw;
+      nid[u] = in ? __ldg(&T.nid[s]) : -1;
+      par[u] = in ? __ldg(&T.par[s]) : -1;
+      seg[u] = in ? __ldg(&T.seg[s]) : SEG_NONE;
+      ha[u] = in ? __ldg(&T.hasanc[s]) : 0;
+      ak[u] = in ? __ldg(&T.akind[s]) : 0;
+      if (cand.keys) {
+        ref[u] = in ? __ldg(&T.ref[s]) : 0;
+        kind[u] = in ? __ldg(&T.kind[s]) : 0;
+        last[u] = in ? __ldg(&T.last[s]) : 0;
+        hits[u] = (in && pol == P_LFU) ? __ldg(&T.hits[s]) : 0;
+      }
+    }
+    double ps[UNR];
+    bool act[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+      const int32_t sg = seg[u];
+      ps[u] = (sg != SEG_NONE && sg >= 0 && sg < T.npri) ? __ldg(&T.pri[sg]) : 0.0;
+      act[u] = cand.keys && pol == P_LRU_ACTIVE && act_of(T, sg);
+    }
     Key3 k[UNR];
-    uint64_t v[UNR];
     bool pos[UNR];
     unsigned nt = 0;
 #pragma unroll
     for (int u = 0; u < UNR; u++) {
       const int64_t s = s0 + u * gsz + threadIdx.x;
-      int64_t w = 0;
-      const bool c = s < hw && cand((int32_t)s, k[u], v[u], w);
+      pos[u] = false;
+      if (s >= hw) continue;
+      T.prot[s] = 0;
+      const bool live = s != ROOT && nid[u] >= 0 && par[u] >= 0;
+      if (cand.keys) {
+        if (!live) {
+          T.eff[s] = EFF_DEAD;
+        } else {
+          const bool blocked = ref[u] > 0 || (pol == P_DART && kind[u] == K_SYSTEM);
+          T.kw[s] = make_key_v(pol, last[u], nid[u], kind[u], false, ps[u], hits[u], act[u]);
+          T.eff[s] = blocked ? EFF_BLOCKED : (int32_t)s;
+        }
+      }
+      const bool c = live && ha[u] && ak[u] == K_REUSABLE;
       ccount += c ? 1 : 0;
-      pos[u] = c && pri_of(cand.T, cand.T.seg[(int32_t)s]) > 0.0;
+      if (c) {
+        const int32_t sv = seg[u] == SEG_NONE ? -1 : seg[u];
+        k[u] = {0, 0, 0};
+        shl_or(k[u], 64, ord_f64(-ps[u]));
+        shl_or(k[u], 32, (uint64_t)((uint32_t)sv ^ 0x80000000u));
+        shl_or(k[u], 40, (uint64_t)nid[u] & ((1ull << 40) - 1));
+      }
+      pos[u] = c && ps[u] > 0.0;
       nt += pos[u] ? 1 : 0;
     }
     unsigned long long p = block_reserve(nt, &B.st->tf_n, s_w, &s_base);
@@ -1334,7 +1384,7 @@ __global__ void __launch_bounds__(SS_TPB) k_tf_scan(ProtCand cand, CoopBufs B) {
     for (int u = 0; u < UNR; u++)
       if (pos[u]) {
         B.k1[p] = k[u];
-        B.v1[p] = v[u];
+        B.v1[p] = (uint64_t)(uint32_t)(s0 + u * gsz + threadIdx.x);
         p++;
       }
   }

@@ -210,34 +210,46 @@ __device__ inline double pri_of(const DT &T, int32_t s) {
 //   LRU        (last:40, id:40)
 //   LFU        (hits:32, last:40, id:40)
 //   LRU_ACTIVE (active:1, last:40, id:40)
-__device__ inline Key3 make_key(const DT &T, int32_t s) {
+// the packing from already-loaded fields (pseg: P-hat of the node's segment,
+// act: its LRU_ACTIVE flag; each read only by its policy)
+__device__ inline Key3 make_key_v(int32_t policy, int64_t last_, int64_t nid, int kind, bool prot, double pseg,
+                                  int32_t hits, bool act) {
   Key3 k = {0, 0, 0};
-  const uint64_t last = (uint64_t)T.last[s] & ((1ull << 40) - 1);
-  const uint64_t id = (uint64_t)T.nid[s] & ((1ull << 40) - 1);
-  switch (T.policy) {
+  const uint64_t last = (uint64_t)last_ & ((1ull << 40) - 1);
+  const uint64_t id = (uint64_t)nid & ((1ull << 40) - 1);
+  switch (policy) {
     case P_DART: {
-      const int kd = T.kind[s];
-      uint32_t cls = (kd == K_PRIVATE) ? 0u : (T.prot[s] ? 2u : 1u);
-      double p = cls == 1u ? pri_of(T, T.seg[s]) : 0.0;
+      uint32_t cls = (kind == K_PRIVATE) ? 0u : (prot ? 2u : 1u);
+      double p = cls == 1u ? pseg : 0.0;
       shl_or(k, 2, cls);
       shl_or(k, 64, ord_f64(p));
       break;
     }
     case P_LFU:
-      shl_or(k, 32, (uint64_t)(uint32_t)T.hits[s]);
+      shl_or(k, 32, (uint64_t)(uint32_t)hits);
       break;
-    case P_LRU_ACTIVE: {
-      int32_t sg = T.seg[s];
-      uint64_t a = (sg != SEG_NONE && sg >= 0 && sg < T.nact && T.act[sg]) ? 1 : 0;
-      shl_or(k, 1, a);
+    case P_LRU_ACTIVE:
+      shl_or(k, 1, act ? 1ull : 0ull);
       break;
-    }
     default:
       break;
   }
   shl_or(k, 40, last);
   shl_or(k, 40, id);
   return k;
+}
+
+__device__ inline bool act_of(const DT &T, int32_t sg) {
+  return sg != SEG_NONE && sg >= 0 && sg < T.nact && T.act[sg];
+}
+
+__device__ inline Key3 make_key(const DT &T, int32_t s) {
+  const int32_t p = T.policy;
+  const int32_t sg = (p == P_DART || p == P_LRU_ACTIVE) ? T.seg[s] : SEG_NONE;
+  const int kd = p == P_DART ? (int)T.kind[s] : 0;
+  const bool pr = p == P_DART && kd != K_PRIVATE && T.prot[s];
+  return make_key_v(p, T.last[s], T.nid[s], kd, pr, (p == P_DART && kd != K_PRIVATE && !pr) ? pri_of(T, sg) : 0.0,
+                    p == P_LFU ? T.hits[s] : 0, p == P_LRU_ACTIVE && act_of(T, sg));
 }
 
 // bits used by the eviction sort key: policy key + 32-bit depth tiebreak
