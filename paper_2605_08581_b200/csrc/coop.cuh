@@ -527,8 +527,96 @@ __device__ inline unsigned long long block_reserve(unsigned c, unsigned long lon
 // compares instead of the O(n^2) of a plain rank sort, two barriers instead of
 // the O(log^2 n) of a bitonic network.
 constexpr int MS_CH = 64;
+
+__device__ __forceinline__ Key3 shfl_xor_key(const Key3 &x, int m) {
+  return {__shfl_xor_sync(0xffffffffu, x.w0, m), __shfl_xor_sync(0xffffffffu, x.w1, m),
+          __shfl_xor_sync(0xffffffffu, x.w2, m)};
+}
+
+// Shared-memory sort of (k, v)[0..n) into (ko, vo) (ko may be global memory or
+// alias k; k / v and the scratch tk / tv are clobbered; v null: keys only):
+// every warp sorts 32-key runs in registers (bitonic over shuffles), then
+// log2(n / 32) rounds merge run pairs -- an item's place is its index in its
+// run plus its rank in the partner run (binary search; equal keys of the left
+// run first), so every round is one barrier and no item waits on another.
+__device__ inline void block_sort(Key3 *k, uint64_t *v, int n, Key3 *tk, uint64_t *tv, Key3 *ko, uint64_t *vo) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r0 = 0; r0 < n; r0 += 32 * nw) {
+    const int i = r0 + wid * 32 + lane;
+    const bool in = i < n;
+    Key3 x = in ? k[i] : Key3{~0ull, ~0ull, ~0ull};
+    uint64_t vx = (in && v) ? v[i] : 0ull;
+    for (int size = 2; size <= 32; size <<= 1) {
+      for (int j = size >> 1; j > 0; j >>= 1) {
+        const Key3 y = shfl_xor_key(x, j);
+        const uint64_t vy = __shfl_xor_sync(0xffffffffu, vx, j);
+        const bool take_min = ((lane & j) == 0) == ((lane & size) == 0);
+        if (take_min ? key_less(y, x) : key_less(x, y)) {
+          x = y;
+          vx = vy;
+        }
+      }
+    }
+    if (in) {
+      k[i] = x;
+      if (v) v[i] = vx;
+    }
+  }
+  __syncthreads();
+  Key3 *src = k, *dst = tk;
+  uint64_t *vsrc = v, *vdst = tv;
+  for (int w = 32; w < n; w <<= 1) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int r = i / w, os = r * w;
+      const Key3 x = src[i];
+      int pos = i;
+      if ((r & 1) == 0) {  // left run: keys of the right run strictly below x
+        int lo = os + w, hi = min(os + 2 * w, n);
+        const int base = lo;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (key_less(src[mid], x)) lo = mid + 1;
+          else hi = mid;
+        }
+        pos = i + (lo - base);
+      } else {  // right run: keys of the left run at most x
+        int lo = os - w, hi = os;
+        const int base = lo;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (!key_less(x, src[mid])) lo = mid + 1;
+          else hi = mid;
+        }
+        pos = base + (i - os) + (lo - base);
+      }
+      dst[pos] = x;
+      if (v) vdst[pos] = vsrc[i];
+    }
+    __syncthreads();
+    Key3 *t = src;
+    src = dst;
+    dst = t;
+    uint64_t *tt = vsrc;
+    vsrc = vdst;
+    vdst = tt;
+  }
+  if (src != ko) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      ko[i] = src[i];
+      if (vo) vo[i] = v ? vsrc[i] : 0ull;
+    }
+  } else if (vo && !v) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) vo[i] = 0ull;
+  }
+  __syncthreads();
+}
+
 __device__ inline void block_merge_sort(const Key3 *k, const uint64_t *v, int n, Key3 *tk, uint64_t *tv, Key3 *ko,
                                         uint64_t *vo) {
+  if (n > MS_CH) {  // (every caller's input is shared-memory scratch it may lose)
+    block_sort(const_cast<Key3 *>(k), const_cast<uint64_t *>(v), n, tk, tv, ko, vo);
+    return;
+  }
   const int nch = (n + MS_CH - 1) / MS_CH;
   int tpi = 1;  // threads per item (a power of two <= 8): small sets use the whole block
   while (tpi < 8 && 2 * tpi * n <= (int)blockDim.x) tpi <<= 1;
