@@ -1084,21 +1084,25 @@ __global__ void __launch_bounds__(SS_SEL_TPB) k_ss_select(Cand cand, CoopBufs B,
     const Key3 tau = fk[s_misc[3]];
     // splitters: every sample <= tau (warp-aggregated appends)
     bool ovf = false;
-    for (int i0 = 0; i0 < ns; i0 += blockDim.x) {
-      const int i = i0 + threadIdx.x;
-      Key3 k = {0, 0, 0};
-      bool t = false;
-      if (i < ns) {
-        k = B.k1[i];
-        t = !key_less(tau, k);
+    constexpr int SPU = 4;  // sample loads in flight per thread
+    for (int i0 = 0; i0 < ns; i0 += SPU * blockDim.x) {
+      Key3 k[SPU];
+#pragma unroll
+      for (int u = 0; u < SPU; u++) {
+        const int i = i0 + u * blockDim.x + threadIdx.x;
+        k[u] = i < ns ? B.k1[i] : tau;
       }
-      const unsigned mt = __ballot_sync(0xffffffffu, t);
-      int p = 0;
-      if (lane == 0 && mt) p = atomicAdd(&s_nsel, __popc(mt));
-      p = __shfl_sync(0xffffffffu, p, 0) + __popc(mt & ((1u << lane) - 1u));
-      if (t) {
-        if (p < SS_SPL) selk[p] = k;
-        else ovf = true;
+#pragma unroll
+      for (int u = 0; u < SPU; u++) {
+        const bool t = i0 + u * (int)blockDim.x + (int)threadIdx.x < ns && !key_less(tau, k[u]);
+        const unsigned mt = __ballot_sync(0xffffffffu, t);
+        int p = 0;
+        if (lane == 0 && mt) p = atomicAdd(&s_nsel, __popc(mt));
+        p = __shfl_sync(0xffffffffu, p, 0) + __popc(mt & ((1u << lane) - 1u));
+        if (t) {
+          if (p < SS_SPL) selk[p] = k[u];
+          else ovf = true;
+        }
       }
     }
     if (__syncthreads_or(ovf)) fail = 3;
