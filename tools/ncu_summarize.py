@@ -20,7 +20,7 @@ PHASE = [  # (phase, kernel-name substrings); first match wins
     ("protect", ("k_prot_", "k_protect_coop", "<prism::ProtCand>", "k_tf_")),
     ("build", ("k_build_keys", "k_propagate", "k_gather", "k_list_ready", "k_build_coop", "<prism::EvictCand>")),
     ("select", ("k_ss_",)),  # shared sample-select kernels (build and protection)
-    ("commit", ("k_wp_", "k_wc_", "k_dscan_", "k_commit")),
+    ("commit", ("k_wp_", "k_wc_", "k_dscan_", "k_vscan_", "k_commit")),
     ("prematch", ("k_prematch",)),
     ("release", ("k_release",)),
     ("qas", ("k_qas_small", "q_")),
