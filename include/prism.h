@@ -154,8 +154,11 @@ int prism_last_op(prism_tree *t, int64_t *out);
 int64_t prism_compactions(prism_tree *t);
 /* Sizing of the selected eviction-order prefix: key 0 = minimum tokens for
  * the ordered commit (default 2^18), 1 = slack tokens for the parallel
- * commit (4096), 2 = candidate count below which all are sorted (4096).
- * Semantics do not depend on them (exhausted prefixes are rebuilt). */
+ * commit (4096), 2 = candidate count below which all are sorted (4096),
+ * 3 = cooperative build/protection kernels (1), 4 = sample select (1),
+ * 5 = fused wave: subtree maxima + sample of the order on the protection
+ * stream (1).  Semantics do not depend on them (exhausted prefixes are
+ * rebuilt). */
 int prism_tune(prism_tree *t, int32_t key, int64_t value);
 /* Phase timeline of the last cooperative eviction-list build (diagnostics):
  * out[0..*n) %globaltimer ns stamps, out[39] = selected-prefix size. */

@@ -1027,7 +1027,9 @@ __global__ void __launch_bounds__(SS_SEL_TPB) k_ss_select(Cand cand, CoopBufs B,
   coop_mark(st);
   const double mq = (double)m * q;
   long long need = nsub > 0 ? (long long)(((double)W * 1.25 + 3.0 * mq * ((double)tot / nsub)) / mq) + 1 : 1;
-  int fail = (nsub == 0 || (unsigned long long)need > tot) ? 1 : 0;  // (nearly) everything: sort it all
+  // (nearly) everything, or the whole order asked for (W <= 0; a sample taken
+  // ahead of W, see prebuild_order): sort it all
+  int fail = (W <= 0 || nsub == 0 || (unsigned long long)need > tot) ? 1 : 0;
   int nU = nsub;
   const int *cur = nullptr;  // null: the undecided set is in the flags
   Key3 gmin, gmax;

@@ -70,6 +70,7 @@ struct prism_tree {
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;  // caller stream <-> tree stream (graph-capturable)
   int aux_pending = 0;
   int keys_fresh = 0;  // the protection pass left the eviction keys (k_build_keys not needed)
+  int prebuilt = 0;    // ... and the subtree maxima + the sample of the order (prebuild_order)
   DT d{};
   Ctrl *hctrl = nullptr;  // pinned
   int64_t protect_budget = 0;
@@ -140,6 +141,7 @@ struct prism_tree {
   int64_t sel_min_candidates = 4096;   // below this many candidates, sort them all
   int64_t use_coop = 1;                // cooperative single-kernel build / protection
   int64_t use_sample = 1;              // sample select before the materialising selection
+  int64_t prebuild = 1;                // fused wave: subtree maxima + sample on the auxiliary stream
 };
 
 enum { PH_COMMIT = 0, PH_BUILD = 1, PH_PROTECT = 2, PH_PREMATCH = 3, PH_RELEASE = 4, PH_NOTE = 5, PH_MAINT = 6 };
@@ -171,6 +173,7 @@ inline void join_aux(prism_tree *t) {
 inline void api_enter(prism_tree *t) {
   join_aux(t);
   t->keys_fresh = 0;
+  t->prebuilt = 0;
 }
 
 // ----------------------------------------------------------------- slot arrays
@@ -364,7 +367,8 @@ int coop_grid(prism_tree *t) {
 
 // the sample-select launches (coop.cuh) ahead of the cooperative finaliser
 template <class Cand>
-int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const int64_t *dW, int64_t min_cand) {
+int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const int64_t *dW, int64_t min_cand,
+                  bool sampled_already = false) {
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(k_ss_select<EvictCand>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SEL_SMEM));
@@ -376,7 +380,7 @@ int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const 
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev));
   cudaStream_t st = t->st;
-  k_ss_sample<Cand><<<SS_SAMP / SS_TPB, SS_TPB, 0, st>>>(cand, B, W, dW, min_cand);
+  if (!sampled_already) k_ss_sample<Cand><<<SS_SAMP / SS_TPB, SS_TPB, 0, st>>>(cand, B, W, dW, min_cand);
   k_ss_select<Cand><<<1, SS_SEL_TPB, SS_SEL_SMEM, st>>>(cand, B, W, dW);
   k_ss_filter<Cand><<<4 * sms, SS_TPB, SS_FILTER_SMEM, st>>>(cand, B);
   k_ss_scatter<<<2 * sms, SS_TPB, 0, st>>>(B, W, dW);
@@ -401,18 +405,24 @@ int build_list(prism_tree *t, int64_t W, const int64_t *dW = nullptr) {
     int grid = coop_grid(t);
     if (grid < 0) return PRISM_FATAL;
     prof_begin(t);
-    CK(cudaMemsetAsync(t->cst, 0, offsetof(CoopState, ts), t->st));
-    // keys / subtree maxima / gather at full occupancy over the slot range
-    // (each reads hw from the control block; the count lands in cst->cand)
+    // the fused wave's build may find the subtree maxima and the sample
+    // already taken on the auxiliary stream (prebuild_order)
+    const bool pre = t->prebuilt && dW != nullptr;
+    t->prebuilt = 0;
     const int64_t S = t->d.S;
-    if (!t->keys_fresh) k_build_keys<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1, dW);
+    if (!pre) {
+      CK(cudaMemsetAsync(t->cst, 0, offsetof(CoopState, ts), t->st));
+      // keys / subtree maxima / gather at full occupancy over the slot range
+      // (each reads hw from the control block; the count lands in cst->cand)
+      if (!t->keys_fresh) k_build_keys<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1, dW);
+      k_propagate<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1, dW);
+    }
     t->keys_fresh = 0;  // consumed (the commit mutates the tree next)
-    k_propagate<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1, dW);
     CoopBufs B = coop_bufs(t);
     int64_t minc = t->sel_min_candidates, small = std::min<int64_t>(SEL_SMALL, t->sel_min_candidates);
     int32_t sampled = (t->use_sample && (dW || W > 0)) ? 1 : 0;
     if (sampled) {
-      int rc = sample_select(t, EvictCand{t->d}, B, W, dW, minc);
+      int rc = sample_select(t, EvictCand{t->d}, B, W, dW, minc, pre);
       if (rc) return rc;
     }
     void *args[] = {(void *)&t->d, (void *)&B, (void *)&W, (void *)&dW, (void *)&minc, (void *)&small,
@@ -1203,6 +1213,24 @@ int prism_set_protection_device(prism_tree *t, const double *d_pri, int32_t nseg
   return prism_set_protection_device_impl(t, d_pri, nseg, out_ids, n_out);
 }
 
+// The first launches of the next eviction-order build, on the auxiliary
+// stream right after the protection pass that left the keys: subtree maxima
+// and the sample of the order.  Neither needs the wave's eviction demand W
+// (k_ss_select, on the tree stream, gives the whole order when W <= 0), and
+// the tree stream's commit plan in the meantime only reads the tree, so the
+// two overlap.  The build of the same fused wave picks them up (t->prebuilt).
+static int prebuild_order(prism_tree *t) {
+  CK(cudaMemsetAsync(t->cst, 0, offsetof(CoopState, ts), t->st));
+  k_propagate<<<blocks_for(t->d.S), TPB, 0, t->st>>>(t->d, -1, nullptr);
+  CoopBufs B = coop_bufs(t);
+  k_ss_sample<EvictCand><<<SS_SAMP / SS_TPB, SS_TPB, 0, t->st>>>(EvictCand{t->d}, B, 1, nullptr,
+                                                                   t->sel_min_candidates);
+  CK(cudaGetLastError());
+  t->launches[PH_BUILD] += 2;
+  t->prebuilt = 1;
+  return PRISM_OK;
+}
+
 // set_protection from a dense device P-hat array, on the auxiliary stream:
 // ordered after the tree stream's work so far, joined by the tree stream
 // before the next eviction-order build or API call (join_aux)
@@ -1215,6 +1243,7 @@ int prism_set_protection_device_async(prism_tree *t, const double *d_pri, int32_
   // the pass over every node also leaves the eviction keys (cooperative path)
   const int32_t keys = t->use_coop ? 1 : 0;
   int rc = prism_set_protection_device_impl(t, d_pri, nseg, nullptr, nullptr, keys);
+  if (!rc && keys && t->use_sample && t->prebuild) rc = prebuild_order(t);
   std::swap(t->st, t->st_aux);
   if (rc) return rc;
   CK(cudaEventRecord(t->ev_aux, t->st_aux));
@@ -1677,6 +1706,7 @@ int prism_tune(prism_tree *t, int32_t key, int64_t value) {
     case 2: t->sel_min_candidates = std::max<int64_t>(value, 0); break;
     case 3: t->use_coop = value ? 1 : 0; break;
     case 4: t->use_sample = value ? 1 : 0; break;
+    case 5: t->prebuild = value ? 1 : 0; break;
     default: return fail(PRISM_INVALID, "unknown tunable");
   }
   return PRISM_OK;

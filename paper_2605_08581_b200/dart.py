@@ -213,7 +213,7 @@ class DeviceRadixCache:
         self._dirty()
 
     TUNABLES = {"list_min_tokens": 0, "list_slack_tokens": 1, "sel_min_candidates": 2, "use_coop": 3,
-                "use_sample": 4}
+                "use_sample": 4, "prebuild": 5}
 
     def tune(self, **kw) -> None:
         """Eviction-list prefix sizing (semantics-free; tests force tiny prefixes)."""

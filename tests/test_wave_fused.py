@@ -56,7 +56,7 @@ def _pending_arrays(reqs):
 
 
 def run_case(seed, policy, mode, nseg=40, hot=6, kmin=2, kmax=5, suffixes=(2, 4), sys=8, chunk=4, cap=600,
-             wave=24, nwaves=8, protect=3, cold=2, tiny=False, coop=1, sample=1, reo=1.0):
+             wave=24, nwaves=8, protect=3, cold=2, tiny=False, coop=1, sample=1, reo=1.0, prebuild=1):
     import torch
 
     from paper_2605_08581_b200.wave import DevicePending, WaveEngine
@@ -66,7 +66,7 @@ def run_case(seed, policy, mode, nseg=40, hot=6, kmin=2, kmax=5, suffixes=(2, 4)
     scfg = SchedulerConfig(dispatch_budget=wave, cold_quota=cold)
     eng = WaveEngine(cfg, scfg, nseg, sys, chunk, device=0)
     eng.set_commit_mode(mode)
-    eng.tune(use_coop=coop, use_sample=sample)
+    eng.tune(use_coop=coop, use_sample=sample, prebuild=prebuild)
     if tiny:  # minimal selected prefixes of the eviction order
         eng.tune(list_min_tokens=1, list_slack_tokens=0, sel_min_candidates=0)
     ora = OracleRadixCache(cfg)
@@ -144,6 +144,9 @@ def test_ordered_commit_matches_oracle(policy):
     dict(coop=0, tiny=True),
     dict(sample=0),                                    # materialising radix selection only
     dict(sample=0, tiny=True),
+    dict(prebuild=0),                                  # whole build on the tree stream
+    dict(prebuild=0, tiny=True),
+    dict(cap=100_000, nwaves=4, tiny=True),            # sample taken ahead, no eviction demand
     dict(reo=0.0),                                     # non-reorderable skeletons (no front-alignment)
     dict(reo=0.5, kmin=1, kmax=6),                     # mixed
     dict(nseg=300, hot=8, kmin=20, kmax=40, suffixes=(0, 8), wave=16, nwaves=6, cap=6000),  # agent-like deep paths
@@ -174,11 +177,11 @@ def test_sampled_selection_at_scale(protect):
 
     dev = torch.device("cuda", 0)
     runs = []
-    for sample in (1, 0):
+    for sample, pre in ((1, 1), (0, 0), (1, 0)):
         rng = np.random.default_rng(5)
         cfg = CacheConfig(capacity_tokens=1_000_000, policy=CachePolicy.DART, protect_budget=protect)
         eng = WaveEngine(cfg, SchedulerConfig(dispatch_budget=2048, cold_quota=16), 20 + 200_000, 12, 8, device=0)
-        eng.tune(use_sample=sample)
+        eng.tune(use_sample=sample, prebuild=pre)
         nid, prev, out, sampled = 0, 0, [], 0
         for w in range(30):
             pend = DevicePending.from_host(*_mu_pool(rng, nid, 2048), dev)
@@ -191,12 +194,12 @@ def test_sampled_selection_at_scale(protect):
         view = eng.cache_view()
         runs.append((out, view.victim_log(), view.debug_nodes(), eng.stats()["live_nodes"], sampled))
         eng.close()
-    (o1, v1, d1, n1, s1), (o0, v0, d0, n0, s0) = runs
+    (o1, v1, d1, n1, s1), (o0, v0, d0, n0, s0), (o2, v2, d2, n2, s2) = runs
     assert n1 > 100_000 and len(v1) > 10_000
-    assert s1 > 0 and s0 == 0  # the sampled path ran (and only where enabled)
-    assert o1 == o0
-    assert v1 == v0
-    assert d1 == d0
+    assert s1 > 0 and s2 > 0 and s0 == 0  # the sampled path ran (and only where enabled)
+    assert o1 == o0 == o2
+    assert v1 == v0 == v2
+    assert d1 == d0 == d2
 
 
 def test_graph_replay_matches_plain_launches():
