@@ -316,6 +316,33 @@ __device__ inline int qs_warp_reserve(int c, int32_t *ctr) {
   return __shfl_sync(0xffffffffu, base, 31) + x - c;
 }
 
+// qs_warp_reserve for a whole CTA (one counter atomic per CTA instead of per
+// warp: every warp of a sweep appending hammers one address); block-uniform
+__device__ inline int qs_block_reserve(int c, int32_t *ctr) {
+  __shared__ int s_w[33];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int t = lane < nw ? s_w[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nw) s_w[lane] = t;  // inclusive per-warp prefix
+    if (lane == 31) s_w[32] = t ? atomicAdd(ctr, t) : 0;
+  }
+  __syncthreads();
+  const int r = s_w[32] + (wid ? s_w[wid - 1] : 0) + x - c;
+  __syncthreads();  // (s_w reused by the next call)
+  return r;
+}
+
 // cold lane (242-245) in block 0: the nc smallest leftovers by (arrival, id),
 // sorted.  Leftovers are compacted into shared memory; when fewer than all of
 // them are taken, an MSB-first byte radix select over the 128-bit keys finds
@@ -483,7 +510,7 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
       unsigned long long *f = (unsigned long long *)&A.prio[s];
       nt = __ldcg(f) == 0ull && atomicCAS(f, 0ull, 0xFFF0000000000001ull) == 0ull;
     }
-    const int p = qs_warp_reserve(nt ? 1 : 0, &A.touched_n[0]);
+    const int p = qs_block_reserve(nt ? 1 : 0, &A.touched_n[0]);
     if (nt) A.touched[p] = s;
   }
   for (int pass = 1; pass < 2; pass++) {  // active set: one thread per request
@@ -509,15 +536,7 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
           }
         });
       }
-      const int lane = tid & 31;
-      int x = nn;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      int base = 0;
-      if (lane == 31 && x) base = atomicAdd(&A.touched_n[0], x);
-      base = __shfl_sync(0xffffffffu, base, 31) + x - nn;
+      const int base = qs_block_reserve(nn, &A.touched_n[0]);
       for (int q = 0; q < nn; q++) A.touched[base + q] = newt[q];
     }
   }
@@ -640,13 +659,14 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
 #pragma unroll
     for (int u = 0; u < IPT; u++) {
       const int64_t i = (int64_t)tid * IPT + u;
-      key[u] = i < P ? (unsigned)sbk[first[u]] : (unsigned)QS_MAXP;  // padding sorts last
+      key[u] = i < P ? (unsigned)sbk[first[u]] : (unsigned)nb;  // padding (bucket id nb) sorts last
       val[u] = (unsigned)i;
     }
     __syncthreads();
     static_assert(sizeof(typename BRS::TempStorage) <= sizeof(QKey) * QS_MAXP, "radix-sort storage");
     typename BRS::TempStorage &ts = *reinterpret_cast<typename BRS::TempStorage *>(sk);
-    BRS(ts).Sort(key, val, 0, 13);  // stable: pending order inside a bucket (ids < 2^13)
+    // stable: pending order inside a bucket; only the bits of ids <= nb
+    BRS(ts).Sort(key, val, 0, 32 - __clz(nb > 0 ? nb : 1));
     __syncthreads();
     // thread tid now holds sorted positions tid*IPT + u; sv: the sorted keys
 #pragma unroll
@@ -708,7 +728,7 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
         if (np) atomicAdd(&A.nsegs[bk], 1);
       }
     }
-    const int p = qs_warp_reserve(np ? 1 : 0, (int32_t *)&A.counts[5]);  // (low word of the zeroed int64)
+    const int p = qs_block_reserve(np ? 1 : 0, (int32_t *)&A.counts[5]);  // (low word of the zeroed int64)
     if (np) A.plist[p] = npos;
   }
   qs_gsync();
@@ -770,12 +790,17 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   // 10. hot lane, and n_disp of its members (247-248)
   for (int64_t i0 = 0; i0 < P; i0 += gs) {
     const int64_t i = i0 + qs_ilv(gs);
-    if (i >= P) continue;
-    const int32_t b = A.bucket[i];
-    const bool h = A.rank[i] < qs_ld(&A.nsegs[b]);
-    A.bidx[i] = h ? 1 : 0;  // reuse: hot flag
-    if (h) A.hot[(int64_t)__ldcg((const unsigned long long *)&A.isum[b]) + A.rank[i]] = i;
-    else A.longl[atomicAdd((unsigned long long *)&A.counts[6], 1ull)] = (int32_t)i;  // leftover (cold lane)
+    bool lf = false;
+    if (i < P) {
+      const int32_t b = A.bucket[i];
+      const bool h = A.rank[i] < qs_ld(&A.nsegs[b]);
+      A.bidx[i] = h ? 1 : 0;  // reuse: hot flag
+      if (h) A.hot[(int64_t)__ldcg((const unsigned long long *)&A.isum[b]) + A.rank[i]] = i;
+      lf = !h;
+    }
+    // leftovers (cold lane), one counter atomic per CTA (low word of the zeroed int64)
+    const int p = qs_block_reserve(lf ? 1 : 0, (int32_t *)&A.counts[6]);
+    if (lf) A.longl[p] = (int32_t)i;
   }
   for (int64_t e = gt; e < nsk; e += gs) {  // n_disp of the hot members: one thread per skeleton entry
     const int64_t i = A.emap[e];
