@@ -49,6 +49,7 @@ struct CoopState {
   unsigned int ss_off[SS_SPL + 4];  // bucket offsets
   int ss_ok;                    // the sample select produced the sorted prefix
   unsigned long long tf_n;      // top-f protection: candidates with a positive P-hat
+  int tf_done;                  // top-f protection applied by k_tf_merge (k_protect_coop returns)
   unsigned long long ss_dbg[24];
   unsigned long long ss_prof[8];  // diagnostics: k_ss_sort clock64 sums (load, sort, buckets, items)  // diagnostics: [0] max bucket, [1] rounds, [2+3r..] (undecided, selected, shift)
   int ss_nb;                    // diagnostics: splitters of the last sample select
@@ -1517,7 +1518,7 @@ __global__ void __launch_bounds__(SS_TPB) k_tf_local(CoopBufs B, int64_t f) {
 // The slices' sorted top-f lists are merged pairwise in a tree: an item's
 // place in the merge of lists A and B is its index plus its rank in the other
 // list (a binary search over f), and only places < f are kept.
-__global__ void __launch_bounds__(SS_SEL_TPB) k_tf_merge(DT T, CoopBufs B, int64_t f) {
+__global__ void __launch_bounds__(SS_SEL_TPB) k_tf_merge(DT T, CoopBufs B, int64_t f, int32_t keys) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const int64_t n = (int64_t)B.st->tf_n;
   if (n < f || f <= 0) return;  // ss_ok stays 0: the materialising path decides
@@ -1571,7 +1572,19 @@ __global__ void __launch_bounds__(SS_SEL_TPB) k_tf_merge(DT T, CoopBufs B, int64
     T.Lk[i] = ak[i];
     T.Lv[i] = av[i];
   }
-  if (threadIdx.x == 0) B.st->ss_ok = 1;
+  __syncthreads();
+  // and k_protect_coop's last step (f <= n here), so that launch returns at once
+  for (int i = threadIdx.x; i < F; i += blockDim.x) {
+    const int32_t s = (int32_t)(av[i] & 0xffffffffu);
+    T.prot[s] = 1;
+    if (keys) T.kw[s] = make_key(T, s);  // protected: class 2 (kvcache.py:405-406)
+    if (B.out_ids) B.out_ids[i] = T.nid[s];
+  }
+  if (threadIdx.x == 0) {
+    B.st->ss_ok = 1;
+    B.st->prot_n = F;
+    B.st->tf_done = 1;
+  }
 }
 
 // set_protection (kvcache.py:364-383): top-f reusable anchors by (-P-hat, seg
@@ -1580,6 +1593,7 @@ __global__ void __launch_bounds__(COOP_TPB) k_protect_coop(DT T, CoopBufs B, int
                                                            int64_t small, int32_t sampled, int32_t keys) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ Key3 smin[COOP_TPB + 1], smax[COOP_TPB + 1];
+  if (sampled && B.st->tf_done) return;  // the small top-f path already protected
   cg::grid_group grid = cg::this_grid();
   const int32_t hw = T.ctrl->hw;
   const int64_t gsz = (int64_t)gridDim.x * blockDim.x;

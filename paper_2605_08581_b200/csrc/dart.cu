@@ -1111,7 +1111,7 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out, int3
       }
       k_tf_scan<<<4 * sms, SS_TPB, 0, t->st>>>(ProtCand{t->d, keys}, B);
       k_tf_local<<<2 * sms, SS_TPB, TF_SMEM, t->st>>>(B, ff);
-      k_tf_merge<<<1, SS_SEL_TPB, TF_MERGE_SMEM, t->st>>>(t->d, B, ff);
+      k_tf_merge<<<1, SS_SEL_TPB, TF_MERGE_SMEM, t->st>>>(t->d, B, ff, keys);
       CK(cudaGetLastError());
       t->launches[PH_PROTECT] += 3;
     } else if (sampled) {
