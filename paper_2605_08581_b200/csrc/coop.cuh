@@ -941,7 +941,7 @@ constexpr int SS_TPB = 256;
 constexpr int SS_SEL_TPB = 512;
 constexpr int SS_BMAX = 1024;  // buckets up to this size: k_ss_sort (merge sort, several CTAs per SM)
 constexpr int SS_BBIG = CHUNK; // larger ones up to this: k_ss_sort_big (in-place bitonic); beyond: fallback
-constexpr int SS_SUB = 2048;  // sub-sample the selection rounds run on
+constexpr int SS_SUB = 1024;  // sub-sample the selection rounds run on
 constexpr size_t SS_SEL_SMEM =
     2 * sizeof(Key3) * SS_SPL + 8 * SS_U + 2 * (sizeof(Key3) + 8) * SS_SEL_TPB + (sizeof(Key3) + 9) * SS_SUB;
 constexpr size_t SS_FILTER_SMEM = sizeof(Key3) * SS_SPL + 4 * SS_SPL;
