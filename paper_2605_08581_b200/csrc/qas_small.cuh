@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   // and the touched list (prio's bit pattern doubles as the "listed" flag)
   // pending: one thread per skeleton entry (all probes of a request in flight)
   for (int64_t e0 = 0; e0 < nsk; e0 += gs) {
-    const int64_t e = e0 + gt;
+    const int64_t e = e0 + qs_ilv(gs);
     int32_t s = 0;
     bool nt = false;
     if (e < nsk && qs_first(A.sk, A.off[A.emap[e]], e, s)) {
@@ -698,7 +698,7 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   // 7. distinct (bucket, segment) pairs; provisional = first hot_cap members (146-171)
   const int64_t hot_cap = c.budget - c.cold;
   for (int64_t e0 = 0; e0 < nsk; e0 += gs) {  // one thread per skeleton entry
-    const int64_t e = e0 + gt;
+    const int64_t e = e0 + qs_ilv(gs);
     int32_t s = 0, bk = 0;
     bool np = false;
     int32_t npos = 0;
@@ -733,29 +733,33 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   }
   qs_gsync();
   QS_TS(5);
-  // 8. utility terms of the distinct pairs, summed exactly (integral weights)
+  // 8. utility terms of the distinct pairs, summed exactly (integral weights):
+  // per-CTA partial sums per bucket in shared memory (exact 64-bit integer
+  // adds), then one global add per bucket and CTA (hot buckets collect many
+  // pairs, in any order of the pair list)
   const int64_t npairs = (int64_t)__ldcg((const unsigned long long *)&A.counts[5]);
-  for (int64_t t0 = 0; t0 < npairs; t0 += gs) {  // warp-combined per bucket (hot buckets collect many pairs)
-    const int64_t t = t0 + gt;
-    int32_t bk = -1 - (int32_t)(tid & 31);
-    unsigned long long v = 0;
-    if (t < npairs) {
-      const int32_t pos = A.plist[t];
-      const uint64_t key = __ldcg((const unsigned long long *)&A.ptab_key[pos]);
-      bk = (int32_t)(key >> 32);
-      const int32_t s = (int32_t)(key & 0xffffffffu);
-      const double t1 = __dmul_rn(c.wg, (double)A.g[s]);
-      const double t2 = __dmul_rn(c.wa, (double)A.a[s]);
-      const double t3 = __dmul_rn(c.wn, (double)qs_ld(&A.ptab_cnt[pos]));
-      v = (unsigned long long)(long long)__dadd_rn(__dadd_rn(t1, t2), t3);
+  {
+    const int32_t nbk = (int32_t)__ldcg((const unsigned long long *)&A.counts[2]);
+    unsigned long long *lsum = reinterpret_cast<unsigned long long *>(sk);  // [nbk <= QS_MAXP]
+    for (int q = tid; q < nbk; q += blockDim.x) lsum[q] = 0ull;
+    __syncthreads();
+    for (int64_t t0 = 0; t0 < npairs; t0 += gs) {
+      const int64_t t = t0 + gt;
+      if (t < npairs) {
+        const int32_t pos = A.plist[t];
+        const uint64_t key = __ldcg((const unsigned long long *)&A.ptab_key[pos]);
+        const int32_t bk = (int32_t)(key >> 32);
+        const int32_t s = (int32_t)(key & 0xffffffffu);
+        const double t1 = __dmul_rn(c.wg, (double)A.g[s]);
+        const double t2 = __dmul_rn(c.wa, (double)A.a[s]);
+        const double t3 = __dmul_rn(c.wn, (double)qs_ld(&A.ptab_cnt[pos]));
+        atomicAdd(&lsum[bk], (unsigned long long)(long long)__dadd_rn(__dadd_rn(t1, t2), t3));
+      }
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, bk);
-    // exact 64-bit sum over the peers from three 24/24/16-bit partial sums
-    const unsigned long long s0 = __reduce_add_sync(peers, (unsigned)(v & 0xFFFFFFull));
-    const unsigned long long s1 = __reduce_add_sync(peers, (unsigned)((v >> 24) & 0xFFFFFFull));
-    const unsigned long long s2 = __reduce_add_sync(peers, (unsigned)(v >> 48));
-    if (t < npairs && (int)(tid & 31) == __ffs(peers) - 1)
-      atomicAdd((unsigned long long *)&A.isum[bk], s0 + (s1 << 24) + (s2 << 48));
+    __syncthreads();
+    for (int q = tid; q < nbk; q += blockDim.x)
+      if (lsum[q]) atomicAdd((unsigned long long *)&A.isum[q], lsum[q]);
+    __syncthreads();  // (sk is block 0's scratch in the next phase)
   }
   qs_gsync();
   QS_TS(6);
