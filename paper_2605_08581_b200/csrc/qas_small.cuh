@@ -806,7 +806,9 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
     const int p = qs_block_reserve(lf ? 1 : 0, (int32_t *)&A.counts[6]);
     if (lf) A.longl[p] = (int32_t)i;
   }
-  for (int64_t e = gt; e < nsk; e += gs) {  // n_disp of the hot members: one thread per skeleton entry
+  for (int64_t e0 = 0; e0 < nsk; e0 += gs) {  // n_disp of the hot members: one thread per skeleton entry
+    const int64_t e = e0 + qs_ilv(gs);
+    if (e >= nsk) continue;
     const int64_t i = A.emap[e];
     const int32_t b = A.bucket[i];
     int32_t s = 0;
@@ -824,7 +826,9 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   QS_TS(9);
   // 12. priorities over the domain (249-251)
   const int32_t ntouch = qs_ld(&A.touched_n[0]);
-  for (int64_t i = gt; i < ntouch; i += gs) {
+  for (int64_t i0 = 0; i0 < ntouch; i0 += gs) {
+    const int64_t i = i0 + qs_ilv(gs);
+    if (i >= ntouch) continue;
     const int32_t s = A.touched[i];
     const int32_t g = A.g[s], a = A.a[s], n = qs_ld(&A.nd[s]);
     const bool in = g > 0 || a > 0 || n > 0;
