@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
     const int gl = tid & 15, gb = tid & 16;  // lane in the group, the group's first lane in the warp
     const int64_t ng = gs >> 4;
     for (int64_t g0 = 0; g0 < P; g0 += ng) {
-      const int64_t i = g0 + (gt >> 4);
+      const int64_t i = g0 + (int64_t)(tid >> 4) * gridDim.x + blockIdx.x;  // groups interleaved over the CTAs
       const bool vi = i < P;
       const int64_t b = vi ? A.off[i] : 0;
       const int k = vi ? (int)(A.off[i + 1] - b) : 0;
