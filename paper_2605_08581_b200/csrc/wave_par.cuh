@@ -495,16 +495,19 @@ __global__ void k_wc_begin(DT T, WaveCtl *wc, const int32_t *abort) {
 // exclusive scans cnew -> idb, tail -> arb (B + 1 entries) and the inclusive
 // scan miss -> dem (B entries), one CTA
 __global__ void __launch_bounds__(1024) k_wp_scan3(int64_t B, WaveTmp X) {
-  // three single-sequence scans (one at a time keeps the tile in registers)
-  block_scan4<1, 8>(
-      B + 1, [&](int, int64_t i) -> int64_t { return i < B ? X.cnew[i] : 0; },
-      [&](int, int64_t i, int64_t ex, int64_t) { X.idb[i] = ex; });
-  block_scan4<1, 8>(
-      B + 1, [&](int, int64_t i) -> int64_t { return i < B ? X.tail[i] : 0; },
-      [&](int, int64_t i, int64_t ex, int64_t) { X.arb[i] = ex; });
-  block_scan4<1, 8>(
-      B, [&](int, int64_t i) -> int64_t { return X.miss[i]; },
-      [&](int, int64_t i, int64_t, int64_t in) { X.dem[i] = in; });
+  // the three scans in one pass (one load round trip; B + 1 <= 5 * 1024 items
+  // make a single tile at the bench's wave size)
+  block_scan4<3, 5>(
+      B + 1,
+      [&](int a, int64_t i) -> int64_t {
+        if (i >= B) return 0;
+        return a == 0 ? X.cnew[i] : (a == 1 ? X.tail[i] : X.miss[i]);
+      },
+      [&](int a, int64_t i, int64_t ex, int64_t in) {
+        if (a == 0) X.idb[i] = ex;
+        else if (a == 1) X.arb[i] = ex;
+        else if (i < B) X.dem[i] = in;
+      });
 }
 
 // plan verdict: fallback flags, capacity headroom (slots, arena, child table),
