@@ -683,19 +683,14 @@ int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *lea
   WaveCtl *wc = t->wc;
   int rc;
   prof_begin(t);
-  CK(cudaMemsetAsync(X.lt_key, 0xFF, sizeof(uint64_t) * (size_t)t->wx_lt, st));
-  CK(cudaMemsetAsync(X.lt_min, 0x7F, sizeof(int32_t) * (size_t)t->wx_lt, st));
-  CK(cudaMemsetAsync(X.flags, 0, sizeof(int32_t), st));
-  CK(cudaMemsetAsync(X.misc, 0, sizeof(int64_t) * 8, st));
-  CK(cudaMemsetAsync(X.misc + 1, 0x7F, sizeof(int64_t), st));  // poison index: "none"
-  k_wc_begin<<<1, 1, 0, st>>>(t->d, wc, abort);
+  k_wc_begin<<<(int)std::min<int64_t>(std::max<int64_t>((t->wx_lt + 255) / 256, 1), 4 * sms), 256, 0, st>>>(
+      t->d, wc, abort, X, t->wx_lt);
   k_wp_plan<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_levels<<<blocks_for(B * WP_PL), TPB, 0, st>>>(W, X);
   k_wp_hits<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X);
-  k_wp_scan3<<<1, 1024, 0, st>>>(B, X);
-  k_wc_plan<<<1, 1, 0, st>>>(t->d, B, X, wc, t->list_slack_tokens, force_full);
+  k_wp_scan3<<<1, 1024, 0, st>>>(t->d, B, X, wc, t->list_slack_tokens, force_full);  // + the plan verdict
   CK(cudaGetLastError());
-  t->launches[PH_COMMIT] += 6;
+  t->launches[PH_COMMIT] += 5;
   prof_end(t, PH_COMMIT);
   const int64_t *dW = &wc->W;
   if (t->use_coop) {

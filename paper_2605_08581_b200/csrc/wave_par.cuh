@@ -474,7 +474,17 @@ __global__ void k_wp_label(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc, int64_t
 // ------------------------------------------------------------ device-side control
 
 // epoch + control-block snapshot the wave commits from
-__global__ void k_wc_begin(DT T, WaveCtl *wc, const int32_t *abort) {
+__global__ void k_wc_begin(DT T, WaveCtl *wc, const int32_t *abort, WaveTmp X, int64_t nlt) {
+  // the wave's scratch: empty level table, flags, device scalars (misc[1]:
+  // the poison index "none")
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nlt; i += (int64_t)gridDim.x * blockDim.x) {
+    X.lt_key[i] = ~0ull;
+    X.lt_min[i] = 0x7F7F7F7F;
+  }
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  *X.flags = 0;
+  for (int q = 0; q < 8; q++) X.misc[q] = 0;
+  X.misc[1] = 0x7F7F7F7F7F7F7F7Fll;
   Ctrl *C = T.ctrl;
   C->epoch++;
   WaveCtl w{};
@@ -494,25 +504,9 @@ __global__ void k_wc_begin(DT T, WaveCtl *wc, const int32_t *abort) {
 
 // exclusive scans cnew -> idb, tail -> arb (B + 1 entries) and the inclusive
 // scan miss -> dem (B entries), one CTA
-__global__ void __launch_bounds__(1024) k_wp_scan3(int64_t B, WaveTmp X) {
-  // the three scans in one pass (one load round trip; B + 1 <= 5 * 1024 items
-  // make a single tile at the bench's wave size)
-  block_scan4<3, 5>(
-      B + 1,
-      [&](int a, int64_t i) -> int64_t {
-        if (i >= B) return 0;
-        return a == 0 ? X.cnew[i] : (a == 1 ? X.tail[i] : X.miss[i]);
-      },
-      [&](int a, int64_t i, int64_t ex, int64_t in) {
-        if (a == 0) X.idb[i] = ex;
-        else if (a == 1) X.arb[i] = ex;
-        else if (i < B) X.dem[i] = in;
-      });
-}
-
 // plan verdict: fallback flags, capacity headroom (slots, arena, child table),
 // and the eviction demand -> the prefix of the order to select (-1: none)
-__global__ void k_wc_plan(DT T, int64_t B, WaveTmp X, WaveCtl *wc, int64_t slack, int32_t force_full) {
+__device__ inline void wc_plan_body(DT T, int64_t B, WaveTmp X, WaveCtl *wc, int64_t slack, int32_t force_full) {
   if (wc->stop) {  // aborted before the plan
     wc->W = -1;
     return;
@@ -538,6 +532,26 @@ __global__ void k_wc_plan(DT T, int64_t B, WaveTmp X, WaveCtl *wc, int64_t slack
   const int64_t D = wc->R0 + nmiss - T.capacity;
   wc->W = D > 0 ? (force_full ? 0 : D + D / 4 + slack) : -1;
 }
+
+__global__ void __launch_bounds__(1024) k_wp_scan3(DT T, int64_t B, WaveTmp X, WaveCtl *wc, int64_t slack,
+                                                  int32_t force_full) {
+  // the three scans in one pass (one load round trip; B + 1 <= 5 * 1024 items
+  // make a single tile at the bench's wave size)
+  block_scan4<3, 5>(
+      B + 1,
+      [&](int a, int64_t i) -> int64_t {
+        if (i >= B) return 0;
+        return a == 0 ? X.cnew[i] : (a == 1 ? X.tail[i] : X.miss[i]);
+      },
+      [&](int a, int64_t i, int64_t ex, int64_t in) {
+        if (a == 0) X.idb[i] = ex;
+        else if (a == 1) X.arb[i] = ex;
+        else if (i < B) X.dem[i] = in;
+      });
+  // and the plan verdict (block_scan4 ends on a barrier: the sums are visible)
+  if (threadIdx.x == 0) wc_plan_body(T, B, X, wc, slack, force_full);
+}
+
 
 // the victims: nv = entries consumed through the last member, checks that the
 // prefix sufficed and that no consumed entry is pinned/guarded; the number of
