@@ -690,9 +690,10 @@ int qas_small_prepare(prism_qas *q, int64_t P, int32_t nseg, const QCfg &c, int6
 }
 
 // the one-launch round itself (capturable): counters reset, the kernel
-int qas_small_launch(prism_qas *q, const QIn &in, int64_t P, int64_t A, int64_t bt_mask, const QCfg &c, int64_t G) {
+int qas_small_launch(prism_qas *q, const QIn &in, int64_t P, int64_t A, int64_t bt_mask, const QCfg &c, int64_t G,
+                     bool zeroed = false) {
   cudaStream_t st = q->st;
-  QCK(cudaMemsetAsync(q->qcounts, 0, 8 * sizeof(int64_t), st));
+  if (!zeroed) QCK(cudaMemsetAsync(q->qcounts, 0, 8 * sizeof(int64_t), st));
   qsmall::QsArgs qa{};
   qa.P = P;
   qa.A = A;
@@ -1138,7 +1139,8 @@ __global__ void q_stage(int64_t P, const int64_t *__restrict__ ids, const double
                         const int64_t *__restrict__ off, const int32_t *__restrict__ sk,
                         const uint8_t *__restrict__ reo, const int32_t *__restrict__ sfx, int64_t *__restrict__ gids,
                         double *__restrict__ garr, int64_t *__restrict__ goff, int32_t *__restrict__ gsk,
-                        uint8_t *__restrict__ greo, int32_t *__restrict__ gsfx, int64_t skcap, int32_t *abort) {
+                        uint8_t *__restrict__ greo, int32_t *__restrict__ gsfx, int64_t skcap, int32_t *abort,
+                        int64_t *__restrict__ qcounts, int32_t *__restrict__ err0) {
   const int64_t nsk = off[P];
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = gt; i <= P; i += gs) {
@@ -1152,7 +1154,12 @@ __global__ void q_stage(int64_t P, const int64_t *__restrict__ ids, const double
   }
   const int64_t n = nsk < skcap ? nsk : skcap;
   for (int64_t e = gt; e < n; e += gs) gsk[e] = sk[e];
-  if (gt == 0) *abort = nsk > skcap ? 1 : 0;
+  if (gt == 0) {
+    *abort = nsk > skcap ? 1 : 0;
+    // the wave graph's counters (no memset nodes in the graph)
+    for (int q = 0; q < 8; q++) qcounts[q] = 0;
+    *err0 = 0;
+  }
 }
 
 // the fused wave's stage verdict: the one-launch round overflowed (redo), the
@@ -1369,15 +1376,14 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
   if ((rc = prism_wave_commit_prepare(t, B))) return rc;
   int32_t *abort = q->err + 1;
   q_stage<<<nblk(P * 8), TPB, 0, st>>>(P, ids, arrival, sk_off, sk, reorderable, suffix, q->gids, q->garr, q->goff,
-                                       q->gsk, q->greo, q->gsfx, q->gsk_cap, abort);
+                                       q->gsk, q->greo, q->gsfx, q->gsk_cap, abort, q->qcounts, q->err);
   QCK(cudaGetLastError());
   const QIn gin{q->gids, q->garr, q->goff, q->gsk, q->greo, nullptr, nullptr};
   const int64_t btmask = qas_small_btmask(P);
   const int64_t tok_cap = q->tok_cap, anc_cap = std::min(q->a_off_cap, q->a_snap_cap / 3);
   auto body = [&]() -> int {
     int r;
-    if ((r = qas_small_launch(q, gin, P, 0, btmask, c, G))) return r;
-    QCK(cudaMemsetAsync(q->err, 0, sizeof(int32_t), st));
+    if ((r = qas_small_launch(q, gin, P, 0, btmask, c, G, true))) return r;  // (q_stage zeroed the counters)
     q_members_len<<<nblk(B), TPB, 0, st>>>(nh, nc, q->hot, q->cv2, q->gids, q->goff, q->gsfx, sys_len, chunk,
                                            members, q->plen, q->alen, q->err);
     q_scan2<<<1, 1024, 0, st>>>(B, q->plen, q->alen, q->poff, q->aoffs, q->tmp_tot);
