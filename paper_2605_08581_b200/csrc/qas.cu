@@ -1162,6 +1162,29 @@ __global__ void q_stage(int64_t P, const int64_t *__restrict__ ids, const double
   }
 }
 
+// the wave graph's results straight into pinned host memory (one kernel node
+// instead of a copy node per array): the round's counters and verdicts, and
+// (host entry) the dispatch order and hits
+__global__ void q_results(const int64_t *__restrict__ qcounts, const int64_t *__restrict__ tot,
+                          const int32_t *__restrict__ err, int64_t *hres, int64_t B,
+                          const int64_t *__restrict__ members, const int64_t *__restrict__ hits, int64_t *hm,
+                          int64_t *hh) {
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+  if (gt == 0) {
+    hres[0] = qcounts[2];
+    hres[1] = qcounts[3];
+    hres[2] = tot[0];
+    hres[3] = tot[1];
+    reinterpret_cast<int32_t *>(hres + 4)[0] = err[0];
+    reinterpret_cast<int32_t *>(hres + 4)[1] = err[1];
+  }
+  if (hm)
+    for (int64_t i = gt; i < B; i += gs) {
+      hm[i] = members[i];
+      hh[i] = hits[i];
+    }
+}
+
 // the fused wave's stage verdict: the one-launch round overflowed (redo), the
 // layout check failed, or the paths / anchors exceed the serialization buffers
 __global__ void q_capcheck(const int64_t *__restrict__ qcounts, const int64_t *__restrict__ tot, int64_t tok_cap,
@@ -1399,13 +1422,10 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
                                        q->goff, q->aligned, sys_len, chunk, hits, leaf_slots, leaf_ids, (void *)st,
                                        abort)))
       return r;
-    if (host_out) {  // the wave's results straight to pinned host memory (fixed buffers)
-      QCK(cudaMemcpyAsync(q->hout_mem, members, sizeof(int64_t) * B, cudaMemcpyDeviceToHost, st));
-      QCK(cudaMemcpyAsync(q->hout_hit, hits, sizeof(int64_t) * B, cudaMemcpyDeviceToHost, st));
-    }
-    QCK(cudaMemcpyAsync(q->hres, q->qcounts + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    QCK(cudaMemcpyAsync(q->hres + 2, q->tmp_tot, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    QCK(cudaMemcpyAsync(q->hres + 4, q->err, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    // the wave's results straight to pinned host memory (fixed buffers, mapped)
+    q_results<<<host_out ? 32 : 1, TPB, 0, st>>>(q->qcounts, q->tmp_tot, q->err, q->hres, B, members, hits,
+                                                 host_out ? q->hout_mem : nullptr, host_out ? q->hout_hit : nullptr);
+    QCK(cudaGetLastError());
     return PRISM_OK;
   };
   uint64_t key = prism_wave_commit_key(t);
