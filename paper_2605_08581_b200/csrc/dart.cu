@@ -712,11 +712,9 @@ int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *lea
   k_wp_create<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_touch<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_label<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc, hits, leaf_slots, leaf_ids);
-  k_wc_finalize<<<1, 1, 0, st>>>(t->d, B, X, wc);
+  k_wc_finalize<<<1, 1, 0, st>>>(t->d, B, X, wc, t->h_wc, t->hctrl);  // + verdict, control block to the host
   CK(cudaGetLastError());
   t->launches[PH_COMMIT] += 13;
-  CK(cudaMemcpyAsync(t->h_wc, wc, sizeof(WaveCtl), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(t->hctrl, t->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
   return PRISM_OK;
 }
 

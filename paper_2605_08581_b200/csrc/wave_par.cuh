@@ -590,8 +590,7 @@ __global__ void __launch_bounds__(1024) k_wc_cut(DT T, int64_t B, WaveTmp X, Wav
 }
 
 // the control block after the committed wave (what the ordered commit leaves)
-__global__ void k_wc_finalize(DT T, int64_t B, WaveTmp X, const WaveCtl *wc) {
-  if (wc->stop) return;
+__device__ inline void wc_finalize_body(DT T, int64_t B, const WaveTmp &X, const WaveCtl *wc) {
   Ctrl *C = T.ctrl;
   const int64_t nv = wc->nv, ncreate = wc->ncreate;
   const int32_t ft1 = wc->ft0 + (int32_t)nv;
@@ -615,6 +614,14 @@ __global__ void k_wc_finalize(DT T, int64_t B, WaveTmp X, const WaveCtl *wc) {
   C->status = ST_DONE;
   C->L_valid = 0;
   C->H_n = 0;
+}
+
+// the wave's control block after the commit, and the verdict + control block
+// written straight to the host's pinned (mapped) copies: no copy nodes
+__global__ void k_wc_finalize(DT T, int64_t B, WaveTmp X, const WaveCtl *wc, WaveCtl *h_wc, Ctrl *h_ctrl) {
+  if (!wc->stop) wc_finalize_body(T, B, X, wc);
+  *h_wc = *wc;
+  *h_ctrl = *T.ctrl;
 }
 
 // device-sized scans: k_dscan_b scans the per-block sums of k_vscan_a (below)
