@@ -1213,8 +1213,9 @@ int prism_set_protection_device(prism_tree *t, const double *d_pri, int32_t nseg
 // the tree stream's commit plan in the meantime only reads the tree, so the
 // two overlap.  The build of the same fused wave picks them up (t->prebuilt).
 static int prebuild_order(prism_tree *t) {
-  CK(cudaMemsetAsync(t->cst, 0, offsetof(CoopState, ts), t->st));
-  k_propagate<<<blocks_for(t->d.S), TPB, 0, t->st>>>(t->d, -1, nullptr);
+  static_assert(offsetof(CoopState, ts) % 8 == 0, "CoopState clear in 8-byte words");
+  k_propagate<<<blocks_for(t->d.S), TPB, 0, t->st>>>(t->d, -1, nullptr, (unsigned long long *)t->cst,
+                                                     (int64_t)(offsetof(CoopState, ts) / 8));
   CoopBufs B = coop_bufs(t);
   k_ss_sample<EvictCand><<<SS_SAMP / SS_TPB, SS_TPB, 0, t->st>>>(EvictCand{t->d}, B, 1, nullptr,
                                                                    t->sel_min_candidates);

@@ -835,7 +835,12 @@ __global__ void k_build_keys(DT T, int32_t hw, const int64_t *dW = nullptr) {
 // eff[v] = slot of the maximum key in v's subtree (EFF_BLOCKED if any node of
 // the subtree can never be evicted): each node carries its own value upward
 // until an ancestor already holds something at least as large.
-__global__ void k_propagate(DT T, int32_t hw, const int64_t *dW = nullptr) {
+__global__ void k_propagate(DT T, int32_t hw, const int64_t *dW = nullptr, unsigned long long *clr = nullptr,
+                            int64_t nclr = 0) {
+  // (optionally) clear the selection state for the launches that follow (in
+  // place of a memset node in the wave's graph)
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nclr; i += (int64_t)gridDim.x * blockDim.x)
+    clr[i] = 0ull;
   if (dW && *dW < 0) return;
   if (hw < 0) hw = T.ctrl->hw;
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
