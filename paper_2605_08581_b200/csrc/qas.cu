@@ -1185,13 +1185,6 @@ __global__ void q_results(const int64_t *__restrict__ qcounts, const int64_t *__
     }
 }
 
-// the fused wave's stage verdict: the one-launch round overflowed (redo), the
-// layout check failed, or the paths / anchors exceed the serialization buffers
-__global__ void q_capcheck(const int64_t *__restrict__ qcounts, const int64_t *__restrict__ tot, int64_t tok_cap,
-                           int64_t anc_cap, const int32_t *err, int32_t *abort) {
-  if (qcounts[3] || *err || tot[0] > tok_cap || tot[1] > anc_cap) *abort = 1;
-}
-
 // the wave's dispatch order (hot lane, then cold) with each member's path and
 // anchor counts, and the uint32 token-layout check of its private suffix
 // (workload.py:147-154), before anything is serialised
@@ -1221,6 +1214,42 @@ __global__ void __launch_bounds__(1024) q_scan2(int64_t B, const int64_t *__rest
         (a == 0 ? poff : aoffs)[i] = ex;
         if (i == B) tot[a] = ex;
       });
+}
+
+// the fused wave's member stage in one CTA: q_members_len, q_scan2 and
+// q_capcheck (three dependent launches) as one
+__global__ void __launch_bounds__(1024) q_members_scan(int64_t nh, int64_t nc, const int64_t *__restrict__ hot,
+                                                       const int64_t *__restrict__ cold,
+                                                       const int64_t *__restrict__ ids, const int64_t *__restrict__ off,
+                                                       const int32_t *__restrict__ suffix, int64_t sys, int64_t chunk,
+                                                       int64_t *__restrict__ members, int64_t *__restrict__ plen,
+                                                       int64_t *__restrict__ alen, int64_t *__restrict__ poff,
+                                                       int64_t *__restrict__ aoffs, int64_t *__restrict__ tot,
+                                                       const int64_t *__restrict__ qcounts, int64_t tok_cap,
+                                                       int64_t anc_cap, int32_t *err, int32_t *abort) {
+  const int64_t B = nh + nc;
+  __shared__ int s_err;
+  if (threadIdx.x == 0) s_err = 0;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < B; i += blockDim.x) {
+    const int64_t m = i < nh ? hot[i] : cold[i - nh];
+    members[i] = m;
+    const int64_t k = off[m + 1] - off[m], sfx = suffix[m];
+    plen[i] = sys + k * chunk + sfx;
+    alen[i] = (sys > 0 ? 1 : 0) + k + (sfx > 0 ? 1 : 0);
+    if (SUFFIX_TOKEN_BASE + (uint64_t)ids[m] * (uint64_t)sfx + (uint64_t)sfx > 0xFFFFFFFFull) s_err = 2;
+  }
+  __syncthreads();  // (the CTA's global writes are visible to the CTA after the barrier)
+  prism::block_scan4<2, 8>(
+      B + 1, [&](int a, int64_t i) -> int64_t { return i >= B ? 0 : (a == 0 ? plen[i] : alen[i]); },
+      [&](int a, int64_t i, int64_t ex, int64_t) {
+        (a == 0 ? poff : aoffs)[i] = ex;
+        if (i == B) tot[a] = ex;
+      });
+  if (threadIdx.x == 0) {  // block_scan4 ends on a barrier: tot is visible
+    if (s_err) *err = s_err;
+    if (qcounts[3] || *err || tot[0] > tok_cap || tot[1] > anc_cap) *abort = 1;
+  }
 }
 
 // one warp per member: token path and anchors
@@ -1407,10 +1436,9 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
   auto body = [&]() -> int {
     int r;
     if ((r = qas_small_launch(q, gin, P, 0, btmask, c, G, true))) return r;  // (q_stage zeroed the counters)
-    q_members_len<<<nblk(B), TPB, 0, st>>>(nh, nc, q->hot, q->cv2, q->gids, q->goff, q->gsfx, sys_len, chunk,
-                                           members, q->plen, q->alen, q->err);
-    q_scan2<<<1, 1024, 0, st>>>(B, q->plen, q->alen, q->poff, q->aoffs, q->tmp_tot);
-    q_capcheck<<<1, 1, 0, st>>>(q->qcounts, q->tmp_tot, tok_cap, anc_cap, q->err, abort);
+    q_members_scan<<<1, 1024, 0, st>>>(nh, nc, q->hot, q->cv2, q->gids, q->goff, q->gsfx, sys_len, chunk, members,
+                                       q->plen, q->alen, q->poff, q->aoffs, q->tmp_tot, q->qcounts, tok_cap,
+                                       anc_cap, q->err, abort);
     QCK(cudaEventRecord(q->ev_t, st));
     QCK(cudaStreamWaitEvent((cudaStream_t)prism_tree_stream(t), q->ev_t, 0));
     if ((r = prism_set_protection_device_async(t, q->prio, nseg))) return r;  // overlaps serialization
