@@ -654,7 +654,7 @@ int cub_scan(prism_tree *t, In in, Out out, int64_t n, bool inclusive) {
 // Parallel commit of a segment-structured wave (wave_par.cuh), driven on the
 // device: plan -> scans -> plan verdict (k_wc_plan: fallback flags, capacity
 // headroom, eviction demand) -> the eviction-order prefix it needs (read on
-// the device) -> victim cuts + verdict (k_wc_cut) -> apply -> control block
+// the device) -> victim cuts + verdict (k_wp_cuts, its last CTA) -> apply -> control block
 // (k_wc_finalize), one stream of launches with a single host round trip at
 // the end.  Returns PRISM_OK with *applied = 1 when the wave was committed,
 // *applied = 0 when an exactness guard tripped (nothing was mutated; the
@@ -702,10 +702,8 @@ int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *lea
   }
   prof_begin(t);
   k_vscan_a<<<DS_BLOCKS, 256, 0, st>>>(t->d, X, t->ds_part, wc);
-  k_dscan_b<<<1, 1024, 0, st>>>(t->ds_part, DS_BLOCKS, wc);
   k_vscan_c<<<DS_BLOCKS, 256, 0, st>>>(t->d, X, t->ds_part, wc);
-  k_wp_cuts<<<blocks_for(B), TPB, 0, st>>>(t->d, B, X, wc);
-  k_wc_cut<<<1, 1024, 0, st>>>(t->d, B, X, wc);
+  k_wp_cuts<<<blocks_for(B), TPB, 0, st>>>(t->d, B, X, wc);  // + the cut verdict (last CTA)
   k_wp_evict<<<2 * sms, TPB, 0, st>>>(t->d, wc);
   k_wp_alloc<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_label_reset<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
@@ -714,7 +712,7 @@ int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *lea
   k_wp_label<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc, hits, leaf_slots, leaf_ids);
   k_wc_finalize<<<1, 1, 0, st>>>(t->d, B, X, wc, t->h_wc, t->hctrl);  // + verdict, control block to the host
   CK(cudaGetLastError());
-  t->launches[PH_COMMIT] += 13;
+  t->launches[PH_COMMIT] += 11;
   return PRISM_OK;
 }
 
@@ -757,7 +755,7 @@ int wave_par_verdict(prism_tree *t, int *applied, int *again, int32_t *force_ful
 // Parallel commit of a segment-structured wave (wave_par.cuh), driven on the
 // device: plan -> scans -> plan verdict (k_wc_plan: fallback flags, capacity
 // headroom, eviction demand) -> the eviction-order prefix it needs (read on
-// the device) -> victim cuts + verdict (k_wc_cut) -> apply -> control block
+// the device) -> victim cuts + verdict (k_wp_cuts, its last CTA) -> apply -> control block
 // (k_wc_finalize), one stream of launches with a single host round trip at
 // the end.  Returns PRISM_OK with *applied = 1 when the wave was committed,
 // *applied = 0 when an exactness guard tripped (nothing was mutated; the

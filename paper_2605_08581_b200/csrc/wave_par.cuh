@@ -258,29 +258,6 @@ __global__ void k_wp_hits(DT T, WaveIn W, WaveTmp X) {
   X.miss[j] = n - hit;
 }
 
-// per member: number of list entries consumed through member j (first F >= D_j)
-__global__ void k_wp_cuts(DT T, int64_t B, WaveTmp X, const WaveCtl *wc) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= B || wc->stop) return;
-  const int64_t D = wc->R0 + X.dem[j] - T.capacity;  // dem = inclusive sum of missing
-  int64_t c = 0;
-  if (D > 0) {
-    const int64_t Tn = T.ctrl->L_n;
-    int64_t lo = 0, hi = Tn;  // first idx with F[idx] >= D
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (X.F[mid] >= D) hi = mid;
-      else lo = mid + 1;
-    }
-    if (lo >= Tn) {
-      atomicOr(X.flags, WPF_CAPACITY);
-      c = Tn;
-    } else {
-      c = lo + 1;
-    }
-  }
-  X.cut[j] = c;
-}
 
 // apply the consumed victims [0, nv) of the stream (stream order == victim order)
 __global__ void k_wp_evict(DT T, const WaveCtl *wc) {
@@ -556,19 +533,18 @@ __global__ void __launch_bounds__(1024) k_wp_scan3(DT T, int64_t B, WaveTmp X, W
 // the victims: nv = entries consumed through the last member, checks that the
 // prefix sufficed and that no consumed entry is pinned/guarded; the number of
 // evict calls (members whose cut advances) and the tokens freed
-__global__ void __launch_bounds__(1024) k_wc_cut(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
+__device__ inline void wc_cut_body(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
   __shared__ int64_t s_calls[32];
-  if (wc->stop) return;
   int64_t calls = 0;
-  for (int64_t j = threadIdx.x; j < B; j += blockDim.x) calls += X.cut[j] > (j ? X.cut[j - 1] : 0) ? 1 : 0;
+  for (int64_t j = threadIdx.x; j < B; j += blockDim.x) calls += __ldcg(&X.cut[j]) > (j ? __ldcg(&X.cut[j - 1]) : 0) ? 1 : 0;
   for (int o = 16; o > 0; o >>= 1) calls += __shfl_xor_sync(0xffffffffu, calls, o);
   if ((threadIdx.x & 31) == 0) s_calls[threadIdx.x >> 5] = calls;
   __syncthreads();
   if (threadIdx.x) return;
   calls = 0;
   for (int w = 0; w < (int)(blockDim.x >> 5); w++) calls += s_calls[w];
-  const int64_t nv = X.cut[B - 1];
-  const int32_t flags = *X.flags;
+  const int64_t nv = __ldcg(&X.cut[B - 1]);
+  const int32_t flags = __ldcg(X.flags);
   const int64_t poison = X.misc[1];
   if (flags & WPF_CAPACITY) {
     if (T.ctrl->L_partial) {
@@ -587,6 +563,42 @@ __global__ void __launch_bounds__(1024) k_wc_cut(DT T, int64_t B, WaveTmp X, Wav
   wc->nv = nv;
   wc->calls = calls;
   wc->freed = nv > 0 ? X.F[nv - 1] : 0;
+}
+
+// per member: number of list entries consumed through member j (first F >= D_j);
+// the last CTA to finish then takes the verdict (wc_cut_body)
+__global__ void k_wp_cuts(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
+  __shared__ bool s_last;
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (wc->stop) return;  // (uniform over the grid)
+  if (j < B) {
+    const int64_t D = wc->R0 + X.dem[j] - T.capacity;  // dem = inclusive sum of missing
+    int64_t c = 0;
+    if (D > 0) {
+      const int64_t Tn = T.ctrl->L_n;
+      int64_t lo = 0, hi = Tn;  // first idx with F[idx] >= D
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (X.F[mid] >= D) hi = mid;
+        else lo = mid + 1;
+      }
+      if (lo >= Tn) {
+        atomicOr(X.flags, WPF_CAPACITY);
+        c = Tn;
+      } else {
+        c = lo + 1;
+      }
+    }
+    X.cut[j] = c;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    s_last = atomicAdd((unsigned long long *)&X.misc[7], 1ull) == (unsigned long long)gridDim.x - 1ull;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  wc_cut_body(T, B, X, wc);
 }
 
 // the control block after the committed wave (what the ordered commit leaves)
@@ -624,23 +636,8 @@ __global__ void k_wc_finalize(DT T, int64_t B, WaveTmp X, const WaveCtl *wc, Wav
   *h_ctrl = *T.ctrl;
 }
 
-// device-sized scans: k_dscan_b scans the per-block sums of k_vscan_a (below)
+// device-sized scans over DS_BLOCKS partitions (k_vscan_a / k_vscan_c below)
 constexpr int DS_BLOCKS = 296;
-
-__global__ void __launch_bounds__(1024) k_dscan_b(int64_t *part, int nparts, const WaveCtl *wc) {
-  if (wc && (wc->stop || wc->W < 0)) return;
-  __shared__ int64_t s[1024];
-  const int i = threadIdx.x;
-  s[i] = i < nparts ? part[i] : 0;
-  __syncthreads();
-  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
-    const int64_t y = i >= o ? s[i - o] : 0;
-    __syncthreads();
-    s[i] += y;
-    __syncthreads();
-  }
-  if (i < nparts) part[i] = s[i] - (i < nparts ? part[i] : 0);  // exclusive
-}
 
 
 
@@ -648,7 +645,7 @@ __global__ void __launch_bounds__(1024) k_dscan_b(int64_t *part, int nparts, con
 // i of the list counts elen when it is still the node it was listed as and
 // evictable by the wave's members, else 0 (and marks the first such entry:
 // misc[1], the victim guard).  k_vscan_a: per-block sums (+ the guard),
-// k_dscan_b: their scan, k_vscan_c: the inclusive prefix F.
+// k_vscan_c: each CTA reduces the sums before it, then the inclusive prefix F.
 __device__ __forceinline__ int64_t wp_vlen(const DT &T, const WaveTmp &X, int64_t i, uint32_t epoch, bool mark) {
   const uint64_t v = T.Lv[i];
   const int32_t s = (int32_t)(v & 0xffffffffu);
@@ -683,8 +680,19 @@ __global__ void __launch_bounds__(256) k_vscan_c(DT T, WaveTmp X, const int64_t 
   const int64_t b0 = blockIdx.x * per, b1 = b0 + per < n ? b0 + per : n;
   const uint32_t epoch = wc->epoch;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = part[blockIdx.x];
-  __syncthreads();
+  {  // this CTA's carry: the sums of the partitions before it (k_vscan_a), reduced here
+    int64_t x = 0;
+    for (int q = threadIdx.x; q < (int)blockIdx.x; q += blockDim.x) x += part[q];
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) sw[wid] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t c = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); w++) c += sw[w];
+      carry = c;
+    }
+    __syncthreads();
+  }
   for (int64_t t0 = b0; t0 < b1; t0 += blockDim.x) {
     const int64_t i = t0 + threadIdx.x;
     int64_t x = i < b1 ? wp_vlen(T, X, i, epoch, false) : 0;
