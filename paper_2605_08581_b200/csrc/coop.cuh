@@ -1294,10 +1294,8 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_sort(CoopBufs B, Key3 *kout, uint
 }
 
 // the rare buckets above SS_BMAX (geometric sizes): in-place bitonic in shared memory
-__global__ void __launch_bounds__(512) k_ss_sort_big(CoopBufs B, Key3 *kout, uint64_t *vout) {
-  extern __shared__ __align__(16) unsigned char dsm[];
+__device__ inline void ss_sort_big_body(const CoopBufs &B, Key3 *kout, uint64_t *vout, unsigned char *dsm) {
   CoopState *st = B.st;
-  if (!st->ss_ok) return;
   const int nb = st->ss_nb;
   Key3 *sk = reinterpret_cast<Key3 *>(dsm);
   uint64_t *sv = reinterpret_cast<uint64_t *>(sk + SS_BBIG);
@@ -1324,7 +1322,14 @@ __global__ void __launch_bounds__(512) k_ss_sort_big(CoopBufs B, Key3 *kout, uin
     __syncthreads();
   }
 }
+
+__global__ void __launch_bounds__(512) k_ss_sort_big(CoopBufs B, Key3 *kout, uint64_t *vout) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  if (!B.st->ss_ok) return;
+  ss_sort_big_body(B, kout, vout, dsm);
+}
 constexpr size_t SS_BIG_SMEM = (sizeof(Key3) + 8) * SS_BBIG;
+static_assert(SS_BIG_SMEM <= COOP_SMEM, "k_build_coop sorts the big buckets in its own shared memory");
 
 // the eviction-order build after keys / subtree maxima (full-occupancy
 // kernels k_build_keys, k_propagate) and the sample select: the prefix of the
@@ -1349,6 +1354,8 @@ __global__ void __launch_bounds__(COOP_TPB) k_build_coop(DT T, CoopBufs B, int64
   if (fast) {
     nsel = (int64_t)B.st->ss_n;
     n = (int64_t)B.st->ss_cand;
+    // the rare buckets above SS_BMAX (k_ss_sort_big's work; same shared memory)
+    if (sampled == 2) ss_sort_big_body(B, T.Lk, T.Lv, dsm);
   } else {
     coop_gather(B, hw, cand);
     grid.sync();

@@ -368,7 +368,7 @@ int coop_grid(prism_tree *t) {
 // the sample-select launches (coop.cuh) ahead of the cooperative finaliser
 template <class Cand>
 int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const int64_t *dW, int64_t min_cand,
-                  bool sampled_already = false) {
+                  bool sampled_already = false, bool big_in_finaliser = false) {
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(k_ss_select<EvictCand>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SEL_SMEM));
@@ -385,7 +385,7 @@ int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const 
   k_ss_filter<Cand><<<4 * sms, SS_TPB, SS_FILTER_SMEM, st>>>(cand, B);
   k_ss_scatter<<<2 * sms, SS_TPB, 0, st>>>(B, W, dW);
   k_ss_sort<<<3 * sms, SS_TPB, SS_SORT_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
-  k_ss_sort_big<<<sms, 512, SS_BIG_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
+  if (!big_in_finaliser) k_ss_sort_big<<<sms, 512, SS_BIG_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
   CK(cudaGetLastError());
   return PRISM_OK;
 }
@@ -422,8 +422,9 @@ int build_list(prism_tree *t, int64_t W, const int64_t *dW = nullptr) {
     int64_t minc = t->sel_min_candidates, small = std::min<int64_t>(SEL_SMALL, t->sel_min_candidates);
     int32_t sampled = (t->use_sample && (dW || W > 0)) ? 1 : 0;
     if (sampled) {
-      int rc = sample_select(t, EvictCand{t->d}, B, W, dW, minc, pre);
+      int rc = sample_select(t, EvictCand{t->d}, B, W, dW, minc, pre, true);
       if (rc) return rc;
+      sampled = 2;  // k_build_coop sorts the big buckets itself
     }
     void *args[] = {(void *)&t->d, (void *)&B, (void *)&W, (void *)&dW, (void *)&minc, (void *)&small,
                     (void *)&sampled};
