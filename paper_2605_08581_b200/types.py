@@ -272,3 +272,29 @@ def serialize_tokens(request, catalog, skeleton: Sequence[int] | None = None) ->
     """workload.py:157-164"""
     order = request.skeleton if skeleton is None else skeleton
     return serialize_skeleton(order, catalog, request.id, request.suffix_len)
+
+
+# ----------------------------------------------------------------- engine.py
+
+
+def build_anchors(request, aligned_skeleton: Sequence[int], snapshots: dict) -> list[Anchor]:
+    """The hint hand-off glue, engine.py:269-292: SYSTEM@sys_len, REUSABLE@each segment end, PRIVATE@path_len."""
+    anchors: list[Anchor] = []
+    if request.sys_len > 0:
+        anchors.append(Anchor(offset=request.sys_len, kind=NodeKind.SYSTEM))
+    m = len(aligned_skeleton)
+    chunk = request.reuse_len // m if m else 0
+    depth = request.sys_len
+    for seg in aligned_skeleton:
+        depth += chunk
+        anchors.append(
+            Anchor(
+                offset=depth,
+                kind=NodeKind.REUSABLE,
+                segment_id=seg,
+                counter_snapshot=snapshots.get(seg, (0, 0, 0)),
+            )
+        )
+    if request.suffix_len > 0:
+        anchors.append(Anchor(offset=request.path_len, kind=NodeKind.PRIVATE))
+    return anchors

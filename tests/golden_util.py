@@ -13,7 +13,7 @@ import json
 import os
 from functools import lru_cache
 
-from paper_2605_08581_b200.engine import SimConfig, run_simulation
+from sim_harness import SimConfig, run_simulation
 from paper_2605_08581_b200.types import (
     Anchor,
     CacheConfig,
@@ -25,7 +25,7 @@ from paper_2605_08581_b200.types import (
     Request,
     SchedulerConfig,
 )
-from paper_2605_08581_b200.workload import load_trace
+from traces.refgen import load_trace
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 

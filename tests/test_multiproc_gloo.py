@@ -20,7 +20,7 @@ import torch.multiprocessing as mp
 
 from paper_2605_08581_b200.shard import max_over_ranks, route, shard_requests
 from paper_2605_08581_b200.types import SegmentCatalog
-from paper_2605_08581_b200.workload import WorkloadConfig, generate_trace
+from traces.refgen import WorkloadConfig, generate_trace
 
 
 def _free_port() -> int:
@@ -53,7 +53,7 @@ def _worker(rank, world, port, out):
     t = max_over_ranks(float(rank + 1))
     # sharded oracle run on this replica's sub-trace
     from oracle.oracle import OracleRadixCache, oracle_schedule_round
-    from paper_2605_08581_b200.engine import SimConfig, run_simulation
+    from sim_harness import SimConfig, run_simulation
     from paper_2605_08581_b200.types import CacheConfig, SchedulerConfig, Trace
 
     cfg = SimConfig(prefill_rate=5000.0, decode_rate=20000.0, cache=CacheConfig(capacity_tokens=600, protect_budget=4),
@@ -81,7 +81,7 @@ def test_two_replicas_gloo():
     assert res[0]["max"] == res[1]["max"] == 2.0
     # each replica equals the oracle run on its own sub-trace alone
     from oracle.oracle import OracleRadixCache, oracle_schedule_round
-    from paper_2605_08581_b200.engine import SimConfig, run_simulation
+    from sim_harness import SimConfig, run_simulation
     from paper_2605_08581_b200.types import CacheConfig, SchedulerConfig, Trace
 
     cfg = SimConfig(prefill_rate=5000.0, decode_rate=20000.0, cache=CacheConfig(capacity_tokens=600, protect_budget=4),

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 from oracle.oracle import OracleRadixCache, oracle_schedule_round
-from paper_2605_08581_b200.engine import build_anchors
+from paper_2605_08581_b200.types import build_anchors
 from paper_2605_08581_b200.types import (
     CacheConfig,
     CachePolicy,

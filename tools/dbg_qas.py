@@ -3,7 +3,7 @@ sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "t
 import golden_util as G
 from oracle.oracle import oracle_schedule_round, OracleRadixCache
 from paper_2605_08581_b200.qas import DeviceScheduler
-from paper_2605_08581_b200.engine import run_simulation
+from sim_harness import run_simulation
 run, trace, cfg = G.engine_case(0)
 ds = DeviceScheduler()
 n = [0]

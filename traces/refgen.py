@@ -1,4 +1,4 @@
-"""Trace I/O and synthetic trace generation (host side, input preparation only).
+"""Reference-compatible trace generation and JSONL I/O (INPUT PREPARATION, not product).
 
 ``load_trace``/``save_trace`` read and write the reference's JSON-lines trace
 format (workload.py:232-313).  ``generate_trace`` reproduces the reference's
@@ -20,7 +20,7 @@ from typing import IO
 
 import numpy as np
 
-from .types import Request, SegmentCatalog, Trace
+from paper_2605_08581_b200.types import Request, SegmentCatalog, Trace
 
 
 @dataclass(frozen=True)
