@@ -6,18 +6,32 @@ DART tree.  One *decision* = one admitted request: its exact-prefix match and
 its insert including _reserve/evict, with the wave's QAS round and
 protection pass amortised.
 
-Workload ("mu1M"): a DART tree warm-started with 125,000
-paths (system prefix 28 tokens + 8 segments x 16 tokens + 16-token private
-suffix; segment 0 uniform over 50, the others uniform over 2M) -- about
-1.0M nodes / 16M tokens at capacity_tokens = 16,000,000, so every admission
-evicts.  A *step* is one serving-loop wave (engine.py:189-213) of 4096 new
-requests: device QAS round -> protection hand-off -> serialization -> ordered
-match+insert+evict -> release of the previous wave's pins.  Synthetic data,
-deterministic seeds; one independent replica tree per GPU (weak scaling) with
-one NCCL all-reduce of the per-window demand counters per step when N > 1.
+Workloads (traces/synth.py); ``--workload``:
+  c3   (default) the agent / tool-output trace: 40 segments of 32 tokens after
+       a 1024-token system prompt plus a 128-token private suffix (2432-token
+       paths), Zipf(1.1)-skewed 24-level segment chains, reorderable=false;
+       capacity sized so the steady-state tree holds ~1M nodes.
+  mu1m the 1M-node micro-benchmark (8 x 16-token segments, uniform).
+  c4   the RAG generator's shape at 100K segments (the sharded 10M trace).
+A *step* is one serving-loop wave (engine.py:189-213) per replica: device QAS
+round -> protection hand-off -> serialization -> ordered match+insert+evict
+-> release of the previous wave's pins.  Synthetic data, deterministic seeds.
 
-    python bench.py [--gpus N --steps K --warmup W]       # our B200 path
-    python bench.py --impl reference ...                   # reference algorithm on host cores
+Multi-GPU: one replica tree per GPU; requests of ONE global stream are routed
+to replicas by splitmix64(skeleton[0]) mod N; each replica's
+wave takes the next M requests of its shard (weak scaling); one NCCL
+all-reduce of the per-window demand counters per step.  ``--gpus N`` without
+torchrun re-launches itself under torch.distributed.run.
+
+Parity (``cpu_baseline`` leg, N=1, rank 0): the CPU oracle (oracle/, the
+reference algorithm restated in C and pinned to the reference's own outputs)
+runs the same warm start and ``--parity-waves`` evicting windows as a fresh
+device replica, in a background process started before CUDA is touched; the
+line reports whether dispatch order, hits, leaf ids, every victim and the whole
+final tree are identical, and times the oracle on those windows.
+
+    python bench.py [--gpus N --steps K --warmup W --workload c3|mu1m|c4]
+    python bench.py --impl reference ...     # the reference algorithm on host cores
 
 Prints exactly one JSON line (rank 0).
 """
@@ -26,8 +40,8 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -39,55 +53,72 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from traces import synth as S  # noqa: E402
+
 METRIC = "prefix-match+admit+evict decisions/sec @1M-node DART; hit-rate parity; HBM GB/s"
 UNIT = "decisions/s"
-SYS_LEN, K_SEG, CHUNK, SUFFIX = 28, 8, 16, 16
-SLOT0, OTHERS = 50, 2_000_000
-NSEG = SLOT0 + OTHERS
+
+# per-workload defaults: requests in the warm start, capacity (tokens), wave size
+DEFAULTS = {
+    "c3": {"warm": 8 * 4096, "capacity": 36_000_000, "wave": 4096},
+    "mu1m": {"warm": 125_000, "capacity": 16_000_000, "wave": 4096},
+    "c4": {"warm": 16 * 1024, "capacity": 4_000_000, "wave": 1024},
+}
+DESCR = {
+    "c3": "C3 agent trace: 2432-token paths (sys 1024 + 40 x 32-token segments + 128-token suffix), Zipf(1.1) "
+          "24-level segment chains over a 2^20 catalog, reorderable=false; DART tree warm-started to capacity "
+          "(~1M nodes), every wave evicts",
+    "mu1m": "mu1M: 172-token paths (sys 28 + 8 x 16 + 16), slot 0 uniform over 50, others over 2M; DART tree "
+            "warm-started with 125K paths (~1M nodes, ~16M tokens), every admission evicts",
+    "c4": "C4 RAG shape: 768-token paths (sys 28 + 5 x 128 + 100), 100K-segment catalog, Zipf(1.1) over 1000 hot, "
+          "r_hot 0.7",
+}
 
 
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--wave", type=int, default=4096)
-    ap.add_argument("--paths", type=int, default=125_000)
-    ap.add_argument("--capacity", type=int, default=16_000_000)
+    ap.add_argument("--workload", default="c3", choices=sorted(DEFAULTS))
+    ap.add_argument("--wave", type=int, default=0)
+    ap.add_argument("--warm", type=int, default=-1, help="warm-start requests per replica")
+    ap.add_argument("--capacity", type=int, default=0)
     ap.add_argument("--protect", type=int, default=20)
     ap.add_argument("--cold-quota", type=int, default=64)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--parity-waves", type=int, default=-1,
+                    help="evicting windows checked against the CPU oracle (default 2 at N=1, 0 at N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=-1)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baseline/e2e)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (tests on one GPU)")
+    ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baseline/e2e/parity)")
     ap.add_argument("--profile-steps", type=int, default=3,
                     help="extra waves AFTER the timed region with the per-phase device profile on (roofline)")
-    return ap.parse_args()
+    ap.add_argument("--ref-seconds", type=float, default=0.5, help="reference arm: seconds per step per worker")
+    a = ap.parse_args()
+    d = DEFAULTS[a.workload]
+    a.wave = a.wave or d["wave"]
+    a.capacity = a.capacity or d["capacity"]
+    a.warm = d["warm"] if a.warm < 0 else a.warm
+    return a
 
 
-# ---------------------------------------------------------------- workload
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
-def make_pool(first_id: int, n: int, rng: np.random.Generator) -> dict:
-    """n synthetic requests (ids first_id..): mu1M skeletons, dense segment ids."""
-    sk = np.empty((n, K_SEG), dtype=np.int32)
-    sk[:, 0] = rng.integers(0, SLOT0, size=n)
-    sk[:, 1:] = SLOT0 + rng.integers(0, OTHERS, size=(n, K_SEG - 1))
-    ids = np.arange(first_id, first_id + n, dtype=np.int64)
-    return {
-        "ids": ids,
-        "arrival": ids.astype(np.float64) * 1e-3,
-        "sk_off": np.arange(n + 1, dtype=np.int64) * K_SEG,
-        "sk": sk.reshape(-1),
-        "reorderable": np.ones(n, dtype=np.uint8),
-        "suffix": np.full(n, SUFFIX, dtype=np.int32),
-    }
+def _configs(args):
+    from paper_2605_08581_b200.types import CacheConfig, CachePolicy, SchedulerConfig
 
-
-def pool_bytes(pool: dict) -> int:
-    return int(sum(v.nbytes for v in pool.values()))
+    return (CacheConfig(capacity_tokens=args.capacity, policy=CachePolicy.DART, protect_budget=args.protect),
+            SchedulerConfig(dispatch_budget=args.wave, cold_quota=args.cold_quota))
 
 
 # ---------------------------------------------------------------- clocks
@@ -144,112 +175,155 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ---------------------------------------------------------------- CPU oracle sample
+# ---------------------------------------------------------------- oracle legs (checker / CPU baseline)
 
 
-def oracle_sample(seconds: float, paths: int, capacity: int, protect: int, wave: int, seed: int) -> dict:
-    """The reference algorithm (oracle/ C restatement, full scan + heap per
-    evict) on the same workload: warm start, then one wave timed for a bounded
-    number of decisions.  TEST/BASELINE INFRASTRUCTURE ONLY."""
-    from oracle.oracle import OracleRadixCache, _ptr, lib as olib, oracle_round_arrays
-    from paper_2605_08581_b200.qas_host import MarshaledRound
-    from paper_2605_08581_b200.types import CacheConfig, CachePolicy, SchedulerConfig
+def parity_windows(args, world: int, rank: int):
+    """The windows both sides of the parity check run: the warm start (to
+    capacity) then ``--parity-waves`` evicting windows, from a dedicated
+    stream of this replica's shard."""
+    st = S.ShardStream(args.workload, args.seed + 7_777, world, rank)
+    warm = [st.take(min(args.wave, args.warm - i)) for i in range(0, args.warm, args.wave)]
+    check = [st.take(args.wave) for _ in range(args.parity_waves)]
+    return warm, check
 
-    rng = np.random.default_rng(seed)
-    cache = OracleRadixCache(CacheConfig(capacity_tokens=capacity, policy=CachePolicy.DART, protect_budget=protect))
-    L = olib()
-    plen = SYS_LEN + K_SEG * CHUNK + SUFFIX
-    a_off = np.array([SYS_LEN] + [SYS_LEN + CHUNK * (j + 1) for j in range(K_SEG)] + [plen], dtype=np.int64)
-    a_kind = np.array([0] + [1] * K_SEG + [2], dtype=np.int8)
-    seg_none = -(2**63)
-    leaf = np.zeros(1, np.int64)
-    nv = np.zeros(1, np.int64)
 
-    def path_of(rid: int, segs: np.ndarray) -> np.ndarray:
-        p = np.empty(plen, dtype=np.uint32)
-        p[:SYS_LEN] = np.arange(SYS_LEN)
-        p[SYS_LEN:SYS_LEN + K_SEG * CHUNK] = (1_000_000 + segs[:, None].astype(np.int64) * CHUNK
-                                              + np.arange(CHUNK)).reshape(-1)
-        p[SYS_LEN + K_SEG * CHUNK:] = 2_000_000_000 + rid * SUFFIX + np.arange(SUFFIX)
-        return p
+def oracle_parity_job(args, world: int, rank: int, out_path: str) -> None:
+    """Background process: the oracle replica through the parity windows."""
+    from oracle.oracle import build
+    from oracle.windows import OracleReplica, concat_pools, drop_members
 
-    def insert(rid, segs, snaps):
-        p = path_of(rid, segs)
-        a_seg = np.concatenate([[seg_none], segs.astype(np.int64), [seg_none]])
-        L.ot_match(cache._h, _ptr(p), plen, None, _ptr(nv))
-        return L.ot_insert(cache._h, _ptr(p), plen, len(a_off), _ptr(a_off), _ptr(a_kind), _ptr(a_seg),
-                           _ptr(snaps), _ptr(leaf))
-
-    zero_snap = np.zeros(3 * len(a_off), np.int64)
-    pool = make_pool(0, paths, rng)
-    sk = pool["sk"].reshape(paths, K_SEG)
-    for i in range(paths):  # warm start (untimed)
-        insert(i, sk[i], zero_snap)
-        L.ot_release(cache._h, int(leaf[0]))
-    # one timed wave: QAS round + protection + ordered admissions until the budget
-    pend = make_pool(paths, wave, rng)
-    sched = SchedulerConfig(dispatch_budget=wave, cold_quota=64)
+    build()
+    cache, sched = _configs(args)
+    spec = S.SPECS[args.workload]
+    rep = OracleReplica(cache, sched, spec.nseg, spec.sys_len, spec.chunk)
+    warm, check = parity_windows(args, world, rank)
     t0 = time.perf_counter()
-    m = MarshaledRound(list(range(wave)), np.arange(NSEG, dtype=np.int64), pend["ids"], pend["arrival"],
-                       pend["sk_off"], pend["sk"], pend["reorderable"], np.zeros(1, np.int64),
-                       np.zeros(0, np.int32))
-    out = oracle_round_arrays(m, sched)
-    dom = np.flatnonzero(out.dom)
-    cache.set_protection(dict(zip(dom.tolist(), out.prio[dom].tolist())))
-    members = np.concatenate([out.hot, out.cold])
-    done = 0
-    for i in members:
-        al = out.aligned[i * K_SEG:(i + 1) * K_SEG]
-        snaps = np.zeros(3 * len(a_off), np.int64)
-        snaps[3:3 + 3 * K_SEG] = np.stack([out.g[al], out.a[al], out.nd[al]], axis=1).reshape(-1)
-        rc = insert(int(pend["ids"][i]), al, snaps)
-        if rc != 0:
-            break
-        done += 1
-        if time.perf_counter() - t0 > seconds:
-            break
-    el = time.perf_counter() - t0
-    return {"decisions": done, "seconds": el, "value": done / el}
+    pend = None
+    res = {}
+    for i, pool in enumerate(warm + check):
+        pend = concat_pools(pend, pool)
+        if i == len(warm):
+            rep.decisions, rep.decision_seconds = 0, 0.0  # the CPU baseline times the evicting windows only
+            res["warm_s"] = time.perf_counter() - t0
+        r = rep.step(pend)
+        if i >= len(warm):
+            j = i - len(warm)
+            res[f"m{j}"], res[f"h{j}"], res[f"l{j}"] = r["members"], r["hits"], r["leaf_ids"]
+        pend = drop_members(pend, r["members"][: r["n_admitted"]])
+    res["table"] = rep.table()
+    res["victims"] = rep.victims()
+    res["resident"] = np.array([rep.resident])
+    res["timing"] = np.array([rep.decisions, rep.decision_seconds, time.perf_counter() - t0])
+    np.savez(out_path, **res)
 
 
-def _ref_worker(args):
-    seconds, paths, capacity, protect, wave, seed = args
-    return oracle_sample(seconds, paths, capacity, protect, wave, seed)
+def device_parity(args, engine_kw, world: int, rank: int, dev) -> dict:
+    """A fresh device replica through the same windows; returns its outputs."""
+    from oracle.windows import concat_pools, device_table, device_victims, drop_members
+    from paper_2605_08581_b200.wave import DevicePending, WaveEngine
+
+    eng = WaveEngine(**engine_kw)
+    warm, check = parity_windows(args, world, rank)
+    pend, prev, out = None, 0, {}
+    for i, pool in enumerate(warm + check):
+        pend = concat_pools(pend, pool)
+        eng.release(eng.leaf_slots, prev)
+        nm, na = eng.step(DevicePending.from_host(pend["ids"], pend["arrival"], pend["sk_off"], pend["sk"],
+                                                  pend["reorderable"], pend["suffix"], dev))
+        members = eng.members[:nm].cpu().numpy()
+        if i >= len(warm):
+            j = i - len(warm)
+            out[f"m{j}"], out[f"h{j}"] = members, eng.hits[:na].cpu().numpy()
+            out[f"l{j}"] = eng.leaf_ids[:na].cpu().numpy()
+        prev = na
+        pend = drop_members(pend, members[:na])
+    view = eng.cache_view()
+    out["table"] = device_table(view)
+    out["victims"], out["vfirst"] = device_victims(view)
+    out["resident"] = view.resident_tokens
+    out["stats"] = eng.wave_stats()
+    eng.close()
+    return out
+
+
+def compare_parity(d: dict, o, waves: int, path_len: int) -> dict:
+    from oracle.windows import compare_tables
+
+    diffs = []
+    for j in range(waves):
+        for key, name in (("m", "dispatch order"), ("h", "hits"), ("l", "leaf ids")):
+            if not np.array_equal(np.asarray(d[f"{key}{j}"]), o[f"{key}{j}"]):
+                diffs.append(f"window {j}: {name}")
+    ov = o["victims"]
+    dv = d["victims"]
+    if not np.array_equal(dv, ov[d["vfirst"]:]) or d["vfirst"] + len(dv) != len(ov):
+        diffs.append(f"victims ({len(ov)} oracle, {d['vfirst'] + len(dv)} device)")
+    t = compare_tables(d["table"], o["table"])
+    if t:
+        diffs.append("tree: " + t)
+    if int(d["resident"]) != int(o["resident"][0]):
+        diffs.append("resident tokens")
+    adm = sum(len(o[f"l{j}"]) for j in range(waves))
+    hit = sum(int(o[f"h{j}"].sum()) for j in range(waves))
+    return {"waves_checked": waves, "identical": not diffs, "differences": diffs[:5],
+            "decisions_checked": adm, "victims_checked": int(len(ov)), "tree_nodes_checked": int(len(o["table"])),
+            "hit_rate": hit / max(adm * path_len, 1),
+            "device_commit": d["stats"]}
 
 
 # ---------------------------------------------------------------- reference arm
 
 
+def _ref_worker(job):
+    args, world, rank, seconds = job
+    from oracle.windows import OracleReplica, concat_pools, drop_members
+
+    cache, sched = _configs(args)
+    spec = S.SPECS[args.workload]
+    rep = OracleReplica(cache, sched, spec.nseg, spec.sys_len, spec.chunk)
+    st = S.ShardStream(args.workload, args.seed + 31 * rank + 1, world, rank)
+    pend = None
+    for i in range(0, args.warm, args.wave):  # warm start (untimed)
+        pend = concat_pools(pend, st.take(min(args.wave, args.warm - i)))
+        r = rep.step(pend)
+        pend = drop_members(pend, r["members"][: r["n_admitted"]])
+    rep.decisions, rep.decision_seconds = 0, 0.0
+    deadline = time.perf_counter() + seconds
+    while time.perf_counter() < deadline:
+        pend = concat_pools(pend, st.take(args.wave))
+        r = rep.step(pend, deadline=deadline)
+        pend = drop_members(pend, r["members"][: r["n_admitted"]])
+    return {"decisions": rep.decisions, "seconds": rep.decision_seconds}
+
+
 def run_reference(args) -> None:
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return  # rank 0 alone runs and prints the host-core baseline
     import multiprocessing as mp
 
     from oracle import oracle as O
 
     O.build()
-    cores = max(1, min(len(os.sched_getaffinity(0)), 8))
-    per_step = 0.5  # seconds of decisions per step per worker (bounded sample)
-    total = max(args.steps, 1) * per_step
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
-        res = pool.map(_ref_worker, [(total, args.paths, args.capacity, args.protect, args.wave,
-                                      args.seed + 17 * w) for w in range(cores)])
-    value = sum(r["value"] for r in res)
+    cores = max(1, min(len(os.sched_getaffinity(0)), 32))
+    seconds = max(args.steps, 1) * args.ref_seconds
+    with mp.get_context("fork").Pool(cores) as pool:
+        res = pool.map(_ref_worker, [(args, cores, w, seconds) for w in range(cores)])
+    value = sum(r["decisions"] / max(r["seconds"], 1e-9) for r in res)
     decisions = sum(r["decisions"] for r in res)
     secs = max(r["seconds"] for r in res)
-    ms_per_step = 1000.0 * secs / max(args.steps, 1)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": "mu1M DART tree (125K warm paths, ~1M nodes, cap 16M tokens), waves of 4096",
-                   "wave": args.wave, "policy": "DART"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * secs / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": DESCR[args.workload], "wave": args.wave, "capacity_tokens": args.capacity,
+                   "warm_requests": args.warm, "policy": "DART"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{decisions} decisions over {cores} replica processes x {total:.1f}s after "
-                                   f"a {args.paths}-path warm start (oracle/ C restatement of kvcache.py/"
-                                   f"scheduler.py: full scan + heap per evict)"},
+                         "sample": f"{decisions} decisions: {cores} replica processes (one per host core, each a "
+                                   f"segment-hash shard of one global stream), each warm-started to capacity and "
+                                   f"then timed for {seconds:.1f}s of evicting windows (oracle/: C restatement of "
+                                   f"kvcache.py/scheduler.py, full scan + heap per evict, pinned to the "
+                                   f"reference's outputs; the Python reference itself is ~100x slower)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -259,62 +333,79 @@ def run_reference(args) -> None:
 
 
 def run_ours(args) -> None:
-    import torch
-    import torch.distributed as dist
-
-    from paper_2605_08581_b200.types import CacheConfig, CachePolicy, SchedulerConfig
-    from paper_2605_08581_b200.wave import DevicePending, WaveEngine
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    spec = S.SPECS[args.workload]
+    if args.parity_waves < 0:
+        args.parity_waves = 2 if world == 1 else 0
+    if args.profile_only:
+        args.parity_waves = 0
+    # the oracle parity replica starts BEFORE CUDA is initialised (fork-safe)
+    par_proc = par_path = None
+    if args.parity_waves > 0 and not args.no_cpu_baseline:
+        import multiprocessing as mp
+
+        fd, par_path = tempfile.mkstemp(suffix=".npz")
+        os.close(fd)
+        par_proc = mp.get_context("fork").Process(target=oracle_parity_job, args=(args, world, rank, par_path))
+        par_proc.start()
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_08581_b200.wave import DevicePending, WaveEngine
+
     if world > 1:
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        dist.init_process_group(args.backend)
+    gpu = 0 if args.same_device else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     B = args.wave
-    engine = WaveEngine(
-        CacheConfig(capacity_tokens=args.capacity, policy=CachePolicy.DART, protect_budget=args.protect),
-        SchedulerConfig(dispatch_budget=B, cold_quota=args.cold_quota),
-        NSEG, SYS_LEN, CHUNK, device=local, initial_slots=1 << 21, initial_arena_tokens=1 << 28,
-    )
-    rng = np.random.default_rng(args.seed + 1000 * rank)  # shard = independent sub-trace
+    cache, sched = _configs(args)
+    engine_kw = dict(cache=cache, sched=sched, nseg=spec.nseg, sys_len=spec.sys_len, chunk=spec.chunk, device=gpu,
+                     initial_slots=1 << 21, initial_arena_tokens=max(1 << 26, 4 * args.capacity))
+    engine = WaveEngine(**engine_kw)
     stream = engine.stream
-    demand = torch.zeros(NSEG, dtype=torch.int32, device=dev) if world > 1 else None
+    stream_in = S.ShardStream(args.workload, args.seed, world, rank)
+    demand = torch.zeros(spec.nseg, dtype=torch.int32, device=dev) if world > 1 else None
+
+    def allreduce_demand():
+        if demand is None:
+            return
+        with torch.cuda.stream(stream):  # per-window demand counters across replicas (NVLink)
+            engine.demand_counters(demand)
+            if args.backend == "nccl":
+                dist.all_reduce(demand)
+            else:
+                h = demand.cpu()
+                dist.all_reduce(h)
+                demand.copy_(h)
 
     def to_dev(pool):
         return DevicePending.from_host(pool["ids"], pool["arrival"], pool["sk_off"], pool["sk"],
                                        pool["reorderable"], pool["suffix"], dev)
 
-    # warm start (untimed): the mu1M tree through the same fused path
-    next_id, prev = 0, 0
-    t_ws = time.perf_counter()
-    while next_id < args.paths:
-        n = min(B, args.paths - next_id)
-        engine.release(engine.leaf_slots, prev)
-        _, prev = engine.step(to_dev(make_pool(next_id, n, rng)))
-        next_id += n
-    engine.release(engine.leaf_slots, prev)
+    # warm start (untimed): the tree through the same fused path, to capacity
     prev = 0
+    t_ws = time.perf_counter()
+    for i in range(0, args.warm, B):
+        engine.release(engine.leaf_slots, prev)
+        _, prev = engine.step(to_dev(stream_in.take(min(B, args.warm - i))))
     torch.cuda.synchronize()
     warm_s = time.perf_counter() - t_ws
-    st0 = engine.stats()
 
     nsteps = args.warmup + args.steps
     nprof = max(args.profile_steps, 1)
-    pools = [make_pool(next_id + s * B, B, rng) for s in range(nsteps + nprof)]
-    next_id += (nsteps + nprof) * B
-    dpools = [to_dev(p) for p in pools]
+    dpools = [to_dev(stream_in.take(B)) for _ in range(nsteps + nprof)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    hitsum = torch.zeros(1, dtype=torch.int64, device=dev)
 
     def one_step(pend):
         nonlocal prev
         engine.release(engine.leaf_slots, prev)
         nm, na = engine.step(pend)
-        if demand is not None:  # per-window demand counters across replicas (NVLink)
-            with torch.cuda.stream(stream):
-                engine.demand_counters(demand)
-                dist.all_reduce(demand)
+        allreduce_demand()
         prev = na
         return nm, na
 
@@ -323,9 +414,9 @@ def run_ours(args) -> None:
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    prof0 = engine.profile_read()  # (launch counters; the profile itself stays off while timing)
+    prof0 = engine.profile_read()
     st1 = engine.stats()
-    clocks = Clocks(local)
+    clocks = Clocks(gpu)
     clocks.start()
     torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" scopes profiles here
     evs = []
@@ -339,6 +430,8 @@ def run_ours(args) -> None:
         nm, na = one_step(dpools[s])
         e1.record(stream)
         evs.append((e0, e1))
+        with torch.cuda.stream(stream):  # outside the events: the hit-rate numerator
+            hitsum.add_(engine.hits[:na].sum())
         admitted += na
         members += nm
     torch.cuda.synchronize()
@@ -349,11 +442,13 @@ def run_ours(args) -> None:
     prof1 = engine.profile_read()
     st2 = engine.stats()
     ms = sum(a.elapsed_time(b) for a, b in evs)
+    hit_tokens = int(hitsum.item())
+    hit_rate = hit_tokens / max(admitted * spec.path_len, 1)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms], dtype=torch.float64, device=dev if args.backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        c = torch.tensor([admitted], dtype=torch.int64, device=dev)
+        c = torch.tensor([admitted], dtype=torch.int64, device=dev if args.backend == "nccl" else "cpu")
         dist.all_reduce(c)
         admitted_all = int(c.item())
     else:
@@ -365,44 +460,38 @@ def run_ours(args) -> None:
     e2e = None
     if e2e_steps > 0 and not args.profile_only:
         ew = max(args.warmup, 3)  # untimed: the first waves of the host-buffer shape capture its graph
-        hpools = [make_pool(next_id + s * B, B, rng) for s in range(e2e_steps + ew)]
-        next_id += (e2e_steps + ew) * B
-        pinned = [{k: torch.from_numpy(v).pin_memory() for k, v in p.items()} for p in hpools]
+        hpools = [stream_in.take(B) for _ in range(e2e_steps + ew)]
+        pinned = [{k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in p.items()} for p in hpools]
         out_mem = np.empty(B, dtype=np.int64)
         out_hits = np.empty(B, dtype=np.int64)
         h2d = sum(v.numel() * v.element_size() for v in pinned[0].values())
         for s in range(ew):
             _, prev = engine.step_host(pinned[e2e_steps + s], out_mem, out_hits, release_n=prev)
+            allreduce_demand()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        adm2 = 0
-        d2h = 0
+        adm2 = d2h = 0
         wall = []
         for s in range(e2e_steps):
-            # host pinned inputs read in place by the wave, results back in host arrays,
-            # the previous wave's pins released by the same call
             tw = time.perf_counter()
             nm, na = engine.step_host(pinned[s], out_mem, out_hits, release_n=prev)
             wall.append((time.perf_counter() - tw) * 1e3)
             prev = na
-            if demand is not None:
-                with torch.cuda.stream(stream):
-                    engine.demand_counters(demand)
-                    dist.all_reduce(demand)
+            allreduce_demand()
             d2h += 8 * (na + nm)
             adm2 += na
         e1.record(stream)
         torch.cuda.synchronize()
         ms2 = e0.elapsed_time(e1)
         if world > 1:
-            t = torch.tensor([ms2], dtype=torch.float64, device=dev)
+            t = torch.tensor([ms2], dtype=torch.float64, device=dev if args.backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms2 = float(t.item())
-            c = torch.tensor([adm2], dtype=torch.int64, device=dev)
+            c = torch.tensor([adm2], dtype=torch.int64, device=dev if args.backend == "nccl" else "cpu")
             dist.all_reduce(c)
             adm2 = int(c.item())
         e2e = {"value": adm2 / (ms2 / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
@@ -411,9 +500,9 @@ def run_ours(args) -> None:
                "copied to host inside the wave; the previous wave's pins released by the same call)",
                "host_ms_per_call": {"median": round(statistics.median(wall), 4), "max": round(max(wall), 4)}}
 
-    # ---- roofline of the dominant kernel: a few more waves of the same workload
-    # AFTER the timed region with the live per-phase profile on (its per-phase
-    # event syncs would otherwise sit inside the timed region)
+    # ---- roofline of the dominant phase: a few more waves AFTER the timed
+    # region with the live per-phase profile on (its per-phase event syncs
+    # would otherwise sit inside the timed region)
     gpu_launches = int(sum(prof1[p]["launches"] - prof0[p]["launches"]
                            for p in ("commit", "build", "protect", "prematch", "release", "qas")))
     torch.cuda.synchronize()
@@ -426,69 +515,85 @@ def run_ours(args) -> None:
     prof3 = engine.profile_read()
     st4 = engine.stats()
     engine.profile(False)
-    d = {p: {k: prof3[p][k] - prof2[p][k] for k in ("ms", "calls", "launches")}
-         for p in ("commit", "build", "protect", "prematch", "release", "qas")}
+    phases = ("commit", "build", "protect", "prematch", "release", "qas")
+    d = {p: {k: prof3[p][k] - prof2[p][k] for k in ("ms", "calls", "launches")} for p in phases}
     victims = st4["victims"] - st3["victims"]
     created = st4["next_id"] - st3["next_id"]
     chain = prof3["chain_nodes"] - prof2["chain_nodes"]
     toks = prof3["inserted_tokens"] - prof2["inserted_tokens"]
     live = st4["live_nodes"]
+    anchors = engine.reusable_anchors()
     members_prof = nprof * B
-    algo = {  # SURVEY.md 8(d) algorithmic bytes, per phase over the timed region
-        "commit": 8 * toks + 32 * (chain + created + victims),
-        "build": 16 * live * d["build"]["calls"],
-        "protect": 16 * live * d["protect"]["calls"],
-        "prematch": 4 * toks + 32 * chain,
-        "qas": members_prof * (4 * K_SEG + 16),
+    algo = {  # SURVEY.md 8(d) algorithmic bytes over the profiled waves: per request 8l + 32(d + c + v)
+        "prematch": 4 * toks + 32 * chain,              # read the query + the matched resident chain
+        "commit": 4 * toks + 32 * (created + victims),  # write the new tokens + created / victim records
+        "build": 16 * live * min(d["build"]["calls"], nprof),       # eviction-key scan, <= once per wave
+        "protect": 16 * anchors * min(d["protect"]["calls"], nprof),  # protection scan over A anchors
+        "qas": members_prof * (4 * spec.k + 16),
         "release": 0,
     }
-    # dominant phase by device time; "one launch" = one wave's worth of that
-    # phase (its kernels back to back, SURVEY.md 8(d) bytes per wave)
     dom = max(("commit", "build", "protect", "prematch", "qas"), key=lambda p: d[p]["ms"])
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
-    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {}
+    peak = float(peaks.get("hbm_gbs", 7672.0))
+    peak_src = ("MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks
+                else "B200_PROFILING.md fallback")
     per_wave_bytes = algo[dom] / nprof
     per_wave_s = d[dom]["ms"] / 1000.0 / nprof
     achieved = per_wave_bytes / per_wave_s / 1e9 if per_wave_s > 0 else 0.0
     traffic = None
-    summ = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    summ = os.path.join(ROOT, "profiles", f"ncu_summary_{args.workload}.json")
     if os.path.exists(summ):
         try:
             traffic = json.load(open(summ)).get("phases", {}).get(dom, {}).get("dram_bytes_per_wave")
         except Exception:
             traffic = None
     wave_bytes = sum(algo.values()) / nprof
+    step_ms = ms / max(args.steps, 1)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": dom,
-                "launch": f"one wave's {dom} phase (its kernels back to back)",
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+                "launch": f"one wave's {dom} phase (its kernels back to back)", "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": per_wave_bytes, "launch_ms": per_wave_s * 1000.0,
                 "phase_ms_per_wave": {p: round(d[p]["ms"] / nprof, 4) for p in d}, "profiled_waves": nprof,
-                "wave": {"algorithmic_bytes": wave_bytes, "ms": ms / max(args.steps, 1),
-                         "achieved_gbs": wave_bytes / (ms / max(args.steps, 1) / 1000.0) / 1e9}}
+                "algorithmic_bytes_per_wave": {p: round(algo[p] / nprof) for p in algo},
+                "wave": {"algorithmic_bytes": wave_bytes, "ms": step_ms,
+                         "achieved_gbs": wave_bytes / (step_ms / 1000.0) / 1e9,
+                         "frac": wave_bytes / (step_ms / 1000.0) / 1e9 / peak}}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
-        r = oracle_sample(args.cpu_seconds, args.paths, args.capacity, args.protect, B, args.seed + 99)
-        cpu = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"{r['decisions']} decisions in {r['seconds']:.1f}s: one QAS round + set_protection + "
-                         f"ordered match/insert(+evict) on a {args.paths}-path (~1M-node) oracle tree "
-                         f"(oracle/ C restatement, single thread)"}
+    # ---- parity + CPU baseline (the oracle replica started at the top)
+    cpu = parity = None
+    if par_proc is not None:
+        dres = device_parity(args, engine_kw, world, rank, dev)
+        par_proc.join()
+        if par_proc.exitcode == 0:
+            o = np.load(par_path)
+            parity = compare_parity(dres, o, args.parity_waves, spec.path_len)
+            ndec, secs, total_s = o["timing"].tolist()
+            if rank == 0 and world == 1:
+                cpu = {"value": ndec / max(secs, 1e-9), "unit": UNIT, "cores": 1, "kind": "port",
+                       "sample": f"{int(ndec)} decisions in {secs:.1f}s: the {args.parity_waves} evicting "
+                                 f"{B}-request parity windows after a {args.warm}-request warm start to capacity "
+                                 f"(oracle/: C restatement of kvcache.py/scheduler.py, full scan + heap per evict, "
+                                 f"one thread; {total_s:.0f}s including the warm start)"}
+        else:
+            parity = {"waves_checked": 0, "identical": False, "differences": ["oracle process failed"]}
+        os.unlink(par_path)
+    if world > 1 and parity is not None:
+        flag = torch.tensor([1 if parity["identical"] else 0], dtype=torch.int64,
+                            device=dev if args.backend == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        parity["identical_all_shards"] = bool(flag.item())
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / max(args.steps, 1), "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {
-                "workload": "mu1M: DART tree warm-started with 125K paths (~1M nodes, ~16M tokens, "
-                            "capacity 16M tokens so every admission evicts); step = one 4096-request wave "
-                            "(device QAS round + protection + serialization + ordered match/insert/evict + "
-                            "release)",
-                "wave": B, "paths": args.paths, "capacity_tokens": args.capacity, "policy": "DART",
+                "workload": DESCR[args.workload], "name": spec.name, "wave": B, "path_tokens": spec.path_len,
+                "warm_requests": args.warm, "capacity_tokens": args.capacity, "policy": "DART",
                 "protect_budget": args.protect, "cold_quota": args.cold_quota,
-                "parallelism": f"replicas x{world} (segment-hash shards)",
+                "parallelism": f"replicas x{world} (splitmix64(skeleton[0]) mod {world} shards of one stream)",
                 "l2": "flushed between timed steps (256 MiB write)",
                 "tree_nodes": st2["live_nodes"], "resident_tokens": st2["resident"],
                 "warm_start_s": round(warm_s, 2), "admitted_per_rank": admitted,
@@ -498,8 +603,9 @@ def run_ours(args) -> None:
                 "profile": "per-phase device profile taken on extra waves after the timed region",
                 "commit": engine.wave_stats(),
                 "cuda_graph": engine.graph_stats(),
-                "last_list_build": engine.build_timeline(),
             },
+            "hit_rate": hit_rate,
+            "parity": parity,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -508,6 +614,7 @@ def run_ours(args) -> None:
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
+    engine.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -516,6 +623,12 @@ def main():
     args = parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     else:
         run_ours(args)
 

@@ -691,3 +691,31 @@ int64_t ot_edge_tokens(const OTree *t, int64_t id, uint32_t *out, int64_t cap) {
   if (out) memcpy(out, t->toks + n->tok_off, sizeof(uint32_t) * m);
   return n->len;
 }
+
+/* Every attached node (root excluded) as 11 int64 in node-id order:
+ * [id, parent, edge_len, kind, seg, ref, last, hits, prot, has_anchor, first_tok]
+ * -- the fields debug_nodes() lists (kvcache.py:473-492) plus the first edge
+ * token, for whole-tree parity at 1M nodes without per-node calls. */
+int64_t ot_dump(const OTree *t, int64_t *out, int64_t cap) {
+  int64_t k = 0;
+  for (int64_t id = 1; id < t->nnodes; id++) {
+    const ONode *n = &t->nodes[id];
+    if (!n->attached) continue;
+    if (out && k < cap) {
+      int64_t *o = out + 11 * k;
+      o[0] = id;
+      o[1] = n->parent;
+      o[2] = n->len;
+      o[3] = n->kind;
+      o[4] = n->seg;
+      o[5] = n->ref;
+      o[6] = n->last;
+      o[7] = n->hits;
+      o[8] = n->prot;
+      o[9] = n->has_anchor;
+      o[10] = n->len > 0 ? (int64_t)t->toks[n->tok_off] : -1;
+    }
+    k++;
+  }
+  return k;
+}

@@ -75,6 +75,8 @@ def _load() -> C.CDLL:
     lib.ot_edge_tokens.restype = _i64
     lib.ot_edge_tokens.argtypes = [_p, _i64, _p, _i64]
     lib.ot_evict_key.argtypes = [_p, _i64, _p, _p]
+    lib.ot_dump.restype = _i64
+    lib.ot_dump.argtypes = [_p, _p, _i64]
     lib.oq_round.restype = C.c_int
     lib.oq_round.argtypes = [_i64, _p, _p, _p, _p, _p, _i64, _p, _p, C.c_int32, _p] + [_p] * 16
     return lib

@@ -1,0 +1,210 @@
+"""Windowed parity driver: the CPU oracle run through the SAME serving-loop
+windows as the device's fused wave (``WaveEngine.step``), plus whole-tree
+comparison tables.
+
+TEST INFRASTRUCTURE ONLY (imported by tests/ and by bench.py's cpu_baseline
+leg, which both times the oracle and checks the device against it).
+
+One window (engine.py:171-213 as the device wave runs it):
+  1. release the previous window's admitted leaves (engine.py:177-181);
+  2. ``schedule_round(pending, active=[], ...)`` (scheduler.py:192-273);
+  3. ``set_protection(P-hat)`` for DART (engine.py:193-194) or
+     ``note_active_segments`` for LRU_ACTIVE (engine.py:195-197);
+  4. for every member in dispatch order: ``serialize_tokens`` of the aligned
+     skeleton (workload.py:136-164), ``match_prefix``, ``_build_anchors``
+     (engine.py:269-292), ``insert_path``; stop at the first CapacityError
+     (engine.py:209-212).
+Pending requests that were not admitted stay pending, in arrival order.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from oracle.oracle import OracleRadixCache, _ptr, lib as olib, oracle_round_arrays
+from paper_2605_08581_b200.qas_host import MarshaledRound
+from paper_2605_08581_b200.types import (
+    SEGMENT_TOKEN_BASE,
+    SUFFIX_TOKEN_BASE,
+    CacheConfig,
+    CachePolicy,
+    SchedulerConfig,
+)
+
+SEG_NONE64 = -(2**63)
+FIELDS = ("id", "parent", "edge_len", "kind", "seg", "ref", "last", "hits", "prot", "has_anchor", "first_tok")
+POOL_KEYS = ("ids", "arrival", "sk_off", "sk", "reorderable", "suffix")
+
+
+def concat_pools(a: dict | None, b: dict) -> dict:
+    """Pending CSR ``a`` followed by ``b``."""
+    if a is None or len(a["ids"]) == 0:
+        return {k: np.ascontiguousarray(v) for k, v in b.items()}
+    out = {}
+    for k in ("ids", "arrival", "reorderable", "suffix", "sk"):
+        out[k] = np.concatenate([a[k], b[k]])
+    out["sk_off"] = np.concatenate([a["sk_off"], a["sk_off"][-1] + b["sk_off"][1:]])
+    return out
+
+
+def drop_members(pool: dict, taken: np.ndarray) -> dict:
+    """The pending CSR without the (admitted) indices ``taken``, order kept."""
+    P = len(pool["ids"])
+    keep = np.ones(P, dtype=bool)
+    keep[np.asarray(taken, dtype=np.int64)] = False
+    idx = np.flatnonzero(keep)
+    lens = np.diff(pool["sk_off"])[idx]
+    off = np.zeros(len(idx) + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    rows = [pool["sk"][pool["sk_off"][i]:pool["sk_off"][i + 1]] for i in idx.tolist()]
+    sk = np.concatenate(rows).astype(np.int32) if rows else np.zeros(0, np.int32)
+    return {"ids": pool["ids"][idx], "arrival": pool["arrival"][idx], "sk_off": off, "sk": sk,
+            "reorderable": pool["reorderable"][idx], "suffix": pool["suffix"][idx]}
+
+
+class OracleReplica:
+    """One replica (tree + scheduler) on the CPU oracle, stepped window by window."""
+
+    def __init__(self, cache: CacheConfig, sched: SchedulerConfig, nseg: int, sys_len: int, chunk: int):
+        self.cache = OracleRadixCache(cache)
+        self.sched = sched
+        self.policy = cache.policy
+        self.nseg, self.sys_len, self.chunk = nseg, sys_len, chunk
+        self.L = olib()
+        self.prev: list[int] = []
+        self.segs = np.arange(nseg, dtype=np.int64)
+        self._leaf = np.zeros(1, np.int64)
+        self._nv = np.zeros(1, np.int64)
+        self.decision_seconds = 0.0
+        self.decisions = 0
+
+    def _path(self, rid: int, segs: np.ndarray, suffix: int) -> np.ndarray:
+        s, c = self.sys_len, self.chunk
+        p = np.empty(s + len(segs) * c + suffix, dtype=np.uint32)
+        p[:s] = np.arange(s)
+        p[s:s + len(segs) * c] = (SEGMENT_TOKEN_BASE + segs[:, None].astype(np.int64) * c + np.arange(c)).reshape(-1)
+        p[s + len(segs) * c:] = SUFFIX_TOKEN_BASE + rid * suffix + np.arange(suffix)
+        return p
+
+    def step(self, pool: dict, deadline: float | None = None) -> dict:
+        """One window over the pending CSR ``pool``; returns dispatch order
+        (pending indices), hits, leaf ids and the admitted count."""
+        L, h = self.L, self.cache._h
+        for leaf in self.prev:
+            L.ot_release(h, leaf)
+        self.prev = []
+        P = len(pool["ids"])
+        m = MarshaledRound(list(range(P)), self.segs, pool["ids"], pool["arrival"], pool["sk_off"],
+                           pool["sk"].astype(np.int32), pool["reorderable"], np.zeros(1, np.int64),
+                           np.zeros(0, np.int32))
+        t0 = time.perf_counter()
+        out = oracle_round_arrays(m, self.sched)
+        if self.policy is CachePolicy.DART:
+            dom = np.flatnonzero(out.dom)
+            self.cache.set_protection(dict(zip(dom.tolist(), out.prio[dom].tolist())))
+        elif self.policy is CachePolicy.LRU_ACTIVE:
+            self.cache.note_active_segments(np.flatnonzero((out.a > 0) | (out.nd > 0)).tolist())
+        members = np.concatenate([out.hot, out.cold]).astype(np.int64)
+        hits, leaves = [], []
+        for i in members.tolist():
+            lo, hi = int(pool["sk_off"][i]), int(pool["sk_off"][i + 1])
+            al = out.aligned[lo:hi].astype(np.int64)
+            rid, sfx = int(pool["ids"][i]), int(pool["suffix"][i])
+            p = self._path(rid, al, sfx)
+            k = len(al)
+            na = (1 if self.sys_len > 0 else 0) + k + (1 if sfx > 0 else 0)
+            a_off = np.empty(na, np.int64)
+            a_kind = np.empty(na, np.int8)
+            a_seg = np.full(na, SEG_NONE64, np.int64)
+            snaps = np.zeros(3 * na, np.int64)
+            j = 0
+            if self.sys_len > 0:
+                a_off[0], a_kind[0] = self.sys_len, 0
+                j = 1
+            a_off[j:j + k] = self.sys_len + self.chunk * np.arange(1, k + 1)
+            a_kind[j:j + k] = 1
+            a_seg[j:j + k] = al
+            snaps[3 * j:3 * (j + k)] = np.stack([out.g[al], out.a[al], out.nd[al]], axis=1).reshape(-1)
+            if sfx > 0:
+                a_off[na - 1], a_kind[na - 1] = len(p), 2
+            hit = L.ot_match(h, _ptr(p), len(p), None, _ptr(self._nv))
+            rc = L.ot_insert(h, _ptr(p), len(p), na, _ptr(a_off), _ptr(a_kind), _ptr(a_seg), _ptr(snaps),
+                             _ptr(self._leaf))
+            if rc == 1:  # CapacityError: the wave stops (engine.py:209-212)
+                break
+            if rc != 0:
+                raise ValueError(f"oracle insert failed ({rc})")
+            hits.append(int(hit))
+            leaves.append(int(self._leaf[0]))
+            if deadline is not None and time.perf_counter() > deadline:
+                break
+        el = time.perf_counter() - t0
+        self.decision_seconds += el
+        self.decisions += len(leaves)
+        self.prev = leaves
+        return {"members": members, "hits": np.array(hits, np.int64), "leaf_ids": np.array(leaves, np.int64),
+                "n_admitted": len(leaves), "seconds": el}
+
+    def table(self) -> np.ndarray:
+        n = int(self.L.ot_dump(self.cache._h, None, 0))
+        out = np.zeros((max(n, 1), 11), dtype=np.int64)
+        self.L.ot_dump(self.cache._h, _ptr(out), n)
+        out = out[:n]
+        out[out[:, 4] == SEG_NONE64, 4] = -1
+        return out
+
+    def victims(self) -> np.ndarray:
+        n = int(self.L.ot_victim_log(self.cache._h, None, 0))
+        out = np.zeros(max(n, 1), dtype=np.int64)
+        self.L.ot_victim_log(self.cache._h, _ptr(out), n)
+        return out[:n]
+
+    @property
+    def resident(self) -> int:
+        return int(self.L.ot_resident(self.cache._h))
+
+
+def device_table(view) -> np.ndarray:
+    """The same 11-column table from a device tree (``DeviceRadixCache`` view)."""
+    s = view._snapshot()
+    nid, par = s["nid"], s["par"]
+    n = len(nid)
+    live = np.flatnonzero((nid >= 0) & (par >= 0) & (np.arange(n) != 0))
+    seg = s["seg"][live].astype(np.int64)
+    seg[seg == -(2**31)] = -1
+    ftok = np.where(s["elen"][live] > 0, s["ftok"][live].astype(np.int64), -1)
+    t = np.stack([nid[live], nid[par[live]], s["elen"][live], s["kind"][live], seg, s["ref"][live],
+                  s["last"][live], s["hits"][live], s["prot"][live], s["hasanc"][live], ftok], axis=1)
+    t = t.astype(np.int64)
+    return t[np.argsort(t[:, 0], kind="stable")]
+
+
+def device_victims(view) -> np.ndarray:
+    total = view.stats()["victims"]
+    ids = np.zeros(max(total, 1), dtype=np.int64)
+    z8 = np.zeros(max(total, 1), dtype=np.int8)
+    z32 = np.zeros(max(total, 1), dtype=np.int32)
+    zu = np.zeros(max(total, 1), dtype=np.uint32)
+    z64 = np.zeros(max(total, 1), dtype=np.int64)
+    if total:
+        first = max(0, total - (1 << 20))  # the device ring keeps the last 2^20 records
+        cnt = total - first
+        from paper_2605_08581_b200._lib import check
+
+        check(view._L.prism_victims(view._h, first, cnt, _ptr(ids), _ptr(z8), _ptr(z32), _ptr(zu), _ptr(z32),
+                                    _ptr(z64)))
+        return ids[:cnt], first
+    return ids[:0], 0
+
+
+def compare_tables(a: np.ndarray, b: np.ndarray) -> str | None:
+    """None when identical, else a one-line description of the first difference."""
+    if a.shape != b.shape:
+        return f"node count {a.shape[0]} vs {b.shape[0]}"
+    diff = np.argwhere(a != b)
+    if len(diff) == 0:
+        return None
+    r, c = diff[0]
+    return f"node {a[r, 0]} field {FIELDS[c]}: {a[r, c]} vs {b[r, c]} ({len(np.unique(diff[:, 0]))} nodes differ)"

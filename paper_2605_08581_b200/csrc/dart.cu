@@ -303,10 +303,9 @@ int sort_compact(prism_tree *t, int64_t n, const Key3 *kin, const uint64_t *vin,
     return PRISM_OK;
   }
   if (n <= BSORT_MAX) {  // one CTA: bitonic sort in shared memory
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr = 0;
+    if (prism::attr_once(attr)) {
       CK(cudaFuncSetAttribute(k_block_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BSORT_SMEM));
-      attr = true;
     }
     k_block_sort<<<1, 1024, BSORT_SMEM, t->st>>>(kin, vin, (int)n, kout, vout);
     CK(cudaGetLastError());
@@ -369,13 +368,12 @@ int coop_grid(prism_tree *t) {
 template <class Cand>
 int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const int64_t *dW, int64_t min_cand,
                   bool sampled_already = false, bool big_in_finaliser = false) {
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr = 0;
+  if (prism::attr_once(attr)) {
     CK(cudaFuncSetAttribute(k_ss_select<EvictCand>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SEL_SMEM));
     CK(cudaFuncSetAttribute(k_ss_select<ProtCand>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SEL_SMEM));
     CK(cudaFuncSetAttribute(k_ss_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SORT_SMEM));
     CK(cudaFuncSetAttribute(k_ss_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_BIG_SMEM));
-    attr = true;
   }
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev));
@@ -536,10 +534,9 @@ int compact_arena(prism_tree *t, int64_t need) {
 
 // run the commit kernel until DONE/CAPACITY, servicing resumable stops
 int run_commit(prism_tree *t, CommitArgs a) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_set = 0;
+  if (prism::attr_once(attr_set)) {
     CK(cudaFuncSetAttribute(k_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)COMMIT_SMEM));
-    attr_set = true;
   }
   // a rebuild that made no progress (the prefix held only entries the stopped
   // call may not evict, e.g. its own guarded path) is retried with a doubled
@@ -1096,10 +1093,9 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out, int3
     if (sampled && f <= TF_MAX) {  // small budget: the positive-P-hat list and its top f
       int sms = 0;
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev));
-      static bool tf_attr = false;
-      if (!tf_attr) {
+      static uint64_t tf_attr = 0;
+      if (prism::attr_once(tf_attr)) {
         CK(cudaFuncSetAttribute(k_tf_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TF_MERGE_SMEM));
-        tf_attr = true;
       }
       k_tf_scan<<<4 * sms, SS_TPB, 0, t->st>>>(ProtCand{t->d, keys}, B);
       k_tf_local<<<2 * sms, SS_TPB, TF_SMEM, t->st>>>(B, ff);

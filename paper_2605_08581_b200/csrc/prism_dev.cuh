@@ -269,4 +269,17 @@ __device__ inline Key3 composite(Key3 kmax, int32_t dend) {
   return kmax;
 }
 
+// Function attributes (dynamic shared-memory limits) belong to a device
+// context: true the first time it is called for the current device with this
+// per-call-site bitmask, so a second tree / scheduler on another GPU of the
+// same process sets them again.
+inline bool attr_once(uint64_t &mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return true;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (mask & bit) return false;
+  mask |= bit;
+  return true;
+}
+
 }  // namespace prism

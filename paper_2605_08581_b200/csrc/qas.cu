@@ -970,11 +970,10 @@ int qas_run_multi(prism_qas *q, const QIn &in, int64_t P, int64_t A, int32_t nse
     int64_t nsel = 0;
     QCK(prism::sel_run(sb, P, nc, st, &nsel, &q->launches));
     if (nsel <= prism::BSORT_MAX) {
-      static bool attr = false;
-      if (!attr) {
+      static uint64_t attr = 0;
+      if (prism::attr_once(attr)) {
         QCK(cudaFuncSetAttribute(prism::k_block_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)prism::BSORT_SMEM));
-        attr = true;
       }
       prism::k_block_sort<<<1, 1024, prism::BSORT_SMEM, st>>>(q->cks, q->cvs, (int)nsel, (prism::Key3 *)q->ck2,
                                                               (uint64_t *)q->cv2);

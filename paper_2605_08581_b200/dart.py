@@ -168,7 +168,7 @@ class DeviceRadixCache:
         self._record = record_victims
         self._vlog_seen = 0
         self._victim_ids: list[int] = []
-        self._last: tuple[int, int] = (0, 0)  # victim-log range of the last evict call
+        self._last: tuple[int, int] | None = (0, 0)  # victim-log range of the last evict call
         self._snap_cache = None
         self._op = np.zeros(8, dtype=np.int64)
 
@@ -206,10 +206,14 @@ class DeviceRadixCache:
     def _dirty(self) -> None:
         self._snap_cache = None
 
+    _VLOG_DRAIN = 1 << 19  # half the device victim ring (dart.cu): drain before it wraps
+
     def _after_op(self) -> None:
         self._L.prism_last_op(self._h, _ptr(self._op))
         if self._op[0]:
             self._last = (int(self._op[1]), int(self._op[2]))
+            if self._record and int(self._op[2]) - self._vlog_seen > self._VLOG_DRAIN:
+                self._log_victims()
         self._dirty()
 
     TUNABLES = {"list_min_tokens": 0, "list_slack_tokens": 1, "sel_min_candidates": 2, "use_coop": 3,
@@ -298,6 +302,9 @@ class DeviceRadixCache:
 
     @property
     def last_evicted(self) -> list[DeviceNode]:
+        if self._last is None:
+            raise RuntimeError("last_evicted is not tracked across admit_wave (one batched call covers many "
+                               "evict calls); use victim_log()")
         first, end = self._last
         out = []
         for v in self._victims(first, end - first):
@@ -410,6 +417,9 @@ class DeviceRadixCache:
                                        _ptr(kind), _ptr(seg), _ptr(snap), _ptr(hits), _ptr(slots),
                                        _ptr(ids), _ptr(nadm)))
         self._dirty()
+        self._last = None
+        if self._record and self.stats()["victims"] - self._vlog_seen > self._VLOG_DRAIN:
+            self._log_victims()
         k = int(nadm[0])
         return hits[:k].tolist(), [DeviceNode(self, int(slots[i]), int(ids[i])) for i in range(k)]
 

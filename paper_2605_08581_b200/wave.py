@@ -211,6 +211,13 @@ class WaveEngine:
 
         return DeviceRadixCache.attach(self.t, self.cache_cfg)
 
+    def reusable_anchors(self) -> int:
+        """Live nodes carrying a REUSABLE anchor: the A of the protection scan's
+        16-A algorithmic bytes (kvcache.py:374-376)."""
+        s = self.cache_view()._snapshot()
+        live = (s["nid"] >= 0) & (s["par"] >= 0)
+        return int(np.count_nonzero(live & (s["hasanc"] != 0) & (s["akind"] == 1)))
+
     def profile(self, enable: bool) -> None:
         check(self.L.prism_profile(self.t, 1 if enable else 0))
         check(self.L.prism_qas_profile(self.q, 1 if enable else 0))
