@@ -191,7 +191,7 @@ def parity_windows(args, world: int, rank: int):
 def oracle_parity_job(args, world: int, rank: int, out_path: str) -> None:
     """Background process: the oracle replica through the parity windows."""
     from oracle.oracle import build
-    from oracle.windows import OracleReplica, concat_pools, drop_members
+    from oracle.windows import OracleReplica, oracle_windows
 
     build()
     cache, sched = _configs(args)
@@ -199,77 +199,21 @@ def oracle_parity_job(args, world: int, rank: int, out_path: str) -> None:
     rep = OracleReplica(cache, sched, spec.nseg, spec.sys_len, spec.chunk)
     warm, check = parity_windows(args, world, rank)
     t0 = time.perf_counter()
-    pend = None
-    res = {}
-    for i, pool in enumerate(warm + check):
-        pend = concat_pools(pend, pool)
-        if i == len(warm):
-            rep.decisions, rep.decision_seconds = 0, 0.0  # the CPU baseline times the evicting windows only
-            res["warm_s"] = time.perf_counter() - t0
-        r = rep.step(pend)
-        if i >= len(warm):
-            j = i - len(warm)
-            res[f"m{j}"], res[f"h{j}"], res[f"l{j}"] = r["members"], r["hits"], r["leaf_ids"]
-        pend = drop_members(pend, r["members"][: r["n_admitted"]])
-    res["table"] = rep.table()
-    res["victims"] = rep.victims()
-    res["resident"] = np.array([rep.resident])
-    res["timing"] = np.array([rep.decisions, rep.decision_seconds, time.perf_counter() - t0])
+    res = oracle_windows(rep, warm + check, record_from=len(warm))
+    res["timing"] = np.append(res["timing"], time.perf_counter() - t0)
     np.savez(out_path, **res)
 
 
 def device_parity(args, engine_kw, world: int, rank: int, dev) -> dict:
-    """A fresh device replica through the same windows; returns its outputs."""
-    from oracle.windows import concat_pools, device_table, device_victims, drop_members
-    from paper_2605_08581_b200.wave import DevicePending, WaveEngine
+    """A fresh device replica through the same windows."""
+    from oracle.windows import device_windows
+    from paper_2605_08581_b200.wave import WaveEngine
 
     eng = WaveEngine(**engine_kw)
     warm, check = parity_windows(args, world, rank)
-    pend, prev, out = None, 0, {}
-    for i, pool in enumerate(warm + check):
-        pend = concat_pools(pend, pool)
-        eng.release(eng.leaf_slots, prev)
-        nm, na = eng.step(DevicePending.from_host(pend["ids"], pend["arrival"], pend["sk_off"], pend["sk"],
-                                                  pend["reorderable"], pend["suffix"], dev))
-        members = eng.members[:nm].cpu().numpy()
-        if i >= len(warm):
-            j = i - len(warm)
-            out[f"m{j}"], out[f"h{j}"] = members, eng.hits[:na].cpu().numpy()
-            out[f"l{j}"] = eng.leaf_ids[:na].cpu().numpy()
-        prev = na
-        pend = drop_members(pend, members[:na])
-    view = eng.cache_view()
-    out["table"] = device_table(view)
-    out["victims"], out["vfirst"] = device_victims(view)
-    out["resident"] = view.resident_tokens
-    out["stats"] = eng.wave_stats()
+    out = device_windows(eng, warm + check, dev, record_from=len(warm))
     eng.close()
     return out
-
-
-def compare_parity(d: dict, o, waves: int, path_len: int) -> dict:
-    from oracle.windows import compare_tables
-
-    diffs = []
-    for j in range(waves):
-        for key, name in (("m", "dispatch order"), ("h", "hits"), ("l", "leaf ids")):
-            if not np.array_equal(np.asarray(d[f"{key}{j}"]), o[f"{key}{j}"]):
-                diffs.append(f"window {j}: {name}")
-    ov = o["victims"]
-    dv = d["victims"]
-    if not np.array_equal(dv, ov[d["vfirst"]:]) or d["vfirst"] + len(dv) != len(ov):
-        diffs.append(f"victims ({len(ov)} oracle, {d['vfirst'] + len(dv)} device)")
-    t = compare_tables(d["table"], o["table"])
-    if t:
-        diffs.append("tree: " + t)
-    if int(d["resident"]) != int(o["resident"][0]):
-        diffs.append("resident tokens")
-    adm = sum(len(o[f"l{j}"]) for j in range(waves))
-    hit = sum(int(o[f"h{j}"].sum()) for j in range(waves))
-    return {"waves_checked": waves, "identical": not diffs, "differences": diffs[:5],
-            "decisions_checked": adm, "victims_checked": int(len(ov)), "tree_nodes_checked": int(len(o["table"])),
-            "hit_rate": hit / max(adm * path_len, 1),
-            "device_commit": d["stats"]}
 
 
 # ---------------------------------------------------------------- reference arm
@@ -567,7 +511,9 @@ def run_ours(args) -> None:
         par_proc.join()
         if par_proc.exitcode == 0:
             o = np.load(par_path)
-            parity = compare_parity(dres, o, args.parity_waves, spec.path_len)
+            from oracle.windows import compare_windows
+
+            parity = compare_windows(dres, o, args.parity_waves, spec.path_len)
             ndec, secs, total_s = o["timing"].tolist()
             if rank == 0 and world == 1:
                 cpu = {"value": ndec / max(secs, 1e-9), "unit": UNIT, "cores": 1, "kind": "port",

@@ -208,3 +208,75 @@ def compare_tables(a: np.ndarray, b: np.ndarray) -> str | None:
         return None
     r, c = diff[0]
     return f"node {a[r, 0]} field {FIELDS[c]}: {a[r, c]} vs {b[r, c]} ({len(np.unique(diff[:, 0]))} nodes differ)"
+
+
+def oracle_windows(rep: OracleReplica, windows: list, record_from: int = 0) -> dict:
+    """Drive the oracle replica through ``windows`` (arrival pools; requests
+    not admitted stay pending).  Records dispatch order / hits / leaf ids of
+    the windows from ``record_from`` on, the victim log and the final tree."""
+    pend, res = None, {}
+    for i, pool in enumerate(windows):
+        pend = concat_pools(pend, pool)
+        if i == record_from:
+            rep.decisions, rep.decision_seconds = 0, 0.0
+        r = rep.step(pend)
+        if i >= record_from:
+            j = i - record_from
+            res[f"m{j}"], res[f"h{j}"], res[f"l{j}"] = r["members"], r["hits"], r["leaf_ids"]
+        pend = drop_members(pend, r["members"][: r["n_admitted"]])
+    res["table"] = rep.table()
+    res["victims"] = rep.victims()
+    res["resident"] = np.array([rep.resident])
+    res["timing"] = np.array([rep.decisions, rep.decision_seconds])
+    return res
+
+
+def device_windows(eng, windows: list, device, record_from: int = 0) -> dict:
+    """The same windows through a device replica (``WaveEngine.step``)."""
+    from paper_2605_08581_b200.wave import DevicePending
+
+    pend, prev, out = None, 0, {}
+    for i, pool in enumerate(windows):
+        pend = concat_pools(pend, pool)
+        eng.release(eng.leaf_slots, prev)
+        nm, na = eng.step(DevicePending.from_host(pend["ids"], pend["arrival"], pend["sk_off"], pend["sk"],
+                                                  pend["reorderable"], pend["suffix"], device))
+        members = eng.members[:nm].cpu().numpy()
+        if i >= record_from:
+            j = i - record_from
+            out[f"m{j}"], out[f"h{j}"] = members, eng.hits[:na].cpu().numpy()
+            out[f"l{j}"] = eng.leaf_ids[:na].cpu().numpy()
+        prev = na
+        pend = drop_members(pend, members[:na])
+    view = eng.cache_view()
+    out["table"] = device_table(view)
+    out["victims"], out["vfirst"] = device_victims(view)
+    out["resident"] = view.resident_tokens
+    out["stats"] = eng.wave_stats()
+    return out
+
+
+def compare_windows(d: dict, o, waves: int, path_len: int | None = None) -> dict:
+    """Parity verdict of device outputs ``d`` against oracle outputs ``o``."""
+    diffs = []
+    for j in range(waves):
+        for key, name in (("m", "dispatch order"), ("h", "hits"), ("l", "leaf ids")):
+            if not np.array_equal(np.asarray(d[f"{key}{j}"]), np.asarray(o[f"{key}{j}"])):
+                diffs.append(f"window {j}: {name}")
+    ov = np.asarray(o["victims"])
+    dv = d["victims"]
+    if d["vfirst"] + len(dv) != len(ov) or not np.array_equal(dv, ov[d["vfirst"]:]):
+        diffs.append(f"victims ({len(ov)} oracle, {d['vfirst'] + len(dv)} device)")
+    t = compare_tables(d["table"], np.asarray(o["table"]))
+    if t:
+        diffs.append("tree: " + t)
+    if int(d["resident"]) != int(np.asarray(o["resident"]).reshape(-1)[0]):
+        diffs.append("resident tokens")
+    adm = sum(len(o[f"l{j}"]) for j in range(waves))
+    hit = sum(int(np.asarray(o[f"h{j}"]).sum()) for j in range(waves))
+    out = {"waves_checked": waves, "identical": not diffs, "differences": diffs[:5], "decisions_checked": adm,
+           "victims_checked": int(len(ov)), "tree_nodes_checked": int(len(o["table"])),
+           "device_commit": d["stats"]}
+    if path_len:
+        out["hit_rate"] = hit / max(adm * path_len, 1)
+    return out

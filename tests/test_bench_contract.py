@@ -24,8 +24,8 @@ def _run(args, timeout=600):
 
 
 def test_reference_arm_line():
-    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1", "--paths", "3000", "--wave", "256",
-              "--capacity", "300000"])
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1", "--workload", "mu1m", "--warm", "3000",
+              "--wave", "256", "--capacity", "300000"])
     assert BASE_KEYS <= set(d)
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
@@ -34,8 +34,8 @@ def test_reference_arm_line():
 
 @pytest.mark.gpu
 def test_device_arm_line():
-    d = _run(["--steps", "4", "--warmup", "3", "--paths", "20000", "--wave", "1024", "--capacity", "2000000",
-              "--no-cpu-baseline", "--profile-steps", "2"])
+    d = _run(["--steps", "4", "--warmup", "3", "--workload", "mu1m", "--warm", "20000", "--wave", "1024",
+              "--capacity", "2000000", "--parity-waves", "1", "--profile-steps", "2"])
     assert BASE_KEYS <= set(d)
     assert d["value"] > 0 and d["unit"] == "decisions/s" and d["scaling"] == "weak"
     r = d["roofline"]
@@ -43,4 +43,27 @@ def test_device_arm_line():
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
     assert d["config"]["commit"]["parallel_waves"] > 0
+    assert 0 < d["hit_rate"] < 1
+    assert d["parity"]["identical"] and d["parity"]["waves_checked"] == 1, d["parity"]
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["value"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+@pytest.mark.gpu
+def test_device_arm_two_replicas_one_gpu():
+    """bench.py --gpus 2 relaunches itself under torch.distributed.run; both
+    replicas (here on cuda:0, gloo for the demand all-reduce) take their
+    segment-hash shard of one stream, and each shard matches the oracle."""
+    d = _run(["--gpus", "2", "--same-device", "--backend", "gloo", "--workload", "c3", "--warm", "1024",
+              "--wave", "256", "--capacity", "700000", "--steps", "3", "--warmup", "3", "--parity-waves", "1",
+              "--profile-steps", "1", "--e2e-steps", "2"], timeout=900)
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["parity"]["identical"] and d["parity"]["identical_all_shards"], d["parity"]
+    assert d["config"]["admitted_per_rank"] > 0
+    assert d["cpu_baseline"] is None  # the CPU baseline is an N=1 leg
+
+
+def test_reference_arm_n2():
+    d = _run(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1", "--workload", "mu1m",
+              "--warm", "2000", "--wave", "256", "--capacity", "200000", "--ref-seconds", "0.5"])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
