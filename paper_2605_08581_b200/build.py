@@ -25,10 +25,8 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def command(out: str = LIB, extra: list[str] | None = None) -> list[str]:
-    srcs = [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
+def flags(extra: list[str] | None = None) -> list[str]:
     return [
-        nvcc(),
         "-O3",
         "-std=c++17",
         *ARCH,
@@ -37,14 +35,21 @@ def command(out: str = LIB, extra: list[str] | None = None) -> list[str]:
         "--expt-relaxed-constexpr",
         "-Xcompiler",
         "-fPIC",
-        "-shared",
         "-I",
         os.path.join(ROOT, "include"),
         *(extra or []),
-        "-o",
-        out,
-        *srcs,
     ]
+
+
+def commands(out: str = LIB, extra: list[str] | None = None) -> tuple[list[list[str]], list[str]]:
+    """(one compile command per translation unit, the link command): the units
+    compile in parallel into build/, then one nvcc -shared links them."""
+    objdir = os.path.join(ROOT, "build")
+    srcs = [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
+    objs = [os.path.join(objdir, os.path.basename(s) + ".o") for s in srcs]
+    comp = [[nvcc(), *flags(extra), "-c", "-o", o, s] for s, o in zip(srcs, objs)]
+    link = [nvcc(), *ARCH, "-shared", "-o", out, *objs]
+    return comp, link
 
 
 def needs_build() -> bool:
@@ -57,10 +62,19 @@ def needs_build() -> bool:
 
 def build(force: bool = False, verbose: bool = True) -> str:
     if force or needs_build():
-        cmd = command()
+        comp, link = commands()
+        os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
+        procs = []
+        for cmd in comp:
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            procs.append((cmd, subprocess.Popen(cmd)))
+        for cmd, p in procs:
+            if p.wait() != 0:
+                raise subprocess.CalledProcessError(p.returncode, cmd)
         if verbose:
-            print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
+            print(" ".join(link), flush=True)
+        subprocess.run(link, check=True)
     return LIB
 
 

@@ -461,6 +461,9 @@ struct prism_qas {
   X(int32_t, longl) \
   X(int32_t, rk) \
   X(int32_t, emap) \
+  X(uint8_t, efirst) \
+  X(int32_t, btake) \
+  X(int32_t, bbase) \
   X(int64_t, gids) \
   X(int64_t, goff) \
   X(int32_t, gsfx) \
@@ -649,6 +652,9 @@ int qas_small_prepare(prism_qas *q, int64_t P, int32_t nseg, const QCfg &c, int6
   QCK(grow(&q->aligned, q->aligned_cap, P * qsmall::QS_SKCAP));
   QCK(grow(&q->rk, q->rk_cap, q->aligned_cap));
   QCK(grow(&q->emap, q->emap_cap, q->aligned_cap));
+  QCK(grow(&q->efirst, q->efirst_cap, q->aligned_cap));
+  QCK(grow(&q->btake, q->btake_cap, P));
+  QCK(grow(&q->bbase, q->bbase_cap, P));
   QCK(grow(&q->longl, q->longl_cap, P));
   QCK(grow(&q->sig, q->sig_cap, P * c.kappa));
   QCK(grow(&q->siglen, q->siglen_cap, P));
@@ -736,7 +742,10 @@ int qas_small_launch(prism_qas *q, const QIn &in, int64_t P, int64_t A, int64_t 
   qa.longl = q->longl;
   qa.rk = q->rk;
   qa.emap = q->emap;
-  qa.aligned_cap = std::min(std::min(q->aligned_cap, q->rk_cap), q->emap_cap);
+  qa.efirst = q->efirst;
+  qa.btake = q->btake;
+  qa.bbase = q->bbase;
+  qa.aligned_cap = std::min(std::min(std::min(q->aligned_cap, q->rk_cap), q->emap_cap), q->efirst_cap);
   qa.ts = q->prof_on ? q->qts : nullptr;
   const qsmall::QsCfg qc{c.budget, c.cold, c.front, c.kappa, c.wg, c.wa, c.wn, c.alpha, c.beta};
   if (G == 1) {
@@ -1460,12 +1469,12 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
     const void *ptrs[] = {members, hits, leaf_slots, leaf_ids, q->gids, q->goff, q->gsfx, q->garr, q->greo, q->gsk,
                           q->aligned, q->g, q->a, q->nd, q->prio, q->dom, q->poff, q->aoffs, q->plen, q->alen,
                           q->tok, q->a_off, q->a_kind, q->a_seg, q->a_snap, q->err, q->tmp_tot, q->qcounts, q->hres,
-                          q->touched, q->tn, q->rk, q->emap, q->longl, q->sig, q->siglen, q->tkey, q->tmin,
+                          q->touched, q->tn, q->rk, q->emap, q->efirst, q->btake, q->bbase, q->longl, q->sig, q->siglen, q->tkey, q->tmin,
                           q->slot_of, q->bmin, q->bstart, q->bend, q->score, q->take, q->rank, q->bucket, q->hot,
                           q->cv2, q->pk, q->pv, q->plist, host_out ? q->hout_mem : nullptr,
                           host_out ? q->hout_hit : nullptr};
     const int64_t dims[] = {P, B, G, btmask, nseg, sys_len, chunk, tok_cap, anc_cap, q->pk_cap, q->pv_cap,
-                            q->aligned_cap, q->rk_cap, q->emap_cap, (int64_t)q->prof_on};
+                            q->aligned_cap, q->rk_cap, q->emap_cap, q->efirst_cap, (int64_t)q->prof_on};
     const double cw[] = {c.wg, c.wa, c.wn, c.alpha, c.beta, (double)c.budget, (double)c.cold, (double)c.front,
                          (double)c.kappa};
     auto mixin = [&](const void *p, size_t n) {

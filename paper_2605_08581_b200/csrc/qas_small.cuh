@@ -19,13 +19,13 @@
 #pragma once
 #include <cooperative_groups.h>
 #include <cstdint>
-#include <cub/block/block_radix_sort.cuh>
 
 namespace qsmall {
 
 constexpr int QS_TPB = 1024;
 constexpr int QS_MAXP = 4096;  // bitonic sort capacity (shared memory)
-constexpr int QS_MAXK = 16;   // per-thread alignment; longer skeletons: a whole block
+constexpr int QS_MAXK = 16;   // alignment by a 16-lane group (two requests per warp)
+constexpr int QS_MAXW = 64;   // alignment by one warp (two entries per lane); longer skeletons: a whole block
 constexpr int QS_SKCAP = 64;  // skeleton entries per request provisioned (aligned, pair table)
 constexpr uint64_t QS_EMPTY = ~0ull;
 
@@ -60,6 +60,7 @@ struct QsArgs {
   uint64_t *btab_key;  // signature table, size 2*QS_MAXP (power of two)
   int32_t *btab_min, *slot_of, *bidx;
   int32_t *bsize, *nsegs;
+  int32_t *btake, *bbase;  // per bucket: hot-lane members taken, first hot-lane position
   long long *isum;
   uint64_t *ptab_key;  // (bucket, seg) pair table (the kernel uses 2*nsk slots of it)
   int32_t *ptab_cnt;
@@ -68,6 +69,7 @@ struct QsArgs {
   int32_t *longl;       // requests with skeletons longer than QS_MAXK
   int32_t *rk;          // rank scratch for them (aligned_cap ints)
   int32_t *emap;        // pending skeleton entry -> its request (aligned_cap ints)
+  uint8_t *efirst;      // pending skeleton entry is its segment's first occurrence in the skeleton
   int64_t aligned_cap;  // capacity of aligned / rk in skeleton entries
   unsigned long long *ts;  // QS_NTS phase stamps, or null
 };
@@ -222,7 +224,7 @@ __device__ inline void block_bitonic(QKey *k, int32_t *v, int n) {
   }
 }
 
-constexpr size_t QS_SMEM = (sizeof(QKey) + 3 * sizeof(int32_t)) * QS_MAXP;
+constexpr size_t QS_SMEM = (sizeof(QKey) + 2 * sizeof(int32_t)) * QS_MAXP;
 
 // 3. bucket of request i's signature tuple; first member via atomicMin
 // (scheduler.py:211-223).  Open addressing on (hash, first index seen).
@@ -300,6 +302,132 @@ __device__ inline bool qs_first(const int32_t *sk, int64_t b, int64_t e, int32_t
   for (int64_t q = b; q < e; q++)
     if (sk[q] == s) return false;
   return true;
+}
+
+// first-occurrence flags and the entry -> request map of request i's skeleton
+// [b, b+k), by one warp (count_segments' per-request dedup, scheduler.py:83-89):
+// k <= 64 by __match_any over the lanes (entries lane, lane+32), longer
+// skeletons by a strided backward scan
+__device__ inline void qs_flags_warp(const QsArgs &A, int64_t i, int64_t b, int64_t k) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  if (k <= QS_MAXW) {
+    const int32_t s0 = lane < k ? A.sk[b + lane] : -1;
+    const int32_t s1 = lane + 32 < k ? A.sk[b + lane + 32] : -1;
+    const bool f0 = (__match_any_sync(0xffffffffu, s0) & lt) == 0u;
+    bool f1 = (__match_any_sync(0xffffffffu, s1) & lt) == 0u;
+    if (k > 32) {
+#pragma unroll 8
+      for (int q = 0; q < 32; q++) f1 &= __shfl_sync(0xffffffffu, s0, q) != s1;
+    }
+    if (lane < k) {
+      A.emap[b + lane] = (int32_t)i;
+      A.efirst[b + lane] = f0 ? 1 : 0;
+    }
+    if (lane + 32 < k) {
+      A.emap[b + lane + 32] = (int32_t)i;
+      A.efirst[b + lane + 32] = f1 ? 1 : 0;
+    }
+  } else {
+    for (int64_t e = b + lane; e < b + k; e += 32) {
+      int32_t s = 0;
+      A.emap[e] = (int32_t)i;
+      A.efirst[e] = qs_first(A.sk, b, e, s) ? 1 : 0;
+    }
+  }
+}
+
+// one selection candidate: (priority, segment, index) -- ranked by (-pri, seg, index)
+struct QsCand {
+  double p;
+  int32_t s, x;
+  bool v;
+};
+__device__ __forceinline__ bool qs_cand_better(const QsCand &a, const QsCand &b) {
+  return a.v && (!b.v || qrank_before(a.p, a.s, a.x, b.p, b.s, b.x));
+}
+// the warp's best candidate (every lane gets it; a strict total order, so the
+// butterfly converges to the same element everywhere)
+__device__ __forceinline__ QsCand qs_warp_best(QsCand m) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    QsCand y;
+    y.p = __shfl_xor_sync(0xffffffffu, m.p, o);
+    y.s = __shfl_xor_sync(0xffffffffu, m.s, o);
+    y.x = __shfl_xor_sync(0xffffffffu, m.x, o);
+    y.v = __shfl_xor_sync(0xffffffffu, m.v ? 1 : 0, o) != 0;
+    if (qs_cand_better(y, m)) m = y;
+  }
+  return m;
+}
+
+// front_align + make_signature (scheduler.py:109-143) of request i with
+// QS_MAXK < k <= QS_MAXW skeleton entries by ONE warp, lane holding entries
+// lane and lane+32 in registers.  The top-f (front) and the top-kappa
+// (signature) are found by f resp. kappa warp-argmax selection rounds over
+// (-pri, seg, index) -- the sorted prefixes the reference takes -- so the cost
+// is O((f + kappa) log 32) shuffles, not a k^2 rank count.
+__device__ inline void qs_align_warp(const QsArgs &A, const QsCfg &c, int64_t i, int64_t b, int k, bool reo) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  int32_t s[2];
+  double p[2];
+  bool v[2];
+  int pos[2] = {lane, lane + 32};
+#pragma unroll
+  for (int u = 0; u < 2; u++) {
+    v[u] = lane + 32 * u < k;
+    s[u] = v[u] ? A.sk[b + lane + 32 * u] : 0;
+    p[u] = v[u] ? qpri0(c, A.g, A.a, s[u]) : 0.0;
+  }
+  if (reo) {  // the top-f to the front in rank order, the rest stable (109-129)
+    const int f = (int)(c.front < k ? c.front : k);
+    int rk[2] = {-1, -1};
+    for (int t = 0; t < f; t++) {
+      QsCand m0{p[0], s[0], lane, v[0] && rk[0] < 0}, m1{p[1], s[1], lane + 32, v[1] && rk[1] < 0};
+      const QsCand w = qs_warp_best(qs_cand_better(m1, m0) ? m1 : m0);
+      if (w.x == lane) rk[0] = t;
+      if (w.x == lane + 32) rk[1] = t;
+    }
+    const unsigned rlo = __ballot_sync(0xffffffffu, v[0] && rk[0] < 0);
+    const unsigned rhi = __ballot_sync(0xffffffffu, v[1] && rk[1] < 0);
+    pos[0] = rk[0] >= 0 ? rk[0] : f + __popc(rlo & lt);
+    pos[1] = rk[1] >= 0 ? rk[1] : f + __popc(rlo) + __popc(rhi & lt);
+  }
+#pragma unroll
+  for (int u = 0; u < 2; u++)
+    if (v[u]) A.aligned[b + pos[u]] = s[u];
+  // signature: the top-kappa by (-pri, seg, aligned position), emitted in aligned order (132-143)
+  const int kk = (int)(c.kappa < k ? c.kappa : k);
+  bool ch[2] = {false, false};
+  for (int t = 0; t < kk; t++) {
+    QsCand m0{p[0], s[0], pos[0], v[0] && !ch[0]}, m1{p[1], s[1], pos[1], v[1] && !ch[1]};
+    const QsCand w = qs_warp_best(qs_cand_better(m1, m0) ? m1 : m0);
+    ch[0] |= v[0] && w.x == pos[0];
+    ch[1] |= v[1] && w.x == pos[1];
+  }
+  unsigned mlo = 0u, mhi = 0u;  // chosen aligned positions
+#pragma unroll
+  for (int u = 0; u < 2; u++)
+    if (ch[u]) {
+      if (pos[u] < 32) mlo |= 1u << pos[u];
+      else mhi |= 1u << (pos[u] - 32);
+    }
+  mlo = __reduce_or_sync(0xffffffffu, mlo);
+  mhi = __reduce_or_sync(0xffffffffu, mhi);
+#pragma unroll
+  for (int u = 0; u < 2; u++)
+    if (ch[u]) {
+      const int before = pos[u] < 32 ? __popc(mlo & ((1u << pos[u]) - 1u))
+                                     : __popc(mlo) + __popc(mhi & ((1u << (pos[u] - 32)) - 1u));
+      A.sig[i * c.kappa + before] = s[u];
+    }
+  __syncwarp();
+  if (lane == 0) {
+    const int sl = k > 0 ? kk : 0;
+    A.siglen[i] = sl;
+    qs_bucket_insert(A, c, i, sl);  // 3.
+  }
 }
 
 // warp-aggregated append of c items at *ctr (int32 counter); returns this
@@ -439,10 +567,8 @@ __device__ inline void qs_cold_lane(const QsArgs &A, const QsCfg &c, int64_t P, 
   for (int64_t t = tid; t < nc * QS_MAXK; t += nt) {
     const int64_t i = sv[t / QS_MAXK];
     const int64_t b = A.off[i], e = A.off[i + 1];
-    for (int64_t x = b + t % QS_MAXK; x < e; x += QS_MAXK) {
-      int32_t s = 0;
-      if (qs_first(A.sk, b, x, s)) atomicAdd(&A.nd[s], 1);
-    }
+    for (int64_t x = b + t % QS_MAXK; x < e; x += QS_MAXK)
+      if (A.efirst[x]) atomicAdd(&A.nd[A.sk[x]], 1);
   }
 }
 
@@ -455,7 +581,6 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   QKey *sk = reinterpret_cast<QKey *>(qs_smem);
   int32_t *sv = reinterpret_cast<int32_t *>(sk + QS_MAXP);
   int32_t *scnt = sv + QS_MAXP;  // per-bucket counters / scan scratch
-  int32_t *sbk = scnt + QS_MAXP;  // bucket of each request (block 0)
   __shared__ int32_t swarp[32];
   const int tid = threadIdx.x;
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + tid, gs = (int64_t)gridDim.x * blockDim.x;
@@ -491,10 +616,12 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
     A.ptab_cnt[i] = 0;
   }
   if (gt == 0) A.touched_n[0] = 0;
-  for (int64_t i0 = 0; i0 < P; i0 += gs) {  // entry -> request map of the pending skeletons
-    const int64_t i = i0 + qs_ilv(gs);
-    if (i < P)
-      for (int64_t e = A.off[i]; e < A.off[i + 1]; e++) A.emap[e] = (int32_t)i;
+  {  // entry -> request map + first-occurrence flags of the pending skeletons: one warp per request
+    const int64_t nw = gs >> 5;
+    for (int64_t w0 = 0; w0 < P; w0 += nw) {
+      const int64_t i = w0 + (int64_t)(tid >> 5) * gridDim.x + blockIdx.x;  // warps interleaved over the CTAs
+      if (i < P) qs_flags_warp(A, i, A.off[i], A.off[i + 1] - A.off[i]);  // (warp-uniform)
+    }
   }
   qs_gsync();
   QS_TS(1);
@@ -505,7 +632,8 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
     const int64_t e = e0 + qs_ilv(gs);
     int32_t s = 0;
     bool nt = false;
-    if (e < nsk && qs_first(A.sk, A.off[A.emap[e]], e, s)) {
+    if (e < nsk && A.efirst[e]) {
+      s = A.sk[e];
       atomicAdd(&A.g[s], 1);
       unsigned long long *f = (unsigned long long *)&A.prio[s];
       nt = __ldcg(f) == 0ull && atomicCAS(f, 0ull, 0xFFF0000000000001ull) == 0ull;
@@ -553,8 +681,8 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
       const bool vi = i < P;
       const int64_t b = vi ? A.off[i] : 0;
       const int k = vi ? (int)(A.off[i + 1] - b) : 0;
-      const bool lng = k > QS_MAXK;
-      if (vi && lng && gl == 0) A.longl[atomicAdd((unsigned long long *)&A.counts[4], 1ull)] = (int32_t)i;
+      const bool lng = k > QS_MAXK;  // a warp's (below) or a block's (k > QS_MAXW, listed)
+      if (vi && k > QS_MAXW && gl == 0) A.longl[atomicAdd((unsigned long long *)&A.counts[4], 1ull)] = (int32_t)i;
       const bool on = vi && !lng && gl < k;
       const int32_t sj = on ? A.sk[b + gl] : 0;
       const double pj = on ? qpri0(c, A.g, A.a, sj) : 0.0;
@@ -599,6 +727,15 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
         qs_bucket_insert(A, c, i, sl);  // 3.
       }
     }
+    // QS_MAXK < k <= QS_MAXW: one warp per request
+    const int64_t nw = gs >> 5;
+    for (int64_t w0 = 0; w0 < P; w0 += nw) {
+      const int64_t i = w0 + (int64_t)(tid >> 5) * gridDim.x + blockIdx.x;
+      if (i >= P) continue;  // (warp-uniform)
+      const int64_t b = A.off[i];
+      const int64_t k = A.off[i + 1] - b;
+      if (k > QS_MAXK && k <= QS_MAXW) qs_align_warp(A, c, i, b, (int)k, A.reo[i] != 0);
+    }
   }
   qs_gsync();
   const int64_t nlong = (int64_t)__ldcg((const unsigned long long *)&A.counts[4]);
@@ -618,80 +755,50 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
     }
     qs_gsync();
   }
-  // 3b. every request's bucket representative = its bucket's first member
-  // (final now that every insert is done), into bidx (scratch until phase 10)
-  for (int64_t i0 = 0; i0 < P; i0 += gs) {
-    const int64_t i = i0 + qs_ilv(gs);
-    if (i < P) A.bidx[i] = qs_ld(&A.btab_min[qs_ld(&A.slot_of[i])]);
-  }
-  qs_gsync();
   QS_TS(3);
-  // 4. (block 0) bucket creation order = order of first members; in-bucket
-  // ranks in pending order (211-223): a stable block radix sort of the bucket
-  // ids (items in pending order) gives each request its position in its bucket
-  if (b0) {
-    using BRS = cub::BlockRadixSort<unsigned, QS_TPB, QS_MAXP / QS_TPB, unsigned>;
-    constexpr int IPT = QS_MAXP / QS_TPB;
-    int32_t *bstart = scnt;  // [nb] first sorted position of each bucket
-    // bucket ids: exclusive count of first members before each first member
-    unsigned first[IPT], fl[IPT];
-    unsigned my = 0;
+  // 4. bucket creation order = order of first members; in-bucket ranks in
+  // pending order (211-223), grid-parallel by counting: every CTA lists each
+  // request's first member in shared memory, then one warp per request counts
+  // the first members before its bucket's (= its bucket id) and its bucket's
+  // members before it (= its rank); a first member also counts its bucket's size
+  {
+    int32_t *sfirst = sv;  // [P <= QS_MAXP]
+    // a request's bucket representative = its bucket's first member (final now that every insert is done)
+    for (int64_t i = tid; i < P; i += blockDim.x) sfirst[i] = qs_ld(&A.btab_min[qs_ld(&A.slot_of[i])]);
+    __syncthreads();
+    const int lane = tid & 31;
+    const int64_t nw = gs >> 5;
+    for (int64_t i = (int64_t)(tid >> 5) * gridDim.x + blockIdx.x; i < P; i += nw) {
+      const int32_t f = sfirst[i];
+      const bool last = i == P - 1;  // (warp-uniform) also counts every bucket
+      int32_t nbef = 0, rk = 0, sz = 0, nall = 0;
+      for (int32_t j = lane; j < (int32_t)i; j += 32) {
+        const int32_t x = sfirst[j];
+        nbef += (j < f && x == j) ? 1 : 0;
+        rk += x == f ? 1 : 0;
+      }
+      if (f == (int32_t)i)
+        for (int32_t j = (int32_t)i + lane; j < (int32_t)P; j += 32) sz += sfirst[j] == f ? 1 : 0;
+      if (last)
+        for (int32_t j = lane; j < (int32_t)P; j += 32) nall += sfirst[j] == j ? 1 : 0;
 #pragma unroll
-    for (int u = 0; u < IPT; u++) {
-      const int64_t i = (int64_t)tid * IPT + u;
-      first[u] = i < P ? (unsigned)qs_ld(&A.bidx[i]) : 0u;
-      fl[u] = (i < P && first[u] == (unsigned)i) ? 1u : 0u;
-      my += fl[u];
-    }
-    sbk[tid] = (int32_t)my;
-    __syncthreads();
-    const int32_t nb = block_exscan(sbk, QS_TPB, swarp);  // per-thread exclusive first-member counts
-    unsigned run = (unsigned)sbk[tid];
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < IPT; u++) {  // sbk[first member] = its bucket id
-      const int64_t i = (int64_t)tid * IPT + u;
-      if (fl[u]) sbk[i] = (int32_t)run;
-      run += fl[u];
-    }
-    __syncthreads();
-    unsigned key[IPT], val[IPT];
-#pragma unroll
-    for (int u = 0; u < IPT; u++) {
-      const int64_t i = (int64_t)tid * IPT + u;
-      key[u] = i < P ? (unsigned)sbk[first[u]] : (unsigned)nb;  // padding (bucket id nb) sorts last
-      val[u] = (unsigned)i;
-    }
-    __syncthreads();
-    static_assert(sizeof(typename BRS::TempStorage) <= sizeof(QKey) * QS_MAXP, "radix-sort storage");
-    typename BRS::TempStorage &ts = *reinterpret_cast<typename BRS::TempStorage *>(sk);
-    // stable: pending order inside a bucket; only the bits of ids <= nb
-    BRS(ts).Sort(key, val, 0, 32 - __clz(nb > 0 ? nb : 1));
-    __syncthreads();
-    // thread tid now holds sorted positions tid*IPT + u; sv: the sorted keys
-#pragma unroll
-    for (int u = 0; u < IPT; u++) sv[tid * IPT + u] = (int32_t)key[u];
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < IPT; u++) {
-      const int pos = tid * IPT + u;
-      if (pos < P && (pos == 0 || sv[pos - 1] != (int32_t)key[u])) bstart[key[u]] = pos;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < IPT; u++) {
-      const int pos = tid * IPT + u;
-      if (pos >= P) continue;
-      const int32_t b = (int32_t)key[u];
-      A.rank[val[u]] = pos - bstart[b];
-      A.bucket[val[u]] = b;
-      if (pos == (int)P - 1 || sv[pos + 1] != b) {  // last of its bucket
-        A.bsize[b] = pos - bstart[b] + 1;
-        A.nsegs[b] = 0;
-        A.isum[b] = 0;
+      for (int o = 16; o > 0; o >>= 1) {
+        nbef += __shfl_xor_sync(0xffffffffu, nbef, o);
+        rk += __shfl_xor_sync(0xffffffffu, rk, o);
+        sz += __shfl_xor_sync(0xffffffffu, sz, o);
+        nall += __shfl_xor_sync(0xffffffffu, nall, o);
+      }
+      if (lane == 0) {
+        A.rank[i] = rk;
+        A.bucket[i] = nbef;
+        if (f == (int32_t)i) {
+          A.bsize[nbef] = sz;
+          A.nsegs[nbef] = 0;
+          A.isum[nbef] = 0;
+        }
+        if (last) A.counts[2] = nall;
       }
     }
-    if (tid == 0) A.counts[2] = nb;
   }
   qs_gsync();
   QS_TS(4);
@@ -704,7 +811,8 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
     int32_t npos = 0;
     if (e < nsk) {
       const int64_t i = A.emap[e];
-      if (qs_first(A.sk, A.off[i], e, s)) {
+      if (A.efirst[e]) {
+        s = A.sk[e];
         bk = A.bucket[i];
         const int prov = A.rank[i] < hot_cap ? 1 : 0;
         const uint64_t key = ((uint64_t)(uint32_t)bk << 32) | (uint32_t)s;
@@ -725,7 +833,6 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
           }
           pos = (pos + 1) & pmask;
         }
-        if (np) atomicAdd(&A.nsegs[bk], 1);
       }
     }
     const int p = qs_block_reserve(np ? 1 : 0, (int32_t *)&A.counts[5]);  // (low word of the zeroed int64)
@@ -741,7 +848,11 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   {
     const int32_t nbk = (int32_t)__ldcg((const unsigned long long *)&A.counts[2]);
     unsigned long long *lsum = reinterpret_cast<unsigned long long *>(sk);  // [nbk <= QS_MAXP]
-    for (int q = tid; q < nbk; q += blockDim.x) lsum[q] = 0ull;
+    int32_t *lcnt = reinterpret_cast<int32_t *>(lsum + QS_MAXP);              // distinct segments per bucket
+    for (int q = tid; q < nbk; q += blockDim.x) {
+      lsum[q] = 0ull;
+      lcnt[q] = 0;
+    }
     __syncthreads();
     for (int64_t t0 = 0; t0 < npairs; t0 += gs) {
       const int64_t t = t0 + gt;
@@ -754,39 +865,50 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
         const double t2 = __dmul_rn(c.wa, (double)A.a[s]);
         const double t3 = __dmul_rn(c.wn, (double)qs_ld(&A.ptab_cnt[pos]));
         atomicAdd(&lsum[bk], (unsigned long long)(long long)__dadd_rn(__dadd_rn(t1, t2), t3));
+        atomicAdd(&lcnt[bk], 1);
       }
     }
     __syncthreads();
-    for (int q = tid; q < nbk; q += blockDim.x)
+    for (int q = tid; q < nbk; q += blockDim.x) {
       if (lsum[q]) atomicAdd((unsigned long long *)&A.isum[q], lsum[q]);
+      if (lcnt[q]) atomicAdd(&A.nsegs[q], lcnt[q]);
+    }
     __syncthreads();  // (sk is block 0's scratch in the next phase)
   }
   qs_gsync();
   QS_TS(6);
-  // 9. (block 0) scores, the (-score, creation order) sort (234), hot-lane
-  // prefix sums of bucket sizes in that order (235-240)
+  // 9. scores (146-171), the (-score, creation order) order (234) and the
+  // hot-lane fill (235-240) without a sort: every CTA lists all nb bucket keys
+  // in shared memory, then one warp per bucket counts the keys before its own
+  // -- its position -- and sums their sizes: the hot-lane base
   const int32_t nb = (int32_t)__ldcg((const unsigned long long *)&A.counts[2]);
-  if (b0) {
+  {
+    int32_t *ssz = sv;
     for (int b = tid; b < nb; b += blockDim.x) {
       const int32_t ns = qs_ld(&A.nsegs[b]);
       const long long is = (long long)__ldcg((const unsigned long long *)&A.isum[b]);
       const double util = ns > 0 ? __ddiv_rn((double)is, (double)ns) : 0.0;
-      const double sc = __dadd_rn(__dmul_rn(c.alpha, (double)A.bsize[b]), __dmul_rn(c.beta, util));
-      A.score[b] = sc;
+      const int32_t bs = qs_ld(&A.bsize[b]);
+      const double sc = __dadd_rn(__dmul_rn(c.alpha, (double)bs), __dmul_rn(c.beta, util));
+      if (b0) A.score[b] = sc;
       sk[b] = {qord(-sc), (uint64_t)b};
-      sv[b] = b;
+      ssz[b] = bs;
     }
     __syncthreads();
-    block_bitonic(sk, sv, nb);
-    for (int q = tid; q < nb; q += blockDim.x) scnt[q] = A.bsize[sv[q]];
-    __syncthreads();
-    block_exscan(scnt, nb, swarp);
-    for (int q = tid; q < nb; q += blockDim.x) {
-      const int32_t b = sv[q];
-      int64_t take = hot_cap - scnt[q];
-      take = take < 0 ? 0 : (take > A.bsize[b] ? A.bsize[b] : take);
-      A.nsegs[b] = (int32_t)take;                         // reuse: take
-      A.isum[b] = scnt[q] < hot_cap ? scnt[q] : hot_cap;  // reuse: base
+    const int lane = tid & 31;
+    const int64_t nw = gs >> 5;
+    for (int64_t b = (int64_t)(tid >> 5) * gridDim.x + blockIdx.x; b < nb; b += nw) {
+      const QKey kb = sk[b];
+      int32_t before = 0;
+      for (int j = lane; j < nb; j += 32) before += qk_less(sk[j], kb) ? ssz[j] : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+      if (lane == 0) {
+        int64_t take = hot_cap - before;
+        take = take < 0 ? 0 : (take > ssz[b] ? ssz[b] : take);
+        A.btake[b] = (int32_t)take;
+        A.bbase[b] = before < hot_cap ? before : (int32_t)hot_cap;
+      }
     }
   }
   qs_gsync();
@@ -797,9 +919,9 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
     bool lf = false;
     if (i < P) {
       const int32_t b = A.bucket[i];
-      const bool h = A.rank[i] < qs_ld(&A.nsegs[b]);
+      const bool h = A.rank[i] < qs_ld(&A.btake[b]);
       A.bidx[i] = h ? 1 : 0;  // reuse: hot flag
-      if (h) A.hot[(int64_t)__ldcg((const unsigned long long *)&A.isum[b]) + A.rank[i]] = i;
+      if (h) A.hot[(int64_t)qs_ld(&A.bbase[b]) + A.rank[i]] = i;
       lf = !h;
     }
     // leftovers (cold lane), one counter atomic per CTA (low word of the zeroed int64)
@@ -811,8 +933,7 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
     if (e >= nsk) continue;
     const int64_t i = A.emap[e];
     const int32_t b = A.bucket[i];
-    int32_t s = 0;
-    if (A.rank[i] < qs_ld(&A.nsegs[b]) && qs_first(A.sk, A.off[i], e, s)) atomicAdd(&A.nd[s], 1);
+    if (A.efirst[e] && A.rank[i] < qs_ld(&A.btake[b])) atomicAdd(&A.nd[A.sk[e]], 1);
   }
   qs_gsync();
   QS_TS(8);

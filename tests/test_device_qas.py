@@ -99,6 +99,45 @@ def test_long_skeletons(small):
                 h.signature, h.rank, h.aligned_skeleton, h.counter_snapshot), (r, rid)
 
 
+@pytest.mark.parametrize("case", range(6))
+def test_warp_aligned_skeletons(case):
+    """Skeletons of 17..64 segments (the agent / C3 regime, k=40) are aligned
+    by one warp per request with selection rounds: duplicates, equal
+    priorities (seg / index tie-breaks), fronts and signatures from 1 to wider
+    than k, reorderable and not, mixed with short (16-lane) and long (block)
+    skeletons in one round."""
+    from paper_2605_08581_b200.qas import DeviceScheduler
+
+    ds = DeviceScheduler()
+    ds.set_small(4096)
+    rng = np.random.default_rng(100 + case)
+    P = [64, 500, 4096, 1000, 3, 2000][case]
+    nseg = [40, 300, 5000, 64, 20, 100000][case]
+    front, kappa = [(3, 1), (40, 4), (70, 64), (2, 2), (64, 64), (3, 1)][case]
+
+    def skel(i):
+        k = int(rng.choice([17, 31, 32, 33, 40, 63, 64])) if i % 7 else int(rng.choice([1, 5, 16, 65, 90]))
+        if case % 2:  # duplicates allowed
+            return [int(x) for x in rng.integers(0, nseg, size=k)]
+        return [int(x) for x in rng.choice(max(nseg, k), size=k, replace=False)]
+
+    pend = [Request(i, float(rng.integers(0, 50)), skel(i), bool(rng.random() < [0.0, 0.5, 1.0][case % 3]), [],
+                    8, 32, 4) for i in range(P)]
+    act = [Request(10**6 + j, 0.0, [int(x) for x in rng.integers(0, nseg, size=40)], True, [], 8, 8, 4)
+           for j in range(case)]
+    cfg = SchedulerConfig(dispatch_budget=min(P, 1024), cold_quota=min(P, 16), front_width=front,
+                          signature_size=kappa)
+    bd = ds.schedule_round(pend, act, cfg, 0.0)
+    bo = oracle_schedule_round(pend, act, cfg)
+    assert [r_.id for r_ in bd.members] == [r_.id for r_ in bo.members]
+    assert bd.priorities == bo.priorities and bd.bucket_scores == bo.bucket_scores
+    assert bd.counters.g == bo.counters.g and bd.counters.a == bo.counters.a and bd.counters.n == bo.counters.n
+    for rid, h in bo.hints.items():
+        d = bd.hints[rid]
+        assert (d.signature, d.rank, d.aligned_skeleton, d.counter_snapshot) == (
+            h.signature, h.rank, h.aligned_skeleton, h.counter_snapshot), rid
+
+
 class TestScheduleRound:
     def test_single_request(self):
         b = sched([make_request(0, [3, 1])], [], SchedulerConfig(dispatch_budget=4, cold_quota=1))

@@ -26,33 +26,33 @@ import bench  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--wave", type=int, default=4096)
-    ap.add_argument("--paths", type=int, default=125_000)
+    ap.add_argument("--workload", default="c3", choices=sorted(bench.DEFAULTS))
     args = ap.parse_args()
     import torch
 
-    from paper_2605_08581_b200.types import CacheConfig, CachePolicy, SchedulerConfig
+    from traces import synth as S
     from paper_2605_08581_b200.wave import DevicePending, WaveEngine
 
-    B = args.wave
-    eng = WaveEngine(CacheConfig(capacity_tokens=16_000_000, policy=CachePolicy.DART, protect_budget=20),
-                     SchedulerConfig(dispatch_budget=B, cold_quota=64), bench.NSEG, bench.SYS_LEN, bench.CHUNK,
-                     device=0, initial_slots=1 << 21, initial_arena_tokens=1 << 26)
+    d = bench.DEFAULTS[args.workload]
+    spec = S.SPECS[args.workload]
+    B = d["wave"]
+    ns = argparse.Namespace(capacity=d["capacity"], protect=20, wave=B, cold_quota=64)
+    cache, sched = bench._configs(ns)
+    eng = WaveEngine(cache, sched, spec.nseg, spec.sys_len, spec.chunk, device=0, initial_slots=1 << 21,
+                     initial_arena_tokens=max(1 << 26, 4 * d["capacity"]))
     L = eng.L
     L.prism_qas_small_timeline.argtypes = [C.c_void_p, C.c_void_p, C.c_int32]
-    rng = np.random.default_rng(0)
+    st = S.ShardStream(args.workload, 0, 1, 0)
 
     def dev(pool):
         return DevicePending.from_host(pool["ids"], pool["arrival"], pool["sk_off"], pool["sk"],
                                        pool["reorderable"], pool["suffix"], torch.device("cuda", 0))
 
-    nid, prev = 0, 0
-    while nid < args.paths:
-        n = min(B, args.paths - nid)
+    prev = 0
+    for i in range(0, d["warm"], B):
         eng.release(eng.leaf_slots, prev)
-        _, prev = eng.step(dev(bench.make_pool(nid, n, rng)))
-        nid += n
-    pools = [dev(bench.make_pool(nid + s * B, B, rng)) for s in range(args.steps + 2)]
+        _, prev = eng.step(dev(st.take(min(B, d["warm"] - i))))
+    pools = [dev(st.take(B)) for s in range(args.steps + 2)]
     for s in range(2):
         eng.release(eng.leaf_slots, prev)
         _, prev = eng.step(pools[s])
