@@ -1494,15 +1494,23 @@ __global__ void __launch_bounds__(SS_TPB) k_tf_scan(ProtCand cand, CoopBufs B) {
   if (lane == 0 && ccount) atomicAdd(&B.st->ss_cand, ccount);
 }
 
-// every CTA: the f smallest keys of its TF_SLICE-item slices of the list -> B.ks/vs[slice * f ..]
+// every CTA: the f smallest keys of ITS slices of the list (slices c = blockIdx.x,
+// + gridDim.x, ...) -> B.ks/vs[blockIdx.x * f ..]: each TF_SLICE-item slice is
+// sorted in shared memory and its top f merged into the CTA's running top f,
+// so the merge CTA sees gridDim.x lists whatever the list length (the grid is
+// sized so that gridDim.x * f <= TF_MERGE_MAX)
 __global__ void __launch_bounds__(SS_TPB) k_tf_local(CoopBufs B, int64_t f) {
   extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ Key3 rk[2][TF_MAX];
+  __shared__ uint64_t rv[2][TF_MAX];
   const int64_t n = (int64_t)B.st->tf_n;
   if (n < f) return;
   Key3 *sk = reinterpret_cast<Key3 *>(dsm);
   uint64_t *sv = reinterpret_cast<uint64_t *>(sk + TF_SLICE);
   Key3 *tk = reinterpret_cast<Key3 *>(sv + TF_SLICE);
   uint64_t *tv = reinterpret_cast<uint64_t *>(tk + TF_SLICE);
+  const int F = (int)f;
+  int have = 0, cur = 0;  // running top list: rk/rv[cur][0..have)
   for (int64_t c = blockIdx.x; c * TF_SLICE < n; c += gridDim.x) {
     const int64_t b0 = c * TF_SLICE;
     const int m = (int)(n - b0 < TF_SLICE ? n - b0 : TF_SLICE);
@@ -1512,12 +1520,34 @@ __global__ void __launch_bounds__(SS_TPB) k_tf_local(CoopBufs B, int64_t f) {
     }
     __syncthreads();
     block_merge_sort(sk, sv, m, tk, tv, sk, sv);
-    const int keep = (int)(f < m ? f : m);
-    for (int i = threadIdx.x; i < f; i += blockDim.x) {
-      B.ks[c * f + i] = i < keep ? sk[i] : Key3{~0ull, ~0ull, ~0ull};
-      B.vs[c * f + i] = i < keep ? sv[i] : 0ull;
+    const int keep = m < F ? m : F;
+    // merge the running list (have) and this slice's top (keep): an item's place
+    // is its index plus its rank in the other list (keys are distinct); keep < F
+    const int nxt = cur ^ 1;
+    for (int t = threadIdx.x; t < have + keep; t += blockDim.x) {
+      const bool run = t < have;
+      const int i = run ? t : t - have;
+      const Key3 x = run ? rk[cur][i] : sk[i];
+      const Key3 *O = run ? sk : rk[cur];
+      int lo = 0, hi = run ? keep : have;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (key_less(O[mid], x)) lo = mid + 1;
+        else hi = mid;
+      }
+      const int pos = i + lo;
+      if (pos < F) {
+        rk[nxt][pos] = x;
+        rv[nxt][pos] = run ? rv[cur][i] : sv[i];
+      }
     }
     __syncthreads();
+    have = have + keep < F ? have + keep : F;
+    cur = nxt;
+  }
+  for (int i = threadIdx.x; i < F; i += blockDim.x) {
+    B.ks[(int64_t)blockIdx.x * F + i] = i < have ? rk[cur][i] : Key3{~0ull, ~0ull, ~0ull};
+    B.vs[(int64_t)blockIdx.x * F + i] = i < have ? rv[cur][i] : 0ull;
   }
 }
 
@@ -1525,11 +1555,13 @@ __global__ void __launch_bounds__(SS_TPB) k_tf_local(CoopBufs B, int64_t f) {
 // The slices' sorted top-f lists are merged pairwise in a tree: an item's
 // place in the merge of lists A and B is its index plus its rank in the other
 // list (a binary search over f), and only places < f are kept.
-__global__ void __launch_bounds__(SS_SEL_TPB) k_tf_merge(DT T, CoopBufs B, int64_t f, int32_t keys) {
+__global__ void __launch_bounds__(SS_SEL_TPB) k_tf_merge(DT T, CoopBufs B, int64_t f, int32_t keys,
+                                                        int32_t nlists) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const int64_t n = (int64_t)B.st->tf_n;
   if (n < f || f <= 0) return;  // ss_ok stays 0: the materialising path decides
-  const int nsl = (int)((n + TF_SLICE - 1) / TF_SLICE);
+  const int64_t nslices = (n + TF_SLICE - 1) / TF_SLICE;
+  const int nsl = (int)(nslices < nlists ? nslices : nlists);  // k_tf_local's lists
   const int F = (int)f;
   if ((int64_t)nsl * F > TF_MERGE_MAX) return;  // too many lists for one CTA: the materialising path
   Key3 *ak = reinterpret_cast<Key3 *>(dsm);

@@ -1098,8 +1098,9 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out, int3
         CK(cudaFuncSetAttribute(k_tf_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TF_MERGE_SMEM));
       }
       k_tf_scan<<<4 * sms, SS_TPB, 0, t->st>>>(ProtCand{t->d, keys}, B);
-      k_tf_local<<<2 * sms, SS_TPB, TF_SMEM, t->st>>>(B, ff);
-      k_tf_merge<<<1, SS_SEL_TPB, TF_MERGE_SMEM, t->st>>>(t->d, B, ff, keys);
+      const int nl = (int)std::max<int64_t>(1, std::min<int64_t>(2 * sms, TF_MERGE_MAX / std::max<int64_t>(ff, 1)));
+      k_tf_local<<<nl, SS_TPB, TF_SMEM, t->st>>>(B, ff);
+      k_tf_merge<<<1, SS_SEL_TPB, TF_MERGE_SMEM, t->st>>>(t->d, B, ff, keys, nl);
       CK(cudaGetLastError());
       t->launches[PH_PROTECT] += 3;
     } else if (sampled) {
