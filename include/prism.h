@@ -279,10 +279,11 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids,
  * pending arrays may be pinned host buffers (read in place by the staging
  * kernel), release_slots (device) drops the previous wave's pins first, and
  * the dispatch order / hits are also returned in h_members / h_hits (host).
- * Active sets are not supported here (A = 0). */
+ * The active set (requests in flight, engine.py:189 active.values()) is the
+ * CSR act_off[A+1] / act_sk (pinned host or device; A = 0: none). */
 int prism_wave_step_host(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, const double *arrival,
                          const int64_t *sk_off, const int32_t *sk, const uint8_t *reorderable, const int32_t *suffix,
-                         int32_t nseg, const prism_qas_config *cfg, int64_t sys_len, int64_t chunk,
+                         int64_t A, const int64_t *act_off, const int32_t *act_sk, int32_t nseg, const prism_qas_config *cfg, int64_t sys_len, int64_t chunk,
                          int64_t release_n, const int32_t *release_slots, int64_t *members_out, int64_t *hits,
                          int32_t *leaf_slots, int64_t *leaf_ids, int64_t *h_members, int64_t *h_hits,
                          int64_t *n_members, int64_t *n_admitted);

@@ -1573,13 +1573,14 @@ int prism_wave_step(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
                         sys_len, chunk, members_out, hits, leaf_slots, leaf_ids, n_members, n_admitted, false);
 }
 
-// The fused wave from host memory to host memory: the pending arrays may be
-// pinned host buffers (read in place by the staging kernel), the previous
-// wave's pins are released first, and the dispatch order and hits land in
-// h_members / h_hits (copied inside the wave's graph to fixed pinned buffers).
+// The fused wave from host memory to host memory: the pending arrays (and the
+// active-set CSR) may be pinned host buffers (read in place by the kernels),
+// the previous wave's pins are released first, and the dispatch order and hits
+// land in h_members / h_hits (copied inside the wave's graph to fixed pinned
+// buffers when the wave ran as a graph).
 int prism_wave_step_host(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, const double *arrival,
                          const int64_t *sk_off, const int32_t *sk, const uint8_t *reorderable, const int32_t *suffix,
-                         int32_t nseg, const prism_qas_config *cfg, int64_t sys_len, int64_t chunk,
+                         int64_t A, const int64_t *act_off, const int32_t *act_sk, int32_t nseg, const prism_qas_config *cfg, int64_t sys_len, int64_t chunk,
                          int64_t release_n, const int32_t *release_slots, int64_t *members_out, int64_t *hits,
                          int32_t *leaf_slots, int64_t *leaf_ids, int64_t *h_members, int64_t *h_hits,
                          int64_t *n_members, int64_t *n_admitted) {
@@ -1587,7 +1588,7 @@ int prism_wave_step_host(prism_tree *t, prism_qas *q, int64_t P, const int64_t *
   q->hout_ready = 0;
   int rc;
   if (release_n > 0 && (rc = prism_release_device(t, release_n, release_slots, nullptr, (void *)q->st))) return rc;
-  if ((rc = wave_step_impl(t, q, P, ids, arrival, sk_off, sk, reorderable, suffix, 0, nullptr, nullptr, nseg, cfg,
+  if ((rc = wave_step_impl(t, q, P, ids, arrival, sk_off, sk, reorderable, suffix, A, act_off, act_sk, nseg, cfg,
                            sys_len, chunk, members_out, hits, leaf_slots, leaf_ids, n_members, n_admitted, true)))
     return rc;
   if (q->hout_ready) {

@@ -29,7 +29,8 @@ def _bind(lib):
     sig = {
         "prism_wave_step": (C.c_int, [_p, _p, _i64, _p, _p, _p, _p, _p, _p, _i64, _p, _p, C.c_int32, _p,
                                       _i64, _i64, _p, _p, _p, _p, _p, _p]),
-        "prism_wave_step_host": (C.c_int, [_p, _p, _i64, _p, _p, _p, _p, _p, _p, C.c_int32, _p, _i64, _i64, _i64,
+        "prism_wave_step_host": (C.c_int, [_p, _p, _i64, _p, _p, _p, _p, _p, _p, _i64, _p, _p, C.c_int32, _p, _i64,
+                                           _i64, _i64,
                                            _p, _p, _p, _p, _p, _p, _p, _p, _p]),
         "prism_qas_stream": (_p, [_p]),
         "prism_qas_counters": (C.c_int, [_p, _p, C.c_int32]),
@@ -99,8 +100,6 @@ class WaveEngine:
         self.hits = torch.empty(cap, dtype=torch.int64, device=dev)
         self.leaf_slots = torch.empty(cap, dtype=torch.int32, device=dev)
         self.leaf_ids = torch.empty(cap, dtype=torch.int64, device=dev)
-        self._act_off = torch.zeros(1, dtype=torch.int64, device=dev)
-        self._act_sk = torch.zeros(1, dtype=torch.int32, device=dev)
         self._nm = np.zeros(1, np.int64)
         self._na = np.zeros(1, np.int64)
         self.stream = torch.cuda.ExternalStream(self.L.prism_qas_stream(self.q), device=dev)
@@ -119,37 +118,68 @@ class WaveEngine:
         except Exception:  # pragma: no cover
             pass
 
-    def step(self, pend: DevicePending) -> tuple[int, int]:
-        """One wave; returns (members dispatched, members admitted)."""
+    def step(self, pend: DevicePending, active: DevicePending | None = None) -> tuple[int, int]:
+        """One wave; returns (members dispatched, members admitted).
+
+        ``active``: the requests in flight (engine.py:189 ``active.values()``),
+        whose skeletons (``sk_off`` / ``sk``) feed the round's a-counters
+        (w_a, scheduler.py:203) and, under LRU_ACTIVE, the active-segment flags
+        (engine.py:195-197).  None: no request in flight."""
         P = pend.P
+        A, aoff, ask = self._active(active)
+        self._ensure(P)
+        check(self.L.prism_wave_step(
+            self.t, self.q, P, pend.ids.data_ptr(), pend.arrival.data_ptr(), pend.sk_off.data_ptr(),
+            pend.sk.data_ptr(), pend.reorderable.data_ptr(), pend.suffix.data_ptr(), A, aoff, ask,
+            self.nseg, C.addressof(self._cfg),
+            self.sys_len, self.chunk, self.members.data_ptr(), self.hits.data_ptr(), self.leaf_slots.data_ptr(),
+            self.leaf_ids.data_ptr(), self._nm.ctypes.data, self._na.ctypes.data,
+        ))
+        return int(self._nm[0]), int(self._na[0])
+
+    def _ensure(self, P: int) -> None:
+        """Per-member device outputs for a pending set of P (dispatch <= P)."""
         if P > self.members.shape[0]:
             dev = self.members.device
             self.members = torch.empty(P, dtype=torch.int64, device=dev)
             self.hits = torch.empty(P, dtype=torch.int64, device=dev)
             self.leaf_slots = torch.empty(P, dtype=torch.int32, device=dev)
             self.leaf_ids = torch.empty(P, dtype=torch.int64, device=dev)
-        check(self.L.prism_wave_step(
-            self.t, self.q, P, pend.ids.data_ptr(), pend.arrival.data_ptr(), pend.sk_off.data_ptr(),
-            pend.sk.data_ptr(), pend.reorderable.data_ptr(), pend.suffix.data_ptr(), 0,
-            self._act_off.data_ptr(), self._act_sk.data_ptr(), self.nseg, C.addressof(self._cfg),
-            self.sys_len, self.chunk, self.members.data_ptr(), self.hits.data_ptr(), self.leaf_slots.data_ptr(),
-            self.leaf_ids.data_ptr(), self._nm.ctypes.data, self._na.ctypes.data,
-        ))
-        return int(self._nm[0]), int(self._na[0])
 
-    def step_host(self, pool: dict, out_members: np.ndarray, out_hits: np.ndarray, release_n: int = 0) -> tuple[int, int]:
+    @staticmethod
+    def _active(active) -> tuple[int, int, int]:
+        if active is None:
+            return 0, 0, 0
+        if isinstance(active, dict):
+            off, sk = active["sk_off"], active["sk"]
+        else:
+            off, sk = active.sk_off, active.sk
+        A = int(off.shape[0]) - 1
+        if A <= 0:
+            return 0, 0, 0
+        return A, off.data_ptr(), sk.data_ptr()
+
+    def step_host(self, pool: dict, out_members: np.ndarray, out_hits: np.ndarray, release_n: int = 0,
+                  active: dict | None = None) -> tuple[int, int]:
         """One wave from host memory to host memory (the end-to-end entry point).
 
         ``pool`` maps ids / arrival / sk_off / sk / reorderable / suffix to
         pinned host tensors (read in place by the device); the previous wave's
         ``release_n`` pins (``self.leaf_slots``) are dropped first; the dispatch
-        order and the hits come back in ``out_members`` / ``out_hits`` (int64)."""
+        order and the hits come back in ``out_members`` / ``out_hits`` (int64).
+        ``active``: the in-flight requests' skeleton CSR (``sk_off`` / ``sk``,
+        pinned host tensors), as in ``step``."""
         P = int(pool["ids"].shape[0])
-        if P > self.members.shape[0]:
-            raise ValueError("pending set larger than the engine's dispatch buffers")
+        A, aoff, ask = self._active(active)
+        if release_n > 0 and P > self.members.shape[0]:
+            raise ValueError("release_n refers to leaf_slots, which a larger pending set would reallocate")
+        self._ensure(P)
+        if out_members.shape[0] < min(P, self.sched.dispatch_budget) or out_hits.shape[0] < min(
+                P, self.sched.dispatch_budget):
+            raise ValueError("out_members / out_hits smaller than the wave")
         check(self.L.prism_wave_step_host(
             self.t, self.q, P, pool["ids"].data_ptr(), pool["arrival"].data_ptr(), pool["sk_off"].data_ptr(),
-            pool["sk"].data_ptr(), pool["reorderable"].data_ptr(), pool["suffix"].data_ptr(), self.nseg,
+            pool["sk"].data_ptr(), pool["reorderable"].data_ptr(), pool["suffix"].data_ptr(), A, aoff, ask, self.nseg,
             C.addressof(self._cfg), self.sys_len, self.chunk, release_n, self.leaf_slots.data_ptr(),
             self.members.data_ptr(), self.hits.data_ptr(), self.leaf_slots.data_ptr(), self.leaf_ids.data_ptr(),
             out_members.ctypes.data, out_hits.ctypes.data, self._nm.ctypes.data, self._na.ctypes.data,

@@ -266,3 +266,99 @@ def test_step_host_matches_device_step():
         outs.append((out, eng.cache_view().victim_log()))
         eng.close()
     assert outs[0] == outs[1]
+
+
+def _csr_active(reqs):
+    off = np.zeros(len(reqs) + 1, np.int64)
+    np.cumsum([len(r.skeleton) for r in reqs], out=off[1:])
+    return off, np.array([s for r in reqs for s in r.skeleton], np.int32)
+
+
+def run_inflight(seed, policy, lag=3, host=False, wave=24, pend=30, nwaves=10, cap=700, nseg=40, hot=6,
+                 kmin=2, kmax=5, protect=3, cold=2, mode=0):
+    """Waves with requests in flight (engine.py:171-189): each wave's members
+    stay pinned for ``lag`` waves and form the next rounds' active set, which
+    feeds the a-counters (w_a = 1e6) and, under LRU_ACTIVE, the active-segment
+    flags.  Device (step / step_host with the active CSR) vs the oracle."""
+    import torch
+
+    from paper_2605_08581_b200.wave import DevicePending, WaveEngine
+
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(seed)
+    cfg = CacheConfig(capacity_tokens=cap, policy=policy, protect_budget=protect)
+    scfg = SchedulerConfig(dispatch_budget=wave, cold_quota=cold)
+    eng = WaveEngine(cfg, scfg, nseg, 8, 4, device=0)
+    eng.set_commit_mode(mode)
+    ora = OracleRadixCache(cfg)
+    cat = SegmentCatalog(num_segments=nseg, chunk_tokens=4, hot_set=tuple(range(min(hot, nseg))), sys_prefix_tokens=8)
+    inflight = []  # (wave, admitted requests, device leaf slots, oracle leaves)
+    om, oh = np.empty(max(pend + 6, wave), np.int64), np.empty(max(pend + 6, wave), np.int64)
+    next_id = 0
+    for w in range(nwaves):
+        for f in [x for x in inflight if x[0] <= w - lag]:  # completions
+            eng.release(f[2], f[2].shape[0])
+            for leaf in f[3]:
+                ora.release_path(leaf)
+        inflight = [x for x in inflight if x[0] > w - lag]
+        active = [r for x in inflight for r in x[1]]
+        reqs = _requests(rng, next_id, pend + int(rng.integers(0, 6)), nseg, hot, kmin, kmax, (2, 4), 8, 4)
+        next_id += len(reqs)
+        aoff, ask = _csr_active(active)
+        if host:
+            names = ("ids", "arrival", "sk_off", "sk", "reorderable", "suffix")
+            pool = {k: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+                    for k, a in zip(names, _pending_arrays(reqs))}
+            act = {"sk_off": torch.from_numpy(aoff).pin_memory(), "sk": torch.from_numpy(ask).pin_memory()}
+            nm, na = eng.step_host(pool, om, oh, release_n=0, active=act)
+            members, hits = om[:nm].tolist(), oh[:na].tolist()
+        else:
+            act = DevicePending(torch.zeros(len(active), dtype=torch.int64, device=dev),
+                                torch.zeros(len(active), dtype=torch.float64, device=dev),
+                                torch.from_numpy(aoff).to(dev), torch.from_numpy(ask).to(dev),
+                                torch.zeros(len(active), dtype=torch.uint8, device=dev),
+                                torch.zeros(len(active), dtype=torch.int32, device=dev))
+            nm, na = eng.step(DevicePending.from_host(*_pending_arrays(reqs), dev), act)
+            members, hits = eng.members[:nm].cpu().tolist(), eng.hits[:na].cpu().tolist()
+        leaf_ids = eng.leaf_ids[:na].cpu().tolist()
+        b = oracle_schedule_round(reqs, active, scfg, 0.0)
+        idx = {r.id: i for i, r in enumerate(reqs)}
+        assert members == [idx[r.id] for r in b.members], f"wave {w}: dispatch order"
+        if policy is CachePolicy.DART:
+            ora.set_protection(b.priorities)
+        elif policy is CachePolicy.LRU_ACTIVE:
+            counts = count_segments(list(active) + list(b.members))
+            ora.note_active_segments(r for r, c in counts.items() if c > 0)
+        ohits, oleaves = [], []
+        for r in b.members:
+            h = b.hints[r.id]
+            path = serialize_tokens(r, cat, h.aligned_skeleton)
+            hit = ora.match_prefix(path)[0]
+            try:
+                oleaves.append(ora.insert_path(path, build_anchors(r, h.aligned_skeleton, h.counter_snapshot)))
+            except CapacityError:
+                break
+            ohits.append(hit)
+        assert hits == ohits, f"wave {w}: hits"
+        assert leaf_ids == [x.node_id for x in oleaves], f"wave {w}: leaf ids"
+        inflight.append((w, b.members[:na], eng.leaf_slots[:na].clone(), oleaves))
+    view = eng.cache_view()
+    assert view.debug_nodes() == ora.debug_nodes()
+    assert view.victim_log() == ora.victim_log()
+    eng.close()
+
+
+@pytest.mark.parametrize("policy", list(CachePolicy))
+@pytest.mark.parametrize("host", [False, True])
+def test_inflight_active_set(policy, host):
+    run_inflight(3, policy, host=host)
+
+
+@pytest.mark.parametrize("variant", [
+    dict(lag=1),                                   # nothing in flight at the round (A = 0)
+    dict(lag=5, cap=2000, nwaves=12),              # deep in-flight set
+    dict(mode=1),                                  # ordered commit
+    dict(pend=9000, wave=4096, cold=64, nwaves=4, cap=200_000, nseg=3000, hot=40),  # P > 4096: multi-kernel round
+])
+def test_inflight_variants(variant):
+    run_inflight(7, CachePolicy.DART, **variant)
