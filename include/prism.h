@@ -39,6 +39,7 @@ extern "C" {
 #define PRISM_INVALID 3
 #define PRISM_CUDA 4
 #define PRISM_FATAL 5
+#define PRISM_SIMULATION 6 /* engine.py SimulationError (no progress / path over capacity) */
 
 #define PRISM_SEG_NONE ((int32_t)0x80000000)
 
@@ -287,6 +288,46 @@ int prism_wave_step_host(prism_tree *t, prism_qas *q, int64_t P, const int64_t *
                          int64_t release_n, const int32_t *release_slots, int64_t *members_out, int64_t *hits,
                          int32_t *leaf_slots, int64_t *leaf_ids, int64_t *h_members, int64_t *h_hits,
                          int64_t *n_members, int64_t *n_admitted);
+
+/* ------------------------------------------------------- serving loop
+ * engine.run_simulation (engine.py:141-266) with device-resident state: the
+ * trace, the pending queue, the admission log and the per-request metrics
+ * live in HBM; each wave is prism_wave_step over the gathered pending and
+ * in-flight CSRs.  The trace arrays are HOST arrays in (arrival_time, id)
+ * order (engine.py:158); sys_len = catalog.sys_prefix_tokens, chunk =
+ * catalog.chunk_tokens (reuse_len = len(skeleton) * chunk, workload.py:296);
+ * window_s / prefill_rate / decode_rate / output_tokens / decode_attenuation
+ * are SchedulerConfig.window_s and SimConfig (engine.py:35-48). */
+typedef struct prism_serve prism_serve;
+prism_serve *prism_serve_create(prism_tree *t, prism_qas *q, int64_t n, const int64_t *ids, const double *arrival,
+                                const int64_t *sk_off, const int32_t *sk, const uint8_t *reorderable,
+                                const int32_t *suffix, int32_t nseg, int64_t sys_len, int64_t chunk,
+                                int64_t capacity_tokens, const prism_qas_config *cfg, double window_s,
+                                double prefill_rate, double decode_rate, int64_t output_tokens,
+                                int32_t decode_attenuation);
+void prism_serve_destroy(prism_serve *s);
+/* Run up to max_waves waves (<= 0: until every request completed). */
+int prism_serve_run(prism_serve *s, int64_t max_waves, int64_t *waves_run, int32_t *finished);
+/* out[5]: waves, admitted, windows advanced, completed, pending */
+int prism_serve_counts(prism_serve *s, int64_t *out);
+/* RequestMetrics (engine.py:51-66) in trace order; any pointer may be NULL. */
+int prism_serve_requests(prism_serve *s, double *admit, double *prefill_end, double *first_token,
+                         double *completion, int64_t *hit, int64_t *eff);
+/* WaveRecord (engine.py:69-76): members as trace indices, admission order. */
+int prism_serve_waves(prism_serve *s, double *launch, double *duration, int64_t *uncached, int64_t *cached,
+                      int64_t *member_off, int32_t *members);
+
+/* ------------------------------------------------------- trace ingestion
+ * workload.load_trace (workload.py:258-313) natively: a save_trace JSON-lines
+ * file straight into the skeleton CSR (multi-threaded; threads <= 0: all
+ * cores).  Errors: NULL + "TraceFormatError: line N: ..." as the reference. */
+typedef struct prism_trace prism_trace;
+prism_trace *prism_trace_load_jsonl(const char *path, int32_t threads);
+/* out[6]: requests, skeleton entries, num_segments, chunk_tokens, sys_prefix_tokens, hot-set size */
+int prism_trace_info(prism_trace *tr, int64_t *out);
+int prism_trace_copy(prism_trace *tr, int64_t *ids, double *arrival, int64_t *sk_off, int32_t *sk,
+                     uint8_t *reorderable, int32_t *suffix, int64_t *hot_set);
+void prism_trace_free(prism_trace *tr);
 
 #ifdef __cplusplus
 }

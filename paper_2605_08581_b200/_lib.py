@@ -12,7 +12,7 @@ import os
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libprism.so")
 
-PRISM_OK, PRISM_CAPACITY, PRISM_RELEASE, PRISM_INVALID, PRISM_CUDA, PRISM_FATAL = range(6)
+PRISM_OK, PRISM_CAPACITY, PRISM_RELEASE, PRISM_INVALID, PRISM_CUDA, PRISM_FATAL, PRISM_SIMULATION = range(7)
 SEG_NONE = -(2**31)
 
 _i64, _i32, _p = C.c_int64, C.c_int32, C.c_void_p
@@ -42,6 +42,17 @@ _SIGS = {
     "prism_qas_create": (_p, [_i32]),
     "prism_qas_destroy": (None, [_p]),
     "prism_qas_round": (C.c_int, [_p, _i64, _p, _p, _p, _p, _p, _i64, _p, _p, _i32, _p] + [_p] * 16),
+    "prism_serve_create": (_p, [_p, _p, _i64, _p, _p, _p, _p, _p, _p, _i32, _i64, _i64, _i64, _p, C.c_double,
+                                C.c_double, C.c_double, _i64, _i32]),
+    "prism_serve_destroy": (None, [_p]),
+    "prism_serve_run": (C.c_int, [_p, _i64, _p, _p]),
+    "prism_serve_counts": (C.c_int, [_p, _p]),
+    "prism_serve_requests": (C.c_int, [_p] + [_p] * 6),
+    "prism_serve_waves": (C.c_int, [_p] + [_p] * 6),
+    "prism_trace_load_jsonl": (_p, [C.c_char_p, _i32]),
+    "prism_trace_info": (C.c_int, [_p, _p]),
+    "prism_trace_copy": (C.c_int, [_p] + [_p] * 7),
+    "prism_trace_free": (None, [_p]),
 }
 
 _LIB: C.CDLL | None = None
@@ -84,6 +95,10 @@ def check(rc: int) -> None:
         return
     if rc == PRISM_INVALID:
         raise ValueError(last_error())
+    if rc == PRISM_SIMULATION:
+        from .types import SimulationError
+
+        raise SimulationError(last_error())
     raise PrismError(f"prism status {rc}: {last_error()}")
 
 

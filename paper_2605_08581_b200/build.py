@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libprism.so")
-SOURCES = ["dart.cu", "qas.cu"]
+SOURCES = ["dart.cu", "qas.cu", "serve.cu", "trace_io.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -70,6 +70,14 @@ class ReleaseError(CacheError):
     """Release of a path that is not currently pinned (kvcache.py:40-41)."""
 
 
+class SimulationError(RuntimeError):
+    """The serving loop cannot make progress, or a path exceeds the capacity (engine.py:31-32)."""
+
+
+class TraceFormatError(ValueError):
+    """A trace file fails to parse or validate (workload.py:29-30)."""
+
+
 @dataclass(frozen=True)
 class Anchor:
     """Boundary to materialize during insert (kvcache.py:56-63)."""
