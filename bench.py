@@ -98,6 +98,13 @@ def parse_args():
     ap.add_argument("--profile-steps", type=int, default=3,
                     help="extra waves AFTER the timed region with the per-phase device profile on (roofline)")
     ap.add_argument("--ref-seconds", type=float, default=0.5, help="reference arm: seconds per step per worker")
+    ap.add_argument("--mode", default="wave", choices=["wave", "serve"],
+                    help="wave: timed fused waves on a warm tree; serve: the whole serving loop over a trace")
+    ap.add_argument("--requests", type=int, default=10_000_000, help="serve mode: requests in the global trace")
+    ap.add_argument("--qps", type=float, default=20000.0, help="serve mode: global arrival rate")
+    ap.add_argument("--total-capacity", type=int, default=16_000_000,
+                    help="serve mode: KV capacity (tokens) of the whole job, split evenly over the replicas")
+    ap.add_argument("--parity-requests", type=int, default=60000, help="serve mode: per-shard parity prefix")
     a = ap.parse_args()
     d = DEFAULTS[a.workload]
     a.wave = a.wave or d["wave"]
@@ -565,10 +572,177 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------- serve mode (C4)
+
+
+def _serve_config(args, world: int):
+    """SimConfig (engine.py:35-48) of one replica: per-shard capacity = total / world,
+    prefill rate sized so the shard keeps up (R_pf ~ 1.25 qps_shard L (1 - h))."""
+    from types import SimpleNamespace
+
+    from paper_2605_08581_b200.types import CacheConfig, CachePolicy, SchedulerConfig
+
+    spec = S.SPECS[args.workload]
+    rate = 1.25 * (args.qps / world) * spec.path_len * 0.7
+    return SimpleNamespace(prefill_rate=rate, decode_rate=1e6, output_tokens=32, decode_attenuation_enabled=False,
+                           cache=CacheConfig(capacity_tokens=args.total_capacity // world, policy=CachePolicy.DART,
+                                             protect_budget=args.protect),
+                           scheduler=SchedulerConfig(window_s=0.05, dispatch_budget=args.wave,
+                                                     cold_quota=args.cold_quota))
+
+
+def serve_oracle_job(args, world: int, rank: int, out_path: str) -> None:
+    """Background process: the oracle serving loop on this shard's parity prefix."""
+    from oracle.oracle import build
+    from oracle.serve_loop import oracle_serve
+
+    build()
+    tr = S.prefix_trace(S.shard_trace(S.serve_trace(args.workload, args.requests, args.qps, args.seed), world, rank),
+                        args.parity_requests)
+    t0 = time.perf_counter()
+    o = oracle_serve(tr, _serve_config(args, world))
+    o["timing"] = np.array([o["decisions"], o["seconds"], time.perf_counter() - t0, tr.n])
+    np.savez(out_path, **{k: v for k, v in o.items() if isinstance(v, np.ndarray)})
+
+
+def run_serve(args) -> None:
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    par_proc = par_path = None
+    if args.parity_requests > 0 and not args.no_cpu_baseline:
+        import multiprocessing as mp
+
+        fd, par_path = tempfile.mkstemp(suffix=".npz")
+        os.close(fd)
+        par_proc = mp.get_context("fork").Process(target=serve_oracle_job, args=(args, world, rank, par_path))
+        par_proc.start()
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_08581_b200.serve import DeviceServingLoop
+
+    if world > 1:
+        dist.init_process_group(args.backend)
+    gpu = 0 if args.same_device else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    t_gen = time.perf_counter()
+    trace = S.serve_trace(args.workload, args.requests, args.qps, args.seed)  # every rank: the same global trace
+    mine = S.shard_trace(trace, world, rank)
+    gen_s = time.perf_counter() - t_gen
+    cfg = _serve_config(args, world)
+    kw = dict(device=gpu, initial_slots=1 << 20, initial_arena_tokens=max(1 << 24, 4 * cfg.cache.capacity_tokens))
+    t0 = time.perf_counter()
+    loop = DeviceServingLoop(cfg, mine, **kw)  # the trace's H2D copy (end-to-end)
+    stream = torch.cuda.ExternalStream(loop.L.prism_qas_stream(loop.q), device=dev)
+    loop.run(max_waves=args.warmup)  # untimed: the first waves (allocations, first captures)
+    c0 = loop.counts()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(gpu)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tw = time.perf_counter()
+    e0.record(stream)
+    loop.run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - tw
+    clk = clocks.stop()
+    res = loop.result()  # the metrics' D2H copy (end-to-end)
+    e2e_s = time.perf_counter() - t0
+    c1 = loop.counts()
+    ms = e0.elapsed_time(e1)
+    admitted = c1["admitted"] - c0["admitted"]
+    waves = c1["waves"] - c0["waves"]
+    summ = res.summary()
+    if world > 1:
+        t = torch.tensor([ms, e2e_s], dtype=torch.float64, device=dev if args.backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e_s = (float(x) for x in t.tolist())
+        cnt = torch.tensor([admitted, mine.n], dtype=torch.int64, device=dev if args.backend == "nccl" else "cpu")
+        dist.all_reduce(cnt)
+        admitted_all, n_all = (int(x) for x in cnt.tolist())
+    else:
+        admitted_all, n_all = admitted, mine.n
+    loop.close()
+    parity = cpu = None
+    if par_proc is not None:
+        from paper_2605_08581_b200.serve import DeviceServingLoop as DSL
+
+        sub = S.prefix_trace(mine, args.parity_requests)
+        pl = DSL(cfg, sub, **kw)
+        pl.run()
+        d = pl.result()
+        dv = pl.cache_view().victim_log()
+        pl.close()
+        par_proc.join()
+        if par_proc.exitcode == 0:
+            o = np.load(par_path)
+            diffs = []
+            for name, a, b in (("hits", d.hit_tokens, o["hit"]), ("first_token", d.first_token, o["first_token"]),
+                               ("completion", d.completion, o["completion"]), ("admit", d.admit, o["admit"]),
+                               ("admission order", d.wave_members, o["wave_members"]),
+                               ("wave durations", d.wave_duration, o["wave_duration"])):
+                if not np.array_equal(np.asarray(a), np.asarray(b)):
+                    diffs.append(name)
+            if dv != o["victims"].tolist():
+                diffs.append("victims")
+            ndec, secs, tot, nreq = o["timing"].tolist()
+            parity = {"requests_checked": int(nreq), "waves_checked": int(len(o["wave_launch"])),
+                      "victims_checked": int(len(o["victims"])), "identical": not diffs, "differences": diffs,
+                      "scope": "this shard's first requests through the whole serving loop (admission, hits, "
+                               "TTFT / completion times, every victim)"}
+            if rank == 0:
+                cpu = {"value": ndec / max(secs, 1e-9), "unit": UNIT, "cores": 1, "kind": "port",
+                       "sample": f"{int(ndec)} decisions in {secs:.1f}s inside the waves of the oracle serving loop "
+                                 f"over shard {rank}'s first {int(nreq)} requests ({tot:.0f}s in total)"}
+        else:
+            parity = {"identical": False, "differences": ["oracle process failed"]}
+        os.unlink(par_path)
+        if world > 1:
+            flag = torch.tensor([1 if parity["identical"] else 0], dtype=torch.int64,
+                                device=dev if args.backend == "nccl" else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            parity["identical_all_shards"] = bool(flag.item())
+    if rank == 0:
+        spec = S.SPECS[args.workload]
+        line = {
+            "metric": METRIC, "value": admitted_all / (ms / 1000.0), "unit": UNIT, "n_gpus": world,
+            "steps": waves, "warmup": args.warmup, "ms_per_step": ms / max(waves, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"{spec.name} serving loop: {args.requests} requests "
+                                   f"({DESCR.get(args.workload, '')}), Poisson arrivals at {args.qps:g} QPS, "
+                                   f"routed by splitmix64(skeleton[0]) mod {world}; each replica replays its shard "
+                                   f"through the device-resident run_simulation (windows of 50 ms, budget "
+                                   f"{args.wave}, per-shard capacity {cfg.cache.capacity_tokens} tokens)",
+                       "mode": "serve", "requests": args.requests, "requests_rank0": mine.n,
+                       "requests_all": n_all, "qps": args.qps, "prefill_rate": cfg.prefill_rate,
+                       "capacity_per_shard": cfg.cache.capacity_tokens, "wave_budget": args.wave,
+                       "parallelism": f"replicas x{world}", "trace_gen_s": round(gen_s, 2),
+                       "steps_are": "waves of the serving loop after the untimed warm-up waves, to the trace's end",
+                       "windows": c1["windows"], "host_wall_s": round(wall, 3)},
+            "hit_rate": summ["hit_rate"], "ttft_p50": summ["p50"], "ttft_p99": summ["p99"],
+            "parity": parity, "roofline": None, "cpu_baseline": cpu,
+            "e2e": {"value": admitted_all / e2e_s, "unit": UNIT, "h2d_bytes_per_step": mine.n * 41 // max(waves, 1),
+                    "d2h_bytes_per_step": mine.n * 48 // max(waves, 1),
+                    "api": "DeviceServingLoop (prism_serve_create / run / requests): the shard's trace copied in, "
+                           "the per-request metrics copied out"},
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.mode == "serve" and not (args.gpus > 1 and "WORLD_SIZE" not in os.environ):
+        run_serve(args)
     elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one process per GPU: re-launch under torch.distributed.run
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",

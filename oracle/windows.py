@@ -88,17 +88,22 @@ class OracleReplica:
         p[s + len(segs) * c:] = SUFFIX_TOKEN_BASE + rid * suffix + np.arange(suffix)
         return p
 
-    def step(self, pool: dict, deadline: float | None = None) -> dict:
+    def step(self, pool: dict, deadline: float | None = None, active: tuple | None = None,
+             release_prev: bool = True) -> dict:
         """One window over the pending CSR ``pool``; returns dispatch order
-        (pending indices), hits, leaf ids and the admitted count."""
+        (pending indices), hits, leaf ids and the admitted count.  ``active``:
+        the in-flight set's skeleton CSR (act_off, act_sk); ``release_prev``:
+        drop the previous window's pins first (the fixed-lag windows)."""
         L, h = self.L, self.cache._h
-        for leaf in self.prev:
-            L.ot_release(h, leaf)
-        self.prev = []
+        if release_prev:
+            for leaf in self.prev:
+                L.ot_release(h, leaf)
+            self.prev = []
         P = len(pool["ids"])
+        aoff, ask = active if active is not None else (np.zeros(1, np.int64), np.zeros(0, np.int32))
         m = MarshaledRound(list(range(P)), self.segs, pool["ids"], pool["arrival"], pool["sk_off"],
-                           pool["sk"].astype(np.int32), pool["reorderable"], np.zeros(1, np.int64),
-                           np.zeros(0, np.int32))
+                           pool["sk"].astype(np.int32), pool["reorderable"], np.asarray(aoff, np.int64),
+                           np.asarray(ask, np.int32))
         t0 = time.perf_counter()
         out = oracle_round_arrays(m, self.sched)
         if self.policy is CachePolicy.DART:

@@ -233,3 +233,32 @@ def test_serving_loop_errors():
                     scheduler=SchedulerConfig())
     with pytest.raises(SimulationError, match="exceeds cache capacity"):
         run_simulation(tr, cfg)
+
+
+@pytest.mark.parametrize("variant", [dict(qps=20.0, cap=5760), dict(qps=60.0, cap=12557, attenuate=True),
+                                     dict(qps=40.0, cap=9000, policy="LRU_ACTIVE")])
+def test_oracle_serve_loop_matches_harness(variant):
+    """oracle/serve_loop.py (the array-based checker used at scale) against the
+    per-request restatement of engine.py in tests/sim_harness.py (CPU)."""
+    from oracle.serve_loop import oracle_serve
+    from paper_2605_08581_b200.serve import TraceCSR
+    from paper_2605_08581_b200.types import CacheConfig, CachePolicy, SchedulerConfig
+    from sim_harness import SimConfig
+
+    cat = SegmentCatalog(num_segments=981, chunk_tokens=128, hot_set=tuple(range(20)), sys_prefix_tokens=28)
+    tr = generate_trace(WorkloadConfig(qps=variant["qps"], num_requests=800, k=5, r_hot=0.7, zipf_alpha=1.2,
+                                       suffix_tokens=100, seed=3), cat)
+    cfg = SimConfig(prefill_rate=1e4, decode_rate=4e4, decode_attenuation_enabled=variant.get("attenuate", False),
+                    cache=CacheConfig(capacity_tokens=variant["cap"], policy=CachePolicy(variant.get("policy", "DART")),
+                                      protect_budget=20),
+                    scheduler=SchedulerConfig(window_s=0.05, dispatch_budget=8, cold_quota=2))
+    o = oracle_serve(TraceCSR.from_trace(tr), cfg)
+    ref, cache = _oracle_loop(tr, cfg)
+    assert o["hit"].tolist() == [m.hit_tokens for m in ref.requests]
+    assert o["first_token"].tolist() == [m.first_token for m in ref.requests]
+    assert o["completion"].tolist() == [m.completion for m in ref.requests]
+    ids = TraceCSR.from_trace(tr).ids
+    sizes = np.cumsum(np.concatenate([[0], o["wave_sizes"]]))
+    assert [ids[o["wave_members"][sizes[w]:sizes[w + 1]]].tolist() for w in range(len(sizes) - 1)] == \
+        [w.members for w in ref.waves]
+    assert o["victims"].tolist() == cache.victim_log()

@@ -204,3 +204,47 @@ def _cat(a: dict, b: dict) -> dict:
             "sk": np.concatenate([a["sk"], b["sk"]]), "reorderable": np.concatenate([a["reorderable"],
                                                                                     b["reorderable"]]),
             "suffix": np.concatenate([a["suffix"], b["suffix"]])}
+
+
+def serve_trace(workload: str, n: int, qps: float, seed: int):
+    """A whole trace for the serving loop (paper_2605_08581_b200.serve): ``n``
+    requests of ``workload``'s shape with Poisson arrivals at ``qps``
+    (exponential gaps, workload.py:219-223), ids in arrival order."""
+    from paper_2605_08581_b200.serve import TraceCSR
+
+    spec = SPECS[workload]
+    rng = np.random.default_rng(seed)
+    arrival = np.cumsum(rng.exponential(1.0 / qps, size=n))
+    sk = SKELETONS[workload](n, rng)
+    k = sk.shape[1]
+    return TraceCSR(np.arange(n, dtype=np.int64), arrival, np.arange(n + 1, dtype=np.int64) * k,
+                    np.ascontiguousarray(sk, dtype=np.int32).reshape(-1),
+                    np.full(n, 1 if spec.reorderable else 0, np.uint8), np.full(n, spec.suffix, np.int32),
+                    spec.nseg, spec.chunk, spec.sys_len, tuple(range(1000)) if workload == "c4" else ())
+
+
+def shard_trace(tr, world: int, rank: int):
+    """This replica's sub-trace: splitmix64(skeleton[0]) mod world."""
+    from paper_2605_08581_b200.serve import TraceCSR
+
+    if world == 1:
+        return tr
+    first = tr.sk[tr.sk_off[:-1]].astype(np.uint64)
+    idx = np.flatnonzero((splitmix64(first) % np.uint64(world)).astype(np.int64) == rank)
+    k = np.diff(tr.sk_off)
+    off = np.zeros(len(idx) + 1, np.int64)
+    np.cumsum(k[idx], out=off[1:])
+    if len(idx) and np.all(k == k[0]):
+        sk = tr.sk.reshape(-1, int(k[0]))[idx].reshape(-1)
+    else:
+        sk = np.concatenate([tr.sk[tr.sk_off[i]:tr.sk_off[i + 1]] for i in idx.tolist()] or [np.zeros(0, np.int32)])
+    return TraceCSR(tr.ids[idx], tr.arrival[idx], off, np.ascontiguousarray(sk, np.int32), tr.reorderable[idx],
+                    tr.suffix[idx], tr.num_segments, tr.chunk_tokens, tr.sys_prefix_tokens, tr.hot_set)
+
+
+def prefix_trace(tr, n: int):
+    from paper_2605_08581_b200.serve import TraceCSR
+
+    n = min(n, tr.n)
+    return TraceCSR(tr.ids[:n], tr.arrival[:n], tr.sk_off[:n + 1].copy(), tr.sk[:tr.sk_off[n]], tr.reorderable[:n],
+                    tr.suffix[:n], tr.num_segments, tr.chunk_tokens, tr.sys_prefix_tokens, tr.hot_set)
