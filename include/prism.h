@@ -260,6 +260,15 @@ int prism_qas_small_timeline(prism_qas *q, int64_t *out_ns, int32_t n);
 /* Copy the last round's pending demand counters g[0..nseg) (DEVICE int32) to
  * dst (DEVICE) -- the per-window counter vector the replicas all-reduce. */
 int prism_qas_counters(prism_qas *q, int32_t *dst, int32_t nseg);
+/* count_segments (scheduler.py:83-89) of a DEVICE pending CSR into dense G[nseg]
+ * (DEVICE int32, zeroed first): a replica's per-window demand counters. */
+int prism_qas_demand(prism_qas *q, int64_t P, const int64_t *sk_off, const int32_t *sk, int32_t nseg, int32_t *G);
+/* Global-demand knob (multi-GPU; not in the single-instance reference): when
+ * G (DEVICE int32[nseg], e.g. the all-reduce of every replica's prism_qas_demand)
+ * is set, the protection hand-off of the fused wave uses
+ * P-hat[r] = w_g*G[r] + w_a*a[r] + w_n*n[r] (scheduler.py:247-251 with g := G)
+ * instead of the local round's.  NULL restores the reference behaviour. */
+int prism_qas_set_global_demand(prism_qas *q, const int32_t *G, int32_t nseg);
 
 /* One serving-loop wave entirely on the device (engine.py:189-213):
  * schedule_round over the DEVICE-resident pending CSR, the protection (DART)

@@ -89,7 +89,7 @@ class OracleReplica:
         return p
 
     def step(self, pool: dict, deadline: float | None = None, active: tuple | None = None,
-             release_prev: bool = True) -> dict:
+             release_prev: bool = True, global_g: np.ndarray | None = None) -> dict:
         """One window over the pending CSR ``pool``; returns dispatch order
         (pending indices), hits, leaf ids and the admitted count.  ``active``:
         the in-flight set's skeleton CSR (act_off, act_sk); ``release_prev``:
@@ -106,7 +106,14 @@ class OracleReplica:
                            np.asarray(ask, np.int32))
         t0 = time.perf_counter()
         out = oracle_round_arrays(m, self.sched)
-        if self.policy is CachePolicy.DART:
+        if self.policy is CachePolicy.DART and global_g is not None:
+            # the global-demand knob: scheduler.py:247-251 with g := the replicas' summed demand
+            w = self.sched.weights
+            G = np.asarray(global_g, np.int64)
+            dom = np.flatnonzero((G > 0) | (out.a > 0) | (out.nd > 0))
+            self.cache.set_protection({int(r): (w.w_g * int(G[r]) + w.w_a * int(out.a[r])) + w.w_n * int(out.nd[r])
+                                       for r in dom.tolist()})
+        elif self.policy is CachePolicy.DART:
             dom = np.flatnonzero(out.dom)
             self.cache.set_protection(dict(zip(dom.tolist(), out.prio[dom].tolist())))
         elif self.policy is CachePolicy.LRU_ACTIVE:
@@ -236,16 +243,29 @@ def oracle_windows(rep: OracleReplica, windows: list, record_from: int = 0) -> d
     return res
 
 
-def device_windows(eng, windows: list, device, record_from: int = 0) -> dict:
-    """The same windows through a device replica (``WaveEngine.step``)."""
+def device_windows(eng, windows: list, device, record_from: int = 0, reduce_demand=None) -> dict:
+    """The same windows through a device replica (``WaveEngine.step``).
+    ``reduce_demand(G)``: the global-demand knob -- each window's pending
+    demand is computed on the device and reduced over the replicas in place."""
+    import torch
+
     from paper_2605_08581_b200.wave import DevicePending
 
+    G = None
+    if reduce_demand is not None:
+        G = torch.zeros(eng.nseg, dtype=torch.int32, device=device)
+        eng.set_global_demand(G)
     pend, prev, out = None, 0, {}
     for i, pool in enumerate(windows):
         pend = concat_pools(pend, pool)
         eng.release(eng.leaf_slots, prev)
-        nm, na = eng.step(DevicePending.from_host(pend["ids"], pend["arrival"], pend["sk_off"], pend["sk"],
-                                                  pend["reorderable"], pend["suffix"], device))
+        dp = DevicePending.from_host(pend["ids"], pend["arrival"], pend["sk_off"], pend["sk"], pend["reorderable"],
+                                     pend["suffix"], device)
+        if G is not None:
+            with torch.cuda.stream(eng.stream):
+                eng.demand(dp, G)
+                reduce_demand(G)
+        nm, na = eng.step(dp)
         members = eng.members[:nm].cpu().numpy()
         if i >= record_from:
             j = i - record_from
@@ -285,3 +305,40 @@ def compare_windows(d: dict, o, waves: int, path_len: int | None = None) -> dict
     if path_len:
         out["hit_rate"] = hit / max(adm * path_len, 1)
     return out
+
+
+def pool_demand(pool: dict, nseg: int) -> np.ndarray:
+    """count_segments (scheduler.py:83-89) of a pending CSR, dense int64 [nseg]."""
+    G = np.zeros(nseg, np.int64)
+    off, sk = pool["sk_off"], pool["sk"]
+    for i in range(len(off) - 1):
+        G[np.unique(sk[off[i]:off[i + 1]])] += 1
+    return G
+
+
+def oracle_windows_global(reps: list, windows: list, record_rank: int, record_from: int = 0) -> dict:
+    """The replicas of every shard in lockstep (``windows[r]`` = rank r's
+    arrival pools): each window, every replica's pending demand is summed (the
+    per-window all-reduce) and fed to all of them as P-hat (the global-demand
+    knob); records rank ``record_rank`` like ``oracle_windows``."""
+    world = len(reps)
+    pends = [None] * world
+    res = {}
+    for i in range(len(windows[0])):
+        for r in range(world):
+            pends[r] = concat_pools(pends[r], windows[r][i])
+        G = sum(pool_demand(pends[r], reps[r].nseg) for r in range(world))
+        for r in range(world):
+            if i == record_from:
+                reps[r].decisions, reps[r].decision_seconds = 0, 0.0
+            out = reps[r].step(pends[r], global_g=G)
+            if r == record_rank and i >= record_from:
+                j = i - record_from
+                res[f"m{j}"], res[f"h{j}"], res[f"l{j}"] = out["members"], out["hits"], out["leaf_ids"]
+            pends[r] = drop_members(pends[r], out["members"][: out["n_admitted"]])
+    rep = reps[record_rank]
+    res["table"] = rep.table()
+    res["victims"] = rep.victims()
+    res["resident"] = np.array([rep.resident])
+    res["timing"] = np.array([rep.decisions, rep.decision_seconds])
+    return res

@@ -414,6 +414,20 @@ __global__ void q_cold_keys(int64_t P, const uint8_t *__restrict__ sel, const do
   w[i] = sel[i] ? 0 : 1;  // only leftovers count toward the cold quota
 }
 
+// count_segments (scheduler.py:83-89) of a pending CSR into dense G: one thread
+// per request, each distinct segment once
+__global__ void q_demand(int64_t P, const int64_t *__restrict__ off, const int32_t *__restrict__ sk, int32_t *G) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const int64_t b = off[i], e = off[i + 1];
+  for (int64_t j = b; j < e; j++) {
+    const int32_t s = sk[j];
+    bool dup = false;
+    for (int64_t q = b; q < j && !dup; q++) dup = sk[q] == s;
+    if (!dup) atomicAdd(&G[s], 1);
+  }
+}
+
 __global__ void q_prio(int32_t nseg, const int32_t *__restrict__ g, const int32_t *__restrict__ a,
                        const int32_t *__restrict__ nd, QCfg c, double *__restrict__ prio, uint8_t *__restrict__ dom) {
   const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -463,6 +477,8 @@ struct prism_qas {
   X(int32_t, emap) \
   X(uint8_t, efirst) \
   X(int32_t, btake) \
+  X(double, prio_glob) \
+  X(uint8_t, dom_glob) \
   X(int32_t, bbase) \
   X(int64_t, gids) \
   X(int64_t, goff) \
@@ -553,6 +569,8 @@ struct prism_qas {
   int64_t small_grid = 0;      // CTAs of a one-launch round (0: from small_per_cta)
   int64_t small_per_cta = 32;  // pending requests per CTA when sizing the grid
   int32_t small_coresident = 0;
+  const int32_t *gdem = nullptr;  // all-reduced demand counters feeding P-hat (nullptr: the local round's)
+  int32_t gdem_n = 0;
   int64_t last_small_grid = 0;
   bool full_reset = true;
   int64_t small_rounds = 0;
@@ -1347,6 +1365,22 @@ int prism_qas_small_timeline(prism_qas *q, int64_t *out_ns, int32_t n) {
   return PRISM_OK;
 }
 
+int prism_qas_set_global_demand(prism_qas *q, const int32_t *G, int32_t nseg) {
+  if (G && nseg <= 0) return qfail(PRISM_INVALID, "global demand needs nseg > 0");
+  q->gdem = G;
+  q->gdem_n = G ? nseg : 0;
+  return PRISM_OK;
+}
+
+int prism_qas_demand(prism_qas *q, int64_t P, const int64_t *sk_off, const int32_t *sk, int32_t nseg, int32_t *G) {
+  cudaSetDevice(q->dev);
+  QCK(cudaMemsetAsync(G, 0, sizeof(int32_t) * (size_t)nseg, q->st));
+  if (P > 0) q_demand<<<nblk(P), TPB, 0, q->st>>>(P, sk_off, sk, G);
+  QCK(cudaGetLastError());
+  q->launches++;
+  return PRISM_OK;
+}
+
 int prism_qas_counters(prism_qas *q, int32_t *dst, int32_t nseg) {
   cudaSetDevice(q->dev);
   if (nseg > q->g_cap) return qfail(PRISM_INVALID, "nseg exceeds the last round's counter vector");
@@ -1433,6 +1467,11 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
     q->hout_cap = P;
   }
   if (!q->ev_t) QCK(cudaEventCreateWithFlags(&q->ev_t, cudaEventDisableTiming));
+  if (q->gdem) {
+    if (q->gdem_n != nseg) return qfail(PRISM_INVALID, "global demand vector length != nseg");
+    QCK(grow(&q->prio_glob, q->prio_glob_cap, nseg));
+    QCK(grow(&q->dom_glob, q->dom_glob_cap, nseg));
+  }
   if ((rc = prism_wave_commit_prepare(t, B))) return rc;
   int32_t *abort = q->err + 1;
   q_stage<<<nblk(P * 8), TPB, 0, st>>>(P, ids, arrival, sk_off, sk, reorderable, suffix, q->gids, q->garr, q->goff,
@@ -1447,9 +1486,14 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
     q_members_scan<<<1, 1024, 0, st>>>(nh, nc, q->hot, q->cv2, q->gids, q->goff, q->gsfx, sys_len, chunk, members,
                                        q->plen, q->alen, q->poff, q->aoffs, q->tmp_tot, q->qcounts, tok_cap,
                                        anc_cap, q->err, abort);
-    QCK(cudaEventRecord(q->ev_t, st));
+    const double *pri = q->prio;
+    if (q->gdem) {  // P-hat from the replicas' all-reduced demand (the global-demand knob)
+      q_prio<<<nblk(nseg), TPB, 0, st>>>(nseg, q->gdem, q->a, q->nd, c, q->prio_glob, q->dom_glob);
+      pri = q->prio_glob;
+    }
+    QCK(cudaEventRecord(q->ev_t, st));  // (the protection on the tree's streams reads pri)
     QCK(cudaStreamWaitEvent((cudaStream_t)prism_tree_stream(t), q->ev_t, 0));
-    if ((r = prism_set_protection_device_async(t, q->prio, nseg))) return r;  // overlaps serialization
+    if ((r = prism_set_protection_device_async(t, pri, nseg))) return r;  // overlaps serialization
     q_serialize<<<nblk(B * 32), TPB, 0, st>>>(B, members, q->gids, q->goff, q->aligned, q->gsfx, sys_len, chunk, q->g,
                                               q->a, q->nd, q->poff, q->aoffs, q->tok, q->a_off, q->a_kind, q->a_seg,
                                               q->a_snap, q->err, abort);
@@ -1469,7 +1513,7 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
     const void *ptrs[] = {members, hits, leaf_slots, leaf_ids, q->gids, q->goff, q->gsfx, q->garr, q->greo, q->gsk,
                           q->aligned, q->g, q->a, q->nd, q->prio, q->dom, q->poff, q->aoffs, q->plen, q->alen,
                           q->tok, q->a_off, q->a_kind, q->a_seg, q->a_snap, q->err, q->tmp_tot, q->qcounts, q->hres,
-                          q->touched, q->tn, q->rk, q->emap, q->efirst, q->btake, q->bbase, q->longl, q->sig, q->siglen, q->tkey, q->tmin,
+                          q->touched, q->tn, q->rk, q->emap, q->efirst, q->btake, q->bbase, q->gdem, q->prio_glob, q->dom_glob, q->longl, q->sig, q->siglen, q->tkey, q->tmin,
                           q->slot_of, q->bmin, q->bstart, q->bend, q->score, q->take, q->rank, q->bucket, q->hot,
                           q->cv2, q->pk, q->pv, q->plist, host_out ? q->hout_mem : nullptr,
                           host_out ? q->hout_hit : nullptr};
@@ -1687,9 +1731,17 @@ int wave_step_impl(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, c
     const int32_t pol = prism_tree_policy(t);
     // protection / active hand-off (engine.py:193-197), ordered after the round
     // on the tree's stream by an event (no host wait)
-    QCK(cudaEventRecord(q->ev_t, st));
+    const double *pri = q->prio;
+    if (pol == 0 && q->gdem) {  // P-hat from the replicas' all-reduced demand (the global-demand knob)
+      if (q->gdem_n != nseg) return qfail(PRISM_INVALID, "global demand vector length != nseg");
+      QCK(grow(&q->prio_glob, q->prio_glob_cap, nseg));
+      QCK(grow(&q->dom_glob, q->dom_glob_cap, nseg));
+      q_prio<<<nblk(nseg), TPB, 0, st>>>(nseg, q->gdem, q->a, q->nd, c, q->prio_glob, q->dom_glob);
+      pri = q->prio_glob;
+    }
+    QCK(cudaEventRecord(q->ev_t, st));  // (the protection on the tree's streams reads pri)
     QCK(cudaStreamWaitEvent((cudaStream_t)prism_tree_stream(t), q->ev_t, 0));
-    if (pol == 0) rc = prism_set_protection_device_async(t, q->prio, nseg);  // overlaps the serialization
+    if (pol == 0) rc = prism_set_protection_device_async(t, pri, nseg);  // overlaps the serialization
     else if (pol == 2) rc = prism_note_active_device(t, q->a, q->nd, nseg);
     if (rc) return rc;
     // serialization (K1), then the admission on the tree's stream

@@ -34,6 +34,8 @@ def _bind(lib):
                                            _p, _p, _p, _p, _p, _p, _p, _p, _p]),
         "prism_qas_stream": (_p, [_p]),
         "prism_qas_counters": (C.c_int, [_p, _p, C.c_int32]),
+        "prism_qas_demand": (C.c_int, [_p, _i64, _p, _p, C.c_int32, _p]),
+        "prism_qas_set_global_demand": (C.c_int, [_p, _p, C.c_int32]),
         "prism_set_protection_device": (C.c_int, [_p, _p, C.c_int32, _p, _p]),
         "prism_profile": (C.c_int, [_p, C.c_int32]),
         "prism_profile_read": (C.c_int, [_p, _p]),
@@ -195,6 +197,20 @@ class WaveEngine:
     def demand_counters(self, dst: torch.Tensor) -> None:
         """Last round's pending demand counters g (int32 [nseg]) into dst."""
         check(self.L.prism_qas_counters(self.q, dst.data_ptr(), self.nseg))
+
+    def demand(self, pend: DevicePending, dst: torch.Tensor) -> None:
+        """count_segments(pending) (scheduler.py:83-89) into dst (int32 [nseg],
+        device): this replica's per-window demand counters."""
+        check(self.L.prism_qas_demand(self.q, pend.P, pend.sk_off.data_ptr(), pend.sk.data_ptr(), self.nseg,
+                                      dst.data_ptr()))
+
+    def set_global_demand(self, G: torch.Tensor | None) -> None:
+        """Global-demand knob (multi-GPU): the protection hand-off uses P-hat
+        from G (the replicas' all-reduced demand, read at every wave) instead
+        of the local round's g.  None: the reference behaviour."""
+        self._gdem = G
+        check(self.L.prism_qas_set_global_demand(self.q, G.data_ptr() if G is not None else None,
+                                                 self.nseg if G is not None else 0))
 
     def set_graph(self, enable: bool) -> None:
         """Replay the wave's tail (protection, serialization, commit) as a CUDA graph."""
