@@ -63,6 +63,9 @@ DEFAULTS = {
     "c3": {"warm": 8 * 4096, "capacity": 36_000_000, "wave": 4096},
     "mu1m": {"warm": 125_000, "capacity": 16_000_000, "wave": 4096},
     "c4": {"warm": 16 * 1024, "capacity": 4_000_000, "wave": 1024},
+    # C5: the C4 shape at a KV budget of 10% of the 12.8M-token segment catalog
+    # per replica, the replicas' per-window demand all-reduced into P-hat
+    "c5": {"warm": 4 * 1024, "capacity": 1_280_000, "wave": 1024},
 }
 DESCR = {
     "c3": "C3 agent trace: 2432-token paths (sys 1024 + 40 x 32-token segments + 128-token suffix), Zipf(1.1) "
@@ -72,6 +75,9 @@ DESCR = {
             "warm-started with 125K paths (~1M nodes, ~16M tokens), every admission evicts",
     "c4": "C4 RAG shape: 768-token paths (sys 28 + 5 x 128 + 100), 100K-segment catalog, Zipf(1.1) over 1000 hot, "
           "r_hot 0.7",
+    "c5": "C5 eviction stress: the C4 shape at a per-replica KV budget of 1.28M tokens (10% of the 12.8M-token "
+          "segment catalog), every wave turns most of the tree over; per window the replicas' pending demand is "
+          "all-reduced and feeds P-hat (global-demand knob)",
 }
 
 
@@ -206,9 +212,34 @@ def oracle_parity_job(args, world: int, rank: int, out_path: str) -> None:
     rep = OracleReplica(cache, sched, spec.nseg, spec.sys_len, spec.chunk)
     warm, check = parity_windows(args, world, rank)
     t0 = time.perf_counter()
-    res = oracle_windows(rep, warm + check, record_from=len(warm))
+    if args.workload == "c5":  # every replica in lockstep, P-hat from the summed demand
+        from oracle.windows import oracle_windows_global
+
+        reps = [rep if r == rank else OracleReplica(cache, sched, spec.nseg, spec.sys_len, spec.chunk)
+                for r in range(world)]
+        wins = [(lambda w, c: w + c)(*parity_windows(args, world, r)) for r in range(world)]
+        res = oracle_windows_global(reps, wins, rank, record_from=len(warm))
+    else:
+        res = oracle_windows(rep, warm + check, record_from=len(warm))
     res["timing"] = np.append(res["timing"], time.perf_counter() - t0)
     np.savez(out_path, **res)
+
+
+def _demand_reducer(args, world: int, dev):
+    """In-place sum of a demand vector over the replicas (NCCL over NVLink; gloo via the host)."""
+    import torch.distributed as dist
+
+    def reduce(G):
+        if world == 1:
+            return
+        if args.backend == "nccl":
+            dist.all_reduce(G)
+        else:
+            h = G.cpu()
+            dist.all_reduce(h)
+            G.copy_(h.to(dev))
+
+    return reduce
 
 
 def device_parity(args, engine_kw, world: int, rank: int, dev) -> dict:
@@ -218,7 +249,8 @@ def device_parity(args, engine_kw, world: int, rank: int, dev) -> dict:
 
     eng = WaveEngine(**engine_kw)
     warm, check = parity_windows(args, world, rank)
-    out = device_windows(eng, warm + check, dev, record_from=len(warm))
+    out = device_windows(eng, warm + check, dev, record_from=len(warm),
+                         reduce_demand=_demand_reducer(args, world, dev) if args.workload == "c5" else None)
     eng.close()
     return out
 
@@ -288,8 +320,8 @@ def run_ours(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     spec = S.SPECS[args.workload]
-    if args.parity_waves < 0:
-        args.parity_waves = 2 if world == 1 else 0
+    if args.parity_waves < 0:  # C5's parity (the summed demand) is checked at every N; the others at N=1
+        args.parity_waves = 2 if (world == 1 or args.workload == "c5") else 0
     if args.profile_only:
         args.parity_waves = 0
     # the oracle parity replica starts BEFORE CUDA is initialised (fork-safe)
@@ -321,8 +353,20 @@ def run_ours(args) -> None:
     stream_in = S.ShardStream(args.workload, args.seed, world, rank)
     demand = torch.zeros(spec.nseg, dtype=torch.int32, device=dev) if world > 1 else None
 
+    glob = args.workload == "c5"
+    if glob:  # the global-demand knob: P-hat from the replicas' summed per-window demand
+        demand = torch.zeros(spec.nseg, dtype=torch.int32, device=dev)
+        engine.set_global_demand(demand)
+    reduce_demand = _demand_reducer(args, world, dev)
+
+    def pre_step(pend):
+        if glob:  # this window's demand, summed over the replicas before the wave's hand-off
+            with torch.cuda.stream(stream):
+                engine.demand(pend, demand)
+                reduce_demand(demand)
+
     def allreduce_demand():
-        if demand is None:
+        if demand is None or glob:
             return
         with torch.cuda.stream(stream):  # per-window demand counters across replicas (NVLink)
             engine.demand_counters(demand)
@@ -342,7 +386,9 @@ def run_ours(args) -> None:
     t_ws = time.perf_counter()
     for i in range(0, args.warm, B):
         engine.release(engine.leaf_slots, prev)
-        _, prev = engine.step(to_dev(stream_in.take(min(B, args.warm - i))))
+        wp = to_dev(stream_in.take(min(B, args.warm - i)))
+        pre_step(wp)
+        _, prev = engine.step(wp)
     torch.cuda.synchronize()
     warm_s = time.perf_counter() - t_ws
 
@@ -355,6 +401,7 @@ def run_ours(args) -> None:
     def one_step(pend):
         nonlocal prev
         engine.release(engine.leaf_slots, prev)
+        pre_step(pend)
         nm, na = engine.step(pend)
         allreduce_demand()
         prev = na
@@ -417,6 +464,7 @@ def run_ours(args) -> None:
         out_hits = np.empty(B, dtype=np.int64)
         h2d = sum(v.numel() * v.element_size() for v in pinned[0].values())
         for s in range(ew):
+            pre_step(pinned[e2e_steps + s])
             _, prev = engine.step_host(pinned[e2e_steps + s], out_mem, out_hits, release_n=prev)
             allreduce_demand()
         torch.cuda.synchronize()
@@ -429,6 +477,7 @@ def run_ours(args) -> None:
         wall = []
         for s in range(e2e_steps):
             tw = time.perf_counter()
+            pre_step(pinned[s])
             nm, na = engine.step_host(pinned[s], out_mem, out_hits, release_n=prev)
             wall.append((time.perf_counter() - tw) * 1e3)
             prev = na

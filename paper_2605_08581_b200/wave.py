@@ -198,10 +198,12 @@ class WaveEngine:
         """Last round's pending demand counters g (int32 [nseg]) into dst."""
         check(self.L.prism_qas_counters(self.q, dst.data_ptr(), self.nseg))
 
-    def demand(self, pend: DevicePending, dst: torch.Tensor) -> None:
+    def demand(self, pend, dst: torch.Tensor) -> None:
         """count_segments(pending) (scheduler.py:83-89) into dst (int32 [nseg],
-        device): this replica's per-window demand counters."""
-        check(self.L.prism_qas_demand(self.q, pend.P, pend.sk_off.data_ptr(), pend.sk.data_ptr(), self.nseg,
+        device): this replica's per-window demand counters.  ``pend``: a
+        DevicePending or a pool of pinned host tensors (read in place)."""
+        off, sk = (pend["sk_off"], pend["sk"]) if isinstance(pend, dict) else (pend.sk_off, pend.sk)
+        check(self.L.prism_qas_demand(self.q, int(off.shape[0]) - 1, off.data_ptr(), sk.data_ptr(), self.nseg,
                                       dst.data_ptr()))
 
     def set_global_demand(self, G: torch.Tensor | None) -> None:

@@ -66,7 +66,8 @@ class Spec:
 MU1M = Spec("mu1M", 50 + 2_000_000, 28, 16, 8, 16, True)
 C3 = Spec("C3", 1 << 20, 1024, 32, 40, 128, False)
 C4 = Spec("C4", 100_000, 28, 128, 5, 100, True)
-SPECS = {"mu1m": MU1M, "c3": C3, "c4": C4}
+C5 = Spec("C5", 100_000, 28, 128, 5, 100, True)  # the C4 shape (bench: 10% KV budget + global demand)
+SPECS = {"mu1m": MU1M, "c3": C3, "c4": C4, "c5": C5}
 
 
 def _pool(ids: np.ndarray, sk: np.ndarray, spec: Spec) -> dict:
@@ -136,7 +137,7 @@ def c4_skeletons(n: int, rng: np.random.Generator, hot: int = 1000, r_hot: float
     return sk
 
 
-SKELETONS = {"mu1m": mu1m_skeletons, "c3": c3_skeletons, "c4": c4_skeletons}
+SKELETONS = {"mu1m": mu1m_skeletons, "c3": c3_skeletons, "c4": c4_skeletons, "c5": c4_skeletons}
 
 
 def make_pool(workload: str, first_id: int, n: int, rng: np.random.Generator) -> dict:
