@@ -298,6 +298,27 @@ int prism_wave_step_host(prism_tree *t, prism_qas *q, int64_t P, const int64_t *
                          int32_t *leaf_slots, int64_t *leaf_ids, int64_t *h_members, int64_t *h_hits,
                          int64_t *n_members, int64_t *n_admitted);
 
+/* ------------------------------------------------------- paged KV payload
+ * north_star item (4) / SURVEY.md 8(f)3 (the reference is token-granular and
+ * has no payload): every resident token owns a row of a KV
+ * pool in HBM (rows x bytes_per_token, a multiple of 16), taken from a free
+ * stack when the token becomes resident and returned when its node is
+ * evicted.  Enable on an empty tree; rows >= capacity + the new tokens of one
+ * sync.  prism_kv_sync settles the tree operations since the last sync: rows
+ * for the newly resident tokens (admission order = each admitted member's
+ * uncached tokens; src = their KV in that order, DEVICE, or NULL) and the
+ * victims' rows back on the free stack (dst = their KV in eviction order,
+ * DEVICE, or NULL); out[2] = {new tokens, freed tokens}.  prism_kv_gather: per
+ * leaf slot (DEVICE) the pool row of every path position into table[n, max_len]
+ * (the request's req_to_token), lens[n] = path lengths, and (out != NULL) the
+ * KV rows themselves into out[n, max_len, bytes_per_token] -- all DEVICE. */
+int prism_kv_enable(prism_tree *t, int64_t rows, int64_t bytes_per_token);
+int prism_kv_sync(prism_tree *t, const void *src, void *dst, int64_t *out);
+int prism_kv_gather(prism_tree *t, int64_t n, const int32_t *leaf_slots, int64_t max_len, int32_t *table,
+                    void *out, int64_t *lens);
+/* out[6]: free rows, rows, rows allocated, rows freed, bytes copied in, bytes copied out */
+int prism_kv_stats(prism_tree *t, int64_t *out);
+
 /* ------------------------------------------------------- serving loop
  * engine.run_simulation (engine.py:141-266) with device-resident state: the
  * trace, the pending queue, the admission log and the per-request metrics

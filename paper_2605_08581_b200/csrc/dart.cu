@@ -20,6 +20,7 @@
 #include "select.cuh"
 #include "wave_par.cuh"
 #include "coop.cuh"
+#include "kv.cuh"
 
 using namespace prism;
 
@@ -142,6 +143,15 @@ struct prism_tree {
   int64_t use_coop = 1;                // cooperative single-kernel build / protection
   int64_t use_sample = 1;              // sample select before the materialising selection
   int64_t prebuild = 1;                // fused wave: subtree maxima + sample on the auxiliary stream
+  // paged KV payload (kv.cuh), null when disabled
+  struct Kv {
+    KvDev k{};
+    int32_t *kvx_spare = nullptr;
+    int64_t kvx_cap = 0;
+    int64_t arena_mark = 0, vlog_mark = 0;
+    int64_t *voff = nullptr, *total = nullptr;
+    int64_t voff_cap = 0;
+  } *kv = nullptr;
 };
 
 enum { PH_COMMIT = 0, PH_BUILD = 1, PH_PROTECT = 2, PH_PREMATCH = 3, PH_RELEASE = 4, PH_NOTE = 5, PH_MAINT = 6 };
@@ -484,8 +494,14 @@ int rehash(prism_tree *t, int64_t extra) {
 // compaction of the token arena: live edges packed into the spare arena (kept
 // allocated at the same capacity, so a steady-state compaction is two kernels
 // and a scan, no allocation), then the two swap
+int kv_sync(prism_tree *t, const void *src, void *dst, int64_t *out);
+
 int compact_arena(prism_tree *t, int64_t need) {
   join_aux(t);  // the auxiliary stream must not touch arrays being replaced
+  if (t->kv) {  // settle the payload first: the victims' rows and the new spans move with the arena
+    int rc = kv_sync(t, nullptr, nullptr, nullptr);
+    if (rc) return rc;
+  }
   const int32_t hw = t->hctrl->hw;
   if (hw + 1 > t->cmp_cap) {
     if (t->cmp_len) CK(cudaFree(t->cmp_len));
@@ -515,6 +531,23 @@ int compact_arena(prism_tree *t, int64_t need) {
     t->spare_cap = cap;
   }
   uint32_t *na = t->tok_spare;
+  if (t->kv) {  // the shadow rows follow the spans (before k_compact_copy moves eoff)
+    auto *K = t->kv;
+    if (K->kvx_cap != cap || !K->kvx_spare) {
+      if (K->kvx_spare) CK(cudaFree(K->kvx_spare));
+      CK(dalloc(&K->kvx_spare, cap));
+    }
+    k_kv_compact<<<blocks_for((int64_t)hw * 32), TPB, 0, t->st>>>(t->d, hw, off, K->k.kvx, K->kvx_spare);
+    if (K->kvx_cap == cap) {
+      std::swap(K->k.kvx, K->kvx_spare);
+    } else {
+      CK(cudaFree(K->k.kvx));
+      K->k.kvx = K->kvx_spare;
+      K->kvx_spare = nullptr;
+      K->kvx_cap = cap;
+    }
+    K->arena_mark = live;
+  }
   k_compact_copy<<<blocks_for((int64_t)hw * 32), TPB, 0, t->st>>>(t->d, hw, off, na);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(t->st));
@@ -928,6 +961,13 @@ void prism_tree_destroy(prism_tree *t) {
   if (!t) return;
   cudaSetDevice(t->dev);
   cudaStreamSynchronize(t->st);
+  if (t->kv) {
+    void *kb[] = {t->kv->k.pool, t->kv->k.kvx, t->kv->k.stack, t->kv->k.top, t->kv->k.moved, t->kv->kvx_spare,
+                  t->kv->voff, t->kv->total};
+    for (void *p : kb)
+      if (p) cudaFree(p);
+    delete t->kv;
+  }
   for (auto &f : slot_fields(t)) cudaFree(*f.ptr);
   if (t->tok_spare) cudaFree(t->tok_spare);
   if (t->cmp_len) cudaFree(t->cmp_len);
@@ -1727,6 +1767,130 @@ int prism_profile_read(prism_tree *t, double *out) {
   out[24] = (double)t->lib_calls;
   out[25] = (double)t->hctrl->chain_nodes;
   out[26] = (double)t->hctrl->inserted_tokens;
+  return PRISM_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ paged KV payload (kv.cuh)
+
+namespace {
+__global__ void k_kv_init_stack(int32_t *stack, int64_t rows) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < rows) stack[i] = (int32_t)(rows - 1 - i);  // pops hand out rows 0, 1, 2, ...
+}
+
+// settle the payload after tree operations: rows for the arena grown since the
+// last sync (new resident tokens, admission order; src: their KV, or NULL),
+// the victims logged since the last sync back on the free stack (dst: their
+// KV copied out in eviction order, or NULL).  out[2] = {new tokens, freed tokens}.
+int kv_sync(prism_tree *t, const void *src, void *dst, int64_t *out) {
+  auto *K = t->kv;
+  int rc = pull_ctrl(t);
+  if (rc) return rc;
+  const Ctrl &C = *t->hctrl;
+  const int64_t n_new = C.arena_top - K->arena_mark, nrec = C.vlog_count - K->vlog_mark;
+  if (n_new < 0) return fail(PRISM_FATAL, "KV payload: the arena shrank outside a compaction");
+  if (nrec > t->d.vcap) return fail(PRISM_INVALID, "KV payload: more victims since the last sync than the log keeps");
+  int64_t top = 0;
+  CK(cudaMemcpyAsync(&top, K->k.top, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  if (n_new > top) return fail(PRISM_CAPACITY, "KV pool exhausted (rows must cover capacity + the tokens of one sync)");
+  if (n_new > 0) {
+    k_kv_alloc<<<(unsigned)std::min<int64_t>((n_new * 32 + TPB - 1) / TPB, 65535), TPB, 0, t->st>>>(
+        K->k, K->arena_mark, n_new, (const uint8_t *)src);
+    k_kv_commit_top<<<1, 1, 0, t->st>>>(K->k, -n_new, src ? n_new * K->k.bpt : 0);
+  }
+  int64_t freed = 0;
+  if (nrec > 0) {
+    if (nrec + 1 > K->voff_cap) {
+      if (K->voff) CK(cudaFree(K->voff));
+      K->voff_cap = next_pow2(nrec + 1);
+      CK(dalloc(&K->voff, K->voff_cap));
+    }
+    k_kv_voff<<<1, 1024, 0, t->st>>>(t->d.vlog, t->d.vcap, K->vlog_mark, nrec, K->voff, K->k, K->total, 0);
+    k_kv_free<<<(unsigned)std::min<int64_t>((nrec * 32 + TPB - 1) / TPB, 65535), TPB, 0, t->st>>>(
+        K->k, t->d.vlog, t->d.vcap, K->vlog_mark, nrec, K->voff, (uint8_t *)dst);
+    k_kv_free_top<<<1, 1, 0, t->st>>>(K->k, K->total, dst ? 1 : 0);
+    CK(cudaMemcpyAsync(&freed, K->total, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(t->st));
+  K->arena_mark = C.arena_top;
+  K->vlog_mark = C.vlog_count;
+  if (out) {
+    out[0] = n_new;
+    out[1] = freed;
+  }
+  return PRISM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int prism_kv_enable(prism_tree *t, int64_t rows, int64_t bytes_per_token) {
+  api_enter(t);
+  cudaSetDevice(t->dev);
+  if (t->kv) return fail(PRISM_INVALID, "KV payload already enabled");
+  if (rows <= 0 || rows > INT32_MAX || bytes_per_token <= 0 || bytes_per_token % 16)
+    return fail(PRISM_INVALID, "KV payload: rows in (0, 2^31), bytes_per_token a positive multiple of 16");
+  int rc = pull_ctrl(t);
+  if (rc) return rc;
+  if (t->hctrl->resident != 0) return fail(PRISM_INVALID, "KV payload: enable it on an empty tree");
+  auto *K = new prism_tree::Kv();
+  K->k.bpt = bytes_per_token;
+  K->k.rows = rows;
+  if (cudaMalloc(&K->k.pool, (size_t)rows * (size_t)bytes_per_token) != cudaSuccess) {
+    delete K;
+    return fail(PRISM_CUDA, "KV payload: pool allocation failed");
+  }
+  CK(dalloc(&K->k.kvx, t->d.acap));
+  K->kvx_cap = t->d.acap;
+  CK(dalloc(&K->k.stack, rows));
+  CK(dalloc(&K->k.top, 1));
+  CK(dalloc(&K->k.moved, 4));
+  CK(dalloc(&K->total, 1));
+  k_kv_init_stack<<<blocks_for(rows), TPB, 0, t->st>>>(K->k.stack, rows);
+  CK(cudaMemcpyAsync(K->k.top, &rows, sizeof(int64_t), cudaMemcpyHostToDevice, t->st));
+  CK(cudaMemsetAsync(K->k.moved, 0, 4 * sizeof(int64_t), t->st));
+  CK(cudaStreamSynchronize(t->st));
+  K->arena_mark = t->hctrl->arena_top;
+  K->vlog_mark = t->hctrl->vlog_count;
+  t->kv = K;
+  return PRISM_OK;
+}
+
+int prism_kv_sync(prism_tree *t, const void *src, void *dst, int64_t *out) {
+  api_enter(t);
+  cudaSetDevice(t->dev);
+  if (!t->kv) return fail(PRISM_INVALID, "KV payload not enabled");
+  return kv_sync(t, src, dst, out);
+}
+
+int prism_kv_gather(prism_tree *t, int64_t n, const int32_t *leaf_slots, int64_t max_len, int32_t *table,
+                    void *out, int64_t *lens) {
+  api_enter(t);
+  cudaSetDevice(t->dev);
+  if (!t->kv) return fail(PRISM_INVALID, "KV payload not enabled");
+  if (n <= 0) return PRISM_OK;
+  k_kv_gather<<<(unsigned)((n * 32 + TPB - 1) / TPB), TPB, 0, t->st>>>(t->d, t->kv->k, n, leaf_slots, max_len, table,
+                                                                        (uint8_t *)out, lens);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(t->st));
+  return PRISM_OK;
+}
+
+// out[6]: free rows, rows, rows allocated, rows freed, bytes copied in, bytes copied out
+int prism_kv_stats(prism_tree *t, int64_t *out) {
+  api_enter(t);
+  cudaSetDevice(t->dev);
+  if (!t->kv) return fail(PRISM_INVALID, "KV payload not enabled");
+  int64_t m[4];
+  CK(cudaMemcpyAsync(&out[0], t->kv->k.top, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaMemcpyAsync(m, t->kv->k.moved, sizeof(m), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  out[1] = t->kv->k.rows;
+  for (int i = 0; i < 4; i++) out[2 + i] = m[i];
   return PRISM_OK;
 }
 

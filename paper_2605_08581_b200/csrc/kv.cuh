@@ -1,0 +1,180 @@
+// kv.cuh -- the paged KV payload behind DART (north_star item 4).
+//
+// The reference is token-granular and carries no payload: a
+// node's edge is a token span.  A serving engine attaches KV storage to those
+// tokens; here every resident token owns one row of a KV pool in HBM
+// (bytes_per_token bytes), allocated from a free stack when the token becomes
+// resident and returned when its node is evicted.
+//
+// Mapping: the tree stores every edge as a span of its bump-allocated token
+// arena (a split only moves an offset, compaction moves spans), so the pool
+// row of a resident token is kept in a SHADOW array kvx[arena offset] that
+// travels with the arena.  After any batch of tree operations (a fused wave,
+// a per-call insert / evict) kv_sync settles the payload:
+//   * the arena grown since the last sync = the newly resident tokens, in
+//     admission order (each admitted member's uncached tokens, engine.py:203-
+//     213) -> pop pool rows, optionally copy the new KV in (the prefill's
+//     output, laid out in that order), coalesced 16-B vectors;
+//   * the victim log since the last sync (eviction order, kvcache.py:425-460)
+//     -> optionally copy the victims' KV out (offload, contiguous in eviction
+//     order) and push their rows back (the page-pool free-list update).
+// kv_gather builds, per admitted leaf, the request's row table (req_to_token:
+// pool row of every path position, what an attention kernel reads) by walking
+// the leaf's root chain, and optionally gathers the KV rows themselves.
+#pragma once
+#include <cstdint>
+
+#include "prism_dev.cuh"
+
+namespace prism {
+
+struct KvDev {
+  uint8_t *pool;       // [pool_rows, bpt]
+  int32_t *kvx;        // [acap] pool row of arena token i (valid for live spans)
+  int32_t *stack;      // free rows, [0, top)
+  int64_t *top;        // device scalar: free rows
+  int64_t *moved;      // [0] rows allocated, [1] rows freed, [2] bytes copied in, [3] bytes copied out
+  int64_t bpt;         // bytes per token (multiple of 16)
+  int64_t rows;
+};
+
+// 16-B vector copy of one row
+__device__ __forceinline__ void kv_row_copy(uint8_t *__restrict__ dst, const uint8_t *__restrict__ src, int64_t bpt,
+                                            int lane, int nl) {
+  const int4 *s = reinterpret_cast<const int4 *>(src);
+  int4 *d = reinterpret_cast<int4 *>(dst);
+  for (int64_t v = lane; v < bpt / 16; v += nl) d[v] = s[v];
+}
+
+// newly resident arena tokens [a0, a0 + n): pop rows (stack top - 1 - i) in
+// arena order, optionally copy the payload in (src row i = arena token a0 + i)
+__global__ void k_kv_alloc(KvDev K, int64_t a0, int64_t n, const uint8_t *__restrict__ src) {
+  const int64_t top = *K.top;  // (read by every thread before the last block updates it: see k_kv_commit_top)
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = w; i < n; i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t row = K.stack[top - 1 - i];
+    if (lane == 0) K.kvx[a0 + i] = row;
+    if (src) kv_row_copy(K.pool + (int64_t)row * K.bpt, src + i * K.bpt, K.bpt, lane, 32);  // (warp per row)
+  }
+}
+
+__global__ void k_kv_commit_top(KvDev K, int64_t delta, int64_t bytes_in) {
+  *K.top += delta;
+  if (delta < 0) K.moved[0] += -delta;
+  K.moved[2] += bytes_in;
+}
+
+// victim records [v0, v1) of the log ring: their pool rows, in eviction order,
+// pushed on the stack (record r's rows at top + voff[r] ..), optionally copied
+// out (dst row = voff[r] + i).  voff: exclusive prefix of the records' lengths.
+__global__ void k_kv_free(KvDev K, const VRec *__restrict__ vlog, int64_t vcap, int64_t v0, int64_t nrec,
+                          const int64_t *__restrict__ voff, uint8_t *__restrict__ dst) {
+  const int64_t top = *K.top;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = w; r < nrec; r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const VRec rec = vlog[(v0 + r) % vcap];
+    const int64_t o = voff[r];
+    for (int32_t i = lane; i < rec.elen; i += 32) K.stack[top + o + i] = K.kvx[rec.eoff + i];
+    if (dst) {  // the record's rows back to back, 16-B vectors across the whole record
+      const int64_t vpr = K.bpt / 16, nv = (int64_t)rec.elen * vpr;
+      int4 *d = reinterpret_cast<int4 *>(dst + o * K.bpt);
+      for (int64_t x = lane; x < nv; x += 32) {
+        const int64_t i = x / vpr, v = x - i * vpr;
+        d[x] = reinterpret_cast<const int4 *>(K.pool + (int64_t)K.kvx[rec.eoff + i] * K.bpt)[v];
+      }
+    }
+  }
+}
+
+// exclusive prefix of the victim records' lengths (one CTA) + the total
+__global__ void __launch_bounds__(1024) k_kv_voff(const VRec *__restrict__ vlog, int64_t vcap, int64_t v0,
+                                                  int64_t nrec, int64_t *voff, KvDev K, int64_t *total_out,
+                                                  int64_t copy_bytes) {
+  __shared__ int64_t s_w[32];
+  __shared__ int64_t s_carry;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t b = 0; b < nrec; b += blockDim.x) {
+    const int64_t r = b + threadIdx.x;
+    const int64_t x = r < nrec ? vlog[(v0 + r) % vcap].elen : 0;
+    int64_t inc = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_w[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      int64_t t = lane < nw ? s_w[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      s_w[lane] = t;
+    }
+    __syncthreads();
+    if (r < nrec) voff[r] = s_carry + (wid ? s_w[wid - 1] : 0) + inc - x;
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry += s_w[nw - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *total_out = s_carry;
+    voff[nrec] = s_carry;
+    (void)K;
+    (void)copy_bytes;
+  }
+}
+
+__global__ void k_kv_free_top(KvDev K, const int64_t *total, int64_t copy_out) {
+  *K.top += *total;
+  K.moved[1] += *total;
+  if (copy_out) K.moved[3] += *total * K.bpt;
+}
+
+// arena compaction: the shadow rows follow their spans (same new offsets as k_compact_copy)
+__global__ void k_kv_compact(DT T, int32_t hw, const int64_t *__restrict__ newoff, const int32_t *__restrict__ src,
+                             int32_t *__restrict__ dst) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= hw) return;
+  const int32_t s = (int32_t)w;
+  if (s == ROOT || T.nid[s] < 0 || T.par[s] < 0) return;
+  const int64_t from = T.eoff[s], to = newoff[s];  // (runs before k_compact_copy moves eoff)
+  for (int32_t i = lane_id(); i < T.elen[s]; i += 32) dst[to + i] = src[from + i];
+}
+
+// req_to_token: for leaf j, the pool row of every path position [0, dend(leaf))
+// (row-major [n, max_len]; positions past the path are left alone), by one warp
+// walking the root chain; optionally the KV rows themselves into out[j, p]
+__global__ void k_kv_gather(DT T, KvDev K, int64_t n, const int32_t *__restrict__ leaves, int64_t max_len,
+                            int32_t *__restrict__ table, uint8_t *__restrict__ out, int64_t *__restrict__ lens) {
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  int32_t s = leaves[j];
+  const int64_t len = s > 0 ? T.dend[s] : 0;
+  if (lane == 0) lens[j] = len;
+  int32_t *row = table + j * max_len;
+  while (s > 0) {  // (the root holds no tokens)
+    const int64_t e = T.eoff[s];
+    const int32_t l = T.elen[s];
+    const int64_t p0 = T.dend[s] - l;
+    for (int32_t i = lane; i < l; i += 32)
+      if (p0 + i < max_len) row[p0 + i] = K.kvx[e + i];
+    s = T.par[s];
+  }
+  if (!out) return;
+  __syncwarp();
+  const int64_t m = len < max_len ? len : max_len;
+  const int64_t vpr = K.bpt / 16, nv = m * vpr;
+  int4 *d = reinterpret_cast<int4 *>(out + j * max_len * K.bpt);
+  for (int64_t x = lane; x < nv; x += 32) {  // 16-B vectors across all the request's rows
+    const int64_t p = x / vpr, v = x - p * vpr;
+    d[x] = reinterpret_cast<const int4 *>(K.pool + (int64_t)row[p] * K.bpt)[v];
+  }
+}
+
+}  // namespace prism
