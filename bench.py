@@ -104,6 +104,9 @@ def parse_args():
     ap.add_argument("--profile-steps", type=int, default=3,
                     help="extra waves AFTER the timed region with the per-phase device profile on (roofline)")
     ap.add_argument("--ref-seconds", type=float, default=0.5, help="reference arm: seconds per step per worker")
+    ap.add_argument("--kv-bytes", type=int, default=0,
+                    help="wave mode: attach a paged KV payload of this many bytes per token (copy-in of the new "
+                         "tokens, copy-out of the victims, req_to_token tables inside every timed step)")
     ap.add_argument("--mode", default="wave", choices=["wave", "serve"],
                     help="wave: timed fused waves on a warm tree; serve: the whole serving loop over a trace")
     ap.add_argument("--requests", type=int, default=10_000_000, help="serve mode: requests in the global trace")
@@ -223,6 +226,19 @@ def oracle_parity_job(args, world: int, rank: int, out_path: str) -> None:
         res = oracle_windows(rep, warm + check, record_from=len(warm))
     res["timing"] = np.append(res["timing"], time.perf_counter() - t0)
     np.savez(out_path, **res)
+
+
+def _kv_line(acc: dict, args, peak: float) -> dict:
+    """The paged KV payload's share of the timed steps: copy-in of the new tokens' KV,
+    copy-out of the victims' KV (each read once + written once), req_to_token tables."""
+    w = max(acc["waves"], 1)
+    moved = 2 * (acc["new"] + acc["freed"]) * args.kv_bytes + acc["table_bytes"]
+    gbs = moved / max(acc["ms"], 1e-9) / 1e6
+    return {"bytes_per_token": args.kv_bytes, "ms_per_wave": acc["ms"] / w, "new_tokens_per_wave": acc["new"] / w,
+            "freed_tokens_per_wave": acc["freed"] / w, "bytes_per_wave": moved / w, "achieved_gbs": gbs,
+            "peak_gbs": peak, "frac": gbs / peak,
+            "note": "kv_sync (row alloc + copy-in, victim copy-out + free-list push, with its host syncs) + "
+                    "req_to_token gather, inside the timed steps"}
 
 
 def _demand_reducer(args, world: int, dev):
@@ -353,6 +369,32 @@ def run_ours(args) -> None:
     stream_in = S.ShardStream(args.workload, args.seed, world, rank)
     demand = torch.zeros(spec.nseg, dtype=torch.int32, device=dev) if world > 1 else None
 
+    kv = None
+    if args.kv_bytes > 0:  # the paged KV payload (kv.cuh): a pool row per resident token
+        from paper_2605_08581_b200.kv import KvPool
+
+        max_new = B * spec.path_len
+        kv = KvPool(engine.t, args.capacity + 2 * max_new, args.kv_bytes)
+        kv_src = torch.randint(0, 255, (max_new, args.kv_bytes), dtype=torch.uint8, device=dev)  # the prefill's KV
+        kv_dst = torch.empty((args.capacity, args.kv_bytes), dtype=torch.uint8, device=dev)  # the offload tier
+        kv_acc = {"ms": 0.0, "new": 0, "freed": 0, "table_bytes": 0, "waves": 0}
+
+    def kv_step(na, timed):
+        if kv is None:
+            return
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record(stream)
+        new, freed = kv.sync(kv_src, kv_dst)
+        kv.gather(engine.leaf_slots, na, spec.path_len)
+        k1.record(stream)
+        if timed:
+            k1.synchronize()
+            kv_acc["ms"] += k0.elapsed_time(k1)
+            kv_acc["new"] += new
+            kv_acc["freed"] += freed
+            kv_acc["table_bytes"] += na * spec.path_len * 4
+            kv_acc["waves"] += 1
+
     glob = args.workload == "c5"
     if glob:  # the global-demand knob: P-hat from the replicas' summed per-window demand
         demand = torch.zeros(spec.nseg, dtype=torch.int32, device=dev)
@@ -389,6 +431,7 @@ def run_ours(args) -> None:
         wp = to_dev(stream_in.take(min(B, args.warm - i)))
         pre_step(wp)
         _, prev = engine.step(wp)
+        kv_step(prev, False)
     torch.cuda.synchronize()
     warm_s = time.perf_counter() - t_ws
 
@@ -398,11 +441,14 @@ def run_ours(args) -> None:
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     hitsum = torch.zeros(1, dtype=torch.int64, device=dev)
 
+    timed_now = [False]
+
     def one_step(pend):
         nonlocal prev
         engine.release(engine.leaf_slots, prev)
         pre_step(pend)
         nm, na = engine.step(pend)
+        kv_step(na, timed_now[0])
         allreduce_demand()
         prev = na
         return nm, na
@@ -419,6 +465,7 @@ def run_ours(args) -> None:
     torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" scopes profiles here
     evs = []
     admitted = members = 0
+    timed_now[0] = True
     for s in range(args.warmup, nsteps):
         with torch.cuda.stream(stream):
             flush.zero_()
@@ -433,6 +480,7 @@ def run_ours(args) -> None:
         admitted += na
         members += nm
     torch.cuda.synchronize()
+    timed_now[0] = False
     torch.cuda.nvtx.range_pop()
     if world > 1:
         dist.barrier()
@@ -466,6 +514,7 @@ def run_ours(args) -> None:
         for s in range(ew):
             pre_step(pinned[e2e_steps + s])
             _, prev = engine.step_host(pinned[e2e_steps + s], out_mem, out_hits, release_n=prev)
+            kv_step(prev, False)
             allreduce_demand()
         torch.cuda.synchronize()
         if world > 1:
@@ -479,6 +528,7 @@ def run_ours(args) -> None:
             tw = time.perf_counter()
             pre_step(pinned[s])
             nm, na = engine.step_host(pinned[s], out_mem, out_hits, release_n=prev)
+            kv_step(na, False)
             wall.append((time.perf_counter() - tw) * 1e3)
             prev = na
             allreduce_demand()
@@ -611,6 +661,7 @@ def run_ours(args) -> None:
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "kv_payload": None if kv is None else _kv_line(kv_acc, args, peak),
             "gpu_launches": gpu_launches,
             "lib_calls": prof1["lib_calls"] - prof0["lib_calls"],
             "clocks": clk,
