@@ -445,9 +445,8 @@ def run_ours(args) -> None:
 
     def one_step(pend):
         nonlocal prev
-        engine.release(engine.leaf_slots, prev)
         pre_step(pend)
-        nm, na = engine.step(pend)
+        nm, na = engine.step(pend, release_n=prev)  # the previous wave's pins drop inside the wave
         kv_step(na, timed_now[0])
         allreduce_demand()
         prev = na

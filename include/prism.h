@@ -269,6 +269,10 @@ int prism_qas_demand(prism_qas *q, int64_t P, const int64_t *sk_off, const int32
  * P-hat[r] = w_g*G[r] + w_a*a[r] + w_n*n[r] (scheduler.py:247-251 with g := G)
  * instead of the local round's.  NULL restores the reference behaviour. */
 int prism_qas_set_global_demand(prism_qas *q, const int32_t *G, int32_t nseg);
+/* Completions handed to the next prism_wave_step on this tree (engine.py:171-175):
+ * the n pins of the DEVICE leaf slots are dropped at the start of that wave, on
+ * a forked stream beside its QAS round, joined before the protection hand-off. */
+int prism_qas_defer_release(prism_qas *q, int64_t n, const int32_t *slots);
 
 /* One serving-loop wave entirely on the device (engine.py:189-213):
  * schedule_round over the DEVICE-resident pending CSR, the protection (DART)

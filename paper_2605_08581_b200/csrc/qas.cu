@@ -571,6 +571,12 @@ struct prism_qas {
   int32_t small_coresident = 0;
   const int32_t *gdem = nullptr;  // all-reduced demand counters feeding P-hat (nullptr: the local round's)
   int32_t gdem_n = 0;
+  // pins to drop at the start of the next wave (prism_qas_defer_release): on a
+  // forked stream, overlapping the QAS round, joined before the tree work
+  const int32_t *rel_slots = nullptr;
+  int64_t rel_n = 0;
+  cudaStream_t st_rel = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_rel = nullptr;
   int64_t last_small_grid = 0;
   bool full_reset = true;
   int64_t small_rounds = 0;
@@ -1064,6 +1070,9 @@ void prism_qas_destroy(prism_qas *q) {
   if (q->hout_mem) cudaFreeHost(q->hout_mem);
   if (q->hout_hit) cudaFreeHost(q->hout_hit);
   if (q->ev_t) cudaEventDestroy(q->ev_t);
+  if (q->ev_fork) cudaEventDestroy(q->ev_fork);
+  if (q->ev_rel) cudaEventDestroy(q->ev_rel);
+  if (q->st_rel) cudaStreamDestroy(q->st_rel);
   if (q->e0) cudaEventDestroy(q->e0);
   if (q->e1) cudaEventDestroy(q->e1);
   cudaStreamDestroy(q->st);
@@ -1365,6 +1374,13 @@ int prism_qas_small_timeline(prism_qas *q, int64_t *out_ns, int32_t n) {
   return PRISM_OK;
 }
 
+int prism_qas_defer_release(prism_qas *q, int64_t n, const int32_t *slots) {
+  if (n < 0) return qfail(PRISM_INVALID, "negative release count");
+  q->rel_n = n;
+  q->rel_slots = slots;
+  return PRISM_OK;
+}
+
 int prism_qas_set_global_demand(prism_qas *q, const int32_t *G, int32_t nseg) {
   if (G && nseg <= 0) return qfail(PRISM_INVALID, "global demand needs nseg > 0");
   q->gdem = G;
@@ -1480,8 +1496,22 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
   const QIn gin{q->gids, q->garr, q->goff, q->gsk, q->greo, nullptr, nullptr};
   const int64_t btmask = qas_small_btmask(P);
   const int64_t tok_cap = q->tok_cap, anc_cap = std::min(q->a_off_cap, q->a_snap_cap / 3);
+  const int64_t rel_n = q->rel_n;
+  const int32_t *rel_slots = q->rel_slots;
+  q->rel_n = 0;
+  if (rel_n > 0 && !q->st_rel) {
+    QCK(cudaStreamCreateWithFlags(&q->st_rel, cudaStreamNonBlocking));
+    QCK(cudaEventCreateWithFlags(&q->ev_fork, cudaEventDisableTiming));
+    QCK(cudaEventCreateWithFlags(&q->ev_rel, cudaEventDisableTiming));
+  }
   auto body = [&]() -> int {
     int r;
+    if (rel_n > 0) {  // the previous wave's pins drop beside the round (nothing in it reads ref counts)
+      QCK(cudaEventRecord(q->ev_fork, st));
+      QCK(cudaStreamWaitEvent(q->st_rel, q->ev_fork, 0));
+      if ((r = prism_release_device(t, rel_n, rel_slots, nullptr, (void *)q->st_rel))) return r;
+      QCK(cudaEventRecord(q->ev_rel, q->st_rel));
+    }
     if ((r = qas_small_launch(q, gin, P, 0, btmask, c, G, true))) return r;  // (q_stage zeroed the counters)
     q_members_scan<<<1, 1024, 0, st>>>(nh, nc, q->hot, q->cv2, q->gids, q->goff, q->gsfx, sys_len, chunk, members,
                                        q->plen, q->alen, q->poff, q->aoffs, q->tmp_tot, q->qcounts, tok_cap,
@@ -1491,6 +1521,7 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
       q_prio<<<nblk(nseg), TPB, 0, st>>>(nseg, q->gdem, q->a, q->nd, c, q->prio_glob, q->dom_glob);
       pri = q->prio_glob;
     }
+    if (rel_n > 0) QCK(cudaStreamWaitEvent(st, q->ev_rel, 0));  // the releases, before anything reads ref
     QCK(cudaEventRecord(q->ev_t, st));  // (the protection on the tree's streams reads pri)
     QCK(cudaStreamWaitEvent((cudaStream_t)prism_tree_stream(t), q->ev_t, 0));
     if ((r = prism_set_protection_device_async(t, pri, nseg))) return r;  // overlaps serialization
@@ -1513,11 +1544,11 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
     const void *ptrs[] = {members, hits, leaf_slots, leaf_ids, q->gids, q->goff, q->gsfx, q->garr, q->greo, q->gsk,
                           q->aligned, q->g, q->a, q->nd, q->prio, q->dom, q->poff, q->aoffs, q->plen, q->alen,
                           q->tok, q->a_off, q->a_kind, q->a_seg, q->a_snap, q->err, q->tmp_tot, q->qcounts, q->hres,
-                          q->touched, q->tn, q->rk, q->emap, q->efirst, q->btake, q->bbase, q->gdem, q->prio_glob, q->dom_glob, q->longl, q->sig, q->siglen, q->tkey, q->tmin,
+                          q->touched, q->tn, q->rk, q->emap, q->efirst, q->btake, q->bbase, q->gdem, q->prio_glob, q->dom_glob, rel_slots, q->st_rel, q->longl, q->sig, q->siglen, q->tkey, q->tmin,
                           q->slot_of, q->bmin, q->bstart, q->bend, q->score, q->take, q->rank, q->bucket, q->hot,
                           q->cv2, q->pk, q->pv, q->plist, host_out ? q->hout_mem : nullptr,
                           host_out ? q->hout_hit : nullptr};
-    const int64_t dims[] = {P, B, G, btmask, nseg, sys_len, chunk, tok_cap, anc_cap, q->pk_cap, q->pv_cap,
+    const int64_t dims[] = {P, B, G, btmask, nseg, sys_len, chunk, tok_cap, anc_cap, q->pk_cap, q->pv_cap, rel_n,
                             q->aligned_cap, q->rk_cap, q->emap_cap, q->efirst_cap, (int64_t)q->prof_on};
     const double cw[] = {c.wg, c.wa, c.wn, c.alpha, c.beta, (double)c.budget, (double)c.cold, (double)c.front,
                          (double)c.kappa};
@@ -1631,7 +1662,10 @@ int prism_wave_step_host(prism_tree *t, prism_qas *q, int64_t P, const int64_t *
   cudaSetDevice(q->dev);
   q->hout_ready = 0;
   int rc;
-  if (release_n > 0 && (rc = prism_release_device(t, release_n, release_slots, nullptr, (void *)q->st))) return rc;
+  if (release_n > 0) {  // dropped by the wave itself, beside its QAS round
+    q->rel_n = release_n;
+    q->rel_slots = release_slots;
+  }
   if ((rc = wave_step_impl(t, q, P, ids, arrival, sk_off, sk, reorderable, suffix, A, act_off, act_sk, nseg, cfg,
                            sys_len, chunk, members_out, hits, leaf_slots, leaf_ids, n_members, n_admitted, true)))
     return rc;
@@ -1671,6 +1705,11 @@ int wave_step_impl(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, c
     int rc = wave_step_graph(t, q, P, ids, arrival, sk_off, sk, reorderable, suffix, nseg, c, sys_len, chunk,
                              members_out, hits, leaf_slots, leaf_ids, n_members, n_admitted, &handled, host_out);
     if (rc || handled) return rc;
+  }
+  if (q->rel_n > 0) {  // deferred pins (prism_qas_defer_release) not taken by the graph path
+    int r2 = prism_release_device(t, q->rel_n, q->rel_slots, nullptr, (void *)st);
+    q->rel_n = 0;
+    if (r2) return r2;
   }
   if (q->prof_on) cudaEventRecord(q->e0, st);
   // QAS round (engine.py:189): one launch for the one-CTA/cooperative round

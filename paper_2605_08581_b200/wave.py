@@ -36,6 +36,7 @@ def _bind(lib):
         "prism_qas_counters": (C.c_int, [_p, _p, C.c_int32]),
         "prism_qas_demand": (C.c_int, [_p, _i64, _p, _p, C.c_int32, _p]),
         "prism_qas_set_global_demand": (C.c_int, [_p, _p, C.c_int32]),
+        "prism_qas_defer_release": (C.c_int, [_p, _i64, _p]),
         "prism_set_protection_device": (C.c_int, [_p, _p, C.c_int32, _p, _p]),
         "prism_profile": (C.c_int, [_p, C.c_int32]),
         "prism_profile_read": (C.c_int, [_p, _p]),
@@ -120,7 +121,8 @@ class WaveEngine:
         except Exception:  # pragma: no cover
             pass
 
-    def step(self, pend: DevicePending, active: DevicePending | None = None) -> tuple[int, int]:
+    def step(self, pend: DevicePending, active: DevicePending | None = None, release_n: int = 0,
+             release_slots: torch.Tensor | None = None) -> tuple[int, int]:
         """One wave; returns (members dispatched, members admitted).
 
         ``active``: the requests in flight (engine.py:189 ``active.values()``),
@@ -129,6 +131,11 @@ class WaveEngine:
         (engine.py:195-197).  None: no request in flight."""
         P = pend.P
         A, aoff, ask = self._active(active)
+        if release_n > 0:  # completions dropped by the wave itself, beside its QAS round
+            slots = self.leaf_slots if release_slots is None else release_slots
+            if release_slots is None and P > self.members.shape[0]:
+                raise ValueError("release_n refers to leaf_slots, which a larger pending set would reallocate")
+            check(self.L.prism_qas_defer_release(self.q, int(release_n), slots.data_ptr()))
         self._ensure(P)
         check(self.L.prism_wave_step(
             self.t, self.q, P, pend.ids.data_ptr(), pend.arrival.data_ptr(), pend.sk_off.data_ptr(),
