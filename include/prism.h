@@ -114,8 +114,9 @@ int prism_admit_wave_segmented(prism_tree *t, int64_t B, const int64_t *path_off
                                const int64_t *sk_off, const int32_t *aligned, int64_t sys_len,
                                int64_t chunk, int32_t mode, int64_t *hits, int32_t *leaf_slots,
                                int64_t *leaf_ids, int64_t *n_admitted_host, void *stream);
-/* out[3]: waves committed in parallel, waves committed in order, last
- * fallback reason bit-set (wave_par.cuh WPF_*). */
+/* out[4]: waves committed in parallel, waves committed in order, last
+ * fallback reason bit-set (wave_par.cuh WPF_*), parallel waves that stopped
+ * on a CapacityError (engine.py:209-212). */
 int prism_wave_stats(prism_tree *t, int64_t *out);
 
 /* Batched release of device-resident leaves (engine.py:177-181 for a whole
@@ -231,7 +232,7 @@ int prism_wave_commit_enqueue(prism_tree *t, int64_t B, const int64_t *path_off,
                               const int32_t *a_snap, const int64_t *members, const int64_t *sk_off,
                               const int32_t *aligned, int64_t sys_len, int64_t chunk, int64_t *hits,
                               int32_t *leaf_slots, int64_t *leaf_ids, void *stream, const int32_t *abort);
-int prism_wave_commit_finish(prism_tree *t, int64_t B, int32_t *applied);
+int prism_wave_commit_finish(prism_tree *t, int64_t B, int32_t *applied, int64_t *n_admitted);
 uint64_t prism_wave_commit_key(prism_tree *t);
 /* The cudaStream_t (as void*) the QAS instance launches on; prism_wave_step
  * completes on it, so events recorded there bracket a whole wave. */

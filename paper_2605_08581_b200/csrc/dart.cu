@@ -134,7 +134,7 @@ struct prism_tree {
   int64_t *ds_part = nullptr;
   int sms = 0;
   int64_t wx_cap = 0, wx_lt = 0, wx_T = 0;
-  int64_t par_waves = 0, seq_waves = 0;
+  int64_t par_waves = 0, seq_waves = 0, trunc_waves = 0;
   int32_t last_fallback = 0;
   // tunables (prism_tune): eviction-list prefix sizing
   int64_t list_min_tokens = 1 << 18;   // ordered commit: select >= this many tokens
@@ -201,6 +201,7 @@ std::vector<SlotField> slot_fields(prism_tree *t) {
       {(void **)&d.prot, 1},   {(void **)&d.hasanc, 1}, {(void **)&d.akind, 1},  {(void **)&d.aseg, 4},
       {(void **)&d.aoff, 4},   {(void **)&d.snap, 12},  {(void **)&d.hslot, 4},  {(void **)&d.kver, 4},
       {(void **)&d.wmod, 4},   {(void **)&d.wchild, 4}, {(void **)&d.waitf, 4},  {(void **)&d.guard, 4},
+      {(void **)&d.wchm, 8},
       {(void **)&d.kw, sizeof(Key3)}, {(void **)&d.eff, 4}, {(void **)&d.freelist, 4},
       {(void **)&d.Lk, sizeof(Key3)}, {(void **)&d.Lv, 8},
   };
@@ -735,15 +736,19 @@ int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *lea
   k_vscan_a<<<DS_BLOCKS, 256, 0, st>>>(t->d, X, t->ds_part, wc);
   k_vscan_c<<<DS_BLOCKS, 256, 0, st>>>(t->d, X, t->ds_part, wc);
   k_wp_cuts<<<blocks_for(B), TPB, 0, st>>>(t->d, B, X, wc);  // + the cut verdict (last CTA)
+  k_wp_conflicts<<<2 * sms, TPB, 0, st>>>(t->d, X, wc);     // consumed victims on a running member's chain
   k_wp_evict<<<2 * sms, TPB, 0, st>>>(t->d, wc);
   k_wp_alloc<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_label_reset<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_create<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_touch<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_label<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc, hits, leaf_slots, leaf_ids);
+  // a CapacityError stop: the stopping member's evict call sweeps the rest of the order
+  k_wp_sweep_a<<<DS_BLOCKS, 256, 0, st>>>(t->d, t->ds_part, wc);
+  k_wp_sweep_c<<<DS_BLOCKS, 256, 0, st>>>(t->d, X, t->ds_part, wc);
   k_wc_finalize<<<1, 1, 0, st>>>(t->d, B, X, wc, t->h_wc, t->hctrl);  // + verdict, control block to the host
   CK(cudaGetLastError());
-  t->launches[PH_COMMIT] += 11;
+  t->launches[PH_COMMIT] += 14;
   return PRISM_OK;
 }
 
@@ -1435,7 +1440,8 @@ int prism_admit_wave_segmented(prism_tree *t, int64_t B, const int64_t *path_off
     if (rc) return rc;
     if (applied) {
       t->par_waves++;
-      *n_admitted_host = B;
+      if (t->h_wc->trunc) t->trunc_waves++;
+      *n_admitted_host = t->h_wc->Bc;  // (< B: the wave stopped on a CapacityError)
       if (stream) {
         cudaEvent_t ev;
         CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1489,13 +1495,15 @@ int prism_wave_commit_enqueue(prism_tree *t, int64_t B, const int64_t *path_off,
 }
 
 // *applied = 1: the enqueued attempt committed the wave
-int prism_wave_commit_finish(prism_tree *t, int64_t B, int32_t *applied) {
+int prism_wave_commit_finish(prism_tree *t, int64_t B, int32_t *applied, int64_t *n_admitted) {
   int ap = 0, again = 0;
   int32_t ff = 0;
   int rc = wave_par_verdict(t, &ap, &again, &ff);
   if (rc) return rc;
   *applied = ap;
   if (ap) t->par_waves++;
+  if (ap && t->h_wc->trunc) t->trunc_waves++;
+  if (n_admitted) *n_admitted = ap ? t->h_wc->Bc : 0;
   (void)B;
   return PRISM_OK;
 }
@@ -1527,6 +1535,7 @@ int prism_wave_stats(prism_tree *t, int64_t *out) {
   out[0] = t->par_waves;
   out[1] = t->seq_waves;
   out[2] = t->last_fallback;
+  out[3] = t->trunc_waves;
   return PRISM_OK;
 }
 

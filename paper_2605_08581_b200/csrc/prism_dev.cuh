@@ -128,6 +128,7 @@ struct DT {
   uint32_t *wchild;
   uint32_t *waitf;
   uint32_t *guard;
+  uint64_t *wchm;  // parallel wave: (epoch << 32) | ~(first member whose pre-wave chain holds the node)
   Key3 *kw;
   int32_t *eff;
   int32_t *freelist;

@@ -1614,11 +1614,12 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
   q->rounds++;
   q->small_rounds++;
   int32_t applied = 0;
-  if ((rc = prism_wave_commit_finish(t, B, &applied))) return rc;
+  int64_t nadm = 0;
+  if ((rc = prism_wave_commit_finish(t, B, &applied, &nadm))) return rc;
   *handled = true;
   *n_members = B;
   if (applied) {
-    *n_admitted = B;
+    *n_admitted = nadm;  // (< B: the wave stopped on a CapacityError)
     q->hout_ready = host_out ? 1 : 0;  // results already in the pinned output buffers
     return PRISM_OK;
   }

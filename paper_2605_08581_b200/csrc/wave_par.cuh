@@ -22,6 +22,13 @@
 //   * touches / pins / labels: atomics (hits += 2 per traversing member, last =
 //     max insert tick, ref += 1, label = last writer = max member index).
 //
+// A CapacityError stop (engine.py:209-212) commits in parallel too: with the
+// WHOLE order listed, the first member j* whose demand exceeds every valid
+// entry cannot be satisfied, so members [0, j*) commit as above, j* matches
+// (its touches) and its evict call sweeps every entry still evictable at its
+// time -- valid, unpinned after the earlier members' pins, not on its own
+// guarded chain (kvcache.py:243-273) -- in list order, and the wave stops.
+//
 // Exactness guards (else the host falls back to k_commit for the wave): no
 // pre-match chain overflow, no partially matched pre-wave node, pre-wave
 // chain nodes aligned 1:1 with pieces, no skeleton-hash collision, no
@@ -80,6 +87,9 @@ struct WaveCtl {
   int32_t ft0, hw0;
   uint32_t vctr0, epoch;
   int32_t stop, flags;                     // WC_*; fallback reason (WPF_*)
+  int64_t Bc;                              // members committed (B, or j* on a CapacityError stop)
+  int64_t nsw, swfreed;                    // the stopping member's sweep: victims, tokens
+  int32_t trunc, pad;                      // 1: the wave stops at member Bc (CapacityError)
 };
 
 __device__ inline int64_t wp_end(const WaveIn &W, int p, int k, int64_t n) {
@@ -144,6 +154,8 @@ __global__ void k_wp_plan(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
       const int32_t c = W.pm_chain[j * PM_MAX + p];
       if ((int64_t)T.dend[c] != wp_end(W, p, k, n)) flag |= WPF_ALIGN;
       T.wchild[c] = epoch;  // "on some member's pre-wave chain" (victim guard)
+      atomicMax((unsigned long long *)&T.wchm[c],
+                ((unsigned long long)epoch << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)j));  // first such member
     }
     if (!flag && (d > 0 ? wp_end(W, d - 1, k, n) : 0) != hit_pre) flag |= WPF_ALIGN;
   }
@@ -290,7 +302,7 @@ __global__ void k_wp_evict(DT T, const WaveCtl *wc) {
 __global__ void k_wp_alloc(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, j = t / WP_PL;
   const int pl = (int)(t % WP_PL);
-  if (j >= W.B || wc->stop || X.cnew[j] == 0) return;
+  if (j >= W.B || wc->stop || j >= wc->Bc || X.cnew[j] == 0) return;
   const int64_t id0 = wc->id0;
   const int32_t free_top = wc->ft0 + (int32_t)wc->nv, hw = wc->hw0;
   const uint32_t vctr0 = wc->vctr0 + (uint32_t)wc->nv, epoch = wc->epoch;
@@ -327,7 +339,7 @@ __device__ inline int32_t wp_node(const WaveIn &W, const WaveTmp &X, int64_t j, 
 __global__ void k_wp_create(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = lane_id();
-  if (j >= W.B || wc->stop || X.cnew[j] == 0) return;
+  if (j >= W.B || wc->stop || j >= wc->Bc || X.cnew[j] == 0) return;
   const int64_t arena0 = wc->arena0, clock0 = wc->clock0;
   const int64_t m = W.members[j];
   const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
@@ -383,7 +395,7 @@ __global__ void k_wp_touch(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t j = t % W.B;
   const int lane = threadIdx.x & 31;
-  const bool live = t < (int64_t)W.B * WP_PL;  // (threads past the grid's rows only vote)
+  const bool live = t < (int64_t)W.B * WP_PL && j < wc->Bc;  // (others only vote)
   const int P = live ? X.npieces[j] : 0;
   const int own0 = live ? (X.cnew[j] ? X.p0[j] : P) : 0;
   const unsigned long long base_tick = (unsigned long long)(wc->clock0 + 2);
@@ -404,24 +416,27 @@ __global__ void k_wp_touch(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
       atomicMax(&T.eff[s], (int32_t)jall);
     }
   }
-  const unsigned m0 = __ballot_sync(0xffffffffu, live && t < (int64_t)W.B);
+  const unsigned m0 = __ballot_sync(0xffffffffu, live && t < (int64_t)W.B);  // (members < Bc)
   if (m0 && lane == __ffs(m0) - 1) atomicAdd(&T.ref[ROOT], __popc(m0));  // _pin reaches the root (kvcache.py:344-348)
 }
 
 __global__ void k_wp_label_reset(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, j = t / WP_PL;
   const int pl = (int)(t % WP_PL);
-  if (j >= W.B || wc->stop) return;
+  if (j >= W.B || wc->stop || j >= wc->Bc) return;
   const int own0 = X.cnew[j] ? X.p0[j] : X.npieces[j];
   for (int p = pl; p < own0; p += WP_PL) T.eff[wp_node(W, X, j, p)] = -1;
 }
 
 // W8: the elected (max-index) member writes kind/seg/anchor (kvcache.py:317-340)
+__device__ inline void wp_stop_touch(DT T, const WaveIn &W, const WaveTmp &X, const WaveCtl *wc);
+
 __global__ void k_wp_label(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc, int64_t *hits, int32_t *leaf_slots,
                            int64_t *leaf_ids) {
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x < 32) wp_stop_touch(T, W, X, wc);  // (a CapacityError stop)
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, j = t / WP_PL;
   const int pl = (int)(t % WP_PL);
-  if (j >= W.B || wc->stop) return;
+  if (j >= W.B || wc->stop || j >= wc->Bc) return;
   const int64_t m = W.members[j];
   const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
   const int64_t n = W.poff[j + 1] - W.poff[j];
@@ -462,6 +477,7 @@ __global__ void k_wc_begin(DT T, WaveCtl *wc, const int32_t *abort, WaveTmp X, i
   *X.flags = 0;
   for (int q = 0; q < 8; q++) X.misc[q] = 0;
   X.misc[1] = 0x7F7F7F7F7F7F7F7Fll;
+  X.misc[5] = 0x7F7F7F7F7F7F7F7Fll;  // j*: the first member the whole order cannot satisfy
   Ctrl *C = T.ctrl;
   C->epoch++;
   WaveCtl w{};
@@ -476,6 +492,7 @@ __global__ void k_wc_begin(DT T, WaveCtl *wc, const int32_t *abort, WaveTmp X, i
   w.hw0 = C->hw;
   w.vctr0 = C->vctr;
   w.W = -1;
+  w.Bc = 0;
   *wc = w;
 }
 
@@ -508,6 +525,7 @@ __device__ inline void wc_plan_body(DT T, int64_t B, WaveTmp X, WaveCtl *wc, int
   }
   const int64_t D = wc->R0 + nmiss - T.capacity;
   wc->W = D > 0 ? (force_full ? 0 : D + D / 4 + slack) : -1;
+  wc->Bc = B;
 }
 
 __global__ void __launch_bounds__(1024) k_wp_scan3(DT T, int64_t B, WaveTmp X, WaveCtl *wc, int64_t slack,
@@ -535,33 +553,35 @@ __global__ void __launch_bounds__(1024) k_wp_scan3(DT T, int64_t B, WaveTmp X, W
 // evict calls (members whose cut advances) and the tokens freed
 __device__ inline void wc_cut_body(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
   __shared__ int64_t s_calls[32];
+  const int32_t flags = __ldcg(X.flags);
+  // a CapacityError stop commits the members before it (when the whole order
+  // is listed: a partial prefix proves nothing -- take the whole order)
+  const bool cap = (flags & WPF_CAPACITY) != 0;
+  const int64_t jstar = (int64_t)__ldcg((const unsigned long long *)&X.misc[5]);
+  const int64_t Bc = cap ? (jstar < B ? jstar : B) : B;
   int64_t calls = 0;
-  for (int64_t j = threadIdx.x; j < B; j += blockDim.x) calls += __ldcg(&X.cut[j]) > (j ? __ldcg(&X.cut[j - 1]) : 0) ? 1 : 0;
+  for (int64_t j = threadIdx.x; j < Bc; j += blockDim.x) calls += __ldcg(&X.cut[j]) > (j ? __ldcg(&X.cut[j - 1]) : 0) ? 1 : 0;
   for (int o = 16; o > 0; o >>= 1) calls += __shfl_xor_sync(0xffffffffu, calls, o);
   if ((threadIdx.x & 31) == 0) s_calls[threadIdx.x >> 5] = calls;
   __syncthreads();
   if (threadIdx.x) return;
   calls = 0;
   for (int w = 0; w < (int)(blockDim.x >> 5); w++) calls += s_calls[w];
-  const int64_t nv = __ldcg(&X.cut[B - 1]);
-  const int32_t flags = __ldcg(X.flags);
   const int64_t poison = X.misc[1];
-  if (flags & WPF_CAPACITY) {
-    if (T.ctrl->L_partial) {
-      wc->stop = WC_FULL;  // the selected prefix fell short: the whole order
-    } else {
-      wc->stop = WC_FALLBACK;
-      wc->flags = flags;
-    }
+  if (cap && T.ctrl->L_partial) {
+    wc->stop = WC_FULL;  // the selected prefix fell short: the whole order
     return;
   }
-  if (flags || poison < nv) {
+  const int64_t nv = Bc > 0 ? __ldcg(&X.cut[Bc - 1]) : 0;
+  if ((flags & ~WPF_CAPACITY) || poison < nv) {
     wc->stop = WC_FALLBACK;
-    wc->flags = flags ? flags : WPF_VICTIM;
+    wc->flags = (flags & ~WPF_CAPACITY) ? flags : WPF_VICTIM;
     return;
   }
+  wc->Bc = Bc;
+  wc->trunc = Bc < B ? 1 : 0;
   wc->nv = nv;
-  wc->calls = calls;
+  wc->calls = calls + (Bc < B ? 1 : 0);  // the stopping member's evict call
   wc->freed = nv > 0 ? X.F[nv - 1] : 0;
 }
 
@@ -584,6 +604,7 @@ __global__ void k_wp_cuts(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
       }
       if (lo >= Tn) {
         atomicOr(X.flags, WPF_CAPACITY);
+        atomicMin((unsigned long long *)&X.misc[5], (unsigned long long)j);
         c = Tn;
       } else {
         c = lo + 1;
@@ -603,24 +624,27 @@ __global__ void k_wp_cuts(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
 
 // the control block after the committed wave (what the ordered commit leaves)
 __device__ inline void wc_finalize_body(DT T, int64_t B, const WaveTmp &X, const WaveCtl *wc) {
+  (void)B;
   Ctrl *C = T.ctrl;
-  const int64_t nv = wc->nv, ncreate = wc->ncreate;
+  const int64_t Bc = wc->Bc, nv = wc->nv, nsw = wc->nsw;
+  const int64_t ncreate = X.idb[Bc], ntail = X.arb[Bc], nmiss = Bc > 0 ? X.dem[Bc - 1] : 0;
   const int32_t ft1 = wc->ft0 + (int32_t)nv;
   const int64_t from_free = ncreate < ft1 ? ncreate : ft1;
   const int64_t reused = X.misc[2];
-  C->free_top = ft1 - (int32_t)from_free;
+  C->free_top = ft1 - (int32_t)from_free + (int32_t)nsw;
   C->hw = wc->hw0 + (int32_t)(ncreate - from_free);
-  C->resident = wc->R0 + wc->nmiss - wc->freed;
-  C->clock = wc->clock0 + 2 * B;
+  C->resident = wc->R0 + nmiss - wc->freed - wc->swfreed;
+  C->clock = wc->clock0 + 2 * Bc + (wc->trunc ? 1 : 0);  // the stopping member's match tick
   C->next_id = wc->id0 + ncreate;
-  C->arena_top = wc->arena0 + wc->ntail;
-  C->vlog_count += nv;
-  C->hlive += ncreate - nv;
-  C->htomb += nv - reused;
+  C->arena_top = wc->arena0 + ntail;
+  C->vlog_count += nv + nsw;
+  C->hlive += ncreate - nv - nsw;
+  C->htomb += nv + nsw - reused;
   C->evict_calls += wc->calls;
-  C->vctr = wc->vctr0 + (uint32_t)(nv + ncreate);
-  C->n_admitted = (int32_t)B;
-  C->fast_members += B;
+  C->vctr = wc->vctr0 + (uint32_t)(nv + ncreate + nsw);
+  C->n_admitted = (int32_t)Bc;
+  C->fast_members += Bc;
+  if (wc->trunc) C->gstamp += 1;  // (the sweep's guard stamp)
   C->inserted_tokens += X.misc[3];
   C->chain_nodes += X.misc[4];
   C->status = ST_DONE;
@@ -650,8 +674,26 @@ __device__ __forceinline__ int64_t wp_vlen(const DT &T, const WaveTmp &X, int64_
   const uint64_t v = T.Lv[i];
   const int32_t s = (int32_t)(v & 0xffffffffu);
   const bool valid = T.kver[s] == (uint32_t)(v >> 32) && T.nid[s] >= 0 && T.par[s] >= 0 && T.ref[s] == 0;
-  if (mark && (!valid || T.wchild[s] == epoch)) atomicMin((unsigned long long *)&X.misc[1], (unsigned long long)i);
+  if (mark) {
+    if (!valid) atomicMin((unsigned long long *)&X.misc[1], (unsigned long long)i);
+    // the first member whose pre-wave chain holds it (k_wp_conflicts: a victim a running member matched)
+    const uint64_t m = T.wchm[s];
+    X.vlen[i] = (uint32_t)(m >> 32) == epoch ? (int64_t)(0xFFFFFFFFu - (uint32_t)m) : 0x7FFFFFFFFFFFFFFFll;
+  }
   return valid ? T.elen[s] : 0;
+}
+
+// a victim consumed by the committed members [0, Bc) that lies on the pre-wave
+// chain of a member that runs (index <= Bc: the committed ones and a stopping
+// one) changes that member's match: the exactness guard (nothing applied yet)
+__global__ void k_wp_conflicts(DT T, WaveTmp X, WaveCtl *wc) {
+  if (wc->stop) return;
+  const int64_t nv = wc->nv, Bc = wc->Bc;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x)
+    if (X.vlen[i] <= Bc) {
+      wc->flags = WPF_VICTIM;
+      wc->stop = WC_FALLBACK;
+    }
 }
 
 __global__ void __launch_bounds__(256) k_vscan_a(DT T, WaveTmp X, int64_t *part, const WaveCtl *wc) {
@@ -709,6 +751,122 @@ __global__ void __launch_bounds__(256) k_vscan_c(DT T, WaveTmp X, const int64_t 
     if (threadIdx.x == blockDim.x - 1) carry = before + x;
     __syncthreads();
   }
+}
+
+// ------------------------------------------------------------ CapacityError stop (member Bc = j*)
+
+// j*'s match (kvcache.py:146-171: hits + 1, last = its match tick on every
+// node of its matched prefix) and the guard of its reserve (its pre-wave
+// chain, kvcache.py:252-266), one warp of k_wp_label (after the earlier
+// members' pins, before the sweep)
+__device__ inline void wp_stop_touch(DT T, const WaveIn &W, const WaveTmp &X, const WaveCtl *wc) {
+  if (wc->stop || !wc->trunc) return;
+  const int64_t j = wc->Bc;
+  const int lane = lane_id();
+  const int d = W.pm_meta[4 * j + 1];
+  const uint32_t stamp = T.ctrl->gstamp + 1;
+  for (int p = lane; p < d; p += 32) T.guard[W.pm_chain[j * PM_MAX + p]] = stamp;
+  const int64_t tick = wc->clock0 + 2 * j + 1;
+  for (int p = lane; p < X.p0[j]; p += 32) {
+    const int32_t s = wp_node(W, X, j, p);
+    atomicAdd(&T.hits[s], 1);
+    atomicMax((unsigned long long *)&T.last[s], (unsigned long long)tick);
+  }
+}
+
+// the sweep: list entries [nv, L_n) still evictable at j*'s time, in list order
+__device__ __forceinline__ bool wp_sweepable(const DT &T, int64_t i, uint32_t stamp) {
+  const uint64_t v = T.Lv[i];
+  const int32_t s = (int32_t)(v & 0xffffffffu);
+  return T.kver[s] == (uint32_t)(v >> 32) && T.nid[s] >= 0 && T.par[s] >= 0 && T.ref[s] == 0 && T.guard[s] != stamp;
+}
+
+__global__ void __launch_bounds__(256) k_wp_sweep_a(DT T, int64_t *part, const WaveCtl *wc) {
+  if (wc->stop || !wc->trunc) return;
+  const int64_t nv = wc->nv, n = T.ctrl->L_n - nv, per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = nv + blockIdx.x * per, b1 = b0 + per < nv + n ? b0 + per : nv + n;
+  const uint32_t stamp = T.ctrl->gstamp + 1;
+  int64_t c = 0;
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) c += wp_sweepable(T, i, stamp) ? 1 : 0;
+  __shared__ int64_t sw[8];
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += sw[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+// each CTA: its carry from the counts before it, then its sweepable entries
+// detached in order (victim log, free list, child table, parents' child counts)
+__global__ void __launch_bounds__(256) k_wp_sweep_c(DT T, WaveTmp X, const int64_t *part, WaveCtl *wc) {
+  if (wc->stop || !wc->trunc) return;
+  __shared__ int64_t sw[8];
+  __shared__ int64_t carry;
+  const int64_t nv = wc->nv, n = T.ctrl->L_n - nv, per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = nv + blockIdx.x * per, b1 = b0 + per < nv + n ? b0 + per : nv + n;
+  const uint32_t stamp = T.ctrl->gstamp + 1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  {
+    int64_t x = 0;
+    for (int q = threadIdx.x; q < (int)blockIdx.x; q += blockDim.x) x += part[q];
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) sw[wid] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t c = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); w++) c += sw[w];
+      carry = c;
+    }
+    __syncthreads();
+  }
+  const int64_t Bc = wc->Bc, ncreate = X.idb[Bc];
+  const int32_t ft1 = wc->ft0 + (int32_t)nv;
+  const int64_t fbase = ft1 - (ncreate < ft1 ? ncreate : ft1);  // the free list after this wave's allocations
+  int64_t tok = 0;
+  for (int64_t t0 = b0; t0 < b1; t0 += blockDim.x) {
+    const int64_t i = t0 + threadIdx.x;
+    const bool on = i < b1 && wp_sweepable(T, i, stamp);
+    const unsigned bal = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) sw[wid] = __popc(bal);
+    __syncthreads();
+    int64_t before = carry;
+    for (int w = 0; w < wid; w++) before += sw[w];
+    before += __popc(bal & ((1u << lane) - 1u));
+    if (on) {
+      const int32_t s = (int32_t)(T.Lv[i] & 0xffffffffu);
+      const int32_t p = T.par[s];
+      atomicSub(&T.nch[p], 1);
+      VRec rec;
+      rec.id = T.nid[s];
+      rec.eoff = T.eoff[s];
+      rec.ftok = T.ftok[s];
+      rec.elen = T.elen[s];
+      rec.seg = T.seg[s];
+      rec.kind = (int8_t)T.kind[s];
+      rec.pad[0] = rec.pad[1] = rec.pad[2] = 0;
+      tok += rec.elen;
+      T.ht[T.hslot[s]].key = HTOMB;
+      T.vlog[(wc->vbase + nv + before) % T.vcap] = rec;
+      T.nid[s] = -1;
+      T.par[s] = -1;
+      T.kver[s] = wc->vctr0 + (uint32_t)(nv + ncreate + before) + 1;
+      T.wmod[s] = wc->epoch;
+      T.freelist[fbase + before] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t c = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); w++) c += sw[w];
+      carry += c;
+    }
+    __syncthreads();
+  }
+  for (int o = 16; o > 0; o >>= 1) tok += __shfl_xor_sync(0xffffffffu, tok, o);
+  if (lane == 0 && tok) atomicAdd((unsigned long long *)&wc->swfreed, (unsigned long long)tok);
+  if (threadIdx.x == 0 && blockIdx.x == gridDim.x - 1) wc->nsw = carry;  // (the last CTA's carry: all of them)
 }
 
 }  // namespace prism

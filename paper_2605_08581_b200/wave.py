@@ -237,9 +237,10 @@ class WaveEngine:
         check(self.L.prism_qas_set_commit_mode(self.q, mode))
 
     def wave_stats(self) -> dict:
-        out = np.zeros(3, dtype=np.int64)
+        out = np.zeros(4, dtype=np.int64)
         check(self.L.prism_wave_stats(self.t, out.ctypes.data))
-        return {"parallel_waves": int(out[0]), "ordered_waves": int(out[1]), "last_fallback": int(out[2])}
+        return {"parallel_waves": int(out[0]), "ordered_waves": int(out[1]), "last_fallback": int(out[2]),
+                "capacity_stops": int(out[3])}
 
     def tune(self, **kw) -> None:
         """Eviction-list prefix sizing (see DeviceRadixCache.tune)."""

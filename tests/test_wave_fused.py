@@ -362,3 +362,17 @@ def test_inflight_active_set(policy, host):
 ])
 def test_inflight_variants(variant):
     run_inflight(7, CachePolicy.DART, **variant)
+
+
+@pytest.mark.parametrize("variant", [
+    dict(cap=300, wave=24, nwaves=8, nseg=100_000, hot=0),            # no sharing: no chain conflicts
+    dict(cap=250, wave=32, nwaves=12, suffixes=(0, 2)),
+    dict(cap=500, wave=48, nwaves=8, nseg=50_000, hot=1, kmin=3, kmax=6),
+])
+def test_capacity_stop_commits_in_parallel(variant):
+    """A wave whose demand exceeds the evictable tokens stops at the first member
+    the whole eviction order cannot satisfy (CapacityError, engine.py:209-212):
+    the members before it commit in parallel, the stopping member's match and
+    evict sweep are applied, and everything equals the oracle."""
+    st = run_case(21, CachePolicy.DART, mode=0, protect=2, **variant)
+    assert st["capacity_stops"] > 0, st
