@@ -610,7 +610,7 @@ int run_commit(prism_tree *t, CommitArgs a) {
         rc = grow_slots(t, (int64_t)c.hw + 2 + MAX_ANCH);
         break;
       case ST_NEED_ARENA: {
-        const int64_t n = a.mode == 1 ? (int64_t)MAX_PATH : a.op_n;
+        const int64_t n = std::max<int64_t>(a.mode == 1 ? (int64_t)MAX_PATH : a.op_n, c.need_hint);
         rc = compact_arena(t, n);
         break;
       }
@@ -719,7 +719,7 @@ int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *lea
       t->d, wc, abort, X, t->wx_lt);
   k_wp_plan<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_levels<<<blocks_for(B * WP_PL), TPB, 0, st>>>(W, X);
-  k_wp_hits<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X);
+  k_wp_hits<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_scan3<<<1, 1024, 0, st>>>(t->d, B, X, wc, t->list_slack_tokens, force_full);  // + the plan verdict
   CK(cudaGetLastError());
   t->launches[PH_COMMIT] += 5;
@@ -1009,7 +1009,7 @@ void prism_tree_destroy(prism_tree *t) {
 int prism_match(prism_tree *t, const uint32_t *path, int64_t n, int64_t *hit, int32_t *visited_slots,
                 int64_t *visited_ids, int64_t *n_visited) {
   api_enter(t);
-  if (n < 0 || n > MAX_PATH) return fail(PRISM_INVALID, "path length out of range");
+  if (n < 0 || n > (int64_t)INT32_MAX) return fail(PRISM_INVALID, "path length out of range");
   cudaSetDevice(t->dev);
   int rc = ensure_buf(&t->d_path, t->path_cap, n);
   if (rc) return rc;
@@ -1056,7 +1056,7 @@ int prism_insert(prism_tree *t, const uint32_t *path, int64_t n, int64_t na, con
                  const int8_t *a_kind, const int32_t *a_seg, const int32_t *a_snap, int32_t *leaf_slot,
                  int64_t *leaf_id) {
   api_enter(t);
-  if (n < 0 || n > MAX_PATH) return fail(PRISM_INVALID, "path length out of range");
+  if (n < 0 || n > (int64_t)INT32_MAX) return fail(PRISM_INVALID, "path length out of range");
   int rc = validate_anchors(n, na, a_off, a_kind, a_seg);
   if (rc) return rc;
   cudaSetDevice(t->dev);
@@ -1551,7 +1551,7 @@ int prism_admit_wave(prism_tree *t, int64_t B, const int64_t *path_off, const ui
   }
   for (int64_t j = 0; j < B; j++) {
     const int64_t n = path_off[j + 1] - path_off[j];
-    if (n < 0 || n > MAX_PATH) return fail(PRISM_INVALID, "path length out of range");
+    if (n < 0 || n > (int64_t)INT32_MAX) return fail(PRISM_INVALID, "path length out of range");
     const int64_t a0 = anc_off[j], na = anc_off[j + 1] - a0;
     int rc = validate_anchors(n, na, a_off + a0, a_kind + a0, a_seg + a0);
     if (rc) return rc;

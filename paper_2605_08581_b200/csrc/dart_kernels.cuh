@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
       ab = 0;
       na = A.op_na;
     }
-    if (n > MAX_PATH || na > MAX_ANCH) {
+    if (na > MAX_ANCH) {
       C.fatal = 1;
       C.status = ST_FATAL;
       break;
@@ -494,6 +494,7 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
       }
       if (C.arena_top + n > T.acap) {
         C.status = ST_NEED_ARENA;
+        C.need_hint = n;  // (the host compacts / grows the arena for at least this)
         break;
       }
       if ((C.hlive + C.htomb + need_nodes) * 2 > (int64_t)(T.hmask + 1)) {
@@ -546,8 +547,10 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
       continue;
     }
 
-    // stage the path in shared memory
-    for (int64_t i = lane; i < n; i += 32) sp[i] = A.tok[pb + i];
+    // stage the path in shared memory; longer paths are read from HBM in place
+    const uint32_t *pth = n <= MAX_PATH ? sp : A.tok + pb;
+    if (n <= MAX_PATH)
+      for (int64_t i = lane; i < n; i += 32) sp[i] = A.tok[pb + i];
     if (type == OP_INSERT) {
       for (int64_t i = lane; i < na; i += 32) {
         sa_off[i] = A.a_off[ab + i];
@@ -579,7 +582,7 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
           // member may have added a child with exactly this first token
           if (!(fl & 1) && hit_pre < n) {
             const int32_t tnode = d > 0 ? A.pm_chain[(int64_t)member * PM_MAX + d - 1] : ROOT;
-            if (ht_lookup(T, tnode, sp[hit_pre]) >= 0) bad = true;
+            if (ht_lookup(T, tnode, pth[hit_pre]) >= 0) bad = true;
           }
           valid = !__any_sync(FULL, bad);
           __syncwarp();
@@ -594,7 +597,7 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
       if (valid) {
         C.fast_members += (type == OP_MATCH);
       } else {
-        const WalkOut w = warp_walk(T, sp, n, Ps, MAX_PNODES);
+        const WalkOut w = warp_walk(T, pth, n, Ps, MAX_PNODES);
         if (w.overflow) {
           C.fatal = 2;
           C.status = ST_FATAL;
@@ -707,14 +710,14 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
       const int32_t Tn = alloc_slot(T, C);
       const int64_t len = n - hit;
       const int64_t base = C.arena_top;
-      for (int64_t i = lane; i < len; i += 32) T.tok[base + i] = sp[hit + i];
+      for (int64_t i = lane; i < len; i += 32) T.tok[base + i] = pth[hit + i];
       bool tomb = false;
-      const uint64_t hidx = ht_probe_free(T, ckey(parent, sp[hit]), &tomb);
+      const uint64_t hidx = ht_probe_free(T, ckey(parent, pth[hit]), &tomb);
       const int32_t pn = T.nch[parent];
       __syncwarp();
       if (lane == 0) {
         T.par[Tn] = parent;
-        T.ftok[Tn] = sp[hit];
+        T.ftok[Tn] = pth[hit];
         T.eoff[Tn] = base;
         T.elen[Tn] = (int32_t)len;
         T.dend[Tn] = (int32_t)n;
@@ -725,7 +728,7 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
         T.kind[Tn] = K_PRIVATE;
         T.seg[Tn] = SEG_NONE;
         HEnt e;
-        e.key = ckey(parent, sp[hit]);
+        e.key = ckey(parent, pth[hit]);
         e.val = (uint32_t)Tn;
         e.pad = 0;
         T.ht[hidx] = e;

@@ -1227,9 +1227,10 @@ __global__ void q_members_len(int64_t nh, int64_t nc, const int64_t *__restrict_
                               const int64_t *__restrict__ cold, const int64_t *__restrict__ ids,
                               const int64_t *__restrict__ off, const int32_t *__restrict__ suffix, int64_t sys,
                               int64_t chunk, int64_t *__restrict__ members, int64_t *__restrict__ plen,
-                              int64_t *__restrict__ alen, int32_t *err) {
+                              int64_t *__restrict__ alen, int32_t *err, const int64_t *redo = nullptr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nh + nc) return;
+  if (redo && *redo) return;  // the one-launch round overflowed: no dispatch order to read (redone)
   const int64_t m = i < nh ? hot[i] : cold[i - nh];
   members[i] = m;
   const int64_t k = off[m + 1] - off[m], sfx = suffix[m];
@@ -1263,6 +1264,10 @@ __global__ void __launch_bounds__(1024) q_members_scan(int64_t nh, int64_t nc, c
                                                        const int64_t *__restrict__ qcounts, int64_t tok_cap,
                                                        int64_t anc_cap, int32_t *err, int32_t *abort) {
   const int64_t B = nh + nc;
+  if (qcounts[3]) {  // the one-launch round overflowed its buffers: no dispatch order (uniform)
+    if (threadIdx.x == 0) *abort = 1;
+    return;
+  }
   __shared__ int s_err;
   if (threadIdx.x == 0) s_err = 0;
   __syncthreads();
@@ -1735,7 +1740,7 @@ int wave_step_impl(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, c
     if (B > 0) {
       QCK(cudaMemsetAsync(q->err, 0, sizeof(int32_t), st));
       q_members_len<<<nblk(B), TPB, 0, st>>>(nh, nc, q->hot, q->cv2, ids, sk_off, suffix, sys_len, chunk, members,
-                                             q->plen, q->alen, q->err);
+                                             q->plen, q->alen, q->err, nb < 0 ? q->qcounts + 3 : nullptr);
       q_scan2<<<1, 1024, 0, st>>>(B, q->plen, q->alen, q->poff, q->aoffs, q->tmp_tot);
       q->launches += 2;
     }

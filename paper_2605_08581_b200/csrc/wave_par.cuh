@@ -211,12 +211,16 @@ __global__ void k_wp_levels(WaveIn W, WaveTmp X) {
 }
 
 // W2: intra-wave share, hit, new pieces, demand
-__global__ void k_wp_hits(DT T, WaveIn W, WaveTmp X) {
+__global__ void k_wp_hits(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= W.B) return;
+  if (j >= W.B || wc->stop) return;  // (an aborted wave never ran the plan)
   if (*X.flags) return;
   const int64_t m = W.members[j];
   const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
+  if (k + 2 > WP_MAXP) {  // (the plan flags these shapes; own_at below holds WP_MAXP levels)
+    atomicOr(X.flags, WPF_SHAPE);
+    return;
+  }
   const int32_t *s = W.aligned + W.sk_off[m];
   const int64_t n = W.poff[j + 1] - W.poff[j];
   const int P = X.npieces[j];
