@@ -123,6 +123,10 @@ int prism_wave_stats(prism_tree *t, int64_t *out);
  * completion batch); the leaves must hold valid pins. */
 int prism_release_device(prism_tree *t, int64_t n, const int32_t *slots, const int64_t *ids,
                          void *stream);
+/* The inverse of prism_release_device: +1 ref along each DEVICE leaf slot's
+ * root chain (an explicit lock of a cached prefix; the SGLang-style adapter's
+ * inc_lock_ref).  Released with prism_release_device. */
+int prism_pin_device(prism_tree *t, int64_t n, const int32_t *slots, void *stream);
 
 /* ---------------------------------------------------------- introspection */
 /* out[16]: resident_tokens, clock, next_id, slot high-water mark, live nodes,

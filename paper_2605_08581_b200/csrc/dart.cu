@@ -1109,6 +1109,17 @@ int prism_release_device(prism_tree *t, int64_t n, const int32_t *slots, const i
   return PRISM_OK;
 }
 
+int prism_pin_device(prism_tree *t, int64_t n, const int32_t *slots, void *stream) {
+  api_enter(t);
+  if (n <= 0) return PRISM_OK;
+  cudaSetDevice(t->dev);
+  cudaStream_t s = stream ? (cudaStream_t)stream : t->st;
+  k_pin_par<<<blocks_for(n), TPB, 0, s>>>(t->d, n, slots);
+  CK(cudaGetLastError());
+  t->launches[PH_RELEASE]++;
+  return PRISM_OK;
+}
+
 int prism_evict(prism_tree *t, int64_t k_free, int64_t *freed) {
   api_enter(t);
   if (k_free < 0) return fail(PRISM_INVALID, "k_free must be >= 0");

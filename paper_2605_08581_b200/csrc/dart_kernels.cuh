@@ -1001,6 +1001,19 @@ __global__ void k_release_par(DT T, int64_t n, const int32_t *__restrict__ slots
   }
 }
 
+// the inverse: +1 along each leaf's root chain (an explicit lock of a cached
+// prefix, e.g. the SGLang-style adapter's inc_lock_ref)
+__global__ void k_pin_par(DT T, int64_t n, const int32_t *__restrict__ slots) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int32_t x = i < n ? slots[i] : -1;
+  while (__any_sync(0xffffffffu, x >= 0)) {
+    const unsigned peers = __match_any_sync(0xffffffffu, x);
+    if (x >= 0 && lane == __ffs(peers) - 1) atomicAdd(&T.ref[x], __popc(peers));
+    if (x >= 0) x = T.par[x];
+  }
+}
+
 // ------------------------------------------------------------ maintenance
 
 __global__ void k_rehash(DT T, int32_t hw, int64_t *live) {

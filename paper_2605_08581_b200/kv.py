@@ -45,6 +45,9 @@ class KvPool:
         uint8 [>= new, bytes_per_token] of the new tokens' KV (admission
         order); ``dst``: uint8 [>= freed, bytes_per_token] for the victims' KV."""
         out = np.zeros(2, np.int64)
+        for t in (src, dst):  # (produced on torch's stream; the pool works on the tree's)
+            if t is not None:
+                torch.cuda.current_stream(t.device).synchronize()
         check(self.L.prism_kv_sync(self.h, src.data_ptr() if src is not None else None,
                                    dst.data_ptr() if dst is not None else None, out.ctypes.data))
         return int(out[0]), int(out[1])
@@ -55,6 +58,7 @@ class KvPool:
         table = torch.full((max(n, 1), max_len), -1, dtype=torch.int32, device=dev)
         lens = torch.zeros(max(n, 1), dtype=torch.int64, device=dev)
         out = torch.zeros((max(n, 1), max_len, self.bpt), dtype=torch.uint8, device=dev) if payload else None
+        torch.cuda.current_stream(dev).synchronize()  # (the fills above and leaf_slots: torch's stream)
         check(self.L.prism_kv_gather(self.h, n, leaf_slots.data_ptr(), max_len, table.data_ptr(),
                                      out.data_ptr() if out is not None else None, lens.data_ptr()))
         return table[:n], lens[:n], (out[:n] if out is not None else None)
