@@ -26,8 +26,8 @@ constexpr int COOP_TPB = 512;
 constexpr int COOP_ROUNDS = 14;
 constexpr int CHUNK = 4096;  // bitonic chunk per CTA (shared memory)
 // sample select (coop_sample_select)
-constexpr int SS_SAMP = 8192;  // samples at most
-constexpr int SS_SPL = 1536;   // splitters (selected samples) at most
+constexpr int SS_SAMP = 12288;  // samples at most (the period is the power of two that keeps the sample below this)
+constexpr int SS_SPL = 2560;   // splitters (selected samples) at most
 constexpr int SS_U = 2048;     // undecided samples kept as a list (more: flags only)
 constexpr size_t COOP_SORT_SMEM = (sizeof(Key3) + sizeof(uint64_t)) * CHUNK;
 constexpr size_t COOP_SMEM = COOP_SORT_SMEM;
@@ -1025,6 +1025,8 @@ __global__ void __launch_bounds__(SS_SEL_TPB) k_ss_select(Cand cand, CoopBufs B,
   for (int w = 0; w < (int)(blockDim.x >> 5); w++) tot += s_u64[w];
   __syncthreads();
   // target sub-sample mass: (1.25 W + 3 average sub-samples of slack) / (m q)
+  // (the tau estimate comes from <= SS_SUB sub-samples: ~7% noise; a prefix
+  // short of W costs the materialising selection, so the margin stays wide)
   coop_mark(st);
   const double mq = (double)m * q;
   long long need = nsub > 0 ? (long long)(((double)W * 1.25 + 3.0 * mq * ((double)tot / nsub)) / mq) + 1 : 1;

@@ -383,6 +383,8 @@ int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const 
   if (prism::attr_once(attr)) {
     CK(cudaFuncSetAttribute(k_ss_select<EvictCand>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SEL_SMEM));
     CK(cudaFuncSetAttribute(k_ss_select<ProtCand>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SEL_SMEM));
+    CK(cudaFuncSetAttribute(k_ss_filter<EvictCand>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_FILTER_SMEM));
+    CK(cudaFuncSetAttribute(k_ss_filter<ProtCand>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_FILTER_SMEM));
     CK(cudaFuncSetAttribute(k_ss_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_SORT_SMEM));
     CK(cudaFuncSetAttribute(k_ss_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS_BIG_SMEM));
   }
