@@ -363,7 +363,7 @@ def run_ours(args) -> None:
     B = args.wave
     cache, sched = _configs(args)
     engine_kw = dict(cache=cache, sched=sched, nseg=spec.nseg, sys_len=spec.sys_len, chunk=spec.chunk, device=gpu,
-                     initial_slots=1 << 21, initial_arena_tokens=max(1 << 26, 4 * args.capacity))
+                     initial_slots=1 << 21, initial_arena_tokens=max(1 << 26, 32 * args.capacity))
     engine = WaveEngine(**engine_kw)
     stream = engine.stream
     stream_in = S.ShardStream(args.workload, args.seed, world, rank)
@@ -459,6 +459,7 @@ def run_ours(args) -> None:
         dist.barrier()
     prof0 = engine.profile_read()
     st1 = engine.stats()
+    cmp0 = engine.compactions()
     clocks = Clocks(gpu)
     clocks.start()
     torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" scopes profiles here
@@ -486,7 +487,9 @@ def run_ours(args) -> None:
     clk = clocks.stop()
     prof1 = engine.profile_read()
     st2 = engine.stats()
-    ms = sum(a.elapsed_time(b) for a, b in evs)
+    cmp1 = engine.compactions()
+    per_step = [a.elapsed_time(b) for a, b in evs]
+    ms = sum(per_step)
     hit_tokens = int(hitsum.item())
     hit_rate = hit_tokens / max(admitted * spec.path_len, 1)
     if world > 1:
@@ -653,6 +656,10 @@ def run_ours(args) -> None:
                 "slow_path_members": st2["slow_members"] - st1["slow_members"],
                 "profile": "per-phase device profile taken on extra waves after the timed region",
                 "commit": engine.wave_stats(),
+                "step_ms": {"min": round(min(per_step), 4), "median": round(statistics.median(per_step), 4),
+                            "max": round(max(per_step), 4)},
+                "arena_compactions_timed": cmp1 - cmp0,
+                "arena_tokens": engine_kw["initial_arena_tokens"],
                 "cuda_graph": engine.graph_stats(),
             },
             "hit_rate": hit_rate,
@@ -731,7 +738,7 @@ def run_serve(args) -> None:
     mine = S.shard_trace(trace, world, rank)
     gen_s = time.perf_counter() - t_gen
     cfg = _serve_config(args, world)
-    kw = dict(device=gpu, initial_slots=1 << 20, initial_arena_tokens=max(1 << 24, 4 * cfg.cache.capacity_tokens))
+    kw = dict(device=gpu, initial_slots=1 << 20, initial_arena_tokens=max(1 << 24, 32 * cfg.cache.capacity_tokens))
     t0 = time.perf_counter()
     loop = DeviceServingLoop(cfg, mine, **kw)  # the trace's H2D copy (end-to-end)
     stream = torch.cuda.ExternalStream(loop.L.prism_qas_stream(loop.q), device=dev)

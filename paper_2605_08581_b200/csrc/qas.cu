@@ -567,7 +567,7 @@ struct prism_qas {
 #undef QBUF
   int64_t small_max_p = 4096;  // one-launch rounds up to this many pending (<= QS_MAXP)
   int64_t small_grid = 0;      // CTAs of a one-launch round (0: from small_per_cta)
-  int64_t small_per_cta = 32;  // pending requests per CTA when sizing the grid
+  int64_t small_per_cta = 24;  // pending requests per CTA when sizing the grid (4096 -> every SM)
   int32_t small_coresident = 0;
   const int32_t *gdem = nullptr;  // all-reduced demand counters feeding P-hat (nullptr: the local round's)
   int32_t gdem_n = 0;

@@ -294,6 +294,12 @@ class WaveEngine:
         prof["inserted_tokens"] = int(out[26])
         return prof
 
+    def compactions(self) -> int:
+        """Token-arena compactions so far (maintenance between waves)."""
+        self.L.prism_compactions.restype = C.c_int64
+        self.L.prism_compactions.argtypes = [_p]
+        return int(self.L.prism_compactions(self.t))
+
     def stats(self) -> dict:
         out = np.zeros(16, dtype=np.int64)
         check(self.L.prism_stats(self.t, out.ctypes.data))
