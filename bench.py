@@ -60,6 +60,7 @@ UNIT = "decisions/s"
 
 # per-workload defaults: requests in the warm start, capacity (tokens), wave size
 DEFAULTS = {
+    "c2": {"warm": 0, "capacity": 5760, "wave": 8},  # serve mode only (--mode serve): the QPS sweep
     "c3": {"warm": 8 * 4096, "capacity": 36_000_000, "wave": 4096},
     "mu1m": {"warm": 125_000, "capacity": 16_000_000, "wave": 4096},
     "c4": {"warm": 16 * 1024, "capacity": 4_000_000, "wave": 1024},
@@ -153,6 +154,9 @@ class Clocks:
         self.path = None
 
     def start(self):
+        if os.environ.get("PRISM_BENCH_NO_CLOCKS"):  # (diagnostics only: the bench line then has no clocks)
+            self.proc = None
+            return
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
         try:
@@ -843,10 +847,84 @@ def run_serve(args) -> None:
         dist.destroy_process_group()
 
 
+def run_serve_c2(args) -> None:
+    """C2: the reference's default RAG trace (WorkloadSpec:
+    981 segments, chunk 128, 20 hot, k 5, r_hot 0.7, Zipf 1.2, 2048 requests,
+    seed 1) at the 13B-model KV budget of 5760 tokens, QPS swept over
+    {10, 15, 20, 25, 30}; the whole serving loop on the device per point, each
+    point checked against the oracle serving loop (every request's hit / TTFT,
+    the admission order, every victim)."""
+    from types import SimpleNamespace
+
+    import torch
+
+    from oracle.oracle import build
+    from oracle.serve_loop import oracle_serve
+    from paper_2605_08581_b200.serve import DeviceServingLoop, TraceCSR
+    from paper_2605_08581_b200.types import CacheConfig, CachePolicy, SchedulerConfig, SegmentCatalog
+    from traces.refgen import WorkloadConfig, generate_trace
+
+    build()
+    torch.cuda.set_device(0)
+    cat = SegmentCatalog(num_segments=981, chunk_tokens=128, hot_set=tuple(range(20)), sys_prefix_tokens=28)
+    cfg = SimpleNamespace(prefill_rate=1e4, decode_rate=4e4, output_tokens=32, decode_attenuation_enabled=False,
+                          cache=CacheConfig(capacity_tokens=5760, policy=CachePolicy.DART, protect_budget=20),
+                          scheduler=SchedulerConfig(window_s=0.05, dispatch_budget=8, cold_quota=2))
+    points, adm_all, ms_all, ok_all, cpu_dec, cpu_s = [], 0, 0.0, True, 0, 0.0
+    clocks = Clocks(0)
+    clocks.start()
+    for qps in (10.0, 15.0, 20.0, 25.0, 30.0):
+        tr = TraceCSR.from_trace(generate_trace(WorkloadConfig(qps=qps, num_requests=2048, k=5, r_hot=0.7,
+                                                               zipf_alpha=1.2, suffix_tokens=100, seed=1), cat))
+        loop = DeviceServingLoop(cfg, tr)
+        stream = torch.cuda.ExternalStream(loop.L.prism_qas_stream(loop.q), device=torch.device("cuda", 0))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        loop.run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        res = loop.result()
+        victims = loop.cache_view().victim_log()
+        loop.close()
+        o = oracle_serve(tr, cfg)
+        same = (np.array_equal(res.hit_tokens, o["hit"]) and np.array_equal(res.first_token, o["first_token"])
+                and np.array_equal(res.wave_members, o["wave_members"]) and victims == o["victims"].tolist())
+        ok_all &= same
+        cpu_dec += o["decisions"]
+        cpu_s += o["seconds"]
+        sm = res.summary()
+        points.append({"qps": qps, "decisions_per_s": tr.n / (ms / 1000.0), "ms": round(ms, 3),
+                       "waves": int(len(res.wave_launch)), "hit_rate": sm["hit_rate"], "ttft_p50": sm["p50"],
+                       "ttft_p99": sm["p99"], "victims": len(victims), "identical_to_oracle": bool(same)})
+        adm_all += tr.n
+        ms_all += ms
+    clk = clocks.stop()
+    line = {
+        "metric": METRIC, "value": adm_all / (ms_all / 1000.0), "unit": UNIT, "n_gpus": 1,
+        "steps": sum(p["waves"] for p in points), "warmup": 0, "ms_per_step": ms_all / max(sum(p["waves"] for p in points), 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "C2: the reference default RAG trace (981 segments, chunk 128, 20 hot, k 5, r_hot 0.7, "
+                               "Zipf 1.2, 2048 requests, seed 1) at the 13B-model KV budget (5760 tokens), QPS sweep "
+                               "10..30, whole serving loop on the device (waves of <= 8)", "mode": "serve",
+                   "sweep": points},
+        "parity": {"identical": bool(ok_all), "scope": "every sweep point: per-request hits and TTFTs, admission "
+                                                     "order, every victim vs the oracle serving loop"},
+        "roofline": None,
+        "cpu_baseline": {"value": cpu_dec / max(cpu_s, 1e-9), "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"{cpu_dec} decisions in {cpu_s:.2f}s inside the oracle serving loop's waves, "
+                                   f"all five sweep points"},
+        "e2e": None, "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.mode == "serve" and args.workload == "c2":
+        run_serve_c2(args)
     elif args.mode == "serve" and not (args.gpus > 1 and "WORLD_SIZE" not in os.environ):
         run_serve(args)
     elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:

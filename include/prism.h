@@ -355,6 +355,8 @@ int prism_serve_requests(prism_serve *s, double *admit, double *prefill_end, dou
 /* WaveRecord (engine.py:69-76): members as trace indices, admission order. */
 int prism_serve_waves(prism_serve *s, double *launch, double *duration, int64_t *uncached, int64_t *cached,
                       int64_t *member_off, int32_t *members);
+/* Host wall time (us) of each wave (diagnostics), float[waves]. */
+int prism_serve_wave_times(prism_serve *s, float *out_us);
 
 /* ------------------------------------------------------- trace ingestion
  * workload.load_trace (workload.py:258-313) natively: a save_trace JSON-lines

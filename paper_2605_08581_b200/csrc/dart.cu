@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <cub/cub.cuh>
@@ -579,7 +580,24 @@ int run_commit(prism_tree *t, CommitArgs a) {
   // prefix, then the whole order: any prefix gives the same victims
   int64_t last_hint = -1, last_freed = -1, lastW = 0;
   int stalls = 0;
+  static const bool dbg = getenv("PRISM_DEBUG_COMMIT") != nullptr;
+  int nb = 0, ns = 0, na_ = 0, nh = 0;
+  auto t0 = std::chrono::steady_clock::now();
+  struct Rep {
+    bool on;
+    int *nb, *ns, *na, *nh;
+    std::chrono::steady_clock::time_point t0;
+    int *iters;
+    ~Rep() {
+      if (!on) return;
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      if (ms > 2.0) fprintf(stderr, "[commit] %.2f ms iters %d builds %d slots %d arena %d hash %d\n", ms, *iters, *nb, *ns, *na, *nh);
+    }
+  };
+  int iters = 0;
+  Rep rep{dbg, &nb, &ns, &na_, &nh, t0, &iters};
   for (int iter = 0; iter < 1000000; iter++) {
+    iters = iter + 1;
     prof_begin(t);
     k_commit<<<1, 32, COMMIT_SMEM, t->st>>>(t->d, a);
     CK(cudaGetLastError());
@@ -605,18 +623,22 @@ int run_commit(prism_tree *t, CommitArgs a) {
         last_hint = c.need_hint;
         last_freed = c.resume_freed;
         lastW = W;
+        nb++;
         rc = build_list(t, W);
         break;
       }
       case ST_NEED_SLOTS:
+        ns++;
         rc = grow_slots(t, (int64_t)c.hw + 2 + MAX_ANCH);
         break;
       case ST_NEED_ARENA: {
+        na_++;
         const int64_t n = std::max<int64_t>(a.mode == 1 ? (int64_t)MAX_PATH : a.op_n, c.need_hint);
         rc = compact_arena(t, n);
         break;
       }
       case ST_NEED_HASH:
+        nh++;
         rc = rehash(t, 2 + MAX_ANCH);
         break;
       default:

@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cub/cub.cuh>
 #include <string>
@@ -565,7 +567,7 @@ struct prism_qas {
   int64_t name##_cap = 0;
   QAS_BUFFERS(QBUF)
 #undef QBUF
-  int64_t small_max_p = 4096;  // one-launch rounds up to this many pending (<= QS_MAXP)
+  int64_t small_max_p = qsmall::QS_MAXP;  // one-launch rounds up to this many pending
   int64_t small_grid = 0;      // CTAs of a one-launch round (0: from small_per_cta)
   int64_t small_per_cta = 24;  // pending requests per CTA when sizing the grid (4096 -> every SM)
   int32_t small_coresident = 0;
@@ -1573,6 +1575,8 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
     q->graph_replays++;
     q->launches += hit->kernels;
   } else if (key == q->gkey_seen) {  // second wave of this shape: capture it (LRU slot)
+    static const bool dbg = getenv("PRISM_DEBUG_COMMIT") != nullptr;
+    if (dbg) fprintf(stderr, "[wave] capture P=%lld B=%lld\n", (long long)P, (long long)B);
     prism_qas::GEnt *slot = &q->gcache[0];
     for (auto &e : q->gcache)
       if (!e.exec || e.last < slot->last) slot = &e;

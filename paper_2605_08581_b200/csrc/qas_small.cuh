@@ -23,7 +23,7 @@
 namespace qsmall {
 
 constexpr int QS_TPB = 1024;
-constexpr int QS_MAXP = 4096;  // bitonic sort capacity (shared memory)
+constexpr int QS_MAXP = 8192;  // pending requests of a one-launch round (shared-memory lists / sorts)
 constexpr int QS_MAXK = 16;   // alignment by a 16-lane group (two requests per warp)
 constexpr int QS_MAXW = 64;   // alignment by one warp (two entries per lane); longer skeletons: a whole block
 constexpr int QS_SKCAP = 64;  // skeleton entries per request provisioned (aligned, pair table)
@@ -539,8 +539,9 @@ __device__ inline void qs_cold_lane(const QsArgs &A, const QsCfg &c, int64_t P, 
       __syncthreads();
     }
     // compact the taken keys to the front (each thread reads before any write)
-    QKey kk[4];
-    int32_t vv[4], fl[4];
+    constexpr int PT = QS_MAXP / QS_TPB;  // leftovers per thread
+    QKey kk[PT];
+    int32_t vv[PT], fl[PT];
     int own = 0;
     for (int q = tid; q < m; q += nt, own++) {
       kk[own] = sk[q];

@@ -24,6 +24,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <queue>
@@ -280,6 +283,7 @@ struct prism_serve {
   double busy_until = 0.0;
   bool done = false;
   std::vector<double> w_launch, w_duration;
+  std::vector<float> w_host_us;  // host wall time of each wave (diagnostics)
   std::vector<int64_t> w_uncached, w_cached, w_off{0};
   // in-flight waves: (completion, wave index), earliest first
   std::priority_queue<std::pair<double, int64_t>, std::vector<std::pair<double, int64_t>>,
@@ -567,7 +571,17 @@ int prism_serve_run(prism_serve *s, int64_t max_waves, int64_t *waves_run, int32
     }
     if (s->Pn == 0 || t + 1e-12 < s->busy_until) continue;  // engine.py:180-181
     int64_t adm = 0;
+    const auto h0 = std::chrono::steady_clock::now();
     if ((rc = sv_wave(s, &adm))) return rc;
+    {
+      static const bool dbg = getenv("PRISM_DEBUG_COMMIT") != nullptr;
+      const float us = std::chrono::duration<float, std::micro>(std::chrono::steady_clock::now() - h0).count();
+      if (dbg && us > 3000) fprintf(stderr, "[serve] wave %zu: %.0f us (P=%lld, in flight %lld)\n",
+                                    s->w_launch.size(), us, (long long)s->Pn, (long long)s->n_inflight);
+    }
+    if (adm > 0)
+      s->w_host_us.push_back(
+          std::chrono::duration<float, std::micro>(std::chrono::steady_clock::now() - h0).count());
     ran++;
   }
   if (waves_run) *waves_run = ran;
@@ -619,6 +633,12 @@ int prism_serve_waves(prism_serve *s, double *launch, double *duration, int64_t 
     for (size_t w = 0; w <= W; w++) member_off[w] = s->w_off[w];
   if (members && s->nlog)
     SCK(cudaMemcpy(members, s->log_idx, sizeof(int32_t) * (size_t)s->nlog, cudaMemcpyDeviceToHost));
+  return PRISM_OK;
+}
+
+// host wall time (us) of each admitting wave, in wave order (diagnostics)
+int prism_serve_wave_times(prism_serve *s, float *out_us) {
+  for (size_t w = 0; w < s->w_host_us.size(); w++) out_us[w] = s->w_host_us[w];
   return PRISM_OK;
 }
 

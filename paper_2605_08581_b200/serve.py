@@ -177,6 +177,9 @@ class DeviceServingLoop:
         self.config = config
         self.trace = trace = trace.sorted()
         cache, sched = config.cache, config.scheduler
+        # sized up front (no growth / compaction mid-run): slots <= resident tokens, arena 32x the capacity
+        initial_slots = initial_slots or max(1 << 12, min(cache.capacity_tokens + 2, 1 << 22))
+        initial_arena_tokens = initial_arena_tokens or max(1 << 20, 32 * cache.capacity_tokens)
         self.t = self.L.prism_tree_create(cache.capacity_tokens, POLICY_CODE[policy_of(cache.policy)],
                                           cache.protect_budget, initial_slots, initial_arena_tokens, device)
         if not self.t:

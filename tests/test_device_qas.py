@@ -38,14 +38,16 @@ def test_golden_rounds(small):
             raise AssertionError(f"round {i}: {e}") from e
 
 
-def test_mixed_round_sizes_one_scheduler():
-    """Small (one-CTA) and large (multi-kernel) rounds interleaved on one
+@pytest.mark.parametrize("small", [4096, True])
+def test_mixed_round_sizes_one_scheduler(small):
+    """Small (one-launch) and large (multi-kernel) rounds interleaved on one
     scheduler: the per-round counter reset (touched lists / full resets) must
-    never leak state between rounds."""
+    never leak state between rounds.  small=True: one-launch rounds up to 8192
+    pending (only P=8000+ ... none here above it: every round one launch)."""
     from paper_2605_08581_b200.qas import DeviceScheduler
 
     ds = DeviceScheduler()
-    ds.set_small(4096)
+    ds.set_small(small)
     rng = np.random.default_rng(31)
     for P in (100, 5000, 200, 300, 8000, 50, 4096, 1):
         nseg = int(rng.integers(20, 3000))
