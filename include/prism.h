@@ -317,7 +317,9 @@ int prism_wave_step_host(prism_tree *t, prism_qas *q, int64_t P, const int64_t *
  * for the newly resident tokens (admission order = each admitted member's
  * uncached tokens; src = their KV in that order, DEVICE, or NULL) and the
  * victims' rows back on the free stack (dst = their KV in eviction order,
- * DEVICE, or NULL); out[2] = {new tokens, freed tokens}.  prism_kv_gather: per
+ * DEVICE, or NULL), all on the tree's stream with the sizes read on the device;
+ * out (may be NULL: no host wait) = {new tokens, freed tokens}, and the pool /
+ * log checks.  prism_kv_gather (asynchronous on the tree's stream): per
  * leaf slot (DEVICE) the pool row of every path position into table[n, max_len]
  * (the request's req_to_token), lens[n] = path lengths, and (out != NULL) the
  * KV rows themselves into out[n, max_len, bytes_per_token] -- all DEVICE. */

@@ -27,6 +27,7 @@ _SIGS = {
     "prism_release": (C.c_int, [_p, _i64, _p, _p]),
     "prism_release_device": (C.c_int, [_p, _i64, _p, _p, _p]),
     "prism_pin_device": (C.c_int, [_p, _i64, _p, _p]),
+    "prism_tree_stream": (_p, [_p]),
     "prism_evict": (C.c_int, [_p, _i64, _p]),
     "prism_set_protection": (C.c_int, [_p, _i64, _p, _p, _p, _p]),
     "prism_note_active": (C.c_int, [_p, _i64, _p]),

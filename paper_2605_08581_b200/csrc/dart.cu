@@ -149,7 +149,6 @@ struct prism_tree {
     KvDev k{};
     int32_t *kvx_spare = nullptr;
     int64_t kvx_cap = 0;
-    int64_t arena_mark = 0, vlog_mark = 0;
     int64_t *voff = nullptr, *total = nullptr;
     int64_t voff_cap = 0;
   } *kv = nullptr;
@@ -503,7 +502,8 @@ int kv_sync(prism_tree *t, const void *src, void *dst, int64_t *out);
 int compact_arena(prism_tree *t, int64_t need) {
   join_aux(t);  // the auxiliary stream must not touch arrays being replaced
   if (t->kv) {  // settle the payload first: the victims' rows and the new spans move with the arena
-    int rc = kv_sync(t, nullptr, nullptr, nullptr);
+    int64_t o2[2];
+    int rc = kv_sync(t, nullptr, nullptr, o2);
     if (rc) return rc;
   }
   const int32_t hw = t->hctrl->hw;
@@ -550,7 +550,9 @@ int compact_arena(prism_tree *t, int64_t need) {
       K->kvx_spare = nullptr;
       K->kvx_cap = cap;
     }
-    K->arena_mark = live;
+    const int64_t mark = live;  // (every span synced above: the new arena starts settled)
+    CK(cudaMemcpyAsync(K->k.ctl, &mark, sizeof(int64_t), cudaMemcpyHostToDevice, t->st));
+    CK(cudaStreamSynchronize(t->st));
   }
   k_compact_copy<<<blocks_for((int64_t)hw * 32), TPB, 0, t->st>>>(t->d, hw, off, na);
   CK(cudaGetLastError());
@@ -992,7 +994,7 @@ void prism_tree_destroy(prism_tree *t) {
   cudaStreamSynchronize(t->st);
   if (t->kv) {
     void *kb[] = {t->kv->k.pool, t->kv->k.kvx, t->kv->k.stack, t->kv->k.top, t->kv->k.moved, t->kv->kvx_spare,
-                  t->kv->voff, t->kv->total};
+                  t->kv->voff, t->kv->total, t->kv->k.ctl};
     for (void *p : kb)
       if (p) cudaFree(p);
     delete t->kv;
@@ -1830,41 +1832,30 @@ __global__ void k_kv_init_stack(int32_t *stack, int64_t rows) {
 // KV copied out in eviction order, or NULL).  out[2] = {new tokens, freed tokens}.
 int kv_sync(prism_tree *t, const void *src, void *dst, int64_t *out) {
   auto *K = t->kv;
-  int rc = pull_ctrl(t);
-  if (rc) return rc;
-  const Ctrl &C = *t->hctrl;
-  const int64_t n_new = C.arena_top - K->arena_mark, nrec = C.vlog_count - K->vlog_mark;
-  if (n_new < 0) return fail(PRISM_FATAL, "KV payload: the arena shrank outside a compaction");
-  if (nrec > t->d.vcap) return fail(PRISM_INVALID, "KV payload: more victims since the last sync than the log keeps");
-  int64_t top = 0;
-  CK(cudaMemcpyAsync(&top, K->k.top, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
-  CK(cudaStreamSynchronize(t->st));
-  if (n_new > top) return fail(PRISM_CAPACITY, "KV pool exhausted (rows must cover capacity + the tokens of one sync)");
-  if (n_new > 0) {
-    k_kv_alloc<<<(unsigned)std::min<int64_t>((n_new * 32 + TPB - 1) / TPB, 65535), TPB, 0, t->st>>>(
-        K->k, K->arena_mark, n_new, (const uint8_t *)src);
-    k_kv_commit_top<<<1, 1, 0, t->st>>>(K->k, -n_new, src ? n_new * K->k.bpt : 0);
+  // all on the tree's stream, sizes read on the device (no host round trip)
+  const int64_t cap = t->d.vcap + 1;  // victim records of one sync at most (more: the log lost some)
+  if (cap > K->voff_cap) {
+    if (K->voff) CK(cudaFree(K->voff));
+    K->voff_cap = next_pow2(cap);
+    CK(dalloc(&K->voff, K->voff_cap));
   }
-  int64_t freed = 0;
-  if (nrec > 0) {
-    if (nrec + 1 > K->voff_cap) {
-      if (K->voff) CK(cudaFree(K->voff));
-      K->voff_cap = next_pow2(nrec + 1);
-      CK(dalloc(&K->voff, K->voff_cap));
-    }
-    k_kv_voff<<<1, 1024, 0, t->st>>>(t->d.vlog, t->d.vcap, K->vlog_mark, nrec, K->voff, K->k, K->total, 0);
-    k_kv_free<<<(unsigned)std::min<int64_t>((nrec * 32 + TPB - 1) / TPB, 65535), TPB, 0, t->st>>>(
-        K->k, t->d.vlog, t->d.vcap, K->vlog_mark, nrec, K->voff, (uint8_t *)dst);
-    k_kv_free_top<<<1, 1, 0, t->st>>>(K->k, K->total, dst ? 1 : 0);
-    CK(cudaMemcpyAsync(&freed, K->total, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
-  }
+  int sms = t->sms;
+  if (sms <= 0) CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev));
+  const unsigned grid = (unsigned)(8 * sms);
+  k_kv_prep<<<1, 1, 0, t->st>>>(K->k, t->d.ctrl, t->d.vcap);
+  k_kv_alloc<<<grid, TPB, 0, t->st>>>(K->k, (const uint8_t *)src);
+  k_kv_voff<<<1, 1024, 0, t->st>>>(t->d.vlog, t->d.vcap, K->voff, K->k);
+  k_kv_free<<<grid, TPB, 0, t->st>>>(K->k, t->d.vlog, t->d.vcap, K->voff, (uint8_t *)dst);
+  k_kv_fin<<<1, 1, 0, t->st>>>(K->k, t->d.ctrl, src ? 1 : 0, dst ? 1 : 0);
   CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(t->st));
-  K->arena_mark = C.arena_top;
-  K->vlog_mark = C.vlog_count;
-  if (out) {
-    out[0] = n_new;
-    out[1] = freed;
+  if (out) {  // the counts (and the error check) want the host
+    int64_t c[8];
+    CK(cudaMemcpyAsync(c, K->k.ctl, sizeof(c), cudaMemcpyDeviceToHost, t->st));
+    CK(cudaStreamSynchronize(t->st));
+    if (c[5] == 1) return fail(PRISM_CAPACITY, "KV pool exhausted (rows must cover capacity + the tokens of one sync)");
+    if (c[5] == 2) return fail(PRISM_INVALID, "KV payload: more victims since the last sync than the log keeps");
+    out[0] = c[6];
+    out[1] = c[7];
   }
   return PRISM_OK;
 }
@@ -1894,12 +1885,13 @@ int prism_kv_enable(prism_tree *t, int64_t rows, int64_t bytes_per_token) {
   CK(dalloc(&K->k.top, 1));
   CK(dalloc(&K->k.moved, 4));
   CK(dalloc(&K->total, 1));
+  CK(dalloc(&K->k.ctl, 8));
   k_kv_init_stack<<<blocks_for(rows), TPB, 0, t->st>>>(K->k.stack, rows);
   CK(cudaMemcpyAsync(K->k.top, &rows, sizeof(int64_t), cudaMemcpyHostToDevice, t->st));
   CK(cudaMemsetAsync(K->k.moved, 0, 4 * sizeof(int64_t), t->st));
+  const int64_t marks[8] = {t->hctrl->arena_top, t->hctrl->vlog_count, 0, 0, 0, 0, 0, 0};
+  CK(cudaMemcpyAsync(K->k.ctl, marks, sizeof(marks), cudaMemcpyHostToDevice, t->st));
   CK(cudaStreamSynchronize(t->st));
-  K->arena_mark = t->hctrl->arena_top;
-  K->vlog_mark = t->hctrl->vlog_count;
   t->kv = K;
   return PRISM_OK;
 }
@@ -1919,8 +1911,7 @@ int prism_kv_gather(prism_tree *t, int64_t n, const int32_t *leaf_slots, int64_t
   if (n <= 0) return PRISM_OK;
   k_kv_gather<<<(unsigned)((n * 32 + TPB - 1) / TPB), TPB, 0, t->st>>>(t->d, t->kv->k, n, leaf_slots, max_len, table,
                                                                         (uint8_t *)out, lens);
-  CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(t->st));
+  CK(cudaGetLastError());  // (asynchronous on the tree's stream)
   return PRISM_OK;
 }
 

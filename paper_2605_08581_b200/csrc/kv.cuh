@@ -34,9 +34,38 @@ struct KvDev {
   int32_t *stack;      // free rows, [0, top)
   int64_t *top;        // device scalar: free rows
   int64_t *moved;      // [0] rows allocated, [1] rows freed, [2] bytes copied in, [3] bytes copied out
+  int64_t *ctl;        // [0] arena mark, [1] victim-log mark, [2] new tokens, [3] victim records,
+                       // [4] freed tokens, [5] error (pool exhausted / victims lost), [6] last new, [7] last freed
   int64_t bpt;         // bytes per token (multiple of 16)
   int64_t rows;
 };
+
+// one sync's sizes from the tree's control block (no host round trip): new
+// arena tokens since the arena mark, victim records since the log mark
+__global__ void k_kv_prep(KvDev K, const Ctrl *C, int64_t vcap) {
+  const int64_t n_new = C->arena_top - K.ctl[0], nrec = C->vlog_count - K.ctl[1];
+  const bool bad = n_new < 0 || n_new > *K.top || nrec > vcap;
+  K.ctl[2] = bad ? 0 : n_new;
+  K.ctl[3] = bad ? 0 : nrec;
+  K.ctl[4] = 0;
+  if (bad) K.ctl[5] = n_new > *K.top ? 1 : 2;
+}
+
+// the marks advance, the free-row count and the traffic counters update
+__global__ void k_kv_fin(KvDev K, const Ctrl *C, int32_t copy_in, int32_t copy_out) {
+  const int64_t n_new = K.ctl[2], freed = K.ctl[4];
+  *K.top += freed - n_new;
+  K.moved[0] += n_new;
+  K.moved[1] += freed;
+  if (copy_in) K.moved[2] += n_new * K.bpt;
+  if (copy_out) K.moved[3] += freed * K.bpt;
+  K.ctl[6] = n_new;
+  K.ctl[7] = freed;
+  if (!K.ctl[5]) {
+    K.ctl[0] = C->arena_top;
+    K.ctl[1] = C->vlog_count;
+  }
+}
 
 // 16-B vector copy of one row
 __device__ __forceinline__ void kv_row_copy(uint8_t *__restrict__ dst, const uint8_t *__restrict__ src, int64_t bpt,
@@ -48,50 +77,70 @@ __device__ __forceinline__ void kv_row_copy(uint8_t *__restrict__ dst, const uin
 
 // newly resident arena tokens [a0, a0 + n): pop rows (stack top - 1 - i) in
 // arena order, optionally copy the payload in (src row i = arena token a0 + i)
-__global__ void k_kv_alloc(KvDev K, int64_t a0, int64_t n, const uint8_t *__restrict__ src) {
-  const int64_t top = *K.top;  // (read by every thread before the last block updates it: see k_kv_commit_top)
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  for (int64_t i = w; i < n; i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int32_t row = K.stack[top - 1 - i];
-    if (lane == 0) K.kvx[a0 + i] = row;
-    if (src) kv_row_copy(K.pool + (int64_t)row * K.bpt, src + i * K.bpt, K.bpt, lane, 32);  // (warp per row)
+__global__ void k_kv_alloc(KvDev K, const uint8_t *__restrict__ src) {
+  const int64_t top = *K.top, a0 = K.ctl[0], n = K.ctl[2];  // (k_kv_fin moves top after every reader)
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = t0; i < n; i += gs) K.kvx[a0 + i] = K.stack[top - 1 - i];
+  if (!src) return;
+  // copy-in: 16-B vectors across all the new rows (src row i -> pool row of token a0 + i),
+  // UNR independent vectors in flight per thread
+  constexpr int UNR = 4;
+  const int64_t vpr = K.bpt / 16, nv = n * vpr;
+  const int4 *s4 = reinterpret_cast<const int4 *>(src);
+  for (int64_t x0 = t0; x0 < nv; x0 += UNR * gs) {
+    int4 val[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; u++)
+      if (x0 + u * gs < nv) val[u] = __ldcs(s4 + x0 + u * gs);  // (streamed once)
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+      const int64_t x = x0 + u * gs;
+      if (x >= nv) break;
+      const int64_t i = x / vpr, v = x - i * vpr;
+      reinterpret_cast<int4 *>(K.pool + (int64_t)K.stack[top - 1 - i] * K.bpt)[v] = val[u];
+    }
   }
 }
 
-__global__ void k_kv_commit_top(KvDev K, int64_t delta, int64_t bytes_in) {
-  *K.top += delta;
-  if (delta < 0) K.moved[0] += -delta;
-  K.moved[2] += bytes_in;
-}
 
 // victim records [v0, v1) of the log ring: their pool rows, in eviction order,
 // pushed on the stack (record r's rows at top + voff[r] ..), optionally copied
 // out (dst row = voff[r] + i).  voff: exclusive prefix of the records' lengths.
-__global__ void k_kv_free(KvDev K, const VRec *__restrict__ vlog, int64_t vcap, int64_t v0, int64_t nrec,
-                          const int64_t *__restrict__ voff, uint8_t *__restrict__ dst) {
-  const int64_t top = *K.top;
+__global__ void k_kv_free(KvDev K, const VRec *__restrict__ vlog, int64_t vcap, const int64_t *__restrict__ voff,
+                          uint8_t *__restrict__ dst) {
+  const int64_t top = *K.top - K.ctl[2];  // (the rows k_kv_alloc popped are gone; k_kv_fin moves top)
+  const int64_t v0 = K.ctl[1], nrec = K.ctl[3];
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   for (int64_t r = w; r < nrec; r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const VRec rec = vlog[(v0 + r) % vcap];
     const int64_t o = voff[r];
     for (int32_t i = lane; i < rec.elen; i += 32) K.stack[top + o + i] = K.kvx[rec.eoff + i];
-    if (dst) {  // the record's rows back to back, 16-B vectors across the whole record
+    if (dst) {  // the record's rows back to back, 16-B vectors across the whole record, 4 in flight per lane
       const int64_t vpr = K.bpt / 16, nv = (int64_t)rec.elen * vpr;
       int4 *d = reinterpret_cast<int4 *>(dst + o * K.bpt);
-      for (int64_t x = lane; x < nv; x += 32) {
-        const int64_t i = x / vpr, v = x - i * vpr;
-        d[x] = reinterpret_cast<const int4 *>(K.pool + (int64_t)K.kvx[rec.eoff + i] * K.bpt)[v];
+      for (int64_t x0 = lane; x0 < nv; x0 += 4 * 32) {
+        int4 val[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int64_t x = x0 + u * 32;
+          if (x < nv) {
+            const int64_t i = x / vpr, v = x - i * vpr;
+            val[u] = reinterpret_cast<const int4 *>(K.pool + (int64_t)K.kvx[rec.eoff + i] * K.bpt)[v];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          if (x0 + u * 32 < nv) __stcs(d + x0 + u * 32, val[u]);  // (the offload buffer: streamed)
       }
     }
   }
 }
 
 // exclusive prefix of the victim records' lengths (one CTA) + the total
-__global__ void __launch_bounds__(1024) k_kv_voff(const VRec *__restrict__ vlog, int64_t vcap, int64_t v0,
-                                                  int64_t nrec, int64_t *voff, KvDev K, int64_t *total_out,
-                                                  int64_t copy_bytes) {
+__global__ void __launch_bounds__(1024) k_kv_voff(const VRec *__restrict__ vlog, int64_t vcap, int64_t *voff,
+                                                  KvDev K) {
+  const int64_t v0 = K.ctl[1], nrec = K.ctl[3];
   __shared__ int64_t s_w[32];
   __shared__ int64_t s_carry;
   if (threadIdx.x == 0) s_carry = 0;
@@ -122,17 +171,9 @@ __global__ void __launch_bounds__(1024) k_kv_voff(const VRec *__restrict__ vlog,
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    *total_out = s_carry;
+    K.ctl[4] = s_carry;
     voff[nrec] = s_carry;
-    (void)K;
-    (void)copy_bytes;
   }
-}
-
-__global__ void k_kv_free_top(KvDev K, const int64_t *total, int64_t copy_out) {
-  *K.top += *total;
-  K.moved[1] += *total;
-  if (copy_out) K.moved[3] += *total * K.bpt;
 }
 
 // arena compaction: the shadow rows follow their spans (same new offsets as k_compact_copy)

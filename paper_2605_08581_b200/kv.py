@@ -40,19 +40,22 @@ class KvPool:
         self.rows, self.bpt = int(rows), int(bytes_per_token)
         check(self.L.prism_kv_enable(self.h, self.rows, self.bpt))
 
-    def sync(self, src: torch.Tensor | None = None, dst: torch.Tensor | None = None) -> tuple[int, int]:
+    def sync(self, src: torch.Tensor | None = None, dst: torch.Tensor | None = None,
+             counts: bool = True) -> tuple[int, int] | None:
         """(new resident tokens, freed tokens) since the last sync.  ``src``:
         uint8 [>= new, bytes_per_token] of the new tokens' KV (admission
-        order); ``dst``: uint8 [>= freed, bytes_per_token] for the victims' KV."""
+        order); ``dst``: uint8 [>= freed, bytes_per_token] for the victims' KV.
+        ``counts=False``: no host wait (the work stays queued on the tree's stream)."""
         out = np.zeros(2, np.int64)
         for t in (src, dst):  # (produced on torch's stream; the pool works on the tree's)
             if t is not None:
                 torch.cuda.current_stream(t.device).synchronize()
         check(self.L.prism_kv_sync(self.h, src.data_ptr() if src is not None else None,
-                                   dst.data_ptr() if dst is not None else None, out.ctypes.data))
-        return int(out[0]), int(out[1])
+                                   dst.data_ptr() if dst is not None else None,
+                                   out.ctypes.data if counts else None))
+        return (int(out[0]), int(out[1])) if counts else None
 
-    def gather(self, leaf_slots: torch.Tensor, n: int, max_len: int, payload: bool = False):
+    def gather(self, leaf_slots: torch.Tensor, n: int, max_len: int, payload: bool = False, wait: bool = True):
         """(table int32 [n, max_len], lens int64 [n], kv uint8 [n, max_len, bpt] or None)."""
         dev = leaf_slots.device
         table = torch.full((max(n, 1), max_len), -1, dtype=torch.int32, device=dev)
@@ -61,6 +64,10 @@ class KvPool:
         torch.cuda.current_stream(dev).synchronize()  # (the fills above and leaf_slots: torch's stream)
         check(self.L.prism_kv_gather(self.h, n, leaf_slots.data_ptr(), max_len, table.data_ptr(),
                                      out.data_ptr() if out is not None else None, lens.data_ptr()))
+        if wait:  # (the gather runs on the tree's stream)
+            self.L.prism_tree_stream.restype = C.c_void_p
+            self.L.prism_tree_stream.argtypes = [_p]
+            torch.cuda.ExternalStream(self.L.prism_tree_stream(self.h), device=dev).synchronize()
         return table[:n], lens[:n], (out[:n] if out is not None else None)
 
     def stats(self) -> dict:
