@@ -743,9 +743,9 @@ int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *lea
   prof_begin(t);
   k_wc_begin<<<(int)std::min<int64_t>(std::max<int64_t>((t->wx_lt + 255) / 256, 1), 4 * sms), 256, 0, st>>>(
       t->d, wc, abort, X, t->wx_lt);
-  k_wp_plan<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
-  k_wp_levels<<<blocks_for(B * WP_PL), TPB, 0, st>>>(W, X);
-  k_wp_hits<<<blocks_for(B), TPB, 0, st>>>(t->d, W, X, wc);
+  k_wp_plan<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, W, X, wc);  // (warp per member)
+  k_wp_levels<<<blocks_for(B * WP_PL), TPB, 0, st>>>(W, X, wc);
+  k_wp_hits<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, W, X, wc);  // (warp per member)
   k_wp_scan3<<<1, 1024, 0, st>>>(t->d, B, X, wc, t->list_slack_tokens, force_full);  // + the plan verdict
   CK(cudaGetLastError());
   t->launches[PH_COMMIT] += 5;

@@ -1267,7 +1267,10 @@ __global__ void __launch_bounds__(1024) q_members_scan(int64_t nh, int64_t nc, c
                                                        int64_t anc_cap, int32_t *err, int32_t *abort) {
   const int64_t B = nh + nc;
   if (qcounts[3]) {  // the one-launch round overflowed its buffers: no dispatch order (uniform)
-    if (threadIdx.x == 0) *abort = 1;
+    if (threadIdx.x == 0) {
+      *abort = 1;
+      tot[0] = tot[1] = 0;  // (the host sizes the serialization buffers from these)
+    }
     return;
   }
   __shared__ int s_err;

@@ -132,10 +132,13 @@ __device__ inline int32_t wp_table(const WaveTmp &X, uint64_t key, int32_t j, bo
   }
 }
 
-// W1: per-member plan checks + skeleton-prefix ownership table
+// W1: per-member plan checks, one warp per member (lanes walk the pre-wave
+// chain in parallel): shape, pre-match flags, chain nodes aligned 1:1 with the
+// first pieces, and the chain marks (victim guard; first member per node)
 __global__ void k_wp_plan(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= W.B || wc->stop) return;
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = lane_id();
+  if (j >= W.B || wc->stop) return;  // (warp-uniform)
   const uint32_t epoch = wc->epoch;
   const int64_t m = W.members[j];
   const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
@@ -150,15 +153,18 @@ __global__ void k_wp_plan(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   // pre-wave chain nodes must coincide with the first d pieces
   if (!flag) {
     if (d > P) flag |= WPF_ALIGN;
-    for (int p = 0; p < d && !flag; p++) {
+    bool bad = false;
+    for (int p = lane; p < d && !(flag & WPF_ALIGN); p += 32) {
       const int32_t c = W.pm_chain[j * PM_MAX + p];
-      if ((int64_t)T.dend[c] != wp_end(W, p, k, n)) flag |= WPF_ALIGN;
+      if ((int64_t)T.dend[c] != wp_end(W, p, k, n)) bad = true;
       T.wchild[c] = epoch;  // "on some member's pre-wave chain" (victim guard)
       atomicMax((unsigned long long *)&T.wchm[c],
                 ((unsigned long long)epoch << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)j));  // first such member
     }
+    if (__any_sync(0xffffffffu, bad)) flag |= WPF_ALIGN;
     if (!flag && (d > 0 ? wp_end(W, d - 1, k, n) : 0) != hit_pre) flag |= WPF_ALIGN;
   }
+  if (lane) return;
   if (flag) {
     atomicOr(X.flags, flag);
     return;
@@ -171,7 +177,8 @@ __global__ void k_wp_plan(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
 // segments; the first owner of each prefix by atomicMin.  Level-major (thread
 // = level L of member j, consecutive members in a warp): every member shares
 // the low levels, so each warp inserts one key per distinct prefix.
-__global__ void k_wp_levels(WaveIn W, WaveTmp X) {
+__global__ void k_wp_levels(WaveIn W, WaveTmp X, const WaveCtl *wc) {
+  if (wc->stop) return;  // (an aborted wave: no dispatch order to read)
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t j = t % W.B;
   const int lane = threadIdx.x & 31;
@@ -210,60 +217,89 @@ __global__ void k_wp_levels(WaveIn W, WaveTmp X) {
   }
 }
 
-// W2: intra-wave share, hit, new pieces, demand
+// W2: intra-wave share, hit, new pieces, demand -- one warp per member: lane
+// q holds skeleton levels q and q + 32; every lane runs the prefix-hash chain
+// (ALU + shuffles), then each looks its own levels up in the first-owner table
+// at once (the lookups were a dependent sequence per member)
 __global__ void k_wp_hits(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= W.B || wc->stop) return;  // (an aborted wave never ran the plan)
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = lane_id();
+  if (j >= W.B || wc->stop) return;  // (warp-uniform; an aborted wave never ran the plan)
   if (*X.flags) return;
   const int64_t m = W.members[j];
   const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
-  if (k + 2 > WP_MAXP) {  // (the plan flags these shapes; own_at below holds WP_MAXP levels)
-    atomicOr(X.flags, WPF_SHAPE);
+  if (k > 63) {  // (levels 0..k are held two per lane: <= 63; longer skeletons take the ordered commit)
+    if (lane == 0) atomicOr(X.flags, WPF_SHAPE);
     return;
   }
   const int32_t *s = W.aligned + W.sk_off[m];
   const int64_t n = W.poff[j + 1] - W.poff[j];
   const int P = X.npieces[j];
   const int lmin = W.sys > 0 ? 0 : 1;
-  uint64_t h = 0x51ED270B27ull;
-  int lstar = -1;
-  int32_t own_at[WP_MAXP];
-  for (int L = 0; L <= k; L++) {
-    if (L > 0) h = wp_hash_next(h, s[L - 1]);
-    if (L < lmin) continue;
-    const int32_t o = wp_table(X, wp_level_key(L, h), (int32_t)j, false);
-    if (o < 0 || o >= j) break;
-    own_at[L] = o;
-    lstar = L;
+  // segments q = lane, lane + 32 in registers; level L hashes segments [0, L)
+  const int32_t s0 = lane < k ? s[lane] : 0, s1 = lane + 32 < k ? s[lane + 32] : 0;
+  uint64_t h = 0x51ED270B27ull, hL0 = 0, hL1 = 0;
+  if (lane == 0) hL0 = h;
+  for (int q = 0; q < k; q++) {
+    const int32_t sq = __shfl_sync(0xffffffffu, q < 32 ? s0 : s1, q & 31);
+    h = wp_hash_next(h, sq);
+    if (q + 1 == lane) hL0 = h;
+    if (q + 1 == lane + 32) hL1 = h;
   }
+  // this lane's levels: ok = owned by an earlier member
+  int32_t o0 = -1, o1 = -1;
+  bool ok0 = true, ok1 = true;  // (levels below lmin or above k do not stop the run)
+  if (lane <= k && lane >= lmin) {
+    o0 = wp_table(X, wp_level_key(lane, hL0), (int32_t)j, false);
+    ok0 = o0 >= 0 && o0 < j;
+  }
+  if (lane + 32 <= k && lane + 32 >= lmin) {
+    o1 = wp_table(X, wp_level_key(lane + 32, hL1), (int32_t)j, false);
+    ok1 = o1 >= 0 && o1 < j;
+  }
+  // lstar: the last level of the unbroken run of owned levels from lmin (-1: none)
+  const unsigned bad0 = __ballot_sync(0xffffffffu, !ok0), bad1 = __ballot_sync(0xffffffffu, !ok1);
+  const int first_bad = bad0 ? __ffs(bad0) - 1 : (bad1 ? 32 + __ffs(bad1) - 1 : k + 1);
+  const int lstar = (first_bad > k ? k : first_bad - 1) >= lmin ? (first_bad > k ? k : first_bad - 1) : -1;
+  auto own_at = [&](int L) {  // owner of level L (L <= lstar), from its lane
+    const int32_t v0 = __shfl_sync(0xffffffffu, o0, L & 31), v1 = __shfl_sync(0xffffffffu, o1, L & 31);
+    return L < 32 ? v0 : v1;
+  };
   int64_t lcpw = 0;
   if (lstar >= 0) {
     // verify the owner really shares the skeleton prefix (hash collisions)
-    const int32_t o = own_at[lstar];
+    const int32_t o = own_at(lstar);
     const int64_t mo = W.members[o];
     const int ko = (int)(W.sk_off[mo + 1] - W.sk_off[mo]);
     const int32_t *so = W.aligned + W.sk_off[mo];
-    bool same = ko >= lstar;
-    for (int q = 0; same && q < lstar; q++) same = so[q] == s[q];
-    if (!same) {
-      atomicOr(X.flags, WPF_COLLIDE);
+    bool diff = false;
+    if (ko < lstar) diff = true;
+    for (int q = lane; q < lstar && ko >= lstar; q += 32) diff |= so[q] != s[q];
+    if (__any_sync(0xffffffffu, diff)) {
+      if (lane == 0) atomicOr(X.flags, WPF_COLLIDE);
       return;
     }
     lcpw = W.sys + (int64_t)lstar * W.chunk;
   }
   const int64_t hit_pre = X.pre[j];
   const int64_t hit = hit_pre > lcpw ? hit_pre : lcpw;
-  // first new piece and owners of the shared (intra-wave) pieces
+  // first new piece (warp-uniform) and owners of the shared (intra-wave) pieces
   int p0 = P;
-  for (int p = 0; p < P; p++) {
-    const int64_t e = wp_end(W, p, k, n);
-    if (e > hit) {
+  for (int p = 0; p < P; p++)
+    if (wp_end(W, p, k, n) > hit) {
       p0 = p;
       break;
     }
-    const int L = wp_level_of_piece(W, p);
-    X.owner[j * WP_MAXP + p] = (e > hit_pre && L <= lstar) ? own_at[L] : -1;
+  for (int pb = 0; pb < p0; pb += 32) {  // (all lanes join the shuffles)
+    const int p = pb + lane;
+    const int L = wp_level_of_piece(W, p < p0 ? p : 0);
+    const int32_t ow = own_at(L > 63 ? 63 : L);
+    if (p < p0) {
+      const int64_t e = wp_end(W, p, k, n);
+      X.owner[j * WP_MAXP + p] = (e > hit_pre && L <= lstar) ? ow : -1;
+    }
   }
+  if (lane) return;
   atomicAdd((unsigned long long *)&X.misc[3], (unsigned long long)n);   // inserted path tokens
   atomicAdd((unsigned long long *)&X.misc[4], (unsigned long long)p0);  // matched nodes
   X.hit[j] = (int32_t)hit;
@@ -534,6 +570,11 @@ __device__ inline void wc_plan_body(DT T, int64_t B, WaveTmp X, WaveCtl *wc, int
 
 __global__ void __launch_bounds__(1024) k_wp_scan3(DT T, int64_t B, WaveTmp X, WaveCtl *wc, int64_t slack,
                                                   int32_t force_full) {
+  // an aborted or flagged wave has no plan to scan: straight to the verdict (uniform)
+  if (wc->stop || *X.flags) {
+    if (threadIdx.x == 0) wc_plan_body(T, B, X, wc, slack, force_full);
+    return;
+  }
   // the three scans in one pass (one load round trip; B + 1 <= 5 * 1024 items
   // make a single tile at the bench's wave size)
   block_scan4<3, 5>(
