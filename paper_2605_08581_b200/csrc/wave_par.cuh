@@ -387,7 +387,19 @@ __global__ void k_wp_create(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   const int64_t hit = X.hit[j];
   const uint32_t *path = W.tok + W.poff[j];
   const int64_t ab = arena0 + X.arb[j];
-  for (int64_t i = lane; i < n - hit; i += 32) T.tok[ab + i] = path[hit + i];
+  {  // the tail's tokens into the arena: 4 independent loads in flight per lane
+    const int64_t nt = n - hit;
+    const uint32_t *src = path + hit;
+    uint32_t *dst = T.tok + ab;
+    for (int64_t i0 = lane; i0 < nt; i0 += 128) {
+      uint32_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) v[u] = i0 + 32 * u < nt ? src[i0 + 32 * u] : 0u;
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (i0 + 32 * u < nt) dst[i0 + 32 * u] = v[u];
+    }
+  }
   const int P = X.npieces[j], p0 = X.p0[j];
   const int64_t tick = clock0 + 2 * j + 2;
   for (int p = p0 + lane; p < P; p += 32) {
