@@ -1314,36 +1314,46 @@ __global__ void q_serialize(int64_t B, const int64_t *__restrict__ members, cons
   const int64_t m = members[w], b = off[m], k = off[m + 1] - b, sfx = suffix[m];
   uint32_t *p = tok + poff[w];
   for (int64_t j = lane; j < sys; j += 32) p[j] = (uint32_t)j;
-  for (int64_t j = lane; j < k * chunk; j += 32) {
-    const int64_t r = aligned[b + j / chunk];
-    p[sys + j] = (uint32_t)(SEGMENT_TOKEN_BASE + (uint64_t)r * chunk + (uint64_t)(j % chunk));
+  // segment tokens: 32 segment ids at a time in registers (one load per lane),
+  // then each segment's chunk tokens across the lanes (no per-token division)
+  for (int64_t q0 = 0; q0 < k; q0 += 32) {
+    const int64_t rl = q0 + lane < k ? aligned[b + q0 + lane] : 0;
+    const int64_t nq = k - q0 < 32 ? k - q0 : 32;
+    for (int64_t q = 0; q < nq; q++) {
+      const int64_t r = __shfl_sync(0xffffffffu, rl, (int)q);
+      uint32_t *dst = p + sys + (q0 + q) * chunk;
+      const uint64_t base = SEGMENT_TOKEN_BASE + (uint64_t)r * chunk;
+      for (int64_t jj = lane; jj < chunk; jj += 32) dst[jj] = (uint32_t)(base + jj);
+    }
   }
   const uint64_t sb = SUFFIX_TOKEN_BASE + (uint64_t)ids[m] * (uint64_t)sfx;  // (checked by q_members_len)
   for (int64_t j = lane; j < sfx; j += 32) p[sys + k * chunk + j] = (uint32_t)(sb + j);
-  if (lane == 0) {
-    int64_t q = aoffs[w];
-    if (sys > 0) {
-      a_off[q] = (int32_t)sys;
-      a_kind[q] = 0;  // SYSTEM
-      a_seg[q] = (int32_t)0x80000000;
-      a_snap[3 * q] = a_snap[3 * q + 1] = a_snap[3 * q + 2] = 0;
-      q++;
-    }
-    for (int64_t j = 0; j < k; j++, q++) {
-      const int32_t r = aligned[b + j];
-      a_off[q] = (int32_t)(sys + (j + 1) * chunk);
-      a_kind[q] = 1;  // REUSABLE, counter snapshot (g, a, n) of its segment
-      a_seg[q] = r;
-      a_snap[3 * q] = g[r];
-      a_snap[3 * q + 1] = a[r];
-      a_snap[3 * q + 2] = nd[r];
-    }
-    if (sfx > 0) {
-      a_off[q] = (int32_t)(sys + k * chunk + sfx);
-      a_kind[q] = 2;  // PRIVATE
-      a_seg[q] = (int32_t)0x80000000;
-      a_snap[3 * q] = a_snap[3 * q + 1] = a_snap[3 * q + 2] = 0;
-    }
+  // anchors (_build_anchors, engine.py:269-292): lane j the j-th segment's
+  // (its counter snapshot loads in parallel over the lanes)
+  const int64_t q0 = aoffs[w] + (sys > 0 ? 1 : 0);
+  if (lane == 0 && sys > 0) {
+    const int64_t q = q0 - 1;
+    a_off[q] = (int32_t)sys;
+    a_kind[q] = 0;  // SYSTEM
+    a_seg[q] = (int32_t)0x80000000;
+    a_snap[3 * q] = a_snap[3 * q + 1] = a_snap[3 * q + 2] = 0;
+  }
+  for (int64_t j = lane; j < k; j += 32) {
+    const int64_t q = q0 + j;
+    const int32_t r = aligned[b + j];
+    a_off[q] = (int32_t)(sys + (j + 1) * chunk);
+    a_kind[q] = 1;  // REUSABLE, counter snapshot (g, a, n) of its segment
+    a_seg[q] = r;
+    a_snap[3 * q] = g[r];
+    a_snap[3 * q + 1] = a[r];
+    a_snap[3 * q + 2] = nd[r];
+  }
+  if (lane == 0 && sfx > 0) {
+    const int64_t q = q0 + k;
+    a_off[q] = (int32_t)(sys + k * chunk + sfx);
+    a_kind[q] = 2;  // PRIVATE
+    a_seg[q] = (int32_t)0x80000000;
+    a_snap[3 * q] = a_snap[3 * q + 1] = a_snap[3 * q + 2] = 0;
   }
 }
 
