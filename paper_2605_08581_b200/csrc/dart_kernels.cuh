@@ -56,14 +56,23 @@ __device__ __forceinline__ uint64_t ht_probe_free(const DT &T, uint64_t key, boo
 }
 
 // warp-collective common-prefix length of a[0..lim) and b[0..lim) (kvcache.py:109-114)
+// (4 x 32 tokens per step: the loads of a step are independent, so long edges
+// -- a 1024-token system prompt -- cost a quarter of the round trips)
 __device__ __forceinline__ int64_t warp_lcp(const uint32_t *__restrict__ a, const uint32_t *b,
                                             int64_t lim) {
   const int lane = lane_id();
-  for (int64_t j = 0; j < lim; j += 32) {
-    const int64_t i = j + lane;
-    const bool ne = i < lim && a[i] != b[i];
-    const unsigned m = __ballot_sync(FULL, ne);
-    if (m) return j + __ffs(m) - 1;
+  for (int64_t j = 0; j < lim; j += 128) {
+    bool ne[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int64_t i = j + 32 * u + lane;
+      ne[u] = i < lim && a[i] != b[i];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const unsigned m = __ballot_sync(FULL, ne[u]);
+      if (m) return j + 32 * u + __ffs(m) - 1;
+    }
   }
   return lim;
 }
