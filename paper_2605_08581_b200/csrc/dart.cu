@@ -149,7 +149,7 @@ struct prism_tree {
     KvDev k{};
     int32_t *kvx_spare = nullptr;
     int64_t kvx_cap = 0;
-    int64_t *voff = nullptr, *total = nullptr;
+    int64_t *voff = nullptr, *total = nullptr, *part = nullptr;  // part: k_kv_vsum's chunk sums (1024)
     int64_t voff_cap = 0;
   } *kv = nullptr;
 };
@@ -994,7 +994,7 @@ void prism_tree_destroy(prism_tree *t) {
   cudaStreamSynchronize(t->st);
   if (t->kv) {
     void *kb[] = {t->kv->k.pool, t->kv->k.kvx, t->kv->k.stack, t->kv->k.top, t->kv->k.moved, t->kv->kvx_spare,
-                  t->kv->voff, t->kv->total, t->kv->k.ctl};
+                  t->kv->voff, t->kv->total, t->kv->part, t->kv->k.ctl};
     for (void *p : kb)
       if (p) cudaFree(p);
     delete t->kv;
@@ -1841,10 +1841,12 @@ int kv_sync(prism_tree *t, const void *src, void *dst, int64_t *out) {
   }
   int sms = t->sms;
   if (sms <= 0) CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev));
-  const unsigned grid = (unsigned)(8 * sms);
+  if (!K->part) CK(dalloc(&K->part, 1024));
+  const unsigned grid = (unsigned)(8 * sms), sgrid = (unsigned)std::min(4 * sms, 1024);
   k_kv_prep<<<1, 1, 0, t->st>>>(K->k, t->d.ctrl, t->d.vcap);
   k_kv_alloc<<<grid, TPB, 0, t->st>>>(K->k, (const uint8_t *)src);
-  k_kv_voff<<<1, 1024, 0, t->st>>>(t->d.vlog, t->d.vcap, K->voff, K->k);
+  k_kv_vsum<<<sgrid, 1024, 0, t->st>>>(t->d.vlog, t->d.vcap, K->part, K->k);
+  k_kv_vfill<<<sgrid, 1024, 0, t->st>>>(t->d.vlog, t->d.vcap, K->voff, K->part, K->k);
   k_kv_free<<<grid, TPB, 0, t->st>>>(K->k, t->d.vlog, t->d.vcap, K->voff, (uint8_t *)dst);
   k_kv_fin<<<1, 1, 0, t->st>>>(K->k, t->d.ctrl, src ? 1 : 0, dst ? 1 : 0);
   CK(cudaGetLastError());
