@@ -49,7 +49,8 @@ struct CoopState {
   unsigned int ss_off[SS_SPL + 4];  // bucket offsets
   int ss_ok;                    // the sample select produced the sorted prefix
   unsigned long long tf_n;      // top-f protection: candidates with a positive P-hat
-  int tf_done;                  // top-f protection applied by k_tf_merge (k_protect_coop returns)
+  int tf_done;                  // top-f protection applied by k_tf_local (k_protect_coop returns)
+  unsigned int tf_cl;           // k_tf_local: clusters that published their top f
   unsigned long long ss_dbg[24];
   unsigned long long ss_prof[8];  // diagnostics: k_ss_sort clock64 sums (load, sort, buckets, items)  // diagnostics: [0] max bucket, [1] rounds, [2+3r..] (undecided, selected, shift)
   int ss_nb;                    // diagnostics: splitters of the last sample select
@@ -1404,13 +1405,12 @@ __global__ void __launch_bounds__(COOP_TPB) k_build_coop(DT T, CoopBufs B, int64
 // P-hat -- the pending round's segments, a few thousand nodes -- the top f are
 // among those.  k_tf_scan visits every slot once (clearing the previous flags,
 // leaving the eviction keys when asked) and lists them; every slice of the
-// list keeps its f smallest (k_tf_local), one CTA merges those (k_tf_merge).
+// list keeps its f smallest, merged across each cluster and then by the last
+// cluster (k_tf_local).
 // Otherwise ss_ok stays 0 and k_protect_coop runs the materialising selection.
 constexpr int TF_MAX = 64;     // budgets up to this use the small top-f path
 constexpr int TF_SLICE = 256;  // list items per slice of k_tf_local (shared-memory sort)
 constexpr size_t TF_SMEM = 2 * (sizeof(Key3) + 8) * TF_SLICE;
-constexpr int TF_MERGE_MAX = 3072;  // per-slice winners merged by one CTA
-constexpr size_t TF_MERGE_SMEM = 2 * (sizeof(Key3) + 8) * TF_MERGE_MAX;
 
 __global__ void __launch_bounds__(SS_TPB) k_tf_scan(ProtCand cand, CoopBufs B) {
   __shared__ unsigned s_w[32];
@@ -1496,35 +1496,94 @@ __global__ void __launch_bounds__(SS_TPB) k_tf_scan(ProtCand cand, CoopBufs B) {
   if (lane == 0 && ccount) atomicAdd(&B.st->ss_cand, ccount);
 }
 
-// every CTA: the f smallest keys of ITS slices of the list (slices c = blockIdx.x,
-// + gridDim.x, ...) -> B.ks/vs[blockIdx.x * f ..]: each TF_SLICE-item slice is
-// sorted in shared memory and its top f merged into the CTA's running top f,
-// so the merge CTA sees gridDim.x lists whatever the list length (the grid is
-// sized so that gridDim.x * f <= TF_MERGE_MAX)
-__global__ void __launch_bounds__(SS_TPB) k_tf_local(CoopBufs B, int64_t f) {
+// merge a sorted list of F (rk/rv[cur], padded with all-ones keys) with
+// another sorted list o of F into rk/rv[cur ^ 1]: an item's place is its index
+// plus its rank in the other list (real keys are distinct; the pads rank
+// after every real key, so they only fill places past the real items)
+__device__ __forceinline__ void tf_merge2(Key3 (*rk)[TF_MAX], uint64_t (*rv)[TF_MAX], int cur, const Key3 *ok,
+                                          const uint64_t *ov, int F) {
+  const int nxt = cur ^ 1;
+  for (int t = threadIdx.x; t < 2 * F; t += blockDim.x) {
+    const bool run = t < F;
+    const int i = run ? t : t - F;
+    const Key3 x = run ? rk[cur][i] : ok[i];
+    const Key3 *O = run ? ok : rk[cur];
+    int lo = 0, hi = F;  // the running list's items go before equal ones (pads)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (run ? key_less(O[mid], x) : !key_less(x, O[mid])) lo = mid + 1;
+      else hi = mid;
+    }
+    const int pos = i + lo;
+    if (pos < F) {
+      rk[nxt][pos] = x;
+      rv[nxt][pos] = run ? rv[cur][i] : ov[i];
+    }
+  }
+  __syncthreads();
+}
+
+// The top f of the positive-P-hat list in one launch of TF_CL-CTA clusters:
+//  * every CTA keeps the f smallest keys of ITS slices (c = blockIdx.x,
+//    + gridDim.x, ...): each TF_SLICE-item slice is sorted in shared memory and
+//    its top f merged into the running top f;
+//  * the cluster's rank-0 CTA merges its peers' lists straight out of their
+//    shared memory (DSMEM) and publishes the cluster's top f;
+//  * the last cluster to publish (a counter) merges the <= TF_FIN / f cluster
+//    lists pairwise in shared memory and applies the protection -- what one
+//    separate single-CTA merge over every CTA's list (~3000 items) did before.
+constexpr int TF_CL = 8;      // CTAs per cluster
+constexpr int TF_FIN = 512;   // cluster lists x f merged by the last cluster
+constexpr size_t TF_LOCAL_SMEM =
+    std::max(TF_SMEM, (size_t)2 * (sizeof(Key3) + 8) * TF_FIN);
+
+__global__ void __cluster_dims__(TF_CL, 1, 1) __launch_bounds__(SS_TPB)
+    k_tf_local(DT T, CoopBufs B, int64_t f, int32_t keys) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ Key3 rk[2][TF_MAX];
   __shared__ uint64_t rv[2][TF_MAX];
+  __shared__ Key3 fk[TF_MAX];  // this CTA's top f, read by the cluster's rank 0
+  __shared__ uint64_t fv[TF_MAX];
+  __shared__ bool s_last;
   const int64_t n = (int64_t)B.st->tf_n;
-  if (n < f) return;
+  if (n < f || f <= 0) return;  // (uniform) ss_ok stays 0: the materialising path decides
+  cg::cluster_group cluster = cg::this_cluster();
   Key3 *sk = reinterpret_cast<Key3 *>(dsm);
   uint64_t *sv = reinterpret_cast<uint64_t *>(sk + TF_SLICE);
   Key3 *tk = reinterpret_cast<Key3 *>(sv + TF_SLICE);
   uint64_t *tv = reinterpret_cast<uint64_t *>(tk + TF_SLICE);
   const int F = (int)f;
+  const Key3 PAD{~0ull, ~0ull, ~0ull};
+  __shared__ int s_m;
   int have = 0, cur = 0;  // running top list: rk/rv[cur][0..have)
   for (int64_t c = blockIdx.x; c * TF_SLICE < n; c += gridDim.x) {
     const int64_t b0 = c * TF_SLICE;
-    const int m = (int)(n - b0 < TF_SLICE ? n - b0 : TF_SLICE);
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
-      sk[i] = B.k1[b0 + i];
-      sv[i] = B.v1[b0 + i];
+    int m = (int)(n - b0 < TF_SLICE ? n - b0 : TF_SLICE);
+    if (have == F) {  // (uniform) only the slice's keys below the running f-th can enter: sort just those
+      if (threadIdx.x == 0) s_m = 0;
+      __syncthreads();
+      const Key3 thr = rk[cur][F - 1];
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const Key3 x = B.k1[b0 + i];
+        if (key_less(x, thr)) {
+          const int q = atomicAdd(&s_m, 1);
+          sk[q] = x;
+          sv[q] = B.v1[b0 + i];
+        }
+      }
+      __syncthreads();
+      m = s_m;
+      __syncthreads();
+      if (m == 0) continue;
+    } else {
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        sk[i] = B.k1[b0 + i];
+        sv[i] = B.v1[b0 + i];
+      }
+      __syncthreads();
     }
-    __syncthreads();
     block_merge_sort(sk, sv, m, tk, tv, sk, sv);
     const int keep = m < F ? m : F;
-    // merge the running list (have) and this slice's top (keep): an item's place
-    // is its index plus its rank in the other list (keys are distinct); keep < F
     const int nxt = cur ^ 1;
     for (int t = threadIdx.x; t < have + keep; t += blockDim.x) {
       const bool run = t < have;
@@ -1548,39 +1607,48 @@ __global__ void __launch_bounds__(SS_TPB) k_tf_local(CoopBufs B, int64_t f) {
     cur = nxt;
   }
   for (int i = threadIdx.x; i < F; i += blockDim.x) {
-    B.ks[(int64_t)blockIdx.x * F + i] = i < have ? rk[cur][i] : Key3{~0ull, ~0ull, ~0ull};
-    B.vs[(int64_t)blockIdx.x * F + i] = i < have ? rv[cur][i] : 0ull;
+    fk[i] = i < have ? rk[cur][i] : PAD;
+    fv[i] = i < have ? rv[cur][i] : 0ull;
   }
-}
-
-// one CTA: the f smallest of the per-slice winners -> T.Lk/Lv[0..f), ss_ok.
-// The slices' sorted top-f lists are merged pairwise in a tree: an item's
-// place in the merge of lists A and B is its index plus its rank in the other
-// list (a binary search over f), and only places < f are kept.
-__global__ void __launch_bounds__(SS_SEL_TPB) k_tf_merge(DT T, CoopBufs B, int64_t f, int32_t keys,
-                                                        int32_t nlists) {
-  extern __shared__ __align__(16) unsigned char dsm[];
-  const int64_t n = (int64_t)B.st->tf_n;
-  if (n < f || f <= 0) return;  // ss_ok stays 0: the materialising path decides
-  const int64_t nslices = (n + TF_SLICE - 1) / TF_SLICE;
-  const int nsl = (int)(nslices < nlists ? nslices : nlists);  // k_tf_local's lists
-  const int F = (int)f;
-  if ((int64_t)nsl * F > TF_MERGE_MAX) return;  // too many lists for one CTA: the materialising path
+  cluster.sync();
+  const unsigned cid = blockIdx.x / TF_CL, ncl = gridDim.x / TF_CL;
+  if (cluster.block_rank() == 0) {
+    for (int i = threadIdx.x; i < F; i += blockDim.x) {
+      rk[0][i] = fk[i];
+      rv[0][i] = fv[i];
+    }
+    __syncthreads();
+    int c2 = 0;
+    for (unsigned r = 1; r < TF_CL; r++, c2 ^= 1)
+      tf_merge2(rk, rv, c2, cluster.map_shared_rank(fk, r), cluster.map_shared_rank(fv, r), F);
+    for (int i = threadIdx.x; i < F; i += blockDim.x) {
+      B.ks[(int64_t)cid * F + i] = rk[c2][i];
+      B.vs[(int64_t)cid * F + i] = rv[c2][i];
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&B.st->tf_cl, 1u) == ncl - 1;
+  }
+  cluster.sync();  // (the peers' shared memory stays alive until rank 0 has read it)
+  if (cluster.block_rank() != 0 || !s_last) return;
+  __threadfence();
+  // the last cluster: pairwise rounds over the ncl cluster lists (TF_FIN items at most)
   Key3 *ak = reinterpret_cast<Key3 *>(dsm);
-  uint64_t *av = reinterpret_cast<uint64_t *>(ak + TF_MERGE_MAX);
-  Key3 *bk = reinterpret_cast<Key3 *>(av + TF_MERGE_MAX);
-  uint64_t *bv = reinterpret_cast<uint64_t *>(bk + TF_MERGE_MAX);
-  for (int i = threadIdx.x; i < nsl * F; i += blockDim.x) {
-    ak[i] = B.ks[i];
-    av[i] = B.vs[i];
+  uint64_t *av = reinterpret_cast<uint64_t *>(ak + TF_FIN);
+  Key3 *bk = reinterpret_cast<Key3 *>(av + TF_FIN);
+  uint64_t *bv = reinterpret_cast<uint64_t *>(bk + TF_FIN);
+  for (int i = threadIdx.x; i < (int)ncl * F; i += blockDim.x) {
+    // (other SMs' stores: L2-coherent loads)
+    ak[i] = Key3{__ldcg(&B.ks[i].w0), __ldcg(&B.ks[i].w1), __ldcg(&B.ks[i].w2)};
+    av[i] = __ldcg(&B.vs[i]);
   }
   __syncthreads();
-  int L = nsl;
-  while (L > 1) {
-    const int pairs = L >> 1;
+  int Ln = (int)ncl;
+  while (Ln > 1) {
+    const int pairs = Ln >> 1;
     for (int t = threadIdx.x; t < pairs * 2 * F; t += blockDim.x) {
-      const int p = t / (2 * F), side = (t / F) & 1, i = t % F;
-      const Key3 *A = ak + (2 * p) * F, *Bl = ak + (2 * p + 1) * F;
+      const int q = t / (2 * F), side = (t / F) & 1, i = t % F;
+      const Key3 *A = ak + (2 * q) * F, *Bl = ak + (2 * q + 1) * F;
       const Key3 x = side ? Bl[i] : A[i];
       const Key3 *O = side ? A : Bl;  // the other list
       int lo = 0, hi = F;  // A's items go before equal B items (stable)
@@ -1591,23 +1659,23 @@ __global__ void __launch_bounds__(SS_SEL_TPB) k_tf_merge(DT T, CoopBufs B, int64
       }
       const int pos = i + lo;
       if (pos < F) {
-        bk[p * F + pos] = x;
-        bv[p * F + pos] = side ? av[(2 * p + 1) * F + i] : av[(2 * p) * F + i];
+        bk[q * F + pos] = x;
+        bv[q * F + pos] = side ? av[(2 * q + 1) * F + i] : av[(2 * q) * F + i];
       }
     }
-    if (L & 1)
+    if (Ln & 1)
       for (int i = threadIdx.x; i < F; i += blockDim.x) {
-        bk[pairs * F + i] = ak[(L - 1) * F + i];
-        bv[pairs * F + i] = av[(L - 1) * F + i];
+        bk[pairs * F + i] = ak[(Ln - 1) * F + i];
+        bv[pairs * F + i] = av[(Ln - 1) * F + i];
       }
     __syncthreads();
-    Key3 *tk = ak;
+    Key3 *tk2 = ak;
     ak = bk;
-    bk = tk;
-    uint64_t *tv = av;
+    bk = tk2;
+    uint64_t *tv2 = av;
     av = bv;
-    bv = tv;
-    L = pairs + (L & 1);
+    bv = tv2;
+    Ln = pairs + (Ln & 1);
   }
   for (int i = threadIdx.x; i < F; i += blockDim.x) {
     T.Lk[i] = ak[i];

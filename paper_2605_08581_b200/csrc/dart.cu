@@ -1175,16 +1175,12 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out, int3
     if (sampled && f <= TF_MAX) {  // small budget: the positive-P-hat list and its top f
       int sms = 0;
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev));
-      static uint64_t tf_attr = 0;
-      if (prism::attr_once(tf_attr)) {
-        CK(cudaFuncSetAttribute(k_tf_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TF_MERGE_SMEM));
-      }
       k_tf_scan<<<4 * sms, SS_TPB, 0, t->st>>>(ProtCand{t->d, keys}, B);
-      const int nl = (int)std::max<int64_t>(1, std::min<int64_t>(2 * sms, TF_MERGE_MAX / std::max<int64_t>(ff, 1)));
-      k_tf_local<<<nl, SS_TPB, TF_SMEM, t->st>>>(B, ff);
-      k_tf_merge<<<1, SS_SEL_TPB, TF_MERGE_SMEM, t->st>>>(t->d, B, ff, keys, nl);
+      // clusters of TF_CL CTAs, at most TF_FIN / f of them (the last one's merge)
+      const int ncl = (int)std::max<int64_t>(1, std::min<int64_t>(2 * sms / TF_CL, TF_FIN / std::max<int64_t>(ff, 1)));
+      k_tf_local<<<ncl * TF_CL, SS_TPB, TF_LOCAL_SMEM, t->st>>>(t->d, B, ff, keys);
       CK(cudaGetLastError());
-      t->launches[PH_PROTECT] += 3;
+      t->launches[PH_PROTECT] += 2;
     } else if (sampled) {
       rc = sample_select(t, ProtCand{t->d, keys}, B, ff, nullptr, minc);
       if (rc) return rc;
