@@ -980,9 +980,11 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_sample(Cand cand, CoopBufs B, int
   }
 }
 
+// CTA 0 of k_ss_select's cluster: tau and the (unsorted) splitters in selk;
+// *o_nb of them, *o_fail why not
 template <class Cand>
-__global__ void __launch_bounds__(SS_SEL_TPB) k_ss_select(Cand cand, CoopBufs B, int64_t W, const int64_t *dW) {
-  extern __shared__ __align__(16) unsigned char dsm[];
+__device__ __forceinline__ void ss_select_body(Cand cand, CoopBufs B, int64_t W, const int64_t *dW,
+                                               unsigned char *dsm, int *o_fail, int *o_nb) {
   if (dW) W = *dW;
   __shared__ Key3 smin[33], smax[33];
   __shared__ unsigned s_hn[256];
@@ -1073,18 +1075,19 @@ __global__ void __launch_bounds__(SS_SEL_TPB) k_ss_select(Cand cand, CoopBufs B,
     __syncthreads();
     block_merge_sort(fk, fw, nU, fk2, fw2, fk, fw);
     coop_mark(st);
-    if (threadIdx.x == 0) {
-      long long run = 0;
-      int c = nU - 1;
-      for (int j = 0; j < nU; j++) {
-        run += (long long)fw[j];
-        if (run >= need) {
-          c = j;
-          break;
-        }
+    {  // the crossing sample: the first j whose inclusive weight prefix reaches need (nU <= blockDim)
+      const int j = threadIdx.x, wid = threadIdx.x >> 5;
+      long long inc = j < nU ? (long long)fw[j] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
       }
-      s_misc[3] = c;
-      s_nsel = 0;
+      if (lane == 31) s_u64[wid] = (unsigned long long)inc;
+      if (threadIdx.x == 0) s_misc[3] = nU - 1;
+      __syncthreads();
+      for (int w = 0; w < wid; w++) inc += (long long)s_u64[w];
+      if (j < nU && inc >= need) atomicMin(&s_misc[3], j);
+      if (threadIdx.x == 0) s_nsel = 0;
     }
     __syncthreads();
     const Key3 tau = fk[s_misc[3]];
@@ -1114,17 +1117,71 @@ __global__ void __launch_bounds__(SS_SEL_TPB) k_ss_select(Cand cand, CoopBufs B,
     if (__syncthreads_or(ovf)) fail = 3;
     coop_mark(st);
   }
-  int nb = 0;
-  if (!fail) {  // splitters: the selected samples, sorted exactly
-    nb = s_nsel;
-    block_merge_sort(selk, nullptr, nb, spl, nullptr, selk, nullptr);
-    for (int q = threadIdx.x; q < nb; q += blockDim.x) B.kt[q] = selk[q];
-    coop_mark(st);
-  }
   if (threadIdx.x == 0) {
-    st->ss_nb = fail ? 0 : nb;
-    st->ss_fail = fail;
+    *o_fail = fail;
+    *o_nb = fail ? 0 : s_nsel;
   }
+}
+
+// The sample select: CTA 0 finds tau and the splitters (every sample <= tau,
+// ~2000), then the cluster sorts them -- every CTA sorts a slice pulled from
+// CTA 0's shared memory (DSMEM), gathers the sorted slices from its peers and
+// places each of its keys at (its rank in the slice + its rank in every other
+// slice).  One CTA sorting them alone took ~30 us of the wave.
+constexpr int SS_CL = 8;  // CTAs in k_ss_select's cluster
+template <class Cand>
+__global__ void __cluster_dims__(SS_CL, 1, 1) __launch_bounds__(SS_SEL_TPB)
+    k_ss_select(Cand cand, CoopBufs B, int64_t W, const int64_t *dW) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ int s_fail, s_nb;
+  cg::cluster_group cluster = cg::this_cluster();
+  const unsigned rank = cluster.block_rank();
+  if (rank == 0) ss_select_body(cand, B, W, dW, dsm, &s_fail, &s_nb);
+  cluster.sync();
+  const int fail = *cluster.map_shared_rank(&s_fail, 0), nb = *cluster.map_shared_rank(&s_nb, 0);
+  Key3 *lk = reinterpret_cast<Key3 *>(dsm);  // [SS_SPL / SS_CL] this CTA's slice, then [..] sort scratch
+  Key3 *tk = lk + SS_SPL / SS_CL;
+  Key3 *all = lk + SS_SPL;                   // [SS_SPL] every sorted slice (CTA 0: its selk, read by now)
+  const int per = (nb + SS_CL - 1) / SS_CL;
+  const int b0 = min(nb, (int)rank * per), m = min(nb, b0 + per) - b0;
+  if (!fail) {
+    const Key3 *sel0 = cluster.map_shared_rank(all, 0);  // (CTA 0's selk: the same offset)
+    for (int i = threadIdx.x; i < m; i += blockDim.x) lk[i] = sel0[b0 + i];
+    __syncthreads();
+    block_merge_sort(lk, nullptr, m, tk, nullptr, lk, nullptr);
+  }
+  cluster.sync();  // every slice sorted; CTA 0's selk read
+  if (!fail) {
+    for (int r = 0; r < SS_CL; r++) {
+      const int r0 = min(nb, r * per), rm = min(nb, r0 + per) - r0;
+      const Key3 *src = cluster.map_shared_rank(lk, r);
+      for (int i = threadIdx.x; i < rm; i += blockDim.x) all[r0 + i] = src[i];
+    }
+    __syncthreads();
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      const Key3 x = lk[i];
+      int pos = i;
+      for (int r = 0; r < SS_CL; r++) {
+        if (r == (int)rank) continue;
+        const int r0 = min(nb, r * per), r1 = min(nb, r0 + per);
+        int lo = r0, hi = r1;
+        const bool before = r < (int)rank;  // (equal keys of earlier slices first: a stable order)
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (before ? !key_less(x, all[mid]) : key_less(all[mid], x)) lo = mid + 1;
+          else hi = mid;
+        }
+        pos += lo - r0;
+      }
+      B.kt[pos] = x;
+    }
+  }
+  if (rank == 0 && threadIdx.x == 0) {
+    B.st->ss_nb = fail ? 0 : nb;
+    B.st->ss_fail = fail;
+  }
+  coop_mark(B.st);
+  cluster.sync();  // (the peers' slices stay alive until every CTA has gathered them)
 }
 
 template <class Cand>
