@@ -560,7 +560,6 @@ struct prism_qas {
   X(int32_t, touched) \
   X(int32_t, tn) \
   X(int64_t, qcounts) \
-  X(int32_t, plist) \
   X(unsigned long long, qts)
 #define QBUF(T, name) \
   T *name = nullptr;  \
@@ -702,7 +701,6 @@ int qas_small_prepare(prism_qas *q, int64_t P, int32_t nseg, const QCfg &c, int6
   QCK(grow(&q->cv2, q->cv2_cap, P));
   QCK(grow(&q->pk, q->pk_cap, pt));
   QCK(grow(&q->pv, q->pv_cap, pt));
-  QCK(grow(&q->plist, q->plist_cap, pt / 2));
   QCK(grow(&q->qcounts, q->qcounts_cap, 8));
   if (q->prof_on) QCK(grow(&q->qts, q->qts_cap, qsmall::QS_NTS));
   if (!q->small_coresident) {
@@ -761,8 +759,6 @@ int qas_small_launch(prism_qas *q, const QIn &in, int64_t P, int64_t A, int64_t 
   qa.nsegs = q->bend;
   qa.isum = (long long *)q->take;
   qa.ptab_key = q->pk;
-  qa.ptab_cnt = q->pv;
-  qa.plist = q->plist;
   qa.ptab_cap = std::min(q->pk_cap, q->pv_cap);
   qa.btab_mask = bt_mask;
   qa.longl = q->longl;
@@ -1566,7 +1562,7 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
                           q->tok, q->a_off, q->a_kind, q->a_seg, q->a_snap, q->err, q->tmp_tot, q->qcounts, q->hres,
                           q->touched, q->tn, q->rk, q->emap, q->efirst, q->btake, q->bbase, q->gdem, q->prio_glob, q->dom_glob, rel_slots, q->st_rel, q->longl, q->sig, q->siglen, q->tkey, q->tmin,
                           q->slot_of, q->bmin, q->bstart, q->bend, q->score, q->take, q->rank, q->bucket, q->hot,
-                          q->cv2, q->pk, q->pv, q->plist, host_out ? q->hout_mem : nullptr,
+                          q->cv2, q->pk, q->pv, host_out ? q->hout_mem : nullptr,
                           host_out ? q->hout_hit : nullptr};
     const int64_t dims[] = {P, B, G, btmask, nseg, sys_len, chunk, tok_cap, anc_cap, q->pk_cap, q->pv_cap, rel_n,
                             q->aligned_cap, q->rk_cap, q->emap_cap, q->efirst_cap, (int64_t)q->prof_on};

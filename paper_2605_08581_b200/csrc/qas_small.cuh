@@ -63,8 +63,6 @@ struct QsArgs {
   int32_t *btake, *bbase;  // per bucket: hot-lane members taken, first hot-lane position
   long long *isum;
   uint64_t *ptab_key;  // (bucket, seg) pair table (the kernel uses 2*nsk slots of it)
-  int32_t *ptab_cnt;
-  int32_t *plist;      // inserted pair slots
   int64_t ptab_cap, btab_mask;
   int32_t *longl;       // requests with skeletons longer than QS_MAXK
   int32_t *rk;          // rank scratch for them (aligned_cap ints)
@@ -612,9 +610,10 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
     A.btab_key[i] = QS_EMPTY;
     A.btab_min[i] = 0x7fffffff;
   }
-  for (int64_t i = gt; i < pm; i += gs) {
-    A.ptab_key[i] = QS_EMPTY;
-    A.ptab_cnt[i] = 0;
+  for (int64_t i = gt; i < pm; i += gs) A.ptab_key[i] = QS_EMPTY;
+  for (int64_t i = gt; i < P; i += gs) {  // per-bucket utility sums (bucket ids < P), filled in phases 4 and 7
+    A.isum[i] = 0;
+    A.nsegs[i] = 0;
   }
   if (gt == 0) A.touched_n[0] = 0;
   {  // entry -> request map + first-occurrence flags of the pending skeletons: one warp per request
@@ -762,6 +761,7 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   // request's first member in shared memory, then one warp per request counts
   // the first members before its bucket's (= its bucket id) and its bucket's
   // members before it (= its rank); a first member also counts its bucket's size
+  const int64_t hot_cap = c.budget - c.cold;
   {
     int32_t *sfirst = sv;  // [P <= QS_MAXP]
     // a request's bucket representative = its bucket's first member (final now that every insert is done)
@@ -792,30 +792,32 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
       if (lane == 0) {
         A.rank[i] = rk;
         A.bucket[i] = nbef;
-        if (f == (int32_t)i) {
-          A.bsize[nbef] = sz;
-          A.nsegs[nbef] = 0;
-          A.isum[nbef] = 0;
-        }
+        if (f == (int32_t)i) A.bsize[nbef] = sz;
         if (last) A.counts[2] = nall;
       }
     }
   }
   qs_gsync();
   QS_TS(4);
-  // 7. distinct (bucket, segment) pairs; provisional = first hot_cap members (146-171)
-  const int64_t hot_cap = c.budget - c.cold;
-  for (int64_t e0 = 0; e0 < nsk; e0 += gs) {  // one thread per skeleton entry
-    const int64_t e = e0 + qs_ilv(gs);
-    int32_t s = 0, bk = 0;
-    bool np = false;
-    int32_t npos = 0;
-    if (e < nsk) {
-      const int64_t i = A.emap[e];
-      if (A.efirst[e]) {
-        s = A.sk[e];
-        bk = A.bucket[i];
-        const int prov = A.rank[i] < hot_cap ? 1 : 0;
+  // 7. distinct (bucket, segment) pairs (146-171) and the buckets' utility
+  // sums, one warp per request: the lane that inserts a pair adds its
+  // wg g + wa a and one distinct segment; a provisional member (rank < hot_cap)
+  // adds wn x its distinct segments -- the sum over the bucket's pairs of
+  // wn x count(provisional members holding the segment), regrouped by member
+  // (integral weights: exact in int64 in any order).  One atomic pair per
+  // request, not per pair (hot buckets collect thousands of pairs).
+  {
+    const int lane = tid & 31;
+    const int64_t nw = gs >> 5;
+    for (int64_t i = (int64_t)(tid >> 5) * gridDim.x + blockIdx.x; i < P; i += nw) {  // warps interleaved
+      const int32_t bk = A.bucket[i];
+      const int64_t b = A.off[i], e = A.off[i + 1];
+      unsigned long long su = 0;
+      int32_t np = 0, nds = 0;
+      for (int64_t x = b + lane; x < e; x += 32) {
+        if (!A.efirst[x]) continue;
+        const int32_t s = A.sk[x];
+        nds++;
         const uint64_t key = ((uint64_t)(uint32_t)bk << 32) | (uint32_t)s;
         uint64_t pos = qmix64(key) & pmask;
         for (;;) {
@@ -824,59 +826,31 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
           if (prev == QS_EMPTY) {
             prev = atomicCAS(slot, QS_EMPTY, key);
             if (prev == QS_EMPTY) {
-              np = true;
-              npos = (int32_t)pos;
+              np++;
+              su += (unsigned long long)(long long)__dadd_rn(__dmul_rn(c.wg, (double)A.g[s]),
+                                                             __dmul_rn(c.wa, (double)A.a[s]));
             }
           }
-          if (prev == QS_EMPTY || prev == key) {
-            if (prov) atomicAdd(&A.ptab_cnt[pos], 1);
-            break;
-          }
+          if (prev == QS_EMPTY || prev == key) break;
           pos = (pos + 1) & pmask;
         }
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        su += __shfl_xor_sync(0xffffffffu, su, o);
+        np += __shfl_xor_sync(0xffffffffu, np, o);
+        nds += __shfl_xor_sync(0xffffffffu, nds, o);
+      }
+      if (lane == 0) {
+        if (A.rank[i] < hot_cap) su += (unsigned long long)(long long)__dmul_rn(c.wn, (double)nds);
+        if (su) atomicAdd((unsigned long long *)&A.isum[bk], su);
+        if (np) atomicAdd(&A.nsegs[bk], np);
+      }
     }
-    const int p = qs_block_reserve(np ? 1 : 0, (int32_t *)&A.counts[5]);  // (low word of the zeroed int64)
-    if (np) A.plist[p] = npos;
   }
   qs_gsync();
   QS_TS(5);
-  // 8. utility terms of the distinct pairs, summed exactly (integral weights):
-  // per-CTA partial sums per bucket in shared memory (exact 64-bit integer
-  // adds), then one global add per bucket and CTA (hot buckets collect many
-  // pairs, in any order of the pair list)
-  const int64_t npairs = (int64_t)__ldcg((const unsigned long long *)&A.counts[5]);
-  {
-    const int32_t nbk = (int32_t)__ldcg((const unsigned long long *)&A.counts[2]);
-    unsigned long long *lsum = reinterpret_cast<unsigned long long *>(sk);  // [nbk <= QS_MAXP]
-    int32_t *lcnt = reinterpret_cast<int32_t *>(lsum + QS_MAXP);              // distinct segments per bucket
-    for (int q = tid; q < nbk; q += blockDim.x) {
-      lsum[q] = 0ull;
-      lcnt[q] = 0;
-    }
-    __syncthreads();
-    for (int64_t t0 = 0; t0 < npairs; t0 += gs) {
-      const int64_t t = t0 + gt;
-      if (t < npairs) {
-        const int32_t pos = A.plist[t];
-        const uint64_t key = __ldcg((const unsigned long long *)&A.ptab_key[pos]);
-        const int32_t bk = (int32_t)(key >> 32);
-        const int32_t s = (int32_t)(key & 0xffffffffu);
-        const double t1 = __dmul_rn(c.wg, (double)A.g[s]);
-        const double t2 = __dmul_rn(c.wa, (double)A.a[s]);
-        const double t3 = __dmul_rn(c.wn, (double)qs_ld(&A.ptab_cnt[pos]));
-        atomicAdd(&lsum[bk], (unsigned long long)(long long)__dadd_rn(__dadd_rn(t1, t2), t3));
-        atomicAdd(&lcnt[bk], 1);
-      }
-    }
-    __syncthreads();
-    for (int q = tid; q < nbk; q += blockDim.x) {
-      if (lsum[q]) atomicAdd((unsigned long long *)&A.isum[q], lsum[q]);
-      if (lcnt[q]) atomicAdd(&A.nsegs[q], lcnt[q]);
-    }
-    __syncthreads();  // (sk is block 0's scratch in the next phase)
-  }
-  qs_gsync();
+  // 8. (folded into 4 and 7: the utility sums are complete here)
   QS_TS(6);
   // 9. scores (146-171), the (-score, creation order) order (234) and the
   // hot-lane fill (235-240) without a sort: every CTA lists all nb bucket keys
