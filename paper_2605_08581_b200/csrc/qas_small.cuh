@@ -282,17 +282,6 @@ __device__ inline int64_t qs_ilv(int64_t gs) {
   return (int64_t)threadIdx.x * gridDim.x + blockIdx.x;
 }
 
-// each distinct segment of skeleton [b, e) once (count_segments dedup, 83-89)
-template <class F>
-__device__ inline void qs_distinct(const int32_t *sk, int64_t b, int64_t e, F &&f) {
-  for (int64_t j = b; j < e; j++) {
-    const int32_t s = sk[j];
-    bool dup = false;
-    for (int64_t q = b; q < j && !dup; q++) dup = sk[q] == s;
-    if (!dup) f(s);
-  }
-}
-
 // skeleton entry e of a request starting at entry b: its segment, and whether
 // it is the segment's first occurrence in that skeleton (count_segments dedup)
 __device__ inline bool qs_first(const int32_t *sk, int64_t b, int64_t e, int32_t &s) {
@@ -490,13 +479,35 @@ __device__ inline void qs_cold_lane(const QsArgs &A, const QsCfg &c, int64_t P, 
   int n = m;
   if (nc < m) {
     uint8_t *st = reinterpret_cast<uint8_t *>(tmp);  // 0 candidate, 1 taken, 2 dropped
+    __shared__ unsigned long long s_dh, s_dl;
     for (int q = tid; q < m; q += nt) st[q] = 0;
     if (tid == 0) {
       s_need = (int32_t)nc;
       s_done = 0;
+      s_dh = 0;
+      s_dl = 0;
     }
     __syncthreads();
-    for (int d = 15; d >= 0 && !s_done; d--) {
+    {  // the bytes every leftover shares (arrivals of one window agree in their leading bytes) decide
+       // nothing: the select starts at the highest byte where two keys differ
+      const QKey k0 = sk[0];
+      unsigned long long dh = 0, dl = 0;
+      for (int q = tid; q < m; q += nt) {
+        dh |= sk[q].hi ^ k0.hi;
+        dl |= sk[q].lo ^ k0.lo;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        dh |= __shfl_xor_sync(0xffffffffu, dh, o);
+        dl |= __shfl_xor_sync(0xffffffffu, dl, o);
+      }
+      if ((tid & 31) == 0 && (dh | dl)) {
+        atomicOr(&s_dh, dh);
+        atomicOr(&s_dl, dl);
+      }
+    }
+    __syncthreads();
+    const int dtop = s_dh ? 8 + (63 - __clzll((long long)s_dh)) / 8 : (s_dl ? (63 - __clzll((long long)s_dl)) / 8 : 0);
+    for (int d = dtop; d >= 0 && !s_done; d--) {
       for (int x = tid; x < 256; x += nt) hist[x] = 0;
       __syncthreads();
       for (int q = tid; q < m; q += nt) {
@@ -641,31 +652,31 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
     const int p = qs_block_reserve(nt ? 1 : 0, &A.touched_n[0]);
     if (nt) A.touched[p] = s;
   }
-  for (int pass = 1; pass < 2; pass++) {  // active set: one thread per request
-    const int64_t n = pass == 0 ? P : A.A;
-    const int64_t *off = pass == 0 ? A.off : A.aoff;
-    const int32_t *sk_ = pass == 0 ? A.sk : A.ask;
-    int32_t *cnt = pass == 0 ? A.g : A.a;
-    // requests interleaved over the CTAs (every SM gets a share); the touched
-    // list is appended once per warp and batch (a single counter otherwise
-    // serialises every first touch)
-    for (int64_t i0 = 0; i0 < n; i0 += gs) {
-      const int64_t i = i0 + qs_ilv(gs);
-      int32_t newt[QS_MAXK];
-      int nn = 0;
-      if (i < n) {
-        const int64_t b = off[i], e = off[i + 1];
-        qs_distinct(sk_, b, e, [&](int32_t s) {
-          atomicAdd(&cnt[s], 1);
-          unsigned long long *f = (unsigned long long *)&A.prio[s];
-          if (__ldcg(f) == 0ull && atomicCAS(f, 0ull, 0xFFF0000000000001ull) == 0ull) {
-            if (nn < QS_MAXK) newt[nn++] = s;
-            else A.touched[atomicAdd(&A.touched_n[0], 1)] = s;
-          }
-        });
+  {  // active set: one warp per request, first occurrences by __match_any over the lanes (the
+     // pending skeletons' qs_flags_warp); the touched list appended once per warp
+    const int lane = tid & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t nw = gs >> 5;
+    for (int64_t i = (int64_t)(tid >> 5) * gridDim.x + blockIdx.x; i < A.A; i += nw) {  // warps interleaved
+      const int64_t b = A.aoff[i], k = A.aoff[i + 1] - b;
+      for (int64_t j0 = 0; j0 < k; j0 += 32) {
+        const bool on = j0 + lane < k;
+        const int32_t sj = on ? A.ask[b + j0 + lane] : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, sj);  // (every lane: no short circuit)
+        bool first = on && (peers & lt) == 0u;
+        for (int64_t q = 0; q < j0 && first; q++) first = A.ask[b + q] != sj;  // (entries of earlier rounds)
+        bool nt = false;
+        if (first) {
+          atomicAdd(&A.a[sj], 1);
+          unsigned long long *f = (unsigned long long *)&A.prio[sj];
+          nt = __ldcg(f) == 0ull && atomicCAS(f, 0ull, 0xFFF0000000000001ull) == 0ull;
+        }
+        const unsigned mt = __ballot_sync(0xffffffffu, nt);
+        int base = 0;
+        if (lane == 0 && mt) base = atomicAdd(&A.touched_n[0], __popc(mt));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (nt) A.touched[base + __popc(mt & lt)] = sj;
       }
-      const int base = qs_block_reserve(nn, &A.touched_n[0]);
-      for (int q = 0; q < nn; q++) A.touched[base + q] = newt[q];
     }
   }
   qs_gsync();
@@ -888,27 +899,23 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   }
   qs_gsync();
   QS_TS(7);
-  // 10. hot lane, and n_disp of its members (247-248)
-  for (int64_t i0 = 0; i0 < P; i0 += gs) {
-    const int64_t i = i0 + qs_ilv(gs);
-    bool lf = false;
-    if (i < P) {
-      const int32_t b = A.bucket[i];
-      const bool h = A.rank[i] < qs_ld(&A.btake[b]);
-      A.bidx[i] = h ? 1 : 0;  // reuse: hot flag
-      if (h) A.hot[(int64_t)qs_ld(&A.bbase[b]) + A.rank[i]] = i;
-      lf = !h;
+  // 10. hot lane, and n_disp of its members (247-248): one warp per request
+  // (its bucket's take read once, its skeleton entries over the lanes)
+  {
+    const int lane = tid & 31;
+    const int64_t nw = gs >> 5;
+    for (int64_t i = (int64_t)(tid >> 5) * gridDim.x + blockIdx.x; i < P; i += nw) {  // warps interleaved
+      const int32_t b = A.bucket[i], r = A.rank[i];
+      const bool h = r < qs_ld(&A.btake[b]);
+      if (lane == 0) {
+        A.bidx[i] = h ? 1 : 0;  // reuse: hot flag
+        if (h) A.hot[(int64_t)qs_ld(&A.bbase[b]) + r] = (int32_t)i;
+        else A.longl[atomicAdd((int32_t *)&A.counts[6], 1)] = (int32_t)i;  // leftovers (cold lane; any order)
+      }
+      if (h)
+        for (int64_t x = A.off[i] + lane; x < A.off[i + 1]; x += 32)
+          if (A.efirst[x]) atomicAdd(&A.nd[A.sk[x]], 1);
     }
-    // leftovers (cold lane), one counter atomic per CTA (low word of the zeroed int64)
-    const int p = qs_block_reserve(lf ? 1 : 0, (int32_t *)&A.counts[6]);
-    if (lf) A.longl[p] = (int32_t)i;
-  }
-  for (int64_t e0 = 0; e0 < nsk; e0 += gs) {  // n_disp of the hot members: one thread per skeleton entry
-    const int64_t e = e0 + qs_ilv(gs);
-    if (e >= nsk) continue;
-    const int64_t i = A.emap[e];
-    const int32_t b = A.bucket[i];
-    if (A.efirst[e] && A.rank[i] < qs_ld(&A.btake[b])) atomicAdd(&A.nd[A.sk[e]], 1);
   }
   qs_gsync();
   QS_TS(8);
