@@ -468,14 +468,25 @@ __device__ inline void qs_cold_lane(const QsArgs &A, const QsCfg &c, int64_t P, 
   __shared__ int32_t hist[256];
   __shared__ int32_t s_need, s_digit, s_done;
   const int tid = threadIdx.x, nt = blockDim.x;
-  // the leftovers, listed by the hot-lane phase (any order: the keys are distinct)
-  const int m = (int)__ldcg((const unsigned long long *)&A.counts[6]);
-  for (int q = tid; q < m; q += nt) {
-    const int32_t i = qs_ld(&A.longl[q]);
-    sk[q] = {qord(A.arrival[i]), (uint64_t)A.ids[i] ^ 0x8000000000000000ull};
-    sv[q] = i;
+  // the leftovers (rank >= their bucket's take), listed here -- beside the
+  // other CTAs' hot lane -- in any order (the keys are distinct)
+  __shared__ int32_t s_m;
+  if (tid == 0) s_m = 0;
+  __syncthreads();
+  for (int64_t i0 = 0; i0 < P; i0 += nt) {
+    const int64_t i = i0 + tid;
+    const bool lf = i < P && A.rank[i] >= qs_ld(&A.btake[A.bucket[i]]);
+    const unsigned mt = __ballot_sync(0xffffffffu, lf);
+    int base = 0;
+    if ((tid & 31) == 0 && mt) base = atomicAdd(&s_m, __popc(mt));
+    base = __shfl_sync(0xffffffffu, base, 0) + __popc(mt & ((1u << (tid & 31)) - 1u));
+    if (lf) {
+      sk[base] = {qord(A.arrival[i]), (uint64_t)A.ids[i] ^ 0x8000000000000000ull};
+      sv[base] = (int32_t)i;
+    }
   }
   __syncthreads();
+  const int m = s_m;
   int n = m;
   if (nc < m) {
     uint8_t *st = reinterpret_cast<uint8_t *>(tmp);  // 0 candidate, 1 taken, 2 dropped
@@ -900,32 +911,34 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
   qs_gsync();
   QS_TS(7);
   // 10. hot lane, and n_disp of its members (247-248): one warp per request
-  // (its bucket's take read once, its skeleton entries over the lanes)
-  {
+  // (its bucket's take read once, its skeleton entries over the lanes) -- on
+  // every CTA but 0, which meanwhile runs the cold lane (11: the oldest
+  // cold_quota leftovers by (arrival, id), listed by itself)
+  const int64_t nh = hot_cap < P ? (hot_cap > 0 ? hot_cap : 0) : P;
+  const int64_t nc = c.cold < P - nh ? c.cold : P - nh;
+  const bool split = gridDim.x > 1;
+  if (!split || !b0) {
     const int lane = tid & 31;
-    const int64_t nw = gs >> 5;
-    for (int64_t i = (int64_t)(tid >> 5) * gridDim.x + blockIdx.x; i < P; i += nw) {  // warps interleaved
+    const int64_t nbk = split ? gridDim.x - 1 : 1, bi = split ? blockIdx.x - 1 : 0;
+    const int64_t nw = nbk * (blockDim.x >> 5);
+    for (int64_t i = (int64_t)(tid >> 5) * nbk + bi; i < P; i += nw) {  // warps interleaved over the CTAs
       const int32_t b = A.bucket[i], r = A.rank[i];
       const bool h = r < qs_ld(&A.btake[b]);
       if (lane == 0) {
         A.bidx[i] = h ? 1 : 0;  // reuse: hot flag
         if (h) A.hot[(int64_t)qs_ld(&A.bbase[b]) + r] = (int32_t)i;
-        else A.longl[atomicAdd((int32_t *)&A.counts[6], 1)] = (int32_t)i;  // leftovers (cold lane; any order)
       }
       if (h)
         for (int64_t x = A.off[i] + lane; x < A.off[i + 1]; x += 32)
           if (A.efirst[x]) atomicAdd(&A.nd[A.sk[x]], 1);
     }
   }
-  qs_gsync();
   QS_TS(8);
-  // 11. (block 0) cold lane: the oldest cold_quota leftovers by (arrival, id)
-  const int64_t nh = hot_cap < P ? (hot_cap > 0 ? hot_cap : 0) : P;
-  const int64_t nc = c.cold < P - nh ? c.cold : P - nh;
-  if (nc > 0) {
-    if (b0) qs_cold_lane(A, c, P, nc, sk, sv, scnt, swarp);
-    qs_gsync();
+  if (b0 && nc > 0) {
+    if (!split) __syncthreads();
+    qs_cold_lane(A, c, P, nc, sk, sv, scnt, swarp);
   }
+  qs_gsync();
   QS_TS(9);
   // 12. priorities over the domain (249-251)
   const int32_t ntouch = qs_ld(&A.touched_n[0]);
