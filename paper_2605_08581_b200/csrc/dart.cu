@@ -401,6 +401,12 @@ int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const 
   return PRISM_OK;
 }
 
+// k_propagate's persistent grid: every warp slot of the device (8 CTAs of 256 per SM)
+unsigned prop_blocks(prism_tree *t) {
+  if (!t->sms) cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, t->dev);
+  return (unsigned)(t->sms * (2048 / PROP_TPB));
+}
+
 CoopBufs coop_bufs(prism_tree *t) {
   return CoopBufs{t->ck, t->ck2, t->ks, t->kt, t->cv, t->cv2, t->vs, t->vt, t->cw, t->cw2, t->bmin, t->bmax,
                   t->cst, t->d_prot_ids};
@@ -426,7 +432,7 @@ int build_list(prism_tree *t, int64_t W, const int64_t *dW = nullptr) {
       // keys / subtree maxima / gather at full occupancy over the slot range
       // (each reads hw from the control block; the count lands in cst->cand)
       if (!t->keys_fresh) k_build_keys<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1, dW);
-      k_propagate<<<blocks_for(S), TPB, 0, t->st>>>(t->d, -1, dW);
+      k_propagate<<<prop_blocks(t), PROP_TPB, 0, t->st>>>(t->d, -1, dW);
     }
     t->keys_fresh = 0;  // consumed (the commit mutates the tree next)
     CoopBufs B = coop_bufs(t);
@@ -449,7 +455,7 @@ int build_list(prism_tree *t, int64_t W, const int64_t *dW = nullptr) {
   prof_begin(t);
   CK(cudaMemsetAsync(t->d_count, 0, 2 * sizeof(int64_t), t->st));
   k_build_keys<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw);
-  k_propagate<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw);
+  k_propagate<<<prop_blocks(t), PROP_TPB, 0, t->st>>>(t->d, hw);
   k_gather<<<blocks_for(hw), TPB, 0, t->st>>>(t->d, hw, t->ck, t->cv, t->cw, t->d_count);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(t->h_small, t->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, t->st));
@@ -1009,7 +1015,8 @@ void prism_tree_destroy(prism_tree *t) {
                   t->d_vis_slots, t->d_vis_ids, t->d_poff, t->d_aoffs,  t->d_wtok,    t->d_waoff,
                   t->d_waseg,  t->d_wasnap,  t->d_wakind,  t->d_hits,   t->d_lids,    t->d_lslots,
                   t->d_pm_meta, t->d_pm_chain, t->d_prot_ids, t->ck2, t->cv2, t->cw, t->cw2, t->ks,
-                  t->vs,       t->sel,       t->bmin,      t->bmax};
+                  t->vs,       t->sel,       t->bmin,      t->bmax,      t->kt,       t->vt,
+                  t->cst};
   for (void *p : bufs)
     if (p) cudaFree(p);
   const WaveTmp &X = t->wx;
@@ -1288,7 +1295,7 @@ int prism_set_protection_device(prism_tree *t, const double *d_pri, int32_t nseg
 // two overlap.  The build of the same fused wave picks them up (t->prebuilt).
 static int prebuild_order(prism_tree *t) {
   static_assert(offsetof(CoopState, ts) % 8 == 0, "CoopState clear in 8-byte words");
-  k_propagate<<<blocks_for(t->d.S), TPB, 0, t->st>>>(t->d, -1, nullptr, (unsigned long long *)t->cst,
+  k_propagate<<<prop_blocks(t), PROP_TPB, 0, t->st>>>(t->d, -1, nullptr, (unsigned long long *)t->cst,
                                                      (int64_t)(offsetof(CoopState, ts) / 8));
   CoopBufs B = coop_bufs(t);
   k_ss_sample<EvictCand><<<SS_SAMP / SS_TPB, SS_TPB, 0, t->st>>>(EvictCand{t->d}, B, 1, nullptr,

@@ -847,34 +847,73 @@ __global__ void k_build_keys(DT T, int32_t hw, const int64_t *dW = nullptr) {
 // eff[v] = slot of the maximum key in v's subtree (EFF_BLOCKED if any node of
 // the subtree can never be evicted): each node carries its own value upward
 // until an ancestor already holds something at least as large.
-__global__ void k_propagate(DT T, int32_t hw, const int64_t *dW = nullptr, unsigned long long *clr = nullptr,
-                            int64_t nclr = 0) {
+// Most walks stop after a hop or two, but a freshly touched path is one where
+// every node beats its parent (same access time, larger id), so some walks
+// climb ~40 levels.  One thread per node kept a whole warp -- and its block's
+// SM slot -- waiting on its longest walk, wave after wave of blocks; here a
+// persistent grid of warps owns contiguous slot ranges and every lane whose
+// walk ends takes the next slot of its warp's range at once, so the lanes stay
+// busy and the kernel lasts about one longest walk.  (Ranges claimed from a
+// counter in 128-slot chunks balanced no better and cost more.)
+constexpr int PROP_TPB = 256;
+__global__ void __launch_bounds__(PROP_TPB) k_propagate(DT T, int32_t hw, const int64_t *dW = nullptr,
+                                                        unsigned long long *clr = nullptr, int64_t nclr = 0) {
   // (optionally) clear the selection state for the launches that follow (in
   // place of a memset node in the wave's graph)
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nclr; i += (int64_t)gridDim.x * blockDim.x)
     clr[i] = 0ull;
   if (dW && *dW < 0) return;
   if (hw < 0) hw = T.ctrl->hw;
-  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= hw) return;
-  // k_build_keys left eff[s] = s (evictable so far), EFF_BLOCKED, or EFF_DEAD (root / free)
-  const int32_t e0 = __ldcg(&T.eff[s]);
-  if (e0 == EFF_DEAD) return;
-  const bool blocked = e0 == EFF_BLOCKED;
-  const int32_t val = blocked ? EFF_BLOCKED : s;
-  Key3 kv;
-  if (!blocked) kv = T.kw[s];
-  int32_t p = T.par[s];
-  while (p > 0) {
-    int32_t cur = __ldcg(&T.eff[p]);  // L2-coherent read; CAS only to raise
-    for (;;) {
-      if (cur == EFF_BLOCKED) return;
-      if (!blocked && cur >= 0 && !key_less(T.kw[cur], kv)) return;
-      const int32_t old = atomicCAS(&T.eff[p], cur, val);
-      if (old == cur) break;
-      cur = old;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarp = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t chunk = ((int64_t)hw + nwarp - 1) / nwarp;
+  int64_t next = w * chunk;  // (warp-uniform) the warp's next unclaimed slot
+  const int64_t end = min((int64_t)hw, next + chunk);
+  bool act = false, blocked = false;
+  int32_t val = 0, p = 0;
+  Key3 kv{};
+  for (;;) {
+    const unsigned idle = __ballot_sync(FULL, !act);
+    if (idle && next < end) {  // idle lanes take the next slots of the range
+      if (!act) {
+        const int64_t s = next + __popc(idle & ((1u << lane) - 1u));
+        if (s < end) {
+          // k_build_keys left eff[s] = s (evictable), EFF_BLOCKED or EFF_DEAD (root / free); a
+          // descendant's walk may have raised it since (the node is evictable then)
+          const int32_t e0 = __ldcg(&T.eff[s]);
+          if (e0 != EFF_DEAD) {
+            blocked = e0 == EFF_BLOCKED;
+            val = blocked ? EFF_BLOCKED : (int32_t)s;
+            if (!blocked) kv = T.kw[s];
+            p = T.par[s];
+            act = p > 0;
+          }
+        }
+      }
+      next += __popc(idle);
     }
-    p = T.par[p];
+    if (!__any_sync(FULL, act)) {
+      if (next >= end) break;
+      continue;
+    }
+    if (act) {  // one hop: raise eff[p] to val, or stop
+      int32_t cur = __ldcg(&T.eff[p]);  // L2-coherent read; CAS only to raise
+      const int32_t pp = T.par[p];      // (in flight with it: the next hop needs no load of its own)
+      for (;;) {
+        if (cur == EFF_BLOCKED || (!blocked && cur >= 0 && !key_less(T.kw[cur], kv))) {
+          act = false;
+          break;
+        }
+        const int32_t old = atomicCAS(&T.eff[p], cur, val);
+        if (old == cur) break;
+        cur = old;
+      }
+      if (act) {
+        p = pp;
+        act = p > 0;
+      }
+    }
   }
 }
 
