@@ -753,22 +753,51 @@ __global__ void k_wp_conflicts(DT T, WaveTmp X, WaveCtl *wc) {
     }
 }
 
+// k_vscan_a: each CTA's contiguous partition -- the entries' lengths (one
+// gather pass over the list), their inclusive prefix within the partition
+// into F and the partition's total; k_vscan_c: + the totals of the partitions
+// before it (a streaming add; the gathers are not repeated)
 __global__ void __launch_bounds__(256) k_vscan_a(DT T, WaveTmp X, int64_t *part, const WaveCtl *wc) {
   if (wc->stop || wc->W < 0) return;
+  __shared__ int64_t sw[8];
+  __shared__ int64_t carry;
   const int64_t n = T.ctrl->L_n, per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t b0 = blockIdx.x * per, b1 = b0 + per < n ? b0 + per : n;
   const uint32_t epoch = wc->epoch;
-  int64_t s = 0;
-  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) s += wp_vlen(T, X, i, epoch, true);
-  __shared__ int64_t sw[8];
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t t = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += sw[w];
-    part[blockIdx.x] = t;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  constexpr int U = 4;  // entries per thread per round (their gathers in flight together)
+  for (int64_t t0 = b0; t0 < b1; t0 += U * blockDim.x) {
+    int64_t v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t i = t0 + (int64_t)threadIdx.x * U + u;
+      v[u] = i < b1 ? wp_vlen(T, X, i, epoch, true) : 0;
+    }
+    int64_t x = 0;
+#pragma unroll
+    for (int u = 0; u < U; u++) x += v[u];
+    const int64_t own = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) sw[wid] = x;
+    __syncthreads();
+    int64_t before = carry;
+    for (int w = 0; w < wid; w++) before += sw[w];
+    int64_t run = before + x - own;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t i = t0 + (int64_t)threadIdx.x * U + u;
+      run += v[u];
+      if (i < b1) X.F[i] = run;
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = before + x;
+    __syncthreads();
   }
+  if (threadIdx.x == 0) part[blockIdx.x] = carry;
 }
 
 __global__ void __launch_bounds__(256) k_vscan_c(DT T, WaveTmp X, const int64_t *part, const WaveCtl *wc) {
@@ -777,9 +806,8 @@ __global__ void __launch_bounds__(256) k_vscan_c(DT T, WaveTmp X, const int64_t 
   __shared__ int64_t carry;
   const int64_t n = T.ctrl->L_n, per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t b0 = blockIdx.x * per, b1 = b0 + per < n ? b0 + per : n;
-  const uint32_t epoch = wc->epoch;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  {  // this CTA's carry: the sums of the partitions before it (k_vscan_a), reduced here
+  {  // this CTA's carry: the totals of the partitions before it (k_vscan_a), reduced here
     int64_t x = 0;
     for (int q = threadIdx.x; q < (int)blockIdx.x; q += blockDim.x) x += part[q];
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -792,22 +820,9 @@ __global__ void __launch_bounds__(256) k_vscan_c(DT T, WaveTmp X, const int64_t 
     }
     __syncthreads();
   }
-  for (int64_t t0 = b0; t0 < b1; t0 += blockDim.x) {
-    const int64_t i = t0 + threadIdx.x;
-    int64_t x = i < b1 ? wp_vlen(T, X, i, epoch, false) : 0;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) sw[wid] = x;
-    __syncthreads();
-    int64_t before = carry;
-    for (int w = 0; w < wid; w++) before += sw[w];
-    if (i < b1) X.F[i] = before + x;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = before + x;
-    __syncthreads();
-  }
+  const int64_t c = carry;
+  if (c)
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) X.F[i] += c;
 }
 
 // ------------------------------------------------------------ CapacityError stop (member Bc = j*)
