@@ -957,6 +957,7 @@ __device__ inline int64_t ss_period(int32_t hw) {
 template <class Cand>
 __global__ void __launch_bounds__(SS_TPB) k_ss_sample(Cand cand, CoopBufs B, int64_t W, const int64_t *dW,
                                                       int64_t min_cand) {
+  pdl_wait();
   __shared__ unsigned s_w[32];
   __shared__ unsigned long long s_base;
   if (dW) W = *dW;
@@ -1132,6 +1133,7 @@ constexpr int SS_CL = 8;  // CTAs in k_ss_select's cluster
 template <class Cand>
 __global__ void __cluster_dims__(SS_CL, 1, 1) __launch_bounds__(SS_SEL_TPB)
     k_ss_select(Cand cand, CoopBufs B, int64_t W, const int64_t *dW) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ int s_fail, s_nb;
   cg::cluster_group cluster = cg::this_cluster();
@@ -1186,6 +1188,7 @@ __global__ void __cluster_dims__(SS_CL, 1, 1) __launch_bounds__(SS_SEL_TPB)
 
 template <class Cand>
 __global__ void __launch_bounds__(SS_TPB) k_ss_filter(Cand cand, CoopBufs B) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ unsigned s_w[32];
   __shared__ unsigned long long s_base;
@@ -1257,6 +1260,7 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_filter(Cand cand, CoopBufs B) {
 }
 
 __global__ void __launch_bounds__(SS_TPB) k_ss_scatter(CoopBufs B, int64_t W, const int64_t *dW) {
+  pdl_wait();
   __shared__ unsigned s_off[SS_SPL + 1];
   __shared__ unsigned long long s_tot[32];
   if (dW) W = *dW;
@@ -1323,6 +1327,7 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_scatter(CoopBufs B, int64_t W, co
 
 // the buckets over the CTAs, each sorted in shared memory (block_merge_sort)
 __global__ void __launch_bounds__(SS_TPB) k_ss_sort(CoopBufs B, Key3 *kout, uint64_t *vout) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char dsm[];
   CoopState *st = B.st;
   if (!st->ss_ok) return;
@@ -1384,6 +1389,7 @@ __device__ inline void ss_sort_big_body(const CoopBufs &B, Key3 *kout, uint64_t 
 }
 
 __global__ void __launch_bounds__(512) k_ss_sort_big(CoopBufs B, Key3 *kout, uint64_t *vout) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char dsm[];
   if (!B.st->ss_ok) return;
   ss_sort_big_body(B, kout, vout, dsm);
@@ -1398,6 +1404,7 @@ static_assert(SS_BIG_SMEM <= COOP_SMEM, "k_build_coop sorts the big buckets in i
 // selection (everything when W <= 0) -- one cooperative launch, no host round trip.
 __global__ void __launch_bounds__(COOP_TPB) k_build_coop(DT T, CoopBufs B, int64_t W, const int64_t *dW,
                                                          int64_t min_cand, int64_t small, int32_t sampled) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char dsm[];
   if (dW) {
     W = *dW;
@@ -1470,6 +1477,7 @@ constexpr int TF_SLICE = 256;  // list items per slice of k_tf_local (shared-mem
 constexpr size_t TF_SMEM = 2 * (sizeof(Key3) + 8) * TF_SLICE;
 
 __global__ void __launch_bounds__(SS_TPB) k_tf_scan(ProtCand cand, CoopBufs B) {
+  pdl_wait();
   __shared__ unsigned s_w[32];
   __shared__ unsigned long long s_base;
   const int32_t hw = cand.hw();
@@ -1596,6 +1604,7 @@ constexpr size_t TF_LOCAL_SMEM =
 
 __global__ void __cluster_dims__(TF_CL, 1, 1) __launch_bounds__(SS_TPB)
     k_tf_local(DT T, CoopBufs B, int64_t f, int32_t keys) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ Key3 rk[2][TF_MAX];
   __shared__ uint64_t rv[2][TF_MAX];
@@ -1757,6 +1766,7 @@ __global__ void __cluster_dims__(TF_CL, 1, 1) __launch_bounds__(SS_TPB)
 // or -1, id) -- from the small top-f / sample select when it succeeded, else materialised
 __global__ void __launch_bounds__(COOP_TPB) k_protect_coop(DT T, CoopBufs B, int64_t f, int64_t min_cand,
                                                            int64_t small, int32_t sampled, int32_t keys) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ Key3 smin[COOP_TPB + 1], smax[COOP_TPB + 1];
   if (sampled && B.st->tf_done) return;  // the small top-f path already protected

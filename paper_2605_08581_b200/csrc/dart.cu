@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/prism.h"
+#include "pdl.cuh"
 #include "dart_kernels.cuh"
 #include "select.cuh"
 #include "wave_par.cuh"
@@ -1825,6 +1826,7 @@ int prism_profile_read(prism_tree *t, double *out) {
 
 namespace {
 __global__ void k_kv_init_stack(int32_t *stack, int64_t rows) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < rows) stack[i] = (int32_t)(rows - 1 - i);  // pops hand out rows 0, 1, 2, ...
 }

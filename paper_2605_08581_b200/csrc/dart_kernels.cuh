@@ -123,6 +123,7 @@ __device__ inline WalkOut warp_walk(const DT &T, const uint32_t *p, int64_t n, i
 __global__ void k_prematch(DT T, int64_t B, const int64_t *__restrict__ poff,
                            const uint32_t *__restrict__ tok, int32_t *__restrict__ pm_meta,
                            int32_t *__restrict__ pm_chain, const int32_t *abort = nullptr) {
+  pdl_wait();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= B || (abort && *abort)) return;
   const int64_t b = poff[w], n = poff[w + 1] - b;
@@ -443,6 +444,7 @@ __device__ inline int32_t lower_bound_i32(const int32_t *a, int32_t n, int32_t x
 }
 
 __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t *sp = reinterpret_cast<uint32_t *>(smem);
   int32_t *Ps = reinterpret_cast<int32_t *>(sp + MAX_PATH);
@@ -831,6 +833,7 @@ __global__ void __launch_bounds__(32) k_commit(DT T, CommitArgs A) {
 
 // (hw < 0: read the high-water mark from the control block -- no host sync)
 __global__ void k_build_keys(DT T, int32_t hw, const int64_t *dW = nullptr) {
+  pdl_wait();
   if (dW && *dW < 0) return;  // device-side control: no eviction this wave
   if (hw < 0) hw = T.ctrl->hw;
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -858,6 +861,7 @@ __global__ void k_build_keys(DT T, int32_t hw, const int64_t *dW = nullptr) {
 constexpr int PROP_TPB = 256;
 __global__ void __launch_bounds__(PROP_TPB) k_propagate(DT T, int32_t hw, const int64_t *dW = nullptr,
                                                         unsigned long long *clr = nullptr, int64_t nclr = 0) {
+  pdl_wait();
   // (optionally) clear the selection state for the launches that follow (in
   // place of a memset node in the wave's graph)
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nclr; i += (int64_t)gridDim.x * blockDim.x)
@@ -919,6 +923,7 @@ __global__ void __launch_bounds__(PROP_TPB) k_propagate(DT T, int32_t hw, const 
 
 __global__ void k_gather(DT T, int32_t hw, Key3 *__restrict__ ck, uint64_t *__restrict__ cv,
                          int64_t *__restrict__ cw, int64_t *__restrict__ count) {
+  pdl_wait();
   if (hw < 0) hw = T.ctrl->hw;
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   bool take = false;
@@ -944,6 +949,7 @@ __global__ void k_gather(DT T, int32_t hw, Key3 *__restrict__ ck, uint64_t *__re
 
 // the sorted list is ready: n entries out of `total` candidates
 __global__ void k_list_ready(DT T, int64_t n, int64_t total) {
+  pdl_wait();
   Ctrl *c = T.ctrl;
   c->L_n = n;
   c->L_partial = n < total ? 1 : 0;
@@ -958,6 +964,7 @@ __global__ void k_list_ready(DT T, int64_t n, int64_t total) {
 // set_protection sort key (kvcache.py:375-381): (-P-hat, segment or -1, node_id)
 __global__ void k_prot_gather(DT T, int32_t hw, Key3 *__restrict__ ck, uint64_t *__restrict__ cv,
                               int64_t *__restrict__ cw, int64_t *__restrict__ count) {
+  pdl_wait();
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   bool take = false;
   if (s < hw && s != ROOT) take = T.nid[s] >= 0 && T.par[s] >= 0 && T.hasanc[s] && T.akind[s] == K_REUSABLE;
@@ -983,12 +990,14 @@ __global__ void k_prot_gather(DT T, int32_t hw, Key3 *__restrict__ ck, uint64_t 
 }
 
 __global__ void k_prot_clear(DT T, int32_t hw) {
+  pdl_wait();
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s < hw) T.prot[s] = 0;
 }
 
 __global__ void k_prot_set(DT T, const uint64_t *__restrict__ sorted_v, int64_t f,
                            int64_t *__restrict__ out_ids) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= f) return;
   const int32_t s = (int32_t)(sorted_v[i] & 0xffffffffu);
@@ -999,6 +1008,7 @@ __global__ void k_prot_set(DT T, const uint64_t *__restrict__ sorted_v, int64_t 
 // note_active_segments (kvcache.py:385-393): rewrite the a-bit of every
 // reusable anchor's counter snapshot
 __global__ void k_note_active(DT T, int32_t hw) {
+  pdl_wait();
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= hw || s == ROOT || T.nid[s] < 0 || T.par[s] < 0) return;
   if (!T.hasanc[s] || T.akind[s] != K_REUSABLE) return;
@@ -1008,6 +1018,7 @@ __global__ void k_note_active(DT T, int32_t hw) {
 
 __global__ void k_active_flags(DT T, const int32_t *__restrict__ a, const int32_t *__restrict__ nd,
                                int32_t nseg) {
+  pdl_wait();
   const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < nseg) T.act[r] = (a[r] > 0 || nd[r] > 0) ? 1 : 0;
 }
@@ -1018,6 +1029,7 @@ __global__ void k_active_flags(DT T, const int32_t *__restrict__ a, const int32_
 // invalid one (status written to out[0] = index of failure or -1)
 __global__ void k_release_seq(DT T, int64_t n, const int32_t *__restrict__ slots,
                               const int64_t *__restrict__ ids, int64_t *out) {
+  pdl_wait();
   if (threadIdx.x != 0) return;
   const int32_t hw = T.ctrl->hw;
   for (int64_t i = 0; i < n; i++) {
@@ -1039,6 +1051,7 @@ __global__ void k_release_seq(DT T, int64_t n, const int32_t *__restrict__ slots
 // same node (the shared upper levels: system prompt, popular segments, the
 // root) release it with one combined atomic
 __global__ void k_release_par(DT T, int64_t n, const int32_t *__restrict__ slots) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   int32_t x = i < n ? slots[i] : -1;
@@ -1052,6 +1065,7 @@ __global__ void k_release_par(DT T, int64_t n, const int32_t *__restrict__ slots
 // the inverse: +1 along each leaf's root chain (an explicit lock of a cached
 // prefix, e.g. the SGLang-style adapter's inc_lock_ref)
 __global__ void k_pin_par(DT T, int64_t n, const int32_t *__restrict__ slots) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   int32_t x = i < n ? slots[i] : -1;
@@ -1065,6 +1079,7 @@ __global__ void k_pin_par(DT T, int64_t n, const int32_t *__restrict__ slots) {
 // ------------------------------------------------------------ maintenance
 
 __global__ void k_rehash(DT T, int32_t hw, int64_t *live) {
+  pdl_wait();
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= hw || s == ROOT || T.nid[s] < 0 || T.par[s] < 0) return;
   const uint64_t key = ckey(T.par[s], T.ftok[s]);
@@ -1083,6 +1098,7 @@ __global__ void k_rehash(DT T, int32_t hw, int64_t *live) {
 }
 
 __global__ void k_compact_len(DT T, int32_t hw, int64_t *__restrict__ len) {
+  pdl_wait();
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= hw) return;
   len[s] = (s != ROOT && T.nid[s] >= 0 && T.par[s] >= 0) ? T.elen[s] : 0;
@@ -1090,6 +1106,7 @@ __global__ void k_compact_len(DT T, int32_t hw, int64_t *__restrict__ len) {
 
 __global__ void k_compact_copy(DT T, int32_t hw, const int64_t *__restrict__ newoff,
                                uint32_t *__restrict__ dst) {
+  pdl_wait();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= hw) return;
   const int32_t s = (int32_t)w;
@@ -1102,6 +1119,7 @@ __global__ void k_compact_copy(DT T, int32_t hw, const int64_t *__restrict__ new
 }
 
 __global__ void k_key_of(DT T, int32_t s, Key3 *out) {
+  pdl_wait();
   if (threadIdx.x == 0) *out = make_key(T, s);
 }
 

@@ -43,6 +43,7 @@ struct KvDev {
 // one sync's sizes from the tree's control block (no host round trip): new
 // arena tokens since the arena mark, victim records since the log mark
 __global__ void k_kv_prep(KvDev K, const Ctrl *C, int64_t vcap) {
+  pdl_wait();
   const int64_t n_new = C->arena_top - K.ctl[0], nrec = C->vlog_count - K.ctl[1];
   const bool bad = n_new < 0 || n_new > *K.top || nrec > vcap;
   K.ctl[2] = bad ? 0 : n_new;
@@ -53,6 +54,7 @@ __global__ void k_kv_prep(KvDev K, const Ctrl *C, int64_t vcap) {
 
 // the marks advance, the free-row count and the traffic counters update
 __global__ void k_kv_fin(KvDev K, const Ctrl *C, int32_t copy_in, int32_t copy_out) {
+  pdl_wait();
   const int64_t n_new = K.ctl[2], freed = K.ctl[4];
   *K.top += freed - n_new;
   K.moved[0] += n_new;
@@ -87,6 +89,7 @@ struct VecIt {
 // newly resident arena tokens [a0, a0 + n): pop rows (stack top - 1 - i) in
 // arena order, optionally copy the payload in (src row i = arena token a0 + i)
 __global__ void k_kv_alloc(KvDev K, const uint8_t *__restrict__ src) {
+  pdl_wait();
   const int64_t top = *K.top, a0 = K.ctl[0], n = K.ctl[2];  // (k_kv_fin moves top after every reader)
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = t0; i < n; i += gs) K.kvx[a0 + i] = K.stack[top - 1 - i];
@@ -123,6 +126,7 @@ __global__ void k_kv_alloc(KvDev K, const uint8_t *__restrict__ src) {
 // out (dst row = voff[r] + i).  voff: exclusive prefix of the records' lengths.
 __global__ void k_kv_free(KvDev K, const VRec *__restrict__ vlog, int64_t vcap, const int64_t *__restrict__ voff,
                           uint8_t *__restrict__ dst) {
+  pdl_wait();
   const int64_t top = *K.top - K.ctl[2];  // (the rows k_kv_alloc popped are gone; k_kv_fin moves top)
   const int64_t v0 = K.ctl[1], nrec = K.ctl[3];
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -175,6 +179,7 @@ __device__ __forceinline__ int64_t kv_block_sum(int64_t x, int64_t *s_w) {
 }
 
 __global__ void __launch_bounds__(1024) k_kv_vsum(const VRec *__restrict__ vlog, int64_t vcap, int64_t *part, KvDev K) {
+  pdl_wait();
   __shared__ int64_t s_w[32];
   const int64_t v0 = K.ctl[1];
   int64_t r0, r1, x = 0;
@@ -186,6 +191,7 @@ __global__ void __launch_bounds__(1024) k_kv_vsum(const VRec *__restrict__ vlog,
 
 __global__ void __launch_bounds__(1024) k_kv_vfill(const VRec *__restrict__ vlog, int64_t vcap, int64_t *voff,
                                                    const int64_t *__restrict__ part, KvDev K) {
+  pdl_wait();
   __shared__ int64_t s_w[32];
   __shared__ int64_t s_carry;
   const int64_t v0 = K.ctl[1], nrec = K.ctl[3];
@@ -228,6 +234,7 @@ __global__ void __launch_bounds__(1024) k_kv_vfill(const VRec *__restrict__ vlog
 // arena compaction: the shadow rows follow their spans (same new offsets as k_compact_copy)
 __global__ void k_kv_compact(DT T, int32_t hw, const int64_t *__restrict__ newoff, const int32_t *__restrict__ src,
                              int32_t *__restrict__ dst) {
+  pdl_wait();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= hw) return;
   const int32_t s = (int32_t)w;
@@ -244,6 +251,7 @@ __global__ void k_kv_compact(DT T, int32_t hw, const int64_t *__restrict__ newof
 // rows themselves into out[j, p]
 __global__ void k_kv_gather(DT T, KvDev K, int64_t n, const int32_t *__restrict__ leaves, int64_t max_len,
                             int32_t *__restrict__ table, uint8_t *__restrict__ out, int64_t *__restrict__ lens) {
+  pdl_wait();
   const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (j >= n) return;

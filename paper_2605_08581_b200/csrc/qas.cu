@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "../../include/prism.h"
+#include "pdl.cuh"
 #include "qas_small.cuh"
 #include "scan.cuh"
 #include "select.cuh"
@@ -82,6 +83,7 @@ __device__ inline double pri0(const QCfg &c, const int32_t *g, const int32_t *a,
 // count_segments: each request contributes once per distinct segment
 __global__ void q_count(int64_t P, const int64_t *__restrict__ off, const int32_t *__restrict__ sk,
                         int32_t *__restrict__ cnt, const int64_t *__restrict__ subset) {
+  pdl_wait();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= P) return;
   const int64_t i = subset ? subset[t] : t;
@@ -107,6 +109,7 @@ __global__ void q_align(int64_t P, const int64_t *__restrict__ off, const int32_
                         int32_t *__restrict__ sig, int32_t *__restrict__ siglen,
                         uint32_t *__restrict__ sighash, int32_t *__restrict__ nlong,
                         int32_t *__restrict__ longl) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   const int64_t b = off[i];
@@ -178,6 +181,7 @@ __global__ void q_align_long(const int32_t *__restrict__ nlong, const int32_t *_
                              const int32_t *__restrict__ a, QCfg c, int32_t *__restrict__ aligned,
                              int32_t *__restrict__ sig, int32_t *__restrict__ siglen,
                              uint32_t *__restrict__ sighash, int32_t *__restrict__ rk) {
+  pdl_wait();
   const int n = *nlong;
   for (int t = blockIdx.x; t < n; t += gridDim.x) {
     const int64_t i = longl[t];
@@ -205,6 +209,7 @@ __device__ inline bool sig_eq(const int32_t *sig, const int32_t *siglen, int64_t
 __global__ void q_bucket_insert(int64_t P, const int32_t *__restrict__ sig, const int32_t *__restrict__ siglen,
                                 const uint32_t *__restrict__ sighash, int64_t kappa, uint64_t *tkey,
                                 int32_t *tmin, uint64_t tmask, int32_t *__restrict__ slot_of) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   const uint32_t h = sighash[i];
@@ -228,6 +233,7 @@ __global__ void q_bucket_insert(int64_t P, const int32_t *__restrict__ sig, cons
 
 __global__ void q_bucket_list(int64_t T, const uint64_t *__restrict__ tkey, const int32_t *__restrict__ tmin,
                               int32_t *__restrict__ bmin, int32_t *__restrict__ bslot, int64_t *count) {
+  pdl_wait();
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= T || tkey[p] == QEMPTY) return;
   const int64_t pos = (int64_t)atomicAdd((unsigned long long *)count, 1ull);
@@ -236,12 +242,14 @@ __global__ void q_bucket_list(int64_t T, const uint64_t *__restrict__ tkey, cons
 }
 
 __global__ void q_bucket_index(int64_t nb, const int32_t *__restrict__ sorted_slot, int32_t *__restrict__ bidx_of_slot) {
+  pdl_wait();
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q < nb) bidx_of_slot[sorted_slot[q]] = (int32_t)q;
 }
 
 __global__ void q_bucket_of(int64_t P, const int32_t *__restrict__ slot_of, const int32_t *__restrict__ bidx_of_slot,
                             int32_t *__restrict__ bucket, int32_t *__restrict__ iota) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   bucket[i] = bidx_of_slot[slot_of[i]];
@@ -251,6 +259,7 @@ __global__ void q_bucket_of(int64_t P, const int32_t *__restrict__ slot_of, cons
 // sorted (bucket, index) -> bucket start / rank inside bucket
 __global__ void q_rank(int64_t P, const int32_t *__restrict__ sb, const int32_t *__restrict__ si,
                        int32_t *__restrict__ bstart, int32_t *__restrict__ bend) {
+  pdl_wait();
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= P) return;
   if (q == 0 || sb[q] != sb[q - 1]) bstart[sb[q]] = (int32_t)q;
@@ -259,6 +268,7 @@ __global__ void q_rank(int64_t P, const int32_t *__restrict__ sb, const int32_t 
 
 __global__ void q_rank2(int64_t P, const int32_t *__restrict__ sb, const int32_t *__restrict__ si,
                         const int32_t *__restrict__ bstart, int32_t *__restrict__ rank) {
+  pdl_wait();
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= P) return;
   rank[si[q]] = (int32_t)q - bstart[sb[q]];
@@ -266,6 +276,7 @@ __global__ void q_rank2(int64_t P, const int32_t *__restrict__ sb, const int32_t
 
 __global__ void q_pair_count(int64_t P, const int64_t *__restrict__ off, const int32_t *__restrict__ sk,
                              int64_t *__restrict__ cnt) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   const int64_t b = off[i], e = off[i + 1];
@@ -283,6 +294,7 @@ __global__ void q_pair_emit(int64_t P, const int64_t *__restrict__ off, const in
                             const int32_t *__restrict__ bucket, const int32_t *__restrict__ rank,
                             int64_t hot_cap, const int64_t *__restrict__ pos0, uint64_t *__restrict__ pk,
                             int32_t *__restrict__ pv) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   const int64_t b = off[i], e = off[i + 1];
@@ -299,6 +311,7 @@ __global__ void q_pair_emit(int64_t P, const int64_t *__restrict__ off, const in
 }
 
 __global__ void q_heads(int64_t E, const uint64_t *__restrict__ pk, int32_t *__restrict__ head) {
+  pdl_wait();
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q < E) head[q] = (q == 0 || pk[q] != pk[q - 1]) ? 1 : 0;
 }
@@ -308,6 +321,7 @@ __global__ void q_terms(int64_t E, const uint64_t *__restrict__ pk, const int32_
                         const int32_t *__restrict__ hpos, const int32_t *__restrict__ prov_pref,
                         const int32_t *__restrict__ g, const int32_t *__restrict__ a, QCfg c,
                         int32_t *__restrict__ hstart, double *__restrict__ term, int32_t *__restrict__ hbucket) {
+  pdl_wait();
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= E || !head[q]) return;
   const int32_t j = hpos[q];
@@ -325,6 +339,7 @@ __global__ void q_terms(int64_t E, const uint64_t *__restrict__ pk, const int32_
 
 __global__ void q_bucket_range(int64_t NH, const int32_t *__restrict__ hbucket, int32_t *__restrict__ hb0,
                                int32_t *__restrict__ hb1) {
+  pdl_wait();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= NH) return;
   if (j == 0 || hbucket[j] != hbucket[j - 1]) hb0[hbucket[j]] = (int32_t)j;
@@ -338,6 +353,7 @@ __global__ void q_score(int64_t nb, const int32_t *__restrict__ hb0, const int32
                         const double *__restrict__ term, const int32_t *__restrict__ bstart,
                         const int32_t *__restrict__ bend, QCfg c, double *__restrict__ score,
                         uint64_t *__restrict__ skey, int32_t *__restrict__ sval) {
+  pdl_wait();
   const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (b >= nb) return;
@@ -374,6 +390,7 @@ __global__ void q_score(int64_t nb, const int32_t *__restrict__ hb0, const int32
 
 __global__ void q_sizes_sorted(int64_t nb, const int32_t *__restrict__ order, const int32_t *__restrict__ bstart,
                                const int32_t *__restrict__ bend, int64_t *__restrict__ sz) {
+  pdl_wait();
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q < nb) sz[q] = bend[order[q]] - bstart[order[q]];
 }
@@ -381,6 +398,7 @@ __global__ void q_sizes_sorted(int64_t nb, const int32_t *__restrict__ order, co
 __global__ void q_take(int64_t nb, const int32_t *__restrict__ order, const int64_t *__restrict__ pre,
                        const int64_t *__restrict__ sz, int64_t hot_cap, int64_t *__restrict__ take,
                        int64_t *__restrict__ base) {
+  pdl_wait();
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nb) return;
   const int32_t b = order[q];
@@ -393,6 +411,7 @@ __global__ void q_take(int64_t nb, const int32_t *__restrict__ order, const int6
 __global__ void q_hot(int64_t P, const int32_t *__restrict__ bucket, const int32_t *__restrict__ rank,
                       const int64_t *__restrict__ take, const int64_t *__restrict__ base, int64_t *__restrict__ hot,
                       uint8_t *__restrict__ sel) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   const int32_t b = bucket[i];
@@ -405,6 +424,7 @@ __global__ void q_hot(int64_t P, const int32_t *__restrict__ bucket, const int32
 __global__ void q_cold_keys(int64_t P, const uint8_t *__restrict__ sel, const double *__restrict__ arrival,
                             const int64_t *__restrict__ ids, K3 *__restrict__ k, int64_t *__restrict__ v,
                             int64_t *__restrict__ w) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   K3 x;
@@ -419,6 +439,7 @@ __global__ void q_cold_keys(int64_t P, const uint8_t *__restrict__ sel, const do
 // count_segments (scheduler.py:83-89) of a pending CSR into dense G: one thread
 // per request, each distinct segment once
 __global__ void q_demand(int64_t P, const int64_t *__restrict__ off, const int32_t *__restrict__ sk, int32_t *G) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   const int64_t b = off[i], e = off[i + 1];
@@ -432,6 +453,7 @@ __global__ void q_demand(int64_t P, const int64_t *__restrict__ off, const int32
 
 __global__ void q_prio(int32_t nseg, const int32_t *__restrict__ g, const int32_t *__restrict__ a,
                        const int32_t *__restrict__ nd, QCfg c, double *__restrict__ prio, uint8_t *__restrict__ dom) {
+  pdl_wait();
   const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nseg) return;
   const bool in = g[r] > 0 || a[r] > 0 || nd[r] > 0;
@@ -597,6 +619,7 @@ struct prism_qas {
   int64_t gtick = 0;
   int32_t use_graph = 1;
   int64_t graph_captures = 0, graph_replays = 0;
+  int64_t pdl_edges = 0;  // programmatic kernel -> kernel edges of the last captured wave
   int64_t *hres = nullptr;  // pinned: the fused wave's stage results
   int64_t *hout_mem = nullptr, *hout_hit = nullptr;  // pinned: a wave's dispatch order and hits
   int64_t hout_cap = 0;
@@ -1174,6 +1197,7 @@ __global__ void q_stage(int64_t P, const int64_t *__restrict__ ids, const double
                         double *__restrict__ garr, int64_t *__restrict__ goff, int32_t *__restrict__ gsk,
                         uint8_t *__restrict__ greo, int32_t *__restrict__ gsfx, int64_t skcap, int32_t *abort,
                         int64_t *__restrict__ qcounts, int32_t *__restrict__ err0) {
+  pdl_wait();
   const int64_t nsk = off[P];
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = gt; i <= P; i += gs) {
@@ -1202,6 +1226,7 @@ __global__ void q_results(const int64_t *__restrict__ qcounts, const int64_t *__
                           const int32_t *__restrict__ err, int64_t *hres, int64_t B,
                           const int64_t *__restrict__ members, const int64_t *__restrict__ hits, int64_t *hm,
                           int64_t *hh) {
+  pdl_wait();
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
   if (gt == 0) {
     hres[0] = qcounts[2];
@@ -1226,6 +1251,7 @@ __global__ void q_members_len(int64_t nh, int64_t nc, const int64_t *__restrict_
                               const int64_t *__restrict__ off, const int32_t *__restrict__ suffix, int64_t sys,
                               int64_t chunk, int64_t *__restrict__ members, int64_t *__restrict__ plen,
                               int64_t *__restrict__ alen, int32_t *err, const int64_t *redo = nullptr) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nh + nc) return;
   if (redo && *redo) return;  // the one-launch round overflowed: no dispatch order to read (redone)
@@ -1242,6 +1268,7 @@ __global__ void q_members_len(int64_t nh, int64_t nc, const int64_t *__restrict_
 __global__ void __launch_bounds__(1024) q_scan2(int64_t B, const int64_t *__restrict__ plen,
                                                 const int64_t *__restrict__ alen, int64_t *__restrict__ poff,
                                                 int64_t *__restrict__ aoffs, int64_t *__restrict__ tot) {
+  pdl_wait();
   prism::block_scan4<2, 8>(
       B + 1, [&](int a, int64_t i) -> int64_t { return i >= B ? 0 : (a == 0 ? plen[i] : alen[i]); },
       [&](int a, int64_t i, int64_t ex, int64_t) {
@@ -1261,6 +1288,7 @@ __global__ void __launch_bounds__(1024) q_members_scan(int64_t nh, int64_t nc, c
                                                        int64_t *__restrict__ aoffs, int64_t *__restrict__ tot,
                                                        const int64_t *__restrict__ qcounts, int64_t tok_cap,
                                                        int64_t anc_cap, int32_t *err, int32_t *abort) {
+  pdl_wait();
   const int64_t B = nh + nc;
   if (qcounts[3]) {  // the one-launch round overflowed its buffers: no dispatch order (uniform)
     if (threadIdx.x == 0) {
@@ -1303,6 +1331,7 @@ __global__ void q_serialize(int64_t B, const int64_t *__restrict__ members, cons
                             int32_t *__restrict__ a_off, int8_t *__restrict__ a_kind, int32_t *__restrict__ a_seg,
                             int32_t *__restrict__ a_snap, int32_t *__restrict__ err,
                             const int32_t *abort = nullptr) {
+  pdl_wait();
   if (abort && *abort) return;  // (the fused wave's stage failed: sizes may exceed the buffers)
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -1451,6 +1480,52 @@ namespace {
 // into fixed buffers first.  *handled = false: the stage failed on the device
 // (buffers too small, the one-launch round overflowed, layout check) and
 // nothing was committed -- the caller runs the regular path.
+// Kernel -> kernel edges of a captured wave become programmatic (pdl.cuh): the
+// downstream kernel's CTAs launch once every upstream CTA has begun and wait
+// in pdl_wait() for its completion, so no edge pays a launch latency.  Not
+// into cooperative kernels (their grid needs the whole device at once) nor
+// into or out of library (CUB) kernels, which do not wait.  PRISM_NO_PDL=1
+// keeps plain edges (A/B measurement).
+static int graph_pdl(cudaGraph_t g, int64_t *nconv) {
+  *nconv = 0;
+  static const bool off = getenv("PRISM_NO_PDL") != nullptr;
+  if (off) return 0;
+  size_t ne = 0;
+  if (cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &ne) != cudaSuccess) return -1;
+  std::vector<cudaGraphNode_t> from(ne), to(ne);
+  std::vector<cudaGraphEdgeData> ed(ne);
+  if (cudaGraphGetEdges_v2(g, from.data(), to.data(), ed.data(), &ne) != cudaSuccess) return -1;
+  auto ours = [](cudaGraphNode_t n, bool down) -> bool {
+    cudaGraphNodeType ty;
+    if (cudaGraphNodeGetType(n, &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) return false;
+    cudaKernelNodeParams p;
+    if (cudaGraphKernelNodeGetParams(n, &p) != cudaSuccess) return false;
+    const char *name = nullptr;
+    if (cudaFuncGetName(&name, p.func) != cudaSuccess || !name) return false;
+    if (strstr(name, "cub") || strstr(name, "thrust")) return false;
+    if (down) {
+      cudaLaunchAttributeValue v{};
+      if (cudaGraphKernelNodeGetAttribute(n, cudaLaunchAttributeCooperative, &v) != cudaSuccess || v.cooperative)
+        return false;
+    }
+    return true;
+  };
+  for (size_t e = 0; e < ne; e++) {
+    if (ed[e].type != cudaGraphDependencyTypeDefault || ed[e].from_port != 0) continue;
+    if (!ours(from[e], false) || !ours(to[e], true)) continue;
+    cudaGraphEdgeData nd{};
+    nd.from_port = cudaGraphKernelNodePortProgrammatic;  // (no early trigger: when every upstream CTA has exited)
+    nd.type = cudaGraphDependencyTypeProgrammatic;
+    if (cudaGraphRemoveDependencies_v2(g, &from[e], &to[e], &ed[e], 1) != cudaSuccess) return -1;
+    if (cudaGraphAddDependencies_v2(g, &from[e], &to[e], &nd, 1) != cudaSuccess) {
+      cudaGetLastError();
+      return cudaGraphAddDependencies_v2(g, &from[e], &to[e], &ed[e], 1) == cudaSuccess ? 0 : -1;  // (as it was)
+    }
+    (*nconv)++;
+  }
+  return 0;
+}
+
 int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, const double *arrival,
                     const int64_t *sk_off, const int32_t *sk, const uint8_t *reorderable, const int32_t *suffix,
                     int32_t nseg, const QCfg &c, int64_t sys_len, int64_t chunk, int64_t *members_out, int64_t *hits,
@@ -1608,6 +1683,10 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
       cudaGraphNodeType ty;
       QCK(cudaGraphNodeGetType(nd, &ty));
       slot->kernels += ty == cudaGraphNodeTypeKernel ? 1 : 0;
+    }
+    if (graph_pdl(g, &q->pdl_edges)) {
+      cudaGraphDestroy(g);
+      return qfail(PRISM_CUDA, "wave capture: programmatic edges");
     }
     QCK(cudaGraphInstantiate(&slot->exec, g, 0));
     cudaGraphDestroy(g);
@@ -1847,10 +1926,12 @@ int prism_qas_tune(prism_qas *q, int32_t key, int64_t value, int64_t *out) {
     case 4:  // the fused wave's tail as a CUDA graph (1, default) or plain launches (0)
       q->use_graph = value ? 1 : 0;
       return PRISM_OK;
-    case 5:  // read-only: graph captures, graph replays
+    case 5:  // read-only: graph captures, graph replays (out[2]: programmatic edges of the last capture, when
+             // the caller passes room for it through value = 3)
       if (out) {
         out[0] = q->graph_captures;
         out[1] = q->graph_replays;
+        if (value >= 3) out[2] = q->pdl_edges;
       }
       return PRISM_OK;
     default:

@@ -598,6 +598,7 @@ __device__ inline void qs_cold_lane(const QsArgs &A, const QsCfg &c, int64_t P, 
 // short serial phases (bucket order + in-bucket ranks, score sort + hot-lane
 // prefix, cold lane) in block 0's shared memory.
 __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char qs_smem[];
   QKey *sk = reinterpret_cast<QKey *>(qs_smem);
   int32_t *sv = reinterpret_cast<int32_t *>(sk + QS_MAXP);

@@ -61,6 +61,7 @@ __device__ inline int key_highbit(const Key3 &x) {  // highest set bit of a 192-
 // per-block min and max of U
 static __global__ void k_sel_minmax(const Key3 *__restrict__ k, const SelState *st, Key3 *__restrict__ bmin,
                              Key3 *__restrict__ bmax) {
+  pdl_wait();
   __shared__ Key3 smin[SEL_TPB], smax[SEL_TPB];
   const int64_t n = st->done ? 0 : st->nU;
   Key3 lo = {~0ull, ~0ull, ~0ull}, hi = {0, 0, 0};
@@ -87,6 +88,7 @@ static __global__ void k_sel_minmax(const Key3 *__restrict__ k, const SelState *
 
 // digit position from the global min/max; clears the histogram
 static __global__ void k_sel_digit(SelState *st, const Key3 *__restrict__ bmin, const Key3 *__restrict__ bmax, int nb) {
+  pdl_wait();
   __shared__ Key3 smin[SEL_TPB], smax[SEL_TPB];
   Key3 lo = {~0ull, ~0ull, ~0ull}, hi = {0, 0, 0};
   for (int i = threadIdx.x; i < nb; i += blockDim.x) {
@@ -116,6 +118,7 @@ static __global__ void k_sel_digit(SelState *st, const Key3 *__restrict__ bmin, 
 }
 
 static __global__ void k_sel_hist(const Key3 *__restrict__ k, const int64_t *__restrict__ w, SelState *st) {
+  pdl_wait();
   __shared__ unsigned long long hn[256];
   __shared__ long long hw[256];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
@@ -150,6 +153,7 @@ static __global__ void k_sel_hist(const Key3 *__restrict__ k, const int64_t *__r
 
 // one warp: inclusive scan of the 256 bucket weights, first bucket reaching need
 static __global__ void k_sel_pick(SelState *st) {
+  pdl_wait();
   if (st->done) return;
   const int lane = threadIdx.x & 31;
   if (st->take_all) {  // single key / forced
@@ -197,6 +201,7 @@ static __global__ void k_sel_pick(SelState *st) {
 static __global__ void k_sel_split(const Key3 *__restrict__ kU, const uint64_t *__restrict__ vU, const int64_t *__restrict__ wU,
                             Key3 *__restrict__ kN, uint64_t *__restrict__ vN, int64_t *__restrict__ wN,
                             Key3 *__restrict__ kS, uint64_t *__restrict__ vS, SelState *st) {
+  pdl_wait();
   const int64_t n = st->done ? 0 : st->nU;
   const int shift = st->shift, dstar = st->dstar, all = st->take_all;
   const int lane = threadIdx.x & 31;
@@ -233,6 +238,7 @@ static __global__ void k_sel_split(const Key3 *__restrict__ kU, const uint64_t *
 }
 
 static __global__ void k_sel_next(SelState *st) {
+  pdl_wait();
   if (threadIdx.x != 0 || st->done) return;
   st->rounds++;
   if (st->take_all || st->nUn == 0) {
@@ -248,6 +254,7 @@ static __global__ void k_sel_next(SelState *st) {
 // after the rounds: if not done (pathological), move the remaining U into SEL
 static __global__ void k_sel_flush(const Key3 *__restrict__ kU, const uint64_t *__restrict__ vU, Key3 *__restrict__ kS,
                             uint64_t *__restrict__ vS, SelState *st) {
+  pdl_wait();
   if (st->done) return;
   const int64_t n = st->nU, base = st->nSel;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -261,6 +268,7 @@ static __global__ void k_sel_flush(const Key3 *__restrict__ kU, const uint64_t *
 // preserves the order, and the remaining bits usually fit 64 (class, a few
 // priority bits, the tick range, the id range, the depth).
 static __global__ void k_key_mask(const Key3 *__restrict__ k, int64_t n, unsigned long long *mask) {
+  pdl_wait();
   __shared__ unsigned long long s0[SEL_TPB], s1[SEL_TPB], s2[SEL_TPB];
   const Key3 r = k[0];
   unsigned long long m0 = 0, m1 = 0, m2 = 0;
@@ -300,6 +308,7 @@ __device__ inline uint64_t pext64(uint64_t acc, uint64_t x, uint64_t m) {
 
 static __global__ void k_key_compress(const Key3 *__restrict__ k, int64_t n, Key3 mask, uint64_t *__restrict__ out,
                                uint64_t *__restrict__ idx) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const Key3 x = k[i];
@@ -313,6 +322,7 @@ static __global__ void k_key_compress(const Key3 *__restrict__ k, int64_t n, Key
 static __global__ void k_key_gather(const Key3 *__restrict__ kin, const uint64_t *__restrict__ vin,
                              const uint64_t *__restrict__ order, int64_t n, Key3 *__restrict__ kout,
                              uint64_t *__restrict__ vout) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint64_t j = order[i];
@@ -321,6 +331,7 @@ static __global__ void k_key_gather(const Key3 *__restrict__ kin, const uint64_t
 }
 
 static __global__ void k_sel_flush_done(SelState *st) {
+  pdl_wait();
   if (threadIdx.x == 0 && !st->done) {
     st->nSel += st->nU;
     st->done = 1;
@@ -331,6 +342,7 @@ static __global__ void k_sel_flush_done(SelState *st) {
 constexpr int BSORT_MAX = 4096;
 static __global__ void __launch_bounds__(1024) k_block_sort(const Key3 *__restrict__ kin, const uint64_t *__restrict__ vin,
                                                      int n, Key3 *__restrict__ kout, uint64_t *__restrict__ vout) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char bs_smem[];
   Key3 *sk = reinterpret_cast<Key3 *>(bs_smem);
   uint64_t *sv = reinterpret_cast<uint64_t *>(sk + BSORT_MAX);

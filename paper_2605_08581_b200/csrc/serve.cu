@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "../../include/prism.h"
+#include "pdl.cuh"
 #include "scan.cuh"
 
 namespace {
@@ -60,6 +61,7 @@ struct SvCtl {  // one wave's cost model, written by k_sv_wave_end (mapped pinne
 
 // arrivals [first, first + n) join the queue at position P0 (engine.py:176-178)
 __global__ void k_sv_append(int32_t *pend, int64_t P0, int64_t first, int64_t n) {
+  pdl_wait();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j < n) pend[P0 + j] = (int32_t)(first + j);
 }
@@ -71,6 +73,7 @@ __global__ void __launch_bounds__(SV_TPB) k_sv_gather_pending(const int32_t *pen
                                                               const uint8_t *treo, const int32_t *tsfx, int64_t *gids,
                                                               double *garr, int64_t *goff, uint8_t *greo,
                                                               int32_t *gsfx) {
+  pdl_wait();
   prism::block_scan4<1, 4>(
       P,
       [&](int, int64_t i) {
@@ -93,6 +96,7 @@ __global__ void __launch_bounds__(SV_TPB) k_sv_gather_pending(const int32_t *pen
 __global__ void __launch_bounds__(SV_TPB) k_sv_gather_active(const int64_t *ranges, int32_t R, int64_t A,
                                                              const int32_t *log_idx, const int64_t *toff,
                                                              int32_t *act_ti, int64_t *aoff) {
+  pdl_wait();
   __shared__ int64_t pre[1025];
   // range r covers concatenated positions [pre[r], pre[r+1]) (R <= 1024 here;
   // the host merges adjacent log ranges first)
@@ -130,6 +134,7 @@ __global__ void __launch_bounds__(SV_TPB) k_sv_gather_active(const int64_t *rang
 // skeleton entries of the gathered requests: one warp per request
 __global__ void k_sv_gather_sk(const int32_t *idx, int64_t n, const int64_t *off, const int64_t *toff,
                                const int32_t *tsk, int32_t *sk) {
+  pdl_wait();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= n) return;
@@ -163,6 +168,7 @@ struct SvWaveIn {
 };
 
 __global__ void __launch_bounds__(SV_TPB) k_sv_wave_end(SvWaveIn W) {
+  pdl_wait();
   __shared__ long long s_u[32], s_c[32];
   __shared__ double s_t[4];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;

@@ -136,6 +136,7 @@ __device__ inline int32_t wp_table(const WaveTmp &X, uint64_t key, int32_t j, bo
 // chain in parallel): shape, pre-match flags, chain nodes aligned 1:1 with the
 // first pieces, and the chain marks (victim guard; first member per node)
 __global__ void k_wp_plan(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
+  pdl_wait();
   const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = lane_id();
   if (j >= W.B || wc->stop) return;  // (warp-uniform)
@@ -178,6 +179,7 @@ __global__ void k_wp_plan(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
 // = level L of member j, consecutive members in a warp): every member shares
 // the low levels, so each warp inserts one key per distinct prefix.
 __global__ void k_wp_levels(WaveIn W, WaveTmp X, const WaveCtl *wc) {
+  pdl_wait();
   if (wc->stop) return;  // (an aborted wave: no dispatch order to read)
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t j = t % W.B;
@@ -222,6 +224,7 @@ __global__ void k_wp_levels(WaveIn W, WaveTmp X, const WaveCtl *wc) {
 // (ALU + shuffles), then each looks its own levels up in the first-owner table
 // at once (the lookups were a dependent sequence per member)
 __global__ void k_wp_hits(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
+  pdl_wait();
   const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = lane_id();
   if (j >= W.B || wc->stop) return;  // (warp-uniform; an aborted wave never ran the plan)
@@ -313,6 +316,7 @@ __global__ void k_wp_hits(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
 
 // apply the consumed victims [0, nv) of the stream (stream order == victim order)
 __global__ void k_wp_evict(DT T, const WaveCtl *wc) {
+  pdl_wait();
   if (wc->stop) return;
   const int64_t nv = wc->nv;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
@@ -340,6 +344,7 @@ __global__ void k_wp_evict(DT T, const WaveCtl *wc) {
 // W6a: slot of every new piece (free list LIFO, then the high-water mark)
 
 __global__ void k_wp_alloc(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
+  pdl_wait();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, j = t / WP_PL;
   const int pl = (int)(t % WP_PL);
   if (j >= W.B || wc->stop || j >= wc->Bc || X.cnew[j] == 0) return;
@@ -377,6 +382,7 @@ __device__ inline int32_t wp_node(const WaveIn &W, const WaveTmp &X, int64_t j, 
 
 // W6b: fields, child-table entries and tokens of the new pieces (warp per member)
 __global__ void k_wp_create(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
+  pdl_wait();
   const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = lane_id();
   if (j >= W.B || wc->stop || j >= wc->Bc || X.cnew[j] == 0) return;
@@ -443,6 +449,7 @@ __global__ void k_wp_create(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
 // inside the wave is "old" (pre-existing: match + insert touches) only for the
 // members after its creator, so the touches aggregate over the old peers.
 __global__ void k_wp_touch(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
+  pdl_wait();
   if (wc->stop) return;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t j = t % W.B;
@@ -473,6 +480,7 @@ __global__ void k_wp_touch(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
 }
 
 __global__ void k_wp_label_reset(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
+  pdl_wait();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, j = t / WP_PL;
   const int pl = (int)(t % WP_PL);
   if (j >= W.B || wc->stop || j >= wc->Bc) return;
@@ -485,6 +493,7 @@ __device__ inline void wp_stop_touch(DT T, const WaveIn &W, const WaveTmp &X, co
 
 __global__ void k_wp_label(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc, int64_t *hits, int32_t *leaf_slots,
                            int64_t *leaf_ids) {
+  pdl_wait();
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x < 32) wp_stop_touch(T, W, X, wc);  // (a CapacityError stop)
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, j = t / WP_PL;
   const int pl = (int)(t % WP_PL);
@@ -519,6 +528,7 @@ __global__ void k_wp_label(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc, int64_t
 
 // epoch + control-block snapshot the wave commits from
 __global__ void k_wc_begin(DT T, WaveCtl *wc, const int32_t *abort, WaveTmp X, int64_t nlt) {
+  pdl_wait();
   // the wave's scratch: empty level table, flags, device scalars (misc[1]:
   // the poison index "none")
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nlt; i += (int64_t)gridDim.x * blockDim.x) {
@@ -582,6 +592,7 @@ __device__ inline void wc_plan_body(DT T, int64_t B, WaveTmp X, WaveCtl *wc, int
 
 __global__ void __launch_bounds__(1024) k_wp_scan3(DT T, int64_t B, WaveTmp X, WaveCtl *wc, int64_t slack,
                                                   int32_t force_full) {
+  pdl_wait();
   // an aborted or flagged wave has no plan to scan: straight to the verdict (uniform)
   if (wc->stop || *X.flags) {
     if (threadIdx.x == 0) wc_plan_body(T, B, X, wc, slack, force_full);
@@ -645,6 +656,7 @@ __device__ inline void wc_cut_body(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
 // per member: number of list entries consumed through member j (first F >= D_j);
 // the last CTA to finish then takes the verdict (wc_cut_body)
 __global__ void k_wp_cuts(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
+  pdl_wait();
   __shared__ bool s_last;
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (wc->stop) return;  // (uniform over the grid)
@@ -712,6 +724,7 @@ __device__ inline void wc_finalize_body(DT T, int64_t B, const WaveTmp &X, const
 // the wave's control block after the commit, and the verdict + control block
 // written straight to the host's pinned (mapped) copies: no copy nodes
 __global__ void k_wc_finalize(DT T, int64_t B, WaveTmp X, const WaveCtl *wc, WaveCtl *h_wc, Ctrl *h_ctrl) {
+  pdl_wait();
   if (!wc->stop) wc_finalize_body(T, B, X, wc);
   *h_wc = *wc;
   *h_ctrl = *T.ctrl;
@@ -744,6 +757,7 @@ __device__ __forceinline__ int64_t wp_vlen(const DT &T, const WaveTmp &X, int64_
 // chain of a member that runs (index <= Bc: the committed ones and a stopping
 // one) changes that member's match: the exactness guard (nothing applied yet)
 __global__ void k_wp_conflicts(DT T, WaveTmp X, WaveCtl *wc) {
+  pdl_wait();
   if (wc->stop) return;
   const int64_t nv = wc->nv, Bc = wc->Bc;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x)
@@ -758,6 +772,7 @@ __global__ void k_wp_conflicts(DT T, WaveTmp X, WaveCtl *wc) {
 // into F and the partition's total; k_vscan_c: + the totals of the partitions
 // before it (a streaming add; the gathers are not repeated)
 __global__ void __launch_bounds__(256) k_vscan_a(DT T, WaveTmp X, int64_t *part, const WaveCtl *wc) {
+  pdl_wait();
   if (wc->stop || wc->W < 0) return;
   __shared__ int64_t sw[8];
   __shared__ int64_t carry;
@@ -801,6 +816,7 @@ __global__ void __launch_bounds__(256) k_vscan_a(DT T, WaveTmp X, int64_t *part,
 }
 
 __global__ void __launch_bounds__(256) k_vscan_c(DT T, WaveTmp X, const int64_t *part, const WaveCtl *wc) {
+  pdl_wait();
   if (wc->stop || wc->W < 0) return;
   __shared__ int64_t sw[8];
   __shared__ int64_t carry;
@@ -854,6 +870,7 @@ __device__ __forceinline__ bool wp_sweepable(const DT &T, int64_t i, uint32_t st
 }
 
 __global__ void __launch_bounds__(256) k_wp_sweep_a(DT T, int64_t *part, const WaveCtl *wc) {
+  pdl_wait();
   if (wc->stop || !wc->trunc) return;
   const int64_t nv = wc->nv, n = T.ctrl->L_n - nv, per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t b0 = nv + blockIdx.x * per, b1 = b0 + per < nv + n ? b0 + per : nv + n;
@@ -874,6 +891,7 @@ __global__ void __launch_bounds__(256) k_wp_sweep_a(DT T, int64_t *part, const W
 // each CTA: its carry from the counts before it, then its sweepable entries
 // detached in order (victim log, free list, child table, parents' child counts)
 __global__ void __launch_bounds__(256) k_wp_sweep_c(DT T, WaveTmp X, const int64_t *part, WaveCtl *wc) {
+  pdl_wait();
   if (wc->stop || !wc->trunc) return;
   __shared__ int64_t sw[8];
   __shared__ int64_t carry;

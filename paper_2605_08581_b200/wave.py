@@ -228,9 +228,9 @@ class WaveEngine:
 
     def graph_stats(self) -> dict:
         self.L.prism_qas_tune.argtypes = [_p, C.c_int32, _i64, _p]
-        out = np.zeros(2, dtype=np.int64)
-        check(self.L.prism_qas_tune(self.q, 5, 0, out.ctypes.data))
-        return {"captures": int(out[0]), "replays": int(out[1])}
+        out = np.zeros(3, dtype=np.int64)
+        check(self.L.prism_qas_tune(self.q, 5, 3, out.ctypes.data))
+        return {"captures": int(out[0]), "replays": int(out[1]), "pdl_edges": int(out[2])}
 
     def set_commit_mode(self, mode: int) -> None:
         """0: exact parallel wave commit with ordered fallback; 1: ordered only."""
