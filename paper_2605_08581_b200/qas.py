@@ -34,7 +34,28 @@ class _QasCfg(C.Structure):
     ]
 
 
+_WARNED = False
+
+
+def warn_nonintegral(config: SchedulerConfig) -> None:
+    """Non-integral weights (w_g, w_a, w_n): the device sums each bucket's
+    utility terms in ascending segment order, the reference in Python ``set``
+    iteration order (scheduler.py:163-169), so a score may differ in its last
+    bit and, on an exact tie, the dispatch order with it.  Integral weights
+    (the reference's defaults) are summed exactly in int64: identical."""
+    global _WARNED
+    w = config.weights
+    if _WARNED or all(float(x).is_integer() for x in (w.w_g, w.w_a, w.w_n)):
+        return
+    import warnings
+
+    warnings.warn("non-integral QAS weights: bucket utilities are summed in ascending segment order, the "
+                  "reference in set order; scores may differ in the last bit", RuntimeWarning, stacklevel=3)
+    _WARNED = True
+
+
 def _cfg(config: SchedulerConfig) -> _QasCfg:
+    warn_nonintegral(config)
     w = config.weights
     return _QasCfg(config.dispatch_budget, config.cold_quota, config.front_width, config.signature_size,
                    w.w_g, w.w_a, w.w_n, config.alpha_size, config.beta_util)
