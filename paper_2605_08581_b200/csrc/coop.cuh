@@ -51,6 +51,7 @@ struct CoopState {
   unsigned long long tf_n;      // top-f protection: candidates with a positive P-hat
   int tf_done;                  // top-f protection applied by k_tf_local (k_protect_coop returns)
   unsigned int tf_cl;           // k_tf_local: clusters that published their top f
+  unsigned int ss_next;         // k_ss_sort: next small bucket to take
   unsigned long long ss_dbg[24];
   unsigned long long ss_prof[8];  // diagnostics: k_ss_sort clock64 sums (load, sort, buckets, items)  // diagnostics: [0] max bucket, [1] rounds, [2+3r..] (undecided, selected, shift)
   int ss_nb;                    // diagnostics: splitters of the last sample select
@@ -941,6 +942,7 @@ struct ProtCand {
 constexpr int SS_TPB = 256;
 constexpr int SS_SEL_TPB = 512;
 constexpr int SS_BMAX = 1024;  // buckets up to this size: k_ss_sort (merge sort, several CTAs per SM)
+constexpr int SS_BMID = 384;   // k_ss_sort takes the buckets above this first
 constexpr int SS_BBIG = CHUNK; // larger ones up to this: k_ss_sort_big (in-place bitonic); beyond: fallback
 constexpr int SS_SUB = 1024;  // sub-sample the selection rounds run on
 constexpr size_t SS_SEL_SMEM =
@@ -1336,9 +1338,38 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_sort(CoopBufs B, Key3 *kout, uint
   uint64_t *sv = reinterpret_cast<uint64_t *>(sk + SS_BMAX);
   Key3 *tk = reinterpret_cast<Key3 *>(sv + SS_BMAX);
   uint64_t *tv = reinterpret_cast<uint64_t *>(tk + SS_BMAX);
-  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+  // the buckets above SS_BMID first, one per CTA as they come (a ~1000-key
+  // bucket sorts for ~25 us: started last behind three small ones it set the
+  // kernel's length), then the small ones handed out one at a time
+  __shared__ int s_b;
+  int b = blockIdx.x, pass = 0;
+  for (;;) {
+    if (pass == 0) {
+      while (b < nb) {
+        const int m = (int)(st->ss_off[b + 1] - st->ss_off[b]);
+        if (m > SS_BMID && m <= SS_BMAX) break;
+        b += gridDim.x;
+      }
+      if (b >= nb) {
+        pass = 1;
+        continue;
+      }
+    } else {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int x;
+        do {
+          x = (int)atomicAdd(&st->ss_next, 1u);
+        } while (x < nb && (int)(st->ss_off[x + 1] - st->ss_off[x]) > SS_BMID);
+        s_b = x;
+      }
+      __syncthreads();
+      b = s_b;
+      if (b >= nb) break;
+    }
     const int b0 = (int)st->ss_off[b], m0 = (int)(st->ss_off[b + 1] - st->ss_off[b]);
-    if (m0 == 0 || m0 > SS_BMAX) continue;  // (big buckets: k_ss_sort_big)
+    if (pass == 0) b += gridDim.x;
+    if (m0 == 0) continue;
     const long long c0 = clock64();
     for (int i = threadIdx.x; i < m0; i += blockDim.x) {
       sk[i] = B.ks[b0 + i];
