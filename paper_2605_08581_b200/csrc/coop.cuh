@@ -1222,20 +1222,38 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_filter(Cand cand, CoopBufs B) {
       ccount += c ? 1 : 0;
       bk[u] = (c && !key_less(tau, k[u])) ? 0 : -1;
     }
+    // the bucket of every kept candidate: first splitter >= k (exists: spl[nb-1] = tau >= k), the UNR
+    // binary searches advanced in lock step (independent shared-memory loads in flight)
+    int lo[UNR], hi[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+      lo[u] = 0;
+      hi[u] = bk[u] == 0 ? nb - 1 : 0;
+    }
+    for (int span = nb - 1; span > 0; span >>= 1) {  // (ceil(log2 nb) + 1 rounds bound every search)
+#pragma unroll
+      for (int u = 0; u < UNR; u++)
+        if (lo[u] < hi[u]) {
+          const int mid = (lo[u] + hi[u]) >> 1;
+          if (key_less(spl[mid], k[u])) lo[u] = mid + 1;
+          else hi[u] = mid;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; u++)
+      if (lo[u] < hi[u]) {  // (a last step when nb is not a power of two)
+        const int mid = (lo[u] + hi[u]) >> 1;
+        if (key_less(spl[mid], k[u])) lo[u] = mid + 1;
+        else hi[u] = mid;
+      }
     unsigned nt = 0;
 #pragma unroll
     for (int u = 0; u < UNR; u++) {
       if (bk[u] == 0) {
-        int lo = 0, hi = nb - 1;  // first splitter >= k (exists: spl[nb-1] = tau >= k)
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (key_less(spl[mid], k[u])) lo = mid + 1;
-          else hi = mid;
-        }
-        bk[u] = lo;
+        bk[u] = lo[u];
         nt++;
         mass += (unsigned long long)w[u];
-        atomicAdd(&hcnt[lo], 1u);
+        atomicAdd(&hcnt[lo[u]], 1u);
       }
     }
     unsigned long long p = block_reserve(nt, &st->ss_n, s_w, &s_base);
