@@ -28,7 +28,6 @@ constexpr int CHUNK = 4096;  // bitonic chunk per CTA (shared memory)
 // sample select (coop_sample_select)
 constexpr int SS_SAMP = 12288;  // samples at most (the period is the power of two that keeps the sample below this)
 constexpr int SS_SPL = 2560;   // splitters (selected samples) at most
-constexpr int SS_U = 2048;     // undecided samples kept as a list (more: flags only)
 constexpr size_t COOP_SORT_SMEM = (sizeof(Key3) + sizeof(uint64_t)) * CHUNK;
 constexpr size_t COOP_SMEM = COOP_SORT_SMEM;
 
@@ -661,192 +660,6 @@ __device__ inline void block_merge_sort(const Key3 *k, const uint64_t *v, int n,
   __syncthreads();
 }
 
-// one radix round of CTA 0's sample selection over the undecided samples:
-// digit below the highest bit where the undecided keys differ, the weight
-// histogram, the crossing digit; lower digits join the selected keys, higher
-// ones are dropped, the crossing digit's samples stay undecided.  The
-// undecided set is either the list idx[0..nU) or (idx null) every sample with
-// flag 0 among ns; the next set is written as a list when it fits cap_nxt,
-// else kept in the flags only.  Global sample loads are batched SR_B per
-// thread (the sample lives in L2).
-struct SampleRound {
-  int nU_next;
-  bool listed;
-  long long below;
-  bool overflow;
-};
-constexpr int SR_B = 4;
-
-__device__ inline SampleRound sample_round(const Key3 *sk, const int64_t *sw, const int *idx, int nU, int ns,
-                                           uint8_t *flag, long long need, Key3 *selk, int *s_nsel, int *nxt,
-                                           int cap_nxt, Key3 *smin, Key3 *smax, unsigned *s_hn,
-                                           unsigned *s_hw, int *s_misc, long long *s_ll, Key3 &gmin, Key3 &gmax,
-                                           bool have_mm) {
-  const int lane = threadIdx.x & 31;
-  const int n = idx ? nU : ns;
-  const int step = SR_B * blockDim.x;
-  auto item = [&](int q) -> int {  // sample index of undecided position q, or -1
-    if (q >= n) return -1;
-    const int i = idx ? idx[q] : q;
-    return (idx || flag[i] == 0) ? i : -1;
-  };
-  Key3 lo = {~0ull, ~0ull, ~0ull}, hi = {0, 0, 0};
-  if (!have_mm) {  // (later rounds get the min/max from the previous classification)
-    for (int q0 = threadIdx.x; q0 < n; q0 += step) {
-      Key3 kk[SR_B];
-      int ii[SR_B];
-#pragma unroll
-      for (int u = 0; u < SR_B; u++) {
-        ii[u] = item(q0 + u * blockDim.x);
-        if (ii[u] >= 0) kk[u] = sk[ii[u]];
-      }
-#pragma unroll
-      for (int u = 0; u < SR_B; u++)
-        if (ii[u] >= 0) {
-          if (key_less(kk[u], lo)) lo = kk[u];
-          if (key_less(hi, kk[u])) hi = kk[u];
-        }
-    }
-    block_minmax(lo, hi, smin, smax, &smin[32], &smax[32]);
-    gmin = smin[32];
-    gmax = smax[32];
-    lo = {~0ull, ~0ull, ~0ull};
-    hi = {0, 0, 0};
-  }
-  const Key3 xx = {gmin.w0 ^ gmax.w0, gmin.w1 ^ gmax.w1, gmin.w2 ^ gmax.w2};
-  const int hb = chighbit(xx);
-  const int shift = hb < 7 ? 0 : hb - 7;
-  for (int d = threadIdx.x; d < 256; d += blockDim.x) {
-    s_hn[d] = 0;
-    s_hw[d] = 0;
-  }
-  if (threadIdx.x == 0) s_misc[1] = 0;  // next-list count
-  __syncthreads();
-  {  // per-thread run-length aggregation (samples crowd few digits), warp-aggregated flushes
-    uint32_t cd = 256u;
-    unsigned cn = 0, cw = 0;
-    auto flush = [&]() {
-      const uint32_t d0 = __shfl_sync(0xffffffffu, cd, 0);
-      const unsigned same = __ballot_sync(0xffffffffu, cd == d0);
-      if (same == 0xffffffffu) {  // the common case: one digit across the warp
-        unsigned a = cn, b = cw;
-        for (int o = 16; o > 0; o >>= 1) {
-          a += __shfl_xor_sync(0xffffffffu, a, o);
-          b += __shfl_xor_sync(0xffffffffu, b, o);
-        }
-        if (lane == 0 && d0 < 256u && a) {
-          atomicAdd(&s_hn[d0], a);
-          atomicAdd(&s_hw[d0], b);
-        }
-      } else if (cd < 256u && cn) {
-        atomicAdd(&s_hn[cd], cn);
-        atomicAdd(&s_hw[cd], cw);
-      }
-    };
-    for (int q0 = threadIdx.x; q0 - (int)threadIdx.x < n; q0 += step) {  // warp-uniform trip count
-      uint32_t dd[SR_B];
-      unsigned ww[SR_B];
-#pragma unroll
-      for (int u = 0; u < SR_B; u++) {
-        const int i = item(q0 + u * blockDim.x);
-        dd[u] = i >= 0 ? cdigit(sk[i], shift) : 256u;
-        ww[u] = i >= 0 ? (unsigned)sw[i] : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < SR_B; u++) {
-        if (dd[u] == 256u) continue;
-        if (dd[u] != cd) {
-          if (cd < 256u && cn) {
-            atomicAdd(&s_hn[cd], cn);
-            atomicAdd(&s_hw[cd], cw);
-          }
-          cd = dd[u];
-          cn = 0;
-          cw = 0;
-        }
-        cn++;
-        cw += ww[u];
-      }
-    }
-    flush();
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {  // crossing digit: the first whose cumulative weight reaches need
-    unsigned long long w8[8], run = 0;
-    for (int q = 0; q < 8; q++) {
-      run += s_hw[8 * lane + q];
-      w8[q] = run;
-    }
-    unsigned long long pre = run;
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long y = __shfl_up_sync(0xffffffffu, pre, o);
-      if (lane >= o) pre += y;
-    }
-    const unsigned long long before = pre - run;
-    int dl = 256;
-    for (int q = 0; q < 8; q++)
-      if ((long long)(before + w8[q]) >= need) {
-        dl = 8 * lane + q;
-        break;
-      }
-    const unsigned msk = __ballot_sync(0xffffffffu, dl < 256);
-    const int src = __ffs(msk) - 1;  // need <= mass of the undecided: some digit crosses
-    const int dstar = __shfl_sync(0xffffffffu, dl, src);
-    unsigned long long bb = 0;
-    if (lane == src) bb = before + ((dstar - 8 * src) ? w8[dstar - 8 * src - 1] : 0);
-    bb = __shfl_sync(0xffffffffu, bb, src);
-    if (lane == 0) {
-      s_misc[0] = dstar;
-      *s_ll = (long long)bb;
-    }
-  }
-  __syncthreads();
-  const int dstar = s_misc[0];
-  const int nnext = (int)s_hn[dstar];
-  const bool list = nnext <= cap_nxt;
-  bool ovf = false;
-  for (int q0 = threadIdx.x; q0 - (int)threadIdx.x < n; q0 += step) {  // warp-uniform trip count
-    Key3 kk[SR_B];
-    int ii[SR_B];
-#pragma unroll
-    for (int u = 0; u < SR_B; u++) {
-      ii[u] = item(q0 + u * blockDim.x);
-      if (ii[u] >= 0) kk[u] = sk[ii[u]];
-    }
-#pragma unroll
-    for (int u = 0; u < SR_B; u++) {  // warp-aggregated appends (one atomic per warp and list)
-      const int i = ii[u];
-      const int d = i >= 0 ? (int)cdigit(kk[u], shift) : -1;
-      const bool below = i >= 0 && d < dstar, mid = i >= 0 && d == dstar;
-      if (i >= 0 && d > dstar) flag[i] = 2;
-      if (below) flag[i] = 1;
-      const unsigned mb = __ballot_sync(0xffffffffu, below), mm = __ballot_sync(0xffffffffu, mid && list);
-      int pb = 0, pm = 0;
-      if (lane == 0) {
-        if (mb) pb = atomicAdd(s_nsel, __popc(mb));
-        if (mm) pm = atomicAdd(&s_misc[1], __popc(mm));
-      }
-      pb = __shfl_sync(0xffffffffu, pb, 0) + __popc(mb & ((1u << lane) - 1u));
-      pm = __shfl_sync(0xffffffffu, pm, 0) + __popc(mm & ((1u << lane) - 1u));
-      if (below) {
-        if (pb < SS_SPL) selk[pb] = kk[u];
-        else ovf = true;
-      }
-      if (mid && list) nxt[pm] = i;
-      if (mid) {  // min/max of the next undecided set
-        if (key_less(kk[u], lo)) lo = kk[u];
-        if (key_less(hi, kk[u])) hi = kk[u];
-      }
-    }
-  }
-  block_minmax(lo, hi, smin, smax, &smin[32], &smax[32]);
-  gmin = smin[32];
-  gmax = smax[32];
-  ovf = __syncthreads_or(ovf);
-  SampleRound r{nnext, list, *s_ll, ovf};
-  __syncthreads();
-  return r;
-}
 
 // candidate gather over the slots (the materialising path): cand(s) for every
 // slot s < hw into (B.k0, B.v0, B.w0); the count lands in st->cand
@@ -945,8 +758,7 @@ constexpr int SS_BMAX = 1024;  // buckets up to this size: k_ss_sort (merge sort
 constexpr int SS_BMID = 384;   // k_ss_sort takes the buckets above this first
 constexpr int SS_BBIG = CHUNK; // larger ones up to this: k_ss_sort_big (in-place bitonic); beyond: fallback
 constexpr int SS_SUB = 1024;  // sub-sample the selection rounds run on
-constexpr size_t SS_SEL_SMEM =
-    2 * sizeof(Key3) * SS_SPL + 8 * SS_U + 2 * (sizeof(Key3) + 8) * SS_SEL_TPB + (sizeof(Key3) + 9) * SS_SUB;
+constexpr size_t SS_SEL_SMEM = 3 * sizeof(Key3) * SS_SPL + 3 * 8 * SS_SUB;  // (k_ss_select's lk, tk, all; lw, tw, aw)
 constexpr size_t SS_FILTER_SMEM = sizeof(Key3) * SS_SPL + 4 * SS_SPL;
 constexpr size_t SS_SORT_SMEM = 2 * (sizeof(Key3) + 8) * SS_BMAX;
 
@@ -983,209 +795,194 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_sample(Cand cand, CoopBufs B, int
   }
 }
 
-// CTA 0 of k_ss_select's cluster: tau and the (unsorted) splitters in selk;
-// *o_nb of them, *o_fail why not
-template <class Cand>
-__device__ __forceinline__ void ss_select_body(Cand cand, CoopBufs B, int64_t W, const int64_t *dW,
-                                               unsigned char *dsm, int *o_fail, int *o_nb) {
-  if (dW) W = *dW;
-  __shared__ Key3 smin[33], smax[33];
-  __shared__ unsigned s_hn[256];
-  __shared__ unsigned s_hw[256];
-  __shared__ unsigned long long s_u64[32];
-  __shared__ int s_misc[4];
-  __shared__ long long s_ll;
-  __shared__ int s_nsel;
-  CoopState *st = B.st;
-  const int lane = threadIdx.x & 31;
-  const int64_t m = ss_period(cand.hw());
-  Key3 *spl = reinterpret_cast<Key3 *>(dsm);          // [SS_SPL] sorted splitters
-  Key3 *selk = spl + SS_SPL;                          // [SS_SPL] selected sample keys, unsorted
-  int *ua = reinterpret_cast<int *>(selk + SS_SPL);   // [SS_U] undecided lists (ping-pong)
-  int *ub = ua + SS_U;
-  Key3 *fk = reinterpret_cast<Key3 *>(ub + SS_U);     // [blockDim] the last undecided; sort scratch
-  uint64_t *fw = reinterpret_cast<uint64_t *>(fk + SS_SEL_TPB);
-  Key3 *fk2 = reinterpret_cast<Key3 *>(fw + SS_SEL_TPB);
-  uint64_t *fw2 = reinterpret_cast<uint64_t *>(fk2 + SS_SEL_TPB);
-  Key3 *subk = reinterpret_cast<Key3 *>(fw2 + SS_SEL_TPB);  // [SS_SUB] the sub-sample the rounds run on
-  int64_t *subw = reinterpret_cast<int64_t *>(subk + SS_SUB);
-  uint8_t *flag = reinterpret_cast<uint8_t *>(subw + SS_SUB);  // [SS_SUB] 0 undecided, 1 selected, 2 above
-  coop_mark(st);
-  const int ns = (int)st->ss_ns;
-  // tau comes from every q-th sample (<= SS_SUB of them, in shared memory);
-  // the splitters are then all samples <= tau
-  const int q = (ns + SS_SUB - 1) / SS_SUB > 0 ? (ns + SS_SUB - 1) / SS_SUB : 1;
-  const int nsub = (ns + q - 1) / q;
-  unsigned long long x = 0;
-  for (int j = threadIdx.x; j < nsub; j += blockDim.x) {
-    subk[j] = B.k1[j * q];
-    subw[j] = B.w1[j * q];
-    x += (unsigned long long)subw[j];
-    flag[j] = 0;
+// rank of x among the sorted keys a[0..n): the keys below it (before = false)
+// or at most it (before = true: equal keys of an earlier slice come first)
+__device__ __forceinline__ int ss_rank(const Key3 *a, int n, const Key3 &x, bool before) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (before ? !key_less(x, a[mid]) : key_less(a[mid], x)) lo = mid + 1;
+    else hi = mid;
   }
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  if (lane == 0) s_u64[threadIdx.x >> 5] = x;
-  if (threadIdx.x == 0) s_nsel = 0;
-  __syncthreads();
-  unsigned long long tot = 0;
-  for (int w = 0; w < (int)(blockDim.x >> 5); w++) tot += s_u64[w];
-  __syncthreads();
-  // target sub-sample mass: (1.25 W + 3 average sub-samples of slack) / (m q)
-  // (the tau estimate comes from <= SS_SUB sub-samples: ~7% noise; a prefix
-  // short of W costs the materialising selection, so the margin stays wide)
-  coop_mark(st);
-  const double mq = (double)m * q;
-  long long need = nsub > 0 ? (long long)(((double)W * 1.25 + 3.0 * mq * ((double)tot / nsub)) / mq) + 1 : 1;
-  // (nearly) everything, or the whole order asked for (W <= 0; a sample taken
-  // ahead of W, see prebuild_order): sort it all
-  int fail = (W <= 0 || nsub == 0 || (unsigned long long)need > tot) ? 1 : 0;
-  int nU = nsub;
-  const int *cur = nullptr;  // null: the undecided set is in the flags
-  Key3 gmin, gmax;
-  for (int r = 0; !fail && nU > (int)blockDim.x && r < 48; r++) {
-    int *nxt = (cur == ua) ? ub : ua;
-    const SampleRound R = sample_round(subk, subw, cur, nU, nsub, flag, need, selk, &s_nsel, nxt, SS_U, smin, smax,
-                                       s_hn, s_hw, s_misc, &s_ll, gmin, gmax, r > 0);
-    if (R.overflow) fail = 2;
-    need -= R.below;
-    nU = R.nU_next;
-    cur = R.listed ? nxt : nullptr;
-    if (threadIdx.x == 0) {
-      st->ss_dbg[1] = r + 1;
-      if (r < 3) {
-        st->ss_dbg[2 + 3 * r] = nU;
-        st->ss_dbg[3 + 3 * r] = s_nsel;
-        st->ss_dbg[4 + 3 * r] = (unsigned long long)need;
-      }
-    }
-  }
-  coop_mark(st);
-  if (!fail && nU > (int)blockDim.x) fail = 2;
-  if (!fail) {  // the last undecided samples (<= blockDim): exact sort, then the crossing one
-    if (!cur) {
-      if (threadIdx.x == 0) s_misc[2] = 0;
-      __syncthreads();
-      for (int i = threadIdx.x; i < nsub; i += blockDim.x)
-        if (flag[i] == 0) ua[atomicAdd(&s_misc[2], 1)] = i;
-      __syncthreads();
-      cur = ua;
-    }
-    for (int j = threadIdx.x; j < nU; j += blockDim.x) {
-      const int i = cur[j];
-      fk[j] = subk[i];
-      fw[j] = (uint64_t)subw[i];
-    }
-    __syncthreads();
-    block_merge_sort(fk, fw, nU, fk2, fw2, fk, fw);
-    coop_mark(st);
-    {  // the crossing sample: the first j whose inclusive weight prefix reaches need (nU <= blockDim)
-      const int j = threadIdx.x, wid = threadIdx.x >> 5;
-      long long inc = j < nU ? (long long)fw[j] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        const long long y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-      }
-      if (lane == 31) s_u64[wid] = (unsigned long long)inc;
-      if (threadIdx.x == 0) s_misc[3] = nU - 1;
-      __syncthreads();
-      for (int w = 0; w < wid; w++) inc += (long long)s_u64[w];
-      if (j < nU && inc >= need) atomicMin(&s_misc[3], j);
-      if (threadIdx.x == 0) s_nsel = 0;
-    }
-    __syncthreads();
-    const Key3 tau = fk[s_misc[3]];
-    // splitters: every sample <= tau (warp-aggregated appends)
-    bool ovf = false;
-    constexpr int SPU = 4;  // sample loads in flight per thread
-    for (int i0 = 0; i0 < ns; i0 += SPU * blockDim.x) {
-      Key3 k[SPU];
-#pragma unroll
-      for (int u = 0; u < SPU; u++) {
-        const int i = i0 + u * blockDim.x + threadIdx.x;
-        k[u] = i < ns ? B.k1[i] : tau;
-      }
-#pragma unroll
-      for (int u = 0; u < SPU; u++) {
-        const bool t = i0 + u * (int)blockDim.x + (int)threadIdx.x < ns && !key_less(tau, k[u]);
-        const unsigned mt = __ballot_sync(0xffffffffu, t);
-        int p = 0;
-        if (lane == 0 && mt) p = atomicAdd(&s_nsel, __popc(mt));
-        p = __shfl_sync(0xffffffffu, p, 0) + __popc(mt & ((1u << lane) - 1u));
-        if (t) {
-          if (p < SS_SPL) selk[p] = k[u];
-          else ovf = true;
-        }
-      }
-    }
-    if (__syncthreads_or(ovf)) fail = 3;
-    coop_mark(st);
-  }
-  if (threadIdx.x == 0) {
-    *o_fail = fail;
-    *o_nb = fail ? 0 : s_nsel;
-  }
+  return lo;
 }
 
-// The sample select: CTA 0 finds tau and the splitters (every sample <= tau,
-// ~2000), then the cluster sorts them -- every CTA sorts a slice pulled from
-// CTA 0's shared memory (DSMEM), gathers the sorted slices from its peers and
-// places each of its keys at (its rank in the slice + its rank in every other
-// slice).  One CTA sorting them alone took ~30 us of the wave.
+// The sample select as one 8-CTA cluster, every step spread over the cluster:
+//  1. tau: the sub-sample (every q-th sample, <= SS_SUB) is sorted -- each CTA
+//     sorts a slice, CTA 0 gathers the slices over DSMEM and places every key
+//     by its rank in each slice -- and CTA 0 finds the key where the prefix
+//     weight, scaled by m q, reaches 1.25 W + three average sub-samples;
+//  2. the splitters (every sample <= tau, ~2000): each CTA filters and sorts
+//     its share of the sample, then places its keys by their ranks in every
+//     peer's sorted share (gathered over DSMEM) straight into B.kt.
+// (One CTA ran this with radix rounds and a splitter sort: ~50 us of the wave.)
 constexpr int SS_CL = 8;  // CTAs in k_ss_select's cluster
 template <class Cand>
 __global__ void __cluster_dims__(SS_CL, 1, 1) __launch_bounds__(SS_SEL_TPB)
     k_ss_select(Cand cand, CoopBufs B, int64_t W, const int64_t *dW) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char dsm[];
-  __shared__ int s_fail, s_nb;
+  __shared__ int s_fail, s_n;
+  __shared__ unsigned long long s_u64[32];
+  __shared__ int s_cross;
+  __shared__ Key3 s_tau;
   cg::cluster_group cluster = cg::this_cluster();
-  const unsigned rank = cluster.block_rank();
-  if (rank == 0) ss_select_body(cand, B, W, dW, dsm, &s_fail, &s_nb);
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  CoopState *st = B.st;
+  if (dW) W = *dW;
+  if (rank == 0) coop_mark(st);
+  // shared memory: lk/lw [SS_SPL] this CTA's keys (sub-sample slice, then its
+  // splitters), tk/tw [SS_SPL] sort scratch, all [SS_SPL] every CTA's sorted keys
+  Key3 *lk = reinterpret_cast<Key3 *>(dsm);
+  Key3 *tk = lk + SS_SPL;
+  Key3 *all = tk + SS_SPL;
+  uint64_t *lw = reinterpret_cast<uint64_t *>(all + SS_SPL);
+  uint64_t *tw = lw + SS_SUB;
+  uint64_t *aw = tw + SS_SUB;  // [SS_SUB] CTA 0: the sorted sub-sample's weights
+  const int ns = (int)st->ss_ns;
+  const int64_t m = ss_period(cand.hw());
+  const int q = (ns + SS_SUB - 1) / SS_SUB > 0 ? (ns + SS_SUB - 1) / SS_SUB : 1;
+  const int nsub = (ns + q - 1) / q;
+  // ---- 1. the sorted sub-sample
+  const int sper = (nsub + SS_CL - 1) / SS_CL;
+  const int s0 = min(nsub, rank * sper), sm = min(nsub, s0 + sper) - s0;
+  for (int j = tid; j < sm; j += blockDim.x) {
+    lk[j] = B.k1[(int64_t)(s0 + j) * q];
+    lw[j] = (uint64_t)B.w1[(int64_t)(s0 + j) * q];
+  }
+  __syncthreads();
+  block_merge_sort(lk, lw, sm, tk, tw, lk, lw);
   cluster.sync();
-  const int fail = *cluster.map_shared_rank(&s_fail, 0), nb = *cluster.map_shared_rank(&s_nb, 0);
-  Key3 *lk = reinterpret_cast<Key3 *>(dsm);  // [SS_SPL / SS_CL] this CTA's slice, then [..] sort scratch
-  Key3 *tk = lk + SS_SPL / SS_CL;
-  Key3 *all = lk + SS_SPL;                   // [SS_SPL] every sorted slice (CTA 0: its selk, read by now)
-  const int per = (nb + SS_CL - 1) / SS_CL;
-  const int b0 = min(nb, (int)rank * per), m = min(nb, b0 + per) - b0;
-  if (!fail) {
-    const Key3 *sel0 = cluster.map_shared_rank(all, 0);  // (CTA 0's selk: the same offset)
-    for (int i = threadIdx.x; i < m; i += blockDim.x) lk[i] = sel0[b0 + i];
-    __syncthreads();
-    block_merge_sort(lk, nullptr, m, tk, nullptr, lk, nullptr);
-  }
-  cluster.sync();  // every slice sorted; CTA 0's selk read
-  if (!fail) {
-    for (int r = 0; r < SS_CL; r++) {
-      const int r0 = min(nb, r * per), rm = min(nb, r0 + per) - r0;
-      const Key3 *src = cluster.map_shared_rank(lk, r);
-      for (int i = threadIdx.x; i < rm; i += blockDim.x) all[r0 + i] = src[i];
+  if (rank == 0) {
+    coop_mark(st);
+    // every slice into shared memory (flat over the sub-sample: a thread's
+    // remote loads are independent, one DSMEM round trip), then each key at
+    // its merged place: its index in its slice + its rank in every other slice
+    for (int j = tid; j < nsub; j += blockDim.x) {
+      const int r = j / sper, i = j - r * sper;
+      all[j] = cluster.map_shared_rank(lk, r)[i];
+      tw[j] = cluster.map_shared_rank(lw, r)[i];
     }
     __syncthreads();
-      for (int i = threadIdx.x; i < m; i += blockDim.x) {
-      const Key3 x = lk[i];
+    for (int j = tid; j < nsub; j += blockDim.x) {
+      const int r = j / sper, i = j - r * sper;
+      const Key3 x = all[j];
       int pos = i;
-      for (int r = 0; r < SS_CL; r++) {
-        if (r == (int)rank) continue;
-        const int r0 = min(nb, r * per), r1 = min(nb, r0 + per);
-        int lo = r0, hi = r1;
-        const bool before = r < (int)rank;  // (equal keys of earlier slices first: a stable order)
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (before ? !key_less(x, all[mid]) : key_less(all[mid], x)) lo = mid + 1;
-          else hi = mid;
-        }
-        pos += lo - r0;
+      for (int r2 = 0; r2 < SS_CL; r2++) {
+        if (r2 == r) continue;
+        const int a0 = min(nsub, r2 * sper), an = min(nsub, a0 + sper) - a0;
+        pos += ss_rank(all + a0, an, x, r2 < r);
       }
-      B.kt[pos] = x;
+      tk[pos] = x;
+      aw[pos] = tw[j];
+    }
+    __syncthreads();
+    // the target sub-sample mass: (1.25 W + 3 average sub-samples of slack) / (m q)
+    // (tau comes from <= SS_SUB sub-samples: ~7% noise; a prefix short of W
+    // costs the materialising selection, so the margin stays wide)
+    unsigned long long x = 0;
+    for (int j = tid; j < nsub; j += blockDim.x) x += aw[j];
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) s_u64[wid] = x;
+    __syncthreads();
+    unsigned long long tot = 0;
+    for (int w = 0; w < nw; w++) tot += s_u64[w];
+    __syncthreads();
+    const double mq = (double)m * q;
+    const long long need =
+        nsub > 0 ? (long long)(((double)W * 1.25 + 3.0 * mq * ((double)tot / nsub)) / mq) + 1 : 1;
+    // (W <= 0: the whole order asked for, see prebuild_order: everything is sorted)
+    const int fail = (W <= 0 || nsub == 0 || (unsigned long long)need > tot) ? 1 : 0;
+    if (tid == 0) {
+      s_fail = fail;
+      s_cross = nsub - 1;
+    }
+    __syncthreads();
+    if (!fail) {  // the first place whose inclusive weight prefix reaches need (block scan, a carry per chunk)
+      long long carry = 0;
+      for (int j0 = 0; j0 < nsub; j0 += blockDim.x) {
+        const int j = j0 + tid;
+        long long inc = j < nsub ? (long long)aw[j] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += y;
+        }
+        if (lane == 31) s_u64[wid] = (unsigned long long)inc;
+        __syncthreads();
+        long long before = carry, chunk = 0;
+        for (int w = 0; w < nw; w++) {
+          if (w < wid) before += (long long)s_u64[w];
+          chunk += (long long)s_u64[w];
+        }
+        if (j < nsub && before + inc >= need) atomicMin(&s_cross, j);
+        carry += chunk;
+        __syncthreads();
+      }
+      if (tid == 0) s_tau = tk[s_cross];
+    }
+    coop_mark(st);
+  }
+  cluster.sync();
+  const int fail0 = *cluster.map_shared_rank(&s_fail, 0);
+  int nb = 0, fail = fail0;
+  if (!fail0) {
+    // ---- 2. the splitters: this CTA's share of the sample at or below tau, sorted
+    const Key3 tau = *cluster.map_shared_rank(&s_tau, 0);
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    const int per = (ns + SS_CL - 1) / SS_CL, a0 = min(ns, rank * per), a1 = min(ns, a0 + per);
+    constexpr int SPU = 4;  // sample loads in flight per thread
+    for (int i0 = a0; i0 < a1; i0 += SPU * blockDim.x) {
+      Key3 k[SPU];
+#pragma unroll
+      for (int u = 0; u < SPU; u++) {
+        const int i = i0 + u * blockDim.x + tid;
+        k[u] = i < a1 ? B.k1[i] : tau;
+      }
+#pragma unroll
+      for (int u = 0; u < SPU; u++) {
+        const bool t = i0 + u * (int)blockDim.x + tid < a1 && !key_less(tau, k[u]);
+        const unsigned mt = __ballot_sync(0xffffffffu, t);
+        int p = 0;
+        if (lane == 0 && mt) p = atomicAdd(&s_n, __popc(mt));
+        p = __shfl_sync(0xffffffffu, p, 0) + __popc(mt & ((1u << lane) - 1u));
+        if (t && p < SS_SPL) lk[p] = k[u];
+      }
+    }
+    __syncthreads();
+    const int mine = s_n;
+    if (mine <= SS_SPL) block_merge_sort(lk, nullptr, mine, tk, nullptr, lk, nullptr);
+    cluster.sync();  // every share sorted and counted
+    int off[SS_CL + 1];
+    off[0] = 0;
+    for (int r = 0; r < SS_CL; r++) off[r + 1] = off[r] + *cluster.map_shared_rank(&s_n, r);
+    nb = off[SS_CL];
+    if (nb > SS_SPL) {
+      fail = 3;  // more splitters than a filter CTA holds
+    } else {
+      for (int j = tid; j < nb; j += blockDim.x) {  // (flat: independent remote loads)
+        int r = 0;
+        while (j >= off[r + 1]) r++;
+        all[j] = cluster.map_shared_rank(lk, r)[j - off[r]];
+      }
+      __syncthreads();
+      for (int i = tid; i < mine; i += blockDim.x) {
+        const Key3 x = lk[i];
+        int pos = i;
+        for (int r = 0; r < SS_CL; r++)
+          if (r != rank) pos += ss_rank(all + off[r], off[r + 1] - off[r], x, r < rank);
+        B.kt[pos] = x;
+      }
     }
   }
-  if (rank == 0 && threadIdx.x == 0) {
-    B.st->ss_nb = fail ? 0 : nb;
-    B.st->ss_fail = fail;
+  if (rank == 0 && tid == 0) {
+    st->ss_nb = fail ? 0 : nb;
+    st->ss_fail = fail;
+    st->ss_dbg[1] = (unsigned long long)nb;
   }
-  coop_mark(B.st);
-  cluster.sync();  // (the peers' slices stay alive until every CTA has gathered them)
+  if (rank == 0) coop_mark(st);
+  cluster.sync();  // (the peers' shares stay alive until every CTA has gathered them)
 }
 
 template <class Cand>
