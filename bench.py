@@ -523,6 +523,7 @@ def run_ours(args) -> None:
     admitted = members = 0
     timed_now[0] = True
     kv0 = kv.stats() if kv is not None else None
+    trace_take(engine)  # (diagnostics builds only: the ring starts empty at the timed region)
     for s in range(args.warmup, nsteps):
         with torch.cuda.stream(stream):
             flush.zero_()
@@ -538,6 +539,9 @@ def run_ours(args) -> None:
         members += nm
     torch.cuda.synchronize()
     timed_now[0] = False
+    if os.environ.get("PRISM_TRACE_OUT"):
+        with open(os.environ["PRISM_TRACE_OUT"], "w") as f:
+            json.dump(trace_take(engine), f)
     if kv is not None:  # the payload's share of the timed steps (its own events, on the pool's stream)
         kv1 = kv.stats()
         kv_acc["ms"] = sum(a.elapsed_time(b) for a, b in kv_acc["events"])
@@ -980,6 +984,24 @@ def run_serve_c2(args) -> None:
         "e2e": None, "clocks": clk,
     }
     print(json.dumps(line), flush=True)
+
+
+def trace_take(engine):
+    """Kernel start stamps of a -DPRISM_TRACE diagnostics build (pdl.cuh), both
+    units merged in time order; [] for the product build."""
+    import ctypes as C
+
+    out = []
+    for unit in ("dart", "qas"):
+        fn = getattr(getattr(engine, "L", None), f"prism_trace_dump_{unit}", None)
+        if fn is None:
+            return []
+        cap = 8192
+        t = (C.c_ulonglong * cap)()
+        names = C.create_string_buffer(24 * cap)
+        n = fn(t, names, cap)
+        out += [(int(t[i]), names.raw[24 * i:24 * i + 24].split(b"\0")[0].decode()) for i in range(n)]
+    return sorted(out)
 
 
 def main():

@@ -215,6 +215,11 @@ int prism_set_protection_device(prism_tree *t, const double *d_pri, int32_t nseg
  * far; the tree stream joins it before the next eviction-order build or API
  * call (used by prism_wave_step to overlap protection with serialization). */
 int prism_set_protection_device_async(prism_tree *t, const double *d_pri, int32_t nseg);
+/* Order the tree's auxiliary stream (the next protection pass and eviction-
+ * order prebuild) after a CUDA event (cudaEvent_t as void*) -- prism_wave_step
+ * gates only that stream on the previous wave's releases, which nothing on the
+ * tree stream before the build reads. */
+int prism_tree_aux_wait(prism_tree *t, void *event);
 /* note_active_segments from dense DEVICE counters: active = a > 0 or n > 0
  * (engine.py:195-197). */
 int prism_note_active_device(prism_tree *t, const int32_t *d_a, const int32_t *d_nd, int32_t nseg);

@@ -38,6 +38,7 @@ def flags(extra: list[str] | None = None) -> list[str]:
         "-I",
         os.path.join(ROOT, "include"),
         *(extra or []),
+        *os.environ.get("PRISM_NVCC_EXTRA", "").split(),  # e.g. -DPRISM_TRACE (diagnostics builds)
     ]
 
 

@@ -682,6 +682,11 @@ int wx_ensure(prism_tree *t, int64_t B, int64_t levels, int64_t Tn) {
     CK(regrow(&X.piece_slot, c * WP_MAXP));
     CK(regrow(&X.owner, c * WP_MAXP));
     CK(regrow(&X.cut, c));
+    CK(regrow(&X.pinl, c * WP_MAXP));
+    CK(regrow(&X.pinp, c));
+    CK(regrow(&X.pinv, c));
+    if (!X.pinh) CK(dalloc(&X.pinh, 2));
+    CK(cudaMemsetAsync(X.pinh, 0, 2 * sizeof(int32_t), t->st));  // (the recorded paths are gone)
     if (!X.flags) CK(dalloc(&X.flags, 1));
     if (!X.misc) CK(dalloc(&X.misc, 8));
     t->wx_cap = c;
@@ -720,7 +725,7 @@ int cub_scan(prism_tree *t, In in, Out out, int64_t n, bool inclusive) {
 // device: plan -> scans -> plan verdict (k_wc_plan: fallback flags, capacity
 // headroom, eviction demand) -> the eviction-order prefix it needs (read on
 // the device) -> victim cuts + verdict (k_wp_cuts, its last CTA) -> apply -> control block
-// (k_wc_finalize), one stream of launches with a single host round trip at
+// (k_wp_sweep_c's last CTA), one stream of launches with a single host round trip at
 // the end.  Returns PRISM_OK with *applied = 1 when the wave was committed,
 // *applied = 0 when an exactness guard tripped (nothing was mutated; the
 // caller runs the ordered commit k_commit).  Capacity maintenance and a
@@ -730,7 +735,7 @@ int wave_par_prepare(prism_tree *t, int64_t B, int64_t levels) {
   if (!t->wc) {
     CK(dalloc(&t->wc, 1));
     CK(cudaMallocHost(&t->h_wc, sizeof(WaveCtl)));
-    CK(dalloc(&t->ds_part, DS_BLOCKS));
+    CK(dalloc(&t->ds_part, 2 * DS_BLOCKS));  // partition sums, partition minima
   }
   if (!t->sms) CK(cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, t->dev));
   return wx_ensure(t, B, levels, t->d.S);  // eviction-stream buffers for any prefix length
@@ -750,12 +755,14 @@ int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *lea
   prof_begin(t);
   k_wc_begin<<<(int)std::min<int64_t>(std::max<int64_t>((t->wx_lt + 255) / 256, 1), 4 * sms), 256, 0, st>>>(
       t->d, wc, abort, X, t->wx_lt);
-  k_wp_plan<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, W, X, wc);  // (warp per member)
-  k_wp_levels<<<blocks_for(B * WP_PL), TPB, 0, st>>>(W, X, wc);
+  {
+    const int nplan = (int)blocks_for(B * 32);  // (warp per member) + the level table (thread per level row)
+    k_wp_plan_levels<<<nplan + (int)blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc, nplan);
+  }
   k_wp_hits<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, W, X, wc);  // (warp per member)
   k_wp_scan3<<<1, 1024, 0, st>>>(t->d, B, X, wc, t->list_slack_tokens, force_full);  // + the plan verdict
   CK(cudaGetLastError());
-  t->launches[PH_COMMIT] += 5;
+  t->launches[PH_COMMIT] += 4;
   prof_end(t, PH_COMMIT);
   const int64_t *dW = &wc->W;
   if (t->use_coop) {
@@ -768,20 +775,18 @@ int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *lea
   prof_begin(t);
   k_vscan_a<<<DS_BLOCKS, 256, 0, st>>>(t->d, X, t->ds_part, wc);
   k_vscan_c<<<DS_BLOCKS, 256, 0, st>>>(t->d, X, t->ds_part, wc);
-  k_wp_cuts<<<blocks_for(B), TPB, 0, st>>>(t->d, B, X, wc);  // + the cut verdict (last CTA)
-  k_wp_conflicts<<<2 * sms, TPB, 0, st>>>(t->d, X, wc);     // consumed victims on a running member's chain
+  k_wp_cuts<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, B, X, wc, t->ds_part);  // + the cut and conflict verdict (last CTA)
   k_wp_evict<<<2 * sms, TPB, 0, st>>>(t->d, wc);
-  k_wp_alloc<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
-  k_wp_label_reset<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
+  k_wp_alloc<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);  // + the label-owner reset
   k_wp_create<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_touch<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_label<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc, hits, leaf_slots, leaf_ids);
   // a CapacityError stop: the stopping member's evict call sweeps the rest of the order
   k_wp_sweep_a<<<DS_BLOCKS, 256, 0, st>>>(t->d, t->ds_part, wc);
-  k_wp_sweep_c<<<DS_BLOCKS, 256, 0, st>>>(t->d, X, t->ds_part, wc);
-  k_wc_finalize<<<1, 1, 0, st>>>(t->d, B, X, wc, t->h_wc, t->hctrl);  // + verdict, control block to the host
+  // + the control block after the wave, verdict and control block to the host (last CTA)
+  k_wp_sweep_c<<<DS_BLOCKS, 256, 0, st>>>(t->d, B, X, t->ds_part, wc, t->h_wc, t->hctrl);
   CK(cudaGetLastError());
-  t->launches[PH_COMMIT] += 14;
+  t->launches[PH_COMMIT] += 10;
   return PRISM_OK;
 }
 
@@ -825,7 +830,7 @@ int wave_par_verdict(prism_tree *t, int *applied, int *again, int32_t *force_ful
 // device: plan -> scans -> plan verdict (k_wc_plan: fallback flags, capacity
 // headroom, eviction demand) -> the eviction-order prefix it needs (read on
 // the device) -> victim cuts + verdict (k_wp_cuts, its last CTA) -> apply -> control block
-// (k_wc_finalize), one stream of launches with a single host round trip at
+// (k_wp_sweep_c's last CTA), one stream of launches with a single host round trip at
 // the end.  Returns PRISM_OK with *applied = 1 when the wave was committed,
 // *applied = 0 when an exactness guard tripped (nothing was mutated; the
 // caller runs the ordered commit k_commit).  Capacity maintenance and a
@@ -1022,7 +1027,8 @@ void prism_tree_destroy(prism_tree *t) {
     if (p) cudaFree(p);
   const WaveTmp &X = t->wx;
   void *wbufs[] = {X.hit, X.pre, X.npieces, X.p0, X.lcp_level, X.cnew, X.tail, X.miss, X.idb, X.arb, X.dem,
-                   X.piece_slot, X.owner, X.lt_key, X.lt_min, X.flags, X.vlen, X.F, X.cut, X.misc};
+                   X.piece_slot, X.owner, X.lt_key, X.lt_min, X.flags, X.vlen, X.F, X.cut, X.misc,
+                   X.pinl, X.pinp, X.pinv, X.pinh};
   for (void *p : wbufs)
     if (p) cudaFree(p);
   if (t->ev0) cudaEventDestroy(t->ev0);
@@ -1137,7 +1143,9 @@ int prism_release_device(prism_tree *t, int64_t n, const int32_t *slots, const i
   if (n <= 0) return PRISM_OK;
   cudaSetDevice(t->dev);
   cudaStream_t s = stream ? (cudaStream_t)stream : t->st;
-  k_release_par<<<blocks_for(n), TPB, 0, s>>>(t->d, n, slots);
+  // (the last parallel commit's recorded root paths, when there is one)
+  const WaveTmp &X = t->wx;
+  k_release_par<WP_PL><<<blocks_for(n * WP_PL), TPB, 0, s>>>(t->d, n, slots, X.pinl, X.pinp, X.pinv, X.pinh);
   CK(cudaGetLastError());
   t->launches[PH_RELEASE]++;
   return PRISM_OK;
@@ -1348,6 +1356,12 @@ int prism_note_active_device(prism_tree *t, const int32_t *d_a, const int32_t *d
 }
 
 void *prism_tree_stream(prism_tree *t) { return (void *)t->st; }
+
+int prism_tree_aux_wait(prism_tree *t, void *event) {
+  cudaSetDevice(t->dev);
+  CK(cudaStreamWaitEvent(t->st_aux, (cudaEvent_t)event, 0));
+  return PRISM_OK;
+}
 
 // the tree's part of the fused wave can be captured in a CUDA graph: the
 // cooperative (host-sync-free) build and no live profile
@@ -1937,3 +1951,10 @@ int prism_kv_stats(prism_tree *t, int64_t *out) {
 }
 
 }  // extern "C"
+
+#ifdef PRISM_TRACE
+// diagnostics build only (pdl.cuh): this unit's kernel start stamps
+extern "C" int prism_trace_dump_dart(unsigned long long *t, char *names, int cap) {
+  return prism_trace_take(t, names, cap);
+}
+#endif

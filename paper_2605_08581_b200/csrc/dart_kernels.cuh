@@ -228,6 +228,7 @@ __device__ inline int32_t alloc_slot(const DT &T, Ctrl &C) {
 // _split (kvcache.py:275-291): new upper node over the first k edge tokens of X
 __device__ inline int32_t do_split(const DT &T, Ctrl &C, int32_t X, int32_t k) {
   const int32_t U = alloc_slot(T, C);
+  C.splits++;  // (every lane: the warp's copies of the control block stay identical)
   const int32_t p = T.par[X];
   const int64_t eo = T.eoff[X];
   const int32_t el = T.elen[X];
@@ -1050,16 +1051,45 @@ __global__ void k_release_seq(DT T, int64_t n, const int32_t *__restrict__ slots
 // the lanes of a warp climb their chains in lock step; lanes standing on the
 // same node (the shared upper levels: system prompt, popular segments, the
 // root) release it with one combined atomic
-__global__ void k_release_par(DT T, int64_t n, const int32_t *__restrict__ slots) {
+// release_path (kvcache.py:350-362) of n leaves: -1 on every node of each
+// leaf's root chain.  A leaf whose root path the last parallel commit recorded
+// (same slot, same version, no split since: the path is unchanged) is released
+// from that list -- thread (member j, piece row) piece-major, so the members
+// sharing the upper nodes combine their decrements per warp, with no
+// dependent climb (after the L2 flush each hop of a climb is an HBM round
+// trip); any other leaf climbs its parent chain, lanes in lock step.
+template <int PL>
+__global__ void k_release_par(DT T, int64_t n, const int32_t *__restrict__ slots, const int32_t *pinl,
+                              const int32_t *pinp, const uint32_t *pinv, const int32_t *pinh) {
   pdl_wait();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  int32_t x = i < n ? slots[i] : -1;
+  const int64_t j = t % n;
+  const bool live = t < n * PL;
+  const int32_t leaf = live ? slots[j] : -1;
+  bool listed = false;
+  int P = 0;
+  if (pinh && live && leaf >= 0 && j < __ldcg(&pinh[0]) && __ldcg(&pinh[1]) == T.ctrl->splits) {
+    P = __ldcg(&pinp[j]);
+    listed = __ldcg(&pinv[j]) == T.kver[leaf] && (P > 0 ? __ldcg(&pinl[j * WP_MAXP + P - 1]) : ROOT) == leaf;
+    if (!listed) P = 0;
+  }
+  for (int p = (int)(t / n); __any_sync(0xffffffffu, listed && p < P); p += PL) {
+    const bool on = listed && p < P;
+    const int32_t s = on ? __ldcg(&pinl[j * WP_MAXP + p]) : -1 - lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, s);
+    if (on && lane == __ffs(peers) - 1) atomicSub(&T.ref[s], __popc(peers));
+  }
+  const unsigned m0 = __ballot_sync(0xffffffffu, listed && t < n);  // (each listed member's root pin, once)
+  if (m0 && lane == __ffs(m0) - 1) atomicSub(&T.ref[ROOT], __popc(m0));
+  // the rest climb (one thread per member: the first row)
+  int32_t x = (live && t < n && !listed) ? leaf : -1;
   while (__any_sync(0xffffffffu, x >= 0)) {
     const unsigned peers = __match_any_sync(0xffffffffu, x);
     if (x >= 0 && lane == __ffs(peers) - 1) atomicSub(&T.ref[x], __popc(peers));
     if (x >= 0) x = T.par[x];
   }
+  pdl_trace_end();
 }
 
 // the inverse: +1 along each leaf's root chain (an explicit lock of a cached

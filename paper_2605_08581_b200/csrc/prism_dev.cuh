@@ -50,6 +50,7 @@ constexpr int MAX_PATH = 16384;  // tokens per path staged in shared memory
 constexpr int MAX_PNODES = 4096; // nodes on one root-to-leaf path
 constexpr int MAX_ANCH = 2048;   // anchors per insert
 constexpr int PM_MAX = 64;       // chain entries recorded by the parallel pre-match
+constexpr int WP_MAXP = 66;      // pieces per path of the parallel commit: sys + 64 segments + suffix
 
 struct HEnt {
   uint64_t key;
@@ -88,7 +89,7 @@ struct Ctrl {
   uint32_t vctr;
   int32_t fatal;
   int32_t n_admitted;
-  int32_t pad;
+  int32_t splits;  // do_split count: a root path recorded before a split may be stale (k_release_par)
 };
 
 struct OpRes {

@@ -1612,9 +1612,12 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
       q_prio<<<nblk(nseg), TPB, 0, st>>>(nseg, q->gdem, q->a, q->nd, c, q->prio_glob, q->dom_glob);
       pri = q->prio_glob;
     }
-    if (rel_n > 0) QCK(cudaStreamWaitEvent(st, q->ev_rel, 0));  // the releases, before anything reads ref
     QCK(cudaEventRecord(q->ev_t, st));  // (the protection on the tree's streams reads pri)
     QCK(cudaStreamWaitEvent((cudaStream_t)prism_tree_stream(t), q->ev_t, 0));
+    // the releases, before anything reads ref counts: the protection pass /
+    // eviction keys on the auxiliary stream, which the tree stream joins before
+    // the build -- serialization, pre-match and the commit plan do not wait
+    if (rel_n > 0 && (r = prism_tree_aux_wait(t, (void *)q->ev_rel))) return r;
     if ((r = prism_set_protection_device_async(t, pri, nseg))) return r;  // overlaps serialization
     q_serialize<<<nblk(B * 32), TPB, 0, st>>>(B, members, q->gids, q->goff, q->aligned, q->gsfx, sys_len, chunk, q->g,
                                               q->a, q->nd, q->poff, q->aoffs, q->tok, q->a_off, q->a_kind, q->a_seg,
@@ -1624,6 +1627,7 @@ int wave_step_graph(prism_tree *t, prism_qas *q, int64_t P, const int64_t *ids, 
                                        q->goff, q->aligned, sys_len, chunk, hits, leaf_slots, leaf_ids, (void *)st,
                                        abort)))
       return r;
+    if (rel_n > 0) QCK(cudaStreamWaitEvent(st, q->ev_rel, 0));  // (joined through the tree; explicit for the capture)
     // the wave's results straight to pinned host memory (fixed buffers, mapped)
     q_results<<<host_out ? 32 : 1, TPB, 0, st>>>(q->qcounts, q->tmp_tot, q->err, q->hres, B, members, hits,
                                                  host_out ? q->hout_mem : nullptr, host_out ? q->hout_hit : nullptr);
@@ -1946,3 +1950,10 @@ int prism_qas_set_commit_mode(prism_qas *q, int32_t mode) {
 }
 
 }  // extern "C"
+
+#ifdef PRISM_TRACE
+// diagnostics build only (pdl.cuh): this unit's kernel start stamps
+extern "C" int prism_trace_dump_qas(unsigned long long *t, char *names, int cap) {
+  return prism_trace_take(t, names, cap);
+}
+#endif

@@ -39,9 +39,10 @@
 
 namespace prism {
 
-constexpr int WP_MAXP = 66;  // pieces per path: sys + 64 segments + suffix
 // (member, piece)-parallel kernels: WP_PL threads per member, piece p on thread p % WP_PL
 constexpr int WP_PL = 16;
+// device-sized scans over DS_BLOCKS partitions (k_vscan_a / k_vscan_c, the sweep)
+constexpr int DS_BLOCKS = 296;
 enum { WPF_OVERFLOW = 1, WPF_PARTIAL = 2, WPF_ALIGN = 4, WPF_COLLIDE = 8, WPF_VICTIM = 16, WPF_CAPACITY = 32,
        WPF_SHAPE = 64 };
 
@@ -73,6 +74,12 @@ struct WaveTmp {
   int64_t *vlen, *F;                 // eviction stream prefix
   int64_t *cut;                      // per member: victims consumed through member j
   int64_t *misc;                     // [8] device scalars
+  // root paths pinned by the last parallel commit (its members [0, pinh[0])),
+  // for the next release (k_release_par): node slots per piece, pieces, the
+  // leaf's version; pinh = {members, Ctrl::splits when recorded}
+  int32_t *pinl, *pinp;              // [B * WP_MAXP], [B]
+  uint32_t *pinv;                    // [B]
+  int32_t *pinh;                     // [2]
 };
 
 // device-side control of one parallel wave commit: the control-block snapshot
@@ -135,9 +142,8 @@ __device__ inline int32_t wp_table(const WaveTmp &X, uint64_t key, int32_t j, bo
 // W1: per-member plan checks, one warp per member (lanes walk the pre-wave
 // chain in parallel): shape, pre-match flags, chain nodes aligned 1:1 with the
 // first pieces, and the chain marks (victim guard; first member per node)
-__global__ void k_wp_plan(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
-  pdl_wait();
-  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__device__ __forceinline__ void wp_plan_body(DT T, const WaveIn &W, const WaveTmp &X, const WaveCtl *wc, int64_t blk) {
+  const int64_t j = (blk * blockDim.x + threadIdx.x) >> 5;
   const int lane = lane_id();
   if (j >= W.B || wc->stop) return;  // (warp-uniform)
   const uint32_t epoch = wc->epoch;
@@ -178,10 +184,9 @@ __global__ void k_wp_plan(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
 // segments; the first owner of each prefix by atomicMin.  Level-major (thread
 // = level L of member j, consecutive members in a warp): every member shares
 // the low levels, so each warp inserts one key per distinct prefix.
-__global__ void k_wp_levels(WaveIn W, WaveTmp X, const WaveCtl *wc) {
-  pdl_wait();
+__device__ __forceinline__ void wp_levels_body(const WaveIn &W, const WaveTmp &X, const WaveCtl *wc, int64_t blk) {
   if (wc->stop) return;  // (an aborted wave: no dispatch order to read)
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t t = blk * blockDim.x + threadIdx.x;
   const int64_t j = t % W.B;
   const int lane = threadIdx.x & 31;
   const bool live = t < (int64_t)W.B * WP_PL;
@@ -217,6 +222,14 @@ __global__ void k_wp_levels(WaveIn W, WaveTmp X, const WaveCtl *wc) {
       }
     }
   }
+}
+
+// W1 + W1b in one launch (the level table needs only the dispatch order and
+// the aligned skeletons, not the plan): CTAs [0, nplan) plan, the rest insert levels
+__global__ void k_wp_plan_levels(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc, int nplan) {
+  pdl_wait();
+  if ((int)blockIdx.x < nplan) wp_plan_body(T, W, X, wc, blockIdx.x);
+  else wp_levels_body(W, X, wc, (int64_t)blockIdx.x - nplan);
 }
 
 // W2: intra-wave share, hit, new pieces, demand -- one warp per member: lane
@@ -347,7 +360,13 @@ __global__ void k_wp_alloc(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   pdl_wait();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, j = t / WP_PL;
   const int pl = (int)(t % WP_PL);
-  if (j >= W.B || wc->stop || j >= wc->Bc || X.cnew[j] == 0) return;
+  if (j >= W.B || wc->stop || j >= wc->Bc) return;
+  // label owners reset on the member's pre-wave chain (k_wp_touch elects the
+  // max member per node); its intra-wave shared pieces are new nodes, reset
+  // below by their creator
+  const int d = W.pm_meta[4 * j + 1];
+  for (int p = pl; p < d; p += WP_PL) T.eff[W.pm_chain[j * PM_MAX + p]] = -1;
+  if (X.cnew[j] == 0) return;
   const int64_t id0 = wc->id0;
   const int32_t free_top = wc->ft0 + (int32_t)wc->nv, hw = wc->hw0;
   const uint32_t vctr0 = wc->vctr0 + (uint32_t)wc->nv, epoch = wc->epoch;
@@ -479,15 +498,6 @@ __global__ void k_wp_touch(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   if (m0 && lane == __ffs(m0) - 1) atomicAdd(&T.ref[ROOT], __popc(m0));  // _pin reaches the root (kvcache.py:344-348)
 }
 
-__global__ void k_wp_label_reset(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
-  pdl_wait();
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, j = t / WP_PL;
-  const int pl = (int)(t % WP_PL);
-  if (j >= W.B || wc->stop || j >= wc->Bc) return;
-  const int own0 = X.cnew[j] ? X.p0[j] : X.npieces[j];
-  for (int p = pl; p < own0; p += WP_PL) T.eff[wp_node(W, X, j, p)] = -1;
-}
-
 // W8: the elected (max-index) member writes kind/seg/anchor (kvcache.py:317-340)
 __device__ inline void wp_stop_touch(DT T, const WaveIn &W, const WaveTmp &X, const WaveCtl *wc);
 
@@ -504,6 +514,7 @@ __global__ void k_wp_label(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc, int64_t
   const int P = X.npieces[j];
   for (int p = pl; p < P; p += WP_PL) {
     const int32_t s = wp_node(W, X, j, p);
+    X.pinl[j * WP_MAXP + p] = s;  // (the root path this member pins, for its release)
     if (T.eff[s] != (int32_t)j) continue;
     const int64_t a = W.aoffs[j] + p;
     T.kind[s] = (uint8_t)W.a_kind[a];
@@ -518,6 +529,8 @@ __global__ void k_wp_label(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc, int64_t
   }
   if (pl) return;
   const int32_t leaf = P > 0 ? wp_node(W, X, j, P - 1) : ROOT;
+  X.pinp[j] = P;
+  X.pinv[j] = T.kver[leaf];
   if (hits) hits[j] = X.hit[j];
   if (leaf_slots) leaf_slots[j] = leaf;
   if (leaf_ids) leaf_ids[j] = T.nid[leaf];
@@ -616,10 +629,12 @@ __global__ void __launch_bounds__(1024) k_wp_scan3(DT T, int64_t B, WaveTmp X, W
 }
 
 
+__device__ inline bool wp_conflict(const DT &T, const WaveTmp &X, const int64_t *part, int64_t nv, int64_t Bc);
+
 // the victims: nv = entries consumed through the last member, checks that the
 // prefix sufficed and that no consumed entry is pinned/guarded; the number of
 // evict calls (members whose cut advances) and the tokens freed
-__device__ inline void wc_cut_body(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
+__device__ inline void wc_cut_body(DT T, int64_t B, WaveTmp X, WaveCtl *wc, const int64_t *part) {
   __shared__ int64_t s_calls[32];
   const int32_t flags = __ldcg(X.flags);
   // a CapacityError stop commits the members before it (when the whole order
@@ -631,7 +646,9 @@ __device__ inline void wc_cut_body(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
   for (int64_t j = threadIdx.x; j < Bc; j += blockDim.x) calls += __ldcg(&X.cut[j]) > (j ? __ldcg(&X.cut[j - 1]) : 0) ? 1 : 0;
   for (int o = 16; o > 0; o >>= 1) calls += __shfl_xor_sync(0xffffffffu, calls, o);
   if ((threadIdx.x & 31) == 0) s_calls[threadIdx.x >> 5] = calls;
-  __syncthreads();
+  // (the conflict guard over the consumed prefix, by the whole CTA; used below
+  // only on the path where the victims [0, nv) are final)
+  const bool conflict = wp_conflict(T, X, part, Bc > 0 ? __ldcg(&X.cut[Bc - 1]) : 0, Bc);  // (+ barrier)
   if (threadIdx.x) return;
   calls = 0;
   for (int w = 0; w < (int)(blockDim.x >> 5); w++) calls += s_calls[w];
@@ -646,6 +663,11 @@ __device__ inline void wc_cut_body(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
     wc->flags = (flags & ~WPF_CAPACITY) ? flags : WPF_VICTIM;
     return;
   }
+  if (conflict) {
+    wc->stop = WC_FALLBACK;
+    wc->flags = WPF_VICTIM;
+    return;
+  }
   wc->Bc = Bc;
   wc->trunc = Bc < B ? 1 : 0;
   wc->nv = nv;
@@ -653,33 +675,47 @@ __device__ inline void wc_cut_body(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
   wc->freed = nv > 0 ? X.F[nv - 1] : 0;
 }
 
-// per member: number of list entries consumed through member j (first F >= D_j);
-// the last CTA to finish then takes the verdict (wc_cut_body)
-__global__ void k_wp_cuts(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
+// per member: number of list entries consumed through member j (first F >= D_j),
+// one warp per member: a 32-ary search (32 probes per round, ~4 dependent
+// rounds over a 400K-entry prefix instead of ~19 for a binary search); the
+// last CTA to finish then takes the verdict (wc_cut_body)
+__global__ void k_wp_cuts(DT T, int64_t B, WaveTmp X, WaveCtl *wc, const int64_t *part) {
   pdl_wait();
   __shared__ bool s_last;
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (wc->stop) return;  // (uniform over the grid)
-  if (j < B) {
+  if (j < B) {  // (warp-uniform)
     const int64_t D = wc->R0 + X.dem[j] - T.capacity;  // dem = inclusive sum of missing
     int64_t c = 0;
     if (D > 0) {
       const int64_t Tn = T.ctrl->L_n;
-      int64_t lo = 0, hi = Tn;  // first idx with F[idx] >= D
-      while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (X.F[mid] >= D) hi = mid;
-        else lo = mid + 1;
+      int64_t lo = 0, hi = Tn;  // the first idx with F[idx] >= D lies in [lo, hi] (hi: Tn or known >= D)
+      while (hi - lo > 32) {
+        const int64_t step = (hi - lo + 31) >> 5, p = lo + lane * step;
+        const bool ge = p < hi && __ldcg(&X.F[p]) >= D;
+        const unsigned b = __ballot_sync(0xffffffffu, ge);
+        const unsigned lt = __ballot_sync(0xffffffffu, p < hi && !ge);  // (a prefix of the lanes)
+        if (b) {
+          const int f = __ffs(b) - 1;
+          hi = lo + f * step;
+        }
+        if (lt) lo = lo + (int64_t)(31 - __clz(lt)) * step + 1;  // past the last probe below D
       }
-      if (lo >= Tn) {
-        atomicOr(X.flags, WPF_CAPACITY);
-        atomicMin((unsigned long long *)&X.misc[5], (unsigned long long)j);
+      const int64_t p = lo + lane;
+      const unsigned b = __ballot_sync(0xffffffffu, p < hi && __ldcg(&X.F[p]) >= D);
+      const int64_t a = b ? lo + __ffs(b) - 1 : hi;
+      if (a >= Tn) {
+        if (lane == 0) {
+          atomicOr(X.flags, WPF_CAPACITY);
+          atomicMin((unsigned long long *)&X.misc[5], (unsigned long long)j);
+        }
         c = Tn;
       } else {
-        c = lo + 1;
+        c = a + 1;
       }
     }
-    X.cut[j] = c;
+    if (lane == 0) X.cut[j] = c;
   }
   __threadfence();
   __syncthreads();
@@ -688,21 +724,21 @@ __global__ void k_wp_cuts(DT T, int64_t B, WaveTmp X, WaveCtl *wc) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  wc_cut_body(T, B, X, wc);
+  wc_cut_body(T, B, X, wc, part);
 }
 
 // the control block after the committed wave (what the ordered commit leaves)
 __device__ inline void wc_finalize_body(DT T, int64_t B, const WaveTmp &X, const WaveCtl *wc) {
   (void)B;
   Ctrl *C = T.ctrl;
-  const int64_t Bc = wc->Bc, nv = wc->nv, nsw = wc->nsw;
+  const int64_t Bc = wc->Bc, nv = wc->nv, nsw = __ldcg(&wc->nsw);  // (nsw, swfreed: the sweep's CTAs)
   const int64_t ncreate = X.idb[Bc], ntail = X.arb[Bc], nmiss = Bc > 0 ? X.dem[Bc - 1] : 0;
   const int32_t ft1 = wc->ft0 + (int32_t)nv;
   const int64_t from_free = ncreate < ft1 ? ncreate : ft1;
   const int64_t reused = X.misc[2];
   C->free_top = ft1 - (int32_t)from_free + (int32_t)nsw;
   C->hw = wc->hw0 + (int32_t)(ncreate - from_free);
-  C->resident = wc->R0 + nmiss - wc->freed - wc->swfreed;
+  C->resident = wc->R0 + nmiss - wc->freed - __ldcg(&wc->swfreed);
   C->clock = wc->clock0 + 2 * Bc + (wc->trunc ? 1 : 0);  // the stopping member's match tick
   C->next_id = wc->id0 + ncreate;
   C->arena_top = wc->arena0 + ntail;
@@ -721,17 +757,7 @@ __device__ inline void wc_finalize_body(DT T, int64_t B, const WaveTmp &X, const
   C->H_n = 0;
 }
 
-// the wave's control block after the commit, and the verdict + control block
-// written straight to the host's pinned (mapped) copies: no copy nodes
-__global__ void k_wc_finalize(DT T, int64_t B, WaveTmp X, const WaveCtl *wc, WaveCtl *h_wc, Ctrl *h_ctrl) {
-  pdl_wait();
-  if (!wc->stop) wc_finalize_body(T, B, X, wc);
-  *h_wc = *wc;
-  *h_ctrl = *T.ctrl;
-}
 
-// device-sized scans over DS_BLOCKS partitions (k_vscan_a / k_vscan_c below)
-constexpr int DS_BLOCKS = 296;
 
 
 
@@ -740,31 +766,29 @@ constexpr int DS_BLOCKS = 296;
 // evictable by the wave's members, else 0 (and marks the first such entry:
 // misc[1], the victim guard).  k_vscan_a: per-block sums (+ the guard),
 // k_vscan_c: each CTA reduces the sums before it, then the inclusive prefix F.
-__device__ __forceinline__ int64_t wp_vlen(const DT &T, const WaveTmp &X, int64_t i, uint32_t epoch, bool mark) {
+__device__ __forceinline__ int64_t wp_vlen(const DT &T, const WaveTmp &X, int64_t i, uint32_t epoch, int64_t &mark) {
   const uint64_t v = T.Lv[i];
   const int32_t s = (int32_t)(v & 0xffffffffu);
   const bool valid = T.kver[s] == (uint32_t)(v >> 32) && T.nid[s] >= 0 && T.par[s] >= 0 && T.ref[s] == 0;
-  if (mark) {
-    if (!valid) atomicMin((unsigned long long *)&X.misc[1], (unsigned long long)i);
-    // the first member whose pre-wave chain holds it (k_wp_conflicts: a victim a running member matched)
-    const uint64_t m = T.wchm[s];
-    X.vlen[i] = (uint32_t)(m >> 32) == epoch ? (int64_t)(0xFFFFFFFFu - (uint32_t)m) : 0x7FFFFFFFFFFFFFFFll;
-  }
+  if (!valid) atomicMin((unsigned long long *)&X.misc[1], (unsigned long long)i);
+  // the first member whose pre-wave chain holds it (a victim a running member matched)
+  const uint64_t m = T.wchm[s];
+  mark = (uint32_t)(m >> 32) == epoch ? (int64_t)(0xFFFFFFFFu - (uint32_t)m) : 0x7FFFFFFFFFFFFFFFll;
   return valid ? T.elen[s] : 0;
 }
 
-// a victim consumed by the committed members [0, Bc) that lies on the pre-wave
-// chain of a member that runs (index <= Bc: the committed ones and a stopping
-// one) changes that member's match: the exactness guard (nothing applied yet)
-__global__ void k_wp_conflicts(DT T, WaveTmp X, WaveCtl *wc) {
-  pdl_wait();
-  if (wc->stop) return;
-  const int64_t nv = wc->nv, Bc = wc->Bc;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x)
-    if (X.vlen[i] <= Bc) {
-      wc->flags = WPF_VICTIM;
-      wc->stop = WC_FALLBACK;
-    }
+// the conflict guard, in the cut verdict: a victim consumed by the committed
+// members [0, Bc) that lies on the pre-wave chain of a member that runs
+// (index <= Bc: the committed ones and a stopping one) changes that member's
+// match (nothing applied yet).  vlen holds the in-partition prefix minimum of
+// the first-member marks, part[DS_BLOCKS + b] partition b's minimum (k_vscan_a)
+__device__ inline bool wp_conflict(const DT &T, const WaveTmp &X, const int64_t *part, int64_t nv, int64_t Bc) {
+  if (nv <= 0) return false;
+  const int64_t n = T.ctrl->L_n, per = (n + DS_BLOCKS - 1) / DS_BLOCKS, q = (nv - 1) / per;
+  bool hit = false;
+  for (int64_t b = threadIdx.x; b < q; b += blockDim.x) hit |= __ldcg(&part[DS_BLOCKS + b]) <= Bc;
+  if (threadIdx.x == 0) hit |= __ldcg(&X.vlen[nv - 1]) <= Bc;
+  return __syncthreads_or(hit) != 0;
 }
 
 // k_vscan_a: each CTA's contiguous partition -- the entries' lengths (one
@@ -774,45 +798,50 @@ __global__ void k_wp_conflicts(DT T, WaveTmp X, WaveCtl *wc) {
 __global__ void __launch_bounds__(256) k_vscan_a(DT T, WaveTmp X, int64_t *part, const WaveCtl *wc) {
   pdl_wait();
   if (wc->stop || wc->W < 0) return;
-  __shared__ int64_t sw[8];
-  __shared__ int64_t carry;
+  constexpr int64_t INF = 0x7FFFFFFFFFFFFFFFll;
+  __shared__ int64_t sw[8], sm[8];
+  __shared__ int64_t carry, cmin;
   const int64_t n = T.ctrl->L_n, per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t b0 = blockIdx.x * per, b1 = b0 + per < n ? b0 + per : n;
   const uint32_t epoch = wc->epoch;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
+  if (threadIdx.x == 0) carry = 0, cmin = INF;
   constexpr int U = 4;  // entries per thread per round (their gathers in flight together)
   for (int64_t t0 = b0; t0 < b1; t0 += U * blockDim.x) {
-    int64_t v[U];
+    int64_t v[U], mk[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const int64_t i = t0 + (int64_t)threadIdx.x * U + u;
-      v[u] = i < b1 ? wp_vlen(T, X, i, epoch, true) : 0;
+      mk[u] = INF;
+      v[u] = i < b1 ? wp_vlen(T, X, i, epoch, mk[u]) : 0;
     }
-    int64_t x = 0;
+    int64_t x = 0, y = INF;
 #pragma unroll
-    for (int u = 0; u < U; u++) x += v[u];
+    for (int u = 0; u < U; u++) x += v[u], y = mk[u] < y ? mk[u] : y;
     const int64_t own = x;
     for (int o = 1; o < 32; o <<= 1) {
-      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      const int64_t a = __shfl_up_sync(0xffffffffu, x, o), b = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) x += a, y = b < y ? b : y;
     }
-    if (lane == 31) sw[wid] = x;
+    int64_t yex = __shfl_up_sync(0xffffffffu, y, 1);  // exclusive min within the warp
+    if (lane == 0) yex = INF;
+    if (lane == 31) sw[wid] = x, sm[wid] = y;
     __syncthreads();
-    int64_t before = carry;
-    for (int w = 0; w < wid; w++) before += sw[w];
-    int64_t run = before + x - own;
+    int64_t before = carry, mbefore = cmin;
+    for (int w = 0; w < wid; w++) before += sw[w], mbefore = sm[w] < mbefore ? sm[w] : mbefore;
+    int64_t run = before + x - own, rmin = yex < mbefore ? yex : mbefore;
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const int64_t i = t0 + (int64_t)threadIdx.x * U + u;
       run += v[u];
-      if (i < b1) X.F[i] = run;
+      rmin = mk[u] < rmin ? mk[u] : rmin;
+      if (i < b1) X.F[i] = run, X.vlen[i] = rmin;  // (vlen: in-partition prefix minimum of the marks)
     }
     __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = before + x;
+    if (threadIdx.x == blockDim.x - 1) carry = before + x, cmin = y < mbefore ? y : mbefore;
     __syncthreads();
   }
-  if (threadIdx.x == 0) part[blockIdx.x] = carry;
+  if (threadIdx.x == 0) part[blockIdx.x] = carry, part[DS_BLOCKS + blockIdx.x] = cmin;
 }
 
 __global__ void __launch_bounds__(256) k_vscan_c(DT T, WaveTmp X, const int64_t *part, const WaveCtl *wc) {
@@ -890,9 +919,7 @@ __global__ void __launch_bounds__(256) k_wp_sweep_a(DT T, int64_t *part, const W
 
 // each CTA: its carry from the counts before it, then its sweepable entries
 // detached in order (victim log, free list, child table, parents' child counts)
-__global__ void __launch_bounds__(256) k_wp_sweep_c(DT T, WaveTmp X, const int64_t *part, WaveCtl *wc) {
-  pdl_wait();
-  if (wc->stop || !wc->trunc) return;
+__device__ __forceinline__ void wp_sweep_c_body(DT T, const WaveTmp &X, const int64_t *part, WaveCtl *wc) {
   __shared__ int64_t sw[8];
   __shared__ int64_t carry;
   const int64_t nv = wc->nv, n = T.ctrl->L_n - nv, per = (n + gridDim.x - 1) / gridDim.x;
@@ -957,6 +984,41 @@ __global__ void __launch_bounds__(256) k_wp_sweep_c(DT T, WaveTmp X, const int64
   for (int o = 16; o > 0; o >>= 1) tok += __shfl_xor_sync(0xffffffffu, tok, o);
   if (lane == 0 && tok) atomicAdd((unsigned long long *)&wc->swfreed, (unsigned long long)tok);
   if (threadIdx.x == 0 && blockIdx.x == gridDim.x - 1) wc->nsw = carry;  // (the last CTA's carry: all of them)
+}
+
+// copy of a device struct to its mapped pinned host copy, 8-byte words over the CTA
+template <class S>
+__device__ __forceinline__ void wc_to_host(S *dst, const S *src) {
+  static_assert(sizeof(S) % 8 == 0, "word copy");
+  const unsigned long long *a = (const unsigned long long *)src;
+  unsigned long long *b = (unsigned long long *)dst;
+  for (int w = threadIdx.x; w < (int)(sizeof(S) / 8); w += blockDim.x) b[w] = __ldcg(a + w);
+}
+
+// the sweep (a CapacityError stop; else nothing), then the last CTA to finish
+// writes the control block after the committed wave and the verdict + control
+// block straight to the host's pinned (mapped) copies: no copy nodes
+__global__ void __launch_bounds__(256) k_wp_sweep_c(DT T, int64_t B, WaveTmp X, const int64_t *part, WaveCtl *wc,
+                                                   WaveCtl *h_wc, Ctrl *h_ctrl) {
+  pdl_wait();
+  if (!wc->stop && wc->trunc) wp_sweep_c_body(T, X, part, wc);  // (uniform)
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    s_last = atomicAdd((unsigned long long *)&X.misc[6], 1ull) == (unsigned long long)gridDim.x - 1ull;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0 && !__ldcg(&wc->stop)) {
+    wc_finalize_body(T, B, X, wc);
+    X.pinh[0] = (int32_t)wc->Bc;  // the committed members' recorded root paths
+    X.pinh[1] = T.ctrl->splits;
+  }
+  __threadfence();
+  __syncthreads();
+  wc_to_host(h_wc, wc);
+  wc_to_host(h_ctrl, T.ctrl);
 }
 
 }  // namespace prism

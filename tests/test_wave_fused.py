@@ -56,7 +56,8 @@ def _pending_arrays(reqs):
 
 
 def run_case(seed, policy, mode, nseg=40, hot=6, kmin=2, kmax=5, suffixes=(2, 4), sys=8, chunk=4, cap=600,
-             wave=24, nwaves=8, protect=3, cold=2, tiny=False, coop=1, sample=1, reo=1.0, prebuild=1):
+             wave=24, nwaves=8, protect=3, cold=2, tiny=False, coop=1, sample=1, reo=1.0, prebuild=1,
+             split_waves=()):
     import torch
 
     from paper_2605_08581_b200.wave import DevicePending, WaveEngine
@@ -111,6 +112,19 @@ def run_case(seed, policy, mode, nseg=40, hot=6, kmin=2, kmax=5, suffixes=(2, 4)
         ora_prev = oleaves
         assert hits == ohits, f"wave {w}: hits"
         assert leaf_ids == [x.node_id for x in oleaves], f"wave {w}: leaf ids"
+        if w in split_waves and b.members:
+            # a per-call insert that splits a node on the pinned root path of
+            # this wave's first member (mid-way into its first segment piece),
+            # released at once: the next wave's release must not trust the
+            # root paths the parallel commit recorded (k_release_par)
+            r = b.members[0]
+            path = serialize_tokens(r, cat, b.hints[r.id].aligned_skeleton)
+            cut = sys + max(chunk // 2, 1)
+            probe = list(path[:cut]) + [10_000_000 + 7 * w + q for q in range(3)]
+            view = eng.cache_view()
+            view.release_path(view.insert_path(probe))
+            ora.release_path(ora.insert_path(probe))
+            assert view.debug_nodes() == ora.debug_nodes(), f"wave {w}: split probe"
     view = eng.cache_view()
     assert view.debug_nodes() == ora.debug_nodes()
     assert view.victim_log() == ora.victim_log()
@@ -122,6 +136,15 @@ def run_case(seed, policy, mode, nseg=40, hot=6, kmin=2, kmax=5, suffixes=(2, 4)
 @pytest.mark.parametrize("seed", range(3))
 def test_parallel_commit_matches_oracle(policy, seed):
     st = run_case(seed, policy, mode=0)
+    assert st["parallel_waves"] > 0, st
+
+
+@pytest.mark.parametrize("policy", [CachePolicy.DART, CachePolicy.LRU])
+def test_release_after_split(policy):
+    """Releases of a parallel wave's members after a split on their pinned
+    paths (the recorded root paths are stale: every leaf climbs), and the
+    recorded-path release of the waves without one."""
+    st = run_case(5, policy, mode=0, split_waves=(1, 4, 5), nwaves=9)
     assert st["parallel_waves"] > 0, st
 
 
