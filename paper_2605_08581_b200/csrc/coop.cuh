@@ -754,13 +754,17 @@ struct ProtCand {
 //   k_ss_sort    one CTA per bucket sorts it in shared memory.
 constexpr int SS_TPB = 256;
 constexpr int SS_SEL_TPB = 512;
-constexpr int SS_BMAX = 1024;  // buckets up to this size: k_ss_sort (merge sort, several CTAs per SM)
+constexpr int SS_BMAX = 1024;  // buckets up to this size: k_ss_sort (runs of whole buckets per CTA)
 constexpr int SS_BMID = 384;   // k_ss_sort takes the buckets above this first
 constexpr int SS_BBIG = CHUNK; // larger ones up to this: k_ss_sort_big (in-place bitonic); beyond: fallback
 constexpr int SS_SUB = 1024;  // sub-sample the selection rounds run on
 constexpr size_t SS_SEL_SMEM = 3 * sizeof(Key3) * SS_SPL + 3 * 8 * SS_SUB;  // (k_ss_select's lk, tk, all; lw, tw, aw)
 constexpr size_t SS_FILTER_SMEM = sizeof(Key3) * SS_SPL + 4 * SS_SPL;
-constexpr size_t SS_SORT_SMEM = 2 * (sizeof(Key3) + 8) * SS_BMAX;
+// k_ss_sort: one 1024-thread CTA per SM sorting runs of whole buckets of up to
+// SS_SORT_CAP items (+ scratch, + the bucket offsets) in shared memory
+constexpr int SS_SORT_TPB = 1024;
+constexpr int SS_SORT_CAP = 2048;
+constexpr size_t SS_SORT_SMEM = 2 * (sizeof(Key3) + 8) * SS_SORT_CAP + sizeof(unsigned) * (SS_SPL + 4);
 
 __device__ inline int64_t ss_period(int32_t hw) {
   int64_t m = 8;
@@ -983,6 +987,7 @@ __global__ void __cluster_dims__(SS_CL, 1, 1) __launch_bounds__(SS_SEL_TPB)
   }
   if (rank == 0) coop_mark(st);
   cluster.sync();  // (the peers' shares stay alive until every CTA has gathered them)
+  pdl_trace_end();
 }
 
 template <class Cand>
@@ -1074,6 +1079,7 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_filter(Cand cand, CoopBufs B) {
   __syncthreads();
   for (int q = threadIdx.x; q < nb; q += blockDim.x)
     if (hcnt[q]) atomicAdd(&st->ss_cnt[q], hcnt[q]);
+  pdl_trace_end();
 }
 
 __global__ void __launch_bounds__(SS_TPB) k_ss_scatter(CoopBufs B, int64_t W, const int64_t *dW) {
@@ -1140,68 +1146,62 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_scatter(CoopBufs B, int64_t W, co
       B.vs[p] = B.v0[i];
     }
   }
+  pdl_trace_end();
 }
 
-// the buckets over the CTAs, each sorted in shared memory (block_merge_sort)
-__global__ void __launch_bounds__(SS_TPB) k_ss_sort(CoopBufs B, Key3 *kout, uint64_t *vout) {
+// the buckets over the CTAs: CTA c takes the buckets that start in the c-th
+// 1/G of the selected items, and sorts runs of consecutive buckets (whole
+// buckets, up to SS_SORT_CAP items) as ONE block_sort -- the buckets are in
+// key order, so sorting their concatenation sorts each.  Every CTA sorts about
+// n / G items in one or two passes (a bucket per sort, one at a time, left the
+// kernel as long as a CTA's longest queue).  Buckets above SS_BMAX are
+// k_build_coop's / k_ss_sort_big's.
+__global__ void __launch_bounds__(SS_SORT_TPB, 1) k_ss_sort(CoopBufs B, Key3 *kout, uint64_t *vout) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char dsm[];
   CoopState *st = B.st;
   if (!st->ss_ok) return;
   const int nb = st->ss_nb;
   Key3 *sk = reinterpret_cast<Key3 *>(dsm);
-  uint64_t *sv = reinterpret_cast<uint64_t *>(sk + SS_BMAX);
-  Key3 *tk = reinterpret_cast<Key3 *>(sv + SS_BMAX);
-  uint64_t *tv = reinterpret_cast<uint64_t *>(tk + SS_BMAX);
-  // the buckets above SS_BMID first, one per CTA as they come (a ~1000-key
-  // bucket sorts for ~25 us: started last behind three small ones it set the
-  // kernel's length), then the small ones handed out one at a time
-  __shared__ int s_b;
-  int b = blockIdx.x, pass = 0;
-  for (;;) {
-    if (pass == 0) {
-      while (b < nb) {
-        const int m = (int)(st->ss_off[b + 1] - st->ss_off[b]);
-        if (m > SS_BMID && m <= SS_BMAX) break;
-        b += gridDim.x;
+  uint64_t *sv = reinterpret_cast<uint64_t *>(sk + SS_SORT_CAP);
+  Key3 *tk = reinterpret_cast<Key3 *>(sv + SS_SORT_CAP);
+  uint64_t *tv = reinterpret_cast<uint64_t *>(tk + SS_SORT_CAP);
+  unsigned *off = reinterpret_cast<unsigned *>(tv + SS_SORT_CAP);
+  for (int b = threadIdx.x; b <= nb; b += blockDim.x) off[b] = st->ss_off[b];
+  __syncthreads();
+  const unsigned long long n = off[nb], G = gridDim.x;
+  const unsigned lo = (unsigned)(n * blockIdx.x / G), hi = (unsigned)(n * (blockIdx.x + 1) / G);
+  auto lower = [&](unsigned x) {  // first bucket starting at or after item x
+    int a = 0, z = nb;
+    while (a < z) {
+      const int m = (a + z) >> 1;
+      if (off[m] < x) a = m + 1;
+      else z = m;
+    }
+    return a;
+  };
+  int b = lower(lo);
+  const int bend = lower(hi);
+  while (b < bend) {  // (uniform: every thread reads the same shared offsets)
+    if (off[b + 1] - off[b] > (unsigned)SS_BMAX) {
+      b++;
+      continue;
+    }
+    int e = b + 1;
+    while (e < bend && off[e + 1] - off[e] <= (unsigned)SS_BMAX && off[e + 1] - off[b] <= (unsigned)SS_SORT_CAP) e++;
+    const unsigned c0 = off[b];
+    const int m = (int)(off[e] - c0);
+    if (m > 0) {
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        sk[i] = B.ks[c0 + i];
+        sv[i] = B.vs[c0 + i];
       }
-      if (b >= nb) {
-        pass = 1;
-        continue;
-      }
-    } else {
       __syncthreads();
-      if (threadIdx.x == 0) {
-        int x;
-        do {
-          x = (int)atomicAdd(&st->ss_next, 1u);
-        } while (x < nb && (int)(st->ss_off[x + 1] - st->ss_off[x]) > SS_BMID);
-        s_b = x;
-      }
-      __syncthreads();
-      b = s_b;
-      if (b >= nb) break;
+      block_sort(sk, sv, m, tk, tv, kout + c0, vout + c0);  // (ends on a barrier)
     }
-    const int b0 = (int)st->ss_off[b], m0 = (int)(st->ss_off[b + 1] - st->ss_off[b]);
-    if (pass == 0) b += gridDim.x;
-    if (m0 == 0) continue;
-    const long long c0 = clock64();
-    for (int i = threadIdx.x; i < m0; i += blockDim.x) {
-      sk[i] = B.ks[b0 + i];
-      sv[i] = B.vs[b0 + i];
-    }
-    __syncthreads();
-    const long long c1 = clock64();
-    block_merge_sort(sk, sv, m0, tk, tv, kout + b0, vout + b0);
-    if (threadIdx.x == 0) {
-      const long long c2 = clock64();
-      atomicAdd(&st->ss_prof[0], (unsigned long long)(c1 - c0));
-      atomicAdd(&st->ss_prof[1], (unsigned long long)(c2 - c1));
-      atomicAdd(&st->ss_prof[2], 1ull);
-      atomicAdd(&st->ss_prof[3], (unsigned long long)m0);
-      atomicMax(&st->ss_prof[4], (unsigned long long)(c2 - c0));
-    }
+    b = e;
   }
+  pdl_trace_end();
 }
 
 // the rare buckets above SS_BMAX (geometric sizes): in-place bitonic in shared memory
@@ -1213,6 +1213,15 @@ __device__ inline void ss_sort_big_body(const CoopBufs &B, Key3 *kout, uint64_t 
   for (int b = blockIdx.x; b < nb; b += gridDim.x) {
     const int b0 = (int)st->ss_off[b], m0 = (int)(st->ss_off[b + 1] - st->ss_off[b]);
     if (m0 <= SS_BMAX) continue;
+    if (2 * m0 <= SS_BBIG) {  // run merges (O(n log n)) with the scratch in the other half
+      for (int i = threadIdx.x; i < m0; i += blockDim.x) {
+        sk[i] = B.ks[b0 + i];
+        sv[i] = B.vs[b0 + i];
+      }
+      __syncthreads();
+      block_sort(sk, sv, m0, sk + m0, sv + m0, kout + b0, vout + b0);
+      continue;
+    }
     int mp = 1;
     while (mp < m0) mp <<= 1;
     for (int i = threadIdx.x; i < mp; i += blockDim.x) {
@@ -1307,6 +1316,7 @@ __global__ void __launch_bounds__(COOP_TPB) k_build_coop(DT T, CoopBufs B, int64
     B.st->ts_build[38] = fast ? 1ull : 0ull;        // sampled path taken
     B.st->ts_build[39] = (unsigned long long)nsel;  // selected-prefix size
   }
+  pdl_trace_end();
 }
 
 // ------------------------------------------------------------ small top-f
@@ -1405,6 +1415,7 @@ __global__ void __launch_bounds__(SS_TPB) k_tf_scan(ProtCand cand, CoopBufs B) {
   }
   for (int o = 16; o > 0; o >>= 1) ccount += __shfl_xor_sync(0xffffffffu, ccount, o);
   if (lane == 0 && ccount) atomicAdd(&B.st->ss_cand, ccount);
+  pdl_trace_end();
 }
 
 // merge a sorted list of F (rk/rv[cur], padded with all-ones keys) with
@@ -1606,6 +1617,7 @@ __global__ void __cluster_dims__(TF_CL, 1, 1) __launch_bounds__(SS_TPB)
     B.st->prot_n = F;
     B.st->tf_done = 1;
   }
+  pdl_trace_end();
 }
 
 // set_protection (kvcache.py:364-383): top-f reusable anchors by (-P-hat, seg

@@ -396,7 +396,7 @@ int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const 
   k_ss_select<Cand><<<SS_CL, SS_SEL_TPB, SS_SEL_SMEM, st>>>(cand, B, W, dW);
   k_ss_filter<Cand><<<3 * sms, SS_TPB, SS_FILTER_SMEM, st>>>(cand, B);  // (3 x 72 KB per SM: one wave)
   k_ss_scatter<<<2 * sms, SS_TPB, 0, st>>>(B, W, dW);
-  k_ss_sort<<<3 * sms, SS_TPB, SS_SORT_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
+  k_ss_sort<<<sms, SS_SORT_TPB, SS_SORT_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
   if (!big_in_finaliser) k_ss_sort_big<<<sms, 512, SS_BIG_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
   CK(cudaGetLastError());
   return PRISM_OK;
@@ -1786,6 +1786,19 @@ int prism_coop_timeline(prism_tree *t, uint64_t *out, int32_t *n) {
   cudaSetDevice(t->dev);
   CK(cudaMemcpyAsync(out, t->cst->ts_build, 40 * sizeof(uint64_t), cudaMemcpyDeviceToHost, t->st));
   CK(cudaMemcpyAsync(n, &t->cst->nts_build, sizeof(int32_t), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  return PRISM_OK;
+}
+
+// diagnostics: bucket offsets of the last sample select (CoopState::ss_off, up
+// to cap + 1 entries); *nb = its bucket count
+int prism_coop_buckets(prism_tree *t, uint32_t *off, int32_t cap, int32_t *nb) {
+  api_enter(t);
+  cudaSetDevice(t->dev);
+  CK(cudaMemcpyAsync(nb, &t->cst->ss_nb, sizeof(int32_t), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  const int32_t n = std::min(*nb, cap);
+  if (n > 0) CK(cudaMemcpyAsync(off, t->cst->ss_off, (n + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, t->st));
   CK(cudaStreamSynchronize(t->st));
   return PRISM_OK;
 }

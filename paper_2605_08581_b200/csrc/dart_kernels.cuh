@@ -13,6 +13,7 @@
 //                (see DESIGN.md "Exact eviction order").
 //   protection / note-active / release / rehash / compaction kernels.
 #pragma once
+#include "pdl.cuh"
 #include "prism_dev.cuh"
 
 namespace prism {
@@ -134,6 +135,7 @@ __global__ void k_prematch(DT T, int64_t B, const int64_t *__restrict__ poff,
     pm_meta[4 * w + 2] = r.klast;
     pm_meta[4 * w + 3] = (r.partial ? 1 : 0) | (r.overflow ? 2 : 0);
   }
+  pdl_trace_end();
 }
 
 // ------------------------------------------------------------ commit
@@ -920,6 +922,7 @@ __global__ void __launch_bounds__(PROP_TPB) k_propagate(DT T, int32_t hw, const 
       }
     }
   }
+  pdl_trace_end();
 }
 
 __global__ void k_gather(DT T, int32_t hw, Key3 *__restrict__ ck, uint64_t *__restrict__ cv,

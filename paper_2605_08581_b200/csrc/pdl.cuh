@@ -39,10 +39,9 @@ __device__ __forceinline__ void pdl_wait_traced(const char *fn) {
   }
 }
 #define pdl_wait() pdl_wait_traced(__func__)
-// end stamp of every CTA ("<name>$"; the last one is the kernel's end) -- only
-// in kernels whose threads all reach their last statement
+// end stamp of every CTA whose thread 0 reaches it ("<name>$"; the last one ~
+// the kernel's end); no barrier, so kernels with early returns may use it
 __device__ __forceinline__ void pdl_trace_end_impl(const char *fn) {
-  __syncthreads();
   if (threadIdx.x == 0 && threadIdx.y == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

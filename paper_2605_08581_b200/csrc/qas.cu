@@ -1319,6 +1319,7 @@ __global__ void __launch_bounds__(1024) q_members_scan(int64_t nh, int64_t nc, c
     if (s_err) *err = s_err;
     if (qcounts[3] || *err || tot[0] > tok_cap || tot[1] > anc_cap) *abort = 1;
   }
+  pdl_trace_end();
 }
 
 // one warp per member: token path and anchors
@@ -1380,6 +1381,7 @@ __global__ void q_serialize(int64_t B, const int64_t *__restrict__ members, cons
     a_seg[q] = (int32_t)0x80000000;
     a_snap[3 * q] = a_snap[3 * q + 1] = a_snap[3 * q + 2] = 0;
   }
+  pdl_trace_end();
 }
 
 

@@ -960,6 +960,7 @@ __global__ void __launch_bounds__(QS_TPB, 1) k_qas_small(QsArgs A, QsCfg c) {
     A.touched_n[1] = ntouch;  // this round's list is the next round's reset list
   }
   QS_TS(10);
+  pdl_trace_end();
 }
 
 }  // namespace qsmall

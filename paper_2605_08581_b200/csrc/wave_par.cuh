@@ -230,6 +230,7 @@ __global__ void k_wp_plan_levels(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc, i
   pdl_wait();
   if ((int)blockIdx.x < nplan) wp_plan_body(T, W, X, wc, blockIdx.x);
   else wp_levels_body(W, X, wc, (int64_t)blockIdx.x - nplan);
+  pdl_trace_end();
 }
 
 // W2: intra-wave share, hit, new pieces, demand -- one warp per member: lane
@@ -324,6 +325,7 @@ __global__ void k_wp_hits(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   X.cnew[j] = hit < n ? (P - p0) : 0;
   X.tail[j] = n - hit;
   X.miss[j] = n - hit;
+  pdl_trace_end();
 }
 
 
@@ -459,6 +461,7 @@ __global__ void k_wp_create(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
     T.ht[h].val = (uint32_t)s;
     T.hslot[s] = (int32_t)h;
   }
+  pdl_trace_end();
 }
 
 // W7: touches of pre-existing nodes, pins, and last-writer label election

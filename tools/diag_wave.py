@@ -77,6 +77,14 @@ def main():
         print(f"wave {s}: event {e0.elapsed_time(e1) * 1000:.1f} us, wall {wall:.1f} us, phases(us) {ph}")
         print("  qas one-launch phases (us):", (np.diff(ts) / 1e3).round(1).tolist())
         print("  build:", eng.build_timeline())
+        off = np.zeros(4097, dtype=np.uint32)
+        nb = np.zeros(1, dtype=np.int32)
+        L.prism_coop_buckets.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
+        L.prism_coop_buckets(eng.t, off.ctypes.data, 4096, nb.ctypes.data)
+        sz = np.diff(off[: min(int(nb[0]), 4096) + 1].astype(np.int64))
+        if sz.size:
+            print(f"  buckets: {sz.size}, sum {sz.sum()}, max {sz.max()}, >384: {(sz > 384).sum()}, "
+                  f">1024: {(sz > 1024).sum()}, top: {sorted(sz.tolist())[-8:]}, first/last: {sz[:3].tolist()} {sz[-3:].tolist()}")
     eng.close()
 
 
