@@ -762,8 +762,13 @@ constexpr size_t SS_SEL_SMEM = 3 * sizeof(Key3) * SS_SPL + 3 * 8 * SS_SUB;  // (
 constexpr size_t SS_FILTER_SMEM = sizeof(Key3) * SS_SPL + 4 * SS_SPL;
 // k_ss_sort: one 1024-thread CTA per SM sorting runs of whole buckets of up to
 // SS_SORT_CAP items (+ scratch, + the bucket offsets) in shared memory
-constexpr int SS_SORT_TPB = 1024;
-constexpr int SS_SORT_CAP = 2048;
+#ifndef PRISM_SS_SORT_TPB
+#define PRISM_SS_SORT_TPB 1024
+#define PRISM_SS_SORT_CAP 2048
+#endif
+constexpr int SS_SORT_TPB = PRISM_SS_SORT_TPB;
+constexpr int SS_SORT_CAP = PRISM_SS_SORT_CAP;
+constexpr int SS_SORT_PER_SM = 1024 / SS_SORT_TPB;  // CTAs per SM
 constexpr size_t SS_SORT_SMEM = 2 * (sizeof(Key3) + 8) * SS_SORT_CAP + sizeof(unsigned) * (SS_SPL + 4);
 
 __device__ inline int64_t ss_period(int32_t hw) {
@@ -1156,7 +1161,7 @@ __global__ void __launch_bounds__(SS_TPB) k_ss_scatter(CoopBufs B, int64_t W, co
 // n / G items in one or two passes (a bucket per sort, one at a time, left the
 // kernel as long as a CTA's longest queue).  Buckets above SS_BMAX are
 // k_build_coop's / k_ss_sort_big's.
-__global__ void __launch_bounds__(SS_SORT_TPB, 1) k_ss_sort(CoopBufs B, Key3 *kout, uint64_t *vout) {
+__global__ void __launch_bounds__(SS_SORT_TPB, SS_SORT_PER_SM) k_ss_sort(CoopBufs B, Key3 *kout, uint64_t *vout) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char dsm[];
   CoopState *st = B.st;

@@ -396,7 +396,7 @@ int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const 
   k_ss_select<Cand><<<SS_CL, SS_SEL_TPB, SS_SEL_SMEM, st>>>(cand, B, W, dW);
   k_ss_filter<Cand><<<3 * sms, SS_TPB, SS_FILTER_SMEM, st>>>(cand, B);  // (3 x 72 KB per SM: one wave)
   k_ss_scatter<<<2 * sms, SS_TPB, 0, st>>>(B, W, dW);
-  k_ss_sort<<<sms, SS_SORT_TPB, SS_SORT_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
+  k_ss_sort<<<SS_SORT_PER_SM * sms, SS_SORT_TPB, SS_SORT_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
   if (!big_in_finaliser) k_ss_sort_big<<<sms, 512, SS_BIG_SMEM, st>>>(B, t->d.Lk, t->d.Lv);
   CK(cudaGetLastError());
   return PRISM_OK;

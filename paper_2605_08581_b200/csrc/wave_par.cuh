@@ -394,6 +394,38 @@ __global__ void k_wp_alloc(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   }
 }
 
+// one warp copies n uint32 tokens: 16-byte vectors (4 in flight per lane)
+// when source and destination share their alignment, else words (4 in flight)
+__device__ __forceinline__ void warp_copy_u32(uint32_t *dst, const uint32_t *src, int64_t n, int lane) {
+  int64_t i = 0;
+  if ((((uintptr_t)src ^ (uintptr_t)dst) & 15) == 0) {
+    const int64_t h = (int64_t)((16 - ((uintptr_t)dst & 15)) & 15) >> 2;  // words before dst is aligned
+    const int64_t head = h < n ? h : n;
+    if (lane < head) dst[lane] = src[lane];
+    const int64_t nv = (n - head) >> 2;
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src + head);
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst + head);
+    for (int64_t v0 = lane; v0 < nv; v0 += 128) {
+      uint4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (v0 + 32 * u < nv) x[u] = __ldg(s4 + v0 + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (v0 + 32 * u < nv) d4[v0 + 32 * u] = x[u];
+    }
+    i = head + 4 * nv;
+  }
+  for (int64_t i0 = i + lane; i0 < n; i0 += 128) {
+    uint32_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) v[u] = i0 + 32 * u < n ? src[i0 + 32 * u] : 0u;
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+      if (i0 + 32 * u < n) dst[i0 + 32 * u] = v[u];
+  }
+}
+
 __device__ inline int32_t wp_node(const WaveIn &W, const WaveTmp &X, int64_t j, int p) {
   const int d = W.pm_meta[4 * j + 1];
   if (p < d) return W.pm_chain[j * PM_MAX + p];
@@ -414,19 +446,7 @@ __global__ void k_wp_create(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   const int64_t hit = X.hit[j];
   const uint32_t *path = W.tok + W.poff[j];
   const int64_t ab = arena0 + X.arb[j];
-  {  // the tail's tokens into the arena: 4 independent loads in flight per lane
-    const int64_t nt = n - hit;
-    const uint32_t *src = path + hit;
-    uint32_t *dst = T.tok + ab;
-    for (int64_t i0 = lane; i0 < nt; i0 += 128) {
-      uint32_t v[4];
-#pragma unroll
-      for (int u = 0; u < 4; u++) v[u] = i0 + 32 * u < nt ? src[i0 + 32 * u] : 0u;
-#pragma unroll
-      for (int u = 0; u < 4; u++)
-        if (i0 + 32 * u < nt) dst[i0 + 32 * u] = v[u];
-    }
-  }
+  warp_copy_u32(T.tok + ab, path + hit, n - hit, lane);  // the tail's tokens into the arena
   const int P = X.npieces[j], p0 = X.p0[j];
   const int64_t tick = clock0 + 2 * j + 2;
   for (int p = p0 + lane; p < P; p += 32) {
