@@ -1803,6 +1803,20 @@ int prism_coop_buckets(prism_tree *t, uint32_t *off, int32_t cap, int32_t *nb) {
   return PRISM_OK;
 }
 
+// diagnostics: out[4] = positive-P-hat protection candidates (tf_n), protected
+// (prot_n), order candidates and the selected prefix of the last build
+int prism_coop_counts(prism_tree *t, int64_t *out) {
+  api_enter(t);
+  cudaSetDevice(t->dev);
+  CoopState *c = t->cst;
+  CK(cudaMemcpyAsync(out, &c->tf_n, 8, cudaMemcpyDeviceToHost, t->st));
+  CK(cudaMemcpyAsync(out + 1, &c->prot_n, 8, cudaMemcpyDeviceToHost, t->st));
+  CK(cudaMemcpyAsync(out + 2, &c->ss_cand, 8, cudaMemcpyDeviceToHost, t->st));
+  CK(cudaMemcpyAsync(out + 3, &c->ss_n, 8, cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  return PRISM_OK;
+}
+
 // 0: list_min_tokens, 1: list_slack_tokens, 2: sel_min_candidates (tests use
 // tiny values to force partial eviction lists and their rebuild/resume path),
 // 3: cooperative kernels, 4: sample select (coop.cuh) before the radix selection

@@ -77,6 +77,10 @@ def main():
         print(f"wave {s}: event {e0.elapsed_time(e1) * 1000:.1f} us, wall {wall:.1f} us, phases(us) {ph}")
         print("  qas one-launch phases (us):", (np.diff(ts) / 1e3).round(1).tolist())
         print("  build:", eng.build_timeline())
+        cnt = np.zeros(4, dtype=np.int64)
+        L.prism_coop_counts.argtypes = [C.c_void_p, C.c_void_p]
+        L.prism_coop_counts(eng.t, cnt.ctypes.data)
+        print(f"  coop counts (tf_n, prot_n, order candidates, selected): {cnt.tolist()}")
         off = np.zeros(4097, dtype=np.uint32)
         nb = np.zeros(1, dtype=np.int32)
         L.prism_coop_buckets.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
