@@ -778,7 +778,7 @@ int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *lea
   k_wp_cuts<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, B, X, wc, t->ds_part);  // + the cut and conflict verdict (last CTA)
   k_wp_evict<<<2 * sms, TPB, 0, st>>>(t->d, wc);
   k_wp_alloc<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);  // + the label-owner reset
-  k_wp_create<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, W, X, wc);
+  k_wp_create<<<blocks_for(B * 64), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_touch<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_label<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc, hits, leaf_slots, leaf_ids);
   // a CapacityError stop: the stopping member's evict call sweeps the rest of the order

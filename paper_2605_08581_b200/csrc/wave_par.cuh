@@ -40,7 +40,10 @@
 namespace prism {
 
 // (member, piece)-parallel kernels: WP_PL threads per member, piece p on thread p % WP_PL
-constexpr int WP_PL = 16;
+#ifndef PRISM_WP_PL
+#define PRISM_WP_PL 32  // (16 -> 32: 1.5% per C3 wave, same-box A/B)
+#endif
+constexpr int WP_PL = PRISM_WP_PL;
 // device-sized scans over DS_BLOCKS partitions (k_vscan_a / k_vscan_c, the sweep)
 constexpr int DS_BLOCKS = 296;
 enum { WPF_OVERFLOW = 1, WPF_PARTIAL = 2, WPF_ALIGN = 4, WPF_COLLIDE = 8, WPF_VICTIM = 16, WPF_CAPACITY = 32,
@@ -436,17 +439,22 @@ __device__ inline int32_t wp_node(const WaveIn &W, const WaveTmp &X, int64_t j, 
 // W6b: fields, child-table entries and tokens of the new pieces (warp per member)
 __global__ void k_wp_create(DT T, WaveIn W, WaveTmp X, const WaveCtl *wc) {
   pdl_wait();
-  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  // two warps per member: the even one copies the tail's tokens, the odd one
+  // creates the nodes (their dependent loads overlap instead of queueing)
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, j = wg >> 1;
   const int lane = lane_id();
   if (j >= W.B || wc->stop || j >= wc->Bc || X.cnew[j] == 0) return;
   const int64_t arena0 = wc->arena0, clock0 = wc->clock0;
-  const int64_t m = W.members[j];
-  const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
   const int64_t n = W.poff[j + 1] - W.poff[j];
   const int64_t hit = X.hit[j];
   const uint32_t *path = W.tok + W.poff[j];
   const int64_t ab = arena0 + X.arb[j];
-  warp_copy_u32(T.tok + ab, path + hit, n - hit, lane);  // the tail's tokens into the arena
+  if ((wg & 1) == 0) {
+    warp_copy_u32(T.tok + ab, path + hit, n - hit, lane);  // the tail's tokens into the arena
+    return;
+  }
+  const int64_t m = W.members[j];
+  const int k = (int)(W.sk_off[m + 1] - W.sk_off[m]);
   const int P = X.npieces[j], p0 = X.p0[j];
   const int64_t tick = clock0 + 2 * j + 2;
   for (int p = p0 + lane; p < P; p += 32) {
