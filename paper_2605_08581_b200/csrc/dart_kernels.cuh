@@ -889,7 +889,9 @@ __global__ void __launch_bounds__(PROP_TPB) k_propagate(DT T, int32_t hw, const 
           // k_build_keys left eff[s] = s (evictable), EFF_BLOCKED or EFF_DEAD (root / free); a
           // descendant's walk may have raised it since (the node is evictable then)
           const int32_t e0 = __ldcg(&T.eff[s]);
-          if (e0 != EFF_DEAD) {
+          // raised already by a descendant (e0 >= 0, != s): that walk carries a larger key past s,
+          // so s's own walk could only raise ancestors the descendant raises again -- skip it
+          if (e0 != EFF_DEAD && (e0 < 0 || e0 == (int32_t)s)) {
             blocked = e0 == EFF_BLOCKED;
             val = blocked ? EFF_BLOCKED : (int32_t)s;
             if (!blocked) kv = T.kw[s];
