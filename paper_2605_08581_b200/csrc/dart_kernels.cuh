@@ -875,17 +875,20 @@ __global__ void __launch_bounds__(PROP_TPB) k_propagate(DT T, int32_t hw, const 
   const int64_t nwarp = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t chunk = ((int64_t)hw + nwarp - 1) / nwarp;
-  int64_t next = w * chunk;  // (warp-uniform) the warp's next unclaimed slot
-  const int64_t end = min((int64_t)hw, next + chunk);
+  // the warp's range [beg, end) in DESCENDING slot order: nodes created together
+  // take ascending slots top-down, so children come first and their raises let
+  // the parents skip their own walks
+  const int64_t beg = w * chunk, end = min((int64_t)hw, beg + chunk);
+  int64_t next = end - 1;  // (warp-uniform) the warp's next unclaimed slot
   bool act = false, blocked = false;
   int32_t val = 0, p = 0;
   Key3 kv{};
   for (;;) {
     const unsigned idle = __ballot_sync(FULL, !act);
-    if (idle && next < end) {  // idle lanes take the next slots of the range
+    if (idle && next >= beg) {  // idle lanes take the next slots of the range
       if (!act) {
-        const int64_t s = next + __popc(idle & ((1u << lane) - 1u));
-        if (s < end) {
+        const int64_t s = next - __popc(idle & ((1u << lane) - 1u));
+        if (s >= beg) {
           // k_build_keys left eff[s] = s (evictable), EFF_BLOCKED or EFF_DEAD (root / free); a
           // descendant's walk may have raised it since (the node is evictable then)
           const int32_t e0 = __ldcg(&T.eff[s]);
@@ -900,10 +903,10 @@ __global__ void __launch_bounds__(PROP_TPB) k_propagate(DT T, int32_t hw, const 
           }
         }
       }
-      next += __popc(idle);
+      next -= __popc(idle);
     }
     if (!__any_sync(FULL, act)) {
-      if (next >= end) break;
+      if (next < beg) break;
       continue;
     }
     if (act) {  // one hop: raise eff[p] to val, or stop
