@@ -473,16 +473,36 @@ __device__ inline void qs_cold_lane(const QsArgs &A, const QsCfg &c, int64_t P, 
   __shared__ int32_t s_m;
   if (tid == 0) s_m = 0;
   __syncthreads();
-  for (int64_t i0 = 0; i0 < P; i0 += nt) {
-    const int64_t i = i0 + tid;
-    const bool lf = i < P && A.rank[i] >= qs_ld(&A.btake[A.bucket[i]]);
-    const unsigned mt = __ballot_sync(0xffffffffu, lf);
-    int base = 0;
-    if ((tid & 31) == 0 && mt) base = atomicAdd(&s_m, __popc(mt));
-    base = __shfl_sync(0xffffffffu, base, 0) + __popc(mt & ((1u << (tid & 31)) - 1u));
-    if (lf) {
-      sk[base] = {qord(A.arrival[i]), (uint64_t)A.ids[i] ^ 0x8000000000000000ull};
-      sv[base] = (int32_t)i;
+  constexpr int CU = 4;  // requests per thread per round, their loads in flight together
+  for (int64_t i0 = 0; i0 < P; i0 += (int64_t)CU * nt) {
+    int32_t rk[CU], bk[CU];
+    double ar[CU];
+    int64_t id[CU];
+    bool lf[CU];
+#pragma unroll
+    for (int u = 0; u < CU; u++) {
+      const int64_t i = i0 + (int64_t)u * nt + tid;
+      rk[u] = i < P ? A.rank[i] : 0;
+      bk[u] = i < P ? A.bucket[i] : 0;
+      ar[u] = i < P ? A.arrival[i] : 0.0;
+      id[u] = i < P ? A.ids[i] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < CU; u++) {
+      const int64_t i = i0 + (int64_t)u * nt + tid;
+      lf[u] = i < P && rk[u] >= qs_ld(&A.btake[bk[u]]);
+    }
+#pragma unroll
+    for (int u = 0; u < CU; u++) {
+      const int64_t i = i0 + (int64_t)u * nt + tid;
+      const unsigned mt = __ballot_sync(0xffffffffu, lf[u]);
+      int base = 0;
+      if ((tid & 31) == 0 && mt) base = atomicAdd(&s_m, __popc(mt));
+      base = __shfl_sync(0xffffffffu, base, 0) + __popc(mt & ((1u << (tid & 31)) - 1u));
+      if (lf[u]) {
+        sk[base] = {qord(ar[u]), (uint64_t)id[u] ^ 0x8000000000000000ull};
+        sv[base] = (int32_t)i;
+      }
     }
   }
   __syncthreads();
