@@ -26,7 +26,10 @@ constexpr int COOP_TPB = 512;
 constexpr int COOP_ROUNDS = 14;
 constexpr int CHUNK = 4096;  // bitonic chunk per CTA (shared memory)
 // sample select (coop_sample_select)
-constexpr int SS_SAMP = 12288;  // samples at most (the period is the power of two that keeps the sample below this)
+#ifndef PRISM_SS_SAMP
+#define PRISM_SS_SAMP 12288
+#endif
+constexpr int SS_SAMP = PRISM_SS_SAMP;  // samples at most (the period is the power of two that keeps the sample below this)
 constexpr int SS_SPL = 2560;   // splitters (selected samples) at most
 constexpr size_t COOP_SORT_SMEM = (sizeof(Key3) + sizeof(uint64_t)) * CHUNK;
 constexpr size_t COOP_SMEM = COOP_SORT_SMEM;
@@ -754,7 +757,10 @@ struct ProtCand {
 //   k_ss_sort    one CTA per bucket sorts it in shared memory.
 constexpr int SS_TPB = 256;
 constexpr int SS_SEL_TPB = 512;
-constexpr int SS_BMAX = 1024;  // buckets up to this size: k_ss_sort (runs of whole buckets per CTA)
+#ifndef PRISM_SS_BMAX
+#define PRISM_SS_BMAX 2048  // (= SS_SORT_CAP: a bucket up to a whole run; 1024 -> 2048: 0.7% per C3 wave)
+#endif
+constexpr int SS_BMAX = PRISM_SS_BMAX;  // buckets up to this size: k_ss_sort (runs of whole buckets per CTA)
 constexpr int SS_BMID = 384;   // k_ss_sort takes the buckets above this first
 constexpr int SS_BBIG = CHUNK; // larger ones up to this: k_ss_sort_big (in-place bitonic); beyond: fallback
 constexpr int SS_SUB = 1024;  // sub-sample the selection rounds run on
@@ -769,6 +775,7 @@ constexpr size_t SS_FILTER_SMEM = sizeof(Key3) * SS_SPL + 4 * SS_SPL;
 constexpr int SS_SORT_TPB = PRISM_SS_SORT_TPB;
 constexpr int SS_SORT_CAP = PRISM_SS_SORT_CAP;
 constexpr int SS_SORT_PER_SM = 1024 / SS_SORT_TPB;  // CTAs per SM
+static_assert(SS_BMAX <= SS_SORT_CAP, "k_ss_sort takes every bucket up to SS_BMAX as (part of) one run");
 constexpr size_t SS_SORT_SMEM = 2 * (sizeof(Key3) + 8) * SS_SORT_CAP + sizeof(unsigned) * (SS_SPL + 4);
 
 __device__ inline int64_t ss_period(int32_t hw) {
@@ -1460,7 +1467,10 @@ __device__ __forceinline__ void tf_merge2(Key3 (*rk)[TF_MAX], uint64_t (*rv)[TF_
 //    lists pairwise in shared memory and applies the protection -- what one
 //    separate single-CTA merge over every CTA's list (~3000 items) did before.
 constexpr int TF_CL = 8;      // CTAs per cluster
-constexpr int TF_FIN = 512;   // cluster lists x f merged by the last cluster
+#ifndef PRISM_TF_FIN
+#define PRISM_TF_FIN 512
+#endif
+constexpr int TF_FIN = PRISM_TF_FIN;   // cluster lists x f merged by the last cluster
 constexpr size_t TF_LOCAL_SMEM =
     std::max(TF_SMEM, (size_t)2 * (sizeof(Key3) + 8) * TF_FIN);
 
