@@ -1341,7 +1341,10 @@ __global__ void __launch_bounds__(COOP_TPB) k_build_coop(DT T, CoopBufs B, int64
 // cluster (k_tf_local).
 // Otherwise ss_ok stays 0 and k_protect_coop runs the materialising selection.
 constexpr int TF_MAX = 64;     // budgets up to this use the small top-f path
-constexpr int TF_SLICE = 256;  // list items per slice of k_tf_local (shared-memory sort)
+#ifndef PRISM_TF_SLICE
+#define PRISM_TF_SLICE 256
+#endif
+constexpr int TF_SLICE = PRISM_TF_SLICE;  // list items per slice of k_tf_local (shared-memory sort)
 constexpr size_t TF_SMEM = 2 * (sizeof(Key3) + 8) * TF_SLICE;
 
 __global__ void __launch_bounds__(SS_TPB) k_tf_scan(ProtCand cand, CoopBufs B) {

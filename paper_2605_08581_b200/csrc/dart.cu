@@ -1194,6 +1194,9 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out, int3
       k_tf_scan<<<4 * sms, SS_TPB, 0, t->st>>>(ProtCand{t->d, keys}, B);
       // clusters of TF_CL CTAs, at most TF_FIN / f of them (the last one's merge)
       const int ncl = (int)std::max<int64_t>(1, std::min<int64_t>(2 * sms / TF_CL, TF_FIN / std::max<int64_t>(ff, 1)));
+      static uint64_t attr = 0;
+      if (prism::attr_once(attr))
+        CK(cudaFuncSetAttribute(k_tf_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TF_LOCAL_SMEM));
       k_tf_local<<<ncl * TF_CL, SS_TPB, TF_LOCAL_SMEM, t->st>>>(t->d, B, ff, keys);
       CK(cudaGetLastError());
       t->launches[PH_PROTECT] += 2;
