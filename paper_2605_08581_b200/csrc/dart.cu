@@ -403,9 +403,19 @@ int sample_select(prism_tree *t, Cand cand, const CoopBufs &B, int64_t W, const 
 }
 
 // k_propagate's persistent grid: every warp slot of the device (8 CTAs of 256 per SM)
+// launch shapes (per SM) of a few full-tree / per-victim passes (build-time knobs)
+#ifndef PRISM_PROP_CTAS
+#define PRISM_PROP_CTAS (2048 / PROP_TPB)
+#endif
+#ifndef PRISM_EVICT_CTAS
+#define PRISM_EVICT_CTAS 2
+#endif
+#ifndef PRISM_TFSCAN_CTAS
+#define PRISM_TFSCAN_CTAS 4
+#endif
 unsigned prop_blocks(prism_tree *t) {
   if (!t->sms) cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, t->dev);
-  return (unsigned)(t->sms * (2048 / PROP_TPB));
+  return (unsigned)(t->sms * PRISM_PROP_CTAS);
 }
 
 CoopBufs coop_bufs(prism_tree *t) {
@@ -776,7 +786,7 @@ int wave_par_enqueue(prism_tree *t, const WaveIn &W, int64_t *hits, int32_t *lea
   k_vscan_a<<<DS_BLOCKS, 256, 0, st>>>(t->d, X, t->ds_part, wc);
   k_vscan_c<<<DS_BLOCKS, 256, 0, st>>>(t->d, X, t->ds_part, wc);
   k_wp_cuts<<<blocks_for(B * 32), TPB, 0, st>>>(t->d, B, X, wc, t->ds_part);  // + the cut and conflict verdict (last CTA)
-  k_wp_evict<<<2 * sms, TPB, 0, st>>>(t->d, wc);
+  k_wp_evict<<<PRISM_EVICT_CTAS * sms, TPB, 0, st>>>(t->d, wc);
   k_wp_alloc<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);  // + the label-owner reset
   k_wp_create<<<blocks_for(B * 64), TPB, 0, st>>>(t->d, W, X, wc);
   k_wp_touch<<<blocks_for(B * WP_PL), TPB, 0, st>>>(t->d, W, X, wc);
@@ -1191,7 +1201,7 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out, int3
     if (sampled && f <= TF_MAX) {  // small budget: the positive-P-hat list and its top f
       int sms = 0;
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev));
-      k_tf_scan<<<4 * sms, SS_TPB, 0, t->st>>>(ProtCand{t->d, keys}, B);
+      k_tf_scan<<<PRISM_TFSCAN_CTAS * sms, SS_TPB, 0, t->st>>>(ProtCand{t->d, keys}, B);
       // clusters of TF_CL CTAs, at most TF_FIN / f of them (the last one's merge)
       const int ncl = (int)std::max<int64_t>(1, std::min<int64_t>(2 * sms / TF_CL, TF_FIN / std::max<int64_t>(ff, 1)));
       static uint64_t attr = 0;

@@ -45,7 +45,10 @@ namespace prism {
 #endif
 constexpr int WP_PL = PRISM_WP_PL;
 // device-sized scans over DS_BLOCKS partitions (k_vscan_a / k_vscan_c, the sweep)
-constexpr int DS_BLOCKS = 296;
+#ifndef PRISM_DS_BLOCKS
+#define PRISM_DS_BLOCKS 296
+#endif
+constexpr int DS_BLOCKS = PRISM_DS_BLOCKS;
 enum { WPF_OVERFLOW = 1, WPF_PARTIAL = 2, WPF_ALIGN = 4, WPF_COLLIDE = 8, WPF_VICTIM = 16, WPF_CAPACITY = 32,
        WPF_SHAPE = 64 };
 
