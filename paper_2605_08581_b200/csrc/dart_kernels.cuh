@@ -912,7 +912,11 @@ __global__ void __launch_bounds__(PROP_TPB) k_propagate(DT T, int32_t hw, const 
     if (act) {  // one hop: raise eff[p] to val, or stop
       int32_t cur = __ldcg(&T.eff[p]);  // L2-coherent read; CAS only to raise
       const int32_t pp = T.par[p];      // (in flight with it: the next hop needs no load of its own)
-      for (;;) {
+      // (in flight too) a descendant raised this walk's origin: its walk carries a larger key up
+      // behind this one and raises whatever this one would -- stop here
+      const int32_t eo = blocked ? val : __ldcg(&T.eff[val]);
+      if (eo != val) act = false;
+      for (; act;) {
         if (cur == EFF_BLOCKED || (!blocked && cur >= 0 && !key_less(T.kw[cur], kv))) {
           act = false;
           break;
