@@ -1217,7 +1217,11 @@ static int protect_current(prism_tree *t, int64_t *out_ids, int64_t *n_out, int3
     }
     void *args[] = {(void *)&t->d, (void *)&B, (void *)&ff, (void *)&minc, (void *)&small, (void *)&sampled,
                     (void *)&keys};
-    CK(cudaLaunchCooperativeKernel((void *)k_protect_coop, grid, COOP_TPB, args, COOP_SMEM, t->st));
+    // the fused wave (keys): after the small top-f k_protect_coop is only the rare
+    // fallback (fewer than f positive-P-hat anchors); one CTA needs no whole-GPU
+    // residency, so the launch does not wait for the tree stream's kernels to drain
+    const int pgrid = (keys && sampled && f <= TF_MAX) ? 1 : grid;
+    CK(cudaLaunchCooperativeKernel((void *)k_protect_coop, pgrid, COOP_TPB, args, COOP_SMEM, t->st));
     t->launches[PH_PROTECT] += 1;
     prof_end(t, PH_PROTECT);
     if (out_ids || n_out) {

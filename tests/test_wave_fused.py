@@ -175,6 +175,8 @@ def test_ordered_commit_matches_oracle(policy):
     dict(nseg=300, hot=8, kmin=20, kmax=40, suffixes=(0, 8), wave=16, nwaves=6, cap=6000),  # agent-like deep paths
     dict(nseg=300, hot=8, kmin=20, kmax=40, suffixes=(8,), wave=24, nwaves=8, cap=900, reo=0.0),  # ... evicting
     dict(cap=260, wave=48, nwaves=12, protect=8),      # eviction stress: most of the tree turns over per wave
+    dict(protect=30, nseg=12, hot=3, kmin=1, kmax=2),  # fewer positive-P-hat anchors than the budget (fallback top-f)
+    dict(protect=60, nseg=40, cap=2000, wave=32),      # ... and a budget near the small top-f's limit
 ])
 def test_parallel_commit_variants(variant):
     run_case(5, CachePolicy.DART, mode=0, **variant)
