@@ -861,7 +861,10 @@ __global__ void k_build_keys(DT T, int32_t hw, const int64_t *dW = nullptr) {
 // walk ends takes the next slot of its warp's range at once, so the lanes stay
 // busy and the kernel lasts about one longest walk.  (Ranges claimed from a
 // counter in 128-slot chunks balanced no better and cost more.)
-constexpr int PROP_TPB = 256;
+#ifndef PRISM_PROP_TPB
+#define PRISM_PROP_TPB 256
+#endif
+constexpr int PROP_TPB = PRISM_PROP_TPB;
 __global__ void __launch_bounds__(PROP_TPB) k_propagate(DT T, int32_t hw, const int64_t *dW = nullptr,
                                                         unsigned long long *clr = nullptr, int64_t nclr = 0) {
   pdl_wait();
